@@ -1,0 +1,130 @@
+/* mcmp2dev.h — C ABI of the B200 MC-MP2 walker loop (libmcmp2dev.so).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference has no FFI;
+ * its seam is the private Engine::advance (reference proj/core/src/driver.cpp:440-450),
+ * whose public callees are metropolis_step (sampler.hpp:59-60), TauSampler::sample
+ * (weights.hpp:58), mc_step_estimate (estimator.hpp:55-57) and BlockingAccumulator::add
+ * (estimator.hpp:64). Each entry point below names the reference interface it replaces.
+ * Plain C types only; the caller owns every host buffer, the handle deep-copies inputs at
+ * create time and keeps no host pointers. No exceptions cross this ABI: each call returns
+ * a status and mcmp2dev_last_error() carries the reference's message text.
+ *
+ * Threading: one handle per (device, worker) (driver.cpp:423-438 runs one std::thread per
+ * worker). A handle is used by one host thread at a time; handles on different devices may
+ * run concurrently. There is no global mutable state except the create-failure message.
+ */
+#ifndef MCMP2DEV_H
+#define MCMP2DEV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCMP2DEV_ABI_VERSION 1
+
+/* status codes (SURVEY.md section 8(b) "Errors") */
+enum {
+  MCMP2DEV_OK = 0,
+  MCMP2DEV_INVALID_ARGUMENT = 1, /* reference throws std::invalid_argument */
+  MCMP2DEV_RUNTIME = 2,          /* reference throws std::runtime_error    */
+  MCMP2DEV_CUDA = 3              /* CUDA failure (no reference analogue)   */
+};
+
+/* pair-term convention (reference estimator.cpp:26-32 is LITERAL) */
+enum { MCMP2DEV_ESTIMATOR_LITERAL = 0, MCMP2DEV_ESTIMATOR_PHYSICAL = 1 };
+
+/* Immutable system: SpinorSet + WeightSpec + TauSampler (model.hpp:74-117,
+ * weights.hpp:28-63). Basis functions of all channels are concatenated in channel order
+ * (channel 0..ncomp-1, SPINOR-TEXT `basis` records, model.cpp:302-323). */
+typedef struct mcmp2dev_system {
+  int ncomp;                  /* 1, 2 or 4 (model.cpp:99-100)                               */
+  int n_occ, n_vir;           /* spinor split (model.hpp:81-83)                              */
+  const int* channel_count;   /* [ncomp] functions per channel                               */
+  const double* fn_center;    /* [nfunc][3]                                                  */
+  const int* fn_lm;           /* [nfunc][2] (l, m), l <= 3                                   */
+  const int* fn_prim_offset;  /* [nfunc + 1] into prim arrays                                */
+  const double* prim_zeta;    /* [nprim]                                                     */
+  const double* prim_coeff;   /* [nprim] BasisFunction::evaluation_coeffs (model.hpp:49)     */
+  const double* coeff;        /* [nfunc][n_occ + n_vir][2] complex C, row-major (re, im)     */
+  const double* energies;     /* [n_occ + n_vir] ascending per block (model.cpp:122-129)     */
+  int nsites;                 /* WeightSpec sites, one per nucleus (weights.cpp:57-82)       */
+  const double* site_pos;     /* [nsites][3]                                                 */
+  const double* site_prim;    /* [nsites][2][2] (coeff incl. s norm, zeta) (weights.cpp:74-79) */
+  const double* site_zeta1;   /* [nsites] leading exponent for init spread (weights.hpp:44)  */
+  double ng;                  /* N_g closed form (weights.cpp:84-89)                         */
+  double lambda;              /* TauSampler rate = 2 (eps_LUMO - eps_HOMO) (weights.cpp:113) */
+  double w_direct, w_exchange;/* mp2_pair_prefactors(ncomp) (model.cpp:86-88)                */
+  int estimator;              /* MCMP2DEV_ESTIMATOR_*                                        */
+} mcmp2dev_system;
+
+/* Walker ensemble state, the WalkerEnsemble save/load record (sampler.cpp:95-120) with the
+ * PhiloxRng text state (rng.hpp:36-40, rng.cpp:76-94). `walkers` is caller-owned
+ * [m][9] = r1[3], r2[3], g1, g2, weight. */
+typedef struct mcmp2dev_ensemble {
+  int m;
+  double sigma_step;
+  long long proposed, accepted;
+  uint32_t rng_key[2];
+  uint32_t rng_counter[4];
+  uint32_t rng_idx;
+  double* walkers;
+} mcmp2dev_ensemble;
+
+typedef struct mcmp2dev_handle mcmp2dev_t;
+
+/* Per-step replay result: StepEstimate (estimator.hpp:23-26) plus the pair sums of the
+ * direct and exchange terms before division by C(m,2). */
+typedef struct mcmp2dev_step {
+  double value, imag;
+  double direct_re, direct_im, exchange_re, exchange_im;
+} mcmp2dev_step;
+
+/* ---- lifetime ---------------------------------------------------------------------- */
+/* Deep-copies `sys` to `device`, sized for up to max_walkers electron pairs.
+ * Replaces Engine construction of the per-worker state (driver.cpp:338-374). */
+int mcmp2dev_create(const mcmp2dev_system* sys, int device, int max_walkers, mcmp2dev_t** out);
+int mcmp2dev_destroy(mcmp2dev_t* h);
+/* message of the last failed call on h (or of the last failed create when h is NULL) */
+const char* mcmp2dev_last_error(const mcmp2dev_t* h);
+int mcmp2dev_abi_version(void);
+
+/* ---- ensemble ---------------------------------------------------------------------- */
+/* init_ensemble(m, molecule, spec, seed, stream) (sampler.cpp:21-47), on the device,
+ * consuming the reference's Philox stream in the reference's order. */
+int mcmp2dev_init_ensemble(mcmp2dev_t* h, int m, uint64_t seed, uint32_t stream);
+/* burn_in(ens, spec, n_burn, adapt) (sampler.cpp:81-93); counters reset at the end. */
+int mcmp2dev_burn_in(mcmp2dev_t* h, long n_burn, int adapt);
+int mcmp2dev_set_sigma_step(mcmp2dev_t* h, double sigma);  /* WalkerEnsemble::set_sigma_step */
+/* checkpoint I/O: WalkerEnsemble::load / save (sampler.cpp:95-120) */
+int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e);
+int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e); /* e->walkers: [m][9] */
+
+/* ---- the hot loop ------------------------------------------------------------------ */
+/* nsteps x { metropolis_step; tau = sample(rng.uniform()); mc_step_estimate } with the
+ * per-step (value, imag) written to host arrays so the caller's BlockingAccumulator::add
+ * runs in the reference order (driver.cpp:443-448). values/imags may be NULL (kept on
+ * device; for kernel timing). */
+int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags);
+/* Replay: mc_step_estimate at given walker positions and tau (estimator.cpp:35-63).
+ * walkers [nsteps][m][8] = r1[3], r2[3], g1, g2; tau [nsteps]; out [nsteps]. The device
+ * ensemble is not modified. m = 2 is sample_term (estimator.cpp:65-75). */
+int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
+                    mcmp2dev_step* out);
+
+/* ---- instrumentation (not on the reference surface) -------------------------------- */
+/* Accumulated device time (ms) and launch counts of the kernel classes since the last
+ * reset, measured with CUDA events on the handle's stream:
+ * out[0..3] = ms of {walk, spinor, pair, total}, out[4..7] = launches of the same. */
+int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out);
+/* Algorithmic work of one step at the current m: FLOP of the pair stage
+ * (C(m,2) * F_pair) and of the spinor stage (2m * 4 * R * n_p), bytes written to Phi. */
+int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes);
+/* synchronise the handle's stream */
+int mcmp2dev_synchronize(mcmp2dev_t* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCMP2DEV_H */

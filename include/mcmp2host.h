@@ -1,0 +1,54 @@
+/* mcmp2host.h — C entry points of the host library libmcmp2host.so (the re-hosted
+ * reference driver around libmcmp2dev.so). Used by the Python wrapper, bench.py and the
+ * distributed runner; the CLI `mcmp2` is the C++ front end (reference tools/mcmp2_main.cpp).
+ * Every call returns 0 on success, 1 for the reference's std::invalid_argument, 2 for
+ * std::runtime_error; mcmp2h_last_error() holds the message. */
+#ifndef MCMP2HOST_H
+#define MCMP2HOST_H
+
+#include <stdint.h>
+
+#include "mcmp2dev.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* mcmp2h_last_error(void);
+
+/* mcmp2 run / resume / merge (driver.hpp:74-88); report text as format_report */
+int mcmp2h_run(const char* config_text, char* report, int cap);
+int mcmp2h_run_hooked(const char* config_text, long abort_after_intervals, char* report, int cap);
+int mcmp2h_resume(const char* checkpoint_path, char* report, int cap);
+int mcmp2h_merge(const char* const* paths, int n, double* value, double* sigma_bar, long long* steps);
+int mcmp2h_parse_config(const char* config_text, char* canonical, int cap);
+uint64_t mcmp2h_fnv1a64(const char* bytes, long n);
+
+/* a loaded system: SPINOR-TEXT + weight overrides from config text (model.cpp:275-351,
+ * weights.cpp:57-90), flattened for mcmp2dev_create */
+typedef struct mcmp2h_system mcmp2h_system;
+mcmp2h_system* mcmp2h_system_load(const char* spinor_path, const char* config_text);
+void mcmp2h_system_free(mcmp2h_system* s);
+const mcmp2dev_system* mcmp2h_system_view(const mcmp2h_system* s);
+/* ints: ncomp, n_occ, n_vir, rows; dbls: ng, lambda, orthonormality deviation */
+int mcmp2h_system_info(const mcmp2h_system* s, int* ints, double* dbls);
+int mcmp2h_system_g(const mcmp2h_system* s, const double* pts, int n, double* out);
+int mcmp2h_save_spinor_set(const char* in_path, const char* out_path);
+
+/* one worker on one device (init_ensemble + burn_in at create); the accumulator state is
+ * returned as {steps, sum, imag_sum, mean, sigma_bar, in_block, partial, nblocks}. */
+typedef struct mcmp2h_worker mcmp2h_worker;
+mcmp2h_worker* mcmp2h_worker_create(const char* config_text, int worker_index, int device);
+void mcmp2h_worker_free(mcmp2h_worker* w);
+int mcmp2h_worker_advance(mcmp2h_worker* w, long nsteps, double* values, double* imags);
+int mcmp2h_worker_stats(mcmp2h_worker* w, double* out8);
+int mcmp2h_worker_block_means(mcmp2h_worker* w, double* out, int cap);
+mcmp2dev_t* mcmp2h_worker_device(mcmp2h_worker* w);
+
+/* writes <dir>/<name>.spinor and <dir>/<name>.conf for BASELINE configs cfg1..cfg4, cfg5-N */
+int mcmp2h_generate(const char* name, const char* dir);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,55 @@
+// common.cuh — device-side layouts and helpers shared by the walker, spinor and pair
+// kernels of libmcmp2dev.so (sm_100a).
+//
+// HBM layout of the per-step spinor values ("Phi", the output of the MO transform and the
+// input of the pair kernel), chosen so the pair kernel's DMMA fragments are contiguous:
+//   point pt = 2*walker + electron            (estimator.cpp:39-42: 2p <- r1, 2p+1 <- r2)
+//   k-group g = 4 consecutive spinors; occupied groups [0, Go), virtual groups [Go, Go+Gv)
+//   chunk c = KC4 consecutive groups (the smem stage of the pair kernel)
+//   Phi[c][pt][g % KC4][plane re/im][x*4 + k%4]   (16 doubles per plane, x = channel)
+// so one half-fragment (4 channels x 4 spinors) of one point is 128 contiguous bytes and a
+// stage (16 consecutive points x KC4 groups) is one contiguous TMA bulk copy. Values are
+// scaled by sqrt(guarded_exp(+-eps tau)) so O = Phi_o Phi_o^H and V = Phi_v Phi_v^H carry
+// the full exp(+-eps tau) weight (greens.cpp:63-79).
+#pragma once
+#include <cstdint>
+
+#include "philox.h"
+
+namespace mcmp2dev {
+
+constexpr int KC4 = 4;          // k-groups per pair-kernel stage
+constexpr int WB = 8;           // walkers per pair-kernel tile side
+constexpr int NCH = 4;          // channels per point in the Phi layout (ncomp <= 4, zero padded)
+
+// ------------------------------------------------------------------ device system
+struct DevSites {
+  int n;
+  const double* pos;    // [n][3]
+  const double* prim;   // [n][2][2] (coeff, zeta)
+  const double* zeta1;  // [n]
+};
+
+// walker arrays, SoA: [9][mmax] = r1x r1y r1z r2x r2y r2z g1 g2 weight
+struct WalkerBuf {
+  double* w;
+  int mmax;
+  __device__ double& at(int k, int p) const { return w[size_t(k) * mmax + p]; }
+};
+
+// device-resident per-handle scalars
+struct DevState {
+  unsigned long long pos;     // next u32 of the reference stream
+  double sigma;               // sigma_step
+  double tau, wtau;           // this step's tau and its density (weights.cpp:109-111)
+  long long proposed, accepted;
+  long long win_prop, win_acc;  // burn-in adaptation window (sampler.cpp:82-90)
+  int error;                  // 1: exponential overflow (greens.cpp:10-13)
+  int error_idx;              // spinor index of the overflow
+  int redo;                   // a coincident proposal needs the sequential path
+  unsigned int done_ctas;     // last-CTA counters (walker kernel)
+  unsigned int done_pair;     // (pair kernel)
+  int pad;
+};
+
+}  // namespace mcmp2dev

@@ -1,0 +1,70 @@
+// kernels.h — launch parameters of the libmcmp2dev.so kernels (host + device).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace mcmp2dev {
+
+enum WalkMode { WALK_PRODUCTION = 0, WALK_BURN = 1, WALK_INIT = 2 };
+
+struct WalkParams {
+  WalkerBuf in, out;   // sweep reads `in`, writes `out` (ping-pong)
+  int m;
+  DevSites sites;
+  double ng, lambda;
+  uint32_t k0, k1, stream;
+  DevState* st;
+  int mode;
+  long long sweep;     // 1-based burn-in sweep index (adaptation every 100)
+  int adapt;
+  const double* energies;
+  int n_occ, n_vir;
+  double* sw;          // [n_occ + n_vir] sqrt(guarded_exp) weights of this step
+  int* block_acc;      // per-CTA accept counts
+};
+
+// spinor evaluation + MO transform (model.cpp:55-64, :166-178) into the Phi layout
+struct SpinorParams {
+  int npts;            // 2m valid points
+  int npts_pad;        // points in the Phi layout (multiple of 2*WB)
+  WalkerBuf walkers;
+  int ncomp;
+  const int* ch_fn_off;      // [ncomp + 1] function offsets per channel
+  const double* fn_center;   // [nfunc][3]
+  const int* fn_lm;          // [nfunc][2]
+  const int* fn_prim_off;    // [nfunc + 1]
+  const double* prim_coeff;  // [nprim]
+  const int* prim_uniq;      // [nprim] index into the unique (centre, zeta) table
+  int nuniq;
+  const double* uniq_center; // [nuniq][3]
+  const double* uniq_zeta;   // [nuniq]
+  int max_ch;                // largest channel size
+  const double2* C;          // [nfunc][n_p] complex coefficients
+  int n_occ, n_vir, n_p;
+  int Go, Gtot;              // occupied k-groups, total k-groups (multiple of KC4)
+  const double* sw;
+  double* phi;
+};
+
+struct PairParams {
+  const double* phi;
+  int npts_pad, Go, Gv, Gtot;
+  int m, nb;                 // walkers, walker blocks of WB
+  WalkerBuf walkers;         // g1 (row 6), g2 (row 7)
+  const DevState* st_ro;
+  DevState* st;
+  double ng2, w_direct, w_exchange;
+  double* partials;          // [ntiles][4]
+  double* step_out;          // [6] of this step
+};
+
+void launch_walk(const WalkParams& P, cudaStream_t s);
+void launch_replay_load(const WalkParams& P, const double* walkers, double tau, cudaStream_t s);
+void launch_spinor(const SpinorParams& P, cudaStream_t s);
+int spinor_smem_bytes(const SpinorParams& P);
+void launch_pair(const PairParams& P, cudaStream_t s);
+cudaError_t pair_kernel_setup();
+cudaError_t spinor_kernel_setup();
+
+}  // namespace mcmp2dev

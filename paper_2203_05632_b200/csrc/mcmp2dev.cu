@@ -1,0 +1,588 @@
+// mcmp2dev.cu — handle management and the C ABI of libmcmp2dev.so (include/mcmp2dev.h).
+//
+// One handle = one reference "worker" (driver.cpp:200-205) resident on one device: the
+// immutable system (SpinorSet/WeightSpec/TauSampler), the walker ensemble (ping-pong SoA
+// buffers + Philox stream position) and the per-step work buffers. Each MC step is three
+// launches on the handle's stream: walk (Metropolis sweep + tau), spinor (basis values +
+// MO transform into the Phi layout), pair (O/V GEMMs + integrand + reduction). Per-step
+// StepEstimates stay on the device until the end of a chunk, then one copy returns them.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mcmp2dev.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace mcmp2dev;
+
+namespace {
+
+constexpr int kChunk = 1024;  // steps per device->host copy of StepEstimates
+thread_local std::string g_create_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RtError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* dupload(const T* src, size_t n, std::vector<void*>& owned) {
+  T* d = dalloc<T>(n, owned);
+  if (n) ck(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  return d;
+}
+
+}  // namespace
+
+struct mcmp2dev_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> owned;
+  std::string err;
+
+  // system
+  int ncomp = 0, n_occ = 0, n_vir = 0, n_p = 0, nfunc = 0, rows = 0;
+  int Go = 0, Gv = 0, Gtot = 0;
+  double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
+  int estimator = 0;
+  SpinorParams sp{};
+  DevSites sites{};
+  double* d_energies = nullptr;
+  double* d_sw = nullptr;
+
+  // ensemble
+  int mmax = 0, nbmax = 0, npts_pad = 0;
+  int m = 0;
+  uint32_t k0 = 0, k1 = 0, rstream = 0;
+  bool have_ensemble = false;
+  WalkerBuf buf[2]{}, rbuf{};
+  int cur = 0;
+  DevState* d_state = nullptr;
+  int* d_block_acc = nullptr;
+  double* d_phi = nullptr;
+  double* d_partials = nullptr;
+  double* d_steps = nullptr;
+  double* d_replay = nullptr;
+  double* h_steps = nullptr;  // pinned
+  double* h_replay = nullptr; // pinned [mmax][8]
+
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev[4]{};
+  double prof_ms[4] = {0, 0, 0, 0};
+  double prof_n[4] = {0, 0, 0, 0};
+
+  WalkParams walk_params(int mode, long long sweep, int adapt) {
+    WalkParams P{};
+    P.in = buf[cur];
+    P.out = buf[cur ^ 1];
+    P.m = m;
+    P.sites = sites;
+    P.ng = ng;
+    P.lambda = lambda;
+    P.k0 = k0;
+    P.k1 = k1;
+    P.stream = rstream;
+    P.st = d_state;
+    P.mode = mode;
+    P.sweep = sweep;
+    P.adapt = adapt;
+    P.energies = d_energies;
+    P.n_occ = n_occ;
+    P.n_vir = n_vir;
+    P.sw = d_sw;
+    P.block_acc = d_block_acc;
+    return P;
+  }
+
+  void launch_estimate(const WalkerBuf& wb, int mm, double* step_out) {
+    SpinorParams s = sp;
+    s.npts = 2 * mm;
+    s.walkers = wb;
+    if (prof) ck(cudaEventRecord(ev[1], stream), "event");
+    launch_spinor(s, stream);
+    if (prof) ck(cudaEventRecord(ev[2], stream), "event");
+    PairParams p{};
+    p.phi = d_phi;
+    p.npts_pad = npts_pad;
+    p.Go = Go;
+    p.Gv = Gv;
+    p.Gtot = Gtot;
+    p.m = mm;
+    p.nb = (mm + WB - 1) / WB;
+    p.walkers = wb;
+    p.st_ro = d_state;
+    p.st = d_state;
+    p.ng2 = ng * ng;
+    p.w_direct = w_direct;
+    p.w_exchange = w_exchange;
+    p.partials = d_partials;
+    p.step_out = step_out;
+    launch_pair(p, stream);
+    if (prof) {
+      ck(cudaEventRecord(ev[3], stream), "event");
+      ck(cudaEventSynchronize(ev[3]), "event sync");
+      float a = 0, b = 0, c = 0;
+      ck(cudaEventElapsedTime(&a, ev[0], ev[1]), "elapsed");
+      ck(cudaEventElapsedTime(&b, ev[1], ev[2]), "elapsed");
+      ck(cudaEventElapsedTime(&c, ev[2], ev[3]), "elapsed");
+      prof_ms[0] += a;
+      prof_ms[1] += b;
+      prof_ms[2] += c;
+      prof_ms[3] += a + b + c;
+      prof_n[0] += 1;
+      prof_n[1] += 1;
+      prof_n[2] += 1;
+      prof_n[3] += 1;
+    }
+    ck(cudaGetLastError(), "kernel launch");
+  }
+
+  void check_state_errors() {
+    DevState st;
+    ck(cudaMemcpyAsync(&st, d_state, sizeof st, cudaMemcpyDeviceToHost, stream), "state D2H");
+    ck(cudaStreamSynchronize(stream), "stream sync");
+    if (st.error) {
+      reset_errors();
+      // greens.cpp:10-13
+      throw RtError("greens: exponential overflow for spinor " + std::to_string(st.error_idx) +
+                    " (positive occupied or negative virtual energy with large tau?)");
+    }
+  }
+
+  void reset_errors() {
+    DevState st;
+    ck(cudaMemcpy(&st, d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    st.error = 0;
+    st.error_idx = INT_MAX;
+    ck(cudaMemcpy(d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+  }
+};
+
+namespace {
+
+template <class F>
+int guard(mcmp2dev_t* h, F&& f) {
+  std::string* err = h ? &h->err : &g_create_error;
+  try {
+    if (h) ck(cudaSetDevice(h->device), "cudaSetDevice");
+    f();
+    return MCMP2DEV_OK;
+  } catch (const ArgError& e) {
+    *err = e.what();
+    return MCMP2DEV_INVALID_ARGUMENT;
+  } catch (const RtError& e) {
+    *err = e.what();
+    return MCMP2DEV_RUNTIME;
+  } catch (const CudaError& e) {
+    *err = e.what();
+    return MCMP2DEV_CUDA;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return MCMP2DEV_RUNTIME;
+  }
+}
+
+void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers) {
+  if (!s) throw ArgError("mcmp2dev_create: null system");
+  if (s->ncomp != 1 && s->ncomp != 2 && s->ncomp != 4)
+    throw ArgError("SpinorSet: component count must be 1, 2 or 4");
+  if (s->n_occ < 0 || s->n_vir < 0 || s->n_occ + s->n_vir == 0)
+    throw ArgError("SpinorSet: invalid occupied/virtual counts");
+  if (max_walkers < 2) throw ArgError("init_ensemble: at least two electron-pair walkers");
+  if (s->nsites < 1) throw ArgError("Molecule: at least one nucleus required");
+  if (!(s->lambda > 0.0)) throw ArgError("TauSampler: lambda must be positive");
+  h->device = device;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(pair_kernel_setup(), "pair kernel attributes");
+  ck(spinor_kernel_setup(), "spinor kernel attributes");
+  for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+
+  h->ncomp = s->ncomp;
+  h->n_occ = s->n_occ;
+  h->n_vir = s->n_vir;
+  h->n_p = s->n_occ + s->n_vir;
+  h->ng = s->ng;
+  h->lambda = s->lambda;
+  h->w_direct = s->w_direct;
+  h->w_exchange = s->w_exchange;
+  h->estimator = s->estimator;
+  if (s->estimator != MCMP2DEV_ESTIMATOR_LITERAL)
+    throw ArgError("mcmp2dev_create: only the literal estimator is implemented on the device");
+
+  // ---- basis: flatten, dedupe exp(-zeta r^2) by (centre, zeta) ----
+  std::vector<int> ch_off(s->ncomp + 1, 0);
+  for (int x = 0; x < s->ncomp; ++x) {
+    if (s->channel_count[x] < 1) throw ArgError("SpinorSet: empty basis list for a component");
+    ch_off[x + 1] = ch_off[x] + s->channel_count[x];
+  }
+  const int nfunc = ch_off[s->ncomp];
+  h->nfunc = nfunc;
+  h->rows = nfunc;
+  int max_ch = 0;
+  for (int x = 0; x < s->ncomp; ++x) max_ch = std::max(max_ch, s->channel_count[x]);
+  const int nprim = s->fn_prim_offset[nfunc];
+  std::map<std::tuple<double, double, double, double>, int> uniq;
+  std::vector<double> uc, uz;
+  std::vector<int> prim_uniq(nprim);
+  for (int f = 0; f < nfunc; ++f) {
+    const int l = s->fn_lm[2 * f], mm = s->fn_lm[2 * f + 1];
+    if (l < 0 || l > 3) throw ArgError("BasisFunction: l must be in [0,3]");
+    if (mm < -l || mm > l) throw ArgError("BasisFunction: m out of range");
+    if (s->fn_prim_offset[f + 1] <= s->fn_prim_offset[f])
+      throw ArgError("BasisFunction: needs at least one primitive");
+    for (int k = s->fn_prim_offset[f]; k < s->fn_prim_offset[f + 1]; ++k) {
+      if (!(s->prim_zeta[k] > 0.0)) throw ArgError("BasisFunction: exponents must be strictly positive");
+      const auto key = std::make_tuple(s->fn_center[3 * f], s->fn_center[3 * f + 1],
+                                       s->fn_center[3 * f + 2], s->prim_zeta[k]);
+      auto it = uniq.find(key);
+      if (it == uniq.end()) {
+        it = uniq.emplace(key, int(uz.size())).first;
+        uc.insert(uc.end(), {s->fn_center[3 * f], s->fn_center[3 * f + 1], s->fn_center[3 * f + 2]});
+        uz.push_back(s->prim_zeta[k]);
+      }
+      prim_uniq[k] = it->second;
+    }
+  }
+  for (int p = 1; p < h->n_occ; ++p)
+    if (s->energies[p] < s->energies[p - 1]) throw RtError("SpinorSet: occupied energies not ascending");
+  for (int p = h->n_occ + 1; p < h->n_p; ++p)
+    if (s->energies[p] < s->energies[p - 1]) throw RtError("SpinorSet: virtual energies not ascending");
+
+  auto& o = h->owned;
+  SpinorParams& sp = h->sp;
+  sp.ncomp = s->ncomp;
+  sp.ch_fn_off = dupload(ch_off.data(), ch_off.size(), o);
+  sp.fn_center = dupload(s->fn_center, size_t(3) * nfunc, o);
+  sp.fn_lm = dupload(s->fn_lm, size_t(2) * nfunc, o);
+  sp.fn_prim_off = dupload(s->fn_prim_offset, size_t(nfunc) + 1, o);
+  sp.prim_coeff = dupload(s->prim_coeff, size_t(nprim), o);
+  sp.prim_uniq = dupload(prim_uniq.data(), prim_uniq.size(), o);
+  sp.nuniq = int(uz.size());
+  sp.uniq_center = dupload(uc.data(), uc.size(), o);
+  sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
+  sp.max_ch = max_ch;
+  sp.C = reinterpret_cast<const double2*>(dupload(s->coeff, size_t(2) * nfunc * h->n_p, o));
+  sp.n_occ = h->n_occ;
+  sp.n_vir = h->n_vir;
+  sp.n_p = h->n_p;
+  h->Go = (h->n_occ + 3) / 4;
+  h->Gv = (h->n_vir + 3) / 4;
+  h->Gtot = (h->Go + h->Gv + KC4 - 1) / KC4 * KC4;
+  sp.Go = h->Go;
+  sp.Gtot = h->Gtot;
+  h->d_energies = dupload(s->energies, size_t(h->n_p), o);
+  h->d_sw = dalloc<double>(h->n_p, o);
+  sp.sw = h->d_sw;
+
+  h->sites.n = s->nsites;
+  h->sites.pos = dupload(s->site_pos, size_t(3) * s->nsites, o);
+  h->sites.prim = dupload(s->site_prim, size_t(4) * s->nsites, o);
+  h->sites.zeta1 = dupload(s->site_zeta1, size_t(s->nsites), o);
+
+  // ---- ensemble and work buffers ----
+  h->mmax = max_walkers;
+  h->nbmax = (max_walkers + WB - 1) / WB;
+  h->npts_pad = 2 * WB * h->nbmax;
+  for (auto& b : h->buf) {
+    b.mmax = h->nbmax * WB;
+    b.w = dalloc<double>(size_t(9) * b.mmax, o);
+    ck(cudaMemset(b.w, 0, sizeof(double) * 9 * b.mmax), "memset");
+  }
+  h->rbuf.mmax = h->nbmax * WB;
+  h->rbuf.w = dalloc<double>(size_t(9) * h->rbuf.mmax, o);
+  ck(cudaMemset(h->rbuf.w, 0, sizeof(double) * 9 * h->rbuf.mmax), "memset");
+  h->d_state = dalloc<DevState>(1, o);
+  DevState st{};
+  st.sigma = 1.0;  // sampler.hpp:45
+  st.error_idx = INT_MAX;
+  ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+  h->d_block_acc = dalloc<int>((max_walkers + 127) / 128 + 1, o);
+  const size_t phi_doubles = size_t(h->Gtot) * h->npts_pad * 32;
+  h->d_phi = dalloc<double>(phi_doubles, o);
+  ck(cudaMemset(h->d_phi, 0, phi_doubles * sizeof(double)), "memset phi");
+  sp.phi = h->d_phi;
+  sp.npts_pad = h->npts_pad;
+  const size_t ntiles = size_t(h->nbmax) * (h->nbmax + 1) / 2;
+  h->d_partials = dalloc<double>(ntiles * 4, o);
+  h->d_steps = dalloc<double>(size_t(kChunk) * 6, o);
+  h->d_replay = dalloc<double>(size_t(h->mmax) * 8, o);
+  ck(cudaMallocHost(&h->h_steps, sizeof(double) * kChunk * 6), "cudaMallocHost");
+  ck(cudaMallocHost(&h->h_replay, sizeof(double) * h->mmax * 8), "cudaMallocHost");
+  ck(cudaDeviceSynchronize(), "setup sync");
+}
+
+void require_ensemble(mcmp2dev_t* h) {
+  if (!h->have_ensemble) throw ArgError("mcmp2dev: no walker ensemble (call init_ensemble or set_ensemble)");
+}
+
+}  // namespace
+
+extern "C" {
+
+int mcmp2dev_abi_version(void) { return MCMP2DEV_ABI_VERSION; }
+
+const char* mcmp2dev_last_error(const mcmp2dev_t* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int mcmp2dev_create(const mcmp2dev_system* sys, int device, int max_walkers, mcmp2dev_t** out) {
+  if (!out) {
+    g_create_error = "mcmp2dev_create: null output pointer";
+    return MCMP2DEV_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  auto* h = new mcmp2dev_handle();
+  const int rc = guard(nullptr, [&] { build(h, sys, device, max_walkers); });
+  if (rc != MCMP2DEV_OK) {
+    mcmp2dev_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return MCMP2DEV_OK;
+}
+
+int mcmp2dev_destroy(mcmp2dev_t* h) {
+  if (!h) return MCMP2DEV_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->owned) cudaFree(p);
+  if (h->h_steps) cudaFreeHost(h->h_steps);
+  if (h->h_replay) cudaFreeHost(h->h_replay);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return MCMP2DEV_OK;
+}
+
+int mcmp2dev_init_ensemble(mcmp2dev_t* h, int m, uint64_t seed, uint32_t stream) {
+  return guard(h, [&] {
+    if (m < 2) throw ArgError("init_ensemble: at least two electron-pair walkers");
+    if (m > h->mmax) throw ArgError("init_ensemble: more walkers than the handle was sized for");
+    h->m = m;
+    h->k0 = uint32_t(seed);
+    h->k1 = uint32_t(seed >> 32);
+    h->rstream = stream;
+    DevState st{};
+    st.pos = 0;
+    st.sigma = 1.0;  // sampler.hpp:45
+    st.error_idx = INT_MAX;
+    ck(cudaMemcpyAsync(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice, h->stream), "state H2D");
+    launch_walk(h->walk_params(WALK_INIT, 0, 0), h->stream);
+    h->cur ^= 1;
+    ck(cudaGetLastError(), "walk launch");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    h->have_ensemble = true;
+  });
+}
+
+int mcmp2dev_set_sigma_step(mcmp2dev_t* h, double sigma) {
+  return guard(h, [&] {
+    ck(cudaMemcpyAsync(reinterpret_cast<char*>(h->d_state) + offsetof(DevState, sigma), &sigma,
+                       sizeof sigma, cudaMemcpyHostToDevice, h->stream),
+       "sigma H2D");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+  });
+}
+
+int mcmp2dev_burn_in(mcmp2dev_t* h, long n_burn, int adapt) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    DevState st;
+    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    st.win_acc = st.win_prop = 0;
+    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    for (long s = 1; s <= n_burn; ++s) {
+      launch_walk(h->walk_params(WALK_BURN, s, adapt), h->stream);
+      h->cur ^= 1;
+    }
+    ck(cudaGetLastError(), "walk launch");
+    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    st.proposed = st.accepted = 0;  // sampler.cpp:92
+    st.win_acc = st.win_prop = 0;
+    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+  });
+}
+
+int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e) {
+  return guard(h, [&] {
+    if (!e || !e->walkers) throw ArgError("set_ensemble: null ensemble");
+    if (e->m < 2) throw RtError("checkpoint: malformed ensemble record");
+    if (e->m > h->mmax) throw ArgError("set_ensemble: more walkers than the handle was sized for");
+    // stream position of PhiloxRng state (rng.cpp:46-51, :83-94)
+    if (e->rng_counter[2] != 0) throw ArgError("set_ensemble: rng counter beyond 2^64 blocks");
+    const uint64_t B = uint64_t(e->rng_counter[0]) | (uint64_t(e->rng_counter[1]) << 32);
+    uint64_t pos;
+    if (e->rng_idx >= 4) pos = 4 * B;
+    else {
+      if (B == 0) throw ArgError("set_ensemble: partially consumed block before the first refill");
+      pos = 4 * (B - 1) + e->rng_idx;
+    }
+    h->m = e->m;
+    h->k0 = e->rng_key[0];
+    h->k1 = e->rng_key[1];
+    h->rstream = e->rng_counter[3];
+    std::vector<double> soa(size_t(9) * h->buf[0].mmax, 0.0);
+    for (int p = 0; p < e->m; ++p)
+      for (int k = 0; k < 9; ++k) soa[size_t(k) * h->buf[0].mmax + p] = e->walkers[size_t(p) * 9 + k];
+    ck(cudaMemcpy(h->buf[h->cur].w, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice),
+       "walkers H2D");
+    DevState st{};
+    st.pos = pos;
+    st.sigma = e->sigma_step;
+    st.proposed = e->proposed;
+    st.accepted = e->accepted;
+    st.error_idx = INT_MAX;
+    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    h->have_ensemble = true;
+  });
+}
+
+int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (!e || !e->walkers) throw ArgError("get_ensemble: null ensemble");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    DevState st;
+    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    std::vector<double> soa(size_t(9) * h->buf[0].mmax);
+    ck(cudaMemcpy(soa.data(), h->buf[h->cur].w, soa.size() * sizeof(double), cudaMemcpyDeviceToHost),
+       "walkers D2H");
+    e->m = h->m;
+    for (int p = 0; p < h->m; ++p)
+      for (int k = 0; k < 9; ++k) e->walkers[size_t(p) * 9 + k] = soa[size_t(k) * h->buf[0].mmax + p];
+    e->sigma_step = st.sigma;
+    e->proposed = st.proposed;
+    e->accepted = st.accepted;
+    e->rng_key[0] = h->k0;
+    e->rng_key[1] = h->k1;
+    const uint64_t pos = st.pos;
+    uint64_t B;
+    if (pos % 4 == 0) {
+      B = pos / 4;
+      e->rng_idx = 4;
+    } else {
+      B = pos / 4 + 1;
+      e->rng_idx = uint32_t(pos % 4);
+    }
+    e->rng_counter[0] = uint32_t(B);
+    e->rng_counter[1] = uint32_t(B >> 32);
+    e->rng_counter[2] = 0;
+    e->rng_counter[3] = h->rstream;
+  });
+}
+
+int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (nsteps < 0) throw ArgError("advance: negative step count");
+    long done = 0;
+    while (done < nsteps) {
+      const long n = std::min<long>(kChunk, nsteps - done);
+      for (long s = 0; s < n; ++s) {
+        if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
+        launch_walk(h->walk_params(WALK_PRODUCTION, 0, 0), h->stream);
+        h->cur ^= 1;
+        h->launch_estimate(h->buf[h->cur], h->m, h->d_steps + 6 * s);
+      }
+      if (values || imags) {
+        ck(cudaMemcpyAsync(h->h_steps, h->d_steps, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost,
+                           h->stream),
+           "steps D2H");
+      }
+      h->check_state_errors();  // synchronises
+      for (long s = 0; s < n; ++s) {
+        if (values) values[done + s] = h->h_steps[6 * s];
+        if (imags) imags[done + s] = h->h_steps[6 * s + 1];
+      }
+      done += n;
+    }
+  });
+}
+
+int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
+                    mcmp2dev_step* out) {
+  return guard(h, [&] {
+    if (m < 2) throw ArgError("replay: at least two electron-pair walkers");
+    if (m > h->mmax) throw ArgError("replay: more walkers than the handle was sized for");
+    for (long st = 0; st < nsteps; ++st) {
+      if (tau[st] < 0) throw ArgError("sample_term: tau must be non-negative");
+      std::memcpy(h->h_replay, walkers + size_t(st) * m * 8, sizeof(double) * 8 * m);
+      ck(cudaMemcpyAsync(h->d_replay, h->h_replay, sizeof(double) * 8 * m, cudaMemcpyHostToDevice,
+                         h->stream),
+         "replay H2D");
+      if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
+      WalkParams P = h->walk_params(WALK_PRODUCTION, 0, 0);
+      P.out = h->rbuf;
+      P.m = m;
+      launch_replay_load(P, h->d_replay, tau[st], h->stream);
+      h->launch_estimate(h->rbuf, m, h->d_steps);
+      ck(cudaMemcpyAsync(h->h_steps, h->d_steps, sizeof(double) * 6, cudaMemcpyDeviceToHost, h->stream),
+         "steps D2H");
+      h->check_state_errors();
+      out[st].value = h->h_steps[0];
+      out[st].imag = h->h_steps[1];
+      out[st].direct_re = h->h_steps[2];
+      out[st].direct_im = h->h_steps[3];
+      out[st].exchange_re = h->h_steps[4];
+      out[st].exchange_im = h->h_steps[5];
+    }
+  });
+}
+
+int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out) {
+  return guard(h, [&] {
+    if (out)
+      for (int i = 0; i < 4; ++i) {
+        out[i] = h->prof_ms[i];
+        out[4 + i] = h->prof_n[i];
+      }
+    if (reset)
+      for (int i = 0; i < 4; ++i) h->prof_ms[i] = h->prof_n[i] = 0;
+    h->prof = enable != 0;
+  });
+}
+
+int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes) {
+  return guard(h, [&] {
+    const double m = h->m, nc = h->ncomp;
+    const double fpair = 8.0 * nc * nc * (2.0 * h->n_occ + 4.0 * h->n_vir) + 4.0 * 8.0 * nc * nc;
+    if (pair_flop) *pair_flop = 0.5 * m * (m - 1) * fpair;
+    if (spinor_flop) *spinor_flop = 2.0 * m * 4.0 * h->rows * h->n_p;
+    if (phi_bytes) *phi_bytes = 2.0 * m * nc * h->n_p * 16.0;
+  });
+}
+
+int mcmp2dev_synchronize(mcmp2dev_t* h) {
+  return guard(h, [&] { ck(cudaStreamSynchronize(h->stream), "stream sync"); });
+}
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+// pair.cu — O/V Green's-function blocks for all walker pairs at one tau, the fused
+// direct/exchange integrand and the deterministic block reduction
+// (reference proj/core/src/greens.cpp:73-79, estimator.cpp:15-63).
+//
+// For walkers p < q the reference forms six 4x4 complex blocks (estimator.cpp:17-24):
+//   o1 = O(2p, 2q), o2 = O(2p+1, 2q+1)             O(d,o) = Phi_o(d) diag(w) Phi_o(o)^H
+//   va = V(2q, 2p), vb = V(2q+1, 2p+1), vc = V(2q+1, 2p), vd = V(2q, 2p+1)
+// and the literal element-wise sums f1d = sum o1.va, f2d = sum o2.vb, f1x = sum o1.vc,
+// f2x = sum o2.vd. Over all pairs these are batched Hermitian-type complex GEMMs. Here one
+// CTA owns an 8x8 tile of walker pairs (Q block x P block, Q >= P): the V products over the
+// tile are an (8 walkers x 2 electrons x 4 channels)^2 complex GEMM with K = n_vir, the O
+// products two (8 x 4)^2 GEMMs (one per electron) with K = n_occ. Each complex GEMM is four
+// real DMMA products (mma.sync m8n8k4 f64; tcgen05 has no f64 kind) on real-split operands
+// staged by TMA bulk copies. G is never written to memory: the accumulators are contracted
+// in registers and only four doubles per CTA leave the SM.
+//
+// Warp (wq, wp) owns Q walkers 2wq..2wq+1 x P walkers 4wp..4wp+3 (8 pairs). One m8n8k4
+// accumulator tile of V is exactly one walker pair (rows = q's (electron, channel), cols =
+// p's). The O tiles are computed transposed (rows = Q side) and exchanged through shared
+// memory, since the literal contraction pairs p's channel x with q's channel x.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mcmp2dev {
+
+namespace {
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;
+constexpr int HALF_PTS = 2 * WB;                          // 16 points per walker block
+constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;    // 32 points x KC4 groups x 32
+constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per stage
+constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// C += A conj(B)^T with real-split fragments: re += ar br + ai bi, im += ai br - ar bi
+__device__ __forceinline__ void cmma(double (&re)[2], double (&im)[2], double ar, double ai,
+                                     double nar, double br, double bi) {
+  dmma(re, ar, br);
+  dmma(re, ai, bi);
+  dmma(im, ai, br);
+  dmma(im, nar, bi);
+}
+
+__device__ __forceinline__ void tile_coords(int t, int& bq, int& bp) {
+  // t = bq (bq + 1) / 2 + bp, 0 <= bp <= bq
+  int q = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+  while ((q + 1) * (q + 2) / 2 <= t) ++q;
+  while (q * (q + 1) / 2 > t) --q;
+  bq = q;
+  bp = t - q * (q + 1) / 2;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_DOUBLES);
+  __shared__ double s_red[THREADS / 32][4];
+  __shared__ bool s_last;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wq = warp >> 1, wp = warp & 1;
+  int bq, bp;
+  tile_coords(blockIdx.x, bq, bp);
+  const int nchunks = P.Gtot / KC4;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int c, int stage) {
+    double* dst = sm + stage * STAGE_DOUBLES;
+    const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
+    const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
+    mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
+    bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
+    bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < STAGES && s < nchunks; ++s) issue(s, s);
+
+  double vre[2][4][2], vim[2][4][2], ore[2][2][2], oim[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vre[i][j][0] = vre[i][j][1] = vim[i][j][0] = vim[i][j][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) ore[i][j][0] = ore[i][j][1] = oim[i][j][0] = oim[i][j][1] = 0.0;
+
+  const int hl = lane >> 4, l16 = lane & 15;
+  for (int c = 0; c < nchunks; ++c) {
+    const int stage = c % STAGES;
+    mbar_wait(&full[stage], uint32_t((c / STAGES) & 1));
+    const double* S = sm + stage * STAGE_DOUBLES;
+#pragma unroll
+    for (int gg = 0; gg < KC4; ++gg) {
+      const int g = c * KC4 + gg;
+      auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+      if (g < P.Go) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int pa = 2 * (2 * wq + hl) + e;
+          const double ar = frag(pa, 0), ai = frag(pa, 1), nar = -ar;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pb = HALF_PTS + 2 * (4 * wp + 2 * h + hl) + e;
+            cmma(ore[e][h], oim[e][h], ar, ai, nar, frag(pb, 0), frag(pb, 1));
+          }
+        }
+      } else if (g < P.Go + P.Gv) {
+        double ar[2], ai[2], br[4], bi[4];
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+          const int pa = 2 * (2 * wq + qi) + hl;
+          ar[qi] = frag(pa, 0);
+          ai[qi] = frag(pa, 1);
+        }
+#pragma unroll
+        for (int pj = 0; pj < 4; ++pj) {
+          const int pb = HALF_PTS + 2 * (4 * wp + pj) + hl;
+          br[pj] = frag(pb, 0);
+          bi[pj] = frag(pb, 1);
+        }
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+          const double nar = -ar[qi];
+#pragma unroll
+          for (int pj = 0; pj < 4; ++pj) cmma(vre[qi][pj], vim[qi][pj], ar[qi], ai[qi], nar, br[pj], bi[pj]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && c + STAGES < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + STAGES, stage);
+    }
+  }
+
+  // ---- epilogue: o = conj(O~) through shared memory, literal contraction in registers ----
+  double* sO = sm + warp * 512;  // [e][qi][pj][y][x] complex (stage memory is free now)
+  {
+    const int qi = hl, y = (lane >> 2) & 3;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int pj = 2 * h + ((lane & 3) >> 1), x = 2 * (lane & 1) + j;
+          const int idx = ((((e * 2 + qi) * 4 + pj) * 16) + y * 4 + x) * 2;
+          sO[idx] = ore[e][h][j];
+          sO[idx + 1] = -oim[e][h][j];
+        }
+  }
+  __syncwarp();
+  double acc_dr = 0.0, acc_di = 0.0, acc_xr = 0.0, acc_xi = 0.0;
+  const double wtau = P.st_ro->wtau;
+  const int eq = hl, xx = (lane >> 2) & 3, ep = (lane & 3) >> 1;
+#pragma unroll
+  for (int qi = 0; qi < 2; ++qi)
+#pragma unroll
+    for (int pj = 0; pj < 4; ++pj) {
+      double fr = 0.0, fi = 0.0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int y = 2 * (lane & 1) + j;
+        const int idx = ((((ep * 2 + qi) * 4 + pj) * 16) + y * 4 + xx) * 2;
+        const double orr = sO[idx], oii = sO[idx + 1];
+        const double vr = vre[qi][pj][j], vi = vim[qi][pj][j];
+        fr += orr * vr - oii * vi;
+        fi += orr * vi + oii * vr;
+      }
+#pragma unroll
+      for (int o = 1; o <= 8; o <<= 1) {
+        if (o == 2) continue;
+        fr += __shfl_xor_sync(0xffffffffu, fr, o);
+        fi += __shfl_xor_sync(0xffffffffu, fi, o);
+      }
+      (void)eq;
+      // lane 0: (eq,ep) = (0,0) f1d; lane 18: (1,1) f2d; lane 16: (1,0) f1x; lane 2: (0,1) f2x
+      const double f1dr = __shfl_sync(0xffffffffu, fr, 0), f1di = __shfl_sync(0xffffffffu, fi, 0);
+      const double f2dr = __shfl_sync(0xffffffffu, fr, 18), f2di = __shfl_sync(0xffffffffu, fi, 18);
+      const double f1xr = __shfl_sync(0xffffffffu, fr, 16), f1xi = __shfl_sync(0xffffffffu, fi, 16);
+      const double f2xr = __shfl_sync(0xffffffffu, fr, 2), f2xi = __shfl_sync(0xffffffffu, fi, 2);
+      if (lane == 0) {
+        const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
+        if (q < P.m && p < P.m && q > p) {
+          const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+          const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+          const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+          // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32)
+          const double adr = -P.w_direct * f1dr, adi = -P.w_direct * f1di;
+          const double axr = -P.w_exchange * f1xr, axi = -P.w_exchange * f1xi;
+          acc_dr += (adr * f2dr - adi * f2di) * inv;
+          acc_di += (adr * f2di + adi * f2dr) * inv;
+          acc_xr += (axr * f2xr - axi * f2xi) * inv;
+          acc_xi += (axr * f2xi + axi * f2xr) * inv;
+        }
+      }
+    }
+  if (lane == 0) {
+    s_red[warp][0] = acc_dr;
+    s_red[warp][1] = acc_di;
+    s_red[warp][2] = acc_xr;
+    s_red[warp][3] = acc_xi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double r[4] = {0, 0, 0, 0};
+    for (int w = 0; w < THREADS / 32; ++w)
+      for (int k = 0; k < 4; ++k) r[k] += s_red[w][k];
+    for (int k = 0; k < 4; ++k) P.partials[size_t(blockIdx.x) * 4 + k] = r[k];
+    __threadfence();
+    const unsigned done = atomicAdd(&P.st->done_pair, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- last CTA: fixed-order sum over all tile partials -> StepEstimate ----
+  double r[4] = {0, 0, 0, 0};
+  for (unsigned t = tid; t < gridDim.x; t += THREADS)
+    for (int k = 0; k < 4; ++k) r[k] += P.partials[size_t(t) * 4 + k];
+  double* red = sm;  // [THREADS][4]
+  for (int k = 0; k < 4; ++k) red[tid * 4 + k] = r[k];
+  __syncthreads();
+  for (int s = THREADS / 2; s > 0; s >>= 1) {
+    if (tid < s)
+      for (int k = 0; k < 4; ++k) red[tid * 4 + k] += red[(tid + s) * 4 + k];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const double npairs = 0.5 * P.m * (P.m - 1);  // estimator.cpp:61
+    P.step_out[0] = (red[0] + red[2]) / npairs;
+    P.step_out[1] = (red[1] + red[3]) / npairs;
+    P.step_out[2] = red[0];
+    P.step_out[3] = red[1];
+    P.step_out[4] = red[2];
+    P.step_out[5] = red[3];
+    P.st->done_pair = 0;
+  }
+}
+
+cudaError_t pair_kernel_setup() {
+  return cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
+void launch_pair(const PairParams& P, cudaStream_t s) {
+  const int ntiles = P.nb * (P.nb + 1) / 2;
+  pair_kernel<<<ntiles, THREADS, SMEM_BYTES, s>>>(P);
+}
+
+}  // namespace mcmp2dev

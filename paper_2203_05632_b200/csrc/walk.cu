@@ -1,0 +1,293 @@
+// walk.cu — Metropolis walker-pair update, ensemble initialisation and the tau draw
+// (reference proj/core/src/sampler.cpp:21-93, weights.cpp:92-111, driver.cpp:444-445).
+//
+// Compiled with --fmad=false so that the proposal/weight arithmetic rounds like the
+// reference's (non-contracted) C++ and device chains track the CPU chain.
+//
+// RNG: the reference consumes ONE sequential Philox stream per worker: 18 u32 per pair
+// proposal (two gaussian3 = 2 x 4 uniforms x 2 u32, then one uniform), 2 u32 for tau, 10
+// u32 per electron at initialisation. Because those counts are fixed, walker p's draws
+// start at a computable offset (pos + 18 p), so each thread evaluates its own Philox
+// counters independently (counter-based, per walker) and reproduces the reference chain.
+// The only data-dependent consumption is the reference's redraw of an exactly coincident
+// proposal (sampler.cpp:57-62) / placement (sampler.cpp:38-40); when that happens the last
+// CTA replays the whole sweep sequentially, so the stream stays exact.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mcmp2dev {
+
+namespace {
+
+__device__ __forceinline__ double g_of(const DevSites& s, double x, double y, double z) {
+  // WeightSpec::g (weights.cpp:92-99): sites in order, two primitives each
+  double v = 0.0;
+  for (int i = 0; i < s.n; ++i) {
+    const double dx = x - s.pos[3 * i], dy = y - s.pos[3 * i + 1], dz = z - s.pos[3 * i + 2];
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    v += s.prim[4 * i + 0] * exp(-s.prim[4 * i + 1] * d2);
+    v += s.prim[4 * i + 2] * exp(-s.prim[4 * i + 3] * d2);
+  }
+  return v;
+}
+
+__device__ __forceinline__ void gaussian3(StreamReader& r, double g[3]) {
+  // PhiloxRng::gaussian3 (rng.cpp:66-74): four uniforms, fourth variate discarded
+  const double u1 = r.uniform();
+  const double u2 = r.uniform();
+  const double u3 = r.uniform();
+  const double u4 = r.uniform();
+  const double r1 = sqrt(-2.0 * log1p(-u1));
+  const double r2 = sqrt(-2.0 * log1p(-u2));
+  const double a1 = 2.0 * 3.141592653589793 * u3;
+  const double a2 = 2.0 * 3.141592653589793 * u4;
+  double s1, c1;
+  sincos(a1, &s1, &c1);
+  g[0] = r1 * c1;
+  g[1] = r1 * s1;
+  g[2] = r2 * cos(a2);
+}
+
+struct Walker {
+  double r1[3], r2[3], g1, g2, w;
+};
+
+__device__ __forceinline__ Walker load_walker(const WalkerBuf& b, int p) {
+  Walker x;
+  for (int k = 0; k < 3; ++k) {
+    x.r1[k] = b.at(k, p);
+    x.r2[k] = b.at(3 + k, p);
+  }
+  x.g1 = b.at(6, p);
+  x.g2 = b.at(7, p);
+  x.w = b.at(8, p);
+  return x;
+}
+
+__device__ __forceinline__ void store_walker(const WalkerBuf& b, int p, const Walker& x) {
+  for (int k = 0; k < 3; ++k) {
+    b.at(k, p) = x.r1[k];
+    b.at(3 + k, p) = x.r2[k];
+  }
+  b.at(6, p) = x.g1;
+  b.at(7, p) = x.g2;
+  b.at(8, p) = x.w;
+}
+
+// one proposal attempt for a pair (sampler.cpp:55-62); returns r12
+__device__ __forceinline__ double propose(StreamReader& rd, const Walker& x, double sigma,
+                                          double n1[3], double n2[3]) {
+  double g[3];
+  gaussian3(rd, g);
+  for (int k = 0; k < 3; ++k) n1[k] = x.r1[k] + g[k] * sigma;
+  gaussian3(rd, g);
+  for (int k = 0; k < 3; ++k) n2[k] = x.r2[k] + g[k] * sigma;
+  const double dx = n1[0] - n2[0], dy = n1[1] - n2[1], dz = n1[2] - n2[2];
+  return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+// accept/reject of metropolis_step (sampler.cpp:63-77); returns 1 when accepted
+__device__ __forceinline__ int decide(StreamReader& rd, const WalkParams& P, Walker& x,
+                                      const double n1[3], const double n2[3], double r12) {
+  const double g1 = g_of(P.sites, n1[0], n1[1], n1[2]);
+  const double g2 = g_of(P.sites, n2[0], n2[1], n2[2]);
+  const double wnew = g1 * g2 / (P.ng * r12);
+  const double u = rd.uniform();
+  if (u * x.w < wnew) {
+    for (int k = 0; k < 3; ++k) {
+      x.r1[k] = n1[k];
+      x.r2[k] = n2[k];
+    }
+    x.g1 = g1;
+    x.g2 = g2;
+    x.w = wnew;
+    return 1;
+  }
+  return 0;
+}
+
+// electron placement of init_ensemble (sampler.cpp:30-36)
+__device__ __forceinline__ void place(StreamReader& rd, const DevSites& s, double r[3]) {
+  const double u = rd.uniform();
+  unsigned idx = unsigned(u * double(s.n));
+  if (idx > unsigned(s.n - 1)) idx = unsigned(s.n - 1);
+  const double spread = 1.0 / sqrt(2.0 * s.zeta1[idx]);
+  double g[3];
+  gaussian3(rd, g);
+  for (int k = 0; k < 3; ++k) r[k] = s.pos[3 * idx + k] + g[k] * spread;
+}
+
+__device__ __forceinline__ double dist2(const double a[3], const double b[3]) {
+  const double dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+  return dx * dx + dy * dy + dz * dz;
+}
+
+__device__ __forceinline__ void finish_init(const WalkParams& P, Walker& x) {
+  x.g1 = g_of(P.sites, x.r1[0], x.r1[1], x.r1[2]);
+  x.g2 = g_of(P.sites, x.r2[0], x.r2[1], x.r2[2]);
+  x.w = x.g1 * x.g2 / (P.ng * sqrt(dist2(x.r1, x.r2)));
+}
+
+}  // namespace
+
+// sqrt of guarded_exp (greens.cpp:9-16) for every spinor at the step's tau; overflow is
+// flagged with the first offending spinor index, as the reference throws at set_tau.
+__device__ void tau_weights(const WalkParams& P, double tau) {
+  const int np = P.n_occ + P.n_vir;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const double e = k < P.n_occ ? P.energies[k] * tau : -P.energies[k] * tau;
+    double sw;
+    if (e > 700.0) {
+      atomicMin(&P.st->error_idx, k);
+      P.st->error = 1;
+      sw = 0.0;
+    } else if (e < -700.0) {
+      sw = 0.0;
+    } else {
+      sw = exp(0.5 * e);
+    }
+    P.sw[k] = sw;
+  }
+}
+
+__global__ void walk_kernel(WalkParams P) {
+  __shared__ int s_acc[32];
+  __shared__ bool s_last;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long pos0 = P.st->pos;
+  int acc = 0;
+  if (p < P.m) {
+    if (P.mode == WALK_INIT) {
+      StreamReader rd(P.k0, P.k1, P.stream, pos0 + 20ull * p);
+      Walker x;
+      place(rd, P.sites, x.r1);
+      place(rd, P.sites, x.r2);
+      if (dist2(x.r1, x.r2) == 0.0) P.st->redo = 1;
+      finish_init(P, x);
+      store_walker(P.out, p, x);
+    } else {
+      const double sigma = P.st->sigma;
+      StreamReader rd(P.k0, P.k1, P.stream, pos0 + 18ull * p);
+      Walker x = load_walker(P.in, p);
+      double n1[3], n2[3];
+      const double r12 = propose(rd, x, sigma, n1, n2);
+      if (r12 == 0.0) {
+        P.st->redo = 1;
+      } else {
+        acc = decide(rd, P, x, n1, n2, r12);
+      }
+      store_walker(P.out, p, x);
+    }
+  }
+  // per-CTA accept count (integer: order independent)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s_acc[wid] = acc;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += s_acc[w];
+    P.block_acc[blockIdx.x] = t;
+    __threadfence();
+    const unsigned done = atomicAdd(&P.st->done_ctas, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- last CTA: sequential redo if needed, stream advance, counters, tau ----
+  __shared__ long long s_total;
+  __shared__ unsigned long long s_consumed;
+  if (threadIdx.x == 0) {
+    long long total = 0;
+    unsigned long long consumed;
+    if (P.st->redo) {
+      // replay the whole sweep exactly as the reference's sequential loop
+      StreamReader rd(P.k0, P.k1, P.stream, pos0);
+      for (int q = 0; q < P.m; ++q) {
+        if (P.mode == WALK_INIT) {
+          Walker x;
+          place(rd, P.sites, x.r1);
+          do {
+            place(rd, P.sites, x.r2);
+          } while (dist2(x.r1, x.r2) == 0.0);
+          finish_init(P, x);
+          store_walker(P.out, q, x);
+        } else {
+          Walker x = load_walker(P.in, q);
+          double n1[3], n2[3], r12;
+          do {
+            r12 = propose(rd, x, P.st->sigma, n1, n2);
+          } while (r12 == 0.0);
+          total += decide(rd, P, x, n1, n2, r12);
+          store_walker(P.out, q, x);
+        }
+      }
+      consumed = rd.pos - pos0;
+      P.st->redo = 0;
+    } else {
+      for (unsigned b = 0; b < gridDim.x; ++b) total += P.block_acc[b];
+      consumed = (P.mode == WALK_INIT ? 20ull : 18ull) * unsigned(P.m);
+    }
+    s_total = total;
+    s_consumed = consumed;
+    P.st->pos = pos0 + consumed;
+    P.st->done_ctas = 0;
+    if (P.mode == WALK_PRODUCTION) {
+      P.st->proposed += P.m;
+      P.st->accepted += total;
+      // tau = TauSampler::sample(rng.uniform()) after the sweep (driver.cpp:445)
+      StreamReader rd(P.k0, P.k1, P.stream, P.st->pos);
+      const double u = rd.uniform();
+      P.st->pos += 2;
+      const double tau = -log1p(-u) / P.lambda;
+      P.st->tau = tau;
+      P.st->wtau = P.lambda * exp(-P.lambda * tau);
+    } else if (P.mode == WALK_BURN) {
+      // burn_in window and sigma adaptation (sampler.cpp:82-90)
+      P.st->win_acc += total;
+      P.st->win_prop += P.m;
+      if (P.adapt && P.sweep % 100 == 0) {
+        const double rate = double(P.st->win_acc) / double(P.st->win_prop);
+        P.st->sigma = P.st->sigma * (rate > 0.5 ? 1.1 : 1.0 / 1.1);
+        P.st->win_acc = 0;
+        P.st->win_prop = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (P.mode == WALK_PRODUCTION) tau_weights(P, P.st->tau);
+}
+
+// replay: positions/g from the caller, tau given (estimator input of mc_step_estimate)
+__global__ void replay_load_kernel(WalkParams P, const double* walkers, double tau) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P.m) {
+    for (int k = 0; k < 8; ++k) P.out.at(k, p) = walkers[size_t(p) * 8 + k];
+  }
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      P.st->tau = tau;
+      P.st->wtau = P.lambda * exp(-P.lambda * tau);
+    }
+    tau_weights(P, tau);
+  }
+}
+
+void launch_walk(const WalkParams& P, cudaStream_t s) {
+  const int threads = 128;
+  const int blocks = (P.m + threads - 1) / threads;
+  walk_kernel<<<blocks, threads, 0, s>>>(P);
+}
+
+void launch_replay_load(const WalkParams& P, const double* walkers, double tau, cudaStream_t s) {
+  const int threads = 128;
+  const int blocks = (P.m + threads - 1) / threads;
+  replay_load_kernel<<<blocks, threads, 0, s>>>(P, walkers, tau);
+}
+
+}  // namespace mcmp2dev

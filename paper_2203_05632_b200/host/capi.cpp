@@ -1,0 +1,182 @@
+// capi.cpp — C entry points of libmcmp2host.so (include/mcmp2host.h).
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/mcmp2host.h"
+#include "mcmp2.hpp"
+
+using namespace mcmp2;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+void copy_out(const std::string& s, char* buf, int cap) {
+  if (buf && cap > 0) std::snprintf(buf, std::size_t(cap), "%s", s.c_str());
+}
+}  // namespace
+
+struct mcmp2h_system {
+  SpinorSet spinors;
+  WeightSpec spec;
+  DeviceSystem dev;
+};
+
+struct mcmp2h_worker {
+  RunConfig cfg;
+  std::unique_ptr<SpinorSet> spinors;
+  std::unique_ptr<WeightSpec> spec;
+  std::unique_ptr<DeviceWorker> worker;
+};
+
+extern "C" {
+
+const char* mcmp2h_last_error(void) { return g_err.c_str(); }
+
+int mcmp2h_run(const char* config_text, char* report, int cap) {
+  return guard([&] { copy_out(format_report(run(parse_config_text(config_text))), report, cap); });
+}
+
+int mcmp2h_run_hooked(const char* config_text, long abort_after, char* report, int cap) {
+  return guard([&] {
+    RunHooks h;
+    h.abort_after_intervals = abort_after;
+    copy_out(format_report(run(parse_config_text(config_text), h)), report, cap);
+  });
+}
+
+int mcmp2h_resume(const char* path, char* report, int cap) {
+  return guard([&] { copy_out(format_report(resume(path)), report, cap); });
+}
+
+int mcmp2h_merge(const char* const* paths, int n, double* value, double* sigma_bar, long long* steps) {
+  return guard([&] {
+    std::vector<std::string> p(paths, paths + n);
+    const MergedEstimate m = merge_checkpoint_files(p);
+    *value = m.value;
+    *sigma_bar = m.sigma_bar;
+    *steps = m.total_steps;
+  });
+}
+
+int mcmp2h_parse_config(const char* text, char* canonical, int cap) {
+  return guard([&] {
+    const RunConfig c = parse_config_text(text);
+    c.validate();
+    copy_out(canonical_config_text(c), canonical, cap);
+  });
+}
+
+uint64_t mcmp2h_fnv1a64(const char* bytes, long n) { return fnv1a64(std::string(bytes, std::size_t(n))); }
+
+mcmp2h_system* mcmp2h_system_load(const char* spinor_path, const char* config_text) {
+  mcmp2h_system* out = nullptr;
+  guard([&] {
+    SpinorSet s = load_spinor_set(spinor_path);
+    if (!s.nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
+    const RunConfig c = parse_config_text(config_text ? config_text : "");
+    WeightSpec w(*s.nuclei, c.weight_overrides);
+    DeviceSystem d = make_device_system(s, w, MCMP2DEV_ESTIMATOR_LITERAL);
+    out = new mcmp2h_system{std::move(s), std::move(w), std::move(d)};
+  });
+  return out;
+}
+
+void mcmp2h_system_free(mcmp2h_system* s) { delete s; }
+
+const mcmp2dev_system* mcmp2h_system_view(const mcmp2h_system* s) { return &s->dev.view; }
+
+int mcmp2h_system_info(const mcmp2h_system* s, int* ints, double* dbls) {
+  return guard([&] {
+    ints[0] = s->spinors.ncomp;
+    ints[1] = s->spinors.n_occ;
+    ints[2] = s->spinors.n_vir;
+    ints[3] = s->spinors.rows();
+    dbls[0] = s->spec.ng;
+    dbls[1] = s->dev.view.lambda;
+    dbls[2] = s->spinors.orthonormality_deviation();
+  });
+}
+
+int mcmp2h_system_g(const mcmp2h_system* s, const double* pts, int n, double* out) {
+  return guard([&] {
+    for (int i = 0; i < n; ++i) out[i] = s->spec.g({pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+  });
+}
+
+int mcmp2h_save_spinor_set(const char* in_path, const char* out_path) {
+  return guard([&] { save_spinor_set(load_spinor_set(in_path), out_path); });
+}
+
+mcmp2h_worker* mcmp2h_worker_create(const char* config_text, int worker_index, int device) {
+  mcmp2h_worker* out = nullptr;
+  guard([&] {
+    auto w = std::make_unique<mcmp2h_worker>();
+    w->cfg = parse_config_text(config_text);
+    w->cfg.validate();
+    w->spinors = std::make_unique<SpinorSet>(load_spinor_set(w->cfg.spinor_path));
+    if (!w->spinors->nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
+    w->spec = std::make_unique<WeightSpec>(*w->spinors->nuclei, w->cfg.weight_overrides);
+    w->worker = std::make_unique<DeviceWorker>(*w->spinors, *w->spec, w->cfg, worker_index, device);
+    w->worker->init_and_burn_in();
+    out = w.release();
+  });
+  return out;
+}
+
+void mcmp2h_worker_free(mcmp2h_worker* w) { delete w; }
+
+int mcmp2h_worker_advance(mcmp2h_worker* w, long nsteps, double* values, double* imags) {
+  return guard([&] {
+    w->worker->advance(nsteps);
+    for (long s = 0; s < nsteps; ++s) {
+      if (values) values[s] = w->worker->last_values()[s];
+      if (imags) imags[s] = w->worker->last_imags()[s];
+    }
+  });
+}
+
+int mcmp2h_worker_stats(mcmp2h_worker* w, double* o) {
+  return guard([&] {
+    const auto& a = w->worker->acc;
+    o[0] = double(a.count());
+    o[1] = a.real_sum();
+    o[2] = a.imag_sum();
+    o[3] = a.mean();
+    o[4] = a.sigma_bar();
+    o[5] = double(a.in_block());
+    o[6] = a.partial();
+    o[7] = double(a.block_means().size());
+  });
+}
+
+int mcmp2h_worker_block_means(mcmp2h_worker* w, double* out, int cap) {
+  return guard([&] {
+    const auto& m = w->worker->acc.block_means();
+    for (int i = 0; i < cap && i < int(m.size()); ++i) out[i] = m[i];
+  });
+}
+
+mcmp2dev_t* mcmp2h_worker_device(mcmp2h_worker* w) { return w->worker->handle(); }
+
+int mcmp2h_generate(const char* name, const char* dir) {
+  return guard([&] { write_generated(name, dir); });
+}
+
+}  // extern "C"

@@ -1,0 +1,185 @@
+"""Python mirror of the reference's per-worker walker interface over the device C ABI.
+
+Reference surface (proj/core/include/mcmp2/): init_ensemble / burn_in / metropolis_step
+(sampler.hpp:53-64), TauSampler::sample (weights.hpp:58), mc_step_estimate / sample_term
+(estimator.hpp:51-57), WalkerEnsemble save/load (sampler.hpp:36-37). Every method is one
+C-ABI call into lib/libmcmp2dev.so; errors come back as the reference's exception kinds
+(Mcmp2ArgumentError ~ std::invalid_argument, Mcmp2Error ~ std::runtime_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import native
+from .native import Ensemble, Step, check_dev, check_host, dptr
+
+
+class System:
+    """SpinorSet + WeightSpec + TauSampler loaded by the C++ host (model.cpp:275-351)."""
+
+    def __init__(self, spinor_path: str | Path, config_text: str = ""):
+        h = native.host()
+        self._h = h.mcmp2h_system_load(str(spinor_path).encode(), config_text.encode())
+        if not self._h:
+            msg = h.mcmp2h_last_error().decode()
+            if msg.startswith(("no weight parameters", "Molecule", "BasisFunction", "SpinorSet: component",
+                               "SpinorSet: one basis", "SpinorSet: invalid", "SpinorSet: empty")):
+                raise native.Mcmp2ArgumentError(msg)
+            raise native.Mcmp2Error(msg)
+        ints = (C.c_int * 4)()
+        dbl = (C.c_double * 3)()
+        check_host(h.mcmp2h_system_info(self._h, ints, dbl))
+        self.ncomp, self.n_occ, self.n_vir, self.rows = list(ints)
+        self.ng, self.lambda_, self.orthonormality_deviation = list(dbl)
+
+    @property
+    def view(self):
+        return native.host().mcmp2h_system_view(self._h)
+
+    def g(self, pts: np.ndarray) -> np.ndarray:
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(pts))
+        check_host(native.host().mcmp2h_system_g(self._h, dptr(pts), len(pts), dptr(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            native.host().mcmp2h_system_free(self._h)
+            self._h = None
+
+
+@dataclass
+class EnsembleState:
+    """WalkerEnsemble record (sampler.cpp:95-120): walkers [m, 9] = r1, r2, g1, g2, weight."""
+    walkers: np.ndarray
+    sigma_step: float
+    proposed: int
+    accepted: int
+    rng_key: tuple
+    rng_counter: tuple
+    rng_idx: int
+
+
+class DeviceWalker:
+    """One reference worker resident on one GPU (a mcmp2dev handle)."""
+
+    def __init__(self, system: System, device: int = 0, max_walkers: int = 8):
+        self.system = system
+        self._d = native.dev()
+        h = C.c_void_p()
+        check_dev(self._d.mcmp2dev_create(system.view, device, max_walkers, C.byref(h)), None)
+        self._h = h
+        self.max_walkers = max_walkers
+        self.m = 0
+
+    # -- ensemble -------------------------------------------------------------------
+    def init_ensemble(self, m: int, seed: int, stream: int = 0) -> None:
+        check_dev(self._d.mcmp2dev_init_ensemble(self._h, m, seed, stream), self._h)
+        self.m = m
+
+    def burn_in(self, n_burn: int, adapt: bool = True) -> None:
+        check_dev(self._d.mcmp2dev_burn_in(self._h, n_burn, int(adapt)), self._h)
+
+    def set_sigma_step(self, sigma: float) -> None:
+        check_dev(self._d.mcmp2dev_set_sigma_step(self._h, sigma), self._h)
+
+    def get_ensemble(self) -> EnsembleState:
+        w = np.zeros((self.max_walkers, 9))
+        e = Ensemble()
+        e.walkers = dptr(w)
+        check_dev(self._d.mcmp2dev_get_ensemble(self._h, C.byref(e)), self._h)
+        return EnsembleState(w[: e.m].copy(), e.sigma_step, e.proposed, e.accepted, tuple(e.rng_key),
+                             tuple(e.rng_counter), e.rng_idx)
+
+    def set_ensemble(self, s: EnsembleState) -> None:
+        w = np.ascontiguousarray(s.walkers, dtype=np.float64)
+        e = Ensemble()
+        e.m = len(w)
+        e.sigma_step = s.sigma_step
+        e.proposed = s.proposed
+        e.accepted = s.accepted
+        e.rng_key[:] = s.rng_key
+        e.rng_counter[:] = s.rng_counter
+        e.rng_idx = s.rng_idx
+        e.walkers = dptr(w)
+        check_dev(self._d.mcmp2dev_set_ensemble(self._h, C.byref(e)), self._h)
+        self.m = len(w)
+
+    # -- hot loop -------------------------------------------------------------------
+    def advance(self, nsteps: int, keep_on_device: bool = False):
+        if keep_on_device:
+            check_dev(self._d.mcmp2dev_advance(self._h, nsteps, None, None), self._h)
+            return None
+        v = np.empty(nsteps)
+        im = np.empty(nsteps)
+        check_dev(self._d.mcmp2dev_advance(self._h, nsteps, dptr(v), dptr(im)), self._h)
+        return v, im
+
+    def replay(self, walkers: np.ndarray, tau: np.ndarray) -> np.ndarray:
+        """mc_step_estimate at given positions: walkers [nsteps, m, 8], tau [nsteps] ->
+        [nsteps, 6] = value, imag, direct re/im, exchange re/im (sums before /C(m,2))."""
+        walkers = np.ascontiguousarray(walkers, dtype=np.float64)
+        if walkers.ndim == 2:
+            walkers = walkers[None]
+        tau = np.ascontiguousarray(np.atleast_1d(tau), dtype=np.float64)
+        n, m, _ = walkers.shape
+        out = (Step * n)()
+        check_dev(self._d.mcmp2dev_replay(self._h, m, n, dptr(walkers), dptr(tau), out), self._h)
+        return np.array([[s.value, s.imag, s.direct_re, s.direct_im, s.exchange_re, s.exchange_im]
+                         for s in out])
+
+    # -- instrumentation ------------------------------------------------------------
+    def profile(self, enable: bool = True, reset: bool = True) -> dict:
+        out = np.zeros(8)
+        check_dev(self._d.mcmp2dev_profile(self._h, int(enable), int(reset), dptr(out)), self._h)
+        names = ("walk", "spinor", "pair", "total")
+        return {"ms": dict(zip(names, out[:4])), "launches": dict(zip(names, out[4:].astype(int)))}
+
+    def work(self) -> dict:
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check_dev(self._d.mcmp2dev_work(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h)
+        return {"pair_flop": a.value, "spinor_flop": b.value, "phi_bytes": c.value}
+
+    def synchronize(self) -> None:
+        check_dev(self._d.mcmp2dev_synchronize(self._h), self._h)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._d.mcmp2dev_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def generate_config(name: str, directory: str | Path) -> tuple[Path, Path]:
+    """Writes <dir>/<name>.spinor and <dir>/<name>.conf (host/generate.cpp)."""
+    d = Path(directory)
+    d.mkdir(parents=True, exist_ok=True)
+    check_host(native.host().mcmp2h_generate(name.encode(), str(d).encode()))
+    return d / f"{name}.spinor", d / f"{name}.conf"
+
+
+def run_config_text(text: str, abort_after_intervals: int = -1) -> str:
+    """`mcmp2 run` on config text through the C++ host; returns format_report text."""
+    buf = C.create_string_buffer(1 << 16)
+    h = native.host()
+    check_host(h.mcmp2h_run_hooked(text.encode(), abort_after_intervals, buf, len(buf)))
+    return buf.value.decode()
+
+
+def resume(checkpoint: str | Path) -> str:
+    buf = C.create_string_buffer(1 << 16)
+    check_host(native.host().mcmp2h_resume(str(checkpoint).encode(), buf, len(buf)))
+    return buf.value.decode()
+
+
+def merge(paths) -> tuple[float, float, int]:
+    arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+    v, s, n = C.c_double(), C.c_double(), C.c_longlong()
+    check_host(native.host().mcmp2h_merge(arr, len(paths), C.byref(v), C.byref(s), C.byref(n)))
+    return v.value, s.value, n.value

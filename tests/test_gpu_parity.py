@@ -1,0 +1,117 @@
+"""Parity of the device walker loop with the CPU oracle (the reference restated), through the
+C ABI. Tolerance: per-step estimates and their direct/exchange sums within 1e-10 relative
+(BASELINE.json north_star, replay layer); trajectories within the same bound."""
+import numpy as np
+import pytest
+
+import oracle_py
+from paper_2203_05632_b200 import DeviceWalker, System
+from paper_2203_05632_b200.native import Mcmp2Error
+from paper_2203_05632_b200.walker import EnsembleState
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+def rel_err(got, ref):
+    scale = np.maximum(np.abs(ref), 1e-300)
+    return float(np.max(np.abs(got - ref) / scale))
+
+
+def load(cfgdir, name):
+    sp = cfgdir / f"{name}.spinor"
+    text = (cfgdir / f"{name}.conf").read_text()
+    return sp, text, oracle_py.OracleSystem(sp, text), System(sp, text)
+
+
+@pytest.mark.parametrize("name,m,nsteps", [("cfg1", 16, 6), ("cfg2", 40, 2), ("cfg3", 24, 2), ("cfg4", 20, 1)])
+def test_replay_matches_oracle(cfgdir, name, m, nsteps):
+    sp, text, orc, sysd = load(cfgdir, name)
+    tr = orc.trajectory(seed=11, stream=0, m=m, burn=30, nsteps=nsteps)
+    dw = DeviceWalker(sysd, max_walkers=m)
+    got = dw.replay(tr["walkers"], tr["tau"])
+    ref = tr["est"]
+    assert rel_err(got[:, 0], ref[:, 0]) < REL
+    # direct and exchange pair sums separately (condition-aware: relative to their magnitude)
+    for k in (2, 4):
+        assert rel_err(got[:, k], ref[:, k]) < REL
+    # Kramers-paired 4c input: the literal estimator is real to rounding (test_estimator.cpp:149-165)
+    assert np.all(np.abs(got[:, 1]) <= 1e-8 * np.abs(got[:, 0]) + 1e-300)
+
+
+def test_sample_term_is_m2_replay(cfgdir):
+    """sample_term (estimator.cpp:65-75) == the m = 2 step; tau in {0, 0.13, 0.9}."""
+    sp, text, orc, sysd = load(cfgdir, "cfg1")
+    dw = DeviceWalker(sysd, max_walkers=2)
+    pts = np.array([[0.3, 0.1, -0.2], [-0.4, 0.5, 0.9], [0.8, -0.6, 0.1], [0.2, 0.3, -0.7]])
+    g = orc.g(pts)
+    p = np.r_[pts[0], pts[1], g[0], g[1]]
+    q = np.r_[pts[2], pts[3], g[2], g[3]]
+    for tau in (0.0, 0.13, 0.9):
+        d, x = orc.sample_term(p, q, tau)
+        got = dw.replay(np.stack([p, q])[None], np.array([tau]))[0]
+        assert abs(got[0] - (d + x).real) <= REL * abs((d + x).real)
+        assert abs(complex(got[2], got[3]) - d) <= REL * abs(d)
+        assert abs(complex(got[4], got[5]) - x) <= REL * abs(x)
+
+
+def test_relabeling_invariance(cfgdir):
+    """step estimate invariant under walker relabelling (test_estimator.cpp:128-147)."""
+    sp, text, orc, sysd = load(cfgdir, "cfg2")
+    tr = orc.trajectory(seed=21, stream=0, m=13, burn=20, nsteps=1)
+    dw = DeviceWalker(sysd, max_walkers=13)
+    a = dw.replay(tr["walkers"], tr["tau"])[0, 0]
+    perm = np.random.default_rng(3).permutation(13)
+    b = dw.replay(tr["walkers"][:, perm], tr["tau"])[0, 0]
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_device_init_and_burn_in_follow_reference_stream(cfgdir):
+    """init_ensemble + burn_in on the device consume the reference Philox stream in the
+    reference order (sampler.cpp:21-93): same positions, same sigma, same RNG state."""
+    sp, text, orc, sysd = load(cfgdir, "cfg2")
+    m = 37
+    tr = orc.trajectory(seed=5, stream=3, m=m, burn=300, nsteps=0)
+    ref = oracle_py.state_to_ensemble(tr["init"], m)
+    dw = DeviceWalker(sysd, max_walkers=m)
+    dw.init_ensemble(m, seed=5, stream=3)
+    dw.burn_in(300, adapt=True)
+    st = dw.get_ensemble()
+    assert st.sigma_step == ref["sigma_step"]
+    assert st.rng_key == ref["rng_key"] and st.rng_counter == ref["rng_counter"] and st.rng_idx == ref["rng_idx"]
+    assert np.max(np.abs(st.walkers - ref["walkers"]) / (np.abs(ref["walkers"]) + 1e-300)) < 1e-12
+    assert st.proposed == 0 and st.accepted == 0
+
+
+@pytest.mark.parametrize("name,m,nsteps,step", [("cfg1", 16, 300, 0.3), ("cfg2", 32, 40, 0.0)])
+def test_trajectory_matches_oracle(cfgdir, name, m, nsteps, step):
+    """advance(): Metropolis + tau + estimate on the device follows the oracle's chain step by
+    step when started from the oracle's post-burn-in ensemble (driver.cpp:440-450)."""
+    sp, text, orc, sysd = load(cfgdir, name)
+    tr = orc.trajectory(seed=9, stream=1, m=m, burn=100, nsteps=nsteps, step_size=step, adapt=step == 0.0)
+    dw = DeviceWalker(sysd, max_walkers=m)
+    dw.set_ensemble(EnsembleState(**oracle_py.state_to_ensemble(tr["init"], m)))
+    v, im = dw.advance(nsteps)
+    assert rel_err(v, tr["est"][:, 0]) < REL
+    fin = dw.get_ensemble()
+    ref = oracle_py.state_to_ensemble(tr["final"], m)
+    assert fin.rng_counter == ref["rng_counter"] and fin.rng_idx == ref["rng_idx"]
+    assert fin.proposed == tr["proposed"] and fin.accepted == tr["accepted"]
+    assert np.max(np.abs(fin.walkers - ref["walkers"]) / (np.abs(ref["walkers"]) + 1e-300)) < 1e-10
+
+
+def test_overflow_is_reported_with_spinor_index(cfgdir, tmp_path):
+    """guarded_exp above +700 raises with the spinor index (greens.cpp:9-16, test_greens.cpp:198-202)."""
+    sp = cfgdir / "cfg1.spinor"
+    text = sp.read_text().replace("\n-0.90000000000000002\n-0.90000000000000002\n", "\n0.05\n0.05\n")
+    bad = tmp_path / "posocc.spinor"
+    bad.write_text(text)
+    conf = (cfgdir / "cfg1.conf").read_text()
+    dw = DeviceWalker(System(bad, conf), max_walkers=2)
+    pts = np.zeros((2, 8))
+    pts[:, 6:] = 0.1
+    pts[0, :3] = 0.1
+    pts[1, 3:6] = -0.2
+    with pytest.raises(Mcmp2Error, match="spinor 0"):
+        dw.replay(pts[None], np.array([20000.0]))
