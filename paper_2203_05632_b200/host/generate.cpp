@@ -32,6 +32,7 @@ struct Shell {
   Vec3 center;
   int l;
   double zeta;
+  std::vector<Primitive> prims;  // contracted shell when non-empty (else one unit primitive)
 };
 
 struct Recipe {
@@ -47,11 +48,12 @@ struct Recipe {
   std::optional<double> step_size;
   std::vector<std::string> weights;  // weight lines
   std::uint64_t seed;
+  int ncomp = 4;  // 1: real spatial orbitals (L only); 2: (alpha, beta) Kramers pairs; 4: Dirac
 };
 
 void even_tempered(std::vector<Shell>& out, const Vec3& c, int l, int n, double base, double ratio) {
   double z = base;
-  for (int k = 0; k < n; ++k, z *= ratio) out.push_back({c, l, z});
+  for (int k = 0; k < n; ++k, z *= ratio) out.push_back({c, l, z, {}});
 }
 
 // sequential reference-order Philox uniforms (rng.cpp:46-64)
@@ -118,6 +120,22 @@ Recipe recipe(const std::string& name) {
     r.steps = 20000;
     r.weights = {"weight I 0.1 0.1 0.8 0.6"};
     r.seed = 0x22030004ull;
+  } else if (name == "syn1c" || name == "syn2c") {  // small H2-like test sets (contracted s)
+    const Vec3 h{0, 0, 1.4};
+    r.nuclei = {{1.0, o}, {1.0, h}};
+    for (const Vec3& c : {o, h}) {
+      r.shells.push_back({c, 0, 0.0, {{3.4, 0.15}, {0.62, 0.53}, {0.17, 0.44}}});
+      r.shells.push_back({c, 0, 0.12, {}});
+      r.shells.push_back({c, 1, 0.8, {}});
+    }
+    r.ncomp = name == "syn1c" ? 1 : 2;
+    r.occ_pairs = 1;
+    r.occ_lo = r.occ_hi = -0.6;
+    r.occ_fixed = true;
+    r.vir_lo = 0.2, r.vir_hi = 5.0;
+    r.walkers = 8;
+    r.steps = 2000;
+    r.seed = name == "syn1c" ? 0x22031001ull : 0x22032001ull;
   } else if (name.rfind("cfg5-", 0) == 0) {  // size sweep: single centre, Z = n_elec
     const int n = std::stoi(name.substr(5));
     static const std::map<int, std::string> el = {{2, "He"}, {10, "Ne"}, {18, "Ar"},
@@ -147,7 +165,8 @@ Recipe recipe(const std::string& name) {
 
 // (l, m) functions of one shell in SPINOR-TEXT order m = -l..l
 void shell_functions(const Shell& s, std::vector<BasisFunction>& out) {
-  for (int m = -s.l; m <= s.l; ++m) out.emplace_back(s.center, s.l, m, std::vector<Primitive>{{s.zeta, 1.0}});
+  for (int m = -s.l; m <= s.l; ++m)
+    out.emplace_back(s.center, s.l, m, s.prims.empty() ? std::vector<Primitive>{{s.zeta, 1.0}} : s.prims);
 }
 
 }  // namespace
@@ -156,14 +175,17 @@ SpinorSet generate_spinor_set(const std::string& name) {
   const Recipe r = recipe(name);
   std::vector<BasisFunction> L, S;
   for (const auto& sh : r.shells) shell_functions(sh, L);
-  for (const auto& sh : r.shells) {  // kinetic-balance partners l -> l-1, l+1
-    if (sh.l > 0) shell_functions({sh.center, sh.l - 1, sh.zeta}, S);
-    shell_functions({sh.center, sh.l + 1, sh.zeta}, S);
-  }
+  if (r.ncomp == 4)
+    for (const auto& sh : r.shells) {  // kinetic-balance partners l -> l-1, l+1
+      if (sh.prims.size() > 1) throw std::invalid_argument("generate: kinetic balance of contracted shells");
+      if (sh.l > 0) shell_functions({sh.center, sh.l - 1, sh.zeta, {}}, S);
+      shell_functions({sh.center, sh.l + 1, sh.zeta, {}}, S);
+    }
+  const int nc = r.ncomp;
   const int nL = int(L.size()), nS = int(S.size());
-  const int R = 2 * nL + 2 * nS;
-  const int npairs = nL;  // n_p = 2 n_L positive-energy spinors
-  const int ncols = 2 * npairs;
+  const int R = nc == 4 ? 2 * nL + 2 * nS : nc * nL;
+  const int npairs = nL;  // n_p = nc/2 * 2 n_L positive-energy spinors (1c: n_L orbitals)
+  const int ncols = nc == 1 ? nL : 2 * npairs;
 
   // channel overlap matrices
   auto overlap = [](const std::vector<BasisFunction>& b) {
@@ -178,7 +200,7 @@ SpinorSet generate_spinor_set(const std::string& name) {
   const int len[4] = {nL, nL, nS, nS};
   auto apply_s = [&](const std::vector<Complex>& v) {
     std::vector<Complex> out(R, Complex(0, 0));
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < nc; ++c) {
       const std::vector<double>& Sm = c < 2 ? SL : SS;
       const int n = len[c];
       for (int i = 0; i < n; ++i) {
@@ -196,7 +218,7 @@ SpinorSet generate_spinor_set(const std::string& name) {
   };
   auto kramers = [&](const std::vector<Complex>& v) {
     std::vector<Complex> w(R);
-    for (int d = 0; d < 2; ++d) {
+    for (int d = 0; d < nc / 2; ++d) {
       const int a = off[2 * d], b = off[2 * d + 1], n = len[2 * d];
       for (int i = 0; i < n; ++i) {
         w[a + i] = -std::conj(v[b + i]);
@@ -210,20 +232,22 @@ SpinorSet generate_spinor_set(const std::string& name) {
   // energies (one per Kramers pair), drawn before the coefficients
   std::vector<double> occ(r.occ_pairs), vir(npairs - r.occ_pairs);
   if (r.occ_pairs > npairs) throw std::invalid_argument("generate: more occupied pairs than basis pairs");
+  if (nc == 1) vir.resize(nL - r.occ_pairs);
   for (auto& e : occ) e = r.occ_fixed ? r.occ_lo : r.occ_lo + (r.occ_hi - r.occ_lo) * u.next();
   for (auto& e : vir) e = std::exp(std::log(r.vir_lo) + (std::log(r.vir_hi) - std::log(r.vir_lo)) * u.next());
   std::sort(occ.begin(), occ.end());
   std::sort(vir.begin(), vir.end());
   std::vector<double> eps;
-  for (double e : occ) eps.insert(eps.end(), {e, e});
-  for (double e : vir) eps.insert(eps.end(), {e, e});
+  const int per = nc == 1 ? 1 : 2;  // spinors per energy
+  for (double e : occ) eps.insert(eps.end(), std::size_t(per), e);
+  for (double e : vir) eps.insert(eps.end(), std::size_t(per), e);
 
   std::vector<std::vector<Complex>> cols, scols;  // columns and S * columns
-  for (int p = 0; p < npairs; ++p) {
+  for (int p = 0; p < (nc == 1 ? ncols : npairs); ++p) {
     std::vector<Complex> v(R);
     for (auto& c : v) {
       const double re = u.next() - 0.5;
-      const double im = u.next() - 0.5;
+      const double im = nc == 1 ? 0.0 : u.next() - 0.5;  // 1c: real orbitals
       c = Complex(re, im);
     }
     for (int rep = 0; rep < 2; ++rep)
@@ -239,14 +263,19 @@ SpinorSet generate_spinor_set(const std::string& name) {
     std::vector<Complex> sk = apply_s(k);
     cols.push_back(std::move(v));
     scols.push_back(std::move(sv));
+    if (nc == 1) continue;
     cols.push_back(std::move(k));
     scols.push_back(std::move(sk));
   }
   std::vector<Complex> coeff(std::size_t(R) * ncols);
   for (int j = 0; j < ncols; ++j)
     for (int i = 0; i < R; ++i) coeff[std::size_t(i) * ncols + j] = cols[j][i];
-  return SpinorSet(4, {L, L, S, S}, std::move(coeff), std::move(eps), 2 * r.occ_pairs, ncols - 2 * r.occ_pairs,
-                   r.nuclei);
+  std::vector<std::vector<BasisFunction>> channels;
+  if (nc == 4) channels = {L, L, S, S};
+  else if (nc == 2) channels = {L, L};
+  else channels = {L};
+  const int nocc = per * r.occ_pairs;
+  return SpinorSet(nc, std::move(channels), std::move(coeff), std::move(eps), nocc, ncols - nocc, r.nuclei);
 }
 
 std::string generate_run_config(const std::string& name, const std::string& spinor_path) {
