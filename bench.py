@@ -1,0 +1,275 @@
+#!/usr/bin/env python
+"""Benchmark of the MC-MP2 walker loop (BASELINE.json metric: walker-pair x tau samples/s).
+
+One step = one pass of the hot path over one ensemble: Metropolis sweep of m walker pairs,
+tau draw, spinor values + MO transform at 2m points, O/V Green's-function blocks and the
+fused direct/exchange integrand over all C(m,2) walker pairs, block reduction
+(reference driver.cpp:440-450). samples/step = C(m,2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU; each rank is one reference worker (its own
+ensemble, Philox stream = rank, driver.cpp:354-356), so per-GPU work is fixed ("weak").
+`--impl reference` times the CPU restatement of the reference path (oracle/, the reference
+itself needs Eigen3 and cannot be built here) on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "MC-MP2 walker-pair x tau samples/sec"
+UNIT = "samples/s"
+WALKERS = {"cfg1": 16, "cfg2": 128, "cfg3": 512, "cfg4": 2048}
+WORKLOAD = {
+    "cfg1": "2e atom, 4c, 12s L + 36p S, n_occ 2, n_vir 22, m 16",
+    "cfg2": "10e atom, 4c, 14s9p L (R 274), n_occ 10, n_vir 72, m 128",
+    "cfg3": "18e diatomic, 4c, 17s12p4d+6s2p L (R 556), n_occ 18, n_vir 152, m 512",
+    "cfg4": "54e heavy diatomic, 4c, 24s20p14d+6s2p L (R 1056), n_occ 54, n_vir 278, m 2048/GPU",
+}
+
+
+def clocks_sampler(path: Path):
+    """nvidia-smi clocks + throttle reasons every 200 ms during the timed region."""
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        f = open(path, "w")
+        return subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                                stdout=f, stderr=subprocess.DEVNULL), f
+    except (OSError, FileNotFoundError):
+        return None, None
+
+
+def clocks_summary(path: Path, index: int):
+    rows = []
+    try:
+        for line in path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[0] == str(index):
+                rows.append(parts)
+    except OSError:
+        return None
+    if not rows:
+        return None
+    sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+    reasons = set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for r in rows:
+        for n, v in zip(names, r[5:9]):
+            if v.lower().startswith("active"):
+                reasons.add(n)
+    return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+            "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def peaks():
+    fp64 = json.loads((ROOT / "MEASURED_FP64.json").read_text())
+    return fp64["dmma_tflops"], "MEASURED_FP64.json dmma_tflops (mma.sync m8n8k4 f64 loop on this pool's B200)"
+
+
+def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, quick: bool):
+    """CPU restatement (oracle/, kind 'port') on all host cores, bounded sample per step."""
+    import oracle_py
+    threads = os.cpu_count() or 1
+    orc = oracle_py.OracleSystem(spinor, conf_text)
+    m = WALKERS[cfg]
+    npairs = m * (m - 1) // 2
+    step_size = 0.3 if cfg == "cfg1" else 0.0
+    full = cfg in ("cfg1", "cfg2")
+    if full:  # whole steps fit the time budget
+        if warmup:
+            orc.cpu_baseline(seed=1, m=m, rows=m, burn=20, step_size=step_size, steps=warmup, threads=threads)
+        sec, samples = orc.cpu_baseline(seed=1, m=m, rows=m, burn=20, step_size=step_size, steps=steps,
+                                        threads=threads)
+        return {"value": samples / sec, "unit": UNIT, "cores": threads, "kind": "port", "seconds": sec,
+                "samples": samples, "sample": f"{threads} workers (std::thread, driver.cpp:423-438) x {steps} "
+                f"full steps of m={m}"}
+    # bounded sample: per worker one step restricted to walker rows [0, r) of the pair loop (Metropolis
+    # and spinor values always cover all 2m points); two row counts give the fixed O(m) cost and the
+    # per-sample cost, extrapolated to the full C(m,2) step and stated as such.
+    ra, rb = {"cfg3": (8, 40), "cfg4": (4, 20)}[cfg] if not quick else (1, 2)
+    reps = max(1, steps // 5)
+    ta, na = orc.cpu_baseline(seed=1, m=m, rows=ra, burn=5, step_size=step_size, steps=reps, threads=threads)
+    tb, nb = orc.cpu_baseline(seed=1, m=m, rows=rb, burn=5, step_size=step_size, steps=reps, threads=threads)
+    # ta = reps*T0 + c*na/threads (workers run concurrently), same for tb
+    c = (tb - ta) * threads / max(nb - na, 1)                # s per sample per worker
+    t0 = max(ta - c * na / threads, 0.0) / reps              # fixed s per step per worker
+    t_full = t0 + c * npairs
+    value = threads * npairs / t_full
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "seconds": ta + tb,
+            "samples": na + nb,
+            "sample": f"{threads} workers x {reps} step(s) at walker rows [0,{ra}) and [0,{rb}) of m={m} "
+                      f"({na + nb} pair samples, {ta + tb:.1f} s); full-step rate extrapolated linearly "
+                      f"(fixed {t0:.2f} s/step + {c * 1e6:.2f} us/sample per worker)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(WALKERS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--burnin", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = args.config
+    m = WALKERS[cfg]
+    from paper_2203_05632_b200 import generate_config
+
+    tmp = Path(tempfile.mkdtemp(prefix=f"mcmp2_bench_r{rank}_"))
+    spinor, conf = generate_config(cfg, tmp)
+    conf_text = conf.read_text()
+    samples_per_step = m * (m - 1) // 2
+    config = {"workload": f"{cfg}: {WORKLOAD[cfg]}", "walkers_per_gpu": m, "samples_per_step_per_gpu": samples_per_step,
+              "estimator": "literal (reference estimator.cpp:26-32)", "rng": "reference Philox stream per worker"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        leg = cpu_leg(cfg, spinor, conf_text, args.steps, args.warmup, quick=False)
+        line = {"metric": METRIC, "value": leg["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * leg["seconds"] / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/c128",
+                "data": "synthetic (seeded, host/generate.cpp)", "config": config,
+                "cpu_baseline": {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": leg["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2203_05632_b200 import DeviceWalker, System
+
+    sysd = System(spinor, conf_text)
+    dw = DeviceWalker(sysd, device=local, max_walkers=m)
+    dw.init_ensemble(m, seed=1, stream=rank)
+    if cfg == "cfg1":
+        dw.set_sigma_step(0.3)
+        dw.burn_in(args.burnin, adapt=False)
+    else:
+        dw.burn_in(args.burnin, adapt=True)
+    stream = torch.cuda.ExternalStream(dw.stream_ptr, device=torch.device("cuda", local))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    # warm-up
+    dw.advance(args.warmup, keep_on_device=True)
+    dw.synchronize()
+
+    # ---- timed region: K steps, device time per step on the handle's stream, L2 flushed between ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    smi, smi_f = clocks_sampler(tmp / "clocks.csv") if rank == 0 else (None, None)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            ev[k][0].record(stream)
+        dw.advance(1, keep_on_device=True)
+        with torch.cuda.stream(stream):
+            ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    if smi:
+        time.sleep(0.25)
+        smi.terminate()
+        smi_f.close()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(ms_steps)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = world * samples_per_step * args.steps / (t_max / 1e3)
+
+    # ---- per-kernel device time (profiling pass, events around each launch) ----
+    dw.profile(enable=True, reset=True)
+    nprof = max(2, min(args.steps, 5))
+    dw.advance(nprof, keep_on_device=True)
+    prof = dw.profile(enable=False, reset=True)
+    work = dw.work()
+    pair_ms = prof["ms"]["pair"] / prof["launches"]["pair"]
+    step_ms_prof = prof["ms"]["total"] / prof["launches"]["total"]
+    peak, peak_src = peaks()
+    achieved = work["pair_flop"] / (pair_ms / 1e3) / 1e12
+
+    # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
+    st = dw.get_ensemble()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    dw.set_ensemble(st)                              # H2D walker state (resume)
+    vals, ims = dw.advance(args.steps)               # every step's (value, imag) D2H
+    st2 = dw.get_ensemble()                          # D2H walker state (checkpoint)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * samples_per_step * args.steps / float(te.item())
+    state_bytes = m * 9 * 8 + 64
+    h2d = state_bytes / args.steps
+    d2h = 16 + state_bytes / args.steps
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64/c128", "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
+        "config": dict(config, parallelism=f"{world} independent workers (1 per GPU)",
+                       l2="flushed between timed steps (256 MiB write on the handle's stream)"),
+        "roofline": {"bound": "tensor", "kernel": "pair_kernel (DMMA m8n8k4 f64)", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "pair_flop_per_launch": work["pair_flop"], "pair_ms_per_launch": pair_ms,
+                     "pair_share_of_step": prof["ms"]["pair"] / prof["ms"]["total"],
+                     "spinor_ms_per_launch": prof["ms"]["spinor"] / prof["launches"]["spinor"],
+                     "walk_ms_per_launch": prof["ms"]["walk"] / prof["launches"]["walk"],
+                     "step_ms_profiled": step_ms_prof},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"},
+        "gpu_launches": 3 * args.steps,
+        "step_values_checksum": float(np.sum(vals)),
+    }
+    cl = clocks_summary(tmp / "clocks.csv", local)
+    if cl:
+        line["clocks"] = cl
+    if world == 1 and not args.no_cpu_baseline:
+        leg = cpu_leg(cfg, spinor, conf_text, steps=1, warmup=0, quick=False)
+        line["cpu_baseline"] = {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

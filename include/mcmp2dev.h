@@ -123,6 +123,8 @@ int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out);
 int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes);
 /* synchronise the handle's stream */
 int mcmp2dev_synchronize(mcmp2dev_t* h);
+/* the handle's cudaStream_t (as void*), for callers that time or order work around it */
+void* mcmp2dev_stream(mcmp2dev_t* h);
 
 #ifdef __cplusplus
 }

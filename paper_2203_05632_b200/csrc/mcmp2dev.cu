@@ -581,6 +581,8 @@ int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double*
   });
 }
 
+void* mcmp2dev_stream(mcmp2dev_t* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
 int mcmp2dev_synchronize(mcmp2dev_t* h) {
   return guard(h, [&] { ck(cudaStreamSynchronize(h->stream), "stream sync"); });
 }

@@ -77,6 +77,8 @@ def dev() -> C.CDLL:
         d.mcmp2dev_profile.argtypes = [vp, ip, ip, dp]
         d.mcmp2dev_work.argtypes = [vp, dp, dp, dp]
         d.mcmp2dev_synchronize.argtypes = [vp]
+        d.mcmp2dev_stream.restype = vp
+        d.mcmp2dev_stream.argtypes = [vp]
         d.mcmp2dev_abi_version.restype = ip
         _dev = d
     return _dev

@@ -144,6 +144,10 @@ class DeviceWalker:
         check_dev(self._d.mcmp2dev_work(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h)
         return {"pair_flop": a.value, "spinor_flop": b.value, "phi_bytes": c.value}
 
+    @property
+    def stream_ptr(self) -> int:
+        return int(self._d.mcmp2dev_stream(self._h))
+
     def synchronize(self) -> None:
         check_dev(self._d.mcmp2dev_synchronize(self._h), self._h)
 
