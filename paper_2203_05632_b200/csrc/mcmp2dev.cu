@@ -51,6 +51,14 @@ T* dalloc(size_t n, std::vector<void*>& owned) {
   return static_cast<T*>(p);
 }
 
+// copies ordered on the handle's (non-blocking) stream, then waited for: a plain cudaMemcpy
+// runs on the legacy stream, which does not order against cudaStreamNonBlocking streams
+cudaError_t scopy(cudaStream_t s, void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, n, kind, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
 template <class T>
 T* dupload(const T* src, size_t n, std::vector<void*>& owned) {
   T* d = dalloc<T>(n, owned);
@@ -178,10 +186,10 @@ struct mcmp2dev_handle {
 
   void reset_errors() {
     DevState st;
-    ck(cudaMemcpy(&st, d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    ck(scopy(stream, &st, d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
     st.error = 0;
     st.error_idx = INT_MAX;
-    ck(cudaMemcpy(d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    ck(scopy(stream, d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   }
 };
 
@@ -323,7 +331,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   DevState st{};
   st.sigma = 1.0;  // sampler.hpp:45
   st.error_idx = INT_MAX;
-  ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+  ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   h->d_block_acc = dalloc<int>((max_walkers + 127) / 128 + 1, o);
   const size_t phi_doubles = size_t(h->Gtot) * h->npts_pad * 32;
   h->d_phi = dalloc<double>(phi_doubles, o);
@@ -417,18 +425,18 @@ int mcmp2dev_burn_in(mcmp2dev_t* h, long n_burn, int adapt) {
   return guard(h, [&] {
     require_ensemble(h);
     DevState st;
-    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
     st.win_acc = st.win_prop = 0;
-    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
     for (long s = 1; s <= n_burn; ++s) {
       launch_walk(h->walk_params(WALK_BURN, s, adapt), h->stream);
       h->cur ^= 1;
     }
     ck(cudaGetLastError(), "walk launch");
-    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
     st.proposed = st.accepted = 0;  // sampler.cpp:92
     st.win_acc = st.win_prop = 0;
-    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   });
 }
 
@@ -453,7 +461,7 @@ int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e) {
     std::vector<double> soa(size_t(9) * h->buf[0].mmax, 0.0);
     for (int p = 0; p < e->m; ++p)
       for (int k = 0; k < 9; ++k) soa[size_t(k) * h->buf[0].mmax + p] = e->walkers[size_t(p) * 9 + k];
-    ck(cudaMemcpy(h->buf[h->cur].w, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice),
+    ck(scopy(h->stream, h->buf[h->cur].w, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice),
        "walkers H2D");
     DevState st{};
     st.pos = pos;
@@ -461,7 +469,7 @@ int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e) {
     st.proposed = e->proposed;
     st.accepted = e->accepted;
     st.error_idx = INT_MAX;
-    ck(cudaMemcpy(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
     h->have_ensemble = true;
   });
 }
@@ -472,9 +480,9 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e) {
     if (!e || !e->walkers) throw ArgError("get_ensemble: null ensemble");
     ck(cudaStreamSynchronize(h->stream), "stream sync");
     DevState st;
-    ck(cudaMemcpy(&st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
     std::vector<double> soa(size_t(9) * h->buf[0].mmax);
-    ck(cudaMemcpy(soa.data(), h->buf[h->cur].w, soa.size() * sizeof(double), cudaMemcpyDeviceToHost),
+    ck(scopy(h->stream, soa.data(), h->buf[h->cur].w, soa.size() * sizeof(double), cudaMemcpyDeviceToHost),
        "walkers D2H");
     e->m = h->m;
     for (int p = 0; p < h->m; ++p)
