@@ -48,6 +48,12 @@ mcmp2dev_t* mcmp2h_worker_device(mcmp2h_worker* w);
 /* writes <dir>/<name>.spinor and <dir>/<name>.conf for BASELINE configs cfg1..cfg4, cfg5-N */
 int mcmp2h_generate(const char* name, const char* dir);
 
+/* host-side pieces of the reference surface, for the CPU test suite */
+int mcmp2h_blocking(const double* values, long n, long block_size, double* out4);
+int mcmp2h_merge_estimates(const double* parts, int n, double* out3);
+uint64_t mcmp2h_config_hash(const char* config_text, uint64_t spinor_hash);
+int mcmp2h_philox_stream(uint64_t seed, uint32_t stream, uint64_t pos, int n, uint32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -283,3 +283,20 @@ int orc_cpu_baseline(void* h, std::uint64_t seed, int m, int rows, long burn, do
 }
 
 }  // extern "C"
+
+extern "C" {
+double orc_tau_sample(double lambda, double u) { return TauSampler(lambda).sample(u); }
+double orc_tau_pdf(double lambda, double tau) { return TauSampler(lambda).pdf(tau); }
+
+// BlockingAccumulator over a value stream: out = mean, sigma, sigma_bar, nblocks
+int orc_blocking(const double* v, long n, long nb, double* out) {
+  return guard([&] {
+    BlockingAccumulator a(nb);
+    for (long i = 0; i < n; ++i) a.add(v[i]);
+    out[0] = a.mean();
+    out[1] = a.sigma();
+    out[2] = a.sigma_bar();
+    out[3] = double(a.block_means().size());
+  });
+}
+}

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/mcmp2host.h"
+#include "../csrc/philox.h"
 #include "mcmp2.hpp"
 
 using namespace mcmp2;
@@ -177,6 +178,49 @@ mcmp2dev_t* mcmp2h_worker_device(mcmp2h_worker* w) { return w->worker->handle();
 
 int mcmp2h_generate(const char* name, const char* dir) {
   return guard([&] { write_generated(name, dir); });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// BlockingAccumulator (estimator.cpp:77-121) over a value stream: mean, sigma, sigma_bar, nblocks
+int mcmp2h_blocking(const double* v, long n, long nb, double* out) {
+  return guard([&] {
+    BlockingAccumulator a(nb);
+    for (long i = 0; i < n; ++i) a.add(v[i]);
+    out[0] = a.mean();
+    out[1] = a.sigma();
+    out[2] = a.sigma_bar();
+    out[3] = double(a.block_means().size());
+  });
+}
+
+// merge_estimates (driver.cpp:183-196): parts as {steps, mean, sigma_bar} rows
+int mcmp2h_merge_estimates(const double* parts, int n, double* out3) {
+  return guard([&] {
+    std::vector<WorkerSummary> v;
+    for (int i = 0; i < n; ++i)
+      v.push_back(WorkerSummary{i, (long long)parts[3 * i], parts[3 * i + 1], parts[3 * i + 2], 0.0, 0.0});
+    const MergedEstimate m = merge_estimates(v);
+    out3[0] = m.value;
+    out3[1] = m.sigma_bar;
+    out3[2] = double(m.total_steps);
+  });
+}
+
+uint64_t mcmp2h_config_hash(const char* config_text, uint64_t spinor_hash) {
+  uint64_t h = 0;
+  guard([&] { h = config_hash(parse_config_text(config_text), spinor_hash); });
+  return h;
+}
+
+// u32 draws [pos, pos + n) of the reference stream PhiloxRng(seed, stream), addressed by
+// position exactly as the device kernels do (csrc/philox.h)
+int mcmp2h_philox_stream(uint64_t seed, uint32_t stream, uint64_t pos, int n, uint32_t* out) {
+  mcmp2dev::StreamReader r(uint32_t(seed), uint32_t(seed >> 32), stream, pos);
+  for (int i = 0; i < n; ++i) out[i] = r.next_u32();
+  return 0;
 }
 
 }  // extern "C"

@@ -47,6 +47,9 @@ def lib() -> C.CDLL:
         L.orc_sample_term.argtypes = [vp, dp, dp, C.c_double, ip, dp]
         L.orc_run_config.argtypes = [C.c_char_p, C.c_char_p, ip]
         L.orc_resume.argtypes = [C.c_char_p, C.c_char_p, ip]
+        L.orc_tau_sample.restype = C.c_double
+        L.orc_tau_sample.argtypes = [C.c_double, C.c_double]
+        L.orc_blocking.argtypes = [dp, C.c_long, C.c_long, dp]
         L.orc_cpu_baseline.argtypes = [vp, C.c_uint64, ip, ip, C.c_long, C.c_double, C.c_long, ip, dp,
                                        C.POINTER(C.c_longlong)]
         _lib = L
