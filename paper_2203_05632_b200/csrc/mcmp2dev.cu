@@ -301,9 +301,10 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;
   sp.n_p = h->n_p;
-  h->Go = (h->n_occ + 3) / 4;
+  // occupied k-groups padded to whole pair-kernel chunks, so O and V phases never share a stage
+  h->Go = ((h->n_occ + 3) / 4 + KC4 - 1) / KC4 * KC4;
   h->Gv = (h->n_vir + 3) / 4;
-  h->Gtot = (h->Go + h->Gv + KC4 - 1) / KC4 * KC4;
+  h->Gtot = h->Go + (h->Gv + KC4 - 1) / KC4 * KC4;
   sp.Go = h->Go;
   sp.Gtot = h->Gtot;
   h->d_energies = dupload(s->energies, size_t(h->n_p), o);

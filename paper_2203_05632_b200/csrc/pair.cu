@@ -31,7 +31,7 @@ constexpr int THREADS = 256;
 constexpr int HALF_PTS = 2 * WB;                          // 16 points per walker block
 constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;    // 32 points x KC4 groups x 32
 constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per stage
-constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + 64;
+constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + (THREADS / 32) * 512 * 8 + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return uint32_t(__cvta_generic_to_shared(p));
@@ -73,15 +73,6 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// C += A conj(B)^T with real-split fragments: re += ar br + ai bi, im += ai br - ar bi
-__device__ __forceinline__ void cmma(double (&re)[2], double (&im)[2], double ar, double ai,
-                                     double nar, double br, double bi) {
-  dmma(re, ar, br);
-  dmma(re, ai, bi);
-  dmma(im, ai, br);
-  dmma(im, nar, bi);
-}
-
 __device__ __forceinline__ void tile_coords(int t, int& bq, int& bp) {
   // t = bq (bq + 1) / 2 + bp, 0 <= bp <= bq
   int q = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
@@ -94,7 +85,7 @@ __device__ __forceinline__ void tile_coords(int t, int& bq, int& bp) {
 
 __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_DOUBLES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_DOUBLES + (THREADS / 32) * 512);
   __shared__ double s_red[THREADS / 32][4];
   __shared__ bool s_last;
 
@@ -121,68 +112,55 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   if (tid == 0)
     for (int s = 0; s < STAGES && s < nchunks; ++s) issue(s, s);
 
-  double vre[2][4][2], vim[2][4][2], ore[2][2][2], oim[2][2][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) vre[i][j][0] = vre[i][j][1] = vim[i][j][0] = vim[i][j][1] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) ore[i][j][0] = ore[i][j][1] = oim[i][j][0] = oim[i][j][1] = 0.0;
-
   const int hl = lane >> 4, l16 = lane & 15;
-  for (int c = 0; c < nchunks; ++c) {
-    const int stage = c % STAGES;
-    mbar_wait(&full[stage], uint32_t((c / STAGES) & 1));
-    const double* S = sm + stage * STAGE_DOUBLES;
+  const int cO = P.Go / KC4;  // occupied groups are padded to whole chunks
+  double* sO = sm + STAGES * STAGE_DOUBLES + warp * 512;  // [e][qi][pj][y][x] complex o
+  int c = 0;
+  auto wait_stage = [&](int cc) -> const double* {
+    const int stage = cc % STAGES;
+    mbar_wait(&full[stage], uint32_t((cc / STAGES) & 1));
+    return sm + stage * STAGE_DOUBLES;
+  };
+  auto release_stage = [&](int cc) {
+    __syncthreads();
+    if (tid == 0 && cc + STAGES < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(cc + STAGES, cc % STAGES);
+    }
+  };
+
+  // ---- phase 1: O~_e(q,y; p,x) = sum_i Phi_o(q,e,y,i) conj Phi_o(p,e,x,i), 3M products:
+  //      t1 = ar br, t2 = ai bi, t3 = (ar + ai)(br - bi); re = t1 + t2, im = t3 - t1 + t2 ----
+  {
+    double t1[2][2][2], t2[2][2][2], t3[2][2][2];
 #pragma unroll
-    for (int gg = 0; gg < KC4; ++gg) {
-      const int g = c * KC4 + gg;
-      auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
-      if (g < P.Go) {
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
+    for (; c < cO; ++c) {
+      const double* S = wait_stage(c);
+#pragma unroll
+      for (int gg = 0; gg < KC4; ++gg) {
+        auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int pa = 2 * (2 * wq + hl) + e;
-          const double ar = frag(pa, 0), ai = frag(pa, 1), nar = -ar;
+          const double ar = frag(pa, 0), ai = frag(pa, 1), sa = ar + ai;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int pb = HALF_PTS + 2 * (4 * wp + 2 * h + hl) + e;
-            cmma(ore[e][h], oim[e][h], ar, ai, nar, frag(pb, 0), frag(pb, 1));
+            const double br = frag(pb, 0), bi = frag(pb, 1);
+            dmma(t1[e][h], ar, br);
+            dmma(t2[e][h], ai, bi);
+            dmma(t3[e][h], sa, br - bi);
           }
         }
-      } else if (g < P.Go + P.Gv) {
-        double ar[2], ai[2], br[4], bi[4];
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-          const int pa = 2 * (2 * wq + qi) + hl;
-          ar[qi] = frag(pa, 0);
-          ai[qi] = frag(pa, 1);
-        }
-#pragma unroll
-        for (int pj = 0; pj < 4; ++pj) {
-          const int pb = HALF_PTS + 2 * (4 * wp + pj) + hl;
-          br[pj] = frag(pb, 0);
-          bi[pj] = frag(pb, 1);
-        }
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-          const double nar = -ar[qi];
-#pragma unroll
-          for (int pj = 0; pj < 4; ++pj) cmma(vre[qi][pj], vim[qi][pj], ar[qi], ai[qi], nar, br[pj], bi[pj]);
-        }
       }
+      release_stage(c);
     }
-    __syncthreads();
-    if (tid == 0 && c + STAGES < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(c + STAGES, stage);
-    }
-  }
-
-  // ---- epilogue: o = conj(O~) through shared memory, literal contraction in registers ----
-  double* sO = sm + warp * 512;  // [e][qi][pj][y][x] complex (stage memory is free now)
-  {
+    // o = conj(O~) into this warp's smem slot
     const int qi = hl, y = (lane >> 2) & 3;
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -192,11 +170,51 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
         for (int j = 0; j < 2; ++j) {
           const int pj = 2 * h + ((lane & 3) >> 1), x = 2 * (lane & 1) + j;
           const int idx = ((((e * 2 + qi) * 4 + pj) * 16) + y * 4 + x) * 2;
-          sO[idx] = ore[e][h][j];
-          sO[idx + 1] = -oim[e][h][j];
+          sO[idx] = t1[e][h][j] + t2[e][h][j];
+          sO[idx + 1] = -(t3[e][h][j] - t1[e][h][j] + t2[e][h][j]);
         }
   }
+
+  // ---- phase 2: V(q,e_q,x; p,e_p,y) = sum_a Phi_v(q,e_q,x,a) conj Phi_v(p,e_p,y,a), 3M ----
+  double u1[2][4][2], u2[2][4][2], u3[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
+  for (; c < nchunks; ++c) {
+    const double* S = wait_stage(c);
+#pragma unroll
+    for (int gg = 0; gg < KC4; ++gg) {
+      if (c * KC4 + gg >= P.Go + P.Gv) break;  // zero padding at the end
+      auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+      double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi) {
+        const int pa = 2 * (2 * wq + qi) + hl;
+        ar[qi] = frag(pa, 0);
+        ai[qi] = frag(pa, 1);
+        sa[qi] = ar[qi] + ai[qi];
+      }
+#pragma unroll
+      for (int pj = 0; pj < 4; ++pj) {
+        const int pb = HALF_PTS + 2 * (4 * wp + pj) + hl;
+        br[pj] = frag(pb, 0);
+        bi[pj] = frag(pb, 1);
+        db[pj] = br[pj] - bi[pj];
+      }
+#pragma unroll
+      for (int qi = 0; qi < 2; ++qi)
+#pragma unroll
+        for (int pj = 0; pj < 4; ++pj) {
+          dmma(u1[qi][pj], ar[qi], br[pj]);
+          dmma(u2[qi][pj], ai[qi], bi[pj]);
+          dmma(u3[qi][pj], sa[qi], db[pj]);
+        }
+    }
+    release_stage(c);
+  }
   __syncwarp();
+
   double acc_dr = 0.0, acc_di = 0.0, acc_xr = 0.0, acc_xi = 0.0;
   const double wtau = P.st_ro->wtau;
   const int eq = hl, xx = (lane >> 2) & 3, ep = (lane & 3) >> 1;
@@ -210,7 +228,8 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
         const int y = 2 * (lane & 1) + j;
         const int idx = ((((ep * 2 + qi) * 4 + pj) * 16) + y * 4 + xx) * 2;
         const double orr = sO[idx], oii = sO[idx + 1];
-        const double vr = vre[qi][pj][j], vi = vim[qi][pj][j];
+        const double vr = u1[qi][pj][j] + u2[qi][pj][j];
+        const double vi = u3[qi][pj][j] - u1[qi][pj][j] + u2[qi][pj][j];
         fr += orr * vr - oii * vi;
         fi += orr * vi + oii * vr;
       }
