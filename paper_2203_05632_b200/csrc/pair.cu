@@ -14,6 +14,12 @@
 // staged by TMA bulk copies. G is never written to memory: the accumulators are contracted
 // in registers and only four doubles per CTA leave the SM.
 //
+// Persistent: one CTA per SM walks a static list of tiles. Warp 8 is the TMA producer (bulk
+// copies into a 4-stage ring guarded by full/empty mbarriers, running ahead across tile
+// boundaries so the next tile's first stages land during this tile's epilogue); warps 0-7
+// issue the DMMAs. Complex products use 3 real products (3M): t1 = ar br, t2 = ai bi,
+// t3 = (ar + ai)(br - bi); re = t1 + t2, im = t3 - t1 + t2.
+//
 // Warp (wq, wp) owns Q walkers 2wq..2wq+1 x P walkers 4wp..4wp+3 (8 pairs). One m8n8k4
 // accumulator tile of V is exactly one walker pair (rows = q's (electron, channel), cols =
 // p's). The O tiles are computed transposed (rows = Q side) and exchanged through shared
@@ -26,12 +32,14 @@
 namespace mcmp2dev {
 
 namespace {
-constexpr int STAGES = 3;
-constexpr int THREADS = 256;
+constexpr int STAGES = 4;
+constexpr int CONSUMERS = 8;                              // MMA warps (wq 0..3 x wp 0..1)
+constexpr int THREADS = 32 * (CONSUMERS + 1);             // + one TMA producer warp
 constexpr int HALF_PTS = 2 * WB;                          // 16 points per walker block
 constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;    // 32 points x KC4 groups x 32
 constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per stage
-constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + (THREADS / 32) * 512 * 8 + 64;
+constexpr int SO_DOUBLES = 512;                           // per consumer warp: 2x2x4 blocks of 4x4 complex
+constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return uint32_t(__cvta_generic_to_shared(p));
@@ -45,6 +53,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -85,192 +97,211 @@ __device__ __forceinline__ void tile_coords(int t, int& bq, int& bp) {
 
 __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_DOUBLES + (THREADS / 32) * 512);
-  __shared__ double s_red[THREADS / 32][4];
+  double* const sO = sm + STAGES * STAGE_DOUBLES;  // [warp][e][qi][pj][y][x] complex o
+  uint64_t* const full = reinterpret_cast<uint64_t*>(sO + CONSUMERS * SO_DOUBLES);
+  uint64_t* const empty = full + STAGES;
+  __shared__ double s_red[CONSUMERS][4];
   __shared__ bool s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wq = warp >> 1, wp = warp & 1;
-  int bq, bp;
-  tile_coords(blockIdx.x, bq, bp);
+  const int ntiles = P.nb * (P.nb + 1) / 2;
   const int nchunks = P.Gtot / KC4;
+  const int cO = P.Go / KC4;  // occupied groups are padded to whole chunks
+  const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  auto issue = [&](int c, int stage) {
-    double* dst = sm + stage * STAGE_DOUBLES;
-    const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
-    const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
-    mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
-    bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
-    bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
-  };
-  if (tid == 0)
-    for (int s = 0; s < STAGES && s < nchunks; ++s) issue(s, s);
-
-  const int hl = lane >> 4, l16 = lane & 15;
-  const int cO = P.Go / KC4;  // occupied groups are padded to whole chunks
-  double* sO = sm + STAGES * STAGE_DOUBLES + warp * 512;  // [e][qi][pj][y][x] complex o
-  int c = 0;
-  auto wait_stage = [&](int cc) -> const double* {
-    const int stage = cc % STAGES;
-    mbar_wait(&full[stage], uint32_t((cc / STAGES) & 1));
-    return sm + stage * STAGE_DOUBLES;
-  };
-  auto release_stage = [&](int cc) {
-    __syncthreads();
-    if (tid == 0 && cc + STAGES < nchunks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(cc + STAGES, cc % STAGES);
+  if (warp == CONSUMERS) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      long long seq = 0;
+      for (int it = 0; it < my_tiles; ++it) {
+        int bq, bp;
+        tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+        for (int c = 0; c < nchunks; ++c, ++seq) {
+          const int stage = int(seq % STAGES);
+          mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
+          double* dst = sm + stage * STAGE_DOUBLES;
+          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
+          const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
+          mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
+          bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
+          bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+        }
+      }
     }
-  };
+  } else {
+    // ---------------- DMMA consumers ----------------
+    const int wq = warp >> 1, wp = warp & 1;
+    const int hl = lane >> 4, l16 = lane & 15;
+    double* const so = sO + warp * SO_DOUBLES;
+    const double wtau = P.st_ro->wtau;
+    double acc_dr = 0.0, acc_di = 0.0, acc_xr = 0.0, acc_xi = 0.0;
+    long long seq = 0;
+    auto acquire = [&]() -> const double* {
+      const int stage = int(seq % STAGES);
+      mbar_wait(&full[stage], uint32_t((seq / STAGES) & 1));
+      return sm + stage * STAGE_DOUBLES;
+    };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[int(seq % STAGES)]);
+      ++seq;
+    };
 
-  // ---- phase 1: O~_e(q,y; p,x) = sum_i Phi_o(q,e,y,i) conj Phi_o(p,e,x,i), 3M products:
-  //      t1 = ar br, t2 = ai bi, t3 = (ar + ai)(br - bi); re = t1 + t2, im = t3 - t1 + t2 ----
-  {
-    double t1[2][2][2], t2[2][2][2], t3[2][2][2];
+    for (int it = 0; it < my_tiles; ++it) {
+      int bq, bp;
+      tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+
+      // ---- phase 1: O~_e(q,y; p,x) = sum_i Phi_o(q,e,y,i) conj Phi_o(p,e,x,i) ----
+      {
+        double t1[2][2][2], t2[2][2][2], t3[2][2][2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+        for (int e = 0; e < 2; ++e)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
-    for (; c < cO; ++c) {
-      const double* S = wait_stage(c);
+            for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
+        for (int c = 0; c < cO; ++c) {
+          const double* S = acquire();
 #pragma unroll
-      for (int gg = 0; gg < KC4; ++gg) {
-        auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+          for (int gg = 0; gg < KC4; ++gg) {
+            auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int pa = 2 * (2 * wq + hl) + e;
-          const double ar = frag(pa, 0), ai = frag(pa, 1), sa = ar + ai;
+            for (int e = 0; e < 2; ++e) {
+              const int pa = 2 * (2 * wq + hl) + e;
+              const double ar = frag(pa, 0), ai = frag(pa, 1), sa = ar + ai;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int pb = HALF_PTS + 2 * (4 * wp + 2 * h + hl) + e;
-            const double br = frag(pb, 0), bi = frag(pb, 1);
-            dmma(t1[e][h], ar, br);
-            dmma(t2[e][h], ai, bi);
-            dmma(t3[e][h], sa, br - bi);
+              for (int h = 0; h < 2; ++h) {
+                const int pb = HALF_PTS + 2 * (4 * wp + 2 * h + hl) + e;
+                const double br = frag(pb, 0), bi = frag(pb, 1);
+                dmma(t1[e][h], ar, br);
+                dmma(t2[e][h], ai, bi);
+                dmma(t3[e][h], sa, br - bi);
+              }
+            }
           }
+          release();
         }
+        // o = conj(O~) into this warp's slot
+        const int qi = hl, y = (lane >> 2) & 3;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int pj = 2 * h + ((lane & 3) >> 1), x = 2 * (lane & 1) + j;
+              const int idx = ((((e * 2 + qi) * 4 + pj) * 16) + y * 4 + x) * 2;
+              so[idx] = t1[e][h][j] + t2[e][h][j];
+              so[idx + 1] = -(t3[e][h][j] - t1[e][h][j] + t2[e][h][j]);
+            }
       }
-      release_stage(c);
-    }
-    // o = conj(O~) into this warp's smem slot
-    const int qi = hl, y = (lane >> 2) & 3;
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int pj = 2 * h + ((lane & 3) >> 1), x = 2 * (lane & 1) + j;
-          const int idx = ((((e * 2 + qi) * 4 + pj) * 16) + y * 4 + x) * 2;
-          sO[idx] = t1[e][h][j] + t2[e][h][j];
-          sO[idx + 1] = -(t3[e][h][j] - t1[e][h][j] + t2[e][h][j]);
-        }
-  }
 
-  // ---- phase 2: V(q,e_q,x; p,e_p,y) = sum_a Phi_v(q,e_q,x,a) conj Phi_v(p,e_p,y,a), 3M ----
-  double u1[2][4][2], u2[2][4][2], u3[2][4][2];
+      // ---- phase 2: V(q,e_q,x; p,e_p,y) = sum_a Phi_v(q,e_q,x,a) conj Phi_v(p,e_p,y,a) ----
+      double u1[2][4][2], u2[2][4][2], u3[2][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
-  for (; c < nchunks; ++c) {
-    const double* S = wait_stage(c);
+        for (int j = 0; j < 4; ++j)
+          u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
+      for (int c = cO; c < nchunks; ++c) {
+        const double* S = acquire();
 #pragma unroll
-    for (int gg = 0; gg < KC4; ++gg) {
-      if (c * KC4 + gg >= P.Go + P.Gv) break;  // zero padding at the end
-      auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
-      double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
+        for (int gg = 0; gg < KC4; ++gg) {
+          if (c * KC4 + gg >= P.Go + P.Gv) break;  // zero padding at the end
+          auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+          double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
 #pragma unroll
-      for (int qi = 0; qi < 2; ++qi) {
-        const int pa = 2 * (2 * wq + qi) + hl;
-        ar[qi] = frag(pa, 0);
-        ai[qi] = frag(pa, 1);
-        sa[qi] = ar[qi] + ai[qi];
+          for (int qi = 0; qi < 2; ++qi) {
+            const int pa = 2 * (2 * wq + qi) + hl;
+            ar[qi] = frag(pa, 0);
+            ai[qi] = frag(pa, 1);
+            sa[qi] = ar[qi] + ai[qi];
+          }
+#pragma unroll
+          for (int pj = 0; pj < 4; ++pj) {
+            const int pb = HALF_PTS + 2 * (4 * wp + pj) + hl;
+            br[pj] = frag(pb, 0);
+            bi[pj] = frag(pb, 1);
+            db[pj] = br[pj] - bi[pj];
+          }
+#pragma unroll
+          for (int qi = 0; qi < 2; ++qi)
+#pragma unroll
+            for (int pj = 0; pj < 4; ++pj) {
+              dmma(u1[qi][pj], ar[qi], br[pj]);
+              dmma(u2[qi][pj], ai[qi], bi[pj]);
+              dmma(u3[qi][pj], sa[qi], db[pj]);
+            }
+        }
+        release();
       }
-#pragma unroll
-      for (int pj = 0; pj < 4; ++pj) {
-        const int pb = HALF_PTS + 2 * (4 * wp + pj) + hl;
-        br[pj] = frag(pb, 0);
-        bi[pj] = frag(pb, 1);
-        db[pj] = br[pj] - bi[pj];
-      }
+
+      // ---- epilogue: literal element-wise contraction of o with V (estimator.cpp:26-32) ----
+      const int xx = (lane >> 2) & 3, ep = (lane & 3) >> 1;
 #pragma unroll
       for (int qi = 0; qi < 2; ++qi)
 #pragma unroll
         for (int pj = 0; pj < 4; ++pj) {
-          dmma(u1[qi][pj], ar[qi], br[pj]);
-          dmma(u2[qi][pj], ai[qi], bi[pj]);
-          dmma(u3[qi][pj], sa[qi], db[pj]);
+          double fr = 0.0, fi = 0.0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int y = 2 * (lane & 1) + j;
+            const int idx = ((((ep * 2 + qi) * 4 + pj) * 16) + y * 4 + xx) * 2;
+            const double orr = so[idx], oii = so[idx + 1];
+            const double vr = u1[qi][pj][j] + u2[qi][pj][j];
+            const double vi = u3[qi][pj][j] - u1[qi][pj][j] + u2[qi][pj][j];
+            fr += orr * vr - oii * vi;
+            fi += orr * vi + oii * vr;
+          }
+#pragma unroll
+          for (int o = 1; o <= 8; o <<= 1) {
+            if (o == 2) continue;
+            fr += __shfl_xor_sync(0xffffffffu, fr, o);
+            fi += __shfl_xor_sync(0xffffffffu, fi, o);
+          }
+          // lane 0: (e_q,e_p) = (0,0) f1d; lane 18: (1,1) f2d; lane 16: (1,0) f1x; lane 2: (0,1) f2x
+          const double f1dr = __shfl_sync(0xffffffffu, fr, 0), f1di = __shfl_sync(0xffffffffu, fi, 0);
+          const double f2dr = __shfl_sync(0xffffffffu, fr, 18), f2di = __shfl_sync(0xffffffffu, fi, 18);
+          const double f1xr = __shfl_sync(0xffffffffu, fr, 16), f1xi = __shfl_sync(0xffffffffu, fi, 16);
+          const double f2xr = __shfl_sync(0xffffffffu, fr, 2), f2xi = __shfl_sync(0xffffffffu, fi, 2);
+          if (lane == 0) {
+            const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
+            if (q < P.m && p < P.m && q > p) {
+              const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+              const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+              const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+              // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32)
+              const double adr = -P.w_direct * f1dr, adi = -P.w_direct * f1di;
+              const double axr = -P.w_exchange * f1xr, axi = -P.w_exchange * f1xi;
+              acc_dr += (adr * f2dr - adi * f2di) * inv;
+              acc_di += (adr * f2di + adi * f2dr) * inv;
+              acc_xr += (axr * f2xr - axi * f2xi) * inv;
+              acc_xi += (axr * f2xi + axi * f2xr) * inv;
+            }
+          }
         }
+      __syncwarp();  // all lanes done reading `so` before the next tile rewrites it
     }
-    release_stage(c);
-  }
-  __syncwarp();
-
-  double acc_dr = 0.0, acc_di = 0.0, acc_xr = 0.0, acc_xi = 0.0;
-  const double wtau = P.st_ro->wtau;
-  const int eq = hl, xx = (lane >> 2) & 3, ep = (lane & 3) >> 1;
-#pragma unroll
-  for (int qi = 0; qi < 2; ++qi)
-#pragma unroll
-    for (int pj = 0; pj < 4; ++pj) {
-      double fr = 0.0, fi = 0.0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int y = 2 * (lane & 1) + j;
-        const int idx = ((((ep * 2 + qi) * 4 + pj) * 16) + y * 4 + xx) * 2;
-        const double orr = sO[idx], oii = sO[idx + 1];
-        const double vr = u1[qi][pj][j] + u2[qi][pj][j];
-        const double vi = u3[qi][pj][j] - u1[qi][pj][j] + u2[qi][pj][j];
-        fr += orr * vr - oii * vi;
-        fi += orr * vi + oii * vr;
-      }
-#pragma unroll
-      for (int o = 1; o <= 8; o <<= 1) {
-        if (o == 2) continue;
-        fr += __shfl_xor_sync(0xffffffffu, fr, o);
-        fi += __shfl_xor_sync(0xffffffffu, fi, o);
-      }
-      (void)eq;
-      // lane 0: (eq,ep) = (0,0) f1d; lane 18: (1,1) f2d; lane 16: (1,0) f1x; lane 2: (0,1) f2x
-      const double f1dr = __shfl_sync(0xffffffffu, fr, 0), f1di = __shfl_sync(0xffffffffu, fi, 0);
-      const double f2dr = __shfl_sync(0xffffffffu, fr, 18), f2di = __shfl_sync(0xffffffffu, fi, 18);
-      const double f1xr = __shfl_sync(0xffffffffu, fr, 16), f1xi = __shfl_sync(0xffffffffu, fi, 16);
-      const double f2xr = __shfl_sync(0xffffffffu, fr, 2), f2xi = __shfl_sync(0xffffffffu, fi, 2);
-      if (lane == 0) {
-        const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
-        if (q < P.m && p < P.m && q > p) {
-          const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
-          const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
-          const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
-          // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32)
-          const double adr = -P.w_direct * f1dr, adi = -P.w_direct * f1di;
-          const double axr = -P.w_exchange * f1xr, axi = -P.w_exchange * f1xi;
-          acc_dr += (adr * f2dr - adi * f2di) * inv;
-          acc_di += (adr * f2di + adi * f2dr) * inv;
-          acc_xr += (axr * f2xr - axi * f2xi) * inv;
-          acc_xi += (axr * f2xi + axi * f2xr) * inv;
-        }
-      }
+    if (lane == 0) {
+      s_red[warp][0] = acc_dr;
+      s_red[warp][1] = acc_di;
+      s_red[warp][2] = acc_xr;
+      s_red[warp][3] = acc_xi;
     }
-  if (lane == 0) {
-    s_red[warp][0] = acc_dr;
-    s_red[warp][1] = acc_di;
-    s_red[warp][2] = acc_xr;
-    s_red[warp][3] = acc_xi;
   }
   __syncthreads();
   if (tid == 0) {
     double r[4] = {0, 0, 0, 0};
-    for (int w = 0; w < THREADS / 32; ++w)
+    for (int w = 0; w < CONSUMERS; ++w)
       for (int k = 0; k < 4; ++k) r[k] += s_red[w][k];
     for (int k = 0; k < 4; ++k) P.partials[size_t(blockIdx.x) * 4 + k] = r[k];
     __threadfence();
@@ -281,37 +312,49 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   if (!s_last) return;
   __threadfence();
 
-  // ---- last CTA: fixed-order sum over all tile partials -> StepEstimate ----
+  // ---- last CTA: fixed-order sum over the per-CTA partials -> StepEstimate ----
   double r[4] = {0, 0, 0, 0};
   for (unsigned t = tid; t < gridDim.x; t += THREADS)
     for (int k = 0; k < 4; ++k) r[k] += P.partials[size_t(t) * 4 + k];
   double* red = sm;  // [THREADS][4]
   for (int k = 0; k < 4; ++k) red[tid * 4 + k] = r[k];
   __syncthreads();
-  for (int s = THREADS / 2; s > 0; s >>= 1) {
-    if (tid < s)
-      for (int k = 0; k < 4; ++k) red[tid * 4 + k] += red[(tid + s) * 4 + k];
-    __syncthreads();
-  }
   if (tid == 0) {
+    double a[4] = {0, 0, 0, 0};
+    for (int t = 0; t < THREADS; ++t)
+      for (int k = 0; k < 4; ++k) a[k] += red[t * 4 + k];
     const double npairs = 0.5 * P.m * (P.m - 1);  // estimator.cpp:61
-    P.step_out[0] = (red[0] + red[2]) / npairs;
-    P.step_out[1] = (red[1] + red[3]) / npairs;
-    P.step_out[2] = red[0];
-    P.step_out[3] = red[1];
-    P.step_out[4] = red[2];
-    P.step_out[5] = red[3];
+    P.step_out[0] = (a[0] + a[2]) / npairs;
+    P.step_out[1] = (a[1] + a[3]) / npairs;
+    P.step_out[2] = a[0];
+    P.step_out[3] = a[1];
+    P.step_out[4] = a[2];
+    P.step_out[5] = a[3];
     P.st->done_pair = 0;
   }
 }
 
+namespace {
+int g_sms[64];
+}
+
 cudaError_t pair_kernel_setup() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
   return cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
+int pair_grid(int nb) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int ntiles = nb * (nb + 1) / 2;
+  const int sms = g_sms[dev & 63] > 0 ? g_sms[dev & 63] : 148;
+  return ntiles < sms ? ntiles : sms;
+}
+
 void launch_pair(const PairParams& P, cudaStream_t s) {
-  const int ntiles = P.nb * (P.nb + 1) / 2;
-  pair_kernel<<<ntiles, THREADS, SMEM_BYTES, s>>>(P);
+  pair_kernel<<<pair_grid(P.nb), THREADS, SMEM_BYTES, s>>>(P);
 }
 
 }  // namespace mcmp2dev
