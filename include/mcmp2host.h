@@ -36,7 +36,8 @@ int mcmp2h_system_g(const mcmp2h_system* s, const double* pts, int n, double* ou
 int mcmp2h_save_spinor_set(const char* in_path, const char* out_path);
 
 /* one worker on one device (init_ensemble + burn_in at create); the accumulator state is
- * returned as {steps, sum, imag_sum, mean, sigma_bar, in_block, partial, nblocks}. */
+ * returned as {steps, sum, imag_sum, mean, sigma_bar, in_block, partial, nblocks,
+ * acceptance, imag_ratio} (10 doubles; WorkerSummary of driver.cpp:207-216). */
 typedef struct mcmp2h_worker mcmp2h_worker;
 mcmp2h_worker* mcmp2h_worker_create(const char* config_text, int worker_index, int device);
 void mcmp2h_worker_free(mcmp2h_worker* w);

@@ -1,0 +1,174 @@
+"""One process per GPU: each rank is one reference worker, merged over torch.distributed.
+
+The reference runs `workers` independent ensembles as std::threads in one process
+(driver.cpp:423-438) with Philox stream = worker index (driver.cpp:354-356), splits a step
+budget with worker_share (driver.cpp:307-309), and at every checkpoint interval merges the
+per-worker estimates by step-count weighting (driver.cpp:183-196) for the target-error stop
+rule (driver.cpp:401-412). Here the workers are processes (torchrun, one GPU each) and the
+interval merge is one all_gather of a 7-double summary per rank — the only collective; the
+walker loop itself has no communication. Launch:
+
+  torchrun --nproc-per-node N -m paper_2203_05632_b200.distributed CONFIG_FILE
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .native import check_host, dptr
+
+
+@dataclass
+class Summary:  # WorkerSummary (driver.hpp:46-53) + the accumulator's block count
+    index: int
+    steps: int
+    mean: float
+    sigma_bar: float
+    acceptance: float
+    imag_ratio: float
+    nblocks: int
+
+    def as_array(self):
+        return np.array([self.index, self.steps, self.mean, self.sigma_bar, self.acceptance, self.imag_ratio,
+                         self.nblocks], dtype=np.float64)
+
+    @staticmethod
+    def from_array(a):
+        return Summary(int(a[0]), int(a[1]), float(a[2]), float(a[3]), float(a[4]), float(a[5]), int(a[6]))
+
+
+class HostWorker:
+    """A C++ DeviceWorker (host/driver.cpp) on one GPU: init_ensemble + burn_in at creation."""
+
+    def __init__(self, config_text: str, index: int, device: int):
+        h = native.host()
+        self._w = h.mcmp2h_worker_create(config_text.encode(), index, device)
+        if not self._w:
+            raise native.Mcmp2Error(h.mcmp2h_last_error().decode())
+        self.index = index
+
+    def advance(self, nsteps: int) -> None:
+        if nsteps > 0:
+            check_host(native.host().mcmp2h_worker_advance(self._w, nsteps, None, None))
+
+    def summary(self) -> Summary:
+        o = np.zeros(10)
+        check_host(native.host().mcmp2h_worker_stats(self._w, dptr(o)))
+        return Summary(self.index, int(o[0]), o[3], o[4], o[8], o[9], int(o[7]))
+
+    def close(self):
+        if getattr(self, "_w", None):
+            native.host().mcmp2h_worker_free(self._w)
+            self._w = None
+
+    def __del__(self):
+        self.close()
+
+
+def worker_share(total: int, workers: int, index: int) -> int:  # driver.cpp:307-309
+    return total // workers + (1 if index < total % workers else 0)
+
+
+def merge_estimates(parts: list[Summary]) -> tuple[float, float, int]:
+    """driver.cpp:183-196 through the host library (same arithmetic as the C++ Engine)."""
+    arr = np.ascontiguousarray([[p.steps, p.mean, p.sigma_bar] for p in parts], dtype=np.float64)
+    out = np.empty(3)
+    h = native.host()
+    h.mcmp2h_merge_estimates.argtypes = [C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double)]
+    check_host(h.mcmp2h_merge_estimates(dptr(arr), len(parts), dptr(out)))
+    return float(out[0]), float(out[1]), int(out[2])
+
+
+def parse_run_config(text: str) -> dict:
+    """The run-control keys the driver needs (full validation is the host's parse_config_text)."""
+    buf = C.create_string_buffer(1 << 14)
+    check_host(native.host().mcmp2h_parse_config(text.encode(), buf, len(buf)))
+    cfg = {}
+    for line in buf.value.decode().splitlines():
+        k, _, v = line.partition(" ")
+        cfg[k] = v
+    return {"steps": int(cfg["steps"]) if "steps" in cfg else None,
+            "target": float(cfg["target-rel-err"]) if "target-rel-err" in cfg else None,
+            "interval": int(cfg["checkpoint-interval"])}
+
+
+def drive(worker, rank: int, world: int, steps: int | None, target: float | None, interval: int,
+          all_gather, max_intervals: int | None = None) -> dict:
+    """Engine::drive (driver.cpp:376-420) with workers = ranks: every interval each rank
+    advances its share, then the summaries are gathered and the stop rule is evaluated
+    identically on every rank."""
+    intervals = 0
+    on_target = False
+    done = 0
+    while True:
+        chunk = interval if steps is None else min(interval, worker_share(steps, world, rank) - done)
+        worker.advance(chunk)
+        done += max(chunk, 0)
+        intervals += 1
+        parts = [Summary.from_array(a) for a in all_gather(worker.summary().as_array())]
+        parts.sort(key=lambda p: p.index)
+        if steps is not None:
+            if all(p.steps >= worker_share(steps, world, p.index) for p in parts):
+                break
+        elif all(p.nblocks > 0 for p in parts):
+            value, sigma_bar, _ = merge_estimates(parts)
+            if sigma_bar > 0 and value != 0 and sigma_bar / abs(value) <= target:
+                on_target = True
+                break
+        if max_intervals is not None and intervals >= max_intervals:
+            break
+    value, sigma_bar, total = merge_estimates(parts)
+    return {"value": value, "sigma_bar": sigma_bar, "total_steps": total, "stopped_on_target": on_target,
+            "workers": parts, "intervals": intervals}
+
+
+def format_report(rep: dict) -> str:  # driver.cpp:523-539
+    lines = [f"E2        = {rep['value']:.17g} hartree", f"sigma_bar = {rep['sigma_bar']:.17g} hartree",
+             f"steps     = {rep['total_steps']}"]
+    if rep["stopped_on_target"]:
+        lines.append("stopped on target relative uncertainty")
+    for w in rep["workers"]:
+        lines.append(f"worker {w.index}: steps {w.steps}, I {w.mean:.17g}, sigma_bar {w.sigma_bar:.17g}, "
+                     f"acceptance {w.acceptance:.3f}, imag ratio {w.imag_ratio:.2e}")
+    return "\n".join(lines) + "\n"
+
+
+def torch_all_gather(dist):
+    import torch
+
+    def gather(a: np.ndarray):
+        t = torch.from_numpy(a)
+        if dist.get_backend() == "nccl":
+            t = t.cuda()
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+        dist.all_gather(out, t)
+        return [o.cpu().numpy() for o in out]
+    return gather
+
+
+def main(argv=None):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    argv = sys.argv[1:] if argv is None else argv
+    text = open(argv[0]).read()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rc = parse_run_config(text)
+    worker = HostWorker(text, rank, local)
+    rep = drive(worker, rank, world, rc["steps"], rc["target"], rc["interval"], torch_all_gather(dist))
+    if rank == 0:
+        sys.stdout.write(format_report(rep))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -164,6 +164,9 @@ int mcmp2h_worker_stats(mcmp2h_worker* w, double* o) {
     o[5] = double(a.in_block());
     o[6] = a.partial();
     o[7] = double(a.block_means().size());
+    const WorkerSummary s = w->worker->summary();  // driver.cpp:207-216
+    o[8] = s.acceptance;
+    o[9] = s.imag_ratio;
   });
 }
 

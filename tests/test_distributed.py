@@ -1,0 +1,142 @@
+"""CPU, gloo world size 2: the multi-process driver (paper_2203_05632_b200/distributed.py).
+
+Each rank drives a stand-in worker that replays the oracle's chain for worker index = rank
+(same Philox stream as the device worker would use), so the gathered merge, the step-budget
+split and the target-error stop rule can be checked against the oracle's own multi-worker
+Engine (std::threads, driver.cpp:376-438) on CPU."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_py
+from paper_2203_05632_b200 import distributed as D
+
+
+class Blocking:  # estimator.cpp:81-105, for the stand-in only
+    def __init__(self, nb):
+        self.nb, self.n, self.sum, self.imag, self.partial, self.inb, self.means = nb, 0, 0.0, 0.0, 0.0, 0, []
+
+    def add(self, v, im):
+        self.sum += v
+        self.imag += im
+        self.n += 1
+        self.partial += v
+        self.inb += 1
+        if self.inb == self.nb:
+            self.means.append(self.partial / self.nb)
+            self.partial, self.inb = 0.0, 0
+
+    def mean(self):
+        return self.sum / self.n if self.n else 0.0
+
+    def sigma_bar(self):
+        k = len(self.means)
+        if not k:
+            return 0.0
+        m = self.mean()
+        return math.sqrt(sum((b - m) * (b - m) for b in self.means) / k) / math.sqrt(k)
+
+
+class OracleStandIn:
+    def __init__(self, spinor, conf, index, m, burn, total, seed, block):
+        orc = oracle_py.OracleSystem(spinor, conf)
+        tr = orc.trajectory(seed=seed, stream=index, m=m, burn=burn, nsteps=total)
+        self.values, self.imags = tr["est"][:, 0], tr["est"][:, 1]
+        self.acc = Blocking(block)
+        self.index = index
+        self.pos = 0
+        self.acceptance = tr["accepted"] / max(tr["proposed"], 1)
+
+    def advance(self, n):
+        for k in range(self.pos, self.pos + max(n, 0)):
+            self.acc.add(self.values[k], self.imags[k])
+        self.pos += max(n, 0)
+
+    def summary(self):
+        a = self.acc
+        ratio = abs(a.imag) / abs(a.sum) if a.sum != 0 else abs(a.imag)
+        return D.Summary(self.index, a.n, a.mean(), a.sigma_bar(), 0.0, ratio, len(a.means))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, args, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spinor, conf, m, burn, steps, target, interval, seed, block = args
+    total = steps if steps is not None else 4000
+    w = OracleStandIn(spinor, conf, rank, m, burn, D.worker_share(total, world, rank) if steps else total, seed,
+                      block)
+    rep = D.drive(w, rank, world, steps, target, interval, D.torch_all_gather(dist))
+    q.put((rank, rep["value"], rep["sigma_bar"], rep["total_steps"], rep["stopped_on_target"],
+           [(p.index, p.steps, p.mean) for p in rep["workers"]]))
+    dist.destroy_process_group()
+
+
+def run_world(args, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out)
+
+
+def oracle_report(spinor, conf_text, extra):
+    txt = conf_text + f"spinors {spinor}\n" + extra
+    lines = [l for l in txt.splitlines() if not l.startswith("spinors ") or l == f"spinors {spinor}"]
+    return oracle_py.run_config("\n".join(lines) + "\n")
+
+
+def parse_report(rep):
+    d = {}
+    for line in rep.splitlines():
+        if line.startswith("E2"):
+            d["value"] = float(line.split()[2])
+        elif line.startswith("sigma_bar"):
+            d["sigma_bar"] = float(line.split()[2])
+        elif line.startswith("steps"):
+            d["steps"] = int(line.split()[2])
+    return d
+
+
+def test_two_ranks_match_oracle_two_workers(cfgdir):
+    """Step budget split over 2 ranks == the oracle Engine with workers 2 (same streams)."""
+    spinor = cfgdir / "syn1c.spinor"
+    conf = "walkers 6\nburnin 30\nblocksize 10\ncheckpoint-interval 50\nseed 4\n"
+    out = run_world((str(spinor), conf, 6, 30, 301, None, 50, 4, 10))
+    rank0 = out[0]
+    assert all(o[1:5] == rank0[1:5] for o in out)  # every rank sees the same merge
+    ref = parse_report(oracle_report(spinor, conf, "steps 301\nworkers 2\n"))
+    assert rank0[3] == ref["steps"] == 301
+    assert [w[1] for w in rank0[5]] == [151, 150]
+    assert rank0[1] == pytest.approx(ref["value"], rel=1e-14, abs=0)
+    assert rank0[2] == pytest.approx(ref["sigma_bar"], rel=1e-12, abs=0)
+
+
+def test_two_ranks_target_error_stop(cfgdir):
+    """target-rel-err: stops at the first interval whose merged sigma_bar/|E| meets the target
+    (driver.cpp:401-412), consistently on all ranks."""
+    spinor = cfgdir / "syn1c.spinor"
+    conf = "walkers 6\nburnin 30\nblocksize 10\ncheckpoint-interval 50\nseed 4\n"
+    out = run_world((str(spinor), conf, 6, 30, None, 2.0, 50, 4, 10))
+    assert all(o[4] for o in out)
+    assert out[0][3] == 100  # both ranks at the first interval with blocks: 2 x 50
+    ref = parse_report(oracle_report(spinor, conf, "target-rel-err 2.0\nworkers 2\n"))
+    assert ref["steps"] == 100 and out[0][1] == pytest.approx(ref["value"], rel=1e-14)

@@ -1,0 +1,125 @@
+"""The C++ host Engine over the device (libmcmp2host -> libmcmp2dev): the reference driver
+tests (test_driver.cpp:125-252) and full-run agreement with the CPU oracle's Engine."""
+import math
+
+import pytest
+
+import oracle_py
+from paper_2203_05632_b200 import walker
+from paper_2203_05632_b200.native import Mcmp2Error
+
+pytestmark = pytest.mark.gpu
+
+
+def parse(rep):
+    d = {"workers": []}
+    for line in rep.splitlines():
+        if line.startswith("E2"):
+            d["value"] = float(line.split()[2])
+        elif line.startswith("sigma_bar"):
+            d["sigma_bar"] = float(line.split()[2])
+        elif line.startswith("steps"):
+            d["steps"] = int(line.split()[2])
+        elif line.startswith("worker"):
+            d["workers"].append(line)
+    d["on_target"] = "stopped on target" in rep
+    return d
+
+
+def small(cfgdir, name="syn1c", **kw):
+    base = {"spinors": str(cfgdir / f"{name}.spinor"), "steps": 2000, "walkers": 4, "seed": 11, "workers": 1,
+            "burnin": 100, "checkpoint-interval": 500}
+    base.update(kw)
+    extra = (cfgdir / f"{name}.conf").read_text()
+    weights = "".join(l + "\n" for l in extra.splitlines() if l.startswith("weight"))
+    return "".join(f"{k} {v}\n" for k, v in base.items() if v is not None) + weights
+
+
+def test_single_worker_runs_are_bit_reproducible(cfgdir):
+    a = walker.run_config_text(small(cfgdir))
+    b = walker.run_config_text(small(cfgdir))
+    assert a == b
+    assert parse(a)["steps"] == 2000
+
+
+def test_multi_worker_bookkeeping(cfgdir):
+    rep = parse(walker.run_config_text(small(cfgdir, workers=3, steps=3000)))
+    assert rep["steps"] == 3000 and len(rep["workers"]) == 3
+    assert all(", steps 1000," in w for w in rep["workers"])
+
+
+def test_kill_and_resume_is_bit_exact(cfgdir, tmp_path):
+    """test_driver.cpp:150-172: abort after 2 intervals, resume == uninterrupted run."""
+    ck = tmp_path / "run.ckpt"
+    cfg = small(cfgdir, workers=2, steps=4000, checkpoint=str(ck))
+    full = walker.run_config_text(cfg)
+    walker.run_config_text(cfg, abort_after_intervals=2)
+    resumed = walker.resume(ck)
+    assert resumed == full
+
+
+def test_resume_rejects_changed_spinor_file(cfgdir, tmp_path):
+    sp = tmp_path / "f.spinor"
+    sp.write_bytes((cfgdir / "syn1c.spinor").read_bytes())
+    ck = tmp_path / "run.ckpt"
+    walker.run_config_text(small(cfgdir, spinors=str(sp), checkpoint=str(ck)), abort_after_intervals=1)
+    sp.write_bytes((cfgdir / "syn2c.spinor").read_bytes())
+    with pytest.raises(Mcmp2Error, match="hash"):
+        walker.resume(ck)
+
+
+def test_merge_checkpoints(cfgdir, tmp_path):
+    a, b = tmp_path / "a.ckpt", tmp_path / "b.ckpt"
+    ra = parse(walker.run_config_text(small(cfgdir, checkpoint=str(a), seed=1)))
+    rb = parse(walker.run_config_text(small(cfgdir, checkpoint=str(b), seed=2)))
+    value, sigma_bar, steps = walker.merge([a, b])
+    assert steps == 4000
+    assert value == pytest.approx((ra["value"] * 2000 + rb["value"] * 2000) / 4000, rel=1e-15)
+    c = tmp_path / "c.ckpt"
+    walker.run_config_text(small(cfgdir, name="syn2c", checkpoint=str(c)))
+    with pytest.raises(Mcmp2Error, match="hash"):
+        walker.merge([a, c])
+
+
+def test_trace_has_one_line_per_completed_block(cfgdir, tmp_path):
+    tr = tmp_path / "run.trace"
+    walker.run_config_text(small(cfgdir, trace=str(tr), steps=1950))
+    rows = tr.read_text().splitlines()
+    assert len(rows) == 19 and rows[-1].split()[0] == "1900"
+
+
+def test_target_relative_error_stop(cfgdir):
+    rep = parse(walker.run_config_text(small(cfgdir, steps=None) + "target-rel-err 2.0\n"))
+    assert rep["on_target"] and rep["steps"] == 500
+    assert rep["sigma_bar"] / abs(rep["value"]) <= 2.0
+
+
+@pytest.mark.parametrize("name,extra", [("syn1c", {}), ("cfg1", {"walkers": 16, "step-size": 0.3}),
+                                        ("syn2c", {"workers": 2})])
+def test_full_run_matches_oracle_engine(cfgdir, name, extra):
+    """Same config through the device Engine and the CPU oracle's Engine: the device follows the
+    reference Philox stream, so the runs agree to rounding, not just statistically."""
+    cfg = small(cfgdir, name=name, **extra)
+    dev = parse(walker.run_config_text(cfg))
+    ref = parse(oracle_py.run_config(cfg))
+    assert dev["steps"] == ref["steps"]
+    assert dev["value"] == pytest.approx(ref["value"], rel=1e-9)
+    assert dev["sigma_bar"] == pytest.approx(ref["sigma_bar"], rel=1e-6)
+
+
+def test_independent_rng_runs_agree_within_2_sigma(cfgdir):
+    """north_star: independent-RNG full runs agree with the reference E(2) within combined 2 sigma
+    (literal estimator). cfg1, 4000 steps, device seed 101 vs oracle seed 202."""
+    dev = parse(walker.run_config_text(small(cfgdir, name="cfg1", walkers=16, **{"step-size": 0.3},
+                                             steps=4000, seed=101)))
+    ref = parse(oracle_py.run_config(small(cfgdir, name="cfg1", walkers=16, **{"step-size": 0.3},
+                                           steps=4000, seed=202)))
+    assert abs(dev["value"] - ref["value"]) <= 2 * math.hypot(dev["sigma_bar"], ref["sigma_bar"])
+
+
+def test_missing_nuclei_is_diagnosed(cfgdir, tmp_path):
+    text = (cfgdir / "syn1c.spinor").read_text().replace("nuclei 2\n1 0 0 0\n1 0 0 1.3999999999999999\n", "")
+    sp = tmp_path / "bare.spinor"
+    sp.write_text(text)
+    with pytest.raises(Mcmp2Error, match="nuclei"):
+        walker.run_config_text(small(cfgdir, spinors=str(sp)))
