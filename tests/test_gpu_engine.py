@@ -45,7 +45,7 @@ def test_single_worker_runs_are_bit_reproducible(cfgdir):
 def test_multi_worker_bookkeeping(cfgdir):
     rep = parse(walker.run_config_text(small(cfgdir, workers=3, steps=3000)))
     assert rep["steps"] == 3000 and len(rep["workers"]) == 3
-    assert all(", steps 1000," in w for w in rep["workers"])
+    assert all(": steps 1000," in w for w in rep["workers"])
 
 
 def test_kill_and_resume_is_bit_exact(cfgdir, tmp_path):
