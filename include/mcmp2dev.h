@@ -125,6 +125,11 @@ int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double*
 int mcmp2dev_synchronize(mcmp2dev_t* h);
 /* the handle's cudaStream_t (as void*), for callers that time or order work around it */
 void* mcmp2dev_stream(mcmp2dev_t* h);
+/* Kramers-restricted pair kernel: detected at create when the spinor columns are exact
+ * time-reversal pairs (the only case it is used). mode -1 queries, 0 disables, 1 enables
+ * if eligible; returns the active state (1/0). Results agree with the general path to
+ * rounding (see csrc/pair_kr.cu). */
+int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,9 @@ void launch_spinor(const SpinorParams& P, cudaStream_t s);
 int spinor_smem_bytes(const SpinorParams& P);
 void launch_pair(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kernel_setup();
+// Kramers-restricted variant (pair_kr.cu): half the DMMA work for time-reversal-paired columns
+void launch_pair_kr(const PairParams& P, cudaStream_t s);
+cudaError_t pair_kr_kernel_setup();
 cudaError_t spinor_kernel_setup();
 
 }  // namespace mcmp2dev

@@ -79,6 +79,7 @@ struct mcmp2dev_handle {
   int Go = 0, Gv = 0, Gtot = 0;
   double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
   int estimator = 0;
+  bool kramers_eligible = false, kramers = false;  // pair_kr.cu path
   SpinorParams sp{};
   DevSites sites{};
   double* d_energies = nullptr;
@@ -152,7 +153,8 @@ struct mcmp2dev_handle {
     p.w_exchange = w_exchange;
     p.partials = d_partials;
     p.step_out = step_out;
-    launch_pair(p, stream);
+    if (kramers) launch_pair_kr(p, stream);
+    else launch_pair(p, stream);
     if (prof) {
       ck(cudaEventRecord(ev[3], stream), "event");
       ck(cudaEventSynchronize(ev[3]), "event sync");
@@ -217,6 +219,39 @@ int guard(mcmp2dev_t* h, F&& f) {
   }
 }
 
+// Exact time-reversal pairing of the spinor columns (oracle.cpp:346-355 generalised): channel
+// pairs (0,1) [and (2,3)] carry identical basis lists, columns (2k, 2k+1) satisfy
+// (a, b) -> (-b*, a*) per channel pair bit for bit, and pair energies are equal.
+bool kramers_paired(const mcmp2dev_system* s, const std::vector<int>& ch_off) {
+  if (s->ncomp == 1 || s->n_occ % 2 || s->n_vir % 2) return false;
+  const int np = s->n_occ + s->n_vir;
+  for (int k = 0; k < np; k += 2)
+    if (s->energies[k] != s->energies[k + 1]) return false;
+  for (int pr = 0; pr < s->ncomp / 2; ++pr) {
+    const int a0 = ch_off[2 * pr], b0 = ch_off[2 * pr + 1], n = ch_off[2 * pr + 1] - ch_off[2 * pr];
+    if (ch_off[2 * pr + 2] - b0 != n) return false;
+    for (int i = 0; i < n; ++i) {
+      const int fa = a0 + i, fb = b0 + i;
+      for (int d = 0; d < 3; ++d)
+        if (s->fn_center[3 * fa + d] != s->fn_center[3 * fb + d]) return false;
+      if (s->fn_lm[2 * fa] != s->fn_lm[2 * fb] || s->fn_lm[2 * fa + 1] != s->fn_lm[2 * fb + 1]) return false;
+      const int pa = s->fn_prim_offset[fa], pb = s->fn_prim_offset[fb];
+      const int na = s->fn_prim_offset[fa + 1] - pa;
+      if (s->fn_prim_offset[fb + 1] - pb != na) return false;
+      for (int q = 0; q < na; ++q)
+        if (s->prim_zeta[pa + q] != s->prim_zeta[pb + q] || s->prim_coeff[pa + q] != s->prim_coeff[pb + q])
+          return false;
+      for (int k = 0; k < np; k += 2) {
+        const double* ca = s->coeff + 2 * (size_t(fa) * np + k);  // (a re, a im) of column k
+        const double* cb = s->coeff + 2 * (size_t(fb) * np + k);
+        // partner column k+1: alpha = -conj(beta_k), beta = conj(alpha_k)
+        if (ca[2] != -cb[0] || ca[3] != cb[1] || cb[2] != ca[0] || cb[3] != -ca[1]) return false;
+      }
+    }
+  }
+  return true;
+}
+
 void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers) {
   if (!s) throw ArgError("mcmp2dev_create: null system");
   if (s->ncomp != 1 && s->ncomp != 2 && s->ncomp != 4)
@@ -231,6 +266,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
   ck(pair_kernel_setup(), "pair kernel attributes");
   ck(spinor_kernel_setup(), "spinor kernel attributes");
+  ck(pair_kr_kernel_setup(), "pair_kr kernel attributes");
   for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
 
   h->ncomp = s->ncomp;
@@ -298,6 +334,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
   sp.max_ch = max_ch;
   sp.C = reinterpret_cast<const double2*>(dupload(s->coeff, size_t(2) * nfunc * h->n_p, o));
+  h->kramers_eligible = kramers_paired(s, ch_off);
+  h->kramers = h->kramers_eligible;
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;
   sp.n_p = h->n_p;
@@ -591,6 +629,13 @@ int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double*
 }
 
 void* mcmp2dev_stream(mcmp2dev_t* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int mcmp2dev_kramers(mcmp2dev_t* h, int mode) {
+  if (!h) return -1;
+  if (mode == 0) h->kramers = false;
+  if (mode == 1) h->kramers = h->kramers_eligible;
+  return h->kramers ? 1 : 0;
+}
 
 int mcmp2dev_synchronize(mcmp2dev_t* h) {
   return guard(h, [&] { ck(cudaStreamSynchronize(h->stream), "stream sync"); });

@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "pair_common.cuh"
 
 namespace mcmp2dev {
 
@@ -41,59 +42,8 @@ constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per 
 constexpr int SO_DOUBLES = 512;                           // per consumer warp: 2x2x4 blocks of 4x4 complex
 constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return uint32_t(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void tile_coords(int t, int& bq, int& bp) {
-  // t = bq (bq + 1) / 2 + bp, 0 <= bp <= bq
-  int q = int((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-  while ((q + 1) * (q + 2) / 2 <= t) ++q;
-  while (q * (q + 1) / 2 > t) --q;
-  bq = q;
-  bp = t - q * (q + 1) / 2;
-}
 }  // namespace
+using namespace pairk;
 
 __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];

@@ -1,0 +1,283 @@
+// pair_kr.cu — the pair kernel for Kramers-paired spinor sets (time-reversal symmetric
+// references; the generator's inputs and the reference's syn4c fixture, oracle.cpp:346-393).
+//
+// When the spinor columns come in Kramers pairs (phi, K phi) with K phi = (-Lb*, La*, -Sb*, Sa*)
+// and equal energies, every O/V block M = sum_pairs w (phi phi'^H + K phi (K phi')^H) obeys
+//   M[beta i, beta j] = conj M[alpha i, alpha j],   M[beta i, alpha j] = -conj M[alpha i, beta j]
+// for channels ordered (L alpha, L beta, S alpha, S beta). The literal element-wise sum of the
+// reference pair term (estimator.cpp:26-29) then splits as
+//   sum_{x,y} o(x,y) v(x,y) = 2 Re sum_{x in {La, Sa}, y} o(x,y) v(x,y),
+// so only the alpha rows of V (Q side) and the alpha columns of O~ (P side) are computed: half
+// the DMMA work of pair.cu, with identical results to rounding (f1d, f2d, f1x, f2x are real,
+// the imaginary residue is exactly 0 where the reference carries ~1e-16 noise).
+//
+// Structure as pair.cu (persistent CTAs over 8x8 walker tiles, TMA producer warp, full/empty
+// mbarrier ring, 3M complex products), with 4 MMA warps of 4x4 walker pairs and 2 CTAs per SM.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "pair_common.cuh"
+
+namespace mcmp2dev {
+
+namespace {
+using namespace pairk;
+constexpr int STAGES = 3;
+constexpr int CONSUMERS = 4;                              // (wq, wp) in {0,1}^2, 4x4 walker pairs each
+constexpr int THREADS = 32 * (CONSUMERS + 1);
+constexpr int HALF_PTS = 2 * WB;
+constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;
+constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;
+constexpr int SO_DOUBLES = 2 * 4 * 4 * 4 * 2 * 2;         // [e][qq][pp][y][x_alpha] complex
+constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
+  extern __shared__ __align__(128) double sm[];
+  double* const sO = sm + STAGES * STAGE_DOUBLES;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(sO + CONSUMERS * SO_DOUBLES);
+  uint64_t* const empty = full + STAGES;
+  __shared__ double s_red[CONSUMERS][2];
+  __shared__ bool s_last;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = P.nb * (P.nb + 1) / 2;
+  const int nchunks = P.Gtot / KC4;
+  const int cO = P.Go / KC4;
+  const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == CONSUMERS) {
+    if (lane == 0) {  // TMA producer
+      long long seq = 0;
+      for (int it = 0; it < my_tiles; ++it) {
+        int bq, bp;
+        tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+        for (int c = 0; c < nchunks; ++c, ++seq) {
+          const int stage = int(seq % STAGES);
+          mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
+          double* dst = sm + stage * STAGE_DOUBLES;
+          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
+          const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
+          mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
+          bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
+          bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+        }
+      }
+    }
+  } else {
+    const int wq = warp >> 1, wp = warp & 1;
+    const int hl = lane >> 4, l16 = lane & 15;
+    const int xa_off = 8 * ((lane >> 2) & 1) + (lane & 3);  // alpha channel x = 0 or 2, k = lane & 3
+    double* const so = sO + warp * SO_DOUBLES;
+    const double wtau = P.st_ro->wtau;
+    double acc_d = 0.0, acc_x = 0.0;
+    long long seq = 0;
+    auto acquire = [&]() -> const double* {
+      const int stage = int(seq % STAGES);
+      mbar_wait(&full[stage], uint32_t((seq / STAGES) & 1));
+      return sm + stage * STAGE_DOUBLES;
+    };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[int(seq % STAGES)]);
+      ++seq;
+    };
+
+    for (int it = 0; it < my_tiles; ++it) {
+      int bq, bp;
+      tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+
+      // ---- phase 1: O~_e rows (q, y) all channels, cols (p, x_alpha) ----
+      {
+        double t1[2][2][2], t2[2][2][2], t3[2][2][2];  // [e][hq][j]
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
+        for (int c = 0; c < cO; ++c) {
+          const double* S = acquire();
+#pragma unroll
+          for (int gg = 0; gg < KC4; ++gg) {
+            auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + off]; };
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int pb = HALF_PTS + 2 * (4 * wp + (lane >> 3)) + e;
+              const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int pa = 2 * (4 * wq + 2 * h + hl) + e;
+                const double ar = at(pa, 0, l16), ai = at(pa, 1, l16);
+                dmma(t1[e][h], ar, br);
+                dmma(t2[e][h], ai, bi);
+                dmma(t3[e][h], ar + ai, db);
+              }
+            }
+          }
+          release();
+        }
+        // o_e(x_alpha, y) = conj O~_e for pair (qq, pp)
+        const int y = (lane >> 2) & 3, pp = lane & 3;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int qq = 2 * h + hl;
+              const int idx = ((((e * 4 + qq) * 4 + pp) * 4 + y) * 2 + j) * 2;
+              so[idx] = t1[e][h][j] + t2[e][h][j];
+              so[idx + 1] = -(t3[e][h][j] - t1[e][h][j] + t2[e][h][j]);
+            }
+      }
+
+      // ---- phase 2: V rows (q, e_q, x_alpha), cols (p, e_p, y) ----
+      double u1[2][4][2], u2[2][4][2], u3[2][4][2];  // [hq][pp][j]
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
+      for (int c = cO; c < nchunks; ++c) {
+        const double* S = acquire();
+#pragma unroll
+        for (int gg = 0; gg < KC4; ++gg) {
+          if (c * KC4 + gg >= P.Go + P.Gv) break;
+          auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + off]; };
+          double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pa = 2 * (4 * wq + 2 * h + hl) + ((lane >> 3) & 1);
+            ar[h] = at(pa, 0, xa_off);
+            ai[h] = at(pa, 1, xa_off);
+            sa[h] = ar[h] + ai[h];
+          }
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            const int pb = HALF_PTS + 2 * (4 * wp + pp) + hl;
+            br[pp] = at(pb, 0, l16);
+            bi[pp] = at(pb, 1, l16);
+            db[pp] = br[pp] - bi[pp];
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) {
+              dmma(u1[h][pp], ar[h], br[pp]);
+              dmma(u2[h][pp], ai[h], bi[pp]);
+              dmma(u3[h][pp], sa[h], db[pp]);
+            }
+        }
+        release();
+      }
+
+      // ---- epilogue: f = 2 Re sum_{x alpha, y} o v; real direct/exchange terms ----
+      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          const int qq = 2 * h + hl;
+          double f = 0.0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int y = 2 * (lane & 1) + j;
+            const int idx = ((((ep * 4 + qq) * 4 + pp) * 4 + y) * 2 + xa) * 2;
+            const double vr = u1[h][pp][j] + u2[h][pp][j];
+            const double vi = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+            f += so[idx] * vr - so[idx + 1] * vi;
+          }
+          f += __shfl_xor_sync(0xffffffffu, f, 1);
+          f += __shfl_xor_sync(0xffffffffu, f, 4);
+          // per half-warp hl: lane base + (e_q << 3) + (e_p << 1)
+          const int base = lane & 16;
+          const double f1d = 2.0 * __shfl_sync(0xffffffffu, f, base + 0);
+          const double f2x = 2.0 * __shfl_sync(0xffffffffu, f, base + 2);
+          const double f1x = 2.0 * __shfl_sync(0xffffffffu, f, base + 8);
+          const double f2d = 2.0 * __shfl_sync(0xffffffffu, f, base + 10);
+          if ((lane & 15) == 0) {
+            const int q = WB * bq + 4 * wq + qq, p = WB * bp + 4 * wp + pp;
+            if (q < P.m && p < P.m && q > p) {
+              const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+              const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+              const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+              acc_d += (-P.w_direct * f1d) * f2d * inv;                  // estimator.cpp:32
+              acc_x += (-P.w_exchange * f1x) * f2x * inv;
+            }
+          }
+        }
+      __syncwarp();
+    }
+    acc_d += __shfl_sync(0xffffffffu, acc_d, 16);
+    acc_x += __shfl_sync(0xffffffffu, acc_x, 16);
+    if (lane == 0) {
+      s_red[warp][0] = acc_d;
+      s_red[warp][1] = acc_x;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double d = 0.0, x = 0.0;
+    for (int w = 0; w < CONSUMERS; ++w) {
+      d += s_red[w][0];
+      x += s_red[w][1];
+    }
+    P.partials[size_t(blockIdx.x) * 4 + 0] = d;
+    P.partials[size_t(blockIdx.x) * 4 + 1] = 0.0;
+    P.partials[size_t(blockIdx.x) * 4 + 2] = x;
+    P.partials[size_t(blockIdx.x) * 4 + 3] = 0.0;
+    __threadfence();
+    const unsigned done = atomicAdd(&P.st->done_pair, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {  // fixed-order sum of the per-CTA partials
+    double d = 0.0, x = 0.0;
+    for (unsigned t = 0; t < gridDim.x; ++t) {
+      d += P.partials[size_t(t) * 4 + 0];
+      x += P.partials[size_t(t) * 4 + 2];
+    }
+    const double npairs = 0.5 * P.m * (P.m - 1);
+    P.step_out[0] = (d + x) / npairs;
+    P.step_out[1] = 0.0;
+    P.step_out[2] = d;
+    P.step_out[3] = 0.0;
+    P.step_out[4] = x;
+    P.step_out[5] = 0.0;
+    P.st->done_pair = 0;
+  }
+}
+
+namespace {
+int g_sms_kr[64];
+}
+
+cudaError_t pair_kr_kernel_setup() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms_kr[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return cudaFuncSetAttribute(pair_kr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
+void launch_pair_kr(const PairParams& P, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int ntiles = P.nb * (P.nb + 1) / 2;
+  const int slots = 2 * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
+  pair_kr_kernel<<<ntiles < slots ? ntiles : slots, THREADS, SMEM_BYTES, s>>>(P);
+}
+
+}  // namespace mcmp2dev

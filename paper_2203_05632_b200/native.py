@@ -80,6 +80,7 @@ def dev() -> C.CDLL:
         d.mcmp2dev_stream.restype = vp
         d.mcmp2dev_stream.argtypes = [vp]
         d.mcmp2dev_abi_version.restype = ip
+        d.mcmp2dev_kramers.argtypes = [vp, ip]
         _dev = d
     return _dev
 

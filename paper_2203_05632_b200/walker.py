@@ -144,6 +144,10 @@ class DeviceWalker:
         check_dev(self._d.mcmp2dev_work(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h)
         return {"pair_flop": a.value, "spinor_flop": b.value, "phi_bytes": c.value}
 
+    def kramers(self, mode: int = -1) -> bool:
+        """Kramers-restricted pair kernel: -1 query, 0 off, 1 on when eligible."""
+        return bool(self._d.mcmp2dev_kramers(self._h, mode))
+
     @property
     def stream_ptr(self) -> int:
         return int(self._d.mcmp2dev_stream(self._h))

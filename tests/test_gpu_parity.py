@@ -31,12 +31,15 @@ def test_replay_matches_oracle(cfgdir, name, m, nsteps):
     sp, text, orc, sysd = load(cfgdir, name)
     tr = orc.trajectory(seed=11, stream=0, m=m, burn=30, nsteps=nsteps)
     dw = DeviceWalker(sysd, max_walkers=m)
-    got = dw.replay(tr["walkers"], tr["tau"])
+    assert dw.kramers() == (orc.ncomp > 1)  # generated 2c/4c sets are exact Kramers pairs
     ref = tr["est"]
-    assert rel_err(got[:, 0], ref[:, 0]) < REL
-    # direct and exchange pair sums separately (condition-aware: relative to their magnitude)
-    for k in (2, 4):
-        assert rel_err(got[:, k], ref[:, k]) < REL
+    for mode in (1, 0):  # Kramers-restricted kernel, then the general kernel
+        dw.kramers(mode)
+        got = dw.replay(tr["walkers"], tr["tau"])
+        assert rel_err(got[:, 0], ref[:, 0]) < REL
+        # direct and exchange pair sums separately (condition-aware: relative to their magnitude)
+        for k in (2, 4):
+            assert rel_err(got[:, k], ref[:, k]) < REL
     if orc.ncomp == 1:  # real orbitals: imaginary residue exactly zero (test_estimator.cpp:255-267)
         assert np.all(got[:, 1] == 0.0)
     else:  # Kramers-paired input: real to rounding (test_estimator.cpp:149-165)
