@@ -218,6 +218,12 @@ def main():
     step_ms_prof = prof["ms"]["total"] / prof["launches"]["total"]
     peak, peak_src = peaks()
     achieved = work["pair_flop"] / (pair_ms / 1e3) / 1e12
+    kramers = dw.kramers()
+    kernel_name = "pair_kr_kernel (DMMA m8n8k4 f64, Kramers-restricted)" if kramers else "pair_kernel (DMMA m8n8k4 f64)"
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{cfg}.json"  # dram bytes per launch from the committed ncu --set full capture
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
 
     # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
     st = dw.get_ensemble()
@@ -248,8 +254,18 @@ def main():
         "dtype": "f64/c128", "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
         "config": dict(config, parallelism=f"{world} independent workers (1 per GPU)",
                        l2="flushed between timed steps (256 MiB write on the handle's stream)"),
-        "roofline": {"bound": "tensor", "kernel": "pair_kernel (DMMA m8n8k4 f64)", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "roofline": {"bound": "tensor", "kernel": kernel_name, "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "achieved_basis": "algorithmic: C(m,2) x F_pair, F_pair = 8 nc^2 (2 n_occ + 4 n_vir) + 32 nc^2 "
+                                       "(SURVEY 8d, 8 FLOP per complex MAC of the reference's full 4x4 blocks)",
+                     "executed_dmma_flop_per_launch": work["pair_dmma_flop_executed"],
+                     "executed_tflops": work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12,
+                     "executed_frac": work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12 / peak,
+                     "why_frac_above_1": "the kernel issues fewer DMMA FLOPs than the algorithmic count: complex "
+                                         "products as 3 real products (3M) and, for exact Kramers pairs, only the "
+                                         "alpha rows of each 4x4 block (pair_kr.cu); executed_frac is the tensor-pipe "
+                                         "utilisation" if kramers else "3M complex products (3 real per complex)",
+                     "kramers_path": kramers,
                      "pair_flop_per_launch": work["pair_flop"], "pair_ms_per_launch": pair_ms,
                      "pair_share_of_step": prof["ms"]["pair"] / prof["ms"]["total"],
                      "spinor_ms_per_launch": prof["ms"]["spinor"] / prof["launches"]["spinor"],

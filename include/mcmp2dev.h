@@ -121,6 +121,10 @@ int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out);
 /* Algorithmic work of one step at the current m: FLOP of the pair stage
  * (C(m,2) * F_pair) and of the spinor stage (2m * 4 * R * n_p), bytes written to Phi. */
 int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes);
+/* FP64 tensor work the pair kernel actually issues per step at the current m (DMMA count x
+ * 512 FLOP, including tile/k padding): 3 real products per complex product, and half the
+ * blocks on the Kramers path. pair_flop / executed is the algorithmic saving. */
+int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop);
 /* synchronise the handle's stream */
 int mcmp2dev_synchronize(mcmp2dev_t* h);
 /* the handle's cudaStream_t (as void*), for callers that time or order work around it */

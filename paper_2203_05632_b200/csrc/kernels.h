@@ -30,8 +30,15 @@ struct SpinorParams {
   int npts_pad;        // points in the Phi layout (multiple of 2*WB)
   WalkerBuf walkers;
   int ncomp;
-  const int* ch_fn_off;      // [ncomp + 1] function offsets per channel
-  const double* fn_center;   // [nfunc][3]
+  // basis groups: one per channel, or one per Kramers channel pair (shared basis list)
+  int ngroups;
+  int grp_fn_off[4], grp_nfn[4], grp_k4[4], grp_nf[4];
+  int grp_chan[8];             // (x_a, x_b) per group; x_b = -1 for a single channel
+  long long grp_chi_off[4], grp_b_off[4];
+  int max_nf;
+  double* chi;                 // A fragments per group: [pt/8][mu/4][32]
+  const double* bfrag;         // B fragments per group: [mu/4][nf][32]
+  const double* fn_center;     // [nfunc][3]
   const int* fn_lm;          // [nfunc][2]
   const int* fn_prim_off;    // [nfunc + 1]
   const double* prim_coeff;  // [nprim]
@@ -39,8 +46,6 @@ struct SpinorParams {
   int nuniq;
   const double* uniq_center; // [nuniq][3]
   const double* uniq_zeta;   // [nuniq]
-  int max_ch;                // largest channel size
-  const double2* C;          // [nfunc][n_p] complex coefficients
   int n_occ, n_vir, n_p;
   int Go, Gtot;              // occupied k-groups, total k-groups (multiple of KC4)
   const double* sw;

@@ -80,7 +80,7 @@ struct mcmp2dev_handle {
   double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
   int estimator = 0;
   bool kramers_eligible = false, kramers = false;  // pair_kr.cu path
-  SpinorParams sp{};
+  SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
   DevSites sites{};
   double* d_energies = nullptr;
   double* d_sw = nullptr;
@@ -131,7 +131,7 @@ struct mcmp2dev_handle {
   }
 
   void launch_estimate(const WalkerBuf& wb, int mm, double* step_out) {
-    SpinorParams s = sp;
+    SpinorParams s = kramers ? sp_kr : sp;
     s.npts = 2 * mm;
     s.walkers = wb;
     if (prof) ck(cudaEventRecord(ev[1], stream), "event");
@@ -252,6 +252,58 @@ bool kramers_paired(const mcmp2dev_system* s, const std::vector<int>& ch_off) {
   return true;
 }
 
+// Basis groups of the MO transform and the coefficient matrix in DMMA B-fragment order
+// B[mu/4][nf][lane] (lane: mu%4 = lane%4, real column = lane/4 of fragment nf).
+//  general: one group per channel; per unit of 8 columns two fragments (re, im).
+//  kramers: one group per channel pair (a, b) sharing a basis list; per unit of 8 even
+//           columns 2j four fragments (a re, a im, b re, b im); odd columns follow exactly.
+void build_groups(SpinorParams& sp, const mcmp2dev_system* s, const std::vector<int>& ch_off, bool kramers,
+                  int ptf_max, std::vector<void*>& owned) {
+  const int np = s->n_occ + s->n_vir;
+  sp.ngroups = kramers ? s->ncomp / 2 : s->ncomp;
+  std::vector<double> bfrag;
+  long long chi_doubles = 0;
+  sp.max_nf = 0;
+  for (int g = 0; g < sp.ngroups; ++g) {
+    const int xa = kramers ? 2 * g : g, xb = kramers ? 2 * g + 1 : -1;
+    const int nfn = ch_off[xa + 1] - ch_off[xa], k4n = (nfn + 3) / 4;
+    int units = kramers ? (np / 2 + 7) / 8 : (np + 7) / 8;
+    if (!kramers) units += units & 1;  // warps take 4 fragments
+    const int nf = units * (kramers ? 4 : 2);
+    sp.grp_fn_off[g] = ch_off[xa];
+    sp.grp_nfn[g] = nfn;
+    sp.grp_k4[g] = k4n;
+    sp.grp_nf[g] = nf;
+    sp.grp_chan[2 * g] = xa;
+    sp.grp_chan[2 * g + 1] = xb;
+    sp.grp_chi_off[g] = chi_doubles;
+    sp.grp_b_off[g] = (long long)bfrag.size();
+    sp.max_nf = std::max(sp.max_nf, nf);
+    chi_doubles += (long long)ptf_max * k4n * 32;
+    const size_t base = bfrag.size();
+    bfrag.resize(base + size_t(k4n) * nf * 32, 0.0);
+    for (int k4 = 0; k4 < k4n; ++k4)
+      for (int f = 0; f < nf; ++f)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int mu = k4 * 4 + (lane & 3), r8 = lane >> 2;
+          if (mu >= nfn) continue;
+          double v = 0.0;
+          if (!kramers) {
+            const int col = (f >> 1) * 8 + r8, plane = f & 1;
+            if (col < np) v = s->coeff[2 * (size_t(ch_off[xa] + mu) * np + col) + plane];
+          } else {
+            const int col = 2 * ((f >> 2) * 8 + r8), sub = f & 3;
+            const int x = sub < 2 ? xa : xb, plane = sub & 1;
+            if (col < np) v = s->coeff[2 * (size_t(ch_off[x] + mu) * np + col) + plane];
+          }
+          bfrag[base + (size_t(k4) * nf + f) * 32 + lane] = v;
+        }
+  }
+  sp.bfrag = dupload(bfrag.data(), bfrag.size(), owned);
+  sp.chi = dalloc<double>(size_t(chi_doubles), owned);
+  ck(cudaMemset(sp.chi, 0, size_t(chi_doubles) * sizeof(double)), "memset chi");
+}
+
 void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers) {
   if (!s) throw ArgError("mcmp2dev_create: null system");
   if (s->ncomp != 1 && s->ncomp != 2 && s->ncomp != 4)
@@ -290,8 +342,6 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   const int nfunc = ch_off[s->ncomp];
   h->nfunc = nfunc;
   h->rows = nfunc;
-  int max_ch = 0;
-  for (int x = 0; x < s->ncomp; ++x) max_ch = std::max(max_ch, s->channel_count[x]);
   const int nprim = s->fn_prim_offset[nfunc];
   std::map<std::tuple<double, double, double, double>, int> uniq;
   std::vector<double> uc, uz;
@@ -323,7 +373,6 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   auto& o = h->owned;
   SpinorParams& sp = h->sp;
   sp.ncomp = s->ncomp;
-  sp.ch_fn_off = dupload(ch_off.data(), ch_off.size(), o);
   sp.fn_center = dupload(s->fn_center, size_t(3) * nfunc, o);
   sp.fn_lm = dupload(s->fn_lm, size_t(2) * nfunc, o);
   sp.fn_prim_off = dupload(s->fn_prim_offset, size_t(nfunc) + 1, o);
@@ -332,8 +381,6 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.nuniq = int(uz.size());
   sp.uniq_center = dupload(uc.data(), uc.size(), o);
   sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
-  sp.max_ch = max_ch;
-  sp.C = reinterpret_cast<const double2*>(dupload(s->coeff, size_t(2) * nfunc * h->n_p, o));
   h->kramers_eligible = kramers_paired(s, ch_off);
   h->kramers = h->kramers_eligible;
   sp.n_occ = h->n_occ;
@@ -377,6 +424,11 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(cudaMemset(h->d_phi, 0, phi_doubles * sizeof(double)), "memset phi");
   sp.phi = h->d_phi;
   sp.npts_pad = h->npts_pad;
+  // MO-transform operands: basis groups, B fragments of C, A-fragment buffer for chi
+  const int ptf_max = (h->npts_pad + 63) / 64 * 8;  // point fragments, padded to the 64-point tile
+  h->sp_kr = sp;
+  build_groups(h->sp, s, ch_off, false, ptf_max, o);
+  if (h->kramers_eligible) build_groups(h->sp_kr, s, ch_off, true, ptf_max, o);
   const size_t ntiles = size_t(h->nbmax) * (h->nbmax + 1) / 2;
   h->d_partials = dalloc<double>(ntiles * 4, o);
   h->d_steps = dalloc<double>(size_t(kChunk) * 6, o);
@@ -629,6 +681,16 @@ int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double*
 }
 
 void* mcmp2dev_stream(mcmp2dev_t* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
+  return guard(h, [&] {
+    const double nb = (h->m + WB - 1) / WB, ntiles = nb * (nb + 1) / 2;
+    // DMMAs per tile per k-group (all warps): O phase and V phase, 3 per complex product
+    const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
+    const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
+    *pair_dmma_flop = ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
+  });
+}
 
 int mcmp2dev_kramers(mcmp2dev_t* h, int mode) {
   if (!h) return -1;

@@ -1,23 +1,32 @@
-// spinor.cu — spinor evaluation at the walker points and the MO transform
+// spinor.cu — spinor values at the walker points and the MO transform
 // (reference proj/core/src/model.cpp:55-64 BasisFunction::value, :166-178
 // SpinorSet::evaluate_into, greens.cpp:63-71 set_tau scaling).
 //
-// One CTA owns PTS points and one channel x:
-//   1. exp(-zeta |r - A|^2) once per unique (centre, zeta) and point (the reference
-//      evaluates it per primitive per function; values are identical),
-//   2. chi^x_mu(pt) = S_lm(r - A) * sum_k c_k exp(...) into shared memory ([mu][pt]),
-//   3. Phi^x[pt][p] = sum_mu chi^x_mu(pt) C[off_x + mu][p] (real x complex), scaled by
-//      sqrt(guarded_exp(+-eps_p tau)) and scattered into the pair kernel's fragment layout.
+// Two kernels per step:
+//  chi_kernel  basis values chi^g_mu(pt) for every basis group g (a channel, or a Kramers
+//              channel pair sharing one basis list), exp(-zeta |r-A|^2) once per unique
+//              (centre, zeta) and point, written in DMMA A-fragment order
+//              A_g[pt/8][mu/4][lane] (lane = (pt%8)*4 + mu%4).
+//  mo_kernel   Phi = chi C as a real x (re|im) DMMA GEMM (mma.sync m8n8k4 f64). B is the
+//              coefficient matrix pre-arranged at create time in B-fragment order, so both
+//              operands stream from L2 as coalesced 256-byte warp loads. The epilogue scales
+//              by sqrt(guarded_exp(+-eps tau)) and scatters into the pair kernel's Phi layout.
+// On the Kramers path (exact time-reversal pairs, see pair_kr.cu) only the even columns are
+// transformed: for the partner column, Phi^{a}_{2j+1} = -conj Phi^{b}_{2j} and
+// Phi^{b}_{2j+1} = conj Phi^{a}_{2j} exactly (same products, negated), halving the GEMM.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "pair_common.cuh"
 
 namespace mcmp2dev {
 
 namespace {
-constexpr int PTS = 16;
-constexpr int THREADS = 128;
+using pairk::dmma;
+constexpr int CHI_PTS = 8;
+constexpr int CHI_THREADS = 256;
+constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
 
 __device__ __forceinline__ double ipow(double x, int n) {
   // std::pow(x, n) for n in 0..3 (gaussian.cpp:87-92)
@@ -27,10 +36,9 @@ __device__ __forceinline__ double ipow(double x, int n) {
 // real solid harmonic S_lm as Cartesian monomials (gaussian.cpp:21-39, 87-92)
 __device__ double solid_harmonic(int l, int m, double x, double y, double z) {
   constexpr double kS00 = 0.28209479177387814, kS1 = 0.4886025119029199;
-  constexpr double kS2a = 1.0925484305920792, kS2b = 0.31539156525252005,
-                   kS2c = 0.5462742152960396;
-  constexpr double kS3a = 0.5900435899266435, kS3b = 2.890611442640554,
-                   kS3c = 0.4570457994644658, kS3d = 0.3731763325901154;
+  constexpr double kS2a = 1.0925484305920792, kS2b = 0.31539156525252005, kS2c = 0.5462742152960396;
+  constexpr double kS3a = 0.5900435899266435, kS3b = 2.890611442640554, kS3c = 0.4570457994644658,
+                   kS3d = 0.3731763325901154;
   double s = 0.0;
   auto t = [&](double c, int ix, int iy, int iz) { s += c * ipow(x, ix) * ipow(y, iy) * ipow(z, iz); };
   switch (l) {
@@ -64,97 +72,124 @@ __device__ double solid_harmonic(int l, int m, double x, double y, double z) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS) spinor_kernel(SpinorParams P) {
+__global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   extern __shared__ double smem[];
-  const int x = blockIdx.y;                      // channel
-  const int pt0 = blockIdx.x * PTS;
-  const int f0 = P.ch_fn_off[x], nx = P.ch_fn_off[x + 1] - f0;
-  double* s_pos = smem;                          // [PTS][3]
-  double* s_exp = s_pos + 3 * PTS;               // [nuniq][PTS]
-  double* s_chi = s_exp + P.nuniq * PTS;         // [nx][PTS]
-  const int tid = threadIdx.x;
-
-  if (tid < 3 * PTS) {
-    const int pt = tid / 3, k = tid % 3;
-    const int gp = pt0 + pt;
-    double v = 0.0;
-    if (gp < P.npts) v = P.walkers.at((gp & 1) * 3 + k, gp >> 1);  // 2p <- r1, 2p+1 <- r2
-    s_pos[tid] = v;
+  double* s_pos = smem;              // [CHI_PTS][3]
+  double* s_exp = s_pos + 3 * CHI_PTS;  // [nuniq][CHI_PTS]
+  const int tid = threadIdx.x, pf = blockIdx.x, pt0 = pf * CHI_PTS;
+  if (tid < 3 * CHI_PTS) {
+    const int pt = tid / 3, k = tid % 3, gp = pt0 + pt;
+    s_pos[tid] = gp < P.npts ? P.walkers.at((gp & 1) * 3 + k, gp >> 1) : 0.0;  // 2p <- r1, 2p+1 <- r2
   }
   __syncthreads();
-  for (int i = tid; i < P.nuniq * PTS; i += THREADS) {
-    const int u = i / PTS, pt = i % PTS;
+  for (int i = tid; i < P.nuniq * CHI_PTS; i += CHI_THREADS) {
+    const int u = i / CHI_PTS, pt = i % CHI_PTS;
     const double dx = s_pos[3 * pt] - P.uniq_center[3 * u];
     const double dy = s_pos[3 * pt + 1] - P.uniq_center[3 * u + 1];
     const double dz = s_pos[3 * pt + 2] - P.uniq_center[3 * u + 2];
-    const double r2 = dx * dx + dy * dy + dz * dz;
-    s_exp[i] = exp(-P.uniq_zeta[u] * r2);
+    s_exp[i] = exp(-P.uniq_zeta[u] * (dx * dx + dy * dy + dz * dz));
   }
   __syncthreads();
-  for (int i = tid; i < nx * PTS; i += THREADS) {
-    const int mu = i / PTS, pt = i % PTS, f = f0 + mu;
-    const double dx = s_pos[3 * pt] - P.fn_center[3 * f];
-    const double dy = s_pos[3 * pt + 1] - P.fn_center[3 * f + 1];
-    const double dz = s_pos[3 * pt + 2] - P.fn_center[3 * f + 2];
-    const double ang = solid_harmonic(P.fn_lm[2 * f], P.fn_lm[2 * f + 1], dx, dy, dz);
-    double v = 0.0;
-    if (ang != 0.0) {  // model.cpp:58 early-out
-      double radial = 0.0;
-      for (int k = P.fn_prim_off[f]; k < P.fn_prim_off[f + 1]; ++k)
-        radial += P.prim_coeff[k] * s_exp[P.prim_uniq[k] * PTS + pt];
-      v = ang * radial;
-    }
-    s_chi[i] = v;
-  }
-  __syncthreads();
-
-  for (int col = tid; col < P.n_p; col += THREADS) {
-    double ar[PTS], ai[PTS];
-#pragma unroll
-    for (int p = 0; p < PTS; ++p) ar[p] = ai[p] = 0.0;
-    const double2* cptr = P.C + size_t(f0) * P.n_p + col;
-    for (int mu = 0; mu < nx; ++mu) {
-      const double2 c = __ldg(cptr + size_t(mu) * P.n_p);
-      const double2* chi2 = reinterpret_cast<const double2*>(s_chi + mu * PTS);
-#pragma unroll
-      for (int p = 0; p < PTS / 2; ++p) {
-        const double2 h = chi2[p];
-        ar[2 * p] += h.x * c.x;
-        ai[2 * p] += h.x * c.y;
-        ar[2 * p + 1] += h.y * c.x;
-        ai[2 * p + 1] += h.y * c.y;
+  for (int g = 0; g < P.ngroups; ++g) {
+    const int f0 = P.grp_fn_off[g], nx = P.grp_nfn[g], k4n = P.grp_k4[g];
+    double* A = P.chi + P.grp_chi_off[g] + size_t(pf) * k4n * 32;
+    for (int i = tid; i < k4n * 32; i += CHI_THREADS) {
+      const int k4 = i >> 5, l = i & 31, pt = l >> 2, mu = k4 * 4 + (l & 3);
+      double v = 0.0;
+      if (mu < nx && pt0 + pt < P.npts) {
+        const int f = f0 + mu;
+        const double dx = s_pos[3 * pt] - P.fn_center[3 * f];
+        const double dy = s_pos[3 * pt + 1] - P.fn_center[3 * f + 1];
+        const double dz = s_pos[3 * pt + 2] - P.fn_center[3 * f + 2];
+        const double ang = solid_harmonic(P.fn_lm[2 * f], P.fn_lm[2 * f + 1], dx, dy, dz);
+        if (ang != 0.0) {  // model.cpp:58 early-out
+          double radial = 0.0;
+          for (int k = P.fn_prim_off[f]; k < P.fn_prim_off[f + 1]; ++k)
+            radial += P.prim_coeff[k] * s_exp[P.prim_uniq[k] * CHI_PTS + pt];
+          v = ang * radial;
+        }
       }
+      A[i] = v;
     }
+  }
+}
+
+__global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
+  const int g = blockIdx.z;
+  const int k4n = P.grp_k4[g], nf_total = P.grp_nf[g];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ptf0 = blockIdx.x * 8 + (warp >> 1) * 4;       // 4 point fragments per warp
+  const int nf0 = blockIdx.y * 8 + (warp & 1) * 4;         // 4 n fragments per warp
+  if (nf0 >= nf_total) return;
+  const double* A = P.chi + P.grp_chi_off[g];
+  const double* B = P.bfrag + P.grp_b_off[g];
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
+#pragma unroll 2
+  for (int k4 = 0; k4 < k4n; ++k4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __ldg(A + (size_t(ptf0 + i) * k4n + k4) * 32 + lane);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) b[f] = __ldg(B + (size_t(k4) * nf_total + nf0 + f) * 32 + lane);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) dmma(acc[i][f], a[i], b[f]);
+  }
+  // epilogue: scale and scatter into Phi[chunk][pt][g%KC4][re|im][x*4 + k%4]
+  auto put = [&](int x, int pt, int col, double re, double im) {
     const double w = P.sw[col];
     const bool occ = col < P.n_occ;
     const int kidx = occ ? col : col - P.n_occ;
-    const int g = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
-    const int kk = kidx & 3;
-    const int chunk = g / KC4, gg = g % KC4;
+    const int grp = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
+    double* dst = P.phi + ((size_t(grp / KC4) * P.npts_pad + pt) * KC4 + grp % KC4) * 32 + x * 4 + (kidx & 3);
+    dst[0] = re * w;
+    dst[16] = im * w;
+  };
+  const int xa = P.grp_chan[2 * g], xb = P.grp_chan[2 * g + 1];
 #pragma unroll
-    for (int p = 0; p < PTS; ++p) {
-      const int gp = pt0 + p;
-      if (gp < P.npts) {
-        double* dst = P.phi + ((size_t(chunk) * P.npts_pad + gp) * KC4 + gg) * 32 + x * 4 + kk;
-        dst[0] = ar[p] * w;
-        dst[16] = ai[p] * w;
+  for (int i = 0; i < 4; ++i) {
+    const int pt = (ptf0 + i) * 8 + (lane >> 2);
+    if (pt >= P.npts) continue;
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int r8 = 2 * (lane & 3) + jj;
+      if (xb < 0) {  // general: two units of 8 columns, fragments (re, im)
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const int col = (nf0 / 2 + uu) * 8 + r8;
+          if (col < P.n_p) put(xa, pt, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
+        }
+      } else {  // Kramers pair: fragments (a re, a im, b re, b im) of even column 2j
+        const int j = (nf0 / 4) * 8 + r8, col = 2 * j;
+        if (col < P.n_p) {
+          const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
+          put(xa, pt, col, ar, ai);
+          put(xb, pt, col, br, bi);
+          put(xa, pt, col + 1, -br, bi);  // -conj(Phi^b_2j)
+          put(xb, pt, col + 1, ar, -ai);  //  conj(Phi^a_2j)
+        }
       }
     }
   }
 }
 
-int spinor_smem_bytes(const SpinorParams& P) {
-  return int(sizeof(double)) * (3 * PTS + P.nuniq * PTS + P.max_ch * PTS);
-}
+int spinor_smem_bytes(const SpinorParams& P) { return int(sizeof(double)) * (3 * CHI_PTS + P.nuniq * CHI_PTS); }
 
 cudaError_t spinor_kernel_setup() {
-  return cudaFuncSetAttribute(spinor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return cudaFuncSetAttribute(chi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 void launch_spinor(const SpinorParams& P, cudaStream_t s) {
-  const int smem = spinor_smem_bytes(P);
-  dim3 grid((P.npts + PTS - 1) / PTS, P.ncomp);
-  spinor_kernel<<<grid, THREADS, smem, s>>>(P);
+  const int ptf = (P.npts + CHI_PTS - 1) / CHI_PTS;
+  chi_kernel<<<ptf, CHI_THREADS, spinor_smem_bytes(P), s>>>(P);
+  const int mtiles = (P.npts + 63) / 64;
+  dim3 grid(mtiles, (P.max_nf + 7) / 8, P.ngroups);
+  mo_kernel<<<grid, MO_THREADS, 0, s>>>(P);
 }
 
 }  // namespace mcmp2dev

@@ -81,6 +81,7 @@ def dev() -> C.CDLL:
         d.mcmp2dev_stream.argtypes = [vp]
         d.mcmp2dev_abi_version.restype = ip
         d.mcmp2dev_kramers.argtypes = [vp, ip]
+        d.mcmp2dev_work_executed.argtypes = [vp, dp]
         _dev = d
     return _dev
 

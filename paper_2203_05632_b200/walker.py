@@ -142,7 +142,10 @@ class DeviceWalker:
     def work(self) -> dict:
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         check_dev(self._d.mcmp2dev_work(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h)
-        return {"pair_flop": a.value, "spinor_flop": b.value, "phi_bytes": c.value}
+        e = C.c_double()
+        check_dev(self._d.mcmp2dev_work_executed(self._h, C.byref(e)), self._h)
+        return {"pair_flop": a.value, "spinor_flop": b.value, "phi_bytes": c.value,
+                "pair_dmma_flop_executed": e.value}
 
     def kramers(self, mode: int = -1) -> bool:
         """Kramers-restricted pair kernel: -1 query, 0 off, 1 on when eligible."""
