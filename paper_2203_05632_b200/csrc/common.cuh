@@ -22,6 +22,12 @@ constexpr int KC4 = 4;          // k-groups per pair-kernel stage
 constexpr int WB = 8;           // walkers per pair-kernel tile side
 constexpr int NCH = 4;          // channels per point in the Phi layout (ncomp <= 4, zero padded)
 
+// Bank swizzle of the Phi layout: element (x, k) of point pt sits at (x*4 + k) ^ phi_swz(pt).
+// Points pt and pt^1, and pt and pt^2, land on different halves of the 32 banks, so the
+// alpha-row fragment loads of pair_kr.cu (4 doubles from each of 4 points per half-warp) are
+// conflict-free; whole half-fragment loads stay permutations of one 128-byte row.
+__host__ __device__ __forceinline__ int phi_swz(int pt) { return ((pt ^ (pt >> 1)) & 1) << 2; }
+
 // ------------------------------------------------------------------ device system
 struct DevSites {
   int n;

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           const double* S = acquire();
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
-            auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+            auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int pa = 2 * (2 * wq + hl) + e;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
 #pragma unroll
         for (int gg = 0; gg < KC4; ++gg) {
           if (c * KC4 + gg >= P.Go + P.Gv) break;  // zero padding at the end
-          auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + l16]; };
+          auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
           double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
 #pragma unroll
           for (int qi = 0; qi < 2; ++qi) {

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
           const double* S = acquire();
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
-            auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + off]; };
+            auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))]; };
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int pb = HALF_PTS + 2 * (4 * wp + (lane >> 3)) + e;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
 #pragma unroll
         for (int gg = 0; gg < KC4; ++gg) {
           if (c * KC4 + gg >= P.Go + P.Gv) break;
-          auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + off]; };
+          auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))]; };
           double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {

@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
     const bool occ = col < P.n_occ;
     const int kidx = occ ? col : col - P.n_occ;
     const int grp = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
-    double* dst = P.phi + ((size_t(grp / KC4) * P.npts_pad + pt) * KC4 + grp % KC4) * 32 + x * 4 + (kidx & 3);
+    double* dst = P.phi + ((size_t(grp / KC4) * P.npts_pad + pt) * KC4 + grp % KC4) * 32 +
+                  ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
     dst[0] = re * w;
     dst[16] = im * w;
   };
