@@ -1039,6 +1039,12 @@ RunConfig parse_config_text(const std::string& text) {  // driver.cpp:65-121
     else if (key == "checkpoint-interval") { want(1); cfg.checkpoint_interval = long(to_ll(toks[1], key)); }
     else if (key == "trace") { want(1); cfg.trace_path = toks[1]; }
     else if (key == "step-size") { want(1); cfg.step_size = to_d(toks[1], key); }
+    else if (key == "estimator") {
+      want(1);
+      if (toks[1] != "literal" && toks[1] != "physical")
+        throw std::runtime_error("config: key 'estimator' expects literal or physical, got '" + toks[1] + "'");
+      cfg.physical = toks[1] == "physical";
+    }
     else if (key == "weight") {
       want(5);
       const int z = atomic_number(toks[1]);
@@ -1078,6 +1084,7 @@ std::string canonical_config_text(const RunConfig& c) {  // driver.cpp:140-159
   os << "seed " << c.seed << "\n";
   os << "spinors " << c.spinor_path << "\n";
   if (c.step_size) os << "step-size " << format_double(*c.step_size) << "\n";
+  if (c.physical) os << "estimator physical\n";
   if (c.steps) os << "steps " << *c.steps << "\n";
   if (c.target_rel_err) os << "target-rel-err " << format_double(*c.target_rel_err) << "\n";
   if (!c.trace_path.empty()) os << "trace " << c.trace_path << "\n";
@@ -1093,6 +1100,7 @@ std::uint64_t config_hash(const RunConfig& c, std::uint64_t spinor_hash) {  // d
   os << "burnin " << c.burn_in << "\n";
   os << "spinorhash " << spinor_hash << "\n";
   if (c.step_size) os << "step-size " << format_double(*c.step_size) << "\n";
+  if (c.physical) os << "estimator physical\n";
   os << "walkers " << c.walkers << "\n";
   weight_lines(os, c);
   return fnv1a64(os.str());
@@ -1345,6 +1353,7 @@ class Engine {  // driver.cpp:336-475
   void advance(WorkerState& w, long long nsteps, std::vector<StepRecord>* rec) {  // :440-450
     if (nsteps <= 0) return;
     EstimatorWorkspace ws(spinors_, cfg_.walkers);
+    ws.physical = cfg_.physical;
     for (long long s = 0; s < nsteps; ++s) {
       metropolis_step(w.ensemble, *spec_);
       const double tau = tau_->sample(w.ensemble.rng.uniform());

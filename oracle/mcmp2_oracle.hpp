@@ -302,6 +302,7 @@ struct RunConfig {  // driver.hpp:17-32 (+ `step-size` extension, SURVEY section
   std::string trace_path;
   std::map<int, WeightParams> weight_overrides;
   std::optional<double> step_size;  // extension: fixed sigma_step, burn-in without adaptation
+  bool physical = false;            // extension: `estimator physical`
   void validate() const;            // driver.cpp:50-63
 };
 

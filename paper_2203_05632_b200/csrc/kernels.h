@@ -60,6 +60,7 @@ struct PairParams {
   const DevState* st_ro;
   DevState* st;
   double ng2, w_direct, w_exchange;
+  int physical;              // 1: Tr(o1 va) Tr(o2 vb), Tr(o1 vd o2 vc) epilogue (opt-in)
   double* partials;          // [ntiles][4]
   double* step_out;          // [6] of this step
 };

@@ -151,6 +151,7 @@ struct mcmp2dev_handle {
     p.ng2 = ng * ng;
     p.w_direct = w_direct;
     p.w_exchange = w_exchange;
+    p.physical = estimator == MCMP2DEV_ESTIMATOR_PHYSICAL;
     p.partials = d_partials;
     p.step_out = step_out;
     if (kramers) launch_pair_kr(p, stream);
@@ -330,8 +331,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   h->w_direct = s->w_direct;
   h->w_exchange = s->w_exchange;
   h->estimator = s->estimator;
-  if (s->estimator != MCMP2DEV_ESTIMATOR_LITERAL)
-    throw ArgError("mcmp2dev_create: only the literal estimator is implemented on the device");
+  if (s->estimator != MCMP2DEV_ESTIMATOR_LITERAL && s->estimator != MCMP2DEV_ESTIMATOR_PHYSICAL)
+    throw ArgError("mcmp2dev_create: unknown estimator");
 
   // ---- basis: flatten, dedupe exp(-zeta r^2) by (centre, zeta) ----
   std::vector<int> ch_off(s->ncomp + 1, 0);
@@ -382,6 +383,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.uniq_center = dupload(uc.data(), uc.size(), o);
   sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
   h->kramers_eligible = kramers_paired(s, ch_off);
+  // the Kramers kernel implements the literal contraction only
+  h->kramers_eligible = h->kramers_eligible && h->estimator == MCMP2DEV_ESTIMATOR_LITERAL;
   h->kramers = h->kramers_eligible;
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;

@@ -33,22 +33,31 @@
 namespace mcmp2dev {
 
 namespace {
-constexpr int STAGES = 4;
 constexpr int CONSUMERS = 8;                              // MMA warps (wq 0..3 x wp 0..1)
 constexpr int THREADS = 32 * (CONSUMERS + 1);             // + one TMA producer warp
 constexpr int HALF_PTS = 2 * WB;                          // 16 points per walker block
 constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;    // 32 points x KC4 groups x 32
 constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per stage
 constexpr int SO_DOUBLES = 512;                           // per consumer warp: 2x2x4 blocks of 4x4 complex
-constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
+constexpr int SV_DOUBLES = 8 * 64 * 2;                    // physical epilogue: 8 pairs x 8x8 complex V
+
+template <bool PHYS>
+struct Cfg {
+  static constexpr int STAGES = PHYS ? 3 : 4;
+  static constexpr int SMEM_BYTES =
+      (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES + (PHYS ? CONSUMERS * SV_DOUBLES : 0)) * 8 + 2 * STAGES * 8;
+};
 
 }  // namespace
 using namespace pairk;
 
+template <bool PHYS>
 __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
+  constexpr int STAGES = Cfg<PHYS>::STAGES;
   extern __shared__ __align__(128) double sm[];
   double* const sO = sm + STAGES * STAGE_DOUBLES;  // [warp][e][qi][pj][y][x] complex o
-  uint64_t* const full = reinterpret_cast<uint64_t*>(sO + CONSUMERS * SO_DOUBLES);
+  double* const sV = sO + CONSUMERS * SO_DOUBLES;  // PHYS only: [warp][pair][e_q][e_p][x][y]
+  uint64_t* const full = reinterpret_cast<uint64_t*>(sV + (PHYS ? CONSUMERS * SV_DOUBLES : 0));
   uint64_t* const empty = full + STAGES;
   __shared__ double s_red[CONSUMERS][4];
   __shared__ bool s_last;
@@ -195,6 +204,78 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
         release();
       }
 
+      if constexpr (PHYS) {
+        // ---- opt-in physical epilogue: -w_d Tr(o1 va) Tr(o2 vb), -w_x Tr(o1 vd o2 vc)
+        double* const sv = sV + warp * SV_DOUBLES;  // [pair][e_q][e_p][x][y] complex
+        {
+          const int eq = hl, x = (lane >> 2) & 3, ep = (lane & 3) >> 1;
+#pragma unroll
+          for (int qi = 0; qi < 2; ++qi)
+#pragma unroll
+            for (int pj = 0; pj < 4; ++pj)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int y = 2 * (lane & 1) + j;
+                const int idx = (((((qi * 4 + pj) * 2 + eq) * 2 + ep) * 16) + x * 4 + y) * 2;
+                sv[idx] = u1[qi][pj][j] + u2[qi][pj][j];
+                sv[idx + 1] = u3[qi][pj][j] - u1[qi][pj][j] + u2[qi][pj][j];
+              }
+        }
+        __syncwarp();
+        if (lane < 8) {
+          const int qi = lane >> 2, pj = lane & 3;
+          const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
+          if (q < P.m && p < P.m && q > p) {
+            auto O = [&](int e, int x, int y, int c) { return so[((((e * 2 + qi) * 4 + pj) * 16) + y * 4 + x) * 2 + c]; };
+            auto V = [&](int eq, int ep, int x, int y, int c) {
+              return sv[(((((qi * 4 + pj) * 2 + eq) * 2 + ep) * 16) + x * 4 + y) * 2 + c];
+            };
+            // t1 = Tr(o1 va), t2 = Tr(o2 vb): va = V(eq 0, ep 0), vb = V(1, 1)
+            double t1r = 0, t1i = 0, t2r = 0, t2i = 0;
+            for (int x = 0; x < 4; ++x)
+              for (int y = 0; y < 4; ++y) {
+                double ar = O(0, x, y, 0), ai = O(0, x, y, 1), br = V(0, 0, y, x, 0), bi = V(0, 0, y, x, 1);
+                t1r += ar * br - ai * bi;
+                t1i += ar * bi + ai * br;
+                ar = O(1, x, y, 0), ai = O(1, x, y, 1), br = V(1, 1, y, x, 0), bi = V(1, 1, y, x, 1);
+                t2r += ar * br - ai * bi;
+                t2i += ar * bi + ai * br;
+              }
+            // tx = Tr(m1 m2), m1 = o1 vd (vd = V(0, 1)), m2 = o2 vc (vc = V(1, 0))
+            double m1[4][4][2], m2[4][4][2];
+            for (int x = 0; x < 4; ++x)
+              for (int y = 0; y < 4; ++y) {
+                double ar = 0, ai = 0, br = 0, bi = 0;
+                for (int k = 0; k < 4; ++k) {
+                  const double o1r = O(0, x, k, 0), o1i = O(0, x, k, 1), dr = V(0, 1, k, y, 0), di = V(0, 1, k, y, 1);
+                  ar += o1r * dr - o1i * di;
+                  ai += o1r * di + o1i * dr;
+                  const double o2r = O(1, x, k, 0), o2i = O(1, x, k, 1), cr = V(1, 0, k, y, 0), ci = V(1, 0, k, y, 1);
+                  br += o2r * cr - o2i * ci;
+                  bi += o2r * ci + o2i * cr;
+                }
+                m1[x][y][0] = ar, m1[x][y][1] = ai, m2[x][y][0] = br, m2[x][y][1] = bi;
+              }
+            double txr = 0, txi = 0;
+            for (int x = 0; x < 4; ++x)
+              for (int y = 0; y < 4; ++y) {
+                txr += m1[x][y][0] * m2[y][x][0] - m1[x][y][1] * m2[y][x][1];
+                txi += m1[x][y][0] * m2[y][x][1] + m1[x][y][1] * m2[y][x][0];
+              }
+            const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+            const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+            const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);
+            const double adr = -P.w_direct * t1r, adi = -P.w_direct * t1i;
+            acc_dr += (adr * t2r - adi * t2i) * inv;
+            acc_di += (adr * t2i + adi * t2r) * inv;
+            acc_xr += -P.w_exchange * txr * inv;
+            acc_xi += -P.w_exchange * txi * inv;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+
       // ---- epilogue: literal element-wise contraction of o with V (estimator.cpp:26-32) ----
       const int xx = (lane >> 2) & 3, ep = (lane & 3) >> 1;
 #pragma unroll
@@ -240,6 +321,15 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           }
         }
       __syncwarp();  // all lanes done reading `so` before the next tile rewrites it
+    }
+    if constexpr (PHYS) {  // lanes 0..7 hold partial sums: fixed shuffle tree into lane 0
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        acc_dr += __shfl_down_sync(0xffffffffu, acc_dr, o);
+        acc_di += __shfl_down_sync(0xffffffffu, acc_di, o);
+        acc_xr += __shfl_down_sync(0xffffffffu, acc_xr, o);
+        acc_xi += __shfl_down_sync(0xffffffffu, acc_xi, o);
+      }
     }
     if (lane == 0) {
       s_red[warp][0] = acc_dr;
@@ -292,7 +382,10 @@ cudaError_t pair_kernel_setup() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg<false>::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<true>::SMEM_BYTES);
 }
 
 int pair_grid(int nb) {
@@ -304,7 +397,10 @@ int pair_grid(int nb) {
 }
 
 void launch_pair(const PairParams& P, cudaStream_t s) {
-  pair_kernel<<<pair_grid(P.nb), THREADS, SMEM_BYTES, s>>>(P);
+  if (P.physical)
+    pair_kernel<true><<<pair_grid(P.nb), THREADS, Cfg<true>::SMEM_BYTES, s>>>(P);
+  else
+    pair_kernel<false><<<pair_grid(P.nb), THREADS, Cfg<false>::SMEM_BYTES, s>>>(P);
 }
 
 }  // namespace mcmp2dev

@@ -93,7 +93,7 @@ mcmp2h_system* mcmp2h_system_load(const char* spinor_path, const char* config_te
     if (!s.nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
     const RunConfig c = parse_config_text(config_text ? config_text : "");
     WeightSpec w(*s.nuclei, c.weight_overrides);
-    DeviceSystem d = make_device_system(s, w, MCMP2DEV_ESTIMATOR_LITERAL);
+    DeviceSystem d = make_device_system(s, w, c.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
     out = new mcmp2h_system{std::move(s), std::move(w), std::move(d)};
   });
   return out;

@@ -143,6 +143,12 @@ RunConfig parse_config_text(const std::string& text) {
     else if (k == "checkpoint-interval") arity(1), c.checkpoint_interval = long(as_int(t[1], k));
     else if (k == "trace") arity(1), c.trace_path = t[1];
     else if (k == "step-size") arity(1), c.step_size = as_num(t[1], k);
+    else if (k == "estimator") {
+      arity(1);
+      if (t[1] != "literal" && t[1] != "physical")
+        throw std::runtime_error("config: key 'estimator' expects literal or physical, got '" + t[1] + "'");
+      c.physical = t[1] == "physical";
+    }
     else if (k == "weight") {
       arity(5);
       c.weight_overrides[atomic_number(t[1])] = {as_num(t[2], k), as_num(t[3], k), as_num(t[4], k), as_num(t[5], k)};
@@ -173,6 +179,7 @@ std::string canonical_config_text(const RunConfig& c) {  // driver.cpp:140-159, 
   os << "checkpoint-interval " << c.checkpoint_interval << "\n" << "seed " << c.seed << "\n";
   os << "spinors " << c.spinor_path << "\n";
   if (c.step_size) os << "step-size " << format_double(*c.step_size) << "\n";
+  if (c.physical) os << "estimator physical\n";
   if (c.steps) os << "steps " << *c.steps << "\n";
   if (c.target_rel_err) os << "target-rel-err " << format_double(*c.target_rel_err) << "\n";
   if (!c.trace_path.empty()) os << "trace " << c.trace_path << "\n";
@@ -187,6 +194,7 @@ std::uint64_t config_hash(const RunConfig& c, std::uint64_t spinor_hash) {  // d
   os << "blocksize " << c.block_size << "\n" << "burnin " << c.burn_in << "\n";
   os << "spinorhash " << spinor_hash << "\n";
   if (c.step_size) os << "step-size " << format_double(*c.step_size) << "\n";
+  if (c.physical) os << "estimator physical\n";
   os << "walkers " << c.walkers << "\n";
   put_weights(os, c);
   return fnv1a64(os.str());
@@ -229,7 +237,7 @@ void check_dev(int rc, const mcmp2dev_t* h) {
 
 DeviceWorker::DeviceWorker(const SpinorSet& s, const WeightSpec& w, const RunConfig& cfg, int index, int device)
     : acc(cfg.block_size), index_(index), walkers_(cfg.walkers), cfg_(&cfg) {
-  DeviceSystem sys = make_device_system(s, w, MCMP2DEV_ESTIMATOR_LITERAL);
+  DeviceSystem sys = make_device_system(s, w, cfg.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
   check_dev(mcmp2dev_create(&sys.view, device, cfg.walkers, &h_), nullptr);
 }
 

@@ -144,6 +144,7 @@ struct RunConfig {
   std::string trace_path;
   std::map<int, WeightParams> weight_overrides;
   std::optional<double> step_size;  // extension: fixed sigma_step, no adaptation
+  bool physical = false;            // extension: `estimator physical`, default literal
   void validate() const;
 };
 RunConfig parse_config_text(const std::string& text);

@@ -1,0 +1,77 @@
+"""syn4c (reference oracle.cpp:357-393): deterministic energies for both estimator forms, the
+oracle's MC against them (CPU), and the device against both (GPU).
+
+SURVEY.md section 0 finding 2: the reference's literal element-wise estimator converges to
++0.013087649253 on syn4c, while the physical MP2 energy is -0.003932252921; the physical trace
+form Tr(o1 va) Tr(o2 vb), Tr(o1 vd o2 vc) is the opt-in `estimator physical`."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle_py
+import syn4c
+
+E2_PHYSICAL = -0.003932252921   # SURVEY.md section 0 (oracle_mp2_energy of syn4c)
+E2_LITERAL = 0.013087649253     # SURVEY.md section 0 (exact limit of the literal estimator)
+
+
+@pytest.fixture(scope="module")
+def syn4c_file(tmp_path_factory):
+    p = tmp_path_factory.mktemp("syn4c") / "syn4c.spinor"
+    C = syn4c.write_spinor_file(p)
+    return p, C
+
+
+def test_deterministic_energies_pin_survey_values(syn4c_file):
+    _, C = syn4c_file
+    assert syn4c.mp2_energy(C) == pytest.approx(E2_PHYSICAL, abs=5e-13)
+    assert syn4c.literal_limit(C) == pytest.approx(E2_LITERAL, abs=5e-13)
+
+
+def blocked(values, nb=100):
+    v = np.asarray(values)
+    bm = v[: len(v) // nb * nb].reshape(-1, nb).mean(1)
+    return v.mean(), bm.std() / math.sqrt(len(bm))
+
+
+@pytest.mark.parametrize("physical,target", [(False, E2_LITERAL), (True, E2_PHYSICAL)])
+def test_oracle_mc_converges_to_deterministic(syn4c_file, physical, target):
+    sp, _ = syn4c_file
+    o = oracle_py.OracleSystem(sp, "")
+    vals = [o.trajectory(seed=100 + s, stream=0, m=16, burn=300, nsteps=3000, physical=physical)["est"][:, 0]
+            for s in range(4)]
+    mean, err = blocked(np.concatenate(vals))
+    assert abs(mean - target) < 4 * err
+
+
+@pytest.mark.gpu
+def test_device_physical_replay_matches_oracle(syn4c_file, cfgdir):
+    from paper_2203_05632_b200 import DeviceWalker, System
+    cases = [(syn4c_file[0], "", 9), (cfgdir / "cfg2.spinor", (cfgdir / "cfg2.conf").read_text(), 12),
+             (cfgdir / "syn1c.spinor", "", 7)]
+    for sp, conf, m in cases:
+        o = oracle_py.OracleSystem(sp, conf)
+        tr = o.trajectory(seed=5, stream=0, m=m, burn=30, nsteps=3, physical=True)
+        dw = DeviceWalker(System(sp, conf + "estimator physical\n"), max_walkers=m)
+        assert not dw.kramers()  # the Kramers kernel is literal-only
+        got = dw.replay(tr["walkers"], tr["tau"])
+        ref = tr["est"]
+        for k in (0, 2, 4):
+            assert np.max(np.abs(got[:, k] - ref[:, k]) / np.abs(ref[:, k])) < 1e-10
+        assert np.max(np.abs(got[:, 1] - ref[:, 1])) <= 1e-10 * np.max(np.abs(ref[:, 0]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("physical,target", [(False, E2_LITERAL), (True, E2_PHYSICAL)])
+def test_device_mc_converges_to_deterministic(syn4c_file, physical, target):
+    """8 workers x 25000 steps of m = 32 through the host Engine on the device."""
+    from paper_2203_05632_b200 import walker
+    sp, _ = syn4c_file
+    cfg = (f"spinors {sp}\nsteps 200000\nwalkers 32\nworkers 8\nseed 7\nburnin 500\n"
+           f"checkpoint-interval 25000\n" + ("estimator physical\n" if physical else ""))
+    rep = walker.run_config_text(cfg)
+    value = float(rep.splitlines()[0].split()[2])
+    sigma = float(rep.splitlines()[1].split()[2])
+    assert abs(value - target) < 4 * sigma, (value, sigma, target)
+    assert sigma < abs(target) / 3  # the run resolves the sign of the two limits
