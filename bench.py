@@ -41,6 +41,49 @@ WORKLOAD = {
 }
 
 
+class NvmlClocks:
+    """SM clock and clock-event reasons polled every 5 ms via NVML while the timed region runs."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, local_rank: int):
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(local_rank)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = get_reasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+            time.sleep(0.005)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join()
+
+    def summary(self):
+        mx = self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "NVML, 5 ms polling"}
+
+
 def clocks_sampler(path: Path):
     """nvidia-smi clocks + throttle reasons every 200 ms during the timed region."""
     q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -120,7 +163,7 @@ def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, qui
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4", choices=sorted(WALKERS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -182,10 +225,16 @@ def main():
 
     # ---- timed region: K steps, device time per step on the handle's stream, L2 flushed between ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    smi, smi_f = clocks_sampler(tmp / "clocks.csv") if rank == 0 else (None, None)
+    try:
+        clk = NvmlClocks(local)
+    except Exception:  # NVML unavailable: fall back to nvidia-smi sampling
+        clk = None
+    smi, smi_f = clocks_sampler(tmp / "clocks.csv") if (rank == 0 and clk is None) else (None, None)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    if clk:
+        clk.__enter__()
     for k in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -194,6 +243,8 @@ def main():
         with torch.cuda.stream(stream):
             ev[k][1].record(stream)
     torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
     if dist:
         dist.barrier()
     if smi:
@@ -276,7 +327,7 @@ def main():
         "gpu_launches": 3 * args.steps,
         "step_values_checksum": float(np.sum(vals)),
     }
-    cl = clocks_summary(tmp / "clocks.csv", local)
+    cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", local)
     if cl:
         line["clocks"] = cl
     if world == 1 and not args.no_cpu_baseline:
