@@ -27,6 +27,7 @@ using namespace mcmp2dev;
 namespace {
 
 constexpr int kChunk = 1024;  // steps per device->host copy of StepEstimates
+constexpr int kGraphSteps = 32;  // production steps per captured CUDA graph (even)
 thread_local std::string g_create_error;
 
 struct CudaError : std::runtime_error {
@@ -106,6 +107,34 @@ struct mcmp2dev_handle {
   cudaEvent_t ev[4]{};
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_n[4] = {0, 0, 0, 0};
+
+  // captured production steps: valid for one (m, parity, RNG key/stream, kernel path)
+  cudaGraphExec_t graph_exec = nullptr;
+  double* d_gsteps = nullptr;  // [kGraphSteps][6] step results written by the graph
+  struct GraphKey {
+    int m = -1, cur = -1, kramers = -1;
+    uint32_t k0 = 0, k1 = 0, stream = 0;
+    bool operator==(const GraphKey&) const = default;
+  } graph_key;
+
+  void ensure_graph() {
+    const GraphKey key{m, cur, kramers ? 1 : 0, k0, k1, rstream};
+    if (graph_exec && key == graph_key) return;
+    if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+    const int c0 = cur;
+    for (int s = 0; s < kGraphSteps; ++s) {  // even count: the walker parity returns to c0
+      launch_walk(walk_params(WALK_PRODUCTION, 0, 0), stream);
+      cur ^= 1;
+      launch_estimate(buf[cur], m, d_gsteps + 6 * s);
+    }
+    cur = c0;
+    ck(cudaStreamEndCapture(stream, &g), "graph capture end");
+    ck(cudaGraphInstantiate(&graph_exec, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    graph_key = key;
+  }
 
   WalkParams walk_params(int mode, long long sweep, int adapt) {
     WalkParams P{};
@@ -435,6 +464,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   const size_t ntiles = size_t(h->nbmax) * (h->nbmax + 1) / 2;
   h->d_partials = dalloc<double>(ntiles * 4, o);
   h->d_steps = dalloc<double>(size_t(kChunk) * 6, o);
+  h->d_gsteps = dalloc<double>(size_t(kGraphSteps) * 6, o);
   h->d_replay = dalloc<double>(size_t(h->mmax) * 8, o);
   ck(cudaMallocHost(&h->h_steps, sizeof(double) * kChunk * 6), "cudaMallocHost");
   ck(cudaMallocHost(&h->h_replay, sizeof(double) * h->mmax * 8), "cudaMallocHost");
@@ -480,6 +510,7 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
   if (h->h_replay) cudaFreeHost(h->h_replay);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return MCMP2DEV_OK;
@@ -607,17 +638,31 @@ int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) 
     require_ensemble(h);
     if (nsteps < 0) throw ArgError("advance: negative step count");
     long done = 0;
+    const bool want = values || imags;
     while (done < nsteps) {
       const long n = std::min<long>(kChunk, nsteps - done);
-      for (long s = 0; s < n; ++s) {
+      long s = 0;
+      // whole blocks of kGraphSteps steps replay one captured CUDA graph (4 launches per step)
+      if (!h->prof && n >= kGraphSteps) {
+        h->ensure_graph();
+        for (; s + kGraphSteps <= n; s += kGraphSteps) {
+          ck(cudaGraphLaunch(h->graph_exec, h->stream), "cudaGraphLaunch");
+          if (want)
+            ck(cudaMemcpyAsync(h->h_steps + 6 * s, h->d_gsteps, sizeof(double) * 6 * kGraphSteps,
+                               cudaMemcpyDeviceToHost, h->stream),
+               "steps D2H");
+        }
+      }
+      const long s0 = s;
+      for (; s < n; ++s) {
         if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
         launch_walk(h->walk_params(WALK_PRODUCTION, 0, 0), h->stream);
         h->cur ^= 1;
         h->launch_estimate(h->buf[h->cur], h->m, h->d_steps + 6 * s);
       }
-      if (values || imags) {
-        ck(cudaMemcpyAsync(h->h_steps, h->d_steps, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost,
-                           h->stream),
+      if (want && n > s0) {
+        ck(cudaMemcpyAsync(h->h_steps + 6 * s0, h->d_steps + 6 * s0, sizeof(double) * 6 * (n - s0),
+                           cudaMemcpyDeviceToHost, h->stream),
            "steps D2H");
       }
       h->check_state_errors();  // synchronises
