@@ -277,6 +277,7 @@ def main():
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
 
     # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
+    dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
     st = dw.get_ensemble()
     torch.cuda.synchronize()
     if dist:

@@ -107,6 +107,9 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e); /* e->walkers: [
  * runs in the reference order (driver.cpp:443-448). values/imags may be NULL (kept on
  * device; for kernel timing). */
 int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags);
+/* Optional: capture the CUDA graphs advance() replays (32 steps each) for the current
+ * ensemble now, so the first advance() does not pay the capture; executes nothing. */
+int mcmp2dev_prepare(mcmp2dev_t* h);
 /* Replay: mc_step_estimate at given walker positions and tau (estimator.cpp:35-63).
  * walkers [nsteps][m][8] = r1[3], r2[3], g1, g2; tau [nsteps]; out [nsteps]. The device
  * ensemble is not modified. m = 2 is sample_term (estimator.cpp:65-75). */

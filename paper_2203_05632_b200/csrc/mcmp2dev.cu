@@ -108,18 +108,20 @@ struct mcmp2dev_handle {
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_n[4] = {0, 0, 0, 0};
 
-  // captured production steps: valid for one (m, parity, RNG key/stream, kernel path)
-  cudaGraphExec_t graph_exec = nullptr;
+  // captured production steps, one per walker-buffer parity; valid for one (m, RNG key/stream,
+  // kernel path)
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   double* d_gsteps = nullptr;  // [kGraphSteps][6] step results written by the graph
   struct GraphKey {
-    int m = -1, cur = -1, kramers = -1;
+    int m = -1, kramers = -1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
     bool operator==(const GraphKey&) const = default;
-  } graph_key;
+  } graph_keys[2];
 
-  void ensure_graph() {
-    const GraphKey key{m, cur, kramers ? 1 : 0, k0, k1, rstream};
-    if (graph_exec && key == graph_key) return;
+  cudaGraphExec_t ensure_graph() {
+    const GraphKey key{m, kramers ? 1 : 0, k0, k1, rstream};
+    cudaGraphExec_t& graph_exec = graphs[cur];
+    if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
     cudaGraph_t g = nullptr;
     ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "graph capture");
@@ -133,7 +135,8 @@ struct mcmp2dev_handle {
     ck(cudaStreamEndCapture(stream, &g), "graph capture end");
     ck(cudaGraphInstantiate(&graph_exec, g, 0), "graph instantiate");
     cudaGraphDestroy(g);
-    graph_key = key;
+    graph_keys[cur] = key;
+    return graph_exec;
   }
 
   WalkParams walk_params(int mode, long long sweep, int adapt) {
@@ -510,7 +513,8 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
   if (h->h_replay) cudaFreeHost(h->h_replay);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
-  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  for (auto& g : h->graphs)
+    if (g) cudaGraphExecDestroy(g);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return MCMP2DEV_OK;
@@ -644,9 +648,9 @@ int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) 
       long s = 0;
       // whole blocks of kGraphSteps steps replay one captured CUDA graph (4 launches per step)
       if (!h->prof && n >= kGraphSteps) {
-        h->ensure_graph();
+        cudaGraphExec_t graph = h->ensure_graph();
         for (; s + kGraphSteps <= n; s += kGraphSteps) {
-          ck(cudaGraphLaunch(h->graph_exec, h->stream), "cudaGraphLaunch");
+          ck(cudaGraphLaunch(graph, h->stream), "cudaGraphLaunch");
           if (want)
             ck(cudaMemcpyAsync(h->h_steps + 6 * s, h->d_gsteps, sizeof(double) * 6 * kGraphSteps,
                                cudaMemcpyDeviceToHost, h->stream),
@@ -729,6 +733,16 @@ int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double*
 }
 
 void* mcmp2dev_stream(mcmp2dev_t* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int mcmp2dev_prepare(mcmp2dev_t* h) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    for (int k = 0; k < 2; ++k) {  // both walker-buffer parities; nothing is executed
+      h->ensure_graph();
+      h->cur ^= 1;
+    }
+  });
+}
 
 int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
   return guard(h, [&] {

@@ -247,6 +247,7 @@ void DeviceWorker::init_and_burn_in() {  // driver.cpp:354-358 (+ step-size exte
   check_dev(mcmp2dev_init_ensemble(h_, walkers_, cfg_->seed, std::uint32_t(index_)), h_);
   if (cfg_->step_size) check_dev(mcmp2dev_set_sigma_step(h_, *cfg_->step_size), h_);
   check_dev(mcmp2dev_burn_in(h_, cfg_->burn_in, cfg_->step_size ? 0 : 1), h_);
+  check_dev(mcmp2dev_prepare(h_), h_);
 }
 
 void DeviceWorker::advance(long long nsteps) {  // driver.cpp:440-450
@@ -302,6 +303,7 @@ void DeviceWorker::load_ensemble(const std::string& text) {  // sampler.cpp:107-
     if (!(is >> v)) throw std::runtime_error("checkpoint: malformed walker record");
   e.walkers = w.data();
   check_dev(mcmp2dev_set_ensemble(h_, &e), h_);
+  check_dev(mcmp2dev_prepare(h_), h_);
 }
 
 // ------------------------------------------------------------------ checkpoint (driver.cpp:218-305)

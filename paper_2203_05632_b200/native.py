@@ -82,6 +82,7 @@ def dev() -> C.CDLL:
         d.mcmp2dev_abi_version.restype = ip
         d.mcmp2dev_kramers.argtypes = [vp, ip]
         d.mcmp2dev_work_executed.argtypes = [vp, dp]
+        d.mcmp2dev_prepare.argtypes = [vp]
         _dev = d
     return _dev
 

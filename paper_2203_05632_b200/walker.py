@@ -119,6 +119,10 @@ class DeviceWalker:
         check_dev(self._d.mcmp2dev_advance(self._h, nsteps, dptr(v), dptr(im)), self._h)
         return v, im
 
+    def prepare(self) -> None:
+        """Capture the CUDA graphs advance() replays (setup cost, executes nothing)."""
+        check_dev(self._d.mcmp2dev_prepare(self._h), self._h)
+
     def replay(self, walkers: np.ndarray, tau: np.ndarray) -> np.ndarray:
         """mc_step_estimate at given positions: walkers [nsteps, m, 8], tau [nsteps] ->
         [nsteps, 6] = value, imag, direct re/im, exchange re/im (sums before /C(m,2))."""
