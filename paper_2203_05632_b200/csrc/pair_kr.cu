@@ -23,7 +23,10 @@ namespace mcmp2dev {
 
 namespace {
 using namespace pairk;
-constexpr int STAGES = 3;
+#ifndef KR_STAGES
+#define KR_STAGES 3
+#endif
+constexpr int STAGES = KR_STAGES;
 constexpr int CONSUMERS = 4;                              // (wq, wp) in {0,1}^2, 4x4 walker pairs each
 constexpr int THREADS = 32 * (CONSUMERS + 1);
 constexpr int HALF_PTS = 2 * WB;
@@ -182,6 +185,9 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
         release();
       }
 
+#ifdef KR_SKIP_EPILOGUE  // timing experiment only: results are wrong
+      if (u1[0][0][0] != 12345.0) continue;
+#endif
       // ---- epilogue: f = 2 Re sum_{x alpha, y} o v; real direct/exchange terms ----
       const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
 #pragma unroll

@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB = PKG / "lib"
+LIB = Path(os.environ.get("MCMP2_LIBDIR", PKG / "lib"))  # override only for kernel-variant experiments
 
 OK, INVALID_ARGUMENT, RUNTIME, CUDA = 0, 1, 2, 3
 
