@@ -18,7 +18,10 @@
 
 namespace mcmp2dev {
 
-constexpr int KC4 = 4;          // k-groups per pair-kernel stage
+#ifndef KC4_GROUPS
+#define KC4_GROUPS 4
+#endif
+constexpr int KC4 = KC4_GROUPS;  // k-groups per pair-kernel stage
 constexpr int WB = 8;           // walkers per pair-kernel tile side
 constexpr int NCH = 4;          // channels per point in the Phi layout (ncomp <= 4, zero padded)
 

@@ -24,7 +24,7 @@ namespace mcmp2dev {
 namespace {
 using namespace pairk;
 #ifndef KR_STAGES
-#define KR_STAGES 3
+#define KR_STAGES 2  // measured on B200 cfg4: 2 stages 4.29 ms, 3 stages 4.35 ms, 4 stages (1 CTA/SM) 5.52 ms
 #endif
 constexpr int STAGES = KR_STAGES;
 constexpr int CONSUMERS = 4;                              // (wq, wp) in {0,1}^2, 4x4 walker pairs each
@@ -36,7 +36,10 @@ constexpr int SO_DOUBLES = 2 * 4 * 4 * 4 * 2 * 2;         // [e][qq][pp][y][x_al
 constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
+#ifndef KR_MINB
+#define KR_MINB 2
+#endif
+__global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO + CONSUMERS * SO_DOUBLES);
@@ -282,7 +285,7 @@ void launch_pair_kr(const PairParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int ntiles = P.nb * (P.nb + 1) / 2;
-  const int slots = 2 * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
+  const int slots = KR_MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   pair_kr_kernel<<<ntiles < slots ? ntiles : slots, THREADS, SMEM_BYTES, s>>>(P);
 }
 
