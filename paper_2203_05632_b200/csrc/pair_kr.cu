@@ -11,8 +11,14 @@
 // the DMMA work of pair.cu, with identical results to rounding (f1d, f2d, f1x, f2x are real,
 // the imaginary residue is exactly 0 where the reference carries ~1e-16 noise).
 //
-// Structure as pair.cu (persistent CTAs over 8x8 walker tiles, TMA producer warp, full/empty
-// mbarrier ring, 3M complex products), with 4 MMA warps of 4x4 walker pairs and 2 CTAs per SM.
+// Structure: persistent CTAs over 8x8 walker tiles, a TMA producer warp filling a 2-stage ring
+// (full/empty mbarriers, running ahead across tiles), 8 DMMA warps, 3M complex products.
+//  * phase 1 (O, K = n_occ): warp w computes O~_e for e = w&1 over 4 Q x 4 P walkers and
+//    writes o = conj O~ into the CTA's shared o table (named barrier between the phases);
+//  * phase 2 (V, K = n_vir): warp (wq, wp) owns 4 Q x 2 P walkers (12 accumulator tiles, ~110
+//    registers), so two CTAs put 16 DMMA warps on each SM;
+//  * epilogue: the element-wise contraction is reduced with shuffles, and the per-pair scalar
+//    work (weights, products) runs on 8 lanes at once from a small smem table.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -24,25 +30,32 @@ namespace mcmp2dev {
 namespace {
 using namespace pairk;
 #ifndef KR_STAGES
-#define KR_STAGES 2  // measured on B200 cfg4: 2 stages 4.29 ms, 3 stages 4.35 ms, 4 stages (1 CTA/SM) 5.52 ms
+#define KR_STAGES 2
 #endif
 constexpr int STAGES = KR_STAGES;
-constexpr int CONSUMERS = 4;                              // (wq, wp) in {0,1}^2, 4x4 walker pairs each
+constexpr int CONSUMERS = 8;
 constexpr int THREADS = 32 * (CONSUMERS + 1);
 constexpr int HALF_PTS = 2 * WB;
 constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;
 constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;
-constexpr int SO_DOUBLES = 2 * 4 * 4 * 4 * 2 * 2;         // [e][qq][pp][y][x_alpha] complex
-constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES) * 8 + 2 * STAGES * 8;
+constexpr int SO_DOUBLES = 2 * WB * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
+constexpr int SF_DOUBLES = 8 * 4;                     // per warp: 8 pairs x (f1d, f2x, f1x, f2d)
+constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * STAGES * 8;
+
+__device__ __forceinline__ void consumer_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
+}
+
+__device__ __forceinline__ int o_index(int e, int q, int p, int y, int xa) {
+  return ((((e * WB + q) * WB + p) * 4 + y) * 2 + xa) * 2;
+}
 }  // namespace
 
-#ifndef KR_MINB
-#define KR_MINB 2
-#endif
-__global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P) {
+__global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO = sm + STAGES * STAGE_DOUBLES;
-  uint64_t* const full = reinterpret_cast<uint64_t*>(sO + CONSUMERS * SO_DOUBLES);
+  double* const sF = sO + SO_DOUBLES;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(sF + CONSUMERS * SF_DOUBLES);
   uint64_t* const empty = full + STAGES;
   __shared__ double s_red[CONSUMERS][2];
   __shared__ bool s_last;
@@ -81,10 +94,13 @@ __global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P)
       }
     }
   } else {
-    const int wq = warp >> 1, wp = warp & 1;
     const int hl = lane >> 4, l16 = lane & 15;
     const int xa_off = 8 * ((lane >> 2) & 1) + (lane & 3);  // alpha channel x = 0 or 2, k = lane & 3
-    double* const so = sO + warp * SO_DOUBLES;
+    // phase-1 role: electron e1, 4 Q walkers (4 q1w ..), 4 P walkers (4 p1w ..)
+    const int e1 = warp & 1, p1w = (warp >> 1) & 1, q1w = warp >> 2;
+    // phase-2 role: 4 Q walkers (4 wq ..) x 2 P walkers (2 wp ..)
+    const int wq = warp >> 2, wp = warp & 3;
+    double* const sf = sF + warp * SF_DOUBLES;
     const double wtau = P.st_ro->wtau;
     double acc_d = 0.0, acc_x = 0.0;
     long long seq = 0;
@@ -103,65 +119,60 @@ __global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P)
       int bq, bp;
       tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
 
-      // ---- phase 1: O~_e rows (q, y) all channels, cols (p, x_alpha) ----
+      // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
-        double t1[2][2][2], t2[2][2][2], t3[2][2][2];  // [e][hq][j]
+        double t1[2][2], t2[2][2], t3[2][2];  // [h][j]
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
+        for (int h = 0; h < 2; ++h) t1[h][0] = t1[h][1] = t2[h][0] = t2[h][1] = t3[h][0] = t3[h][1] = 0.0;
         for (int c = 0; c < cO; ++c) {
           const double* S = acquire();
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
-            auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))]; };
+            auto at = [&](int ptl, int plane, int off) {
+              return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
+            };
+            const int pb = HALF_PTS + 2 * (4 * p1w + (lane >> 3)) + e1;
+            const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int pb = HALF_PTS + 2 * (4 * wp + (lane >> 3)) + e;
-              const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int pa = 2 * (4 * wq + 2 * h + hl) + e;
-                const double ar = at(pa, 0, l16), ai = at(pa, 1, l16);
-                dmma(t1[e][h], ar, br);
-                dmma(t2[e][h], ai, bi);
-                dmma(t3[e][h], ar + ai, db);
-              }
+            for (int h = 0; h < 2; ++h) {
+              const int pa = 2 * (4 * q1w + 2 * h + hl) + e1;
+              const double ar = at(pa, 0, l16), ai = at(pa, 1, l16);
+              dmma(t1[h], ar, br);
+              dmma(t2[h], ai, bi);
+              dmma(t3[h], ar + ai, db);
             }
           }
           release();
         }
-        // o_e(x_alpha, y) = conj O~_e for pair (qq, pp)
+        consumer_barrier();  // every warp is done reading the previous tile's o table
         const int y = (lane >> 2) & 3, pp = lane & 3;
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int qq = 2 * h + hl;
-              const int idx = ((((e * 4 + qq) * 4 + pp) * 4 + y) * 2 + j) * 2;
-              so[idx] = t1[e][h][j] + t2[e][h][j];
-              so[idx + 1] = -(t3[e][h][j] - t1[e][h][j] + t2[e][h][j]);
-            }
+          for (int j = 0; j < 2; ++j) {
+            const int idx = o_index(e1, 4 * q1w + 2 * h + hl, 4 * p1w + pp, y, j);
+            sO[idx] = t1[h][j] + t2[h][j];                   // o = conj O~
+            sO[idx + 1] = -(t3[h][j] - t1[h][j] + t2[h][j]);
+          }
+        consumer_barrier();  // o table complete
       }
 
       // ---- phase 2: V rows (q, e_q, x_alpha), cols (p, e_p, y) ----
-      double u1[2][4][2], u2[2][4][2], u3[2][4][2];  // [hq][pp][j]
+      double u1[2][2][2], u2[2][2][2], u3[2][2][2];  // [hq][pp][j]
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 2; ++j)
           u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
       for (int c = cO; c < nchunks; ++c) {
         const double* S = acquire();
 #pragma unroll
         for (int gg = 0; gg < KC4; ++gg) {
           if (c * KC4 + gg >= P.Go + P.Gv) break;
-          auto at = [&](int ptl, int plane, int off) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))]; };
-          double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
+          auto at = [&](int ptl, int plane, int off) {
+            return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
+          };
+          double ar[2], ai[2], sa[2], br[2], bi[2], db[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int pa = 2 * (4 * wq + 2 * h + hl) + ((lane >> 3) & 1);
@@ -170,8 +181,8 @@ __global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P)
             sa[h] = ar[h] + ai[h];
           }
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) {
-            const int pb = HALF_PTS + 2 * (4 * wp + pp) + hl;
+          for (int pp = 0; pp < 2; ++pp) {
+            const int pb = HALF_PTS + 2 * (2 * wp + pp) + hl;
             br[pp] = at(pb, 0, l16);
             bi[pp] = at(pb, 1, l16);
             db[pp] = br[pp] - bi[pp];
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int pp = 0; pp < 4; ++pp) {
+            for (int pp = 0; pp < 2; ++pp) {
               dmma(u1[h][pp], ar[h], br[pp]);
               dmma(u2[h][pp], ai[h], bi[pp]);
               dmma(u3[h][pp], sa[h], db[pp]);
@@ -188,48 +199,47 @@ __global__ void __launch_bounds__(THREADS, KR_MINB) pair_kr_kernel(PairParams P)
         release();
       }
 
-#ifdef KR_SKIP_EPILOGUE  // timing experiment only: results are wrong
-      if (u1[0][0][0] != 12345.0) continue;
-#endif
-      // ---- epilogue: f = 2 Re sum_{x alpha, y} o v; real direct/exchange terms ----
-      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
+      // ---- epilogue: f = 2 Re sum_{x alpha, y} o v per (e_q, e_p), then real pair terms ----
+      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1, eq = (lane >> 3) & 1;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-          const int qq = 2 * h + hl;
+        for (int pp = 0; pp < 2; ++pp) {
+          const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
           double f = 0.0;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int y = 2 * (lane & 1) + j;
-            const int idx = ((((ep * 4 + qq) * 4 + pp) * 4 + y) * 2 + xa) * 2;
+            const int idx = o_index(ep, q, p, y, xa);
             const double vr = u1[h][pp][j] + u2[h][pp][j];
             const double vi = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
-            f += so[idx] * vr - so[idx + 1] * vi;
+            f += sO[idx] * vr - sO[idx + 1] * vi;
           }
           f += __shfl_xor_sync(0xffffffffu, f, 1);
           f += __shfl_xor_sync(0xffffffffu, f, 4);
-          // per half-warp hl: lane base + (e_q << 3) + (e_p << 1)
-          const int base = lane & 16;
-          const double f1d = 2.0 * __shfl_sync(0xffffffffu, f, base + 0);
-          const double f2x = 2.0 * __shfl_sync(0xffffffffu, f, base + 2);
-          const double f1x = 2.0 * __shfl_sync(0xffffffffu, f, base + 8);
-          const double f2d = 2.0 * __shfl_sync(0xffffffffu, f, base + 10);
-          if ((lane & 15) == 0) {
-            const int q = WB * bq + 4 * wq + qq, p = WB * bp + 4 * wp + pp;
-            if (q < P.m && p < P.m && q > p) {
-              const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
-              const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
-              const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
-              acc_d += (-P.w_direct * f1d) * f2d * inv;                  // estimator.cpp:32
-              acc_x += (-P.w_exchange * f1x) * f2x * inv;
-            }
-          }
+          // lanes hl*16 + (e_q << 3) + (e_p << 1) hold f(e_q, e_p) of pair (q, p)
+          if ((lane & 5) == 0) sf[((h * 2 + pp) * 2 + hl) * 4 + ((eq << 1) | ep)] = 2.0 * f;
         }
       __syncwarp();
+      if (lane < 8) {  // one pair per lane: lane = (h, pp, hl)
+        const int h = lane >> 2, pp = (lane >> 1) & 1, hh = lane & 1;
+        const int q = WB * bq + 4 * wq + 2 * h + hh, p = WB * bp + 2 * wp + pp;
+        if (q < P.m && p < P.m && q > p) {
+          const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
+          const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+          const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+          const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+          acc_d += (-P.w_direct * F[0]) * F[3] * inv;                // estimator.cpp:32
+          acc_x += (-P.w_exchange * F[2]) * F[1] * inv;
+        }
+      }
+      __syncwarp();
     }
-    acc_d += __shfl_sync(0xffffffffu, acc_d, 16);
-    acc_x += __shfl_sync(0xffffffffu, acc_x, 16);
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {  // fixed tree over lanes 0..7
+      acc_d += __shfl_down_sync(0xffffffffu, acc_d, o);
+      acc_x += __shfl_down_sync(0xffffffffu, acc_x, o);
+    }
     if (lane == 0) {
       s_red[warp][0] = acc_d;
       s_red[warp][1] = acc_x;
@@ -285,7 +295,7 @@ void launch_pair_kr(const PairParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int ntiles = P.nb * (P.nb + 1) / 2;
-  const int slots = KR_MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
+  const int slots = 2 * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   pair_kr_kernel<<<ntiles < slots ? ntiles : slots, THREADS, SMEM_BYTES, s>>>(P);
 }
 
