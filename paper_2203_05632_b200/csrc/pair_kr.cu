@@ -118,15 +118,6 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
     for (int it = 0; it < my_tiles; ++it) {
       int bq, bp;
       tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
-      // walker weights of this lane's epilogue pair (lanes 0..7), fetched now so the global
-      // loads overlap the GEMMs instead of the epilogue
-      double g1p = 1.0, g2p = 1.0, g1q = 1.0, g2q = 1.0;
-      const int eq_q = WB * bq + 4 * wq + 2 * (lane >> 2 & 1) + (lane & 1), eq_p = WB * bp + 2 * wp + ((lane >> 1) & 1);
-      const bool eq_valid = lane < 8 && eq_q < P.m && eq_p < P.m && eq_q > eq_p;
-      if (eq_valid) {
-        g1p = P.walkers.at(6, eq_p), g2p = P.walkers.at(7, eq_p);
-        g1q = P.walkers.at(6, eq_q), g2q = P.walkers.at(7, eq_q);
-      }
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
@@ -230,11 +221,17 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
           if ((lane & 5) == 0) sf[((h * 2 + pp) * 2 + hl) * 4 + ((eq << 1) | ep)] = 2.0 * f;
         }
       __syncwarp();
-      if (eq_valid) {  // one pair per lane: lane = (h, pp, hl) -> sf row `lane`
-        const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
-        const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
-        acc_d += (-P.w_direct * F[0]) * F[3] * inv;                // estimator.cpp:32
-        acc_x += (-P.w_exchange * F[2]) * F[1] * inv;
+      if (lane < 8) {  // one pair per lane: lane = (h, pp, hl)
+        const int h = lane >> 2, pp = (lane >> 1) & 1, hh = lane & 1;
+        const int q = WB * bq + 4 * wq + 2 * h + hh, p = WB * bp + 2 * wp + pp;
+        if (q < P.m && p < P.m && q > p) {
+          const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
+          const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
+          const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
+          const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+          acc_d += (-P.w_direct * F[0]) * F[3] * inv;                // estimator.cpp:32
+          acc_x += (-P.w_exchange * F[2]) * F[1] * inv;
+        }
       }
       __syncwarp();
     }
