@@ -439,7 +439,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   // ---- ensemble and work buffers ----
   h->mmax = max_walkers;
   h->nbmax = (max_walkers + WB - 1) / WB;
-  h->npts_pad = 2 * WB * h->nbmax;
+  h->npts_pad = 2 * WB * ((h->nbmax + 1) / 2 * 2);  // whole 16-walker Q rows for pair_kr tiles
   for (auto& b : h->buf) {
     b.mmax = h->nbmax * WB;
     b.w = dalloc<double>(size_t(9) * b.mmax, o);

@@ -32,13 +32,23 @@ using namespace pairk;
 #ifndef KR_STAGES
 #define KR_STAGES 2
 #endif
+#ifndef KR_QB
+// Q-side walker blocks (of WB) per tile: tile = 8 QB Q walkers x 8 P walkers. Measured cfg4:
+// QB 2 (16 DMMA warps, 1 CTA/SM, 25% less stage traffic per DMMA) 4.09 ms, QB 1 (2 CTAs/SM) 4.18 ms
+#define KR_QB 2
+#endif
 constexpr int STAGES = KR_STAGES;
-constexpr int CONSUMERS = 8;
+constexpr int QB = KR_QB;
+constexpr int QW = WB * QB;                           // Q walkers per tile
+constexpr int CONSUMERS = 8 * QB;
 constexpr int THREADS = 32 * (CONSUMERS + 1);
-constexpr int HALF_PTS = 2 * WB;
-constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;
+constexpr int MINB = QB == 1 ? 2 : 1;                 // CTAs per SM
+constexpr int HALF_PTS = 2 * WB;                      // P points per tile
+constexpr int QPTS = 2 * QW;                          // Q points per tile
+constexpr int STAGE_DOUBLES = (QPTS + HALF_PTS) * KC4 * 32;
 constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;
-constexpr int SO_DOUBLES = 2 * WB * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
+constexpr uint32_t Q_BYTES = QPTS * KC4 * 32 * 8;
+constexpr int SO_DOUBLES = 2 * QW * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
 constexpr int SF_DOUBLES = 8 * 4;                     // per warp: 8 pairs x (f1d, f2x, f1x, f2d)
 constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * STAGES * 8;
 
@@ -47,11 +57,26 @@ __device__ __forceinline__ void consumer_barrier() {
 }
 
 __device__ __forceinline__ int o_index(int e, int q, int p, int y, int xa) {
-  return ((((e * WB + q) * WB + p) * 4 + y) * 2 + xa) * 2;
+  return ((((e * QW + q) * WB + p) * 4 + y) * 2 + xa) * 2;
+}
+
+// tiles: Q row a covers walker blocks [QB a, QB a + QB), P block b in [0, QB a + QB);
+// t = QB a (a + 1) / 2 + b
+__device__ __forceinline__ void kr_tile(int t, int& a, int& b) {
+  int r = int((sqrt(8.0 * double(t) / QB + 1.0) - 1.0) * 0.5);
+  while (QB * (r + 1) * (r + 2) / 2 <= t) ++r;
+  while (QB * r * (r + 1) / 2 > t) --r;
+  a = r;
+  b = t - QB * r * (r + 1) / 2;
+}
+
+__host__ __device__ constexpr int kr_ntiles(int nb) {
+  const int nbq = (nb + QB - 1) / QB;
+  return QB * nbq * (nbq + 1) / 2;
 }
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
+__global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO = sm + STAGES * STAGE_DOUBLES;
   double* const sF = sO + SO_DOUBLES;
@@ -61,7 +86,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
   __shared__ bool s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ntiles = P.nb * (P.nb + 1) / 2;
+  const int ntiles = kr_ntiles(P.nb);
   const int nchunks = P.Gtot / KC4;
   const int cO = P.Go / KC4;
   const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
@@ -79,17 +104,17 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
     if (lane == 0) {  // TMA producer
       long long seq = 0;
       for (int it = 0; it < my_tiles; ++it) {
-        int bq, bp;
-        tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+        int ta, bp;
+        kr_tile(int(blockIdx.x) + it * int(gridDim.x), ta, bp);
         for (int c = 0; c < nchunks; ++c, ++seq) {
           const int stage = int(seq % STAGES);
           mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
           double* dst = sm + stage * STAGE_DOUBLES;
-          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
+          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(QPTS) * ta) * KC4 * 32;
           const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
-          mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
-          bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
-          bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+          mbar_expect_tx(&full[stage], Q_BYTES + HALF_BYTES);
+          bulk_g2s(dst, srcq, Q_BYTES, &full[stage]);
+          bulk_g2s(dst + QPTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
         }
       }
     }
@@ -116,8 +141,9 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
     };
 
     for (int it = 0; it < my_tiles; ++it) {
-      int bq, bp;
-      tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+      int ta, bp;
+      kr_tile(int(blockIdx.x) + it * int(gridDim.x), ta, bp);
+      const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
@@ -131,7 +157,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
             auto at = [&](int ptl, int plane, int off) {
               return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
             };
-            const int pb = HALF_PTS + 2 * (4 * p1w + (lane >> 3)) + e1;
+            const int pb = QPTS + 2 * (4 * p1w + (lane >> 3)) + e1;
             const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -182,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
           }
 #pragma unroll
           for (int pp = 0; pp < 2; ++pp) {
-            const int pb = HALF_PTS + 2 * (2 * wp + pp) + hl;
+            const int pb = QPTS + 2 * (2 * wp + pp) + hl;
             br[pp] = at(pb, 0, l16);
             bi[pp] = at(pb, 1, l16);
             db[pp] = br[pp] - bi[pp];
@@ -223,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 2) pair_kr_kernel(PairParams P) {
       __syncwarp();
       if (lane < 8) {  // one pair per lane: lane = (h, pp, hl)
         const int h = lane >> 2, pp = (lane >> 1) & 1, hh = lane & 1;
-        const int q = WB * bq + 4 * wq + 2 * h + hh, p = WB * bp + 2 * wp + pp;
+        const int q = q0 + 4 * wq + 2 * h + hh, p = p0 + 2 * wp + pp;
         if (q < P.m && p < P.m && q > p) {
           const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
           const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
@@ -294,8 +320,8 @@ cudaError_t pair_kr_kernel_setup() {
 void launch_pair_kr(const PairParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const int ntiles = P.nb * (P.nb + 1) / 2;
-  const int slots = 2 * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
+  const int ntiles = kr_ntiles(P.nb);
+  const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   pair_kr_kernel<<<ntiles < slots ? ntiles : slots, THREADS, SMEM_BYTES, s>>>(P);
 }
 
