@@ -11,12 +11,13 @@
 // the DMMA work of pair.cu, with identical results to rounding (f1d, f2d, f1x, f2x are real,
 // the imaginary residue is exactly 0 where the reference carries ~1e-16 noise).
 //
-// Structure: persistent CTAs over 8x8 walker tiles, a TMA producer warp filling a 2-stage ring
-// (full/empty mbarriers, running ahead across tiles), 8 DMMA warps, 3M complex products.
+// Structure: persistent CTAs over (8 QB) x 8 walker tiles (QB = 2: 16 Q x 8 P), a TMA producer
+// warp filling a 2-stage ring (full/empty mbarriers, running ahead across tiles), 8 QB DMMA
+// warps, 3M complex products.
 //  * phase 1 (O, K = n_occ): warp w computes O~_e for e = w&1 over 4 Q x 4 P walkers and
 //    writes o = conj O~ into the CTA's shared o table (named barrier between the phases);
-//  * phase 2 (V, K = n_vir): warp (wq, wp) owns 4 Q x 2 P walkers (12 accumulator tiles, ~110
-//    registers), so two CTAs put 16 DMMA warps on each SM;
+//  * phase 2 (V, K = n_vir): warp (wq, wp) owns 4 Q x 2 P walkers (12 accumulator tiles, 96
+//    registers), 16 DMMA warps per SM;
 //  * epilogue: the element-wise contraction is reduced with shuffles, and the per-pair scalar
 //    work (weights, products) runs on 8 lanes at once from a small smem table.
 #include <cuda_runtime.h>
