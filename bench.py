@@ -144,8 +144,8 @@ def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, qui
     # bounded sample: per worker one step restricted to walker rows [0, r) of the pair loop (Metropolis
     # and spinor values always cover all 2m points); two row counts give the fixed O(m) cost and the
     # per-sample cost, extrapolated to the full C(m,2) step and stated as such.
-    ra, rb = {"cfg3": (8, 40), "cfg4": (4, 20)}[cfg] if not quick else (1, 2)
-    reps = max(1, steps // 5)
+    ra, rb = {"cfg3": (8, 48), "cfg4": (4, 36)}[cfg] if not quick else (1, 2)
+    reps = max(2, steps // 8)
     ta, na = orc.cpu_baseline(seed=1, m=m, rows=ra, burn=5, step_size=step_size, steps=reps, threads=threads)
     tb, nb = orc.cpu_baseline(seed=1, m=m, rows=rb, burn=5, step_size=step_size, steps=reps, threads=threads)
     # ta = reps*T0 + c*na/threads (workers run concurrently), same for tb
@@ -201,23 +201,35 @@ def main():
     import numpy as np
     import torch
 
-    torch.cuda.set_device(local)
+    dev = local % torch.cuda.device_count()  # == local on a real node; lets a 1-GPU box host a 2-rank check
+    torch.cuda.set_device(dev)
     dist = None
+    backend = os.environ.get("MCMP2_DIST_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+
+    def reduce_max(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     from paper_2203_05632_b200 import DeviceWalker, System
 
     sysd = System(spinor, conf_text)
-    dw = DeviceWalker(sysd, device=local, max_walkers=m)
+    dw = DeviceWalker(sysd, device=dev, max_walkers=m)
     dw.init_ensemble(m, seed=1, stream=rank)
     if cfg == "cfg1":
         dw.set_sigma_step(0.3)
         dw.burn_in(args.burnin, adapt=False)
     else:
         dw.burn_in(args.burnin, adapt=True)
-    stream = torch.cuda.ExternalStream(dw.stream_ptr, device=torch.device("cuda", local))
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(dw.stream_ptr, device=torch.device("cuda", dev))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
 
     # warm-up
     dw.advance(args.warmup, keep_on_device=True)
@@ -226,7 +238,7 @@ def main():
     # ---- timed region: K steps, device time per step on the handle's stream, L2 flushed between ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     try:
-        clk = NvmlClocks(local)
+        clk = NvmlClocks(dev)
     except Exception:  # NVML unavailable: fall back to nvidia-smi sampling
         clk = None
     smi, smi_f = clocks_sampler(tmp / "clocks.csv") if (rank == 0 and clk is None) else (None, None)
@@ -253,10 +265,7 @@ def main():
         smi_f.close()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     t_ms = sum(ms_steps)
-    t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
+    t_max = reduce_max(t_ms)
     value = world * samples_per_step * args.steps / (t_max / 1e3)
 
     # ---- per-kernel device time (profiling pass, events around each launch) ----
@@ -287,10 +296,7 @@ def main():
     vals, ims = dw.advance(args.steps)               # every step's (value, imag) D2H
     st2 = dw.get_ensemble()                          # D2H walker state (checkpoint)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-    if dist:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * samples_per_step * args.steps / float(te.item())
+    e2e_value = world * samples_per_step * args.steps / reduce_max(e2e_s)
     state_bytes = m * 9 * 8 + 64
     h2d = state_bytes / args.steps
     d2h = 16 + state_bytes / args.steps
@@ -328,7 +334,7 @@ def main():
         "gpu_launches": 3 * args.steps,
         "step_values_checksum": float(np.sum(vals)),
     }
-    cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", local)
+    cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", dev)
     if cl:
         line["clocks"] = cl
     if world == 1 and not args.no_cpu_baseline:
