@@ -27,6 +27,10 @@ using pairk::dmma;
 constexpr int CHI_PTS = 8;
 constexpr int CHI_THREADS = 256;
 constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
+#ifndef MO_UNROLL
+#define MO_UNROLL 2
+#endif
+constexpr int kMoUnroll = MO_UNROLL;  // k4 steps in flight in the MO-transform loop
 
 __device__ __forceinline__ double ipow(double x, int n) {
   // std::pow(x, n) for n in 0..3 (gaussian.cpp:87-92)
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
-#pragma unroll 2
+#pragma unroll kMoUnroll
   for (int k4 = 0; k4 < k4n; ++k4) {
     double a[4], b[4];
 #pragma unroll
