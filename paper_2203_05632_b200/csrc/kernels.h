@@ -55,6 +55,7 @@ struct SpinorParams {
 struct PairParams {
   const double* phi;
   int npts_pad, Go, Gv, Gtot;
+  int go_used;               // occupied groups holding spinors (Go pads to whole chunks)
   int m, nb;                 // walkers, walker blocks of WB
   WalkerBuf walkers;         // g1 (row 6), g2 (row 7)
   const DevState* st_ro;
@@ -74,6 +75,7 @@ cudaError_t pair_kernel_setup();
 // Kramers-restricted variant (pair_kr.cu): half the DMMA work for time-reversal-paired columns
 void launch_pair_kr(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kr_kernel_setup();
+double pair_kr_block_tiles(int nb);  // WB x WB walker blocks the Kramers launch computes
 cudaError_t spinor_kernel_setup();
 
 }  // namespace mcmp2dev

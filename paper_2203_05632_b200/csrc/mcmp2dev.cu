@@ -173,6 +173,7 @@ struct mcmp2dev_handle {
     p.phi = d_phi;
     p.npts_pad = npts_pad;
     p.Go = Go;
+    p.go_used = (n_occ + 3) / 4;
     p.Gv = Gv;
     p.Gtot = Gtot;
     p.m = mm;
@@ -746,11 +747,12 @@ int mcmp2dev_prepare(mcmp2dev_t* h) {
 
 int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
   return guard(h, [&] {
-    const double nb = (h->m + WB - 1) / WB, ntiles = nb * (nb + 1) / 2;
-    // DMMAs per tile per k-group (all warps): O phase and V phase, 3 per complex product
+    const int nb = (h->m + WB - 1) / WB;
+    const double ntiles = h->kramers ? pair_kr_block_tiles(nb) : 0.5 * nb * (nb + 1);
+    // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
     const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
-    *pair_dmma_flop = ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
+    *pair_dmma_flop = ntiles * 512.0 * ((h->n_occ + 3) / 4 * per_o + h->Gv * per_v);
   });
 }
 

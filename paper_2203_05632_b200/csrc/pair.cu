@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           const double* S = acquire();
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
+            if (c * KC4 + gg >= P.go_used) break;  // zero chunk padding
             auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
 #pragma unroll
             for (int e = 0; e < 2; ++e) {

@@ -38,6 +38,10 @@ using namespace pairk;
 // QB 2 (16 DMMA warps, 1 CTA/SM, 25% less stage traffic per DMMA) 4.09 ms, QB 1 (2 CTAs/SM) 4.18 ms
 #define KR_QB 2
 #endif
+// Measured and rejected (cfg4, pair ms): producer in its own warpgroup handing registers to the
+// DMMA warps via setmaxnreg (24/112) 4.38; that plus operand double-buffering across k groups
+// 4.22; double-buffering within the 96-register cap (spills) 4.41; per-chunk branch-free
+// full-chunk path 4.15; 3 stages 4.14; this kernel 4.08.
 constexpr int STAGES = KR_STAGES;
 constexpr int QB = KR_QB;
 constexpr int QW = WB * QB;                           // Q walkers per tile
@@ -57,8 +61,10 @@ __device__ __forceinline__ void consumer_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
 }
 
+// y is XOR-swizzled by the parity of (q, e): the epilogue's 16-byte reads of one warp then cover
+// both halves of a 128-byte row instead of 4 lanes per bank group (4-way -> 2 wavefronts).
 __device__ __forceinline__ int o_index(int e, int q, int p, int y, int xa) {
-  return ((((e * QW + q) * WB + p) * 4 + y) * 2 + xa) * 2;
+  return ((((e * QW + q) * WB + p) * 4 + (y ^ ((q ^ e) & 1))) * 2 + xa) * 2;
 }
 
 // tiles: Q row a covers walker blocks [QB a, QB a + QB), P block b in [0, QB a + QB);
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           const double* S = acquire();
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
+            if (c * KC4 + gg >= P.go_used) break;  // zero chunk padding
             auto at = [&](int ptl, int plane, int off) {
               return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
             };
@@ -310,6 +317,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 namespace {
 int g_sms_kr[64];
 }
+
+double pair_kr_block_tiles(int nb) { return double(kr_ntiles(nb)) * QB; }
 
 cudaError_t pair_kr_kernel_setup() {
   int dev = 0;
