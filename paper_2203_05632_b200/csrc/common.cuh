@@ -19,7 +19,9 @@
 namespace mcmp2dev {
 
 #ifndef KC4_GROUPS
-#define KC4_GROUPS 4
+// cfg4 Kramers pair kernel (ms): KC4 4 -> 4.08, 5 -> 4.03, 6 -> 4.04, 7 -> 4.02 (2 stages of
+// 86 KB); 8 does not fit two stages next to the o table. General kernel neutral, physical -2%.
+#define KC4_GROUPS 7
 #endif
 constexpr int KC4 = KC4_GROUPS;  // k-groups per pair-kernel stage
 constexpr int WB = 8;           // walkers per pair-kernel tile side

@@ -43,9 +43,11 @@ constexpr int SV_DOUBLES = 8 * 64 * 2;                    // physical epilogue: 
 
 template <bool PHYS>
 struct Cfg {
-  static constexpr int STAGES = PHYS ? 3 : 4;
-  static constexpr int SMEM_BYTES =
-      (STAGES * STAGE_DOUBLES + CONSUMERS * SO_DOUBLES + (PHYS ? CONSUMERS * SV_DOUBLES : 0)) * 8 + 2 * STAGES * 8;
+  static constexpr int FIXED_BYTES = (CONSUMERS * SO_DOUBLES + (PHYS ? CONSUMERS * SV_DOUBLES : 0)) * 8;
+  static constexpr int FIT = (227 * 1024 - FIXED_BYTES) / (STAGE_DOUBLES * 8 + 16);  // stages that fit
+  static constexpr int STAGES = (PHYS ? 3 : 4) < FIT ? (PHYS ? 3 : 4) : FIT;
+  static_assert(STAGES >= 2, "KC4 too large for a two-stage ring");
+  static constexpr int SMEM_BYTES = FIXED_BYTES + STAGES * (STAGE_DOUBLES * 8 + 16);
 };
 
 }  // namespace
