@@ -27,10 +27,12 @@ using pairk::dmma;
 constexpr int CHI_PTS = 8;
 constexpr int CHI_THREADS = 256;
 constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
-#ifndef MO_UNROLL
-#define MO_UNROLL 2
+#ifndef MO_KS
+#define MO_KS 4
 #endif
-constexpr int kMoUnroll = MO_UNROLL;  // k4 steps in flight in the MO-transform loop
+#ifndef MO_STAGES
+#define MO_STAGES 3
+#endif
 
 __device__ __forceinline__ double ipow(double x, int n) {
   // std::pow(x, n) for n in 0..3 (gaussian.cpp:87-92)
@@ -118,32 +120,78 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   }
 }
 
-__global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
-  const int g = blockIdx.z;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  // 16-byte cp.async, zero-filled when !ok (src-size 0)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(pairk::smem_u32(dst)), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+
+// Tile: 64 points (8 point fragments) x 8 n fragments of one basis group; 2x2 warps of 4 x 4
+// fragments. A (chi) and B (coefficients) k-slices of MO_KS k4 steps stream through a
+// MO_STAGES-deep cp.async ring in shared memory, so the DMMAs wait on shared memory, not on
+// L2 latency.
+using StageA = double[8][MO_KS][32];  // [ptf][k4][lane]
+using StageB = double[MO_KS][8][32];  // [k4][nf][lane]
+__device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_base, int nf_base, StageA* sA,
+                                        StageB* sB) {
   const int k4n = P.grp_k4[g], nf_total = P.grp_nf[g];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ptf0 = blockIdx.x * 8 + (warp >> 1) * 4;       // 4 point fragments per warp
-  const int nf0 = blockIdx.y * 8 + (warp & 1) * 4;         // 4 n fragments per warp
-  if (nf0 >= nf_total) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ptf0 = ptf_base + (warp >> 1) * 4;  // 4 point fragments per warp
+  const int nf0 = nf_base + (warp & 1) * 4;     // 4 n fragments per warp (nf_total is a multiple of 4)
+  const bool active = nf0 < nf_total;
   const double* A = P.chi + P.grp_chi_off[g];
   const double* B = P.bfrag + P.grp_b_off[g];
+  const int nkb = (k4n + MO_KS - 1) / MO_KS;
+  auto load_stage = [&](int kb, int st) {
+#pragma unroll
+    for (int i = tid; i < 8 * MO_KS * 16; i += MO_THREADS) {  // A: 16-byte pieces
+      const int ptf = i / (MO_KS * 16), k = (i / 16) % MO_KS, c = i % 16;
+      const int k4 = kb * MO_KS + k;
+      const bool ok = k4 < k4n;
+      cp_async16(&sA[st][ptf][k][2 * c], A + (size_t(ptf_base + ptf) * k4n + (ok ? k4 : 0)) * 32 + 2 * c, ok);
+    }
+#pragma unroll
+    for (int i = tid; i < MO_KS * 8 * 16; i += MO_THREADS) {  // B
+      const int k = i / 128, f = (i / 16) % 8, c = i % 16;
+      const int k4 = kb * MO_KS + k, nf = nf_base + f;
+      const bool ok = k4 < k4n && nf < nf_total;
+      cp_async16(&sB[st][k][f][2 * c], B + (size_t(ok ? k4 : 0) * nf_total + (ok ? nf : 0)) * 32 + 2 * c, ok);
+    }
+  };
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
-#pragma unroll kMoUnroll
-  for (int k4 = 0; k4 < k4n; ++k4) {
-    double a[4], b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = __ldg(A + (size_t(ptf0 + i) * k4n + k4) * 32 + lane);
-#pragma unroll
-    for (int f = 0; f < 4; ++f) b[f] = __ldg(B + (size_t(k4) * nf_total + nf0 + f) * 32 + lane);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int f = 0; f < 4; ++f) dmma(acc[i][f], a[i], b[f]);
+  for (int st = 0; st < MO_STAGES - 1; ++st) {
+    if (st < nkb) load_stage(st, st);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  for (int kb = 0; kb < nkb; ++kb) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(MO_STAGES - 2) : "memory");
+    __syncthreads();  // stage kb landed for every thread; stage kb-1 is free
+    const int nk = kb + MO_STAGES - 1;
+    if (nk < nkb) load_stage(nk, nk % MO_STAGES);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (active) {
+      const int st = kb % MO_STAGES;
+#pragma unroll
+      for (int k = 0; k < MO_KS; ++k) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sA[st][(warp >> 1) * 4 + i][k][lane];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) b[f] = sB[st][k][(warp & 1) * 4 + f][lane];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int f = 0; f < 4; ++f) dmma(acc[i][f], a[i], b[f]);
+      }
+    }
+  }
+  if (!active) return;
   // epilogue: scale and scatter into Phi[chunk][pt][g%KC4][re|im][x*4 + k%4]
   auto put = [&](int x, int pt, int col, double re, double im) {
     const double w = P.sw[col];
@@ -181,6 +229,16 @@ __global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
       }
     }
   }
+}
+
+// One tile per CTA (measured faster than persistent CTAs walking the tiles largest-K first:
+// cfg4 spinor stage 0.172 vs 0.186 ms).
+__global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
+  __shared__ __align__(128) StageA sA[MO_STAGES];
+  __shared__ __align__(128) StageB sB[MO_STAGES];
+  const int g = blockIdx.z, nf_base = blockIdx.y * 8;
+  if (nf_base >= P.grp_nf[g]) return;  // uniform over the CTA
+  mo_tile(P, g, blockIdx.x * 8, nf_base, sA, sB);
 }
 
 int spinor_smem_bytes(const SpinorParams& P) { return int(sizeof(double)) * (3 * CHI_PTS + P.nuniq * CHI_PTS); }
