@@ -50,6 +50,7 @@ struct SpinorParams {
   int Go, Gtot;              // occupied k-groups, total k-groups (multiple of KC4)
   const double* sw;
   double* phi;
+  double* hinv;              // [m] 1 / (g1 g2) per walker, for the pair epilogue
 };
 
 struct PairParams {
@@ -58,6 +59,7 @@ struct PairParams {
   int go_used;               // occupied groups holding spinors (Go pads to whole chunks)
   int m, nb;                 // walkers, walker blocks of WB
   WalkerBuf walkers;         // g1 (row 6), g2 (row 7)
+  const double* hinv;        // [m] 1 / (g1 g2), written by chi_kernel this step
   const DevState* st_ro;
   DevState* st;
   double ng2, w_direct, w_exchange;

@@ -96,6 +96,7 @@ struct mcmp2dev_handle {
   DevState* d_state = nullptr;
   int* d_block_acc = nullptr;
   double* d_phi = nullptr;
+  double* d_hinv = nullptr;
   double* d_partials = nullptr;
   double* d_steps = nullptr;
   double* d_replay = nullptr;
@@ -179,6 +180,7 @@ struct mcmp2dev_handle {
     p.m = mm;
     p.nb = (mm + WB - 1) / WB;
     p.walkers = wb;
+    p.hinv = d_hinv;
     p.st_ro = d_state;
     p.st = d_state;
     p.ng2 = ng * ng;
@@ -460,6 +462,9 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(cudaMemset(h->d_phi, 0, phi_doubles * sizeof(double)), "memset phi");
   sp.phi = h->d_phi;
   sp.npts_pad = h->npts_pad;
+  h->d_hinv = dalloc<double>(size_t(h->npts_pad) / 2, o);
+  ck(cudaMemset(h->d_hinv, 0, sizeof(double) * h->npts_pad / 2), "memset hinv");
+  sp.hinv = h->d_hinv;
   // MO-transform operands: basis groups, B fragments of C, A-fragment buffer for chi
   const int ptf_max = (h->npts_pad + 63) / 64 * 8;  // point fragments, padded to the 64-point tile
   h->sp_kr = sp;

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
     const int wq = warp >> 1, wp = warp & 1;
     const int hl = lane >> 4, l16 = lane & 15;
     double* const so = sO + warp * SO_DOUBLES;
-    const double wtau = P.st_ro->wtau;
+    const double cw = P.ng2 / P.st_ro->wtau;
     double acc_dr = 0.0, acc_di = 0.0, acc_xr = 0.0, acc_xi = 0.0;
     long long seq = 0;
     auto acquire = [&]() -> const double* {
@@ -265,9 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
                 txr += m1[x][y][0] * m2[y][x][0] - m1[x][y][1] * m2[y][x][1];
                 txi += m1[x][y][0] * m2[y][x][1] + m1[x][y][1] * m2[y][x][0];
               }
-            const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
-            const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
-            const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);
+            const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
             const double adr = -P.w_direct * t1r, adi = -P.w_direct * t1i;
             acc_dr += (adr * t2r - adi * t2i) * inv;
             acc_di += (adr * t2i + adi * t2r) * inv;
@@ -310,9 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           if (lane == 0) {
             const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
             if (q < P.m && p < P.m && q > p) {
-              const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
-              const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
-              const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+              const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
               // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32)
               const double adr = -P.w_direct * f1dr, adi = -P.w_direct * f1di;
               const double axr = -P.w_exchange * f1xr, axi = -P.w_exchange * f1xi;

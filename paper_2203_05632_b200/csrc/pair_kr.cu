@@ -41,7 +41,8 @@ using namespace pairk;
 // Measured and rejected (cfg4, pair ms): producer in its own warpgroup handing registers to the
 // DMMA warps via setmaxnreg (24/112) 4.38; that plus operand double-buffering across k groups
 // 4.22; double-buffering within the 96-register cap (spills) 4.41; per-chunk branch-free
-// full-chunk path 4.15; 3 stages 4.14; this kernel 4.08.
+// full-chunk path 4.15; 3 stages 4.14; epilogue hinv prefetched at tile start (spills) 4.07;
+// this kernel 4.00.
 constexpr int STAGES = KR_STAGES;
 constexpr int QB = KR_QB;
 constexpr int QW = WB * QB;                           // Q walkers per tile
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
     // phase-2 role: 4 Q walkers (4 wq ..) x 2 P walkers (2 wp ..)
     const int wq = warp >> 2, wp = warp & 3;
     double* const sf = sF + warp * SF_DOUBLES;
-    const double wtau = P.st_ro->wtau;
+    const double cw = P.ng2 / P.st_ro->wtau;
     double acc_d = 0.0, acc_x = 0.0;
     long long seq = 0;
     auto acquire = [&]() -> const double* {
@@ -260,9 +261,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
         const int q = q0 + 4 * wq + 2 * h + hh, p = p0 + 2 * wp + pp;
         if (q < P.m && p < P.m && q > p) {
           const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
-          const double g1p = P.walkers.at(6, p), g2p = P.walkers.at(7, p);
-          const double g1q = P.walkers.at(6, q), g2q = P.walkers.at(7, q);
-          const double inv = P.ng2 / (g1p * g2p * g1q * g2q * wtau);  // estimator.cpp:55
+          const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
           acc_d += (-P.w_direct * F[0]) * F[3] * inv;                // estimator.cpp:32
           acc_x += (-P.w_exchange * F[2]) * F[1] * inv;
         }

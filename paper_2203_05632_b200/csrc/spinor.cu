@@ -86,6 +86,12 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   if (tid < 3 * CHI_PTS) {
     const int pt = tid / 3, k = tid % 3, gp = pt0 + pt;
     s_pos[tid] = gp < P.npts ? P.walkers.at((gp & 1) * 3 + k, gp >> 1) : 0.0;  // 2p <- r1, 2p+1 <- r2
+  } else if (tid < 3 * CHI_PTS + CHI_PTS / 2) {
+    // pair-epilogue weight of walker w: inv_w = N_g^2 / (g1p g2p g1q g2q w(tau)) (estimator.cpp:55)
+    // is evaluated as (N_g^2 / w(tau)) hinv_p hinv_q, hinv = 1 / (g1 g2) (a few ulp from the
+    // reference's association)
+    const int w = (pt0 >> 1) + tid - 3 * CHI_PTS;
+    if (2 * w < P.npts) P.hinv[w] = 1.0 / (P.walkers.at(6, w) * P.walkers.at(7, w));
   }
   __syncthreads();
   for (int i = tid; i < P.nuniq * CHI_PTS; i += CHI_THREADS) {
