@@ -41,7 +41,8 @@ using namespace pairk;
 // Measured and rejected (cfg4, pair ms): producer in its own warpgroup handing registers to the
 // DMMA warps via setmaxnreg (24/112) 4.38; that plus operand double-buffering across k groups
 // 4.22; double-buffering within the 96-register cap (spills) 4.41; per-chunk branch-free
-// full-chunk path 4.15; 3 stages 4.14; epilogue hinv prefetched at tile start (spills) 4.07;
+// full-chunk path 4.15; 3 stages 4.14; epilogue hinv prefetched at tile start (spills) 4.07; no
+// producer warp, the last DMMA warp to release a stage refills it (16 warps, 109 registers) 4.58;
 // this kernel 4.00.
 constexpr int STAGES = KR_STAGES;
 constexpr int QB = KR_QB;
