@@ -60,7 +60,7 @@ struct DevState {
   int redo;                   // a coincident proposal needs the sequential path
   unsigned int done_ctas;     // last-CTA counters (walker kernel)
   unsigned int done_pair;     // (pair kernel)
-  int pad;
+  int spec_error_idx;         // overflow index from the speculative tau draw (INT_MAX: none)
 };
 
 }  // namespace mcmp2dev

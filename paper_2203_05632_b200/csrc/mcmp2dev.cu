@@ -227,6 +227,7 @@ struct mcmp2dev_handle {
     ck(scopy(stream, &st, d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
     st.error = 0;
     st.error_idx = INT_MAX;
+    st.spec_error_idx = INT_MAX;
     ck(scopy(stream, d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   }
 };
@@ -455,8 +456,9 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   DevState st{};
   st.sigma = 1.0;  // sampler.hpp:45
   st.error_idx = INT_MAX;
+  st.spec_error_idx = INT_MAX;
   ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
-  h->d_block_acc = dalloc<int>((max_walkers + 127) / 128 + 1, o);
+  h->d_block_acc = dalloc<int>((max_walkers + 63) / 64 + 2, o);  // 64 walkers per walk CTA + tau CTA
   const size_t phi_doubles = size_t(h->Gtot) * h->npts_pad * 32;
   h->d_phi = dalloc<double>(phi_doubles, o);
   ck(cudaMemset(h->d_phi, 0, phi_doubles * sizeof(double)), "memset phi");
@@ -538,6 +540,7 @@ int mcmp2dev_init_ensemble(mcmp2dev_t* h, int m, uint64_t seed, uint32_t stream)
     st.pos = 0;
     st.sigma = 1.0;  // sampler.hpp:45
     st.error_idx = INT_MAX;
+    st.spec_error_idx = INT_MAX;
     ck(cudaMemcpyAsync(h->d_state, &st, sizeof st, cudaMemcpyHostToDevice, h->stream), "state H2D");
     launch_walk(h->walk_params(WALK_INIT, 0, 0), h->stream);
     h->cur ^= 1;
@@ -604,6 +607,7 @@ int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e) {
     st.proposed = e->proposed;
     st.accepted = e->accepted;
     st.error_idx = INT_MAX;
+    st.spec_error_idx = INT_MAX;
     ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
     h->have_ensemble = true;
   });

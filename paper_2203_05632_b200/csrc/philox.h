@@ -58,7 +58,8 @@ struct StreamReader {
       buf = philox_block(uint32_t(b), uint32_t(b >> 32), 0u, stream, k0, k1);
       cached_block = b;
     }
-    const uint32_t v = buf.v[pos & 3];
+    const unsigned i = unsigned(pos & 3);  // select, not an indexed load (keeps buf in registers)
+    const uint32_t v = i == 0 ? buf.v[0] : i == 1 ? buf.v[1] : i == 2 ? buf.v[2] : buf.v[3];
     ++pos;
     return v;
   }

@@ -14,6 +14,8 @@
 // CTA replays the whole sweep sequentially, so the stream stays exact.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -134,14 +136,18 @@ __device__ __forceinline__ void finish_init(const WalkParams& P, Walker& x) {
 
 // sqrt of guarded_exp (greens.cpp:9-16) for every spinor at the step's tau; overflow is
 // flagged with the first offending spinor index, as the reference throws at set_tau.
-__device__ void tau_weights(const WalkParams& P, double tau) {
+__device__ void tau_weights(const WalkParams& P, double tau, bool speculative = false) {
   const int np = P.n_occ + P.n_vir;
   for (int k = threadIdx.x; k < np; k += blockDim.x) {
     const double e = k < P.n_occ ? P.energies[k] * tau : -P.energies[k] * tau;
     double sw;
     if (e > 700.0) {
-      atomicMin(&P.st->error_idx, k);
-      P.st->error = 1;
+      if (speculative) {  // confirmed by the last CTA unless the sweep redrew a proposal
+        atomicMin(&P.st->spec_error_idx, k);
+      } else {
+        atomicMin(&P.st->error_idx, k);
+        P.st->error = 1;
+      }
       sw = 0.0;
     } else if (e < -700.0) {
       sw = 0.0;
@@ -152,31 +158,88 @@ __device__ void tau_weights(const WalkParams& P, double tau) {
   }
 }
 
-__global__ void walk_kernel(WalkParams P) {
-  __shared__ int s_acc[32];
+// Two threads per walker (lane pair = electrons 1 and 2): each draws its electron's proposal
+// from its own offset of the walker's 18 u32 (gaussian3 of electron 1 at +0, electron 2 at +8,
+// the acceptance uniform at +16) and evaluates g at it; electron 1's thread then decides.
+constexpr int WALK_THREADS = 128;
+
+// tau = TauSampler::sample(rng.uniform()) after the sweep (driver.cpp:445), u32 at `pos`
+__device__ double draw_tau(const WalkParams& P, unsigned long long pos) {
+  StreamReader rd(P.k0, P.k1, P.stream, pos);
+  const double u = rd.uniform();
+  const double tau = -log1p(-u) / P.lambda;
+  P.st->tau = tau;
+  P.st->wtau = P.lambda * exp(-P.lambda * tau);
+  return tau;
+}
+
+__global__ void __launch_bounds__(WALK_THREADS) walk_kernel(WalkParams P) {
+  __shared__ int s_acc[WALK_THREADS / 32];
   __shared__ bool s_last;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = gt >> 1, e = gt & 1;
+  // PRODUCTION launches one extra CTA that draws tau and the spinor weights speculatively at
+  // the stream position the sweep ends at when no proposal is redrawn (pos + 18 m); the last
+  // CTA redraws them in the rare redo case.
+  const bool tau_cta = P.mode == WALK_PRODUCTION && blockIdx.x == gridDim.x - 1;
+  const bool valid = p < P.m && !tau_cta;
   const unsigned long long pos0 = P.st->pos;
   int acc = 0;
-  if (p < P.m) {
+  double n[3] = {0.0, 0.0, 0.0}, gn = 1.0;
+  if (tau_cta) {
+    __shared__ double s_tau;
+    if (threadIdx.x == 0) s_tau = draw_tau(P, pos0 + 18ull * unsigned(P.m));
+    __syncthreads();
+    tau_weights(P, s_tau, true);
+  } else if (P.mode == WALK_INIT) {
+    if (valid) {  // placement of electron e: 10 u32 (sampler.cpp:30-36)
+      StreamReader rd(P.k0, P.k1, P.stream, pos0 + 20ull * p + 10ull * e);
+      place(rd, P.sites, n);
+      gn = g_of(P.sites, n[0], n[1], n[2]);
+    }
+  } else if (valid) {  // proposal of electron e (sampler.cpp:55-56)
+    StreamReader rd(P.k0, P.k1, P.stream, pos0 + 18ull * p + 8ull * e);
+    double g[3];
+    gaussian3(rd, g);
+    const double sigma = P.st->sigma;
+    for (int k = 0; k < 3; ++k) n[k] = P.in.at(3 * e + k, p) + g[k] * sigma;
+    gn = g_of(P.sites, n[0], n[1], n[2]);
+  }
+  double m2[3];
+  for (int k = 0; k < 3; ++k) m2[k] = __shfl_xor_sync(0xffffffffu, n[k], 1);
+  const double g2n = __shfl_xor_sync(0xffffffffu, gn, 1);
+  if (valid && e == 0) {
     if (P.mode == WALK_INIT) {
-      StreamReader rd(P.k0, P.k1, P.stream, pos0 + 20ull * p);
       Walker x;
-      place(rd, P.sites, x.r1);
-      place(rd, P.sites, x.r2);
+      for (int k = 0; k < 3; ++k) {
+        x.r1[k] = n[k];
+        x.r2[k] = m2[k];
+      }
       if (dist2(x.r1, x.r2) == 0.0) P.st->redo = 1;
-      finish_init(P, x);
+      x.g1 = gn;
+      x.g2 = g2n;
+      x.w = x.g1 * x.g2 / (P.ng * sqrt(dist2(x.r1, x.r2)));
       store_walker(P.out, p, x);
     } else {
-      const double sigma = P.st->sigma;
-      StreamReader rd(P.k0, P.k1, P.stream, pos0 + 18ull * p);
       Walker x = load_walker(P.in, p);
-      double n1[3], n2[3];
-      const double r12 = propose(rd, x, sigma, n1, n2);
+      const double dx = n[0] - m2[0], dy = n[1] - m2[1], dz = n[2] - m2[2];
+      const double r12 = sqrt(dx * dx + dy * dy + dz * dz);
       if (r12 == 0.0) {
         P.st->redo = 1;
-      } else {
-        acc = decide(rd, P, x, n1, n2, r12);
+      } else {  // sampler.cpp:63-77
+        StreamReader rd(P.k0, P.k1, P.stream, pos0 + 18ull * p + 16ull);
+        const double wnew = gn * g2n / (P.ng * r12);
+        const double u = rd.uniform();
+        if (u * x.w < wnew) {
+          for (int k = 0; k < 3; ++k) {
+            x.r1[k] = n[k];
+            x.r2[k] = m2[k];
+          }
+          x.g1 = gn;
+          x.g2 = g2n;
+          x.w = wnew;
+          acc = 1;
+        }
       }
       store_walker(P.out, p, x);
     }
@@ -189,7 +252,7 @@ __global__ void walk_kernel(WalkParams P) {
   __syncthreads();
   if (threadIdx.x == 0) {
     int t = 0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += s_acc[w];
+    for (int w = 0; w < WALK_THREADS / 32; ++w) t += s_acc[w];
     P.block_acc[blockIdx.x] = t;
     __threadfence();
     const unsigned done = atomicAdd(&P.st->done_ctas, 1u);
@@ -198,14 +261,24 @@ __global__ void walk_kernel(WalkParams P) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  __shared__ long long s_sum;
+  if (threadIdx.x < 32) {  // sum of the per-CTA counts, one warp
+    long long t = 0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) t += P.block_acc[b];
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) s_sum = t;
+  }
+  __syncthreads();
 
   // ---- last CTA: sequential redo if needed, stream advance, counters, tau ----
   __shared__ long long s_total;
   __shared__ unsigned long long s_consumed;
+  __shared__ int s_redo;
   if (threadIdx.x == 0) {
     long long total = 0;
     unsigned long long consumed;
-    if (P.st->redo) {
+    s_redo = P.st->redo;
+    if (s_redo) {
       // replay the whole sweep exactly as the reference's sequential loop
       StreamReader rd(P.k0, P.k1, P.stream, pos0);
       for (int q = 0; q < P.m; ++q) {
@@ -230,7 +303,7 @@ __global__ void walk_kernel(WalkParams P) {
       consumed = rd.pos - pos0;
       P.st->redo = 0;
     } else {
-      for (unsigned b = 0; b < gridDim.x; ++b) total += P.block_acc[b];
+      total = s_sum;
       consumed = (P.mode == WALK_INIT ? 20ull : 18ull) * unsigned(P.m);
     }
     s_total = total;
@@ -240,13 +313,14 @@ __global__ void walk_kernel(WalkParams P) {
     if (P.mode == WALK_PRODUCTION) {
       P.st->proposed += P.m;
       P.st->accepted += total;
-      // tau = TauSampler::sample(rng.uniform()) after the sweep (driver.cpp:445)
-      StreamReader rd(P.k0, P.k1, P.stream, P.st->pos);
-      const double u = rd.uniform();
+      if (s_redo) {
+        draw_tau(P, P.st->pos);  // the speculative draw used the wrong position
+      } else if (P.st->spec_error_idx != INT_MAX) {
+        P.st->error = 1;
+        P.st->error_idx = min(P.st->error_idx, P.st->spec_error_idx);
+      }
+      P.st->spec_error_idx = INT_MAX;
       P.st->pos += 2;
-      const double tau = -log1p(-u) / P.lambda;
-      P.st->tau = tau;
-      P.st->wtau = P.lambda * exp(-P.lambda * tau);
     } else if (P.mode == WALK_BURN) {
       // burn_in window and sigma adaptation (sampler.cpp:82-90)
       P.st->win_acc += total;
@@ -260,7 +334,7 @@ __global__ void walk_kernel(WalkParams P) {
     }
   }
   __syncthreads();
-  if (P.mode == WALK_PRODUCTION) tau_weights(P, P.st->tau);
+  if (P.mode == WALK_PRODUCTION && s_redo) tau_weights(P, P.st->tau);
 }
 
 // replay: positions/g from the caller, tau given (estimator input of mc_step_estimate)
@@ -279,9 +353,8 @@ __global__ void replay_load_kernel(WalkParams P, const double* walkers, double t
 }
 
 void launch_walk(const WalkParams& P, cudaStream_t s) {
-  const int threads = 128;
-  const int blocks = (P.m + threads - 1) / threads;
-  walk_kernel<<<blocks, threads, 0, s>>>(P);
+  const int blocks = (2 * P.m + WALK_THREADS - 1) / WALK_THREADS + (P.mode == WALK_PRODUCTION ? 1 : 0);
+  walk_kernel<<<blocks, WALK_THREADS, 0, s>>>(P);
 }
 
 void launch_replay_load(const WalkParams& P, const double* walkers, double tau, cudaStream_t s) {

@@ -26,4 +26,5 @@ with tempfile.TemporaryDirectory() as d:
     dw.advance(6, keep_on_device=True)
     p = dw.profile(False, True)
     print(os.environ.get("MCMP2_LIBDIR", "lib"), cfg, mode, "pair ms", round(p["ms"]["pair"] / p["launches"]["pair"], 4),
-          "spinor ms", round(p["ms"]["spinor"] / p["launches"]["spinor"], 4))
+          "spinor ms", round(p["ms"]["spinor"] / p["launches"]["spinor"], 4),
+          "walk ms", round(p["ms"]["walk"] / max(p["launches"]["walk"], 1), 4))
