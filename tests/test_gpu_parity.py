@@ -152,3 +152,21 @@ def test_overflow_is_reported_with_spinor_index(cfgdir, tmp_path):
     pts[1, 3:6] = -0.2
     with pytest.raises(Mcmp2Error, match="spinor 0"):
         dw.replay(pts[None], np.array([20000.0]))
+
+
+def test_overflow_during_advance_is_reported(cfgdir, tmp_path):
+    """The production sweep's tau draw (walk_kernel's speculative tau CTA) reports the overflow of
+    set_tau too: every energy shifted by +1e5 makes gexp(+eps_i tau) overflow for any tau drawn
+    (lambda is unchanged), first at occupied spinor 0."""
+    lines = (cfgdir / "cfg1.spinor").read_text().splitlines()
+    i = next(k for k, l in enumerate(lines) if l.startswith("energies"))
+    n = sum(int(x) for x in lines[i].split()[1:])
+    for k in range(i + 1, i + 1 + n):
+        lines[k] = repr(float(lines[k]) + 1e5)
+    bad = tmp_path / "shifted.spinor"
+    bad.write_text("\n".join(lines) + "\n")
+    conf = (cfgdir / "cfg1.conf").read_text()
+    dw = DeviceWalker(System(bad, conf), max_walkers=16)
+    dw.init_ensemble(16, seed=3)
+    with pytest.raises(Mcmp2Error, match="spinor 0"):
+        dw.advance(2)
