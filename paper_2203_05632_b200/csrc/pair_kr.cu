@@ -57,7 +57,15 @@ constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;
 constexpr uint32_t Q_BYTES = QPTS * KC4 * 32 * 8;
 constexpr int SO_DOUBLES = 2 * QW * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
 constexpr int SF_DOUBLES = 8 * 4;                     // per warp: 8 pairs x (f1d, f2x, f1x, f2d)
-constexpr int SMEM_BYTES = (STAGES * STAGE_DOUBLES + SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * STAGES * 8;
+#ifndef KR_OBUF
+#define KR_OBUF ((STAGES * STAGE_DOUBLES + 2 * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 64 <= 227 * 1024 ? 2 : 1)
+#endif
+// o tables: with two, tile t writes table t % 2 while no warp can still read it (every warp
+// passed tile t-1's "o table complete" barrier after its tile t-2 epilogue), so one CTA barrier
+// per tile suffices
+constexpr int OBUF = KR_OBUF;
+constexpr int SMEM_BYTES =
+    (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * STAGES * 8;
 
 __device__ __forceinline__ void consumer_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
@@ -87,8 +95,8 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 
 __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
-  double* const sO = sm + STAGES * STAGE_DOUBLES;
-  double* const sF = sO + SO_DOUBLES;
+  double* const sO0 = sm + STAGES * STAGE_DOUBLES;
+  double* const sF = sO0 + OBUF * SO_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sF + CONSUMERS * SF_DOUBLES);
   uint64_t* const empty = full + STAGES;
   __shared__ double s_red[CONSUMERS][2];
@@ -153,6 +161,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
       int ta, bp;
       kr_tile(int(blockIdx.x) + it * int(gridDim.x), ta, bp);
       const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile
+      double* const sO = sO0 + (it % OBUF) * SO_DOUBLES;
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           }
           release();
         }
-        consumer_barrier();  // every warp is done reading the previous tile's o table
+        if constexpr (OBUF == 1) consumer_barrier();  // every warp is done reading the previous o table
         const int y = (lane >> 2) & 3, pp = lane & 3;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
