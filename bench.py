@@ -331,7 +331,7 @@ def main():
                      "step_ms_profiled": step_ms_prof},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,  # walk_kernel, chi_kernel, mo_kernel, pair kernel per step
         "step_values_checksum": float(np.sum(vals)),
     }
     cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", dev)
