@@ -213,6 +213,44 @@ int orc_replay(void* h, int m, long nsteps, const double* walkers, const double*
   });
 }
 
+// One replay step at full size with `threads` std::threads, each summing the pair terms of a
+// contiguous band of walker rows (bands balanced by pair count), partial results added in
+// band order: the full-size parity check (association differs from the sequential loop only
+// in the band split).
+int orc_replay_parallel(void* h, int m, const double* walkers, double tau, int threads, double* est) {
+  auto* s = static_cast<System*>(h);
+  return guard([&] {
+    const WalkerEnsemble ens = from_walkers(walkers, m);
+    const double total = 0.5 * double(m) * (m - 1);
+    std::vector<int> cut(threads + 1, m);
+    cut[0] = 0;
+    double acc = 0.0;
+    int t = 1;
+    for (int p = 0; p < m && t < threads; ++p) {  // row p holds m - 1 - p pairs
+      acc += m - 1 - p;
+      if (acc >= total * t / threads) cut[t++] = p + 1;
+    }
+    std::vector<StepEstimate> part(threads);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < threads; ++k)
+      pool.emplace_back([&, k] {
+        EstimatorWorkspace ws(s->spinors, m);
+        part[k] = mc_step_estimate_rows(s->spinors, ens, tau, s->spec, s->tau, ws, cut[k], cut[k + 1], nullptr);
+      });
+    for (auto& th : pool) th.join();
+    StepEstimate e;
+    e.value = 0.0;
+    e.imag = 0.0;
+    for (const auto& q : part) {
+      e.value += q.value;
+      e.imag += q.imag;
+      e.direct_sum += q.direct_sum;
+      e.exchange_sum += q.exchange_sum;
+    }
+    est_to(e, est);
+  });
+}
+
 // sample_term (estimator.cpp:65-75): p, q = 8 doubles each; out: direct re/im, exchange re/im
 int orc_sample_term(void* h, const double* p, const double* q, double tau, int physical, double* out) {
   auto* s = static_cast<System*>(h);

@@ -113,6 +113,14 @@ class OracleSystem:
         check(lib().orc_replay(self.h, m, n, _d(walkers), _d(tau), int(physical), _d(est)))
         return est
 
+    def replay_parallel(self, walkers, tau, threads):
+        """One full-size replay step (m x 8 walkers), pair rows split over `threads` threads."""
+        walkers = np.ascontiguousarray(walkers, dtype=np.float64)
+        est = np.empty(6)
+        check(lib().orc_replay_parallel(self.h, walkers.shape[0], _d(walkers), C.c_double(tau), int(threads),
+                                        _d(est)))
+        return est
+
     def sample_term(self, p, q, tau, physical=False):
         p = np.ascontiguousarray(p, dtype=np.float64)
         q = np.ascontiguousarray(q, dtype=np.float64)

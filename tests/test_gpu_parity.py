@@ -170,3 +170,26 @@ def test_overflow_during_advance_is_reported(cfgdir, tmp_path):
     dw.init_ensemble(16, seed=3)
     with pytest.raises(Mcmp2Error, match="spinor 0"):
         dw.advance(2)
+
+
+@pytest.mark.parametrize("name,m", [("cfg3", 512), ("cfg4", 2048)])
+def test_full_size_replay_matches_oracle(cfgdir, name, m):
+    """BASELINE sizes: one step of the device estimator at the full walker count (the bench's
+    own configuration, every pair tile of the production launch) against the oracle's full
+    C(m,2) pair loop (rows split over host threads), both Kramers and general kernels."""
+    import os
+
+    sp, text, orc, sysd = load(cfgdir, name)
+    dw = DeviceWalker(sysd, max_walkers=m)
+    dw.init_ensemble(m, seed=5)
+    dw.burn_in(20)
+    dw.advance(1)
+    w = dw.get_ensemble().walkers[:, :8]
+    tau = 0.37
+    ref = orc.replay_parallel(w, tau, threads=max(1, min(32, os.cpu_count() or 1)))
+    for mode in (1, 0):
+        dw.kramers(mode)
+        got = dw.replay(w[None], np.array([tau]))[0]
+        assert abs(got[0] - ref[0]) <= REL * abs(ref[0])
+        for k in (2, 4):
+            assert abs(got[k] - ref[k]) <= REL * abs(ref[k])
