@@ -5,10 +5,14 @@
 // input of the pair kernel), chosen so the pair kernel's DMMA fragments are contiguous:
 //   point pt = 2*walker + electron            (estimator.cpp:39-42: 2p <- r1, 2p+1 <- r2)
 //   k-group g = 4 consecutive spinors; occupied groups [0, Go), virtual groups [Go, Go+Gv)
-//   chunk c = KC4 consecutive groups (the smem stage of the pair kernel)
-//   Phi[c][pt][g % KC4][plane re/im][x*4 + k%4]   (16 doubles per plane, x = channel)
+//   chunk c = up to KC4 consecutive groups of one kind (the smem stage of the pair kernel):
+//     the occupied groups in chunks of KC4, the last one narrower, then the virtual ones
+//   chunk c holding groups [first, first + width):
+//     Phi[first * npts_pad + pt * width + (g - first)][plane re/im][x*4 + k%4]
+//     (32 doubles per (point, group); 16 per plane, x = channel)
 // so one half-fragment (4 channels x 4 spinors) of one point is 128 contiguous bytes and a
-// stage (16 consecutive points x KC4 groups) is one contiguous TMA bulk copy. Values are
+// stage (consecutive points x width groups) is one contiguous TMA bulk copy with no padding
+// groups. Values are
 // scaled by sqrt(guarded_exp(+-eps tau)) so O = Phi_o Phi_o^H and V = Phi_v Phi_v^H carry
 // the full exp(+-eps tau) weight (greens.cpp:63-79).
 #pragma once
@@ -32,6 +36,27 @@ constexpr int NCH = 4;          // channels per point in the Phi layout (ncomp <
 // alpha-row fragment loads of pair_kr.cu (4 doubles from each of 4 points per half-warp) are
 // conflict-free; whole half-fragment loads stay permutations of one 128-byte row.
 __host__ __device__ __forceinline__ int phi_swz(int pt) { return ((pt ^ (pt >> 1)) & 1) << 2; }
+
+// chunking of the k-groups (see the layout above); identical on host and device
+struct PhiChunks {
+  int Go, Gv;  // occupied and virtual k-groups
+  __host__ __device__ int occ_chunks() const { return (Go + KC4 - 1) / KC4; }
+  __host__ __device__ int count() const { return occ_chunks() + (Gv + KC4 - 1) / KC4; }
+  __host__ __device__ int first(int c) const {
+    const int co = occ_chunks();
+    return c < co ? c * KC4 : Go + (c - co) * KC4;
+  }
+  __host__ __device__ int width(int c) const {
+    const int co = occ_chunks(), r = c < co ? Go - c * KC4 : Gv - (c - co) * KC4;
+    return r < KC4 ? r : KC4;
+  }
+  __host__ __device__ int chunk_of(int g) const { return g < Go ? g / KC4 : occ_chunks() + (g - Go) / KC4; }
+  // offset in doubles of (group g, point pt)
+  __host__ __device__ size_t offset(int g, int pt, int npts_pad) const {
+    const int c = chunk_of(g), f = first(c);
+    return (size_t(f) * npts_pad + size_t(pt) * width(c) + (g - f)) * 32;
+  }
+};
 
 // ------------------------------------------------------------------ device system
 struct DevSites {

@@ -47,7 +47,7 @@ struct SpinorParams {
   const double* uniq_center; // [nuniq][3]
   const double* uniq_zeta;   // [nuniq]
   int n_occ, n_vir, n_p;
-  int Go, Gtot;              // occupied k-groups, total k-groups (multiple of KC4)
+  int Go, Gv;                // occupied and virtual k-groups (PhiChunks)
   const double* sw;
   double* phi;
   double* hinv;              // [m] 1 / (g1 g2) per walker, for the pair epilogue
@@ -55,8 +55,8 @@ struct SpinorParams {
 
 struct PairParams {
   const double* phi;
-  int npts_pad, Go, Gv, Gtot;
-  int go_used;               // occupied groups holding spinors (Go pads to whole chunks)
+  int npts_pad, Go, Gv;      // Phi layout (PhiChunks)
+  int ring, ring_doubles;    // pair_kr: stage ring depth and stage size for this layout
   int m, nb;                 // walkers, walker blocks of WB
   WalkerBuf walkers;         // g1 (row 6), g2 (row 7)
   const double* hinv;        // [m] 1 / (g1 g2), written by chi_kernel this step
@@ -77,7 +77,8 @@ cudaError_t pair_kernel_setup();
 // Kramers-restricted variant (pair_kr.cu): half the DMMA work for time-reversal-paired columns
 void launch_pair_kr(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kr_kernel_setup();
-double pair_kr_block_tiles(int nb);  // WB x WB walker blocks the Kramers launch computes
+double pair_kr_block_tiles(int nb);
+void pair_kr_ring(int max_width, int& ring, int& ring_doubles);  // stage ring for the widest chunk  // WB x WB walker blocks the Kramers launch computes
 cudaError_t spinor_kernel_setup();
 
 }  // namespace mcmp2dev

@@ -77,7 +77,7 @@ struct mcmp2dev_handle {
 
   // system
   int ncomp = 0, n_occ = 0, n_vir = 0, n_p = 0, nfunc = 0, rows = 0;
-  int Go = 0, Gv = 0, Gtot = 0;
+  int Go = 0, Gv = 0;
   double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
   int estimator = 0;
   bool kramers_eligible = false, kramers = false;  // pair_kr.cu path
@@ -174,9 +174,11 @@ struct mcmp2dev_handle {
     p.phi = d_phi;
     p.npts_pad = npts_pad;
     p.Go = Go;
-    p.go_used = (n_occ + 3) / 4;
     p.Gv = Gv;
-    p.Gtot = Gtot;
+    {
+      const int wmax = std::min(KC4, std::max(Go, Gv));
+      pair_kr_ring(wmax > 0 ? wmax : 1, p.ring, p.ring_doubles);
+    }
     p.m = mm;
     p.nb = (mm + WB - 1) / WB;
     p.walkers = wb;
@@ -425,12 +427,11 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;
   sp.n_p = h->n_p;
-  // occupied k-groups padded to whole pair-kernel chunks, so O and V phases never share a stage
-  h->Go = ((h->n_occ + 3) / 4 + KC4 - 1) / KC4 * KC4;
+  // k-groups of 4 spinors; chunked per kind (PhiChunks), so O and V phases never share a stage
+  h->Go = (h->n_occ + 3) / 4;
   h->Gv = (h->n_vir + 3) / 4;
-  h->Gtot = h->Go + (h->Gv + KC4 - 1) / KC4 * KC4;
   sp.Go = h->Go;
-  sp.Gtot = h->Gtot;
+  sp.Gv = h->Gv;
   h->d_energies = dupload(s->energies, size_t(h->n_p), o);
   h->d_sw = dalloc<double>(h->n_p, o);
   sp.sw = h->d_sw;
@@ -459,7 +460,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   st.spec_error_idx = INT_MAX;
   ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   h->d_block_acc = dalloc<int>((max_walkers + 63) / 64 + 2, o);  // 64 walkers per walk CTA + tau CTA
-  const size_t phi_doubles = size_t(h->Gtot) * h->npts_pad * 32;
+  const size_t phi_doubles = size_t(h->Go + h->Gv) * h->npts_pad * 32;
   h->d_phi = dalloc<double>(phi_doubles, o);
   ck(cudaMemset(h->d_phi, 0, phi_doubles * sizeof(double)), "memset phi");
   sp.phi = h->d_phi;
@@ -761,7 +762,7 @@ int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
     // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
     const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
-    *pair_dmma_flop = ntiles * 512.0 * ((h->n_occ + 3) / 4 * per_o + h->Gv * per_v);
+    *pair_dmma_flop = ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
   });
 }
 

@@ -37,7 +37,6 @@ constexpr int CONSUMERS = 8;                              // MMA warps (wq 0..3 
 constexpr int THREADS = 32 * (CONSUMERS + 1);             // + one TMA producer warp
 constexpr int HALF_PTS = 2 * WB;                          // 16 points per walker block
 constexpr int STAGE_DOUBLES = 2 * HALF_PTS * KC4 * 32;    // 32 points x KC4 groups x 32
-constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;  // 16 KB per side per stage
 constexpr int SO_DOUBLES = 512;                           // per consumer warp: 2x2x4 blocks of 4x4 complex
 constexpr int SV_DOUBLES = 8 * 64 * 2;                    // physical epilogue: 8 pairs x 8x8 complex V
 
@@ -66,8 +65,9 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntiles = P.nb * (P.nb + 1) / 2;
-  const int nchunks = P.Gtot / KC4;
-  const int cO = P.Go / KC4;  // occupied groups are padded to whole chunks
+  const PhiChunks ch{P.Go, P.Gv};
+  const int nchunks = ch.count();
+  const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
   const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (tid == 0) {
@@ -90,11 +90,13 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           const int stage = int(seq % STAGES);
           mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
           double* dst = sm + stage * STAGE_DOUBLES;
-          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bq) * KC4 * 32;
-          const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
-          mbar_expect_tx(&full[stage], 2 * HALF_BYTES);
-          bulk_g2s(dst, srcq, HALF_BYTES, &full[stage]);
-          bulk_g2s(dst + HALF_PTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+          const int f = ch.first(c), uc = ch.width(c);
+          const uint32_t half_bytes = HALF_PTS * uc * 32 * 8;
+          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bq * uc) * 32;
+          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bp * uc) * 32;
+          mbar_expect_tx(&full[stage], 2 * half_bytes);
+          bulk_g2s(dst, srcq, half_bytes, &full[stage]);
+          bulk_g2s(dst + HALF_PTS * uc * 32, srcp, half_bytes, &full[stage]);
         }
       }
     }
@@ -132,10 +134,11 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
             for (int j = 0; j < 2; ++j) t1[e][h][j] = t2[e][h][j] = t3[e][h][j] = 0.0;
         for (int c = 0; c < cO; ++c) {
           const double* S = acquire();
+          const int uc = ch.width(c);
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
-            if (c * KC4 + gg >= P.go_used) break;  // zero chunk padding
-            auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
+            if (gg >= uc) break;  // narrower last chunk
+            auto frag = [&](int ptl, int plane) { return S[(ptl * uc + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int pa = 2 * (2 * wq + hl) + e;
@@ -176,10 +179,11 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
       for (int c = cO; c < nchunks; ++c) {
         const double* S = acquire();
+        const int uc = ch.width(c);
 #pragma unroll
         for (int gg = 0; gg < KC4; ++gg) {
-          if (c * KC4 + gg >= P.Go + P.Gv) break;  // zero padding at the end
-          auto frag = [&](int ptl, int plane) { return S[(ptl * KC4 + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
+          if (gg >= uc) break;  // narrower last chunk
+          auto frag = [&](int ptl, int plane) { return S[(ptl * uc + gg) * 32 + plane * 16 + (l16 ^ phi_swz(ptl))]; };
           double ar[2], ai[2], sa[2], br[4], bi[4], db[4];
 #pragma unroll
           for (int qi = 0; qi < 2; ++qi) {

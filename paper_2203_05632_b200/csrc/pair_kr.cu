@@ -44,7 +44,8 @@ using namespace pairk;
 // full-chunk path 4.15; 3 stages 4.14; epilogue hinv prefetched at tile start (spills) 4.07; no
 // producer warp, the last DMMA warp to release a stage refills it (16 warps, 109 registers) 4.58;
 // this kernel 4.00.
-constexpr int STAGES = KR_STAGES;
+constexpr int STAGES = KR_STAGES;  // ring depth at the widest chunk (KC4 groups)
+constexpr int MAX_RING = 16;       // ring depth for narrow chunks: same bytes, more stages
 constexpr int QB = KR_QB;
 constexpr int QW = WB * QB;                           // Q walkers per tile
 constexpr int CONSUMERS = 8 * QB;
@@ -53,28 +54,27 @@ constexpr int MINB = QB == 1 ? 2 : 1;                 // CTAs per SM
 constexpr int HALF_PTS = 2 * WB;                      // P points per tile
 constexpr int QPTS = 2 * QW;                          // Q points per tile
 constexpr int STAGE_DOUBLES = (QPTS + HALF_PTS) * KC4 * 32;
-constexpr uint32_t HALF_BYTES = HALF_PTS * KC4 * 32 * 8;
-constexpr uint32_t Q_BYTES = QPTS * KC4 * 32 * 8;
 constexpr int SO_DOUBLES = 2 * QW * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
 constexpr int SF_DOUBLES = 8 * 4;                     // per warp: 8 pairs x (f1d, f2x, f1x, f2d)
 #ifndef KR_OBUF
-#define KR_OBUF ((STAGES * STAGE_DOUBLES + 2 * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 64 <= 227 * 1024 ? 2 : 1)
+#define KR_OBUF ((STAGES * STAGE_DOUBLES + 2 * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * MAX_RING * 8 <= 227 * 1024 ? 2 : 1)
 #endif
 // o tables: with two, tile t writes table t % 2 while no warp can still read it (every warp
 // passed tile t-1's "o table complete" barrier after its tile t-2 epilogue), so one CTA barrier
 // per tile suffices
 constexpr int OBUF = KR_OBUF;
 constexpr int SMEM_BYTES =
-    (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * STAGES * 8;
+    (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * MAX_RING * 8;
 
 __device__ __forceinline__ void consumer_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
 }
 
 // y is XOR-swizzled by the parity of (q, e): the epilogue's 16-byte reads of one warp then cover
-// both halves of a 128-byte row instead of 4 lanes per bank group (4-way -> 2 wavefronts).
+// both halves of a 128-byte row instead of 4 lanes per bank group (4-way -> 2 wavefronts); x_alpha
+// by the parity of p, so the phase-1 writes spread over all 8 16-byte slots (8 -> 4 wavefronts).
 __device__ __forceinline__ int o_index(int e, int q, int p, int y, int xa) {
-  return ((((e * QW + q) * WB + p) * 4 + (y ^ ((q ^ e) & 1))) * 2 + xa) * 2;
+  return ((((e * QW + q) * WB + p) * 4 + (y ^ ((q ^ e) & 1))) * 2 + (xa ^ (p & 1))) * 2;
 }
 
 // tiles: Q row a covers walker blocks [QB a, QB a + QB), P block b in [0, QB a + QB);
@@ -87,6 +87,19 @@ __device__ __forceinline__ void kr_tile(int t, int& a, int& b) {
   b = t - QB * r * (r + 1) / 2;
 }
 
+// the CTA's tile sequence t0, t0 + stride, ... walked without the square root of kr_tile
+struct TileWalk {
+  int a, b;
+  __device__ explicit TileWalk(int t0) { kr_tile(t0, a, b); }
+  __device__ void next(int stride) {
+    b += stride;
+    while (b >= QB * (a + 1)) {  // row a holds QB (a + 1) tiles
+      b -= QB * (a + 1);
+      ++a;
+    }
+  }
+};
+
 __host__ __device__ constexpr int kr_ntiles(int nb) {
   const int nbq = (nb + QB - 1) / QB;
   return QB * nbq * (nbq + 1) / 2;
@@ -98,18 +111,22 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   double* const sF = sO0 + OBUF * SO_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sF + CONSUMERS * SF_DOUBLES);
-  uint64_t* const empty = full + STAGES;
+  uint64_t* const empty = full + MAX_RING;
+  // ring of P.ring stages of P.ring_doubles each, sized on the host from the widest chunk:
+  // the stage region holds STAGES widest stages, and more when every chunk is narrower
+  const int ring = P.ring, ring_doubles = P.ring_doubles;
   __shared__ double s_red[CONSUMERS][2];
   __shared__ bool s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntiles = kr_ntiles(P.nb);
-  const int nchunks = P.Gtot / KC4;
-  const int cO = P.Go / KC4;
+  const PhiChunks ch{P.Go, P.Gv};
+  const int nchunks = ch.count();
+  const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
   const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < ring; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CONSUMERS);
     }
@@ -119,19 +136,25 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 
   if (warp == CONSUMERS) {
     if (lane == 0) {  // TMA producer
-      long long seq = 0;
-      for (int it = 0; it < my_tiles; ++it) {
-        int ta, bp;
-        kr_tile(int(blockIdx.x) + it * int(gridDim.x), ta, bp);
-        for (int c = 0; c < nchunks; ++c, ++seq) {
-          const int stage = int(seq % STAGES);
-          mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
-          double* dst = sm + stage * STAGE_DOUBLES;
-          const double* srcq = P.phi + (size_t(c) * P.npts_pad + size_t(QPTS) * ta) * KC4 * 32;
-          const double* srcp = P.phi + (size_t(c) * P.npts_pad + size_t(HALF_PTS) * bp) * KC4 * 32;
-          mbar_expect_tx(&full[stage], Q_BYTES + HALF_BYTES);
-          bulk_g2s(dst, srcq, Q_BYTES, &full[stage]);
-          bulk_g2s(dst + QPTS * KC4 * 32, srcp, HALF_BYTES, &full[stage]);
+      int stage = 0;
+      uint32_t phase = 0;
+      TileWalk tw(int(blockIdx.x));
+      for (int it = 0; it < my_tiles; ++it, tw.next(int(gridDim.x))) {
+        const int ta = tw.a, bp = tw.b;
+        for (int c = 0; c < nchunks; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          double* dst = sm + stage * ring_doubles;
+          const int f = ch.first(c), uc = ch.width(c);
+          const uint32_t q_bytes = QPTS * uc * 32 * 8, p_bytes = HALF_PTS * uc * 32 * 8;
+          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(QPTS) * ta * uc) * 32;
+          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bp * uc) * 32;
+          mbar_expect_tx(&full[stage], q_bytes + p_bytes);
+          bulk_g2s(dst, srcq, q_bytes, &full[stage]);
+          bulk_g2s(dst + QPTS * uc * 32, srcp, p_bytes, &full[stage]);
+          if (++stage == ring) {
+            stage = 0;
+            phase ^= 1u;
+          }
         }
       }
     }
@@ -145,21 +168,24 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
     double* const sf = sF + warp * SF_DOUBLES;
     const double cw = P.ng2 / P.st_ro->wtau;
     double acc_d = 0.0, acc_x = 0.0;
-    long long seq = 0;
+    int stage = 0;
+    uint32_t phase = 0;
     auto acquire = [&]() -> const double* {
-      const int stage = int(seq % STAGES);
-      mbar_wait(&full[stage], uint32_t((seq / STAGES) & 1));
-      return sm + stage * STAGE_DOUBLES;
+      mbar_wait(&full[stage], phase);
+      return sm + stage * ring_doubles;
     };
     auto release = [&]() {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[int(seq % STAGES)]);
-      ++seq;
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == ring) {
+        stage = 0;
+        phase ^= 1u;
+      }
     };
 
-    for (int it = 0; it < my_tiles; ++it) {
-      int ta, bp;
-      kr_tile(int(blockIdx.x) + it * int(gridDim.x), ta, bp);
+    TileWalk tw(int(blockIdx.x));
+    for (int it = 0; it < my_tiles; ++it, tw.next(int(gridDim.x))) {
+      const int ta = tw.a, bp = tw.b;
       const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile
       double* const sO = sO0 + (it % OBUF) * SO_DOUBLES;
 
@@ -170,11 +196,12 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
         for (int h = 0; h < 2; ++h) t1[h][0] = t1[h][1] = t2[h][0] = t2[h][1] = t3[h][0] = t3[h][1] = 0.0;
         for (int c = 0; c < cO; ++c) {
           const double* S = acquire();
+          const int uc = ch.width(c);
 #pragma unroll
           for (int gg = 0; gg < KC4; ++gg) {
-            if (c * KC4 + gg >= P.go_used) break;  // zero chunk padding
+            if (gg >= uc) break;  // narrower last chunk
             auto at = [&](int ptl, int plane, int off) {
-              return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
+              return S[(ptl * uc + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
             };
             const int pb = QPTS + 2 * (4 * p1w + (lane >> 3)) + e1;
             const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
@@ -211,11 +238,12 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
       for (int c = cO; c < nchunks; ++c) {
         const double* S = acquire();
+        const int uc = ch.width(c);
 #pragma unroll
         for (int gg = 0; gg < KC4; ++gg) {
-          if (c * KC4 + gg >= P.Go + P.Gv) break;
+          if (gg >= uc) break;  // narrower last chunk
           auto at = [&](int ptl, int plane, int off) {
-            return S[(ptl * KC4 + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
+            return S[(ptl * uc + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
           };
           double ar[2], ai[2], sa[2], br[2], bi[2], db[2];
 #pragma unroll
@@ -328,6 +356,12 @@ int g_sms_kr[64];
 }
 
 double pair_kr_block_tiles(int nb) { return double(kr_ntiles(nb)) * QB; }
+
+void pair_kr_ring(int max_width, int& ring, int& ring_doubles) {
+  ring_doubles = (QPTS + HALF_PTS) * max_width * 32;
+  ring = (STAGES * STAGE_DOUBLES) / ring_doubles;
+  if (ring > MAX_RING) ring = MAX_RING;
+}
 
 cudaError_t pair_kr_kernel_setup() {
   int dev = 0;

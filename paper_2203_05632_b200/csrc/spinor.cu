@@ -198,14 +198,14 @@ __device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_ba
     }
   }
   if (!active) return;
-  // epilogue: scale and scatter into Phi[chunk][pt][g%KC4][re|im][x*4 + k%4]
+  // epilogue: scale and scatter into Phi (layout in common.cuh)
+  const PhiChunks ch{P.Go, P.Gv};
   auto put = [&](int x, int pt, int col, double re, double im) {
     const double w = P.sw[col];
     const bool occ = col < P.n_occ;
     const int kidx = occ ? col : col - P.n_occ;
     const int grp = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
-    double* dst = P.phi + ((size_t(grp / KC4) * P.npts_pad + pt) * KC4 + grp % KC4) * 32 +
-                  ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
+    double* dst = P.phi + ch.offset(grp, pt, P.npts_pad) + ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
     dst[0] = re * w;
     dst[16] = im * w;
   };

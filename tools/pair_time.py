@@ -9,6 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2203_05632_b200 import DeviceWalker, System, generate_config  # noqa: E402
 
 W = {"cfg1": 16, "cfg2": 128, "cfg3": 512, "cfg4": 2048}
+W.update({f"cfg5-{n}": 8192 for n in (2, 10, 18, 36, 54, 86)})
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 with tempfile.TemporaryDirectory() as d:
     sp, conf = generate_config(cfg, d)
