@@ -17,6 +17,6 @@ def cfgdir(tmp_path_factory):
     """BASELINE configs generated once per session by the C++ host (host/generate.cpp)."""
     from paper_2203_05632_b200 import generate_config
     d = tmp_path_factory.mktemp("cfg")
-    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "syn1c", "syn2c"):
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "syn1c", "syn2c", "cfg5-2", "cfg5-10"):
         generate_config(name, d)
     return d

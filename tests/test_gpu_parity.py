@@ -26,7 +26,9 @@ def load(cfgdir, name):
 
 
 @pytest.mark.parametrize("name,m,nsteps", [("cfg1", 16, 6), ("cfg2", 40, 2), ("cfg3", 24, 2), ("cfg4", 20, 1),
-                                           ("syn1c", 9, 4), ("syn2c", 7, 4)])
+                                           ("syn1c", 9, 4), ("syn2c", 7, 4),
+                                           # narrow chunks: cfg5-2 runs a 4-deep stage ring, cfg5-10 has a 1-group virtual chunk
+                                           ("cfg5-2", 72, 2), ("cfg5-10", 56, 2)])
 def test_replay_matches_oracle(cfgdir, name, m, nsteps):
     sp, text, orc, sysd = load(cfgdir, name)
     tr = orc.trajectory(seed=11, stream=0, m=m, burn=30, nsteps=nsteps)
