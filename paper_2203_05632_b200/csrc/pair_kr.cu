@@ -66,8 +66,17 @@ constexpr int OBUF = KR_OBUF;
 constexpr int SMEM_BYTES =
     (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * MAX_RING * 8;
 
-__device__ __forceinline__ void consumer_barrier() {
-  asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
+// The o table rows of Q walkers 4g..4g+3 are written in phase 1 by warps 4g..4g+3 (all (p1w, e1))
+// and read in phase 2 by the same four warps (wp = 0..3), so the phase switch synchronises
+// groups of four warps (named barriers 1..QB*2), not the whole CTA.
+#ifndef KR_GROUP_BARRIER
+#define KR_GROUP_BARRIER 1
+#endif
+__device__ __forceinline__ void consumer_barrier(int group) {
+  if (KR_GROUP_BARRIER)
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
+  else
+    asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
 }
 
 // y is XOR-swizzled by the parity of (q, e): the epilogue's 16-byte reads of one warp then cover
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           }
           release();
         }
-        if constexpr (OBUF == 1) consumer_barrier();  // every warp is done reading the previous o table
+        if constexpr (OBUF == 1) consumer_barrier(q1w);  // the group is done reading the previous o rows
         const int y = (lane >> 2) & 3, pp = lane & 3;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
             sO[idx] = t1[h][j] + t2[h][j];                   // o = conj O~
             sO[idx + 1] = -(t3[h][j] - t1[h][j] + t2[h][j]);
           }
-        consumer_barrier();  // o table complete
+        consumer_barrier(q1w);  // the group's o rows are complete
       }
 
       // ---- phase 2: V rows (q, e_q, x_alpha), cols (p, e_p, y) ----
