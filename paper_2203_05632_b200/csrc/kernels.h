@@ -50,7 +50,7 @@ struct SpinorParams {
   int Go, Gv;                // occupied and virtual k-groups (PhiChunks)
   const double* sw;
   double* phi;
-  double* hinv;              // [m] 1 / (g1 g2) per walker, for the pair epilogue
+  double* hinv;              // [m] 1 / (g1 g2) per walker (chi_kernel), folded into Phi_v by mo_kernel
 };
 
 struct PairParams {
@@ -59,7 +59,6 @@ struct PairParams {
   int ring, ring_doubles;    // pair_kr: stage ring depth and stage size for this layout
   int m, nb;                 // walkers, walker blocks of WB
   WalkerBuf walkers;         // g1 (row 6), g2 (row 7)
-  const double* hinv;        // [m] 1 / (g1 g2), written by chi_kernel this step
   const DevState* st_ro;
   DevState* st;
   double ng2, w_direct, w_exchange;

@@ -182,7 +182,6 @@ struct mcmp2dev_handle {
     p.m = mm;
     p.nb = (mm + WB - 1) / WB;
     p.walkers = wb;
-    p.hinv = d_hinv;
     p.st_ro = d_state;
     p.st = d_state;
     p.ng2 = ng * ng;

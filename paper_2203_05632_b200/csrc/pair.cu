@@ -269,12 +269,12 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
                 txr += m1[x][y][0] * m2[y][x][0] - m1[x][y][1] * m2[y][x][1];
                 txi += m1[x][y][0] * m2[y][x][1] + m1[x][y][1] * m2[y][x][0];
               }
-            const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
+            // hinv_p hinv_q of inv_w ride in Phi_v (mo_kernel); N_g^2 / w(tau) is applied per warp
             const double adr = -P.w_direct * t1r, adi = -P.w_direct * t1i;
-            acc_dr += (adr * t2r - adi * t2i) * inv;
-            acc_di += (adr * t2i + adi * t2r) * inv;
-            acc_xr += -P.w_exchange * txr * inv;
-            acc_xi += -P.w_exchange * txi * inv;
+            acc_dr += adr * t2r - adi * t2i;
+            acc_di += adr * t2i + adi * t2r;
+            acc_xr += -P.w_exchange * txr;
+            acc_xi += -P.w_exchange * txi;
           }
         }
         __syncwarp();
@@ -312,14 +312,14 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           if (lane == 0) {
             const int q = WB * bq + 2 * wq + qi, p = WB * bp + 4 * wp + pj;
             if (q < P.m && p < P.m && q > p) {
-              const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
-              // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32)
+              // -w_d f1d f2d inv, -w_x f1x f2x inv (estimator.cpp:32); hinv_p hinv_q of inv_w ride
+              // in Phi_v (mo_kernel), N_g^2 / w(tau) is applied per warp
               const double adr = -P.w_direct * f1dr, adi = -P.w_direct * f1di;
               const double axr = -P.w_exchange * f1xr, axi = -P.w_exchange * f1xi;
-              acc_dr += (adr * f2dr - adi * f2di) * inv;
-              acc_di += (adr * f2di + adi * f2dr) * inv;
-              acc_xr += (axr * f2xr - axi * f2xi) * inv;
-              acc_xi += (axr * f2xi + axi * f2xr) * inv;
+              acc_dr += adr * f2dr - adi * f2di;
+              acc_di += adr * f2di + adi * f2dr;
+              acc_xr += axr * f2xr - axi * f2xi;
+              acc_xi += axr * f2xi + axi * f2xr;
             }
           }
         }
@@ -335,10 +335,10 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
       }
     }
     if (lane == 0) {
-      s_red[warp][0] = acc_dr;
-      s_red[warp][1] = acc_di;
-      s_red[warp][2] = acc_xr;
-      s_red[warp][3] = acc_xi;
+      s_red[warp][0] = acc_dr * cw;
+      s_red[warp][1] = acc_di * cw;
+      s_red[warp][2] = acc_xr * cw;
+      s_red[warp][3] = acc_xi * cw;
     }
   }
   __syncthreads();

@@ -308,9 +308,11 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
         const int q = q0 + 4 * wq + 2 * h + hh, p = p0 + 2 * wp + pp;
         if (q < P.m && p < P.m && q > p) {
           const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
-          const double inv = cw * P.hinv[p] * P.hinv[q];  // estimator.cpp:55, see chi_kernel
-          acc_d += (-P.w_direct * F[0]) * F[3] * inv;                // estimator.cpp:32
-          acc_x += (-P.w_exchange * F[2]) * F[1] * inv;
+          // estimator.cpp:32; the walker weights hinv_p hinv_q of inv_w (estimator.cpp:55) ride in
+          // the virtual Phi of the electron-1 points (mo_kernel), the constant N_g^2 / w(tau) is
+          // applied once per warp below
+          acc_d += (-P.w_direct * F[0]) * F[3];
+          acc_x += (-P.w_exchange * F[2]) * F[1];
         }
       }
       __syncwarp();
@@ -321,8 +323,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
       acc_x += __shfl_down_sync(0xffffffffu, acc_x, o);
     }
     if (lane == 0) {
-      s_red[warp][0] = acc_d;
-      s_red[warp][1] = acc_x;
+      s_red[warp][0] = acc_d * cw;
+      s_red[warp][1] = acc_x * cw;
     }
   }
   __syncthreads();

@@ -87,9 +87,9 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
     const int pt = tid / 3, k = tid % 3, gp = pt0 + pt;
     s_pos[tid] = gp < P.npts ? P.walkers.at((gp & 1) * 3 + k, gp >> 1) : 0.0;  // 2p <- r1, 2p+1 <- r2
   } else if (tid < 3 * CHI_PTS + CHI_PTS / 2) {
-    // pair-epilogue weight of walker w: inv_w = N_g^2 / (g1p g2p g1q g2q w(tau)) (estimator.cpp:55)
-    // is evaluated as (N_g^2 / w(tau)) hinv_p hinv_q, hinv = 1 / (g1 g2) (a few ulp from the
-    // reference's association)
+    // walker weight of the pair term: inv_w = N_g^2 / (g1p g2p g1q g2q w(tau)) (estimator.cpp:55)
+    // is evaluated as (N_g^2 / w(tau)) hinv_p hinv_q, hinv = 1 / (g1 g2), with hinv folded into
+    // Phi_v by mo_kernel (a few ulp from the reference's association)
     const int w = (pt0 >> 1) + tid - 3 * CHI_PTS;
     if (2 * w < P.npts) P.hinv[w] = 1.0 / (P.walkers.at(6, w) * P.walkers.at(7, w));
   }
@@ -200,9 +200,13 @@ __device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_ba
   if (!active) return;
   // epilogue: scale and scatter into Phi (layout in common.cuh)
   const PhiChunks ch{P.Go, P.Gv};
-  auto put = [&](int x, int pt, int col, double re, double im) {
-    const double w = P.sw[col];
+  // the walker weight hinv = 1 / (g1 g2) of inv_w (estimator.cpp:55) is folded into the virtual
+  // columns of electron-1 points: V(2q, 2p) then carries hinv_q hinv_p, V(2q+1, 2p) hinv_p and
+  // V(2q, 2p+1) hinv_q, so both the direct (va vb) and the exchange (vc vd) products of a pair
+  // carry exactly hinv_p hinv_q (chi_kernel wrote hinv this step)
+  auto put = [&](int x, int pt, double hp, int col, double re, double im) {
     const bool occ = col < P.n_occ;
+    const double w = occ ? P.sw[col] : P.sw[col] * hp;
     const int kidx = occ ? col : col - P.n_occ;
     const int grp = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
     double* dst = P.phi + ch.offset(grp, pt, P.npts_pad) + ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
@@ -214,6 +218,7 @@ __device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_ba
   for (int i = 0; i < 4; ++i) {
     const int pt = (ptf0 + i) * 8 + (lane >> 2);
     if (pt >= P.npts) continue;
+    const double hp = (pt & 1) ? 1.0 : P.hinv[pt >> 1];
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
       const int r8 = 2 * (lane & 3) + jj;
@@ -221,16 +226,16 @@ __device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_ba
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
           const int col = (nf0 / 2 + uu) * 8 + r8;
-          if (col < P.n_p) put(xa, pt, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
+          if (col < P.n_p) put(xa, pt, hp, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
         }
       } else {  // Kramers pair: fragments (a re, a im, b re, b im) of even column 2j
         const int j = (nf0 / 4) * 8 + r8, col = 2 * j;
         if (col < P.n_p) {
           const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
-          put(xa, pt, col, ar, ai);
-          put(xb, pt, col, br, bi);
-          put(xa, pt, col + 1, -br, bi);  // -conj(Phi^b_2j)
-          put(xb, pt, col + 1, ar, -ai);  //  conj(Phi^a_2j)
+          put(xa, pt, hp, col, ar, ai);
+          put(xb, pt, hp, col, br, bi);
+          put(xa, pt, hp, col + 1, -br, bi);  // -conj(Phi^b_2j)
+          put(xb, pt, hp, col + 1, ar, -ai);  //  conj(Phi^a_2j)
         }
       }
     }
