@@ -15,11 +15,12 @@
 // warp filling a 2-stage ring (full/empty mbarriers, running ahead across tiles), 8 QB DMMA
 // warps, 3M complex products.
 //  * phase 1 (O, K = n_occ): warp w computes O~_e for e = w&1 over 4 Q x 4 P walkers and
-//    writes o = conj O~ into the CTA's shared o table (named barrier between the phases);
+//    writes o = conj O~ into the CTA's shared o table (named barriers of four warps between
+//    the phases);
 //  * phase 2 (V, K = n_vir): warp (wq, wp) owns 4 Q x 2 P walkers (12 accumulator tiles, 96
 //    registers), 16 DMMA warps per SM;
-//  * epilogue: the element-wise contraction is reduced with shuffles, and the per-pair scalar
-//    work (weights, products) runs on 8 lanes at once from a small smem table.
+//  * epilogue: the element-wise contraction is reduced with shuffles and the four f values of a
+//    pair meet in one lane by shuffles; the walker weights are already in Phi_v (mo_kernel).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -55,16 +56,15 @@ constexpr int HALF_PTS = 2 * WB;                      // P points per tile
 constexpr int QPTS = 2 * QW;                          // Q points per tile
 constexpr int STAGE_DOUBLES = (QPTS + HALF_PTS) * KC4 * 32;
 constexpr int SO_DOUBLES = 2 * QW * WB * 4 * 2 * 2;  // CTA o table [e][q][p][y][x_alpha] complex
-constexpr int SF_DOUBLES = 8 * 4;                     // per warp: 8 pairs x (f1d, f2x, f1x, f2d)
 #ifndef KR_OBUF
-#define KR_OBUF ((STAGES * STAGE_DOUBLES + 2 * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * MAX_RING * 8 <= 227 * 1024 ? 2 : 1)
+#define KR_OBUF ((STAGES * STAGE_DOUBLES + 2 * SO_DOUBLES) * 8 + 2 * MAX_RING * 8 <= 227 * 1024 ? 2 : 1)
 #endif
 // o tables: with two, tile t writes table t % 2 while no warp can still read it (every warp
 // passed tile t-1's "o table complete" barrier after its tile t-2 epilogue), so one CTA barrier
 // per tile suffices
 constexpr int OBUF = KR_OBUF;
 constexpr int SMEM_BYTES =
-    (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES + CONSUMERS * SF_DOUBLES) * 8 + 2 * MAX_RING * 8;
+    (STAGES * STAGE_DOUBLES + OBUF * SO_DOUBLES) * 8 + 2 * MAX_RING * 8;
 
 // The o table rows of Q walkers 4g..4g+3 are written in phase 1 by warps 4g..4g+3 (all (p1w, e1))
 // and read in phase 2 by the same four warps (wp = 0..3), so the phase switch synchronises
@@ -118,8 +118,7 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
-  double* const sF = sO0 + OBUF * SO_DOUBLES;
-  uint64_t* const full = reinterpret_cast<uint64_t*>(sF + CONSUMERS * SF_DOUBLES);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);
   uint64_t* const empty = full + MAX_RING;
   // ring of P.ring stages of P.ring_doubles each, sized on the host from the widest chunk:
   // the stage region holds STAGES widest stages, and more when every chunk is narrower
@@ -174,7 +173,6 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
     const int e1 = warp & 1, p1w = (warp >> 1) & 1, q1w = warp >> 2;
     // phase-2 role: 4 Q walkers (4 wq ..) x 2 P walkers (2 wp ..)
     const int wq = warp >> 2, wp = warp & 3;
-    double* const sf = sF + warp * SF_DOUBLES;
     const double cw = P.ng2 / P.st_ro->wtau;
     double acc_d = 0.0, acc_x = 0.0;
     int stage = 0;
@@ -282,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
       }
 
       // ---- epilogue: f = 2 Re sum_{x alpha, y} o v per (e_q, e_p), then real pair terms ----
-      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1, eq = (lane >> 3) & 1;
+      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -299,29 +297,26 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           }
           f += __shfl_xor_sync(0xffffffffu, f, 1);
           f += __shfl_xor_sync(0xffffffffu, f, 4);
-          // lanes hl*16 + (e_q << 3) + (e_p << 1) hold f(e_q, e_p) of pair (q, p)
-          if ((lane & 5) == 0) sf[((h * 2 + pp) * 2 + hl) * 4 + ((eq << 1) | ep)] = 2.0 * f;
+          f *= 2.0;
+          // lanes hl*16 + (e_q << 3) + (e_p << 1) hold f(e_q, e_p) of pair (q, p):
+          // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
+          const double f2d = __shfl_xor_sync(0xffffffffu, f, 10);
+          const double f1x = __shfl_xor_sync(0xffffffffu, f, 8);
+          const double f2x = __shfl_xor_sync(0xffffffffu, f, 2);
+          if ((lane & 15) == 0) {  // lanes 0, 16: pair (q, p) of this hl
+            const int qg = q0 + q, pg = p0 + p;
+            if (qg < P.m && pg < P.m && qg > pg) {
+              // estimator.cpp:32; the walker weights hinv_p hinv_q of inv_w (estimator.cpp:55) ride
+              // in the virtual Phi of the electron-1 points (mo_kernel), the constant
+              // N_g^2 / w(tau) is applied once per warp below
+              acc_d += (-P.w_direct * f) * f2d;
+              acc_x += (-P.w_exchange * f1x) * f2x;
+            }
+          }
         }
-      __syncwarp();
-      if (lane < 8) {  // one pair per lane: lane = (h, pp, hl)
-        const int h = lane >> 2, pp = (lane >> 1) & 1, hh = lane & 1;
-        const int q = q0 + 4 * wq + 2 * h + hh, p = p0 + 2 * wp + pp;
-        if (q < P.m && p < P.m && q > p) {
-          const double* F = sf + lane * 4;  // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
-          // estimator.cpp:32; the walker weights hinv_p hinv_q of inv_w (estimator.cpp:55) ride in
-          // the virtual Phi of the electron-1 points (mo_kernel), the constant N_g^2 / w(tau) is
-          // applied once per warp below
-          acc_d += (-P.w_direct * F[0]) * F[3];
-          acc_x += (-P.w_exchange * F[2]) * F[1];
-        }
-      }
-      __syncwarp();
     }
-#pragma unroll
-    for (int o = 4; o; o >>= 1) {  // fixed tree over lanes 0..7
-      acc_d += __shfl_down_sync(0xffffffffu, acc_d, o);
-      acc_x += __shfl_down_sync(0xffffffffu, acc_x, o);
-    }
+    acc_d += __shfl_down_sync(0xffffffffu, acc_d, 16);  // lanes 0 and 16 hold the sums
+    acc_x += __shfl_down_sync(0xffffffffu, acc_x, 16);
     if (lane == 0) {
       s_red[warp][0] = acc_d * cw;
       s_red[warp][1] = acc_x * cw;
