@@ -302,8 +302,15 @@ void build_groups(SpinorParams& sp, const mcmp2dev_system* s, const std::vector<
   std::vector<double> bfrag;
   long long chi_doubles = 0;
   sp.max_nf = 0;
+  // groups ordered by decreasing basis size: mo_kernel's blockIdx.z = group, so the longest
+  // tiles are dispatched first and the last wave holds the short ones
+  std::vector<int> order(sp.ngroups);
+  for (int g = 0; g < sp.ngroups; ++g) order[g] = g;
+  auto size_of = [&](int g) { const int x = kramers ? 2 * g : g; return ch_off[x + 1] - ch_off[x]; };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return size_of(a) > size_of(b); });
   for (int g = 0; g < sp.ngroups; ++g) {
-    const int xa = kramers ? 2 * g : g, xb = kramers ? 2 * g + 1 : -1;
+    const int src = order[g];
+    const int xa = kramers ? 2 * src : src, xb = kramers ? 2 * src + 1 : -1;
     const int nfn = ch_off[xa + 1] - ch_off[xa], k4n = (nfn + 3) / 4;
     int units = kramers ? (np / 2 + 7) / 8 : (np + 7) / 8;
     if (!kramers) units += units & 1;  // warps take 4 fragments
