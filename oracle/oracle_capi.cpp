@@ -198,6 +198,29 @@ int orc_trajectory(void* h, std::uint64_t seed, std::uint32_t stream, int m, lon
   });
 }
 
+// Metropolis-only chain (sampler.cpp:49-93): init_ensemble + burn_in(burn, adapt), then
+// nsteps sweeps; every `thin`-th sweep the electron separations |r1 - r2| of all walkers are
+// written to u_out (nsteps / thin x m). Returns the production acceptance in *acceptance.
+int orc_chain_r12(void* h, std::uint64_t seed, int m, long burn, long nsteps, long thin, double* u_out,
+                  double* acceptance) {
+  auto* s = static_cast<System*>(h);
+  return guard([&] {
+    WalkerEnsemble ens = init_ensemble(m, *s->spinors.nuclei, s->spec, seed, 0);
+    burn_in(ens, s->spec, burn, true);
+    long k = 0;
+    for (long st = 0; st < nsteps; ++st) {
+      metropolis_step(ens, s->spec);
+      if (st % thin != 0) continue;
+      for (int p = 0; p < m; ++p) {
+        const auto& w = ens.pairs[p];
+        const double dx = w.r1.x - w.r2.x, dy = w.r1.y - w.r2.y, dz = w.r1.z - w.r2.z;
+        u_out[k++] = std::sqrt(dx * dx + dy * dy + dz * dz);
+      }
+    }
+    *acceptance = double(ens.accepted) / double(ens.proposed);
+  });
+}
+
 // estimate at given positions (m x 8 per step) and tau: the replay oracle
 int orc_replay(void* h, int m, long nsteps, const double* walkers, const double* tau, int physical,
                double* est) {

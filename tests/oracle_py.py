@@ -113,6 +113,14 @@ class OracleSystem:
         check(lib().orc_replay(self.h, m, n, _d(walkers), _d(tau), int(physical), _d(est)))
         return est
 
+    def chain_r12(self, seed, m, burn, nsteps, thin):
+        """Metropolis-only chain: (|r1 - r2| samples every `thin` sweeps, production acceptance)."""
+        u = np.empty(((nsteps + thin - 1) // thin) * m)
+        acc = C.c_double()
+        check(lib().orc_chain_r12(self.h, C.c_uint64(seed), int(m), C.c_long(burn), C.c_long(nsteps),
+                                  C.c_long(thin), _d(u), C.byref(acc)))
+        return u, acc.value
+
     def replay_parallel(self, walkers, tau, threads):
         """One full-size replay step (m x 8 walkers), pair rows split over `threads` threads."""
         walkers = np.ascontiguousarray(walkers, dtype=np.float64)
