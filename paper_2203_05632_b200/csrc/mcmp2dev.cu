@@ -426,9 +426,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.nuniq = int(uz.size());
   sp.uniq_center = dupload(uc.data(), uc.size(), o);
   sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
-  h->kramers_eligible = kramers_paired(s, ch_off);
-  // the Kramers kernel implements the literal contraction only
-  h->kramers_eligible = h->kramers_eligible && h->estimator == MCMP2DEV_ESTIMATOR_LITERAL;
+  h->kramers_eligible = kramers_paired(s, ch_off);  // literal and physical epilogues both exist
   h->kramers = h->kramers_eligible;
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;

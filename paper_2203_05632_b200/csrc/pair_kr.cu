@@ -115,6 +115,7 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 }
 }  // namespace
 
+template <bool PHYS>
 __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
@@ -279,41 +280,129 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
         release();
       }
 
-      // ---- epilogue: f = 2 Re sum_{x alpha, y} o v per (e_q, e_p), then real pair terms ----
-      const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
+      if constexpr (PHYS) {
+        // ---- opt-in physical epilogue: -w_d Tr(o1 va) Tr(o2 vb), -w_x Tr(o1 vd o2 vc) ----
+        // Every block M here has the Kramers form M = [[A, B], [-conj B, conj A]] over (alpha | beta)
+        // channels with A[i][k] = M(alpha_i, alpha_k), B[i][k] = M(alpha_i, beta_k) (alpha_i = 2i,
+        // beta_i = 2i + 1), so MN has A = A_M A_N - B_M conj B_N, B = A_M B_N + B_M conj A_N and
+        // Tr(MN) = 2 Re sum_ik (A_M[i][k] A_N[k][i] - B_M[i][k] conj B_N[k][i]). The warp holds the
+        // alpha rows of V; lane bits: 0 = y / 2, 1 = e_p, 2 = x_alpha, 3 = e_q, 4 = hl, and
+        // register j = y % 2. The o table holds the alpha rows of o1 (e = 0) and o2 (e = 1).
+        const int yb = lane & 1, epl = (lane >> 1) & 1, xal = (lane >> 2) & 1, eql = (lane >> 3) & 1;
+        const int base = lane & 16;
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
-          double f = 0.0;
+          for (int pp = 0; pp < 2; ++pp) {
+            const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
+            double vr[2], vi[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int y = 2 * (lane & 1) + j;
-            const int idx = o_index(ep, q, p, y, xa);
-            const double vr = u1[h][pp][j] + u2[h][pp][j];
-            const double vi = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
-            f += sO[idx] * vr - sO[idx + 1] * vi;
-          }
-          f += __shfl_xor_sync(0xffffffffu, f, 1);
-          f += __shfl_xor_sync(0xffffffffu, f, 4);
-          f *= 2.0;
-          // lanes hl*16 + (e_q << 3) + (e_p << 1) hold f(e_q, e_p) of pair (q, p):
-          // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
-          const double f2d = __shfl_xor_sync(0xffffffffu, f, 10);
-          const double f1x = __shfl_xor_sync(0xffffffffu, f, 8);
-          const double f2x = __shfl_xor_sync(0xffffffffu, f, 2);
-          if ((lane & 15) == 0) {  // lanes 0, 16: pair (q, p) of this hl
-            const int qg = q0 + q, pg = p0 + p;
-            if (qg < P.m && pg < P.m && qg > pg) {
-              // estimator.cpp:32; the walker weights hinv_p hinv_q of inv_w (estimator.cpp:55) ride
-              // in the virtual Phi of the electron-1 points (mo_kernel), the constant
-              // N_g^2 / w(tau) is applied once per warp below
-              acc_d += (-P.w_direct * f) * f2d;
-              acc_x += (-P.w_exchange * f1x) * f2x;
+            for (int j = 0; j < 2; ++j) {
+              vr[j] = u1[h][pp][j] + u2[h][pp][j];
+              vi[j] = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+            }
+            auto o = [&](int e, int row, int col, double& re, double& im) {  // o_e(alpha_row, col)
+              const int idx = o_index(e, q, p, col, row);
+              re = sO[idx];
+              im = sO[idx + 1];
+            };
+            // direct traces: lanes of va (e_q = e_p = 0) and vb (1, 1) hold v(alpha_xal, 2 yb + j)
+            double tr = 0.0;
+            {
+              const int e = eql;
+              double ar, ai, br, bi;
+              o(e, yb, 2 * xal, ar, ai);      // A_o[yb][xal] against A_v[xal][yb] = v(alpha_xal, alpha_yb)
+              o(e, yb, 2 * xal + 1, br, bi);  // B_o[yb][xal] against conj B_v[xal][yb] = v(alpha_xal, beta_yb)
+              tr = (ar * vr[0] - ai * vi[0]) - (br * vr[1] + bi * vi[1]);
+            }
+            tr += __shfl_xor_sync(0xffffffffu, tr, 1);
+            tr += __shfl_xor_sync(0xffffffffu, tr, 4);
+            tr *= 2.0;                                            // lane base + 0: Tr(o1 va)
+            const double t2 = __shfl_xor_sync(0xffffffffu, tr, 10);  // lane base + 10: Tr(o2 vb)
+            // exchange: lane (i = xal, k2 = yb) forms A/B of (o1 vd)[i][k2] and (o2 vc)[k2][i]
+            const int i = xal, c2 = yb;
+            double dAr[2], dAi[2], dBr[2], dBi[2], cAr[2], cAi[2], cBr[2], cBi[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int sd = base | (k << 2) | 2 | c2;  // vd = V(e_q 0, e_p 1), column c2
+              const int sc = base | 8 | (k << 2) | i;   // vc = V(e_q 1, e_p 0), column i
+              dAr[k] = __shfl_sync(0xffffffffu, vr[0], sd);
+              dAi[k] = __shfl_sync(0xffffffffu, vi[0], sd);
+              dBr[k] = __shfl_sync(0xffffffffu, vr[1], sd);
+              dBi[k] = __shfl_sync(0xffffffffu, vi[1], sd);
+              cAr[k] = __shfl_sync(0xffffffffu, vr[0], sc);
+              cAi[k] = __shfl_sync(0xffffffffu, vi[0], sc);
+              cBr[k] = __shfl_sync(0xffffffffu, vr[1], sc);
+              cBi[k] = __shfl_sync(0xffffffffu, vi[1], sc);
+            }
+            double a1r = 0, a1i = 0, b1r = 0, b1i = 0, a2r = 0, a2i = 0, b2r = 0, b2i = 0;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              double oar, oai, obr, obi;
+              o(0, i, 2 * k, oar, oai);      // A_o1[i][k]
+              o(0, i, 2 * k + 1, obr, obi);  // B_o1[i][k]
+              // A1 += A_o1 A_vd - B_o1 conj B_vd; B1 += A_o1 B_vd + B_o1 conj A_vd
+              a1r += oar * dAr[k] - oai * dAi[k] - (obr * dBr[k] + obi * dBi[k]);
+              a1i += oar * dAi[k] + oai * dAr[k] - (obi * dBr[k] - obr * dBi[k]);
+              b1r += oar * dBr[k] - oai * dBi[k] + (obr * dAr[k] + obi * dAi[k]);
+              b1i += oar * dBi[k] + oai * dBr[k] + (obi * dAr[k] - obr * dAi[k]);
+              o(1, c2, 2 * k, oar, oai);      // A_o2[c2][k]
+              o(1, c2, 2 * k + 1, obr, obi);  // B_o2[c2][k]
+              a2r += oar * cAr[k] - oai * cAi[k] - (obr * cBr[k] + obi * cBi[k]);
+              a2i += oar * cAi[k] + oai * cAr[k] - (obi * cBr[k] - obr * cBi[k]);
+              b2r += oar * cBr[k] - oai * cBi[k] + (obr * cAr[k] + obi * cAi[k]);
+              b2i += oar * cBi[k] + oai * cBr[k] + (obi * cAr[k] - obr * cAi[k]);
+            }
+            // Re(A1 A2 - B1 conj B2)
+            double tx = (a1r * a2r - a1i * a2i) - (b1r * b2r + b1i * b2i);
+            tx += __shfl_xor_sync(0xffffffffu, tx, 1);
+            tx += __shfl_xor_sync(0xffffffffu, tx, 4);
+            tx *= 2.0;
+            if ((lane & 15) == 0) {
+              const int qg = q0 + q, pg = p0 + p;
+              if (qg < P.m && pg < P.m && qg > pg) {
+                acc_d += (-P.w_direct * tr) * t2;
+                acc_x += -P.w_exchange * tx;
+              }
             }
           }
-        }
+      } else {
+      // ---- epilogue: f = 2 Re sum_{x alpha, y} o v per (e_q, e_p), then real pair terms ----
+        const int xa = (lane >> 2) & 1, ep = (lane & 3) >> 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
+            double f = 0.0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int y = 2 * (lane & 1) + j;
+              const int idx = o_index(ep, q, p, y, xa);
+              const double vr = u1[h][pp][j] + u2[h][pp][j];
+              const double vi = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+              f += sO[idx] * vr - sO[idx + 1] * vi;
+            }
+            f += __shfl_xor_sync(0xffffffffu, f, 1);
+            f += __shfl_xor_sync(0xffffffffu, f, 4);
+            f *= 2.0;
+            // lanes hl*16 + (e_q << 3) + (e_p << 1) hold f(e_q, e_p) of pair (q, p):
+            // f1d = f(0,0), f2x = f(0,1), f1x = f(1,0), f2d = f(1,1)
+            const double f2d = __shfl_xor_sync(0xffffffffu, f, 10);
+            const double f1x = __shfl_xor_sync(0xffffffffu, f, 8);
+            const double f2x = __shfl_xor_sync(0xffffffffu, f, 2);
+            if ((lane & 15) == 0) {  // lanes 0, 16: pair (q, p) of this hl
+              const int qg = q0 + q, pg = p0 + p;
+              if (qg < P.m && pg < P.m && qg > pg) {
+                // estimator.cpp:32; the walker weights hinv_p hinv_q of inv_w (estimator.cpp:55) ride
+                // in the virtual Phi of the electron-1 points (mo_kernel), the constant
+                // N_g^2 / w(tau) is applied once per warp below
+                acc_d += (-P.w_direct * f) * f2d;
+                acc_x += (-P.w_exchange * f1x) * f2x;
+              }
+            }
+          }
+      }
     }
     acc_d += __shfl_down_sync(0xffffffffu, acc_d, 16);  // lanes 0 and 16 hold the sums
     acc_x += __shfl_down_sync(0xffffffffu, acc_x, 16);
@@ -373,7 +462,9 @@ cudaError_t pair_kr_kernel_setup() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_kr[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return cudaFuncSetAttribute(pair_kr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(pair_kr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(pair_kr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
 void launch_pair_kr(const PairParams& P, cudaStream_t s) {
@@ -381,7 +472,11 @@ void launch_pair_kr(const PairParams& P, cudaStream_t s) {
   cudaGetDevice(&dev);
   const int ntiles = kr_ntiles(P.nb);
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
-  pair_kr_kernel<<<ntiles < slots ? ntiles : slots, THREADS, SMEM_BYTES, s>>>(P);
+  const int grid = ntiles < slots ? ntiles : slots;
+  if (P.physical)
+    pair_kr_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(P);
+  else
+    pair_kr_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(P);
 }
 
 }  // namespace mcmp2dev

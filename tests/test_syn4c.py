@@ -49,17 +49,21 @@ def test_oracle_mc_converges_to_deterministic(syn4c_file, physical, target):
 def test_device_physical_replay_matches_oracle(syn4c_file, cfgdir):
     from paper_2203_05632_b200 import DeviceWalker, System
     cases = [(syn4c_file[0], "", 9), (cfgdir / "cfg2.spinor", (cfgdir / "cfg2.conf").read_text(), 12),
-             (cfgdir / "syn1c.spinor", "", 7)]
+             (cfgdir / "cfg4.spinor", (cfgdir / "cfg4.conf").read_text(), 40),
+             (cfgdir / "cfg5-2.spinor", (cfgdir / "cfg5-2.conf").read_text(), 24),
+             (cfgdir / "syn1c.spinor", "", 7), (cfgdir / "syn2c.spinor", "", 6)]
     for sp, conf, m in cases:
         o = oracle_py.OracleSystem(sp, conf)
         tr = o.trajectory(seed=5, stream=0, m=m, burn=30, nsteps=3, physical=True)
         dw = DeviceWalker(System(sp, conf + "estimator physical\n"), max_walkers=m)
-        assert not dw.kramers()  # the Kramers kernel is literal-only
-        got = dw.replay(tr["walkers"], tr["tau"])
+        assert dw.kramers() == (o.ncomp > 1)  # Kramers-paired 2c/4c sets take the pair_kr physical epilogue
         ref = tr["est"]
-        for k in (0, 2, 4):
-            assert np.max(np.abs(got[:, k] - ref[:, k]) / np.abs(ref[:, k])) < 1e-10
-        assert np.max(np.abs(got[:, 1] - ref[:, 1])) <= 1e-10 * np.max(np.abs(ref[:, 0]))
+        for mode in (1, 0):  # Kramers-restricted kernel (where eligible), then the general kernel
+            dw.kramers(mode)
+            got = dw.replay(tr["walkers"], tr["tau"])
+            for k in (0, 2, 4):
+                assert np.max(np.abs(got[:, k] - ref[:, k]) / np.abs(ref[:, k])) < 1e-10, (sp.name, mode, k)
+            assert np.max(np.abs(got[:, 1] - ref[:, 1])) <= 1e-10 * np.max(np.abs(ref[:, 0]))
 
 
 @pytest.mark.gpu
