@@ -49,7 +49,17 @@ constexpr int STAGES = KR_STAGES;  // ring depth at the widest chunk (KC4 groups
 constexpr int MAX_RING = 16;       // ring depth for narrow chunks: same bytes, more stages
 constexpr int QB = KR_QB;
 constexpr int QW = WB * QB;                           // Q walkers per tile
-constexpr int CONSUMERS = 8 * QB;
+#ifndef KR_PW
+// PW 4 (8 DMMA warps of 4 x 4 walkers, 9 warps so 168 registers, no spills): cfg4 3.967 ms vs
+// 3.961 for PW 2 (16 warps, 96 registers); cfg5-2 5.97 vs 5.08 ms
+#define KR_PW 2
+#endif
+constexpr int PW = KR_PW;                             // P walkers per phase-2 warp (2 or 4)
+constexpr int NPW = WB / PW;                          // phase-2 warps per Q group of 4 walkers
+constexpr int CONSUMERS = (QW / 4) * NPW;             // 4 Q walkers x PW P walkers per warp
+constexpr int P1W = CONSUMERS / ((QW / 4) * 2);       // phase-1 P splits (warp: q group, e, split)
+constexpr int NB1 = 2 / P1W;                          // phase-1 n fragments (4 P walkers) per warp
+constexpr int GW = CONSUMERS / (QW / 4);              // warps sharing one Q group's o rows
 constexpr int THREADS = 32 * (CONSUMERS + 1);
 constexpr int MINB = QB == 1 ? 2 : 1;                 // CTAs per SM
 constexpr int HALF_PTS = 2 * WB;                      // P points per tile
@@ -74,7 +84,7 @@ constexpr int SMEM_BYTES =
 #endif
 __device__ __forceinline__ void consumer_barrier(int group) {
   if (KR_GROUP_BARRIER)
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(32 * GW) : "memory");
   else
     asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory");
 }
@@ -170,10 +180,10 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   } else {
     const int hl = lane >> 4, l16 = lane & 15;
     const int xa_off = 8 * ((lane >> 2) & 1) + (lane & 3);  // alpha channel x = 0 or 2, k = lane & 3
-    // phase-1 role: electron e1, 4 Q walkers (4 q1w ..), 4 P walkers (4 p1w ..)
-    const int e1 = warp & 1, p1w = (warp >> 1) & 1, q1w = warp >> 2;
-    // phase-2 role: 4 Q walkers (4 wq ..) x 2 P walkers (2 wp ..)
-    const int wq = warp >> 2, wp = warp & 3;
+    // phase-1 role: electron e1, 4 Q walkers (4 q1w ..), 4 NB1 P walkers (4 NB1 p1w ..)
+    const int e1 = warp & 1, p1w = (warp >> 1) % P1W, q1w = warp / (2 * P1W);
+    // phase-2 role: 4 Q walkers (4 wq ..) x PW P walkers (PW wp ..)
+    const int wq = warp / NPW, wp = warp % NPW;
     const double cw = P.ng2 / P.st_ro->wtau;
     double acc_d = 0.0, acc_x = 0.0;
     int stage = 0;
@@ -199,9 +209,11 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
-        double t1[2][2], t2[2][2], t3[2][2];  // [h][j]
+        double t1[2][NB1][2], t2[2][NB1][2], t3[2][NB1][2];  // [h][n fragment][j]
 #pragma unroll
-        for (int h = 0; h < 2; ++h) t1[h][0] = t1[h][1] = t2[h][0] = t2[h][1] = t3[h][0] = t3[h][1] = 0.0;
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int n = 0; n < NB1; ++n) t1[h][n][0] = t1[h][n][1] = t2[h][n][0] = t2[h][n][1] = t3[h][n][0] = t3[h][n][1] = 0.0;
         for (int c = 0; c < cO; ++c) {
           const double* S = acquire();
           const int uc = ch.width(c);
@@ -211,15 +223,24 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
             auto at = [&](int ptl, int plane, int off) {
               return S[(ptl * uc + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
             };
-            const int pb = QPTS + 2 * (4 * p1w + (lane >> 3)) + e1;
-            const double br = at(pb, 0, xa_off), bi = at(pb, 1, xa_off), db = br - bi;
+            double br[NB1], bi[NB1], db[NB1];
+#pragma unroll
+            for (int n = 0; n < NB1; ++n) {
+              const int pb = QPTS + 2 * (4 * (NB1 * p1w + n) + (lane >> 3)) + e1;
+              br[n] = at(pb, 0, xa_off);
+              bi[n] = at(pb, 1, xa_off);
+              db[n] = br[n] - bi[n];
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int pa = 2 * (4 * q1w + 2 * h + hl) + e1;
-              const double ar = at(pa, 0, l16), ai = at(pa, 1, l16);
-              dmma(t1[h], ar, br);
-              dmma(t2[h], ai, bi);
-              dmma(t3[h], ar + ai, db);
+              const double ar = at(pa, 0, l16), ai = at(pa, 1, l16), sa = ar + ai;
+#pragma unroll
+              for (int n = 0; n < NB1; ++n) {
+                dmma(t1[h][n], ar, br[n]);
+                dmma(t2[h][n], ai, bi[n]);
+                dmma(t3[h][n], sa, db[n]);
+              }
             }
           }
           release();
@@ -229,20 +250,22 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int idx = o_index(e1, 4 * q1w + 2 * h + hl, 4 * p1w + pp, y, j);
-            sO[idx] = t1[h][j] + t2[h][j];                   // o = conj O~
-            sO[idx + 1] = -(t3[h][j] - t1[h][j] + t2[h][j]);
-          }
+          for (int n = 0; n < NB1; ++n)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int idx = o_index(e1, 4 * q1w + 2 * h + hl, 4 * (NB1 * p1w + n) + pp, y, j);
+              sO[idx] = t1[h][n][j] + t2[h][n][j];                   // o = conj O~
+              sO[idx + 1] = -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]);
+            }
         consumer_barrier(q1w);  // the group's o rows are complete
       }
 
       // ---- phase 2: V rows (q, e_q, x_alpha), cols (p, e_p, y) ----
-      double u1[2][2][2], u2[2][2][2], u3[2][2][2];  // [hq][pp][j]
+      double u1[2][PW][2], u2[2][PW][2], u3[2][PW][2];  // [hq][pp][j]
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < PW; ++j)
           u1[i][j][0] = u1[i][j][1] = u2[i][j][0] = u2[i][j][1] = u3[i][j][0] = u3[i][j][1] = 0.0;
       for (int c = cO; c < nchunks; ++c) {
         const double* S = acquire();
@@ -253,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
           auto at = [&](int ptl, int plane, int off) {
             return S[(ptl * uc + gg) * 32 + plane * 16 + (off ^ phi_swz(ptl))];
           };
-          double ar[2], ai[2], sa[2], br[2], bi[2], db[2];
+          double ar[2], ai[2], sa[2], br[PW], bi[PW], db[PW];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int pa = 2 * (4 * wq + 2 * h + hl) + ((lane >> 3) & 1);
@@ -262,8 +285,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
             sa[h] = ar[h] + ai[h];
           }
 #pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const int pb = QPTS + 2 * (2 * wp + pp) + hl;
+          for (int pp = 0; pp < PW; ++pp) {
+            const int pb = QPTS + 2 * (PW * wp + pp) + hl;
             br[pp] = at(pb, 0, l16);
             bi[pp] = at(pb, 1, l16);
             db[pp] = br[pp] - bi[pp];
@@ -271,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int pp = 0; pp < 2; ++pp) {
+            for (int pp = 0; pp < PW; ++pp) {
               dmma(u1[h][pp], ar[h], br[pp]);
               dmma(u2[h][pp], ai[h], bi[pp]);
               dmma(u3[h][pp], sa[h], db[pp]);
@@ -293,8 +316,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
+          for (int pp = 0; pp < PW; ++pp) {
+            const int q = 4 * wq + 2 * h + hl, p = PW * wp + pp;
             double vr[2], vi[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -372,8 +395,8 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const int q = 4 * wq + 2 * h + hl, p = 2 * wp + pp;
+          for (int pp = 0; pp < PW; ++pp) {
+            const int q = 4 * wq + 2 * h + hl, p = PW * wp + pp;
             double f = 0.0;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
