@@ -174,7 +174,7 @@ def test_overflow_during_advance_is_reported(cfgdir, tmp_path):
         dw.advance(2)
 
 
-@pytest.mark.parametrize("name,m", [("cfg3", 512), ("cfg4", 2048)])
+@pytest.mark.parametrize("name,m", [("cfg3", 512), ("cfg4", 2048), ("cfg5-2", 8192)])
 def test_full_size_replay_matches_oracle(cfgdir, name, m):
     """BASELINE sizes: one step of the device estimator at the full walker count (the bench's
     own configuration, every pair tile of the production launch) against the oracle's full
