@@ -240,7 +240,8 @@ int orc_replay(void* h, int m, long nsteps, const double* walkers, const double*
 // contiguous band of walker rows (bands balanced by pair count), partial results added in
 // band order: the full-size parity check (association differs from the sequential loop only
 // in the band split).
-int orc_replay_parallel(void* h, int m, const double* walkers, double tau, int threads, double* est) {
+int orc_replay_parallel(void* h, int m, const double* walkers, double tau, int threads, int physical,
+                        double* est) {
   auto* s = static_cast<System*>(h);
   return guard([&] {
     const WalkerEnsemble ens = from_walkers(walkers, m);
@@ -258,6 +259,7 @@ int orc_replay_parallel(void* h, int m, const double* walkers, double tau, int t
     for (int k = 0; k < threads; ++k)
       pool.emplace_back([&, k] {
         EstimatorWorkspace ws(s->spinors, m);
+        ws.physical = physical != 0;
         part[k] = mc_step_estimate_rows(s->spinors, ens, tau, s->spec, s->tau, ws, cut[k], cut[k + 1], nullptr);
       });
     for (auto& th : pool) th.join();

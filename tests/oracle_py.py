@@ -121,12 +121,12 @@ class OracleSystem:
                                   C.c_long(thin), _d(u), C.byref(acc)))
         return u, acc.value
 
-    def replay_parallel(self, walkers, tau, threads):
+    def replay_parallel(self, walkers, tau, threads, physical=False):
         """One full-size replay step (m x 8 walkers), pair rows split over `threads` threads."""
         walkers = np.ascontiguousarray(walkers, dtype=np.float64)
         est = np.empty(6)
         check(lib().orc_replay_parallel(self.h, walkers.shape[0], _d(walkers), C.c_double(tau), int(threads),
-                                        _d(est)))
+                                        int(physical), _d(est)))
         return est
 
     def sample_term(self, p, q, tau, physical=False):

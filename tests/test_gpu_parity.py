@@ -195,3 +195,27 @@ def test_full_size_replay_matches_oracle(cfgdir, name, m):
         assert abs(got[0] - ref[0]) <= REL * abs(ref[0])
         for k in (2, 4):
             assert abs(got[k] - ref[k]) <= REL * abs(ref[k])
+
+
+def test_full_size_physical_replay_matches_oracle(cfgdir):
+    """estimator physical at the cfg4 walker count: the Kramers physical epilogue (and the general
+    kernel) against the oracle's trace-form pair loop."""
+    import os
+
+    sp = cfgdir / "cfg4.spinor"
+    text = (cfgdir / "cfg4.conf").read_text() + "estimator physical\n"
+    orc = oracle_py.OracleSystem(sp, text)
+    m = 2048
+    dw = DeviceWalker(System(sp, text), max_walkers=m)
+    assert dw.kramers()
+    dw.init_ensemble(m, seed=6)
+    dw.burn_in(20)
+    dw.advance(1)
+    w = dw.get_ensemble().walkers[:, :8]
+    tau = 0.21
+    ref = orc.replay_parallel(w, tau, threads=max(1, min(32, os.cpu_count() or 1)), physical=True)
+    for mode in (1, 0):
+        dw.kramers(mode)
+        got = dw.replay(w[None], np.array([tau]))[0]
+        for k in (0, 2, 4):
+            assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), (mode, k)
