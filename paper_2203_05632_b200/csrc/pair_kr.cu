@@ -44,7 +44,10 @@ using namespace pairk;
 // 4.22; double-buffering within the 96-register cap (spills) 4.41; per-chunk branch-free
 // full-chunk path 4.15; 3 stages 4.14; epilogue hinv prefetched at tile start (spills) 4.07; no
 // producer warp, the last DMMA warp to release a stage refills it (16 warps, 109 registers) 4.58;
-// epilogue hinv fetched by cp.async into shared memory at tile start 4.06; this kernel 3.99.
+// epilogue hinv fetched by cp.async into shared memory at tile start 4.06; V-phase operand sums
+// (ar + ai, br - bi) formed once per stage by the producer warp into shared memory, KC4 6:
+// 9.7 (the one warp cannot keep up; removing the DADDs outright would be worth 4.7%); this
+// kernel 3.96.
 constexpr int STAGES = KR_STAGES;  // ring depth at the widest chunk (KC4 groups)
 constexpr int MAX_RING = 16;       // ring depth for narrow chunks: same bytes, more stages
 constexpr int QB = KR_QB;
