@@ -27,11 +27,13 @@ using pairk::dmma;
 constexpr int CHI_PTS = 8;
 constexpr int CHI_THREADS = 256;
 constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
+// k4 steps per cp.async stage and ring depth; measured cfg4 spinor stage (ms): (4, 3) 0.178,
+// (2, 4) 0.167, (2, 6) 0.170, (4, 2) 0.173, (1, 8) 0.169; cfg2 prefers (4, 3) by 1 us
 #ifndef MO_KS
-#define MO_KS 4
+#define MO_KS 2
 #endif
 #ifndef MO_STAGES
-#define MO_STAGES 3
+#define MO_STAGES 4
 #endif
 
 __device__ __forceinline__ double ipow(double x, int n) {
