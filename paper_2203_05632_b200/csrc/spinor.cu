@@ -25,7 +25,16 @@ namespace mcmp2dev {
 namespace {
 using pairk::dmma;
 constexpr int CHI_PTS = 8;
-constexpr int CHI_THREADS = 256;
+#ifndef CHI_THREADS_N
+// measured (cfg4 / cfg2 spinor stage, ms): 128 -> 0.185 / 0.032, 256 -> 0.168 / 0.028,
+// 512 -> 0.166 / 0.026 (the basis loops are latency-bound: more threads per 8 points)
+#define CHI_THREADS_N 512
+#endif
+constexpr int CHI_THREADS = CHI_THREADS_N;
+#ifndef CHI_UNROLL
+#define CHI_UNROLL 1
+#endif
+constexpr int kChiUnroll = CHI_UNROLL;
 constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
 // k4 steps per cp.async stage and ring depth; measured cfg4 spinor stage (ms): (4, 3) 0.178,
 // (2, 4) 0.167, (2, 6) 0.170, (4, 2) 0.173, (1, 8) 0.169; cfg2 prefers (4, 3) by 1 us
@@ -107,6 +116,7 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   for (int g = 0; g < P.ngroups; ++g) {
     const int f0 = P.grp_fn_off[g], nx = P.grp_nfn[g], k4n = P.grp_k4[g];
     double* A = P.chi + P.grp_chi_off[g] + size_t(pf) * k4n * 32;
+#pragma unroll kChiUnroll
     for (int i = tid; i < k4n * 32; i += CHI_THREADS) {
       const int k4 = i >> 5, l = i & 31, pt = l >> 2, mu = k4 * 4 + (l & 3);
       double v = 0.0;
