@@ -160,6 +160,23 @@ def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, qui
                       f"(fixed {t0:.2f} s/step + {c * 1e6:.2f} us/sample per worker)"}
 
 
+def interval_merge(vals, rank: int, dist):
+    """The checkpoint-interval merge of the multi-GPU driver (distributed.py): each rank's
+    (steps, mean, sigma_bar) summary is all-gathered (NCCL under torchrun) and merged by
+    step-count weighting (driver.cpp:183-196) -- the only collective of the walker loop."""
+    import numpy as np
+    from paper_2203_05632_b200.distributed import Summary, merge_estimates, torch_all_gather
+    nb = 100 if len(vals) >= 200 else max(1, len(vals) // 2)
+    k = len(vals) // nb
+    blocks = np.asarray(vals[: k * nb]).reshape(k, nb).mean(axis=1)
+    mean = float(np.mean(vals))
+    sb = float(np.sqrt(np.sum((blocks - mean) ** 2) / k) / np.sqrt(k)) if k > 0 else 0.0
+    mine = Summary(rank, len(vals), mean, sb, 0.0, 0.0, k)
+    parts = [Summary.from_array(a) for a in torch_all_gather(dist)(mine.as_array())] if dist else [mine]
+    value, sigma_bar, total = merge_estimates(sorted(parts, key=lambda s: s.index))
+    return {"E2": value, "sigma_bar": sigma_bar, "steps": total, "workers": len(parts)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -295,6 +312,7 @@ def main():
     dw.set_ensemble(st)                              # H2D walker state (resume)
     vals, ims = dw.advance(args.steps)               # every step's (value, imag) D2H
     st2 = dw.get_ensemble()                          # D2H walker state (checkpoint)
+    merged = interval_merge(vals, rank, dist)        # per-worker summaries -> one estimate (driver.cpp:183-196)
     e2e_s = time.perf_counter() - t0
     e2e_value = world * samples_per_step * args.steps / reduce_max(e2e_s)
     state_bytes = m * 9 * 8 + 64
@@ -330,7 +348,9 @@ def main():
                      "walk_ms_per_launch": prof["ms"]["walk"] / prof["launches"]["walk"],
                      "step_ms_profiled": step_ms_prof},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"},
+                "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"
+                        " + interval merge (all_gather of per-rank summaries, merge_estimates)",
+                "merged": merged},
         "gpu_launches": 4 * args.steps,  # walk_kernel, chi_kernel, mo_kernel, pair kernel per step
         "step_values_checksum": float(np.sum(vals)),
     }

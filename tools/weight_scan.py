@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20000)
     ap.add_argument("--burnin", type=int, default=1000)
     ap.add_argument("--grid", default="", help="semicolon list of 'f2 z1 z2'")
+    ap.add_argument("--rel", action="store_true",
+                    help="grid entries 'f2 a k' mean z1 = a x (smallest basis exponent), z2 = k x z1")
+    ap.add_argument("--seeds", default="11")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     rows = []
@@ -50,15 +53,18 @@ def main():
         cands = [("current", cur)]
         grid = args.grid or ";".join(f"{f2} {z1} {z2}" for z1 in (0.3, 1.0) for z2 in (3.0, 30.0, 300.0, 3000.0)
                                      for f2 in (0.1, 0.3, 0.6))
+        zmin = min(float(z) for z in re.findall(r"; 1 ; (\S+) 1", sp.read_text()))
         for g in grid.split(";"):
             f2, z1, z2 = map(float, g.split())
+            if args.rel:
+                z1, z2 = z1 * zmin, z2 * z1 * zmin
             c1, c2 = (1 - f2) * z1 ** 0.75, f2 * z2 ** 0.75
             cands.append((g, f"{c1:.6g} {z1:.6g} {c2:.6g} {z2:.6g}"))
-        for name, wl in cands:
+        for (name, wl), seed in [(c, s) for c in cands for s in map(int, args.seeds.split(","))]:
             t = re.sub(r"weight .*\n", f"weight {el} {wl}\n", text)
             t0 = time.perf_counter()
             dw = DeviceWalker(System(sp, t), max_walkers=m)
-            dw.init_ensemble(m, seed=11)
+            dw.init_ensemble(m, seed=seed)
             if "step-size" in t:
                 dw.burn_in(args.burnin, adapt=False)
             else:
@@ -72,7 +78,7 @@ def main():
             _, sb1, _ = blocking(v[:half])
             _, sb2, _ = blocking(v[half:])
             acc = (st2.accepted - st.accepted) / max(st2.proposed - st.proposed, 1)
-            row = {"cand": name, "weight": wl, "E2": mean, "sigma_bar": sb, "var_per_step": sb ** 2 * len(v),
+            row = {"cand": name, "seed": seed, "weight": wl, "E2": mean, "sigma_bar": sb, "var_per_step": sb ** 2 * len(v),
                    "sigma_bar_halves": [sb1, sb2], "acceptance": acc, "sigma_step": st.sigma_step,
                    "max_block_dev": float(np.max(np.abs(b - mean)) / (sb * np.sqrt(len(b)))),
                    "steps_to_1pct": (sb / (0.01 * abs(mean))) ** 2 * len(v), "seconds": time.perf_counter() - t0}
