@@ -304,6 +304,7 @@ def main():
 
     # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
     dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
+    import paper_2203_05632_b200.distributed  # noqa: F401  (module import is setup, not step time)
     st = dw.get_ensemble()
     torch.cuda.synchronize()
     if dist:

@@ -86,6 +86,8 @@ struct DevState {
   unsigned int done_ctas;     // last-CTA counters (walker kernel)
   unsigned int done_pair;     // (pair kernel)
   int spec_error_idx;         // overflow index from the speculative tau draw (INT_MAX: none)
+  unsigned int mo_next;       // mo_kernel tile counter (dynamic scheduling)
+  unsigned int mo_done;       // mo_kernel CTAs finished (the last one resets both)
 };
 
 }  // namespace mcmp2dev

@@ -51,6 +51,11 @@ struct SpinorParams {
   const double* sw;
   double* phi;
   double* hinv;              // [m] 1 / (g1 g2) per walker (chi_kernel), folded into Phi_v by mo_kernel
+  // mo_kernel tiles (64 points x 8 n fragments), numbered group-major: group g owns tiles
+  // [grp_tile0[g], grp_tile0[g] + ptiles * grp_nt[g]); handed out by the DevState counter
+  int grp_nt[4], grp_tile0[4];
+  int mo_ntiles, mo_slots;
+  DevState* st;
 };
 
 struct PairParams {
@@ -79,5 +84,6 @@ cudaError_t pair_kr_kernel_setup();
 double pair_kr_block_tiles(int nb);
 void pair_kr_ring(int max_width, int& ring, int& ring_doubles);  // stage ring for the widest chunk  // WB x WB walker blocks the Kramers launch computes
 cudaError_t spinor_kernel_setup();
+int mo_ctas_per_sm();
 
 }  // namespace mcmp2dev

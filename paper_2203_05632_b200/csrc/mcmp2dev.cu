@@ -324,9 +324,11 @@ void build_groups(SpinorParams& sp, const mcmp2dev_system* s, const std::vector<
     sp.grp_chi_off[g] = chi_doubles;
     sp.grp_b_off[g] = (long long)bfrag.size();
     sp.max_nf = std::max(sp.max_nf, nf);
+    sp.grp_nt[g] = (nf + 7) / 8;
     chi_doubles += (long long)ptf_max * k4n * 32;
     const size_t base = bfrag.size();
-    bfrag.resize(base + size_t(k4n) * nf * 32, 0.0);
+    // [nf / 8][k4][nf % 8][lane]: one k-slice of an 8-fragment n tile is contiguous
+    bfrag.resize(base + size_t(sp.grp_nt[g]) * k4n * 8 * 32, 0.0);
     for (int k4 = 0; k4 < k4n; ++k4)
       for (int f = 0; f < nf; ++f)
         for (int lane = 0; lane < 32; ++lane) {
@@ -341,7 +343,7 @@ void build_groups(SpinorParams& sp, const mcmp2dev_system* s, const std::vector<
             const int x = sub < 2 ? xa : xb, plane = sub & 1;
             if (col < np) v = s->coeff[2 * (size_t(ch_off[x] + mu) * np + col) + plane];
           }
-          bfrag[base + (size_t(k4) * nf + f) * 32 + lane] = v;
+          bfrag[base + ((size_t(f >> 3) * k4n + k4) * 8 + (f & 7)) * 32 + lane] = v;
         }
   }
   sp.bfrag = dupload(bfrag.data(), bfrag.size(), owned);
@@ -473,7 +475,13 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(cudaMemset(h->d_hinv, 0, sizeof(double) * h->npts_pad / 2), "memset hinv");
   sp.hinv = h->d_hinv;
   // MO-transform operands: basis groups, B fragments of C, A-fragment buffer for chi
-  const int ptf_max = (h->npts_pad + 63) / 64 * 8;  // point fragments, padded to the 64-point tile
+  const int ptf_max = (h->npts_pad + 255) / 256 * 32;  // point fragments, padded to any mo_kernel tile (<= 256 points)
+  {
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "SM count");
+    sp.mo_slots = sms * mo_ctas_per_sm();
+  }
+  sp.st = h->d_state;
   h->sp_kr = sp;
   build_groups(h->sp, s, ch_off, false, ptf_max, o);
   if (h->kramers_eligible) build_groups(h->sp_kr, s, ch_off, true, ptf_max, o);

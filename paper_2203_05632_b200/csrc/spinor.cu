@@ -7,10 +7,12 @@
 //              channel pair sharing one basis list), exp(-zeta |r-A|^2) once per unique
 //              (centre, zeta) and point, written in DMMA A-fragment order
 //              A_g[pt/8][mu/4][lane] (lane = (pt%8)*4 + mu%4).
-//  mo_kernel   Phi = chi C as a real x (re|im) DMMA GEMM (mma.sync m8n8k4 f64). B is the
-//              coefficient matrix pre-arranged at create time in B-fragment order, so both
-//              operands stream from L2 as coalesced 256-byte warp loads. The epilogue scales
-//              by sqrt(guarded_exp(+-eps tau)) and scatters into the pair kernel's Phi layout.
+//  mo_kernel   Phi = chi C as a real x (re|im) DMMA GEMM (mma.sync m8n8k4 f64): persistent
+//              CTAs, a producer warp streaming contiguous k-slices of A (chi) and B (the
+//              coefficients, pre-arranged at create time in B-fragment order) by cp.async.bulk
+//              into an mbarrier ring, tiles handed out longest-K first by an atomic counter.
+//              The epilogue scales by sqrt(guarded_exp(+-eps tau)) and scatters into the pair
+//              kernel's Phi layout.
 // On the Kramers path (exact time-reversal pairs, see pair_kr.cu) only the even columns are
 // transformed: for the partner column, Phi^{a}_{2j+1} = -conj Phi^{b}_{2j} and
 // Phi^{b}_{2j+1} = conj Phi^{a}_{2j} exactly (same products, negated), halving the GEMM.
@@ -35,15 +37,26 @@ constexpr int CHI_THREADS = CHI_THREADS_N;
 #define CHI_UNROLL 1
 #endif
 constexpr int kChiUnroll = CHI_UNROLL;
-constexpr int MO_THREADS = 128;  // 2x2 warps, warp tile 32 points x 4 n-fragments
-// k4 steps per cp.async stage and ring depth; measured cfg4 spinor stage (ms): (4, 3) 0.178,
-// (2, 4) 0.167, (2, 6) 0.170, (4, 2) 0.173, (1, 8) 0.169; cfg2 prefers (4, 3) by 1 us
+// k4 steps per ring stage, ring depth and CTAs per SM of mo_kernel. Measured (ms, spinor stage
+// = chi + mo, cfg4 / cfg3): this kernel (KS 4, 4 stages, 3 CTAs, 64-point tiles) 0.163 / 0.042;
+// (2, 6) 0.163 / 0.043; (8, 2) 0.168 / 0.042; 4 CTAs (96 registers, spills) 0.179-0.181;
+// 128-point tiles (8 DMMA warps) 0.177-0.184; 256-point tiles 0.201. ncu (cfg4): DMMA pipe 61% of
+// active cycles; the stall mix is dominated by the epilogue's wait for the last DMMAs of a tile.
+// The previous design (one 64x8 tile per CTA, cp.async ring + __syncthreads, 1408 CTAs) measured
+// (KS 4, 3 stages) 0.178, (2, 4) 0.165 / 0.038, (2, 6) 0.170, (4, 2) 0.173, (1, 8) 0.169
 #ifndef MO_KS
-#define MO_KS 2
+#define MO_KS 4
 #endif
 #ifndef MO_STAGES
 #define MO_STAGES 4
 #endif
+#ifndef MO_CTAS
+#define MO_CTAS 3
+#endif
+#ifndef MO_WP
+#define MO_WP 2  // consumer warps along the points of a tile (tile = 32 MO_WP points x 8 n fragments)
+#endif
+constexpr int MO_PTF = 4 * MO_WP;  // 8-point fragments per tile
 
 __device__ __forceinline__ double ipow(double x, int n) {
   // std::pow(x, n) for n in 0..3 (gaussian.cpp:87-92)
@@ -115,7 +128,9 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   __syncthreads();
   for (int g = 0; g < P.ngroups; ++g) {
     const int f0 = P.grp_fn_off[g], nx = P.grp_nfn[g], k4n = P.grp_k4[g];
-    double* A = P.chi + P.grp_chi_off[g] + size_t(pf) * k4n * 32;
+    // A fragments of a 64-point tile: [pf / 8][k4][pf % 8][lane], so one k-slice of a tile is
+    // contiguous (one bulk copy in mo_kernel)
+    double* A = P.chi + P.grp_chi_off[g] + (size_t(pf / MO_PTF) * k4n * MO_PTF + (pf % MO_PTF)) * 32;
 #pragma unroll kChiUnroll
     for (int i = tid; i < k4n * 32; i += CHI_THREADS) {
       const int k4 = i >> 5, l = i & 31, pt = l >> 2, mu = k4 * 4 + (l & 3);
@@ -133,149 +148,214 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
           v = ang * radial;
         }
       }
-      A[i] = v;
+      A[k4 * MO_PTF * 32 + l] = v;
     }
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
-  // 16-byte cp.async, zero-filled when !ok (src-size 0)
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(pairk::smem_u32(dst)), "l"(src),
-               "r"(ok ? 16 : 0)
-               : "memory");
+// MO transform: persistent, warp-specialised. Tile = 64 points (8 point fragments) x 8 n
+// fragments of one basis group; tiles are handed out longest-K first by an atomic counter
+// (dynamic list scheduling: an SM whose CTAs finish early takes more tiles, no static tail).
+// A producer warp streams the tile's k-slices (MO_KS k4 steps of A = chi and B = coefficient
+// fragments, each one contiguous cp.async.bulk) into a MO_STAGES ring with full/empty
+// mbarriers and runs ahead across tile boundaries; 4 DMMA warps (2 x 2, warp tile 32 points x
+// 4 n fragments) consume the ring and scatter the tile into Phi.
+constexpr int MO_CONSUMERS = 2 * MO_WP;
+constexpr int MO_THREADS = 32 * (MO_CONSUMERS + 1);
+constexpr int MO_ASLICE = MO_PTF * MO_KS * 32;  // doubles of A per stage
+constexpr int MO_BSLICE = 8 * MO_KS * 32;       // doubles of B per stage
+constexpr int MO_STAGE = MO_ASLICE + MO_BSLICE;
+constexpr int MO_SMEM = MO_STAGES * MO_STAGE * 8 + 2 * MO_STAGES * 8 + MO_STAGES * 8;
+
+__device__ __forceinline__ void mo_decode(const SpinorParams& P, int t, int& g, int& ptile, int& ntile) {
+  g = 0;
+  while (g + 1 < P.ngroups && t >= P.grp_tile0[g + 1]) ++g;
+  const int r = t - P.grp_tile0[g];
+  ptile = r / P.grp_nt[g];
+  ntile = r % P.grp_nt[g];
 }
 
-// Tile: 64 points (8 point fragments) x 8 n fragments of one basis group; 2x2 warps of 4 x 4
-// fragments. A (chi) and B (coefficients) k-slices of MO_KS k4 steps stream through a
-// MO_STAGES-deep cp.async ring in shared memory, so the DMMAs wait on shared memory, not on
-// L2 latency.
-using StageA = double[8][MO_KS][32];  // [ptf][k4][lane]
-using StageB = double[MO_KS][8][32];  // [k4][nf][lane]
-__device__ __forceinline__ void mo_tile(const SpinorParams& P, int g, int ptf_base, int nf_base, StageA* sA,
-                                        StageB* sB) {
-  const int k4n = P.grp_k4[g], nf_total = P.grp_nf[g];
+__global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P) {
+  extern __shared__ __align__(128) double mo_sm[];
+  uint64_t* const full = reinterpret_cast<uint64_t*>(mo_sm + MO_STAGES * MO_STAGE);
+  uint64_t* const empty = full + MO_STAGES;
+  int* const head = reinterpret_cast<int*>(empty + MO_STAGES);  // tile id per stage (-1: done)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ptf0 = ptf_base + (warp >> 1) * 4;  // 4 point fragments per warp
-  const int nf0 = nf_base + (warp & 1) * 4;     // 4 n fragments per warp (nf_total is a multiple of 4)
-  const bool active = nf0 < nf_total;
-  const double* A = P.chi + P.grp_chi_off[g];
-  const double* B = P.bfrag + P.grp_b_off[g];
-  const int nkb = (k4n + MO_KS - 1) / MO_KS;
-  auto load_stage = [&](int kb, int st) {
-#pragma unroll
-    for (int i = tid; i < 8 * MO_KS * 16; i += MO_THREADS) {  // A: 16-byte pieces
-      const int ptf = i / (MO_KS * 16), k = (i / 16) % MO_KS, c = i % 16;
-      const int k4 = kb * MO_KS + k;
-      const bool ok = k4 < k4n;
-      cp_async16(&sA[st][ptf][k][2 * c], A + (size_t(ptf_base + ptf) * k4n + (ok ? k4 : 0)) * 32 + 2 * c, ok);
+  const int ntiles = P.mo_ntiles;
+  if (tid == 0) {
+    for (int s = 0; s < MO_STAGES; ++s) {
+      pairk::mbar_init(&full[s], 1);
+      pairk::mbar_init(&empty[s], MO_CONSUMERS);
     }
-#pragma unroll
-    for (int i = tid; i < MO_KS * 8 * 16; i += MO_THREADS) {  // B
-      const int k = i / 128, f = (i / 16) % 8, c = i % 16;
-      const int k4 = kb * MO_KS + k, nf = nf_base + f;
-      const bool ok = k4 < k4n && nf < nf_total;
-      cp_async16(&sB[st][k][f][2 * c], B + (size_t(ok ? k4 : 0) * nf_total + (ok ? nf : 0)) * 32 + 2 * c, ok);
-    }
-  };
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
-#pragma unroll
-  for (int st = 0; st < MO_STAGES - 1; ++st) {
-    if (st < nkb) load_stage(st, st);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int kb = 0; kb < nkb; ++kb) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(MO_STAGES - 2) : "memory");
-    __syncthreads();  // stage kb landed for every thread; stage kb-1 is free
-    const int nk = kb + MO_STAGES - 1;
-    if (nk < nkb) load_stage(nk, nk % MO_STAGES);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    if (active) {
-      const int st = kb % MO_STAGES;
-#pragma unroll
-      for (int k = 0; k < MO_KS; ++k) {
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sA[st][(warp >> 1) * 4 + i][k][lane];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) b[f] = sB[st][k][(warp & 1) * 4 + f][lane];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int f = 0; f < 4; ++f) dmma(acc[i][f], a[i], b[f]);
+  __syncthreads();
+
+  if (warp == MO_CONSUMERS) {
+    if (lane == 0) {  // producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (;;) {
+        const int t = int(atomicAdd(&P.st->mo_next, 1u));
+        pairk::mbar_wait(&empty[stage], phase ^ 1u);
+        if (t >= ntiles) {
+          head[stage] = -1;
+          pairk::mbar_arrive(&full[stage]);
+          break;
+        }
+        int g, ptile, ntile;
+        mo_decode(P, t, g, ptile, ntile);
+        const int k4n = P.grp_k4[g];
+        const double* A = P.chi + P.grp_chi_off[g] + size_t(ptile) * k4n * MO_PTF * 32;
+        const double* B = P.bfrag + P.grp_b_off[g] + size_t(ntile) * k4n * 256;
+        for (int k0 = 0; k0 < k4n; k0 += MO_KS) {
+          if (k0) pairk::mbar_wait(&empty[stage], phase ^ 1u);
+          const int kk = min(MO_KS, k4n - k0);
+          head[stage] = t;
+          double* dst = mo_sm + stage * MO_STAGE;
+          const uint32_t abytes = uint32_t(kk) * MO_PTF * 256u, bbytes = uint32_t(kk) * 2048u;
+          pairk::mbar_expect_tx(&full[stage], abytes + bbytes);
+          pairk::bulk_g2s(dst, A + size_t(k0) * MO_PTF * 32, abytes, &full[stage]);
+          pairk::bulk_g2s(dst + MO_ASLICE, B + size_t(k0) * 256, bbytes, &full[stage]);
+          if (++stage == MO_STAGES) stage = 0, phase ^= 1u;
+        }
       }
     }
-  }
-  if (!active) return;
-  // epilogue: scale and scatter into Phi (layout in common.cuh)
-  const PhiChunks ch{P.Go, P.Gv};
-  // the walker weight hinv = 1 / (g1 g2) of inv_w (estimator.cpp:55) is folded into the virtual
-  // columns of electron-1 points: V(2q, 2p) then carries hinv_q hinv_p, V(2q+1, 2p) hinv_p and
-  // V(2q, 2p+1) hinv_q, so both the direct (va vb) and the exchange (vc vd) products of a pair
-  // carry exactly hinv_p hinv_q (chi_kernel wrote hinv this step)
-  auto put = [&](int x, int pt, double hp, int col, double re, double im) {
-    const bool occ = col < P.n_occ;
-    const double w = occ ? P.sw[col] : P.sw[col] * hp;
-    const int kidx = occ ? col : col - P.n_occ;
-    const int grp = occ ? (kidx >> 2) : P.Go + (kidx >> 2);
-    double* dst = P.phi + ch.offset(grp, pt, P.npts_pad) + ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
-    dst[0] = re * w;
-    dst[16] = im * w;
-  };
-  const int xa = P.grp_chan[2 * g], xb = P.grp_chan[2 * g + 1];
+  } else {
+    const int wp = warp >> 1, wn = warp & 1;  // warp tile: 4 point fragments x 4 n fragments
+    int stage = 0;
+    uint32_t phase = 0;
+    const PhiChunks ch{P.Go, P.Gv};
+    for (;;) {
+      pairk::mbar_wait(&full[stage], phase);
+      const int t = head[stage];
+      if (t < 0) break;
+      int g, ptile, ntile;
+      mo_decode(P, t, g, ptile, ntile);
+      const int k4n = P.grp_k4[g], nf_total = P.grp_nf[g];
+      const int nf0 = ntile * 8 + wn * 4;
+      const int xa = P.grp_chan[2 * g], xb = P.grp_chan[2 * g + 1];
+      // epilogue scale factors, loaded now so their latency hides behind the k loop:
+      // sqrt(guarded_exp) of this thread's columns (Kramers partners share the energy) and the
+      // walker weight hinv of its electron-1 points
+      double swc[2][2], hpv[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int pt = (ptf0 + i) * 8 + (lane >> 2);
-    if (pt >= P.npts) continue;
-    const double hp = (pt & 1) ? 1.0 : P.hinv[pt >> 1];
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      const int r8 = 2 * (lane & 3) + jj;
-      if (xb < 0) {  // general: two units of 8 columns, fragments (re, im)
+      for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
-          const int col = (nf0 / 2 + uu) * 8 + r8;
-          if (col < P.n_p) put(xa, pt, hp, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
+          const int r8 = 2 * (lane & 3) + jj;
+          const int col = xb < 0 ? (nf0 / 2 + uu) * 8 + r8 : 2 * ((nf0 / 4) * 8 + r8);
+          swc[jj][uu] = (nf0 < nf_total && col < P.n_p) ? P.sw[col] : 0.0;
         }
-      } else {  // Kramers pair: fragments (a re, a im, b re, b im) of even column 2j
-        const int j = (nf0 / 4) * 8 + r8, col = 2 * j;
-        if (col < P.n_p) {
-          const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
-          put(xa, pt, hp, col, ar, ai);
-          put(xb, pt, hp, col, br, bi);
-          put(xa, pt, hp, col + 1, -br, bi);  // -conj(Phi^b_2j)
-          put(xb, pt, hp, col + 1, ar, -ai);  //  conj(Phi^a_2j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pt = (ptile * MO_PTF + wp * 4 + i) * 8 + (lane >> 2);
+        hpv[i] = (pt < P.npts && !(pt & 1)) ? P.hinv[pt >> 1] : 1.0;
+      }
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) acc[i][f][0] = acc[i][f][1] = 0.0;
+      for (int k0 = 0; k0 < k4n; k0 += MO_KS) {
+        if (k0) pairk::mbar_wait(&full[stage], phase);
+        const double* sA = mo_sm + stage * MO_STAGE;
+        const double* sB = sA + MO_ASLICE;
+        const int kk = min(MO_KS, k4n - k0);
+#pragma unroll
+        for (int k = 0; k < MO_KS; ++k) {
+          if (k >= kk) break;
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = sA[(k * MO_PTF + wp * 4 + i) * 32 + lane];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) b[f] = sB[(k * 8 + wn * 4 + f) * 32 + lane];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) pairk::dmma(acc[i][f], a[i], b[f]);
+        }
+        __syncwarp();
+        if (lane == 0) pairk::mbar_arrive(&empty[stage]);
+        if (++stage == MO_STAGES) stage = 0, phase ^= 1u;
+      }
+      if (nf0 >= nf_total) continue;
+      // epilogue: scale and scatter into Phi (layout in common.cuh). The walker weight
+      // hinv = 1 / (g1 g2) of inv_w (estimator.cpp:55) is folded into the virtual columns of
+      // electron-1 points: V(2q, 2p) then carries hinv_q hinv_p, V(2q+1, 2p) hinv_p and
+      // V(2q, 2p+1) hinv_q, so both the direct (va vb) and the exchange (vc vd) products of a
+      // pair carry exactly hinv_p hinv_q (chi_kernel wrote hinv this step)
+      auto put = [&](int x, int pt, double w, int col, double re, double im) {
+        const int kidx = col < P.n_occ ? col : col - P.n_occ;
+        const int grp = col < P.n_occ ? (kidx >> 2) : P.Go + (kidx >> 2);
+        double* dst = P.phi + ch.offset(grp, pt, P.npts_pad) + ((x * 4 + (kidx & 3)) ^ phi_swz(pt));
+        dst[0] = re * w;
+        dst[16] = im * w;
+      };
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pt = (ptile * MO_PTF + wp * 4 + i) * 8 + (lane >> 2);
+        if (pt >= P.npts) continue;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int r8 = 2 * (lane & 3) + jj;
+          if (xb < 0) {  // general: two units of 8 columns, fragments (re, im)
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+              const int col = (nf0 / 2 + uu) * 8 + r8;
+              const double w = col < P.n_occ ? swc[jj][uu] : swc[jj][uu] * hpv[i];
+              if (col < P.n_p) put(xa, pt, w, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
+            }
+          } else {  // Kramers pair: fragments (a re, a im, b re, b im) of even column 2j
+            const int j = (nf0 / 4) * 8 + r8, col = 2 * j;
+            if (col < P.n_p) {
+              const double w = col < P.n_occ ? swc[jj][0] : swc[jj][0] * hpv[i];
+              const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
+              put(xa, pt, w, col, ar, ai);
+              put(xb, pt, w, col, br, bi);
+              put(xa, pt, w, col + 1, -br, bi);  // -conj(Phi^b_2j)
+              put(xb, pt, w, col + 1, ar, -ai);  //  conj(Phi^a_2j)
+            }
+          }
         }
       }
     }
   }
-}
-
-// One tile per CTA (measured faster than persistent CTAs walking the tiles largest-K first:
-// cfg4 spinor stage 0.172 vs 0.186 ms).
-__global__ void __launch_bounds__(MO_THREADS) mo_kernel(SpinorParams P) {
-  __shared__ __align__(128) StageA sA[MO_STAGES];
-  __shared__ __align__(128) StageB sB[MO_STAGES];
-  const int g = blockIdx.z, nf_base = blockIdx.y * 8;
-  if (nf_base >= P.grp_nf[g]) return;  // uniform over the CTA
-  mo_tile(P, g, blockIdx.x * 8, nf_base, sA, sB);
+  // the last CTA out resets the tile counter for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&P.st->mo_done, 1u) == gridDim.x - 1) {
+      P.st->mo_next = 0;
+      P.st->mo_done = 0;
+    }
+  }
 }
 
 int spinor_smem_bytes(const SpinorParams& P) { return int(sizeof(double)) * (3 * CHI_PTS + P.nuniq * CHI_PTS); }
 
 cudaError_t spinor_kernel_setup() {
-  return cudaFuncSetAttribute(chi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(chi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(mo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MO_SMEM);
 }
 
 void launch_spinor(const SpinorParams& P, cudaStream_t s) {
   const int ptf = (P.npts + CHI_PTS - 1) / CHI_PTS;
   chi_kernel<<<ptf, CHI_THREADS, spinor_smem_bytes(P), s>>>(P);
-  const int mtiles = (P.npts + 63) / 64;
-  dim3 grid(mtiles, (P.max_nf + 7) / 8, P.ngroups);
-  mo_kernel<<<grid, MO_THREADS, 0, s>>>(P);
+  SpinorParams q = P;
+  const int ptiles = (P.npts + 8 * MO_PTF - 1) / (8 * MO_PTF);  // tiles are numbered group-major, so the tile range of
+  int total = 0;                            // this launch's point count is recomputed here
+  for (int g = 0; g < P.ngroups; ++g) {
+    q.grp_tile0[g] = total;
+    total += ptiles * P.grp_nt[g];
+  }
+  q.mo_ntiles = total;
+  int grid = P.mo_slots;
+  if (grid > total) grid = total;
+  mo_kernel<<<grid, MO_THREADS, MO_SMEM, s>>>(q);
 }
+
+int mo_ctas_per_sm() { return MO_CTAS; }
 
 }  // namespace mcmp2dev
