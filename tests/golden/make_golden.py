@@ -69,15 +69,22 @@ def main():
     from paper_2203_05632_b200 import generate_config
     from paper_2203_05632_b200 import native
     with tempfile.TemporaryDirectory() as d:
-        for name, m, burn, nsteps, step in [("cfg1", 16, 50, 12, 0.3), ("syn1c", 6, 50, 12, 0.0),
-                                            ("syn2c", 5, 50, 12, 0.0), ("cfg2", 12, 30, 3, 0.0)]:
+        # (fixture, generator config, walkers, burn-in, steps, step size, estimator)
+        for tag, name, m, burn, nsteps, step, phys in [
+                ("cfg1", "cfg1", 16, 50, 12, 0.3, False), ("syn1c", "syn1c", 6, 50, 12, 0.0, False),
+                ("syn2c", "syn2c", 5, 50, 12, 0.0, False), ("cfg2", "cfg2", 12, 30, 3, 0.0, False),
+                ("cfg3", "cfg3", 10, 20, 2, 0.0, False), ("cfg4", "cfg4", 6, 10, 1, 0.0, False),
+                ("cfg2_physical", "cfg2", 12, 30, 3, 0.0, True)]:
             sp, conf = generate_config(name, d)
             raw = sp.read_bytes()
             fnv = native.host().mcmp2h_fnv1a64(raw, len(raw))
-            orc = oracle_py.OracleSystem(sp, conf.read_text())
-            tr = orc.trajectory(seed=3, stream=0, m=m, burn=burn, nsteps=nsteps, step_size=step, adapt=step == 0.0)
-            np.savez_compressed(HERE / f"replay_{name}.npz", walkers=tr["walkers"], tau=tr["tau"], est=tr["est"],
-                                init=tr["init"], spinor_fnv1a=np.uint64(fnv), m=m, step_size=step)
+            text = conf.read_text() + ("estimator physical\n" if phys else "")
+            orc = oracle_py.OracleSystem(sp, text)
+            tr = orc.trajectory(seed=3, stream=0, m=m, burn=burn, nsteps=nsteps, step_size=step, adapt=step == 0.0,
+                                physical=phys)
+            np.savez_compressed(HERE / f"replay_{tag}.npz", walkers=tr["walkers"], tau=tr["tau"], est=tr["est"],
+                                init=tr["init"], spinor_fnv1a=np.uint64(fnv), m=m, step_size=step,
+                                config=name, physical=phys)
     print("wrote", sorted(p.name for p in HERE.iterdir()))
 
 

@@ -123,16 +123,19 @@ def test_trajectory_matches_oracle(cfgdir, name, m, nsteps, step):
     assert np.max(np.abs(fin.walkers - ref["walkers"]) / (np.abs(ref["walkers"]) + 1e-300)) < 1e-10
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "syn1c", "syn2c"])
-def test_golden_fixtures(cfgdir, name):
-    """Committed oracle dumps (tests/golden/make_golden.py): replay and the advanced chain."""
+@pytest.mark.parametrize("tag", ["cfg1", "cfg2", "syn1c", "syn2c", "cfg3", "cfg4", "cfg2_physical"])
+def test_golden_fixtures(cfgdir, tag):
+    """Committed oracle dumps (tests/golden/make_golden.py): replay and the advanced chain, for
+    both estimators (the physical one on cfg2)."""
     from pathlib import Path
     from paper_2203_05632_b200 import native
-    g = np.load(Path(__file__).resolve().parent / "golden" / f"replay_{name}.npz")
+    g = np.load(Path(__file__).resolve().parent / "golden" / f"replay_{tag}.npz")
+    name = str(g["config"]) if "config" in g else tag
     raw = (cfgdir / f"{name}.spinor").read_bytes()
     assert native.host().mcmp2h_fnv1a64(raw, len(raw)) == int(g["spinor_fnv1a"]), "generator drifted"
     m = int(g["m"])
-    dw = DeviceWalker(System(cfgdir / f"{name}.spinor", (cfgdir / f"{name}.conf").read_text()), max_walkers=m)
+    text = (cfgdir / f"{name}.conf").read_text() + ("estimator physical\n" if "physical" in g and bool(g["physical"]) else "")
+    dw = DeviceWalker(System(cfgdir / f"{name}.spinor", text), max_walkers=m)
     got = dw.replay(g["walkers"], g["tau"])
     assert rel_err(got[:, 0], g["est"][:, 0]) < REL
     dw.set_ensemble(EnsembleState(**oracle_py.state_to_ensemble(g["init"], m)))
