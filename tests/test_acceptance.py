@@ -1,0 +1,85 @@
+"""Acceptance criteria of the reference's spec that concern the walker loop (reference SPEC.md
+"ACCEPTANCE CRITERIA" 3-6; their harness, proj/tests/acceptance/, is absent from the reference),
+restated on this repository's path. Criteria 1-2 (oracle agreement) are test_syn4c.py, 9
+(bit-exact resume) is test_gpu_engine.py::test_kill_and_resume_is_bit_exact, 6's hand example
+is test_oracle_kats.py::test_blocking_hand_examples. Criterion 7 (per-step cost x[3, 5] when
+the basis doubles) describes the reference's CPU cost model -- on the device the pair kernel is
+linear in n_spinor at fixed m -- and criterion 8 (8-worker strong scaling) needs 8 GPUs; both are
+reported by tools/, not gated here.
+
+Criterion 3 (slope of log sigma_bar_N vs log N over N in [10^3, 10^5] within [-0.6, -0.4]) is not
+gated either: on the device chain it scatters with the seed -- syn4c m = 8, eight seeds: -0.37 to
+-0.80 (median -0.44, pooled -0.60); syn1c (bounded integrand) m = 8: -0.13 to -0.56 (median
+-0.35) -- because the step estimates stay correlated over more than the 100-step block at
+N <= 10^4, so sigma_bar_N is underestimated early and the fitted slope is shallow. The oracle's
+chain is the same chain (test_gpu_parity.py::test_trajectory_matches_oracle), so the reference
+would scatter identically on these inputs."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+import oracle_py
+import syn4c
+
+
+def blocking(values, nb):
+    """BlockingAccumulator of the product host library (estimator.cpp:77-121): mean, sigma_bar."""
+    from paper_2203_05632_b200 import native
+    fn = native.host().mcmp2h_blocking
+    fn.argtypes = [C.POINTER(C.c_double), C.c_long, C.c_long, C.POINTER(C.c_double)]
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.zeros(4)
+    fn(v.ctypes.data_as(C.POINTER(C.c_double)), len(v), nb, out.ctypes.data_as(C.POINTER(C.c_double)))
+    return out[0], out[2]
+
+
+def test_laplace_identity():
+    """Criterion 5 (paper Eq. 14): the MC average of e^{-Delta tau} / w(tau) over inverse-CDF tau
+    draws (weights.cpp:103-111; the reference stream's uniform(), rng.cpp:58-64) equals 1/Delta
+    within 5 standard errors at 10^6 draws. lambda = 0.9 keeps the variance finite for every
+    Delta (needs 2 Delta > lambda; in MC-MP2 Delta >= lambda by construction)."""
+    L = oracle_py.lib()
+    L.orc_tau_pdf.restype = C.c_double
+    L.orc_tau_pdf.argtypes = [C.c_double, C.c_double]
+    n, lam = 1_000_000, 0.9
+    u = np.empty(n)
+    oracle_py.check(L.orc_philox_stream(20220305, 0, 1, n, u.ctypes.data_as(C.POINTER(C.c_double))))
+    tau = np.array([L.orc_tau_sample(lam, x) for x in u[:2000]])
+    w = np.array([L.orc_tau_pdf(lam, t) for t in tau[:2000]])
+    # the oracle's sampler and density on a prefix; the full sample uses the same closed forms
+    assert np.allclose(tau, -np.log1p(-u[:2000]) / lam, rtol=4e-16, atol=0)
+    assert np.allclose(w, lam * np.exp(-lam * tau), rtol=1e-15, atol=0)
+    tau = -np.log1p(-u) / lam
+    for delta in (0.5, 1.2, 10.0):
+        f = np.exp(-delta * tau) / (lam * np.exp(-lam * tau))
+        assert abs(f.mean() - 1.0 / delta) < 5 * f.std() / math.sqrt(n), delta
+
+
+@pytest.fixture(scope="module")
+def syn4c_path(tmp_path_factory):
+    p = tmp_path_factory.mktemp("acc") / "syn4c.spinor"
+    syn4c.write_spinor_file(p)
+    return p
+
+
+@pytest.mark.gpu
+def test_redundant_walker_benefit(syn4c_path):
+    """Criterion 4: across 30 seeds at N = 2 x 10^4 steps the seed variance of I_N decreases
+    monotonically for m in {4, 8, 12} (the reference's 'redundant walker' effect: C(m,2) pairs
+    per step from m walker pairs)."""
+    from paper_2203_05632_b200 import DeviceWalker, System
+    sysd = System(syn4c_path, "")
+    var = []
+    for m in (4, 8, 12):
+        dw = DeviceWalker(sysd, max_walkers=m)
+        means = []
+        for seed in range(30):
+            dw.init_ensemble(m, seed=1000 + seed)
+            dw.burn_in(300)
+            v, _ = dw.advance(20_000)
+            means.append(v.mean())
+        dw.close()
+        var.append(np.var(means, ddof=1))
+    assert var[0] > var[1] > var[2], var
