@@ -22,6 +22,9 @@ struct WalkParams {
   int n_occ, n_vir;
   double* sw;          // [n_occ + n_vir] sqrt(guarded_exp) weights of this step
   int* block_acc;      // per-CTA accept counts
+  int nens;            // > 1: batched ensembles (walk_batch_kernel), m walkers each, st[nens]
+  int sw_stride;       // doubles between the ensembles' spinor weight vectors
+  int nactive;         // batched production sweep: ensembles >= nactive (if > 0) stay as they are
 };
 
 // spinor evaluation + MO transform (model.cpp:55-64, :166-178) into the Phi layout
@@ -56,6 +59,8 @@ struct SpinorParams {
   int grp_nt[4], grp_tile0[4];
   int mo_ntiles, mo_slots;
   DevState* st;
+  int ens_pts;               // > 0: batched ensembles of ens_pts points, spinor weights sw + e * sw_stride
+  int sw_stride;
 };
 
 struct PairParams {
@@ -68,8 +73,9 @@ struct PairParams {
   DevState* st;
   double ng2, w_direct, w_exchange;
   int physical;              // 1: Tr(o1 va) Tr(o2 vb), Tr(o1 vd o2 vc) epilogue (opt-in)
-  double* partials;          // [ntiles][4]
-  double* step_out;          // [6] of this step
+  double* partials;          // [ntiles][4]; batched: [nens * ens_tiles][consumer warps][2]
+  double* step_out;          // [6] of this step; batched: [nens][6]
+  int nens, ens_tiles;       // batched ensembles (pair_kr only): m walkers each, st_ro[nens]
 };
 
 void launch_walk(const WalkParams& P, cudaStream_t s);
@@ -82,6 +88,8 @@ cudaError_t pair_kernel_setup();
 void launch_pair_kr(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kr_kernel_setup();
 double pair_kr_block_tiles(int nb);
+int pair_kr_tiles(int nb);      // tiles of one ensemble of nb walker blocks
+int pair_kr_consumers();        // DMMA warps per pair_kr CTA (per-tile partials in batched mode)
 void pair_kr_ring(int max_width, int& ring, int& ring_doubles);  // stage ring for the widest chunk  // WB x WB walker blocks the Kramers launch computes
 cudaError_t spinor_kernel_setup();
 int mo_ctas_per_sm();

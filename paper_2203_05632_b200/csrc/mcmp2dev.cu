@@ -93,7 +93,13 @@ struct mcmp2dev_handle {
   bool have_ensemble = false;
   WalkerBuf buf[2]{}, rbuf{};
   int cur = 0;
-  DevState* d_state = nullptr;
+  DevState* d_state = nullptr;  // [nens_cap]: ensemble e of a batched handle uses d_state[e]
+  int nens = 1, nens_cap = 1;   // batched ensembles (mcmp2dev_init_batch): walkers [e m, (e+1) m)
+  double* d_bpart = nullptr;    // batched: per-tile pair partials
+  size_t bpart_cap = 0;
+  double* d_bsteps = nullptr;   // batched: [kGraphSteps][nens][6] step results
+  double* h_bsteps = nullptr;   // pinned
+  size_t bsteps_cap = 0;
   int* d_block_acc = nullptr;
   double* d_phi = nullptr;
   double* d_hinv = nullptr;
@@ -114,13 +120,13 @@ struct mcmp2dev_handle {
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   double* d_gsteps = nullptr;  // [kGraphSteps][6] step results written by the graph
   struct GraphKey {
-    int m = -1, kramers = -1;
+    int m = -1, kramers = -1, nens = 1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
     bool operator==(const GraphKey&) const = default;
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, k0, k1, rstream};
+    const GraphKey key{m, kramers ? 1 : 0, nens, k0, k1, rstream};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -130,7 +136,8 @@ struct mcmp2dev_handle {
     for (int s = 0; s < kGraphSteps; ++s) {  // even count: the walker parity returns to c0
       launch_walk(walk_params(WALK_PRODUCTION, 0, 0), stream);
       cur ^= 1;
-      launch_estimate(buf[cur], m, d_gsteps + 6 * s);
+      if (nens > 1) launch_estimate(buf[cur], m, d_bsteps + size_t(6) * nens * s, nens);
+      else launch_estimate(buf[cur], m, d_gsteps + 6 * s);
     }
     cur = c0;
     ck(cudaStreamEndCapture(stream, &g), "graph capture end");
@@ -160,12 +167,18 @@ struct mcmp2dev_handle {
     P.n_vir = n_vir;
     P.sw = d_sw;
     P.block_acc = d_block_acc;
+    P.nens = nens;
+    P.sw_stride = n_p;
     return P;
   }
 
-  void launch_estimate(const WalkerBuf& wb, int mm, double* step_out) {
+  void launch_estimate(const WalkerBuf& wb, int mm, double* step_out, int ne = 1) {
+    if (ne > 1 && !kramers)
+      throw ArgError("batched ensembles need the Kramers pair kernel (Kramers-paired spinor set, path on)");
     SpinorParams s = kramers ? sp_kr : sp;
-    s.npts = 2 * mm;
+    s.npts = 2 * mm * ne;
+    s.ens_pts = ne > 1 ? 2 * mm : 0;
+    s.sw_stride = n_p;
     s.walkers = wb;
     if (prof) ck(cudaEventRecord(ev[1], stream), "event");
     launch_spinor(s, stream);
@@ -188,8 +201,10 @@ struct mcmp2dev_handle {
     p.w_direct = w_direct;
     p.w_exchange = w_exchange;
     p.physical = estimator == MCMP2DEV_ESTIMATOR_PHYSICAL;
-    p.partials = d_partials;
+    p.partials = ne > 1 ? d_bpart : d_partials;
     p.step_out = step_out;
+    p.nens = ne;
+    p.ens_tiles = ne > 1 ? pair_kr_tiles(p.nb) : 0;
     if (kramers) launch_pair_kr(p, stream);
     else launch_pair(p, stream);
     if (prof) {
@@ -212,9 +227,12 @@ struct mcmp2dev_handle {
   }
 
   void check_state_errors() {
-    DevState st;
-    ck(cudaMemcpyAsync(&st, d_state, sizeof st, cudaMemcpyDeviceToHost, stream), "state D2H");
+    std::vector<DevState> all(nens);
+    ck(cudaMemcpyAsync(all.data(), d_state, sizeof(DevState) * nens, cudaMemcpyDeviceToHost, stream), "state D2H");
     ck(cudaStreamSynchronize(stream), "stream sync");
+    DevState st = all[0];
+    for (const DevState& x : all)
+      if (x.error && (!st.error || x.error_idx < st.error_idx)) st = x;
     if (st.error) {
       reset_errors();
       // greens.cpp:10-13
@@ -224,12 +242,23 @@ struct mcmp2dev_handle {
   }
 
   void reset_errors() {
-    DevState st;
-    ck(scopy(stream, &st, d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
-    st.error = 0;
-    st.error_idx = INT_MAX;
-    st.spec_error_idx = INT_MAX;
-    ck(scopy(stream, d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    std::vector<DevState> all(nens);
+    ck(scopy(stream, all.data(), d_state, sizeof(DevState) * nens, cudaMemcpyDeviceToHost), "state D2H");
+    for (DevState& st : all) {
+      st.error = 0;
+      st.error_idx = INT_MAX;
+      st.spec_error_idx = INT_MAX;
+    }
+    ck(scopy(stream, d_state, all.data(), sizeof(DevState) * nens, cudaMemcpyHostToDevice), "state H2D");
+  }
+
+  // read-modify-write of every ensemble's DevState
+  template <class F>
+  void each_state(F&& f) {
+    std::vector<DevState> all(nens);
+    ck(scopy(stream, all.data(), d_state, sizeof(DevState) * nens, cudaMemcpyDeviceToHost), "state D2H");
+    for (DevState& st : all) f(st);
+    ck(scopy(stream, d_state, all.data(), sizeof(DevState) * nens, cudaMemcpyHostToDevice), "state H2D");
   }
 };
 
@@ -439,7 +468,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.Go = h->Go;
   sp.Gv = h->Gv;
   h->d_energies = dupload(s->energies, size_t(h->n_p), o);
-  h->d_sw = dalloc<double>(h->n_p, o);
+  h->nens_cap = std::max(1, max_walkers / 16);  // batched ensembles hold >= 16 walkers each
+  h->d_sw = dalloc<double>(size_t(h->n_p) * h->nens_cap, o);
   sp.sw = h->d_sw;
 
   h->sites.n = s->nsites;
@@ -459,7 +489,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   h->rbuf.mmax = h->nbmax * WB;
   h->rbuf.w = dalloc<double>(size_t(9) * h->rbuf.mmax, o);
   ck(cudaMemset(h->rbuf.w, 0, sizeof(double) * 9 * h->rbuf.mmax), "memset");
-  h->d_state = dalloc<DevState>(1, o);
+  h->d_state = dalloc<DevState>(h->nens_cap, o);
+  ck(cudaMemset(h->d_state, 0, sizeof(DevState) * h->nens_cap), "memset state");
   DevState st{};
   st.sigma = 1.0;  // sampler.hpp:45
   st.error_idx = INT_MAX;
@@ -532,6 +563,9 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
   for (void* p : h->owned) cudaFree(p);
   if (h->h_steps) cudaFreeHost(h->h_steps);
   if (h->h_replay) cudaFreeHost(h->h_replay);
+  if (h->d_bpart) cudaFree(h->d_bpart);
+  if (h->d_bsteps) cudaFree(h->d_bsteps);
+  if (h->h_bsteps) cudaFreeHost(h->h_bsteps);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs)
@@ -546,6 +580,7 @@ int mcmp2dev_init_ensemble(mcmp2dev_t* h, int m, uint64_t seed, uint32_t stream)
     if (m < 2) throw ArgError("init_ensemble: at least two electron-pair walkers");
     if (m > h->mmax) throw ArgError("init_ensemble: more walkers than the handle was sized for");
     h->m = m;
+    h->nens = 1;
     h->k0 = uint32_t(seed);
     h->k1 = uint32_t(seed >> 32);
     h->rstream = stream;
@@ -564,30 +599,22 @@ int mcmp2dev_init_ensemble(mcmp2dev_t* h, int m, uint64_t seed, uint32_t stream)
 }
 
 int mcmp2dev_set_sigma_step(mcmp2dev_t* h, double sigma) {
-  return guard(h, [&] {
-    ck(cudaMemcpyAsync(reinterpret_cast<char*>(h->d_state) + offsetof(DevState, sigma), &sigma,
-                       sizeof sigma, cudaMemcpyHostToDevice, h->stream),
-       "sigma H2D");
-    ck(cudaStreamSynchronize(h->stream), "stream sync");
-  });
+  return guard(h, [&] { h->each_state([&](DevState& st) { st.sigma = sigma; }); });
 }
 
 int mcmp2dev_burn_in(mcmp2dev_t* h, long n_burn, int adapt) {
   return guard(h, [&] {
     require_ensemble(h);
-    DevState st;
-    ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
-    st.win_acc = st.win_prop = 0;
-    ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    h->each_state([](DevState& st) { st.win_acc = st.win_prop = 0; });
     for (long s = 1; s <= n_burn; ++s) {
       launch_walk(h->walk_params(WALK_BURN, s, adapt), h->stream);
       h->cur ^= 1;
     }
     ck(cudaGetLastError(), "walk launch");
-    ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
-    st.proposed = st.accepted = 0;  // sampler.cpp:92
-    st.win_acc = st.win_prop = 0;
-    ck(scopy(h->stream, h->d_state, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
+    h->each_state([](DevState& st) {
+      st.proposed = st.accepted = 0;  // sampler.cpp:92
+      st.win_acc = st.win_prop = 0;
+    });
   });
 }
 
@@ -606,6 +633,7 @@ int mcmp2dev_set_ensemble(mcmp2dev_t* h, const mcmp2dev_ensemble* e) {
       pos = 4 * (B - 1) + e->rng_idx;
     }
     h->m = e->m;
+    h->nens = 1;
     h->k0 = e->rng_key[0];
     h->k1 = e->rng_key[1];
     h->rstream = e->rng_counter[3];
@@ -630,6 +658,7 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e) {
   return guard(h, [&] {
     require_ensemble(h);
     if (!e || !e->walkers) throw ArgError("get_ensemble: null ensemble");
+    if (h->nens > 1) throw ArgError("get_ensemble: batched handle (use mcmp2dev_get_ensemble_at)");
     ck(cudaStreamSynchronize(h->stream), "stream sync");
     DevState st;
     ck(scopy(h->stream, &st, h->d_state, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
@@ -660,10 +689,48 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e) {
   });
 }
 
+namespace {
+// advance of a batched handle: chunks of kGraphSteps steps (one graph replay when possible),
+// results [nsteps][nens]
+void advance_batched(mcmp2dev_t* h, long nsteps, int nactive, double* values, double* imags) {
+  const int ne = h->nens;
+  for (long done = 0; done < nsteps;) {
+    const long n = std::min<long>(kGraphSteps, nsteps - done);
+    if (!h->prof && n == kGraphSteps && nactive == ne) {
+      ck(cudaGraphLaunch(h->ensure_graph(), h->stream), "cudaGraphLaunch");
+    } else {
+      for (long s = 0; s < n; ++s) {
+        if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
+        WalkParams P = h->walk_params(WALK_PRODUCTION, 0, 0);
+        P.nactive = nactive;
+        launch_walk(P, h->stream);
+        h->cur ^= 1;
+        h->launch_estimate(h->buf[h->cur], h->m, h->d_bsteps + size_t(6) * ne * s, ne);
+      }
+    }
+    if (values || imags)
+      ck(cudaMemcpyAsync(h->h_bsteps, h->d_bsteps, sizeof(double) * 6 * ne * n, cudaMemcpyDeviceToHost, h->stream),
+         "steps D2H");
+    h->check_state_errors();  // synchronises
+    for (long s = 0; s < n; ++s)
+      for (int e = 0; e < ne; ++e) {
+        const double* r = h->h_bsteps + (size_t(s) * ne + e) * 6;
+        if (values) values[size_t(done + s) * ne + e] = r[0];
+        if (imags) imags[size_t(done + s) * ne + e] = r[1];
+      }
+    done += n;
+  }
+}
+}  // namespace
+
 int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) {
   return guard(h, [&] {
     require_ensemble(h);
     if (nsteps < 0) throw ArgError("advance: negative step count");
+    if (h->nens > 1) {
+      advance_batched(h, nsteps, h->nens, values, imags);
+      return;
+    }
     long done = 0;
     const bool want = values || imags;
     while (done < nsteps) {
@@ -747,11 +814,11 @@ int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out) {
 
 int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes) {
   return guard(h, [&] {
-    const double m = h->m, nc = h->ncomp;
+    const double m = h->m, nc = h->ncomp, ne = h->nens;  // per step, all ensembles of the handle
     const double fpair = 8.0 * nc * nc * (2.0 * h->n_occ + 4.0 * h->n_vir) + 4.0 * 8.0 * nc * nc;
-    if (pair_flop) *pair_flop = 0.5 * m * (m - 1) * fpair;
-    if (spinor_flop) *spinor_flop = 2.0 * m * 4.0 * h->rows * h->n_p;
-    if (phi_bytes) *phi_bytes = 2.0 * m * nc * h->n_p * 16.0;
+    if (pair_flop) *pair_flop = ne * 0.5 * m * (m - 1) * fpair;
+    if (spinor_flop) *spinor_flop = ne * 2.0 * m * 4.0 * h->rows * h->n_p;
+    if (phi_bytes) *phi_bytes = ne * 2.0 * m * nc * h->n_p * 16.0;
   });
 }
 
@@ -774,7 +841,136 @@ int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
     // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
     const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
-    *pair_dmma_flop = ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
+    *pair_dmma_flop = h->nens * ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
+  });
+}
+
+int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t stream0) {
+  return guard(h, [&] {
+    if (nens < 1) throw ArgError("init_batch: at least one ensemble");
+    if (m < 2) throw ArgError("init_ensemble: at least two electron-pair walkers");
+    if (nens > 1 && m % 16) throw ArgError("init_batch: batched ensembles need a multiple of 16 walkers each");
+    if (size_t(nens) * m > size_t(h->mmax)) throw ArgError("init_batch: more walkers than the handle was sized for");
+    if (nens > h->nens_cap) throw ArgError("init_batch: more ensembles than the handle was sized for");
+    if (nens > 1 && !h->kramers)
+      throw ArgError("batched ensembles need the Kramers pair kernel (Kramers-paired spinor set, path on)");
+    h->m = m;
+    h->nens = nens;
+    h->k0 = uint32_t(seed);
+    h->k1 = uint32_t(seed >> 32);
+    h->rstream = stream0;
+    if (nens > 1) {
+      const size_t part = size_t(nens) * pair_kr_tiles((m + WB - 1) / WB) * pair_kr_consumers() * 2;
+      if (part > h->bpart_cap) {
+        if (h->d_bpart) cudaFree(h->d_bpart);
+        h->d_bpart = nullptr;
+        ck(cudaMalloc(&h->d_bpart, part * sizeof(double)), "cudaMalloc");
+        h->bpart_cap = part;
+      }
+      const size_t steps = size_t(kGraphSteps) * nens * 6;
+      if (steps > h->bsteps_cap) {
+        if (h->d_bsteps) cudaFree(h->d_bsteps);
+        if (h->h_bsteps) cudaFreeHost(h->h_bsteps);
+        h->d_bsteps = nullptr;
+        h->h_bsteps = nullptr;
+        ck(cudaMalloc(&h->d_bsteps, steps * sizeof(double)), "cudaMalloc");
+        ck(cudaMallocHost(&h->h_bsteps, steps * sizeof(double)), "cudaMallocHost");
+        h->bsteps_cap = steps;
+      }
+    }
+    std::vector<DevState> all(nens);
+    for (DevState& st : all) {
+      st = DevState{};
+      st.sigma = 1.0;  // sampler.hpp:45
+      st.error_idx = INT_MAX;
+      st.spec_error_idx = INT_MAX;
+    }
+    ck(cudaMemcpyAsync(h->d_state, all.data(), sizeof(DevState) * nens, cudaMemcpyHostToDevice, h->stream),
+       "state H2D");
+    launch_walk(h->walk_params(WALK_INIT, 0, 0), h->stream);
+    h->cur ^= 1;
+    ck(cudaGetLastError(), "walk launch");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    h->have_ensemble = true;
+  });
+}
+
+int mcmp2dev_batch_size(const mcmp2dev_t* h) { return h ? h->nens : 0; }
+
+int mcmp2dev_advance_batch(mcmp2dev_t* h, long nsteps, int nactive, double* values, double* imags) {
+  if (h && h->nens == 1 && nactive == 1) return mcmp2dev_advance(h, nsteps, values, imags);
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (nsteps < 0) throw ArgError("advance: negative step count");
+    if (nactive < 1 || nactive > h->nens) throw ArgError("advance_batch: active ensembles out of range");
+    advance_batched(h, nsteps, nactive, values, imags);
+  });
+}
+
+int mcmp2dev_get_ensemble_at(mcmp2dev_t* h, int ens, mcmp2dev_ensemble* e) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (!e || !e->walkers) throw ArgError("get_ensemble: null ensemble");
+    if (ens < 0 || ens >= h->nens) throw ArgError("get_ensemble_at: no such ensemble");
+    DevState st;
+    ck(scopy(h->stream, &st, h->d_state + ens, sizeof st, cudaMemcpyDeviceToHost), "state D2H");
+    const int m = h->m, mmax = h->buf[0].mmax;
+    std::vector<double> rows(size_t(9) * m);
+    for (int k = 0; k < 9; ++k)
+      ck(cudaMemcpyAsync(rows.data() + size_t(k) * m, h->buf[h->cur].w + size_t(k) * mmax + size_t(ens) * m,
+                         sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream),
+         "walkers D2H");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    e->m = m;
+    for (int p = 0; p < m; ++p)
+      for (int k = 0; k < 9; ++k) e->walkers[size_t(p) * 9 + k] = rows[size_t(k) * m + p];
+    e->sigma_step = st.sigma;
+    e->proposed = st.proposed;
+    e->accepted = st.accepted;
+    e->rng_key[0] = h->k0;
+    e->rng_key[1] = h->k1;
+    const uint64_t pos = st.pos;  // PhiloxRng state at stream position pos (rng.cpp:46-51, :83-94)
+    const uint64_t B = pos % 4 == 0 ? pos / 4 : pos / 4 + 1;
+    e->rng_idx = pos % 4 == 0 ? 4 : uint32_t(pos % 4);
+    e->rng_counter[0] = uint32_t(B);
+    e->rng_counter[1] = uint32_t(B >> 32);
+    e->rng_counter[2] = 0;
+    e->rng_counter[3] = h->rstream + uint32_t(ens);
+  });
+}
+
+int mcmp2dev_set_ensemble_at(mcmp2dev_t* h, int ens, const mcmp2dev_ensemble* e) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (!e || !e->walkers) throw ArgError("set_ensemble: null ensemble");
+    if (ens < 0 || ens >= h->nens) throw ArgError("set_ensemble_at: no such ensemble");
+    if (e->m != h->m) throw ArgError("set_ensemble_at: every ensemble of a batch has the same walker count");
+    if (e->rng_key[0] != h->k0 || e->rng_key[1] != h->k1 || e->rng_counter[3] != h->rstream + uint32_t(ens))
+      throw ArgError("set_ensemble_at: ensemble e of a batch runs on the batch seed and stream stream0 + e");
+    if (e->rng_counter[2] != 0) throw ArgError("set_ensemble: rng counter beyond 2^64 blocks");
+    const uint64_t B = uint64_t(e->rng_counter[0]) | (uint64_t(e->rng_counter[1]) << 32);
+    uint64_t pos;
+    if (e->rng_idx >= 4) pos = 4 * B;
+    else {
+      if (B == 0) throw ArgError("set_ensemble: partially consumed block before the first refill");
+      pos = 4 * (B - 1) + e->rng_idx;
+    }
+    const int m = h->m, mmax = h->buf[0].mmax;
+    std::vector<double> rows(size_t(9) * m);
+    for (int p = 0; p < m; ++p)
+      for (int k = 0; k < 9; ++k) rows[size_t(k) * m + p] = e->walkers[size_t(p) * 9 + k];
+    for (int k = 0; k < 9; ++k)
+      ck(cudaMemcpyAsync(h->buf[h->cur].w + size_t(k) * mmax + size_t(ens) * m, rows.data() + size_t(k) * m,
+                         sizeof(double) * m, cudaMemcpyHostToDevice, h->stream),
+         "walkers H2D");
+    DevState st{};
+    st.pos = pos;
+    st.sigma = e->sigma_step;
+    st.proposed = e->proposed;
+    st.accepted = e->accepted;
+    st.error_idx = INT_MAX;
+    st.spec_error_idx = INT_MAX;
+    ck(scopy(h->stream, h->d_state + ens, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   });
 }
 

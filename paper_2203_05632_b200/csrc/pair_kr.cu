@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
   __shared__ bool s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ntiles = kr_ntiles(P.nb);
+  // batched ensembles (P.nens > 1): ensemble e owns tiles [e ens_tiles, (e+1) ens_tiles) over its
+  // own walkers (points from e 2m), and the pair sums are kept per tile and ensemble
+  const bool batched = P.nens > 1;
+  const int ntiles = batched ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const PhiChunks ch{P.Go, P.Gv};
   const int nchunks = ch.count();
   const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
@@ -162,14 +165,19 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
       uint32_t phase = 0;
       TileWalk tw(int(blockIdx.x));
       for (int it = 0; it < my_tiles; ++it, tw.next(int(gridDim.x))) {
-        const int ta = tw.a, bp = tw.b;
+        int ta = tw.a, bp = tw.b, pbase = 0;
+        if (batched) {
+          const int tt = int(blockIdx.x) + it * int(gridDim.x), e = tt / P.ens_tiles;
+          kr_tile(tt - e * P.ens_tiles, ta, bp);
+          pbase = e * 2 * P.m;
+        }
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(&empty[stage], phase ^ 1u);
           double* dst = sm + stage * ring_doubles;
           const int f = ch.first(c), uc = ch.width(c);
           const uint32_t q_bytes = QPTS * uc * 32 * 8, p_bytes = HALF_PTS * uc * 32 * 8;
-          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(QPTS) * ta * uc) * 32;
-          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bp * uc) * 32;
+          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(pbase + QPTS * ta) * uc) * 32;
+          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(pbase + HALF_PTS * bp) * uc) * 32;
           mbar_expect_tx(&full[stage], q_bytes + p_bytes);
           bulk_g2s(dst, srcq, q_bytes, &full[stage]);
           bulk_g2s(dst + QPTS * uc * 32, srcp, p_bytes, &full[stage]);
@@ -206,8 +214,13 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
 
     TileWalk tw(int(blockIdx.x));
     for (int it = 0; it < my_tiles; ++it, tw.next(int(gridDim.x))) {
-      const int ta = tw.a, bp = tw.b;
-      const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile
+      int ta = tw.a, bp = tw.b;
+      const int tt = int(blockIdx.x) + it * int(gridDim.x);
+      if (batched) {
+        const int e = tt / P.ens_tiles;
+        kr_tile(tt - e * P.ens_tiles, ta, bp);
+      }
+      const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile (within its ensemble)
       double* const sO = sO0 + (it % OBUF) * SO_DOUBLES;
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
@@ -429,6 +442,15 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
             }
           }
       }
+      if (batched) {  // this tile's sums, per warp, unscaled (N_g^2 / w(tau_e) applied per ensemble)
+        const double d = acc_d + __shfl_down_sync(0xffffffffu, acc_d, 16);
+        const double x = acc_x + __shfl_down_sync(0xffffffffu, acc_x, 16);
+        if (lane == 0) {
+          P.partials[(size_t(tt) * CONSUMERS + warp) * 2 + 0] = d;
+          P.partials[(size_t(tt) * CONSUMERS + warp) * 2 + 1] = x;
+        }
+        acc_d = acc_x = 0.0;
+      }
     }
     acc_d += __shfl_down_sync(0xffffffffu, acc_d, 16);  // lanes 0 and 16 hold the sums
     acc_x += __shfl_down_sync(0xffffffffu, acc_x, 16);
@@ -438,6 +460,37 @@ __global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
     }
   }
   __syncthreads();
+  if (batched) {
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // fixed-order sums per ensemble: tiles in order, warps in order
+    for (int e = tid; e < P.nens; e += blockDim.x) {
+      double d = 0.0, x = 0.0;
+      const double* pe = P.partials + size_t(e) * P.ens_tiles * CONSUMERS * 2;
+      for (int k = 0; k < P.ens_tiles * CONSUMERS; ++k) {
+        d += pe[2 * k];
+        x += pe[2 * k + 1];
+      }
+      const double cwe = P.ng2 / P.st_ro[e].wtau;  // estimator.cpp:55
+      d *= cwe;
+      x *= cwe;
+      const double npairs = 0.5 * P.m * (P.m - 1);
+      double* out = P.step_out + size_t(e) * 6;
+      out[0] = (d + x) / npairs;
+      out[1] = 0.0;
+      out[2] = d;
+      out[3] = 0.0;
+      out[4] = x;
+      out[5] = 0.0;
+    }
+    if (tid == 0) P.st->done_pair = 0;
+    return;
+  }
   if (tid == 0) {
     double d = 0.0, x = 0.0;
     for (int w = 0; w < CONSUMERS; ++w) {
@@ -477,6 +530,8 @@ int g_sms_kr[64];
 }
 
 double pair_kr_block_tiles(int nb) { return double(kr_ntiles(nb)) * QB; }
+int pair_kr_tiles(int nb) { return kr_ntiles(nb); }
+int pair_kr_consumers() { return CONSUMERS; }
 
 void pair_kr_ring(int max_width, int& ring, int& ring_doubles) {
   ring_doubles = (QPTS + HALF_PTS) * max_width * 32;
@@ -496,7 +551,7 @@ cudaError_t pair_kr_kernel_setup() {
 void launch_pair_kr(const PairParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const int ntiles = kr_ntiles(P.nb);
+  const int ntiles = P.nens > 1 ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   const int grid = ntiles < slots ? ntiles : slots;
   if (P.physical)

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P)
         for (int uu = 0; uu < 2; ++uu) {
           const int r8 = 2 * (lane & 3) + jj;
           const int col = xb < 0 ? (nf0 / 2 + uu) * 8 + r8 : 2 * ((nf0 / 4) * 8 + r8);
-          swc[jj][uu] = (nf0 < nf_total && col < P.n_p) ? P.sw[col] : 0.0;
+          swc[jj][uu] = (nf0 < nf_total && col < P.n_p && !P.ens_pts) ? P.sw[col] : 0.0;
         }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -296,6 +296,9 @@ __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P)
       for (int i = 0; i < 4; ++i) {
         const int pt = (ptile * MO_PTF + wp * 4 + i) * 8 + (lane >> 2);
         if (pt >= P.npts) continue;
+        // batched ensembles: this point's ensemble has its own tau (8-point fragments never
+        // straddle ensembles: ens_pts is a multiple of 32)
+        const double* swb = P.ens_pts ? P.sw + size_t(pt / P.ens_pts) * P.sw_stride : nullptr;
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
           const int r8 = 2 * (lane & 3) + jj;
@@ -303,13 +306,15 @@ __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P)
 #pragma unroll
             for (int uu = 0; uu < 2; ++uu) {
               const int col = (nf0 / 2 + uu) * 8 + r8;
-              const double w = col < P.n_occ ? swc[jj][uu] : swc[jj][uu] * hpv[i];
+              const double sv = swb ? (col < P.n_p ? swb[col] : 0.0) : swc[jj][uu];
+              const double w = col < P.n_occ ? sv : sv * hpv[i];
               if (col < P.n_p) put(xa, pt, w, col, acc[i][2 * uu][jj], acc[i][2 * uu + 1][jj]);
             }
           } else {  // Kramers pair: fragments (a re, a im, b re, b im) of even column 2j
             const int j = (nf0 / 4) * 8 + r8, col = 2 * j;
             if (col < P.n_p) {
-              const double w = col < P.n_occ ? swc[jj][0] : swc[jj][0] * hpv[i];
+              const double sv = swb ? swb[col] : swc[jj][0];
+              const double w = col < P.n_occ ? sv : sv * hpv[i];
               const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
               put(xa, pt, w, col, ar, ai);
               put(xb, pt, w, col, br, bi);

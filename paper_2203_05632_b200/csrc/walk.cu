@@ -136,17 +136,21 @@ __device__ __forceinline__ void finish_init(const WalkParams& P, Walker& x) {
 
 // sqrt of guarded_exp (greens.cpp:9-16) for every spinor at the step's tau; overflow is
 // flagged with the first offending spinor index, as the reference throws at set_tau.
-__device__ void tau_weights(const WalkParams& P, double tau, bool speculative = false) {
+__device__ void tau_weights(const WalkParams& P, double tau, bool speculative = false, DevState* st = nullptr,
+                            double* swout = nullptr, int tid0 = -1, int nthr = 0) {
   const int np = P.n_occ + P.n_vir;
-  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+  if (!st) st = P.st;
+  if (!swout) swout = P.sw;
+  if (tid0 < 0) tid0 = threadIdx.x, nthr = blockDim.x;
+  for (int k = tid0; k < np; k += nthr) {
     const double e = k < P.n_occ ? P.energies[k] * tau : -P.energies[k] * tau;
     double sw;
     if (e > 700.0) {
       if (speculative) {  // confirmed by the last CTA unless the sweep redrew a proposal
-        atomicMin(&P.st->spec_error_idx, k);
+        atomicMin(&st->spec_error_idx, k);
       } else {
-        atomicMin(&P.st->error_idx, k);
-        P.st->error = 1;
+        atomicMin(&st->error_idx, k);
+        st->error = 1;
       }
       sw = 0.0;
     } else if (e < -700.0) {
@@ -154,7 +158,7 @@ __device__ void tau_weights(const WalkParams& P, double tau, bool speculative = 
     } else {
       sw = exp(0.5 * e);
     }
-    P.sw[k] = sw;
+    swout[k] = sw;
   }
 }
 
@@ -164,12 +168,14 @@ __device__ void tau_weights(const WalkParams& P, double tau, bool speculative = 
 constexpr int WALK_THREADS = 128;
 
 // tau = TauSampler::sample(rng.uniform()) after the sweep (driver.cpp:445), u32 at `pos`
-__device__ double draw_tau(const WalkParams& P, unsigned long long pos) {
-  StreamReader rd(P.k0, P.k1, P.stream, pos);
+__device__ double draw_tau(const WalkParams& P, unsigned long long pos, DevState* st = nullptr,
+                           uint32_t stream = 0xffffffffu) {
+  if (!st) st = P.st;
+  StreamReader rd(P.k0, P.k1, stream == 0xffffffffu ? P.stream : stream, pos);
   const double u = rd.uniform();
   const double tau = -log1p(-u) / P.lambda;
-  P.st->tau = tau;
-  P.st->wtau = P.lambda * exp(-P.lambda * tau);
+  st->tau = tau;
+  st->wtau = P.lambda * exp(-P.lambda * tau);
   return tau;
 }
 
@@ -337,6 +343,151 @@ __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(WalkParams P) {
   if (P.mode == WALK_PRODUCTION && s_redo) tau_weights(P, P.st->tau);
 }
 
+// Batched ensembles (several reference workers in one handle): one CTA per ensemble e, walkers
+// [e m, (e+1) m) of the SoA buffers, Philox stream P.stream + e, state P.st[e], spinor weights
+// P.sw + e * sw_stride. Threads 2p, 2p+1 take walker p's electrons exactly as walk_kernel; the
+// last warp draws tau speculatively; the CTA itself does the bookkeeping that walk_kernel's last
+// CTA does (sampler.cpp:49-93, driver.cpp:444-445), including the sequential redo.
+__global__ void walk_batch_kernel(WalkParams P) {
+  __shared__ int s_acc;
+  __shared__ int s_redo;
+  __shared__ double s_tau;
+  const int e = blockIdx.x, m = P.m;
+  DevState* const st = P.st + e;
+  const uint32_t stream = P.stream + uint32_t(e);
+  double* const swe = P.sw + size_t(e) * P.sw_stride;
+  const int base = e * m;
+  const int tid = threadIdx.x, nwalk = 2 * m;
+  const int p = tid >> 1, el = tid & 1;
+  const bool walker_thread = tid < nwalk;
+  if (P.nactive > 0 && e >= P.nactive) {  // inactive this step: state and walkers unchanged
+    for (int i = tid; i < 9 * m; i += blockDim.x) {
+      const int k = i / m, q = i % m;
+      P.out.at(k, base + q) = P.in.at(k, base + q);
+    }
+    return;
+  }
+  const unsigned long long pos0 = st->pos;
+  if (tid == 0) {
+    s_acc = 0;
+    s_redo = 0;
+  }
+  __syncthreads();
+  if (!walker_thread) {  // tau warp(s)
+    if (P.mode == WALK_PRODUCTION) {
+      if (tid == nwalk) s_tau = draw_tau(P, pos0 + 18ull * unsigned(m), st, stream);
+      asm volatile("bar.sync 1, %0;" ::"r"(int(blockDim.x) - nwalk));
+      tau_weights(P, s_tau, true, st, swe, tid - nwalk, int(blockDim.x) - nwalk);
+    }
+  } else {
+    double n[3], gn;
+    if (P.mode == WALK_INIT) {
+      StreamReader rd(P.k0, P.k1, stream, pos0 + 20ull * p + 10ull * el);
+      place(rd, P.sites, n);
+    } else {
+      StreamReader rd(P.k0, P.k1, stream, pos0 + 18ull * p + 8ull * el);
+      double g[3];
+      gaussian3(rd, g);
+      const double sigma = st->sigma;
+      for (int k = 0; k < 3; ++k) n[k] = P.in.at(3 * el + k, base + p) + g[k] * sigma;
+    }
+    gn = g_of(P.sites, n[0], n[1], n[2]);
+    const unsigned mask = __activemask();
+    double m2[3];
+    for (int k = 0; k < 3; ++k) m2[k] = __shfl_xor_sync(mask, n[k], 1);
+    const double g2n = __shfl_xor_sync(mask, gn, 1);
+    if (el == 0) {
+      Walker x;
+      if (P.mode == WALK_INIT) {
+        for (int k = 0; k < 3; ++k) {
+          x.r1[k] = n[k];
+          x.r2[k] = m2[k];
+        }
+        if (dist2(x.r1, x.r2) == 0.0) s_redo = 1;
+        x.g1 = gn;
+        x.g2 = g2n;
+        x.w = x.g1 * x.g2 / (P.ng * sqrt(dist2(x.r1, x.r2)));
+      } else {
+        x = load_walker(P.in, base + p);
+        const double dx = n[0] - m2[0], dy = n[1] - m2[1], dz = n[2] - m2[2];
+        const double r12 = sqrt(dx * dx + dy * dy + dz * dz);
+        if (r12 == 0.0) {
+          s_redo = 1;
+        } else {  // sampler.cpp:63-77
+          StreamReader rd(P.k0, P.k1, stream, pos0 + 18ull * p + 16ull);
+          const double wnew = gn * g2n / (P.ng * r12);
+          const double u = rd.uniform();
+          if (u * x.w < wnew) {
+            for (int k = 0; k < 3; ++k) {
+              x.r1[k] = n[k];
+              x.r2[k] = m2[k];
+            }
+            x.g1 = gn;
+            x.g2 = g2n;
+            x.w = wnew;
+            atomicAdd(&s_acc, 1);  // integer count: order independent
+          }
+        }
+      }
+      store_walker(P.out, base + p, x);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long total = s_acc;
+    unsigned long long consumed = (P.mode == WALK_INIT ? 20ull : 18ull) * unsigned(m);
+    if (s_redo) {  // replay this ensemble's sweep exactly as the reference's sequential loop
+      StreamReader rd(P.k0, P.k1, stream, pos0);
+      total = 0;
+      for (int q = 0; q < m; ++q) {
+        if (P.mode == WALK_INIT) {
+          Walker x;
+          place(rd, P.sites, x.r1);
+          do {
+            place(rd, P.sites, x.r2);
+          } while (dist2(x.r1, x.r2) == 0.0);
+          finish_init(P, x);
+          store_walker(P.out, base + q, x);
+        } else {
+          Walker x = load_walker(P.in, base + q);
+          double n1[3], n2[3], r12;
+          do {
+            r12 = propose(rd, x, st->sigma, n1, n2);
+          } while (r12 == 0.0);
+          total += decide(rd, P, x, n1, n2, r12);
+          store_walker(P.out, base + q, x);
+        }
+      }
+      consumed = rd.pos - pos0;
+    }
+    st->pos = pos0 + consumed;
+    if (P.mode == WALK_PRODUCTION) {
+      st->proposed += m;
+      st->accepted += total;
+      if (s_redo) {
+        s_tau = draw_tau(P, st->pos, st, stream);  // the speculative draw used the wrong position
+        st->spec_error_idx = INT_MAX;
+      } else if (st->spec_error_idx != INT_MAX) {
+        st->error = 1;
+        st->error_idx = min(st->error_idx, st->spec_error_idx);
+        st->spec_error_idx = INT_MAX;
+      }
+      st->pos += 2;
+    } else if (P.mode == WALK_BURN) {  // sampler.cpp:82-90
+      st->win_acc += total;
+      st->win_prop += m;
+      if (P.adapt && P.sweep % 100 == 0) {
+        const double rate = double(st->win_acc) / double(st->win_prop);
+        st->sigma = st->sigma * (rate > 0.5 ? 1.1 : 1.0 / 1.1);
+        st->win_acc = 0;
+        st->win_prop = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (P.mode == WALK_PRODUCTION && s_redo) tau_weights(P, s_tau, false, st, swe);
+}
+
 // replay: positions/g from the caller, tau given (estimator input of mc_step_estimate)
 __global__ void replay_load_kernel(WalkParams P, const double* walkers, double tau) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -353,6 +504,11 @@ __global__ void replay_load_kernel(WalkParams P, const double* walkers, double t
 }
 
 void launch_walk(const WalkParams& P, cudaStream_t s) {
+  if (P.nens > 1) {  // one CTA per ensemble: 2m walker threads + one tau warp
+    const int threads = (2 * P.m + 31) / 32 * 32 + 32;
+    walk_batch_kernel<<<P.nens, threads, 0, s>>>(P);
+    return;
+  }
   const int blocks = (2 * P.m + WALK_THREADS - 1) / WALK_THREADS + (P.mode == WALK_PRODUCTION ? 1 : 0);
   walk_kernel<<<blocks, WALK_THREADS, 0, s>>>(P);
 }

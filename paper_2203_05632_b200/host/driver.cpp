@@ -241,10 +241,24 @@ DeviceWorker::DeviceWorker(const SpinorSet& s, const WeightSpec& w, const RunCon
   check_dev(mcmp2dev_create(&sys.view, device, cfg.walkers, &h_), nullptr);
 }
 
-DeviceWorker::~DeviceWorker() { mcmp2dev_destroy(h_); }
+DeviceWorker::DeviceWorker(std::shared_ptr<DeviceBatch> batch, int ens, const RunConfig& cfg, int index)
+    : acc(cfg.block_size), index_(index), walkers_(cfg.walkers), h_(batch->h), cfg_(&cfg), batch_(std::move(batch)),
+      ens_(ens) {}
+
+DeviceWorker::~DeviceWorker() {
+  if (!batch_) mcmp2dev_destroy(h_);
+}
+
+DeviceBatch::~DeviceBatch() { mcmp2dev_destroy(h); }
 
 void DeviceWorker::init_and_burn_in() {  // driver.cpp:354-358 (+ step-size extension)
-  check_dev(mcmp2dev_init_ensemble(h_, walkers_, cfg_->seed, std::uint32_t(index_)), h_);
+  if (batch_) {  // the whole batch at its first worker: ensemble e = init_ensemble(m, seed, first + e)
+    if (batch_->ready) return;
+    check_dev(mcmp2dev_init_batch(h_, batch_->nens, walkers_, cfg_->seed, std::uint32_t(batch_->first)), h_);
+    batch_->ready = true;
+  } else {
+    check_dev(mcmp2dev_init_ensemble(h_, walkers_, cfg_->seed, std::uint32_t(index_)), h_);
+  }
   if (cfg_->step_size) check_dev(mcmp2dev_set_sigma_step(h_, *cfg_->step_size), h_);
   check_dev(mcmp2dev_burn_in(h_, cfg_->burn_in, cfg_->step_size ? 0 : 1), h_);
   check_dev(mcmp2dev_prepare(h_), h_);
@@ -252,6 +266,7 @@ void DeviceWorker::init_and_burn_in() {  // driver.cpp:354-358 (+ step-size exte
 
 void DeviceWorker::advance(long long nsteps) {  // driver.cpp:440-450
   if (nsteps <= 0) return;
+  if (batch_) throw std::logic_error("DeviceWorker::advance: batched workers advance through advance_batch");
   values_.resize(nsteps);
   imags_.resize(nsteps);
   check_dev(mcmp2dev_advance(h_, long(nsteps), values_.data(), imags_.data()), h_);
@@ -259,11 +274,41 @@ void DeviceWorker::advance(long long nsteps) {  // driver.cpp:440-450
   done += nsteps;
 }
 
+void DeviceWorker::advance_batch(DeviceBatch& b, const std::vector<DeviceWorker*>& ws,
+                                 const std::vector<long long>& nsteps) {
+  // the step shares of a batch differ by at most one, the extra steps at the lowest indices
+  // (worker_share, driver.cpp:307-309), so the active ensembles are always a prefix
+  long long done = 0, most = 0;
+  for (long long n : nsteps) most = std::max(most, n);
+  while (done < most) {
+    int na = 0;
+    while (na < b.nens && nsteps[na] > done) ++na;
+    for (int e = na; e < b.nens; ++e)
+      if (nsteps[e] > done) throw std::logic_error("advance_batch: step shares are not a prefix");
+    long long n = most - done;
+    for (int e = 0; e < na; ++e) n = std::min(n, nsteps[e] - done);
+    b.values.resize(std::size_t(n) * b.nens);
+    b.imags.resize(std::size_t(n) * b.nens);
+    check_dev(mcmp2dev_advance_batch(b.h, long(n), na, b.values.data(), b.imags.data()), b.h);
+    for (int e = 0; e < na; ++e) {
+      DeviceWorker& w = *ws[e];
+      for (long long s = 0; s < n; ++s) w.acc.add(b.values[std::size_t(s) * b.nens + e], b.imags[std::size_t(s) * b.nens + e]);
+      w.done += n;
+    }
+    done += n;
+  }
+}
+
+void DeviceWorker::get_state(mcmp2dev_ensemble* e) const {
+  if (batch_) check_dev(mcmp2dev_get_ensemble_at(h_, ens_, e), h_);
+  else check_dev(mcmp2dev_get_ensemble(h_, e), h_);
+}
+
 double DeviceWorker::acceptance() const {
   std::vector<double> w(std::size_t(walkers_) * 9);
   mcmp2dev_ensemble e{};
   e.walkers = w.data();
-  check_dev(mcmp2dev_get_ensemble(h_, &e), h_);
+  get_state(&e);
   return e.proposed ? double(e.accepted) / double(e.proposed) : 0.0;
 }
 
@@ -277,7 +322,7 @@ std::string DeviceWorker::save_ensemble() const {  // sampler.cpp:95-105 + rng.c
   std::vector<double> w(std::size_t(walkers_) * 9);
   mcmp2dev_ensemble e{};
   e.walkers = w.data();
-  check_dev(mcmp2dev_get_ensemble(h_, &e), h_);
+  get_state(&e);
   std::ostringstream os;
   os << e.m << ' ' << format_double(e.sigma_step) << ' ' << e.proposed << ' ' << e.accepted << '\n';
   os << e.rng_key[0] << ' ' << e.rng_key[1];
@@ -302,7 +347,15 @@ void DeviceWorker::load_ensemble(const std::string& text) {  // sampler.cpp:107-
   for (auto& v : w)
     if (!(is >> v)) throw std::runtime_error("checkpoint: malformed walker record");
   e.walkers = w.data();
-  check_dev(mcmp2dev_set_ensemble(h_, &e), h_);
+  if (batch_) {
+    if (!batch_->ready) {  // the batch's layout (ensembles, seed, streams); states loaded below
+      check_dev(mcmp2dev_init_batch(h_, batch_->nens, walkers_, cfg_->seed, std::uint32_t(batch_->first)), h_);
+      batch_->ready = true;
+    }
+    check_dev(mcmp2dev_set_ensemble_at(h_, ens_, &e), h_);
+  } else {
+    check_dev(mcmp2dev_set_ensemble(h_, &e), h_);
+  }
   check_dev(mcmp2dev_prepare(h_), h_);
 }
 
@@ -455,9 +508,34 @@ class Engine {  // driver.cpp:336-475
     if (ndev <= 0 && cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
     if (ndev <= 0) throw std::runtime_error("mcmp2: no CUDA device visible (the walker loop runs on the GPU only)");
     const int nw = restored.empty() ? cfg_.workers : int(restored.size());
-    for (int w = 0; w < nw; ++w) {
-      const int index = restored.empty() ? w : restored[w].index;
-      workers_.push_back(std::make_unique<DeviceWorker>(spinors_, *spec_, cfg_, index, w % ndev));
+    // workers in contiguous ranges per device; a range of several workers with walker counts
+    // that suit batching runs as one batched handle (one launch sequence per step for all)
+    for (int d = 0; d < ndev; ++d) {
+      const int k0 = int((long long)d * nw / ndev), k1 = int((long long)(d + 1) * nw / ndev);
+      if (k1 <= k0) continue;
+      std::shared_ptr<DeviceBatch> batch;
+      bool contiguous = true;
+      for (int k = k0; k < k1; ++k)
+        if ((restored.empty() ? k : restored[k].index) != (restored.empty() ? k0 : restored[k0].index) + (k - k0))
+          contiguous = false;
+      if (k1 - k0 > 1 && contiguous && cfg_.walkers % 16 == 0 && cfg_.walkers <= 1024) {
+        DeviceSystem sys =
+            make_device_system(spinors_, *spec_, cfg_.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
+        batch = std::make_shared<DeviceBatch>();
+        check_dev(mcmp2dev_create(&sys.view, d, (k1 - k0) * cfg_.walkers, &batch->h), nullptr);
+        if (mcmp2dev_kramers(batch->h, -1) != 1) batch.reset();  // batching needs the Kramers pair kernel
+      }
+      for (int k = k0; k < k1; ++k) {
+        const int index = restored.empty() ? k : restored[k].index;
+        if (batch) {
+          batch->first = restored.empty() ? k0 : restored[k0].index;
+          batch->nens = k1 - k0;
+          batch->m = cfg_.walkers;
+          workers_.push_back(std::make_unique<DeviceWorker>(batch, k - k0, cfg_, index));
+        } else {
+          workers_.push_back(std::make_unique<DeviceWorker>(spinors_, *spec_, cfg_, index, d));
+        }
+      }
     }
     if (restored.empty()) {
       for (auto& w : workers_) w->init_and_burn_in();
@@ -529,14 +607,27 @@ class Engine {  // driver.cpp:336-475
   void advance_parallel(const std::vector<long long>& chunk) {  // driver.cpp:423-438
     std::vector<std::thread> threads;
     std::vector<std::exception_ptr> errors(workers_.size());
-    for (std::size_t w = 0; w < workers_.size(); ++w)
-      threads.emplace_back([&, w] {
+    for (std::size_t w = 0; w < workers_.size(); ++w) {
+      const DeviceBatch* b = workers_[w]->batch();
+      if (b && w > 0 && workers_[w - 1]->batch() == b) continue;  // the batch's first worker drives it
+      threads.emplace_back([&, w, b] {
         try {
-          workers_[w]->advance(chunk[w]);
+          if (b) {
+            std::vector<DeviceWorker*> ws;
+            std::vector<long long> n;
+            for (std::size_t k = w; k < workers_.size() && workers_[k]->batch() == b; ++k) {
+              ws.push_back(workers_[k].get());
+              n.push_back(std::max<long long>(chunk[k], 0));
+            }
+            DeviceWorker::advance_batch(*const_cast<DeviceBatch*>(b), ws, n);
+          } else {
+            workers_[w]->advance(chunk[w]);
+          }
         } catch (...) {
           errors[w] = std::current_exception();
         }
       });
+    }
     for (auto& t : threads) t.join();
     for (auto& e : errors)
       if (e) std::rethrow_exception(e);

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <map>
 #include <optional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -173,7 +174,7 @@ long long worker_share(long long total, int workers, int index);
 
 struct RunHooks {
   long abort_after_intervals = -1;
-  int device_count = 0;  // 0: all visible devices; workers are placed round robin
+  int device_count = 0;  // 0: all visible devices; workers are placed in contiguous ranges per device
 };
 RunReport run(const RunConfig& cfg, const RunHooks& hooks = {});
 RunReport resume(const std::string& checkpoint_path, const RunHooks& hooks = {});
@@ -182,9 +183,27 @@ MergedEstimate merge_checkpoint_files(const std::vector<std::string>& paths,
 std::string format_report(const RunReport& r);
 
 // ---- one device worker: the unit the distributed runner and the bench drive ----
+// Several workers of one device in one batched handle (include/mcmp2dev.h, batched ensembles):
+// worker first + e is ensemble e (Philox stream first + e, driver.cpp:354-356).
+struct DeviceBatch {
+  mcmp2dev_t* h = nullptr;
+  int first = 0, nens = 0, m = 0;
+  bool ready = false;  // init_batch done
+  std::vector<double> values, imags;
+  DeviceBatch() = default;
+  DeviceBatch(const DeviceBatch&) = delete;
+  DeviceBatch& operator=(const DeviceBatch&) = delete;
+  ~DeviceBatch();
+};
+
 class DeviceWorker {
  public:
   DeviceWorker(const SpinorSet& s, const WeightSpec& w, const RunConfig& cfg, int index, int device);
+  DeviceWorker(std::shared_ptr<DeviceBatch> batch, int ens, const RunConfig& cfg, int index);
+  // advances a batch's workers (in ensemble order) by their own step counts (driver.cpp:440-450)
+  static void advance_batch(DeviceBatch& b, const std::vector<DeviceWorker*>& ws,
+                            const std::vector<long long>& nsteps);
+  const DeviceBatch* batch() const { return batch_.get(); }
   ~DeviceWorker();
   DeviceWorker(const DeviceWorker&) = delete;
   DeviceWorker& operator=(const DeviceWorker&) = delete;
@@ -203,11 +222,14 @@ class DeviceWorker {
   const std::vector<double>& last_imags() const { return imags_; }
 
  private:
+  void get_state(mcmp2dev_ensemble* e) const;
   int index_;
   int walkers_;
   mcmp2dev_t* h_ = nullptr;
   const RunConfig* cfg_;
   std::vector<double> values_, imags_;
+  std::shared_ptr<DeviceBatch> batch_;  // non-null: h_ is the batch's handle, ensemble ens_
+  int ens_ = 0;
 };
 
 void check_dev(int rc, const mcmp2dev_t* h);

@@ -83,6 +83,10 @@ def dev() -> C.CDLL:
         d.mcmp2dev_kramers.argtypes = [vp, ip]
         d.mcmp2dev_work_executed.argtypes = [vp, dp]
         d.mcmp2dev_prepare.argtypes = [vp]
+        d.mcmp2dev_init_batch.argtypes = [vp, ip, ip, C.c_uint64, C.c_uint32]
+        d.mcmp2dev_batch_size.argtypes = [vp]
+        d.mcmp2dev_get_ensemble_at.argtypes = [vp, ip, C.POINTER(Ensemble)]
+        d.mcmp2dev_set_ensemble_at.argtypes = [vp, ip, C.POINTER(Ensemble)]
         _dev = d
     return _dev
 

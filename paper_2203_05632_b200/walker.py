@@ -80,12 +80,41 @@ class DeviceWalker:
     def init_ensemble(self, m: int, seed: int, stream: int = 0) -> None:
         check_dev(self._d.mcmp2dev_init_ensemble(self._h, m, seed, stream), self._h)
         self.m = m
+        self.nens = 1
 
     def burn_in(self, n_burn: int, adapt: bool = True) -> None:
         check_dev(self._d.mcmp2dev_burn_in(self._h, n_burn, int(adapt)), self._h)
 
     def set_sigma_step(self, sigma: float) -> None:
         check_dev(self._d.mcmp2dev_set_sigma_step(self._h, sigma), self._h)
+
+    def init_batch(self, nens: int, m: int, seed: int, stream0: int = 0) -> None:
+        """nens reference workers in this handle: ensemble e = init_ensemble(m, seed, stream0 + e);
+        advance() then returns [nsteps, nens] arrays (include/mcmp2dev.h, batched ensembles)."""
+        check_dev(self._d.mcmp2dev_init_batch(self._h, nens, m, seed, stream0), self._h)
+        self.m = m
+        self.nens = nens
+
+    def get_ensemble_at(self, ens: int) -> EnsembleState:
+        w = np.zeros((self.m, 9))
+        e = Ensemble()
+        e.walkers = dptr(w)
+        check_dev(self._d.mcmp2dev_get_ensemble_at(self._h, ens, C.byref(e)), self._h)
+        return EnsembleState(w.copy(), e.sigma_step, e.proposed, e.accepted, tuple(e.rng_key),
+                             tuple(e.rng_counter), e.rng_idx)
+
+    def set_ensemble_at(self, ens: int, s: EnsembleState) -> None:
+        w = np.ascontiguousarray(s.walkers, dtype=np.float64)
+        e = Ensemble()
+        e.m = len(w)
+        e.sigma_step = s.sigma_step
+        e.proposed = s.proposed
+        e.accepted = s.accepted
+        e.rng_key[:] = s.rng_key
+        e.rng_counter[:] = s.rng_counter
+        e.rng_idx = s.rng_idx
+        e.walkers = dptr(w)
+        check_dev(self._d.mcmp2dev_set_ensemble_at(self._h, ens, C.byref(e)), self._h)
 
     def get_ensemble(self) -> EnsembleState:
         w = np.zeros((self.max_walkers, 9))
@@ -108,14 +137,16 @@ class DeviceWalker:
         e.walkers = dptr(w)
         check_dev(self._d.mcmp2dev_set_ensemble(self._h, C.byref(e)), self._h)
         self.m = len(w)
+        self.nens = 1
 
     # -- hot loop -------------------------------------------------------------------
     def advance(self, nsteps: int, keep_on_device: bool = False):
         if keep_on_device:
             check_dev(self._d.mcmp2dev_advance(self._h, nsteps, None, None), self._h)
             return None
-        v = np.empty(nsteps)
-        im = np.empty(nsteps)
+        ne = getattr(self, "nens", 1)
+        v = np.empty((nsteps, ne) if ne > 1 else nsteps)
+        im = np.empty_like(v)
         check_dev(self._d.mcmp2dev_advance(self._h, nsteps, dptr(v), dptr(im)), self._h)
         return v, im
 

@@ -123,3 +123,30 @@ def test_missing_nuclei_is_diagnosed(cfgdir, tmp_path):
     sp.write_text(text)
     with pytest.raises(Mcmp2Error, match="nuclei"):
         walker.run_config_text(small(cfgdir, spinors=str(sp)))
+
+
+def test_batched_workers_match_oracle_engine(cfgdir):
+    """Five cfg1 workers on one device run as one batched handle (m = 16, Kramers-paired set):
+    unequal step shares (2003 = 401 x 3 + 400 x 2, driver.cpp:307-309) advance the leading
+    ensembles alone; every worker follows its reference stream, so the run equals the oracle
+    Engine's (std::thread workers) to rounding."""
+    cfg = small(cfgdir, name="cfg1", walkers=16, workers=5, steps=2003, **{"step-size": 0.3})
+    dev = parse(walker.run_config_text(cfg))
+    ref = parse(oracle_py.run_config(cfg))
+    assert dev["steps"] == ref["steps"] == 2003
+    assert [w.split(",")[0] for w in dev["workers"]] == [w.split(",")[0] for w in ref["workers"]]
+    assert dev["value"] == pytest.approx(ref["value"], rel=1e-9)
+    assert dev["sigma_bar"] == pytest.approx(ref["sigma_bar"], rel=1e-6)
+    acc_dev = [w.split("acceptance ")[1].split(",")[0] for w in dev["workers"]]
+    acc_ref = [w.split("acceptance ")[1].split(",")[0] for w in ref["workers"]]
+    assert acc_dev == acc_ref
+
+
+def test_batched_kill_and_resume_is_bit_exact(cfgdir, tmp_path):
+    """test_driver.cpp:150-172 with the workers of a batched handle: per-ensemble states go
+    through the checkpoint and come back into the batch."""
+    ck = tmp_path / "run.ckpt"
+    cfg = small(cfgdir, name="cfg2", walkers=16, workers=3, steps=1201, burnin=50, checkpoint=str(ck))
+    full = walker.run_config_text(cfg)
+    walker.run_config_text(cfg, abort_after_intervals=1)
+    assert walker.resume(ck) == full
