@@ -160,19 +160,26 @@ def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, qui
                       f"(fixed {t0:.2f} s/step + {c * 1e6:.2f} us/sample per worker)"}
 
 
-def interval_merge(vals, rank: int, dist):
-    """The checkpoint-interval merge of the multi-GPU driver (distributed.py): each rank's
-    (steps, mean, sigma_bar) summary is all-gathered (NCCL under torchrun) and merged by
-    step-count weighting (driver.cpp:183-196) -- the only collective of the walker loop."""
+def interval_merge(vals, first_index: int, dist):
+    """The checkpoint-interval merge of the multi-GPU driver (distributed.py): each worker's
+    (steps, mean, sigma_bar) summary (one per ensemble; vals is [steps] or [steps][ensembles]) is
+    all-gathered (NCCL under torchrun) and merged by step-count weighting (driver.cpp:183-196) --
+    the only collective of the walker loop."""
     import numpy as np
     from paper_2203_05632_b200.distributed import Summary, merge_estimates, torch_all_gather
-    nb = 100 if len(vals) >= 200 else max(1, len(vals) // 2)
-    k = len(vals) // nb
-    blocks = np.asarray(vals[: k * nb]).reshape(k, nb).mean(axis=1)
-    mean = float(np.mean(vals))
-    sb = float(np.sqrt(np.sum((blocks - mean) ** 2) / k) / np.sqrt(k)) if k > 0 else 0.0
-    mine = Summary(rank, len(vals), mean, sb, 0.0, 0.0, k)
-    parts = [Summary.from_array(a) for a in torch_all_gather(dist)(mine.as_array())] if dist else [mine]
+    v2 = np.asarray(vals).reshape(len(vals), -1)
+    nb = 100 if len(v2) >= 200 else max(1, len(v2) // 2)
+    k = len(v2) // nb
+    mine = []
+    for e in range(v2.shape[1]):
+        col = v2[:, e]
+        blocks = col[: k * nb].reshape(k, nb).mean(axis=1)
+        mean = float(np.mean(col))
+        sb = float(np.sqrt(np.sum((blocks - mean) ** 2) / k) / np.sqrt(k)) if k > 0 else 0.0
+        mine.append(Summary(first_index + e, len(col), mean, sb, 0.0, 0.0, k).as_array())
+    mine = np.stack(mine)
+    gathered = torch_all_gather(dist)(mine) if dist else [mine]
+    parts = [Summary.from_array(a) for g in gathered for a in g]
     value, sigma_bar, total = merge_estimates(sorted(parts, key=lambda s: s.index))
     return {"E2": value, "sigma_bar": sigma_bar, "steps": total, "workers": len(parts)}
 
@@ -186,6 +193,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--burnin", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ensembles", type=int, default=1,
+                    help="reference workers per GPU, batched in one handle (mcmp2dev_init_batch); each is an "
+                         "independent ensemble of the config's walker count on Philox stream rank*E + e")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -198,8 +208,10 @@ def main():
     tmp = Path(tempfile.mkdtemp(prefix=f"mcmp2_bench_r{rank}_"))
     spinor, conf = generate_config(cfg, tmp)
     conf_text = conf.read_text()
-    samples_per_step = m * (m - 1) // 2
-    config = {"workload": f"{cfg}: {WORKLOAD[cfg]}", "walkers_per_gpu": m, "samples_per_step_per_gpu": samples_per_step,
+    ens = max(1, args.ensembles)
+    samples_per_step = ens * (m * (m - 1) // 2)
+    config = {"workload": f"{cfg}: {WORKLOAD[cfg]}" + (f" x {ens} ensembles per GPU" if ens > 1 else ""),
+              "walkers_per_gpu": ens * m, "ensembles_per_gpu": ens, "samples_per_step_per_gpu": samples_per_step,
               "estimator": "literal (reference estimator.cpp:26-32)", "rng": "reference Philox stream per worker"}
 
     if args.impl == "reference":
@@ -238,8 +250,11 @@ def main():
     from paper_2203_05632_b200 import DeviceWalker, System
 
     sysd = System(spinor, conf_text)
-    dw = DeviceWalker(sysd, device=dev, max_walkers=m)
-    dw.init_ensemble(m, seed=1, stream=rank)
+    dw = DeviceWalker(sysd, device=dev, max_walkers=ens * m)
+    if ens > 1:
+        dw.init_batch(ens, m, seed=1, stream0=rank * ens)
+    else:
+        dw.init_ensemble(m, seed=1, stream=rank)
     if cfg == "cfg1":
         dw.set_sigma_step(0.3)
         dw.burn_in(args.burnin, adapt=False)
@@ -305,20 +320,20 @@ def main():
     # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
     dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
     import paper_2203_05632_b200.distributed  # noqa: F401  (module import is setup, not step time)
-    st = dw.get_ensemble()
+    st = dw.get_ensembles() if ens > 1 else dw.get_ensemble()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
-    dw.set_ensemble(st)                              # H2D walker state (resume)
-    vals, ims = dw.advance(args.steps)               # every step's (value, imag) D2H
-    st2 = dw.get_ensemble()                          # D2H walker state (checkpoint)
-    merged = interval_merge(vals, rank, dist)        # per-worker summaries -> one estimate (driver.cpp:183-196)
+    (dw.set_ensembles if ens > 1 else dw.set_ensemble)(st)   # H2D walker state (resume)
+    vals, ims = dw.advance(args.steps)                       # every step's (value, imag) D2H
+    st2 = dw.get_ensembles() if ens > 1 else dw.get_ensemble()  # D2H walker state (checkpoint)
+    merged = interval_merge(vals, rank * ens, dist)  # per-worker summaries -> one estimate (driver.cpp:183-196)
     e2e_s = time.perf_counter() - t0
     e2e_value = world * samples_per_step * args.steps / reduce_max(e2e_s)
-    state_bytes = m * 9 * 8 + 64
+    state_bytes = ens * (m * 9 * 8 + 64)
     h2d = state_bytes / args.steps
-    d2h = 16 + state_bytes / args.steps
+    d2h = 16 * ens + state_bytes / args.steps
 
     if rank != 0:
         if dist:
@@ -329,7 +344,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64/c128", "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
-        "config": dict(config, parallelism=f"{world} independent workers (1 per GPU)",
+        "config": dict(config, parallelism=f"{world * ens} independent workers ({ens} per GPU)",
                        l2="flushed between timed steps (256 MiB write on the handle's stream)"),
         "roofline": {"bound": "tensor", "kernel": kernel_name, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -105,7 +105,7 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e); /* e->walkers: [
  * Several reference workers in ONE handle (the std::thread workers of driver.cpp:423-438, each
  * with its own ensemble and Philox stream, driver.cpp:354-356), so small systems fill the GPU:
  * ensemble e (0 <= e < nens) is init_ensemble(m, seed, stream0 + e); every step advances all
- * of them in the same launches. Needs m % 16 == 0 and the Kramers pair kernel; the handle must
+ * of them in the same launches. Needs m % 16 == 0, m <= 480 and the Kramers pair kernel; the handle must
  * be created with max_walkers >= nens * m (and nens <= max_walkers / 16). advance() then writes
  * values/imags as [nsteps][nens]; burn_in and set_sigma_step apply to every ensemble;
  * get/set_ensemble_at address one ensemble (same m, the batch seed, stream stream0 + e).
@@ -114,6 +114,9 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
 int mcmp2dev_batch_size(const mcmp2dev_t* h);  /* ensembles advanced per step (1 unless batched) */
 int mcmp2dev_get_ensemble_at(mcmp2dev_t* h, int ens, mcmp2dev_ensemble* e);
 int mcmp2dev_set_ensemble_at(mcmp2dev_t* h, int ens, const mcmp2dev_ensemble* e);
+/* every ensemble at once (two copies): es[nens], each with its own walkers buffer [m][9] */
+int mcmp2dev_get_ensembles(mcmp2dev_t* h, mcmp2dev_ensemble* es);
+int mcmp2dev_set_ensembles(mcmp2dev_t* h, const mcmp2dev_ensemble* es);
 /* advance() of ensembles [0, nactive) only; the others keep walkers, RNG state and counters
  * (unequal step shares, driver.cpp:307-309: the extra steps go to the lowest worker indices).
  * values/imags are [nsteps][nens]; entries of inactive ensembles are not steps. */

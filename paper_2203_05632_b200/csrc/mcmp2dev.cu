@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kChunk = 1024;  // steps per device->host copy of StepEstimates
 constexpr int kGraphSteps = 32;  // production steps per captured CUDA graph (even)
+constexpr int kBatchMaxWalkers = 480;  // per batched ensemble (2m + 32 threads <= 1024, m % 16 == 0)
 thread_local std::string g_create_error;
 
 struct CudaError : std::runtime_error {
@@ -850,6 +851,8 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
     if (nens < 1) throw ArgError("init_batch: at least one ensemble");
     if (m < 2) throw ArgError("init_ensemble: at least two electron-pair walkers");
     if (nens > 1 && m % 16) throw ArgError("init_batch: batched ensembles need a multiple of 16 walkers each");
+    if (nens > 1 && m > kBatchMaxWalkers)  // walk_batch_kernel: one CTA of 2m + 32 threads per ensemble
+      throw ArgError("init_batch: batched ensembles hold at most " + std::to_string(kBatchMaxWalkers) + " walkers each");
     if (size_t(nens) * m > size_t(h->mmax)) throw ArgError("init_batch: more walkers than the handle was sized for");
     if (nens > h->nens_cap) throw ArgError("init_batch: more ensembles than the handle was sized for");
     if (nens > 1 && !h->kramers)
@@ -936,6 +939,77 @@ int mcmp2dev_get_ensemble_at(mcmp2dev_t* h, int ens, mcmp2dev_ensemble* e) {
     e->rng_counter[1] = uint32_t(B >> 32);
     e->rng_counter[2] = 0;
     e->rng_counter[3] = h->rstream + uint32_t(ens);
+  });
+}
+
+int mcmp2dev_get_ensembles(mcmp2dev_t* h, mcmp2dev_ensemble* es) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (!es) throw ArgError("get_ensembles: null array");
+    const int ne = h->nens, m = h->m, mmax = h->buf[0].mmax;
+    std::vector<DevState> all(ne);
+    std::vector<double> soa(size_t(9) * mmax);
+    ck(cudaMemcpyAsync(all.data(), h->d_state, sizeof(DevState) * ne, cudaMemcpyDeviceToHost, h->stream), "state D2H");
+    ck(cudaMemcpyAsync(soa.data(), h->buf[h->cur].w, soa.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream),
+       "walkers D2H");
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    for (int k = 0; k < ne; ++k) {
+      mcmp2dev_ensemble* e = es + k;
+      if (!e->walkers) throw ArgError("get_ensembles: null walker buffer");
+      e->m = m;
+      for (int p = 0; p < m; ++p)
+        for (int c = 0; c < 9; ++c) e->walkers[size_t(p) * 9 + c] = soa[size_t(c) * mmax + size_t(k) * m + p];
+      const DevState& st = all[k];
+      e->sigma_step = st.sigma;
+      e->proposed = st.proposed;
+      e->accepted = st.accepted;
+      e->rng_key[0] = h->k0;
+      e->rng_key[1] = h->k1;
+      const uint64_t B = st.pos % 4 == 0 ? st.pos / 4 : st.pos / 4 + 1;
+      e->rng_idx = st.pos % 4 == 0 ? 4 : uint32_t(st.pos % 4);
+      e->rng_counter[0] = uint32_t(B);
+      e->rng_counter[1] = uint32_t(B >> 32);
+      e->rng_counter[2] = 0;
+      e->rng_counter[3] = h->rstream + uint32_t(k);
+    }
+  });
+}
+
+int mcmp2dev_set_ensembles(mcmp2dev_t* h, const mcmp2dev_ensemble* es) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (!es) throw ArgError("set_ensembles: null array");
+    const int ne = h->nens, m = h->m, mmax = h->buf[0].mmax;
+    std::vector<DevState> all(ne);
+    std::vector<double> soa(size_t(9) * mmax, 0.0);
+    for (int k = 0; k < ne; ++k) {
+      const mcmp2dev_ensemble* e = es + k;
+      if (!e->walkers) throw ArgError("set_ensemble: null ensemble");
+      if (e->m != m) throw ArgError("set_ensemble_at: every ensemble of a batch has the same walker count");
+      if (e->rng_key[0] != h->k0 || e->rng_key[1] != h->k1 || e->rng_counter[3] != h->rstream + uint32_t(k))
+        throw ArgError("set_ensemble_at: ensemble e of a batch runs on the batch seed and stream stream0 + e");
+      if (e->rng_counter[2] != 0) throw ArgError("set_ensemble: rng counter beyond 2^64 blocks");
+      const uint64_t B = uint64_t(e->rng_counter[0]) | (uint64_t(e->rng_counter[1]) << 32);
+      uint64_t pos;
+      if (e->rng_idx >= 4) pos = 4 * B;
+      else {
+        if (B == 0) throw ArgError("set_ensemble: partially consumed block before the first refill");
+        pos = 4 * (B - 1) + e->rng_idx;
+      }
+      for (int p = 0; p < m; ++p)
+        for (int c = 0; c < 9; ++c) soa[size_t(c) * mmax + size_t(k) * m + p] = e->walkers[size_t(p) * 9 + c];
+      DevState& st = all[k];
+      st = DevState{};
+      st.pos = pos;
+      st.sigma = e->sigma_step;
+      st.proposed = e->proposed;
+      st.accepted = e->accepted;
+      st.error_idx = INT_MAX;
+      st.spec_error_idx = INT_MAX;
+    }
+    ck(cudaMemcpyAsync(h->buf[h->cur].w, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream),
+       "walkers H2D");
+    ck(scopy(h->stream, h->d_state, all.data(), sizeof(DevState) * ne, cudaMemcpyHostToDevice), "state H2D");
   });
 }
 

@@ -518,7 +518,7 @@ class Engine {  // driver.cpp:336-475
       for (int k = k0; k < k1; ++k)
         if ((restored.empty() ? k : restored[k].index) != (restored.empty() ? k0 : restored[k0].index) + (k - k0))
           contiguous = false;
-      if (k1 - k0 > 1 && contiguous && cfg_.walkers % 16 == 0 && cfg_.walkers <= 1024) {
+      if (k1 - k0 > 1 && contiguous && cfg_.walkers % 16 == 0 && cfg_.walkers <= 480) {  // mcmp2dev_init_batch limits
         DeviceSystem sys =
             make_device_system(spinors_, *spec_, cfg_.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
         batch = std::make_shared<DeviceBatch>();

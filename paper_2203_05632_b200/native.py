@@ -87,6 +87,9 @@ def dev() -> C.CDLL:
         d.mcmp2dev_batch_size.argtypes = [vp]
         d.mcmp2dev_get_ensemble_at.argtypes = [vp, ip, C.POINTER(Ensemble)]
         d.mcmp2dev_set_ensemble_at.argtypes = [vp, ip, C.POINTER(Ensemble)]
+        d.mcmp2dev_get_ensembles.argtypes = [vp, C.POINTER(Ensemble)]
+        d.mcmp2dev_set_ensembles.argtypes = [vp, C.POINTER(Ensemble)]
+        d.mcmp2dev_advance_batch.argtypes = [vp, C.c_long, ip, dp, dp]
         _dev = d
     return _dev
 

@@ -116,6 +116,33 @@ class DeviceWalker:
         e.walkers = dptr(w)
         check_dev(self._d.mcmp2dev_set_ensemble_at(self._h, ens, C.byref(e)), self._h)
 
+    def get_ensembles(self) -> list[EnsembleState]:
+        """Every ensemble of a batched handle in two device copies."""
+        ne = getattr(self, "nens", 1)
+        ws = [np.zeros((self.m, 9)) for _ in range(ne)]
+        arr = (Ensemble * ne)()
+        for k in range(ne):
+            arr[k].walkers = dptr(ws[k])
+        check_dev(self._d.mcmp2dev_get_ensembles(self._h, arr), self._h)
+        return [EnsembleState(ws[k], arr[k].sigma_step, arr[k].proposed, arr[k].accepted, tuple(arr[k].rng_key),
+                              tuple(arr[k].rng_counter), arr[k].rng_idx) for k in range(ne)]
+
+    def set_ensembles(self, states) -> None:
+        ne = len(states)
+        ws = [np.ascontiguousarray(s.walkers, dtype=np.float64) for s in states]
+        arr = (Ensemble * ne)()
+        for k, s in enumerate(states):
+            e = arr[k]
+            e.m = len(ws[k])
+            e.sigma_step = s.sigma_step
+            e.proposed = s.proposed
+            e.accepted = s.accepted
+            e.rng_key[:] = s.rng_key
+            e.rng_counter[:] = s.rng_counter
+            e.rng_idx = s.rng_idx
+            e.walkers = dptr(ws[k])
+        check_dev(self._d.mcmp2dev_set_ensembles(self._h, arr), self._h)
+
     def get_ensemble(self) -> EnsembleState:
         w = np.zeros((self.max_walkers, 9))
         e = Ensemble()

@@ -81,6 +81,8 @@ def test_batch_argument_errors(cfgdir):
         dw.init_batch(2, 12, seed=1)
     with pytest.raises(Mcmp2ArgumentError, match="sized for"):
         dw.init_batch(5, 16, seed=1)
+    with pytest.raises(Mcmp2ArgumentError, match="at most 480"):
+        DeviceWalker(sysd, max_walkers=1024).init_batch(2, 496, seed=1)
     dw.init_batch(4, 16, seed=1)
     with pytest.raises(Mcmp2ArgumentError, match="get_ensemble_at"):
         dw.get_ensemble()
@@ -95,3 +97,21 @@ def test_batch_argument_errors(cfgdir):
     one_c = System(cfgdir / "syn1c.spinor", "")
     with pytest.raises(Mcmp2ArgumentError, match="Kramers"):
         DeviceWalker(one_c, max_walkers=64).init_batch(2, 16, seed=1)
+
+
+def test_bulk_state_round_trip(cfgdir):
+    """get_ensembles / set_ensembles (all ensembles in two copies) agree with the per-ensemble
+    calls and restore the batch exactly."""
+    sysd = System(cfgdir / "cfg2.spinor", (cfgdir / "cfg2.conf").read_text())
+    dw = DeviceWalker(sysd, max_walkers=4 * 16)
+    dw.init_batch(4, 16, seed=8, stream0=2)
+    dw.burn_in(20)
+    bulk = dw.get_ensembles()
+    for e in range(4):
+        one = dw.get_ensemble_at(e)
+        assert np.array_equal(one.walkers, bulk[e].walkers) and one.rng_counter == bulk[e].rng_counter
+        assert one.rng_idx == bulk[e].rng_idx and one.sigma_step == bulk[e].sigma_step
+    v1, _ = dw.advance(5)
+    dw.set_ensembles(bulk)
+    v2, _ = dw.advance(5)
+    assert np.array_equal(v1, v2)
