@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--probe-steps", type=int, default=200)
     ap.add_argument("--max-seconds", type=float, default=120.0)
     ap.add_argument("--timeout", type=float, default=300.0)
+    ap.add_argument("--workers", type=int, default=1,
+                    help="reference workers (one GPU: batched ensembles in one handle when m allows)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     rows = []
@@ -54,16 +56,18 @@ def main():
             if walkers:
                 base = re.sub(r"walkers \d+", f"walkers {walkers}", base)
             walkers = int(re.search(r"walkers (\d+)", base).group(1))
+            base = re.sub(r"workers \d+\n", "", base) + f"workers {args.workers}\n"
             # probe: fixed budget, gives samples/s and the variance
             t0 = time.perf_counter()
-            rep = walker.run_config_text(base + f"steps {args.probe_steps}\ncheckpoint-interval {args.probe_steps}\n")
+            rep = walker.run_config_text(base + f"steps {args.probe_steps * args.workers}\n"
+                                         f"checkpoint-interval {args.probe_steps}\n")
             t_probe = time.perf_counter() - t0
             e, s, steps = parse(rep)
             pairs = walkers * (walkers - 1) // 2
             rate = steps * pairs / t_probe
             est_steps = steps * (s / (0.01 * abs(e))) ** 2 if e else float("inf")
             est_time = t_probe * est_steps / steps
-            row = {"config": name, "walkers": walkers, "probe_steps": steps, "probe_seconds": t_probe,
+            row = {"config": name, "walkers": walkers, "workers": args.workers, "probe_steps": steps, "probe_seconds": t_probe,
                    "samples_per_s_incl_setup": rate, "E2_probe": e, "sigma_bar_probe": s,
                    "steps_to_1pct_est": est_steps, "seconds_to_1pct_est": est_time}
             if est_time <= args.max_seconds:
