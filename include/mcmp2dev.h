@@ -105,7 +105,7 @@ int mcmp2dev_get_ensemble(mcmp2dev_t* h, mcmp2dev_ensemble* e); /* e->walkers: [
  * Several reference workers in ONE handle (the std::thread workers of driver.cpp:423-438, each
  * with its own ensemble and Philox stream, driver.cpp:354-356), so small systems fill the GPU:
  * ensemble e (0 <= e < nens) is init_ensemble(m, seed, stream0 + e); every step advances all
- * of them in the same launches. Needs m % 16 == 0, m <= 480 and the Kramers pair kernel; the handle must
+ * of them in the same launches. Needs m % 16 == 0 and m <= 480; the handle must
  * be created with max_walkers >= nens * m (and nens <= max_walkers / 16). advance() then writes
  * values/imags as [nsteps][nens]; burn_in and set_sigma_step apply to every ensemble;
  * get/set_ensemble_at address one ensemble (same m, the batch seed, stream stream0 + e).

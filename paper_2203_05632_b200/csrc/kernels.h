@@ -75,7 +75,7 @@ struct PairParams {
   int physical;              // 1: Tr(o1 va) Tr(o2 vb), Tr(o1 vd o2 vc) epilogue (opt-in)
   double* partials;          // [ntiles][4]; batched: [nens * ens_tiles][consumer warps][2]
   double* step_out;          // [6] of this step; batched: [nens][6]
-  int nens, ens_tiles;       // batched ensembles (pair_kr only): m walkers each, st_ro[nens]
+  int nens, ens_tiles;       // batched ensembles: m walkers each, st_ro[nens]
 };
 
 void launch_walk(const WalkParams& P, cudaStream_t s);
@@ -90,6 +90,7 @@ cudaError_t pair_kr_kernel_setup();
 double pair_kr_block_tiles(int nb);
 int pair_kr_tiles(int nb);      // tiles of one ensemble of nb walker blocks
 int pair_kr_consumers();        // DMMA warps per pair_kr CTA (per-tile partials in batched mode)
+int pair_consumers();           // DMMA warps per pair_kernel CTA
 void pair_kr_ring(int max_width, int& ring, int& ring_doubles);  // stage ring for the widest chunk  // WB x WB walker blocks the Kramers launch computes
 cudaError_t spinor_kernel_setup();
 int mo_ctas_per_sm();

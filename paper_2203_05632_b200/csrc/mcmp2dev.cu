@@ -174,8 +174,6 @@ struct mcmp2dev_handle {
   }
 
   void launch_estimate(const WalkerBuf& wb, int mm, double* step_out, int ne = 1) {
-    if (ne > 1 && !kramers)
-      throw ArgError("batched ensembles need the Kramers pair kernel (Kramers-paired spinor set, path on)");
     SpinorParams s = kramers ? sp_kr : sp;
     s.npts = 2 * mm * ne;
     s.ens_pts = ne > 1 ? 2 * mm : 0;
@@ -205,7 +203,7 @@ struct mcmp2dev_handle {
     p.partials = ne > 1 ? d_bpart : d_partials;
     p.step_out = step_out;
     p.nens = ne;
-    p.ens_tiles = ne > 1 ? pair_kr_tiles(p.nb) : 0;
+    p.ens_tiles = ne > 1 ? (kramers ? pair_kr_tiles(p.nb) : p.nb * (p.nb + 1) / 2) : 0;
     if (kramers) launch_pair_kr(p, stream);
     else launch_pair(p, stream);
     if (prof) {
@@ -855,15 +853,15 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
       throw ArgError("init_batch: batched ensembles hold at most " + std::to_string(kBatchMaxWalkers) + " walkers each");
     if (size_t(nens) * m > size_t(h->mmax)) throw ArgError("init_batch: more walkers than the handle was sized for");
     if (nens > h->nens_cap) throw ArgError("init_batch: more ensembles than the handle was sized for");
-    if (nens > 1 && !h->kramers)
-      throw ArgError("batched ensembles need the Kramers pair kernel (Kramers-paired spinor set, path on)");
     h->m = m;
     h->nens = nens;
     h->k0 = uint32_t(seed);
     h->k1 = uint32_t(seed >> 32);
     h->rstream = stream0;
     if (nens > 1) {
-      const size_t part = size_t(nens) * pair_kr_tiles((m + WB - 1) / WB) * pair_kr_consumers() * 2;
+      const int nb = (m + WB - 1) / WB;  // per-tile partials of either pair kernel
+      const size_t part = size_t(nens) * std::max(size_t(pair_kr_tiles(nb)) * pair_kr_consumers() * 2,
+                                                  size_t(nb) * (nb + 1) / 2 * pair_consumers() * 4);
       if (part > h->bpart_cap) {
         if (h->d_bpart) cudaFree(h->d_bpart);
         h->d_bpart = nullptr;

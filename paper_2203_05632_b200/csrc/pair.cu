@@ -64,7 +64,10 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
   __shared__ bool s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ntiles = P.nb * (P.nb + 1) / 2;
+  // batched ensembles (P.nens > 1): ensemble e owns tiles [e ens_tiles, (e+1) ens_tiles) of its
+  // own triangle (points from e 2m); sums are kept per tile and reduced per ensemble
+  const bool batched = P.nens > 1;
+  const int ntiles = batched ? P.nens * P.ens_tiles : P.nb * (P.nb + 1) / 2;
   const PhiChunks ch{P.Go, P.Gv};
   const int nchunks = ch.count();
   const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
@@ -84,16 +87,24 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
     if (lane == 0) {
       long long seq = 0;
       for (int it = 0; it < my_tiles; ++it) {
-        int bq, bp;
-        tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+        int bq, bp, pbase = 0;
+        {
+          int tt = int(blockIdx.x) + it * int(gridDim.x);
+          if (batched) {
+            const int e = tt / P.ens_tiles;
+            tt -= e * P.ens_tiles;
+            pbase = e * 2 * P.m;
+          }
+          tile_coords(tt, bq, bp);
+        }
         for (int c = 0; c < nchunks; ++c, ++seq) {
           const int stage = int(seq % STAGES);
           mbar_wait(&empty[stage], uint32_t(((seq / STAGES) & 1) ^ 1));
           double* dst = sm + stage * STAGE_DOUBLES;
           const int f = ch.first(c), uc = ch.width(c);
           const uint32_t half_bytes = HALF_PTS * uc * 32 * 8;
-          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bq * uc) * 32;
-          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(HALF_PTS) * bp * uc) * 32;
+          const double* srcq = P.phi + (size_t(f) * P.npts_pad + size_t(pbase + HALF_PTS * bq) * uc) * 32;
+          const double* srcp = P.phi + (size_t(f) * P.npts_pad + size_t(pbase + HALF_PTS * bp) * uc) * 32;
           mbar_expect_tx(&full[stage], 2 * half_bytes);
           bulk_g2s(dst, srcq, half_bytes, &full[stage]);
           bulk_g2s(dst + HALF_PTS * uc * 32, srcp, half_bytes, &full[stage]);
@@ -121,7 +132,22 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
 
     for (int it = 0; it < my_tiles; ++it) {
       int bq, bp;
-      tile_coords(int(blockIdx.x) + it * int(gridDim.x), bq, bp);
+      const int tt = int(blockIdx.x) + it * int(gridDim.x);
+      tile_coords(batched ? tt % P.ens_tiles : tt, bq, bp);
+      // batched: this tile's sums, per warp, unscaled (N_g^2 / w(tau_e) applied per ensemble)
+      auto flush_tile = [&]() {
+        if (!batched) return;
+        double r[4] = {acc_dr, acc_di, acc_xr, acc_xi};
+        if constexpr (PHYS) {  // lanes 0..7 hold the tile's partial sums
+#pragma unroll
+          for (int o = 4; o; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r[k] += __shfl_down_sync(0xffffffffu, r[k], o);
+        }
+        if (lane == 0)
+          for (int k = 0; k < 4; ++k) P.partials[(size_t(tt) * CONSUMERS + warp) * 4 + k] = r[k];
+        acc_dr = acc_di = acc_xr = acc_xi = 0.0;
+      };
 
       // ---- phase 1: O~_e(q,y; p,x) = sum_i Phi_o(q,e,y,i) conj Phi_o(p,e,x,i) ----
       {
@@ -278,6 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           }
         }
         __syncwarp();
+        flush_tile();
         continue;
       }
 
@@ -324,6 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
           }
         }
       __syncwarp();  // all lanes done reading `so` before the next tile rewrites it
+      flush_tile();
     }
     if constexpr (PHYS) {  // lanes 0..7 hold partial sums: fixed shuffle tree into lane 0
 #pragma unroll
@@ -342,6 +370,33 @@ __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
     }
   }
   __syncthreads();
+  if (batched) {
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int e = tid; e < P.nens; e += THREADS) {  // fixed order: tiles, then warps
+      double a[4] = {0, 0, 0, 0};
+      const double* pe = P.partials + size_t(e) * P.ens_tiles * CONSUMERS * 4;
+      for (int k = 0; k < P.ens_tiles * CONSUMERS; ++k)
+        for (int j = 0; j < 4; ++j) a[j] += pe[4 * k + j];
+      const double cwe = P.ng2 / P.st_ro[e].wtau;  // estimator.cpp:55
+      for (int j = 0; j < 4; ++j) a[j] *= cwe;
+      const double npairs = 0.5 * P.m * (P.m - 1);  // estimator.cpp:61
+      double* out = P.step_out + size_t(e) * 6;
+      out[0] = (a[0] + a[2]) / npairs;
+      out[1] = (a[1] + a[3]) / npairs;
+      out[2] = a[0];
+      out[3] = a[1];
+      out[4] = a[2];
+      out[5] = a[3];
+    }
+    if (tid == 0) P.st->done_pair = 0;
+    return;
+  }
   if (tid == 0) {
     double r[4] = {0, 0, 0, 0};
     for (int w = 0; w < CONSUMERS; ++w)
@@ -391,19 +446,21 @@ cudaError_t pair_kernel_setup() {
   return cudaFuncSetAttribute(pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<true>::SMEM_BYTES);
 }
 
-int pair_grid(int nb) {
+int pair_grid(int nb, int nens, int ens_tiles) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const int ntiles = nb * (nb + 1) / 2;
+  const int ntiles = nens > 1 ? nens * ens_tiles : nb * (nb + 1) / 2;
   const int sms = g_sms[dev & 63] > 0 ? g_sms[dev & 63] : 148;
   return ntiles < sms ? ntiles : sms;
 }
 
 void launch_pair(const PairParams& P, cudaStream_t s) {
   if (P.physical)
-    pair_kernel<true><<<pair_grid(P.nb), THREADS, Cfg<true>::SMEM_BYTES, s>>>(P);
+    pair_kernel<true><<<pair_grid(P.nb, P.nens, P.ens_tiles), THREADS, Cfg<true>::SMEM_BYTES, s>>>(P);
   else
-    pair_kernel<false><<<pair_grid(P.nb), THREADS, Cfg<false>::SMEM_BYTES, s>>>(P);
+    pair_kernel<false><<<pair_grid(P.nb, P.nens, P.ens_tiles), THREADS, Cfg<false>::SMEM_BYTES, s>>>(P);
 }
+
+int pair_consumers() { return CONSUMERS; }
 
 }  // namespace mcmp2dev

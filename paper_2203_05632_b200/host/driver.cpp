@@ -523,7 +523,6 @@ class Engine {  // driver.cpp:336-475
             make_device_system(spinors_, *spec_, cfg_.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
         batch = std::make_shared<DeviceBatch>();
         check_dev(mcmp2dev_create(&sys.view, d, (k1 - k0) * cfg_.walkers, &batch->h), nullptr);
-        if (mcmp2dev_kramers(batch->h, -1) != 1) batch.reset();  // batching needs the Kramers pair kernel
       }
       for (int k = k0; k < k1; ++k) {
         const int index = restored.empty() ? k : restored[k].index;

@@ -91,12 +91,29 @@ def test_batch_argument_errors(cfgdir):
     st = dw.get_ensemble_at(1)
     with pytest.raises(Mcmp2ArgumentError, match="stream0 \\+ e"):
         dw.set_ensemble_at(2, st)
-    dw.kramers(0)
-    with pytest.raises(Mcmp2ArgumentError, match="Kramers"):
-        dw.advance(1)
-    one_c = System(cfgdir / "syn1c.spinor", "")
-    with pytest.raises(Mcmp2ArgumentError, match="Kramers"):
-        DeviceWalker(one_c, max_walkers=64).init_batch(2, 16, seed=1)
+    from paper_2203_05632_b200.native import check_dev
+    with pytest.raises(Mcmp2ArgumentError, match="active ensembles"):
+        check_dev(dw._d.mcmp2dev_advance_batch(dw._h, 1, 5, None, None), dw._h)
+
+
+@pytest.mark.parametrize("name,kramers,physical", [("syn1c", 0, False), ("syn2c", 0, False),
+                                                   ("cfg2", 0, False), ("cfg2", 0, True)])
+def test_batched_general_kernel_follows_oracle(cfgdir, name, kramers, physical):
+    """The general pair kernel (1c/2c sets, or the Kramers path switched off) batches too."""
+    sp = cfgdir / f"{name}.spinor"
+    text = (cfgdir / f"{name}.conf").read_text() + ("estimator physical\n" if physical else "")
+    orc = oracle_py.OracleSystem(sp, text)
+    m, nens, burn, nsteps = 16, 3, 30, 4
+    dw = DeviceWalker(System(sp, text), max_walkers=nens * m)
+    dw.kramers(kramers)
+    assert not dw.kramers()
+    dw.init_batch(nens, m, seed=6, stream0=1)
+    dw.burn_in(burn)
+    v, im = dw.advance(nsteps)
+    for e in range(nens):
+        tr = orc.trajectory(seed=6, stream=1 + e, m=m, burn=burn, nsteps=nsteps, physical=physical)
+        assert rel_err(v[:, e], tr["est"][:, 0]) < REL, e
+        assert np.max(np.abs(im[:, e] - tr["est"][:, 1])) <= REL * np.max(np.abs(tr["est"][:, 0]))
 
 
 def test_bulk_state_round_trip(cfgdir):
