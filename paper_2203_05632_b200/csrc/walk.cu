@@ -360,6 +360,7 @@ __global__ void walk_batch_kernel(WalkParams P) {
   const int tid = threadIdx.x, nwalk = 2 * m;
   const int p = tid >> 1, el = tid & 1;
   const bool walker_thread = tid < nwalk;
+  const int tau_tid0 = (nwalk + 31) / 32 * 32;  // the tau warp follows the walker warps
   if (P.nactive > 0 && e >= P.nactive) {  // inactive this step: state and walkers unchanged
     for (int i = tid; i < 9 * m; i += blockDim.x) {
       const int k = i / m, q = i % m;
@@ -373,11 +374,11 @@ __global__ void walk_batch_kernel(WalkParams P) {
     s_redo = 0;
   }
   __syncthreads();
-  if (!walker_thread) {  // tau warp(s)
-    if (P.mode == WALK_PRODUCTION) {
-      if (tid == nwalk) s_tau = draw_tau(P, pos0 + 18ull * unsigned(m), st, stream);
-      asm volatile("bar.sync 1, %0;" ::"r"(int(blockDim.x) - nwalk));
-      tau_weights(P, s_tau, true, st, swe, tid - nwalk, int(blockDim.x) - nwalk);
+  if (!walker_thread) {  // the tau warp (idle lanes of the last walker warp do nothing)
+    if (P.mode == WALK_PRODUCTION && tid >= tau_tid0) {
+      if (tid == tau_tid0) s_tau = draw_tau(P, pos0 + 18ull * unsigned(m), st, stream);
+      __syncwarp();
+      tau_weights(P, s_tau, true, st, swe, tid - tau_tid0, 32);
     }
   } else {
     double n[3], gn;
@@ -504,7 +505,9 @@ __global__ void replay_load_kernel(WalkParams P, const double* walkers, double t
 }
 
 void launch_walk(const WalkParams& P, cudaStream_t s) {
-  if (P.nens > 1) {  // one CTA per ensemble: 2m walker threads + one tau warp
+  // one CTA per ensemble (2m walker threads + one tau warp) for batches and for single ensembles
+  // that fit one CTA: no cross-CTA last-CTA round trip
+  if (P.nens > 1 || P.m <= 496) {
     const int threads = (2 * P.m + 31) / 32 * 32 + 32;
     walk_batch_kernel<<<P.nens, threads, 0, s>>>(P);
     return;
