@@ -46,6 +46,17 @@ int mcmp2h_worker_stats(mcmp2h_worker* w, double* out8);
 int mcmp2h_worker_block_means(mcmp2h_worker* w, double* out, int cap);
 mcmp2dev_t* mcmp2h_worker_device(mcmp2h_worker* w);
 
+/* Workers [first_index, first_index + count) of one process on one device (the multi-GPU
+ * driver's rank): one batched handle when the walker count allows it (include/mcmp2dev.h,
+ * batched ensembles), else one handle each; init + burn-in at create (driver.cpp:354-358).
+ * advance: worker k takes nsteps[k] steps; stats: as mcmp2h_worker_stats for worker k. */
+typedef struct mcmp2h_group mcmp2h_group;
+mcmp2h_group* mcmp2h_group_create(const char* config_text, int first_index, int count, int device);
+void mcmp2h_group_free(mcmp2h_group* g);
+int mcmp2h_group_size(const mcmp2h_group* g);
+int mcmp2h_group_advance(mcmp2h_group* g, const long long* nsteps);
+int mcmp2h_group_stats(mcmp2h_group* g, int k, double* out10);
+
 /* writes <dir>/<name>.spinor and <dir>/<name>.conf for BASELINE configs cfg1..cfg4, cfg5-N */
 int mcmp2h_generate(const char* name, const char* dir);
 

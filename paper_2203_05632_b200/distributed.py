@@ -1,12 +1,14 @@
-"""One process per GPU: each rank is one reference worker, merged over torch.distributed.
+"""One process per GPU; the run's reference workers are split over the ranks and merged over
+torch.distributed.
 
 The reference runs `workers` independent ensembles as std::threads in one process
 (driver.cpp:423-438) with Philox stream = worker index (driver.cpp:354-356), splits a step
 budget with worker_share (driver.cpp:307-309), and at every checkpoint interval merges the
 per-worker estimates by step-count weighting (driver.cpp:183-196) for the target-error stop
-rule (driver.cpp:401-412). Here the workers are processes (torchrun, one GPU each) and the
-interval merge is one all_gather of a 7-double summary per rank — the only collective; the
-walker loop itself has no communication. Launch:
+rule (driver.cpp:401-412). Here each rank (torchrun, one GPU each) hosts a contiguous range of
+the workers (at least one; a range of several shares one batched device handle when the walker
+count allows it), and the interval merge is one all_gather of the workers' 7-double summaries --
+the only collective; the walker loop itself has no communication. Launch:
 
   torchrun --nproc-per-node N -m paper_2203_05632_b200.distributed CONFIG_FILE
 """
@@ -93,26 +95,86 @@ def parse_run_config(text: str) -> dict:
         cfg[k] = v
     return {"steps": int(cfg["steps"]) if "steps" in cfg else None,
             "target": float(cfg["target-rel-err"]) if "target-rel-err" in cfg else None,
-            "interval": int(cfg["checkpoint-interval"])}
+            "interval": int(cfg["checkpoint-interval"]), "workers": int(cfg.get("workers", "1"))}
 
 
-def drive(worker, rank: int, world: int, steps: int | None, target: float | None, interval: int,
-          all_gather, max_intervals: int | None = None) -> dict:
-    """Engine::drive (driver.cpp:376-420) with workers = ranks: every interval each rank
-    advances its share, then the summaries are gathered and the stop rule is evaluated
-    identically on every rank."""
+class HostGroup:
+    """The reference workers [first, first + count) this rank hosts on its GPU (host/capi.cpp,
+    mcmp2h_group): one batched device handle when the walker count allows it
+    (include/mcmp2dev.h, batched ensembles), else one handle each; init + burn-in at creation."""
+
+    def __init__(self, config_text: str, first: int, count: int, device: int):
+        h = native.host()
+        self._g = h.mcmp2h_group_create(config_text.encode(), first, count, device)
+        if not self._g:
+            raise native.Mcmp2Error(h.mcmp2h_last_error().decode())
+        self.first, self.count = first, count
+
+    def advance(self, nsteps) -> None:
+        arr = (C.c_longlong * self.count)(*[int(max(n, 0)) for n in nsteps])
+        check_host(native.host().mcmp2h_group_advance(self._g, arr))
+
+    def summaries(self) -> list[Summary]:
+        out = []
+        for k in range(self.count):
+            o = np.zeros(10)
+            check_host(native.host().mcmp2h_group_stats(self._g, k, dptr(o)))
+            out.append(Summary(self.first + k, int(o[0]), o[3], o[4], o[8], o[9], int(o[7])))
+        return out
+
+    def close(self):
+        if getattr(self, "_g", None):
+            native.host().mcmp2h_group_free(self._g)
+            self._g = None
+
+    def __del__(self):
+        self.close()
+
+
+class _OneWorker:
+    """A single worker (advance(n), summary()) seen as a group of one."""
+
+    def __init__(self, worker, index: int):
+        self.w, self.first, self.count = worker, index, 1
+
+    def advance(self, nsteps) -> None:
+        self.w.advance(nsteps[0])
+
+    def summaries(self) -> list[Summary]:
+        return [self.w.summary()]
+
+
+def rank_workers(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Workers of this rank: a contiguous range of the run's `workers` (at least one per rank),
+    split as worker_share splits steps (driver.cpp:307-309)."""
+    total = max(total, world)
+    first = sum(worker_share(total, world, r) for r in range(rank))
+    return first, worker_share(total, world, rank)
+
+
+def drive_group(group, total_workers: int, steps: int | None, target: float | None, interval: int, all_gather,
+                max_intervals: int | None = None) -> dict:
+    """Engine::drive (driver.cpp:376-420) over all ranks' workers: every interval each worker
+    advances its share, the summaries of all workers are gathered (one all_gather; ranks hold
+    different worker counts, so the rows are padded with index -1) and the stop rule is
+    evaluated identically on every rank."""
     intervals = 0
     on_target = False
-    done = 0
+    done = [0] * group.count
     while True:
-        chunk = interval if steps is None else min(interval, worker_share(steps, world, rank) - done)
-        worker.advance(chunk)
-        done += max(chunk, 0)
+        idx = range(group.first, group.first + group.count)
+        chunk = [interval if steps is None else min(interval, worker_share(steps, total_workers, i) - d)
+                 for i, d in zip(idx, done)]
+        group.advance(chunk)
+        done = [d + max(c, 0) for d, c in zip(done, chunk)]
         intervals += 1
-        parts = [Summary.from_array(a) for a in all_gather(worker.summary().as_array())]
+        local = np.stack([s.as_array() for s in group.summaries()])
+        pad = np.full((total_workers - len(local), local.shape[1]), -1.0) if total_workers > len(local) else None
+        send = np.concatenate([local, pad]) if pad is not None else local
+        parts = [Summary.from_array(a) for g in all_gather(send) for a in np.atleast_2d(g) if a[0] >= 0]
         parts.sort(key=lambda p: p.index)
         if steps is not None:
-            if all(p.steps >= worker_share(steps, world, p.index) for p in parts):
+            if all(p.steps >= worker_share(steps, total_workers, p.index) for p in parts):
                 break
         elif all(p.nblocks > 0 for p in parts):
             value, sigma_bar, _ = merge_estimates(parts)
@@ -124,6 +186,12 @@ def drive(worker, rank: int, world: int, steps: int | None, target: float | None
     value, sigma_bar, total = merge_estimates(parts)
     return {"value": value, "sigma_bar": sigma_bar, "total_steps": total, "stopped_on_target": on_target,
             "workers": parts, "intervals": intervals}
+
+
+def drive(worker, rank: int, world: int, steps: int | None, target: float | None, interval: int,
+          all_gather, max_intervals: int | None = None) -> dict:
+    """One worker per rank (worker index = rank): drive_group with groups of one."""
+    return drive_group(_OneWorker(worker, rank), world, steps, target, interval, all_gather, max_intervals)
 
 
 def format_report(rep: dict) -> str:  # driver.cpp:523-539
@@ -163,8 +231,10 @@ def main(argv=None):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rc = parse_run_config(text)
-    worker = HostWorker(text, rank, local)
-    rep = drive(worker, rank, world, rc["steps"], rc["target"], rc["interval"], torch_all_gather(dist))
+    first, count = rank_workers(rc["workers"], world, rank)
+    group = HostGroup(text, first, count, local)
+    rep = drive_group(group, max(rc["workers"], world), rc["steps"], rc["target"], rc["interval"],
+                      torch_all_gather(dist))
     if rank == 0:
         sys.stdout.write(format_report(rep))
     dist.destroy_process_group()

@@ -1,9 +1,11 @@
 // capi.cpp — C entry points of libmcmp2host.so (include/mcmp2host.h).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/mcmp2host.h"
 #include "../csrc/philox.h"
@@ -46,9 +48,85 @@ struct mcmp2h_worker {
   std::unique_ptr<DeviceWorker> worker;
 };
 
+// the workers one process hosts on one device (distributed.py): one batched handle when the
+// walker count allows it (as the Engine does per device), else one handle per worker
+struct mcmp2h_group {
+  RunConfig cfg;
+  std::unique_ptr<SpinorSet> spinors;
+  std::unique_ptr<WeightSpec> spec;
+  std::shared_ptr<DeviceBatch> batch;
+  std::vector<std::unique_ptr<DeviceWorker>> workers;
+};
+
 extern "C" {
 
 const char* mcmp2h_last_error(void) { return g_err.c_str(); }
+
+mcmp2h_group* mcmp2h_group_create(const char* config_text, int first_index, int count, int device) {
+  mcmp2h_group* out = nullptr;
+  guard([&] {
+    if (count < 1) throw std::invalid_argument("group: at least one worker");
+    auto g = std::make_unique<mcmp2h_group>();
+    g->cfg = parse_config_text(config_text);
+    g->cfg.validate();
+    g->spinors = std::make_unique<SpinorSet>(load_spinor_set(g->cfg.spinor_path));
+    if (!g->spinors->nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
+    g->spec = std::make_unique<WeightSpec>(*g->spinors->nuclei, g->cfg.weight_overrides);
+    if (count > 1 && g->cfg.walkers % 16 == 0 && g->cfg.walkers <= 480) {
+      DeviceSystem sys = make_device_system(*g->spinors, *g->spec,
+                                            g->cfg.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
+      g->batch = std::make_shared<DeviceBatch>();
+      check_dev(mcmp2dev_create(&sys.view, device, count * g->cfg.walkers, &g->batch->h), nullptr);
+      g->batch->first = first_index;
+      g->batch->nens = count;
+      g->batch->m = g->cfg.walkers;
+    }
+    for (int k = 0; k < count; ++k) {
+      if (g->batch) g->workers.push_back(std::make_unique<DeviceWorker>(g->batch, k, g->cfg, first_index + k));
+      else g->workers.push_back(std::make_unique<DeviceWorker>(*g->spinors, *g->spec, g->cfg, first_index + k, device));
+    }
+    for (auto& w : g->workers) w->init_and_burn_in();
+    out = g.release();
+  });
+  return out;
+}
+
+void mcmp2h_group_free(mcmp2h_group* g) { delete g; }
+
+int mcmp2h_group_size(const mcmp2h_group* g) { return g ? int(g->workers.size()) : 0; }
+
+int mcmp2h_group_advance(mcmp2h_group* g, const long long* nsteps) {
+  return guard([&] {
+    std::vector<long long> n(nsteps, nsteps + g->workers.size());
+    for (auto& x : n) x = std::max<long long>(x, 0);
+    if (g->batch) {
+      std::vector<DeviceWorker*> ws;
+      for (auto& w : g->workers) ws.push_back(w.get());
+      DeviceWorker::advance_batch(*g->batch, ws, n);
+    } else {
+      for (std::size_t k = 0; k < g->workers.size(); ++k) g->workers[k]->advance(n[k]);
+    }
+  });
+}
+
+int mcmp2h_group_stats(mcmp2h_group* g, int k, double* o) {
+  return guard([&] {
+    if (k < 0 || k >= int(g->workers.size())) throw std::invalid_argument("group: no such worker");
+    const DeviceWorker& w = *g->workers[k];
+    const auto& a = w.acc;
+    o[0] = double(a.count());
+    o[1] = a.real_sum();
+    o[2] = a.imag_sum();
+    o[3] = a.mean();
+    o[4] = a.sigma_bar();
+    o[5] = double(a.in_block());
+    o[6] = a.partial();
+    o[7] = double(a.block_means().size());
+    const WorkerSummary s = w.summary();  // driver.cpp:207-216
+    o[8] = s.acceptance;
+    o[9] = s.imag_ratio;
+  });
+}
 
 int mcmp2h_run(const char* config_text, char* report, int cap) {
   return guard([&] { copy_out(format_report(run(parse_config_text(config_text))), report, cap); });

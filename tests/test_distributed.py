@@ -63,6 +63,57 @@ class OracleStandIn:
         return D.Summary(self.index, a.n, a.mean(), a.sigma_bar(), 0.0, ratio, len(a.means))
 
 
+class OracleGroupStandIn:
+    """Several stand-in workers on one rank (the HostGroup interface)."""
+
+    def __init__(self, spinor, conf, first, count, m, burn, steps, total_workers, seed, block):
+        self.first, self.count = first, count
+        self.ws = [OracleStandIn(spinor, conf, first + k, m, burn,
+                                 D.worker_share(steps, total_workers, first + k), seed, block) for k in range(count)]
+
+    def advance(self, nsteps):
+        for w, n in zip(self.ws, nsteps):
+            w.advance(n)
+
+    def summaries(self):
+        return [w.summary() for w in self.ws]
+
+
+def _group_rank(rank, world, port, args, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spinor, conf, m, burn, steps, interval, seed, block, workers = args
+    first, count = D.rank_workers(workers, world, rank)
+    g = OracleGroupStandIn(spinor, conf, first, count, m, burn, steps, workers, seed, block)
+    rep = D.drive_group(g, workers, steps, None, interval, D.torch_all_gather(dist))
+    q.put((rank, rep["value"], rep["sigma_bar"], rep["total_steps"], [(p.index, p.steps) for p in rep["workers"]]))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_with_several_workers_each(cfgdir):
+    """workers 5 over 2 ranks: ranks host workers [0, 3) and [3, 5) (the device path batches
+    them in one handle per rank); the merge equals the oracle Engine with workers 5."""
+    spinor = cfgdir / "syn1c.spinor"
+    conf = "walkers 6\nburnin 30\nblocksize 10\ncheckpoint-interval 40\nseed 4\n"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = (str(spinor), conf, 6, 30, 203, 40, 4, 10, 5)
+    procs = [ctx.Process(target=_group_rank, args=(r, 2, port, args, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert out[0][1:4] == out[1][1:4]
+    assert [w for w in out[0][4]] == [(0, 41), (1, 41), (2, 41), (3, 40), (4, 40)]
+    ref = parse_report(oracle_report(spinor, conf, "steps 203\nworkers 5\n"))
+    assert out[0][3] == ref["steps"] == 203
+    assert out[0][1] == pytest.approx(ref["value"], rel=1e-14, abs=0)
+    assert out[0][2] == pytest.approx(ref["sigma_bar"], rel=1e-12, abs=0)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -140,3 +191,37 @@ def test_two_ranks_target_error_stop(cfgdir):
     assert out[0][3] == 100  # both ranks at the first interval with blocks: 2 x 50
     ref = parse_report(oracle_report(spinor, conf, "target-rel-err 2.0\nworkers 2\n"))
     assert ref["steps"] == 100 and out[0][1] == pytest.approx(ref["value"], rel=1e-14)
+
+
+def _device_rank(rank, world, port, text, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rc = D.parse_run_config(text)
+    first, count = D.rank_workers(rc["workers"], world, rank)
+    g = D.HostGroup(text, first, count, 0)  # both ranks on cuda:0 (no kernel waits on another rank)
+    rep = D.drive_group(g, rc["workers"], rc["steps"], rc["target"], rc["interval"], D.torch_all_gather(dist))
+    q.put((rank, D.format_report(rep)))
+    g.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_device_groups_over_two_ranks_match_the_engine(cfgdir):
+    """torch.distributed (gloo, 2 ranks on one GPU) with HostGroup: 4 cfg1 workers as two batched
+    handles of 2 give the same report as the C++ Engine running the 4 workers in one batch."""
+    from paper_2203_05632_b200 import walker
+    text = (f"spinors {cfgdir / 'cfg1.spinor'}\nsteps 1002\nwalkers 16\nworkers 4\nseed 9\nburnin 50\n"
+            "checkpoint-interval 200\nstep-size 0.3\n" +
+            "".join(l + "\n" for l in (cfgdir / "cfg1.conf").read_text().splitlines() if l.startswith("weight")))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_rank, args=(r, 2, port, text, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert out[0][1] == out[1][1]
+    assert out[0][1] == walker.run_config_text(text)
