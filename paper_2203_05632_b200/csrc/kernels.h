@@ -87,6 +87,13 @@ cudaError_t pair_kernel_setup();
 // Kramers-restricted variant (pair_kr.cu): half the DMMA work for time-reversal-paired columns
 void launch_pair_kr(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kr_kernel_setup();
+// QB = 1 build of pair_kr.cu (8 x 8 tiles, two CTAs per SM) for ensembles of fewer than 64 walkers
+void launch_pair_kr_qb1(const PairParams& P, cudaStream_t s);
+cudaError_t pair_kr_kernel_setup_qb1();
+double pair_kr_block_tiles_qb1(int nb);
+int pair_kr_tiles_qb1(int nb);
+int pair_kr_consumers_qb1();
+void pair_kr_ring_qb1(int max_width, int& ring, int& ring_doubles);
 double pair_kr_block_tiles(int nb);
 int pair_kr_tiles(int nb);      // tiles of one ensemble of nb walker blocks
 int pair_kr_consumers();        // DMMA warps per pair_kr CTA (per-tile partials in batched mode)

@@ -173,6 +173,8 @@ struct mcmp2dev_handle {
     return P;
   }
 
+  static bool kr_qb1(int mm) { return mm < 64; }
+
   void launch_estimate(const WalkerBuf& wb, int mm, double* step_out, int ne = 1) {
     SpinorParams s = kramers ? sp_kr : sp;
     s.npts = 2 * mm * ne;
@@ -187,9 +189,11 @@ struct mcmp2dev_handle {
     p.npts_pad = npts_pad;
     p.Go = Go;
     p.Gv = Gv;
+    const bool qb1 = kr_qb1(mm);  // small ensembles: the QB = 1 build of pair_kr.cu
     {
       const int wmax = std::min(KC4, std::max(Go, Gv));
-      pair_kr_ring(wmax > 0 ? wmax : 1, p.ring, p.ring_doubles);
+      if (qb1) pair_kr_ring_qb1(wmax > 0 ? wmax : 1, p.ring, p.ring_doubles);
+      else pair_kr_ring(wmax > 0 ? wmax : 1, p.ring, p.ring_doubles);
     }
     p.m = mm;
     p.nb = (mm + WB - 1) / WB;
@@ -203,8 +207,9 @@ struct mcmp2dev_handle {
     p.partials = ne > 1 ? d_bpart : d_partials;
     p.step_out = step_out;
     p.nens = ne;
-    p.ens_tiles = ne > 1 ? (kramers ? pair_kr_tiles(p.nb) : p.nb * (p.nb + 1) / 2) : 0;
-    if (kramers) launch_pair_kr(p, stream);
+    p.ens_tiles = ne > 1 ? (kramers ? (qb1 ? pair_kr_tiles_qb1(p.nb) : pair_kr_tiles(p.nb)) : p.nb * (p.nb + 1) / 2) : 0;
+    if (kramers && qb1) launch_pair_kr_qb1(p, stream);
+    else if (kramers) launch_pair_kr(p, stream);
     else launch_pair(p, stream);
     if (prof) {
       ck(cudaEventRecord(ev[3], stream), "event");
@@ -394,6 +399,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(pair_kernel_setup(), "pair kernel attributes");
   ck(spinor_kernel_setup(), "spinor kernel attributes");
   ck(pair_kr_kernel_setup(), "pair_kr kernel attributes");
+  ck(pair_kr_kernel_setup_qb1(), "pair_kr (QB 1) kernel attributes");
   for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
 
   h->ncomp = s->ncomp;
@@ -515,7 +521,9 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   h->sp_kr = sp;
   build_groups(h->sp, s, ch_off, false, ptf_max, o);
   if (h->kramers_eligible) build_groups(h->sp_kr, s, ch_off, true, ptf_max, o);
-  const size_t ntiles = size_t(h->nbmax) * (h->nbmax + 1) / 2;
+  // per-CTA partials: the grid of any pair kernel is at most its tile count
+  const size_t ntiles = std::max({size_t(h->nbmax) * (h->nbmax + 1) / 2, size_t(pair_kr_tiles(h->nbmax)),
+                                  size_t(pair_kr_tiles_qb1(h->nbmax))});
   h->d_partials = dalloc<double>(ntiles * 4, o);
   h->d_steps = dalloc<double>(size_t(kChunk) * 6, o);
   h->d_gsteps = dalloc<double>(size_t(kGraphSteps) * 6, o);
@@ -836,7 +844,8 @@ int mcmp2dev_prepare(mcmp2dev_t* h) {
 int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
   return guard(h, [&] {
     const int nb = (h->m + WB - 1) / WB;
-    const double ntiles = h->kramers ? pair_kr_block_tiles(nb) : 0.5 * nb * (nb + 1);
+    const double ntiles = h->kramers ? (mcmp2dev_handle::kr_qb1(h->m) ? pair_kr_block_tiles_qb1(nb) : pair_kr_block_tiles(nb))
+                                     : 0.5 * nb * (nb + 1);
     // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
     const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
@@ -860,8 +869,9 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
     h->rstream = stream0;
     if (nens > 1) {
       const int nb = (m + WB - 1) / WB;  // per-tile partials of either pair kernel
-      const size_t part = size_t(nens) * std::max(size_t(pair_kr_tiles(nb)) * pair_kr_consumers() * 2,
-                                                  size_t(nb) * (nb + 1) / 2 * pair_consumers() * 4);
+      const size_t part = size_t(nens) * std::max({size_t(pair_kr_tiles(nb)) * pair_kr_consumers() * 2,
+                                                   size_t(pair_kr_tiles_qb1(nb)) * pair_kr_consumers_qb1() * 2,
+                                                   size_t(nb) * (nb + 1) / 2 * pair_consumers() * 4});
       if (part > h->bpart_cap) {
         if (h->d_bpart) cudaFree(h->d_bpart);
         h->d_bpart = nullptr;

@@ -34,6 +34,18 @@ using namespace pairk;
 #ifndef KR_STAGES
 #define KR_STAGES 2
 #endif
+// This file is compiled twice (csrc/Makefile): the default QB = 2 build, and with
+// -DKR_QB1_VARIANT a QB = 1 build whose entry points carry the suffix _qb1 (kernel
+// pair_kr_kernel_qb1). The host takes the QB = 1 variant for ensembles of fewer than 64 walkers:
+// 8 x 8 tiles waste fewer pairs of the small triangles and two CTAs per SM overlap the short
+// tiles' latencies (batched cfg1, m = 16: pair stage 0.157 -> 0.115 ms at 1184 ensembles), while
+// larger m keeps QB = 2 (batched cfg2: 0.146 vs 0.154 ms; cfg4: 4.09 vs 4.18 ms).
+#ifdef KR_QB1_VARIANT
+#define KR_QB 1
+#define KR_API(name) name##_qb1
+#else
+#define KR_API(name) name
+#endif
 #ifndef KR_QB
 // Q-side walker blocks (of WB) per tile: tile = 8 QB Q walkers x 8 P walkers. Measured cfg4:
 // QB 2 (16 DMMA warps, 1 CTA/SM, 25% less stage traffic per DMMA) 4.09 ms, QB 1 (2 CTAs/SM) 4.18 ms
@@ -129,7 +141,7 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 }  // namespace
 
 template <bool PHYS>
-__global__ void __launch_bounds__(THREADS, MINB) pair_kr_kernel(PairParams P) {
+__global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);
@@ -529,35 +541,35 @@ namespace {
 int g_sms_kr[64];
 }
 
-double pair_kr_block_tiles(int nb) { return double(kr_ntiles(nb)) * QB; }
-int pair_kr_tiles(int nb) { return kr_ntiles(nb); }
-int pair_kr_consumers() { return CONSUMERS; }
+double KR_API(pair_kr_block_tiles)(int nb) { return double(kr_ntiles(nb)) * QB; }
+int KR_API(pair_kr_tiles)(int nb) { return kr_ntiles(nb); }
+int KR_API(pair_kr_consumers)() { return CONSUMERS; }
 
-void pair_kr_ring(int max_width, int& ring, int& ring_doubles) {
+void KR_API(pair_kr_ring)(int max_width, int& ring, int& ring_doubles) {
   ring_doubles = (QPTS + HALF_PTS) * max_width * 32;
   ring = (STAGES * STAGE_DOUBLES) / ring_doubles;
   if (ring > MAX_RING) ring = MAX_RING;
 }
 
-cudaError_t pair_kr_kernel_setup() {
+cudaError_t KR_API(pair_kr_kernel_setup)() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_kr[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaFuncSetAttribute(pair_kr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(KR_API(pair_kr_kernel)<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(pair_kr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  return cudaFuncSetAttribute(KR_API(pair_kr_kernel)<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
-void launch_pair_kr(const PairParams& P, cudaStream_t s) {
+void KR_API(launch_pair_kr)(const PairParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int ntiles = P.nens > 1 ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   const int grid = ntiles < slots ? ntiles : slots;
   if (P.physical)
-    pair_kr_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(P);
+    KR_API(pair_kr_kernel)<true><<<grid, THREADS, SMEM_BYTES, s>>>(P);
   else
-    pair_kr_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(P);
+    KR_API(pair_kr_kernel)<false><<<grid, THREADS, SMEM_BYTES, s>>>(P);
 }
 
 }  // namespace mcmp2dev

@@ -22,6 +22,8 @@ def rel_err(got, ref):
     ("cfg1", 16, 5, 60, 40, 0.3, False),
     ("cfg2", 16, 3, 30, 6, 0.0, False),
     ("cfg2", 32, 2, 30, 4, 0.0, True),
+    ("cfg2", 64, 2, 30, 3, 0.0, False),   # m >= 64: the QB = 2 build of pair_kr.cu
+    ("cfg2", 80, 2, 30, 2, 0.0, True),
 ])
 def test_batched_ensembles_follow_oracle_chains(cfgdir, name, m, nens, burn, nsteps, step, physical):
     sp = cfgdir / f"{name}.spinor"
