@@ -173,7 +173,13 @@ struct mcmp2dev_handle {
     return P;
   }
 
-  static bool kr_qb1(int mm) { return mm < 64; }
+  // the QB = 1 build of pair_kr.cu (8 x 8 tiles, 2 CTAs/SM) for small ensembles (m < 64) and when
+  // the QB = 2 tiles would not cover the SMs (single cfg2, m = 128: 72 tiles; 197 -> 211 M samples/s);
+  // measured slower for batched cfg2 (x4: 370 vs 354 M) and cfg3 (0.171 vs 0.191 ms)
+  int sms = 148;
+  bool kr_qb1(int mm, int ne = 1) const {
+    return mm < 64 || double(ne) * pair_kr_tiles((mm + WB - 1) / WB) < sms;
+  }
 
   void launch_estimate(const WalkerBuf& wb, int mm, double* step_out, int ne = 1) {
     SpinorParams s = kramers ? sp_kr : sp;
@@ -189,7 +195,7 @@ struct mcmp2dev_handle {
     p.npts_pad = npts_pad;
     p.Go = Go;
     p.Gv = Gv;
-    const bool qb1 = kr_qb1(mm);  // small ensembles: the QB = 1 build of pair_kr.cu
+    const bool qb1 = kr_qb1(mm, ne);
     {
       const int wmax = std::min(KC4, std::max(Go, Gv));
       if (qb1) pair_kr_ring_qb1(wmax > 0 ? wmax : 1, p.ring, p.ring_doubles);
@@ -516,6 +522,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "SM count");
     sp.mo_slots = sms * mo_ctas_per_sm();
+    h->sms = sms;
   }
   sp.st = h->d_state;
   h->sp_kr = sp;
@@ -844,7 +851,7 @@ int mcmp2dev_prepare(mcmp2dev_t* h) {
 int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
   return guard(h, [&] {
     const int nb = (h->m + WB - 1) / WB;
-    const double ntiles = h->kramers ? (mcmp2dev_handle::kr_qb1(h->m) ? pair_kr_block_tiles_qb1(nb) : pair_kr_block_tiles(nb))
+    const double ntiles = h->kramers ? (h->kr_qb1(h->m, h->nens) ? pair_kr_block_tiles_qb1(nb) : pair_kr_block_tiles(nb))
                                      : 0.5 * nb * (nb + 1);
     // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
