@@ -32,7 +32,7 @@ constexpr int CHI_PTS = 8;
 // 512 -> 0.166 / 0.026 (the basis loops are latency-bound: more threads per 8 points)
 #define CHI_THREADS_N 512
 #endif
-constexpr int CHI_THREADS = CHI_THREADS_N;
+constexpr int CHI_THREADS = CHI_THREADS_N;  // default; chi_kernel is a template on its thread count
 #ifndef CHI_UNROLL
 #define CHI_UNROLL 1
 #endif
@@ -102,6 +102,7 @@ __device__ double solid_harmonic(int l, int m, double x, double y, double z) {
 }
 }  // namespace
 
+template <int CHI_THREADS>
 __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
   extern __shared__ double smem[];
   double* s_pos = smem;              // [CHI_PTS][3]
@@ -340,14 +341,21 @@ __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P)
 int spinor_smem_bytes(const SpinorParams& P) { return int(sizeof(double)) * (3 * CHI_PTS + P.nuniq * CHI_PTS); }
 
 cudaError_t spinor_kernel_setup() {
-  cudaError_t e = cudaFuncSetAttribute(chi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(chi_kernel<CHI_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(chi_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(mo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MO_SMEM);
 }
 
 void launch_spinor(const SpinorParams& P, cudaStream_t s) {
   const int ptf = (P.npts + CHI_PTS - 1) / CHI_PTS;
-  chi_kernel<<<ptf, CHI_THREADS, spinor_smem_bytes(P), s>>>(P);
+  // small bases (few values per 8-point fragment, e.g. cfg1: 384 values + 96 exps): 128 threads
+  // per fragment, more CTAs resident per SM; measured (cfg1 x 1184 ensembles) in profiles/README
+  int work = P.nuniq * CHI_PTS;
+  for (int g = 0; g < P.ngroups; ++g) work += P.grp_k4[g] * 32;
+  if (work <= 640) chi_kernel<128><<<ptf, 128, spinor_smem_bytes(P), s>>>(P);
+  else chi_kernel<CHI_THREADS><<<ptf, CHI_THREADS, spinor_smem_bytes(P), s>>>(P);
   SpinorParams q = P;
   const int ptiles = (P.npts + 8 * MO_PTF - 1) / (8 * MO_PTF);  // tiles are numbered group-major, so the tile range of
   int total = 0;                            // this launch's point count is recomputed here
