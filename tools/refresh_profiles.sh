@@ -12,6 +12,11 @@ python bench.py > $OUT/${TAG}_bench_cfg4.json 2> $OUT/${TAG}_bench_cfg4.err
 for c in cfg1 cfg2 cfg3; do
   python bench.py --config $c --steps 200 --no-cpu-baseline > $OUT/${TAG}_bench_$c.json 2> $OUT/${TAG}_bench_$c.err
 done
+# several reference workers per GPU as one batched handle
+python bench.py --config cfg1 --ensembles 1184 --steps 200 --no-cpu-baseline > $OUT/${TAG}_bench_cfg1_batched.json 2> $OUT/${TAG}_bench_cfg1_batched.err
+python bench.py --config cfg2 --ensembles 16 --steps 200 --no-cpu-baseline > $OUT/${TAG}_bench_cfg2_batched.json 2> $OUT/${TAG}_bench_cfg2_batched.err
+python tools/batch_scan.py cfg1 --nens 1,16,64,148,296,592,1184 --out $OUT/${TAG}_batch_cfg1.json > /dev/null 2>&1
+python tools/batch_scan.py cfg2 --nens 1,4,8,16,32 --out $OUT/${TAG}_batch_cfg2.json > /dev/null 2>&1
 # launch list of the bench command itself (cold-cache, serialised per-launch times)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches_cfg4.csv \
   python bench.py --steps 3 --warmup 3 --burnin 20 --no-cpu-baseline > $OUT/${TAG}_ncu_launches.log 2>&1
