@@ -18,6 +18,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "philox.h"
 
 namespace mcmp2dev {
@@ -57,6 +59,44 @@ struct PhiChunks {
     return (size_t(f) * npts_pad + size_t(pt) * width(c) + (g - f)) * 32;
   }
 };
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel of a step is launched with programmatic stream serialization (pdl_launch) and
+// starts with pdl_wait(): griddepcontrol.wait blocks until the preceding kernel has completed and
+// its memory is visible (a no-op for a normal launch), so correctness is that of plain stream
+// order, while the launch of a kernel overlaps the tail of the previous one. pdl_trigger()
+// (griddepcontrol.launch_dependents) lets the next kernel launch once every CTA has passed it.
+#ifndef MCMP2_PDL
+#define MCMP2_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if MCMP2_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if MCMP2_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = MCMP2_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+#endif
 
 // ------------------------------------------------------------------ device system
 struct DevSites {

@@ -54,6 +54,8 @@ using namespace pairk;
 
 template <bool PHYS>
 __global__ void __launch_bounds__(THREADS, 1) pair_kernel(PairParams P) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int STAGES = Cfg<PHYS>::STAGES;
   extern __shared__ __align__(128) double sm[];
   double* const sO = sm + STAGES * STAGE_DOUBLES;  // [warp][e][qi][pj][y][x] complex o
@@ -456,9 +458,10 @@ int pair_grid(int nb, int nens, int ens_tiles) {
 
 void launch_pair(const PairParams& P, cudaStream_t s) {
   if (P.physical)
-    pair_kernel<true><<<pair_grid(P.nb, P.nens, P.ens_tiles), THREADS, Cfg<true>::SMEM_BYTES, s>>>(P);
+    pdl_launch(pair_kernel<true>, dim3(pair_grid(P.nb, P.nens, P.ens_tiles)), dim3(THREADS), Cfg<true>::SMEM_BYTES, s, P);
   else
-    pair_kernel<false><<<pair_grid(P.nb, P.nens, P.ens_tiles), THREADS, Cfg<false>::SMEM_BYTES, s>>>(P);
+    pdl_launch(pair_kernel<false>, dim3(pair_grid(P.nb, P.nens, P.ens_tiles)), dim3(THREADS), Cfg<false>::SMEM_BYTES,
+               s, P);
 }
 
 int pair_consumers() { return CONSUMERS; }

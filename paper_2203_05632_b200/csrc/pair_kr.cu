@@ -142,6 +142,8 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 
 template <bool PHYS>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
+  pdl_wait();     // Phi of this step is visible
+  pdl_trigger();  // persistent: the next step's walk may launch next to it
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);
@@ -567,9 +569,9 @@ void KR_API(launch_pair_kr)(const PairParams& P, cudaStream_t s) {
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   const int grid = ntiles < slots ? ntiles : slots;
   if (P.physical)
-    KR_API(pair_kr_kernel)<true><<<grid, THREADS, SMEM_BYTES, s>>>(P);
+    pdl_launch(KR_API(pair_kr_kernel)<true>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
   else
-    KR_API(pair_kr_kernel)<false><<<grid, THREADS, SMEM_BYTES, s>>>(P);
+    pdl_launch(KR_API(pair_kr_kernel)<false>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
 }
 
 }  // namespace mcmp2dev

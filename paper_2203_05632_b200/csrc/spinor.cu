@@ -104,6 +104,7 @@ __device__ double solid_harmonic(int l, int m, double x, double y, double z) {
 
 template <int CHI_THREADS>
 __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
+  pdl_wait();  // this step's walkers are visible
   extern __shared__ double smem[];
   double* s_pos = smem;              // [CHI_PTS][3]
   double* s_exp = s_pos + 3 * CHI_PTS;  // [nuniq][CHI_PTS]
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(CHI_THREADS) chi_kernel(SpinorParams P) {
       A[k4 * MO_PTF * 32 + l] = v;
     }
   }
+  pdl_trigger();  // several waves: the MO transform launches once every CTA is done
 }
 
 // MO transform: persistent, warp-specialised. Tile = 64 points (8 point fragments) x 8 n
@@ -177,6 +179,8 @@ __device__ __forceinline__ void mo_decode(const SpinorParams& P, int t, int& g, 
 }
 
 __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P) {
+  pdl_wait();     // chi of this step is visible
+  pdl_trigger();  // persistent: the pair kernel may launch (it cannot co-reside, so it waits)
   extern __shared__ __align__(128) double mo_sm[];
   uint64_t* const full = reinterpret_cast<uint64_t*>(mo_sm + MO_STAGES * MO_STAGE);
   uint64_t* const empty = full + MO_STAGES;
@@ -354,8 +358,8 @@ void launch_spinor(const SpinorParams& P, cudaStream_t s) {
   // per fragment, more CTAs resident per SM; measured (cfg1 x 1184 ensembles) in profiles/README
   int work = P.nuniq * CHI_PTS;
   for (int g = 0; g < P.ngroups; ++g) work += P.grp_k4[g] * 32;
-  if (work <= 640) chi_kernel<128><<<ptf, 128, spinor_smem_bytes(P), s>>>(P);
-  else chi_kernel<CHI_THREADS><<<ptf, CHI_THREADS, spinor_smem_bytes(P), s>>>(P);
+  if (work <= 640) pdl_launch(chi_kernel<128>, dim3(ptf), dim3(128), spinor_smem_bytes(P), s, P);
+  else pdl_launch(chi_kernel<CHI_THREADS>, dim3(ptf), dim3(CHI_THREADS), spinor_smem_bytes(P), s, P);
   SpinorParams q = P;
   const int ptiles = (P.npts + 8 * MO_PTF - 1) / (8 * MO_PTF);  // tiles are numbered group-major, so the tile range of
   int total = 0;                            // this launch's point count is recomputed here
@@ -366,7 +370,7 @@ void launch_spinor(const SpinorParams& P, cudaStream_t s) {
   q.mo_ntiles = total;
   int grid = P.mo_slots;
   if (grid > total) grid = total;
-  mo_kernel<<<grid, MO_THREADS, MO_SMEM, s>>>(q);
+  pdl_launch(mo_kernel, dim3(grid), dim3(MO_THREADS), MO_SMEM, s, q);
 }
 
 int mo_ctas_per_sm() { return MO_CTAS; }

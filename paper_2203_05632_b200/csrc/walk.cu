@@ -180,6 +180,8 @@ __device__ double draw_tau(const WalkParams& P, unsigned long long pos, DevState
 }
 
 __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(WalkParams P) {
+  pdl_wait();     // the previous kernel's walkers / state are visible
+  pdl_trigger();  // one wave: the next kernel may launch and wait for this one
   __shared__ int s_acc[WALK_THREADS / 32];
   __shared__ bool s_last;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -349,6 +351,8 @@ __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(WalkParams P) {
 // last warp draws tau speculatively; the CTA itself does the bookkeeping that walk_kernel's last
 // CTA does (sampler.cpp:49-93, driver.cpp:444-445), including the sequential redo.
 __global__ void walk_batch_kernel(WalkParams P) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_acc;
   __shared__ int s_redo;
   __shared__ double s_tau;
@@ -491,6 +495,8 @@ __global__ void walk_batch_kernel(WalkParams P) {
 
 // replay: positions/g from the caller, tau given (estimator input of mc_step_estimate)
 __global__ void replay_load_kernel(WalkParams P, const double* walkers, double tau) {
+  pdl_wait();
+  pdl_trigger();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < P.m) {
     for (int k = 0; k < 8; ++k) P.out.at(k, p) = walkers[size_t(p) * 8 + k];
@@ -509,17 +515,17 @@ void launch_walk(const WalkParams& P, cudaStream_t s) {
   // that fit one CTA: no cross-CTA last-CTA round trip
   if (P.nens > 1 || P.m <= 496) {
     const int threads = (2 * P.m + 31) / 32 * 32 + 32;
-    walk_batch_kernel<<<P.nens, threads, 0, s>>>(P);
+    pdl_launch(walk_batch_kernel, dim3(P.nens), dim3(threads), 0, s, P);
     return;
   }
   const int blocks = (2 * P.m + WALK_THREADS - 1) / WALK_THREADS + (P.mode == WALK_PRODUCTION ? 1 : 0);
-  walk_kernel<<<blocks, WALK_THREADS, 0, s>>>(P);
+  pdl_launch(walk_kernel, dim3(blocks), dim3(WALK_THREADS), 0, s, P);
 }
 
 void launch_replay_load(const WalkParams& P, const double* walkers, double tau, cudaStream_t s) {
   const int threads = 128;
   const int blocks = (P.m + threads - 1) / threads;
-  replay_load_kernel<<<blocks, threads, 0, s>>>(P, walkers, tau);
+  pdl_launch(replay_load_kernel, dim3(blocks), dim3(threads), 0, s, P, walkers, tau);
 }
 
 }  // namespace mcmp2dev
