@@ -256,12 +256,14 @@ void DeviceWorker::init_and_burn_in() {  // driver.cpp:354-358 (+ step-size exte
     if (batch_->ready) return;
     check_dev(mcmp2dev_init_batch(h_, batch_->nens, walkers_, cfg_->seed, std::uint32_t(batch_->first)), h_);
     batch_->ready = true;
+    batch_->states_valid = false;
   } else {
     check_dev(mcmp2dev_init_ensemble(h_, walkers_, cfg_->seed, std::uint32_t(index_)), h_);
   }
   if (cfg_->step_size) check_dev(mcmp2dev_set_sigma_step(h_, *cfg_->step_size), h_);
   check_dev(mcmp2dev_burn_in(h_, cfg_->burn_in, cfg_->step_size ? 0 : 1), h_);
   check_dev(mcmp2dev_prepare(h_), h_);
+  if (batch_) batch_->states_valid = false;
 }
 
 void DeviceWorker::advance(long long nsteps) {  // driver.cpp:440-450
@@ -289,6 +291,7 @@ void DeviceWorker::advance_batch(DeviceBatch& b, const std::vector<DeviceWorker*
     for (int e = 0; e < na; ++e) n = std::min(n, nsteps[e] - done);
     b.values.resize(std::size_t(n) * b.nens);
     b.imags.resize(std::size_t(n) * b.nens);
+    b.states_valid = false;
     check_dev(mcmp2dev_advance_batch(b.h, long(n), na, b.values.data(), b.imags.data()), b.h);
     for (int e = 0; e < na; ++e) {
       DeviceWorker& w = *ws[e];
@@ -299,9 +302,27 @@ void DeviceWorker::advance_batch(DeviceBatch& b, const std::vector<DeviceWorker*
   }
 }
 
+const mcmp2dev_ensemble& DeviceBatch::state(int ens) {
+  if (!states_valid) {
+    states.assign(std::size_t(nens), mcmp2dev_ensemble{});
+    state_walkers.resize(std::size_t(nens) * m * 9);
+    for (int k = 0; k < nens; ++k) states[k].walkers = state_walkers.data() + std::size_t(k) * m * 9;
+    check_dev(mcmp2dev_get_ensembles(h, states.data()), h);
+    states_valid = true;
+  }
+  return states[std::size_t(ens)];
+}
+
 void DeviceWorker::get_state(mcmp2dev_ensemble* e) const {
-  if (batch_) check_dev(mcmp2dev_get_ensemble_at(h_, ens_, e), h_);
-  else check_dev(mcmp2dev_get_ensemble(h_, e), h_);
+  if (batch_) {
+    const mcmp2dev_ensemble& s = batch_->state(ens_);
+    double* w = e->walkers;
+    *e = s;
+    e->walkers = w;
+    std::copy(s.walkers, s.walkers + std::size_t(s.m) * 9, w);
+  } else {
+    check_dev(mcmp2dev_get_ensemble(h_, e), h_);
+  }
 }
 
 double DeviceWorker::acceptance() const {
@@ -352,6 +373,7 @@ void DeviceWorker::load_ensemble(const std::string& text) {  // sampler.cpp:107-
       check_dev(mcmp2dev_init_batch(h_, batch_->nens, walkers_, cfg_->seed, std::uint32_t(batch_->first)), h_);
       batch_->ready = true;
     }
+    batch_->states_valid = false;
     check_dev(mcmp2dev_set_ensemble_at(h_, ens_, &e), h_);
   } else {
     check_dev(mcmp2dev_set_ensemble(h_, &e), h_);

@@ -190,6 +190,13 @@ struct DeviceBatch {
   int first = 0, nens = 0, m = 0;
   bool ready = false;  // init_batch done
   std::vector<double> values, imags;
+  // every ensemble's state in one bulk copy (mcmp2dev_get_ensembles), reused until the batch
+  // advances or an ensemble is loaded: reports, traces and checkpoints of k workers cost two
+  // device copies instead of k x 10
+  std::vector<mcmp2dev_ensemble> states;
+  std::vector<double> state_walkers;
+  bool states_valid = false;
+  const mcmp2dev_ensemble& state(int ens);
   DeviceBatch() = default;
   DeviceBatch(const DeviceBatch&) = delete;
   DeviceBatch& operator=(const DeviceBatch&) = delete;
