@@ -19,7 +19,9 @@ struct U32x4 {
 
 MCMP2_HD inline U32x4 philox_block(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                               uint32_t k0, uint32_t k1) {
+#if defined(__CUDACC__)
 #pragma unroll
+#endif
   for (int r = 0; r < 10; ++r) {
     if (r) {
       k0 += 0x9E3779B9u;
@@ -51,7 +53,11 @@ struct StreamReader {
   uint64_t cached_block;
   U32x4 buf;
   MCMP2_HD StreamReader(uint32_t k0_, uint32_t k1_, uint32_t s_, uint64_t pos_)
-      : k0(k0_), k1(k1_), stream(s_), pos(pos_), cached_block(~uint64_t(0)) {}
+      : k0(k0_), k1(k1_), stream(s_), pos(pos_), cached_block(~uint64_t(0)) {
+#if !defined(__CUDA_ARCH__)
+    buf = U32x4{{0u, 0u, 0u, 0u}};  // host: never read before the first refill; keeps -Wall quiet
+#endif
+  }
   MCMP2_HD uint32_t next_u32() {
     const uint64_t b = pos >> 2;
     if (b != cached_block) {
