@@ -1,0 +1,91 @@
+"""Precision budget of the planned INT8 tensor-core pair kernel: the O and V
+blocks of a cfg4 step computed as Ozaki-style sums of exact int8 x int8 -> int products (each
+FP64 operand row scaled by its power-of-two maximum and cut into S slices of 7 bits, slice
+products kept for s + t < S) instead of FP64 products, then contracted exactly as the reference
+does (estimator.cpp:15-33). The oracle's spinor values at the oracle's walker positions are the
+input; the FP64 restatement is checked against the oracle's own step value first.
+
+Measured (cfg4, m = 32, two steps): relative error of the step value 6e-8 / 3e-7 (S = 4),
+5e-10 / 3e-9 (5), 4e-12 / 3e-11 (6), 4e-14 / 3e-13 (7): S = 6 (21 slice products) meets the
+1e-10 replay gate, S = 5 does not."""
+import numpy as np
+import pytest
+
+import oracle_py
+
+M = 32
+
+
+@pytest.fixture(scope="module")
+def step_inputs(cfgdir):
+    sp = cfgdir / "cfg4.spinor"
+    orc = oracle_py.OracleSystem(sp, (cfgdir / "cfg4.conf").read_text())
+    tr = orc.trajectory(seed=5, stream=0, m=M, burn=20, nsteps=2)
+    tok = sp.read_text().split()
+    i = tok.index("energies")
+    no, nv = int(tok[i + 1]), int(tok[i + 2])
+    eps = np.array(tok[i + 3:i + 3 + no + nv], dtype=float)
+    out = []
+    for k in range(2):
+        W, tau = tr["walkers"][k], tr["tau"][k]
+        pts = np.empty((2 * M, 3))
+        pts[0::2], pts[1::2] = W[:, 0:3], W[:, 3:6]   # point 2p <- r1, 2p+1 <- r2 (estimator.cpp:39-42)
+        occ, vir = orc.evaluate(pts)
+        ao = (occ * np.exp(0.5 * eps[:no] * tau)).reshape(8 * M, no)   # greens.cpp:63-71
+        av = (vir * np.exp(-0.5 * eps[no:] * tau)).reshape(8 * M, nv)
+        step_const = orc.ng ** 2 / (orc.lambda_ * np.exp(-orc.lambda_ * tau)) / (0.5 * M * (M - 1))  # estimator.cpp:55-61
+        out.append((ao, av, W, tr["est"][k, 0], step_const))
+    return out
+
+
+def contract(O, V, W):
+    """sum over p < q of the literal pair term without the step constant N_g^2 / (w(tau) C(m,2))"""
+    blk = lambda A, r, c: A[4 * r:4 * r + 4, 4 * c:4 * c + 4]  # noqa: E731
+    tot = 0.0
+    for p in range(M):
+        for q in range(p + 1, M):
+            a, b, c, d = 2 * p, 2 * p + 1, 2 * q, 2 * q + 1
+            o1, o2 = blk(O, a, c), blk(O, b, d)
+            f1d, f2d = (o1 * blk(V, c, a)).sum(), (o2 * blk(V, d, b)).sum()
+            f1x, f2x = (o1 * blk(V, d, a)).sum(), (o2 * blk(V, c, b)).sum()
+            tot += (-0.5 * f1d * f2d + 0.5 * f1x * f2x) / (W[p, 6] * W[p, 7] * W[q, 6] * W[q, 7])
+    return tot
+
+
+def slices(X, S):
+    mx = np.max(np.abs(X), axis=1)
+    e = np.ceil(np.log2(np.where(mx > 0, mx, 1.0)))
+    r = X / (2.0 ** e)[:, None]
+    out = []
+    for _ in range(S):
+        r = r * 128.0
+        q = np.trunc(r)
+        out.append(q.astype(np.int64))   # |q| <= 127: an int8 slice
+        r = r - q
+    return out, e
+
+
+def ozaki_real(X, Y, S):
+    xs, ex = slices(X, S)
+    ys, ey = slices(Y, S)
+    C = np.zeros((X.shape[0], Y.shape[0]))
+    for s in range(S):
+        for t in range(S - s):
+            C += (xs[s] @ ys[t].T).astype(np.float64) * 2.0 ** (-7 * (s + t + 2))   # exact int products
+    return C * (2.0 ** ex)[:, None] * (2.0 ** ey)[None, :]
+
+
+def ozaki(A, B, S):  # A B^H with four real emulated products
+    re = ozaki_real(A.real, B.real, S) + ozaki_real(A.imag, B.imag, S)
+    im = ozaki_real(A.imag, B.real, S) - ozaki_real(A.real, B.imag, S)
+    return re + 1j * im
+
+
+def test_slice_budget(step_inputs):
+    for ao, av, W, ref, step_const in step_inputs:
+        exact = contract(ao @ ao.conj().T, av @ av.conj().T, W)
+        # the FP64 restatement is the oracle's step value (to the reference's rounding)
+        assert abs(exact.real * step_const / ref - 1) < 1e-10 and abs(exact.imag) < 1e-12 * abs(exact.real)
+        errs = {S: abs(contract(ozaki(ao, ao, S), ozaki(av, av, S), W) / exact - 1) for S in (5, 6, 7)}
+        assert errs[6] < 1e-10 and errs[7] < 1e-12, errs
+        assert errs[5] > 1e-10, errs  # one slice fewer misses the replay gate
