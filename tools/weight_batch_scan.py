@@ -28,12 +28,13 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--repeats", type=int, default=3)
     ap.add_argument("--grid", default="0.25 2 10;0.1 2 30;0.25 1 10;0.1 1 100;0.05 2 300")
+    ap.add_argument("--physical", action="store_true", help="opt-in physical estimator")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     rows = []
     with tempfile.TemporaryDirectory() as d:
         sp, conf = generate_config(args.config, d)
-        text = conf.read_text()
+        text = conf.read_text() + ("estimator physical\n" if args.physical else "")
         el, cur = re.search(r"weight (\S+) (.*)\n", text).groups()
         zmin = min(float(z) for z in re.findall(r"; 1 ; (\S+) 1", sp.read_text()))
         cands = [("current", cur)]
