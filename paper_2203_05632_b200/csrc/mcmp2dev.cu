@@ -1,11 +1,13 @@
 // mcmp2dev.cu — handle management and the C ABI of libmcmp2dev.so (include/mcmp2dev.h).
 //
-// One handle = one reference "worker" (driver.cpp:200-205) resident on one device: the
-// immutable system (SpinorSet/WeightSpec/TauSampler), the walker ensemble (ping-pong SoA
-// buffers + Philox stream position) and the per-step work buffers. Each MC step is three
-// launches on the handle's stream: walk (Metropolis sweep + tau), spinor (basis values +
-// MO transform into the Phi layout), pair (O/V GEMMs + integrand + reduction). Per-step
-// StepEstimates stay on the device until the end of a chunk, then one copy returns them.
+// One handle = one reference "worker" (driver.cpp:200-205) resident on one device -- or, after
+// mcmp2dev_init_batch, several workers as batched ensembles: the immutable system
+// (SpinorSet/WeightSpec/TauSampler), the walker ensembles (ping-pong SoA buffers + a DevState
+// per ensemble with its Philox stream position) and the per-step work buffers. Each MC step is
+// four launches on the handle's stream (programmatic dependent launches, captured in CUDA
+// graphs of 32 steps): walk (Metropolis sweep + tau), chi (basis values), mo (MO transform into
+// the Phi layout), pair (O/V GEMMs + integrand + reduction). Per-step StepEstimates stay on the
+// device until the end of a chunk, then one copy returns them.
 #include <cuda_runtime.h>
 
 #include <algorithm>
