@@ -158,6 +158,15 @@ void* mcmp2dev_stream(mcmp2dev_t* h);
  * if eligible; returns the active state (1/0). Results agree with the general path to
  * rounding (see csrc/pair_kr.cu). */
 int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
+/* V blocks of the Kramers pair stage (K = n_vir, ~90% of the pair work) on the INT8 tensor
+ * cores: FP64 operands split into six 7-bit slices (Ozaki), exact int8 products summed in
+ * int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers
+ * path with n_vir <= 512 and the 16 x 8 pair tiles (m >= 64 walkers, enough tiles for the
+ * SMs); elsewhere the DMMA V phase runs. mode -1 queries, 0 selects DMMA, 1 selects INT8
+ * (the default); returns 1 when the INT8 V path is selected and the system is eligible.
+ * Agreement with the FP64 path: step values within ~3e-11 relative at cfg4
+ * (tests/test_ozaki_budget.py, tests/test_gpu_oz.py). */
+int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
 
 #ifdef __cplusplus
 }

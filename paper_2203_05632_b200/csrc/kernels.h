@@ -76,7 +76,31 @@ struct PairParams {
   double* partials;          // [ntiles][4]; batched: [nens * ens_tiles][consumer warps][2]
   double* step_out;          // [6] of this step; batched: [nens][6]
   int nens, ens_tiles;       // batched ensembles: m walkers each, st_ro[nens]
+  const double* vtiles;      // pair_kr only, single ensemble: V blocks of every tile from
+                             // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
 };
+
+// INT8 (Ozaki) V blocks of the Kramers pair stage (pair_oz.cu)
+#define OZ_SLICES 6
+struct OzParams {
+  const double* phi;
+  int npts_pad, Go, Gv;      // Phi layout (PhiChunks)
+  int n_vir;
+  int npts;                  // 2m points with data
+  int npts_oz;               // points covered by the slice blocks (32 per Q block)
+  int kh, ks;                // K' = 2 kh = 32 ks
+  int ntiles;                // pair_kr tile triangle (16 x 8 walkers)
+  int8_t* sa;                // [npts_oz / 32][ks][slice][128 rows x 32] A slices (Q side)
+  int8_t* sb;                // [npts_oz / 16][ks][slice][64 rows x 32] B slices (P side)
+  double* sa_scale;          // [npts_oz / 32][128]: 2^(e - 49)
+  double* sb_scale;          // [npts_oz / 16][64]: 2^e
+  double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order
+};
+void oz_layout(int n_vir, int& kh, int& ks);
+size_t oz_slice_bytes_a(int npts_oz, int ks);
+size_t oz_slice_bytes_b(int npts_oz, int ks);
+void launch_oz(const OzParams& P, cudaStream_t s);
+cudaError_t oz_kernel_setup();
 
 void launch_walk(const WalkParams& P, cudaStream_t s);
 void launch_replay_load(const WalkParams& P, const double* walkers, double tau, cudaStream_t s);

@@ -84,6 +84,11 @@ struct mcmp2dev_handle {
   double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
   int estimator = 0;
   bool kramers_eligible = false, kramers = false;  // pair_kr.cu path
+  // V blocks of the Kramers pair stage on the INT8 tensor cores (pair_oz.cu), single ensembles
+  // of QB = 2 tiles; buffers sized for oz_m walkers, grown outside graph capture (ensure_oz)
+  bool oz = true;
+  int oz_m = 0;
+  OzParams ozp{};
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
   DevSites sites{};
   double* d_energies = nullptr;
@@ -123,13 +128,13 @@ struct mcmp2dev_handle {
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   double* d_gsteps = nullptr;  // [kGraphSteps][6] step results written by the graph
   struct GraphKey {
-    int m = -1, kramers = -1, nens = 1;
+    int m = -1, kramers = -1, nens = 1, oz = -1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
     bool operator==(const GraphKey&) const = default;
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, nens, k0, k1, rstream};
+    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, k0, k1, rstream};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -183,6 +188,33 @@ struct mcmp2dev_handle {
     return mm < 64 || double(ne) * pair_kr_tiles((mm + WB - 1) / WB) < sms;
   }
 
+  bool oz_active(int mm, int ne) const {
+    return oz && kramers && ne == 1 && mm >= 2 && !kr_qb1(mm, ne) && n_vir > 0 && n_vir <= 512;
+  }
+  void oz_free() {
+    for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v})
+      if (p) cudaFree(p);
+    ozp.sa = ozp.sb = nullptr;
+    ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
+    oz_m = 0;
+  }
+  // buffers of the INT8 V path for mm walkers (no-op when inactive or already large enough)
+  void ensure_oz(int mm) {
+    if (!oz_active(mm, 1) || mm <= oz_m) return;
+    oz_free();
+    const int nbq = (mm + 15) / 16, npts_oz = 32 * nbq;
+    int kh = 0, ks = 0;
+    oz_layout(n_vir, kh, ks);
+    const size_t ntiles = size_t(nbq) * (nbq + 1);
+    ck(cudaStreamSynchronize(stream), "oz sync");
+    ck(cudaMalloc(&ozp.sa, oz_slice_bytes_a(npts_oz, ks)), "cudaMalloc oz slices");
+    ck(cudaMalloc(&ozp.sb, oz_slice_bytes_b(npts_oz, ks)), "cudaMalloc oz slices");
+    ck(cudaMalloc(&ozp.sa_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
+    ck(cudaMalloc(&ozp.sb_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
+    ck(cudaMalloc(&ozp.v, sizeof(double) * 8192 * ntiles), "cudaMalloc oz V blocks");
+    oz_m = 16 * nbq;
+  }
+
   void launch_estimate(const WalkerBuf& wb, int mm, double* step_out, int ne = 1) {
     SpinorParams s = kramers ? sp_kr : sp;
     s.npts = 2 * mm * ne;
@@ -216,6 +248,23 @@ struct mcmp2dev_handle {
     p.step_out = step_out;
     p.nens = ne;
     p.ens_tiles = ne > 1 ? (kramers ? (qb1 ? pair_kr_tiles_qb1(p.nb) : pair_kr_tiles(p.nb)) : p.nb * (p.nb + 1) / 2) : 0;
+    p.vtiles = nullptr;
+    if (oz_active(mm, ne)) {
+      if (mm > oz_m) throw RtError("mcmp2dev: INT8 V buffers not prepared for this ensemble size");
+      OzParams o = ozp;
+      o.phi = d_phi;
+      o.npts_pad = npts_pad;
+      o.Go = Go;
+      o.Gv = Gv;
+      o.n_vir = n_vir;
+      o.npts = 2 * mm;
+      const int nbq = (mm + 15) / 16;
+      o.npts_oz = 32 * nbq;
+      oz_layout(n_vir, o.kh, o.ks);
+      o.ntiles = nbq * (nbq + 1);
+      launch_oz(o, stream);
+      p.vtiles = o.v;
+    }
     if (kramers && qb1) launch_pair_kr_qb1(p, stream);
     else if (kramers) launch_pair_kr(p, stream);
     else launch_pair(p, stream);
@@ -408,6 +457,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(spinor_kernel_setup(), "spinor kernel attributes");
   ck(pair_kr_kernel_setup(), "pair_kr kernel attributes");
   ck(pair_kr_kernel_setup_qb1(), "pair_kr (QB 1) kernel attributes");
+  ck(oz_kernel_setup(), "pair_oz kernel attributes");
   for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
 
   h->ncomp = s->ncomp;
@@ -580,6 +630,7 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
   if (h->h_steps) cudaFreeHost(h->h_steps);
   if (h->h_replay) cudaFreeHost(h->h_replay);
   if (h->d_bpart) cudaFree(h->d_bpart);
+  h->oz_free();
   if (h->d_bsteps) cudaFree(h->d_bsteps);
   if (h->h_bsteps) cudaFreeHost(h->h_bsteps);
   for (auto& e : h->ev)
@@ -747,6 +798,7 @@ int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) 
       advance_batched(h, nsteps, h->nens, values, imags);
       return;
     }
+    h->ensure_oz(h->m);
     long done = 0;
     const bool want = values || imags;
     while (done < nsteps) {
@@ -790,6 +842,7 @@ int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, co
   return guard(h, [&] {
     if (m < 2) throw ArgError("replay: at least two electron-pair walkers");
     if (m > h->mmax) throw ArgError("replay: more walkers than the handle was sized for");
+    h->ensure_oz(m);
     for (long st = 0; st < nsteps; ++st) {
       if (tau[st] < 0) throw ArgError("sample_term: tau must be non-negative");
       std::memcpy(h->h_replay, walkers + size_t(st) * m * 8, sizeof(double) * 8 * m);
@@ -843,6 +896,7 @@ void* mcmp2dev_stream(mcmp2dev_t* h) { return h ? static_cast<void*>(h->stream) 
 int mcmp2dev_prepare(mcmp2dev_t* h) {
   return guard(h, [&] {
     require_ensemble(h);
+    h->ensure_oz(h->m);
     for (int k = 0; k < 2; ++k) {  // both walker-buffer parities; nothing is executed
       h->ensure_graph();
       h->cur ^= 1;
@@ -857,7 +911,7 @@ int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop) {
                                      : 0.5 * nb * (nb + 1);
     // DMMAs per WB x WB block per k-group (all warps): O phase and V phase, 3 per complex product
     const double per_o = h->kramers ? 4 * 2 * 2 * 3 : 8 * 2 * 2 * 3;
-    const double per_v = h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
+    const double per_v = h->oz_active(h->m, h->nens) ? 0.0 : h->kramers ? 4 * 2 * 4 * 3 : 8 * 2 * 4 * 3;
     *pair_dmma_flop = h->nens * ntiles * 512.0 * (h->Go * per_o + h->Gv * per_v);
   });
 }
@@ -883,6 +937,7 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
                                                    size_t(nb) * (nb + 1) / 2 * pair_consumers() * 4});
       if (part > h->bpart_cap) {
         if (h->d_bpart) cudaFree(h->d_bpart);
+  h->oz_free();
         h->d_bpart = nullptr;
         ck(cudaMalloc(&h->d_bpart, part * sizeof(double)), "cudaMalloc");
         h->bpart_cap = part;
@@ -1070,6 +1125,13 @@ int mcmp2dev_kramers(mcmp2dev_t* h, int mode) {
   if (mode == 0) h->kramers = false;
   if (mode == 1) h->kramers = h->kramers_eligible;
   return h->kramers ? 1 : 0;
+}
+
+int mcmp2dev_pair_path(mcmp2dev_t* h, int mode) {
+  if (!h) return -1;
+  if (mode == 0) h->oz = false;
+  if (mode == 1) h->oz = true;
+  return h->oz && h->kramers && h->n_vir > 0 && h->n_vir <= 512 ? 1 : 0;
 }
 
 int mcmp2dev_synchronize(mcmp2dev_t* h) {

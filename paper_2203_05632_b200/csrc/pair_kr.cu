@@ -140,7 +140,9 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 }
 }  // namespace
 
-template <bool PHYS>
+// OZ: the V blocks come precomputed per tile from pair_oz.cu (P.vtiles, single ensemble): the
+// ring streams the occupied chunks only, and the V phase becomes one load per lane and (h, pp)
+template <bool PHYS, bool OZ>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
   pdl_wait();     // Phi of this step is visible
   pdl_trigger();  // persistent: the next step's walk may launch next to it
@@ -160,8 +162,8 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
   const bool batched = P.nens > 1;
   const int ntiles = batched ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const PhiChunks ch{P.Go, P.Gv};
-  const int nchunks = ch.count();
   const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
+  const int nchunks = OZ ? cO : ch.count();
   const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (tid == 0) {
@@ -236,6 +238,19 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
       }
       const int q0 = QW * ta, p0 = WB * bp;  // first walkers of the tile (within its ensemble)
       double* const sO = sO0 + (it % OBUF) * SO_DOUBLES;
+      // OZ: this lane's V values (h, pp) of the tile, loaded before the O phase hides their latency
+      double2 ovr[2][PW], ovi[2][PW];
+      if constexpr (OZ) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int pp = 0; pp < PW; ++pp) {
+            const double* src = P.vtiles + size_t(tt) * 8192 + (4 * wq + 2 * h + hl) * 512 + (PW * wp + pp) * 64 +
+                                (lane & 15) * 2;
+            ovr[h][pp] = __ldcs(reinterpret_cast<const double2*>(src));
+            ovi[h][pp] = __ldcs(reinterpret_cast<const double2*>(src + 32));
+          }
+      }
 
       // ---- phase 1: O~_e1 rows (q, y) all channels, cols (p, x_alpha) ----
       {
@@ -349,10 +364,14 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
           for (int pp = 0; pp < PW; ++pp) {
             const int q = 4 * wq + 2 * h + hl, p = PW * wp + pp;
             double vr[2], vi[2];
+            if constexpr (OZ) {
+              vr[0] = ovr[h][pp].x, vr[1] = ovr[h][pp].y, vi[0] = ovi[h][pp].x, vi[1] = ovi[h][pp].y;
+            } else {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              vr[j] = u1[h][pp][j] + u2[h][pp][j];
-              vi[j] = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+              for (int j = 0; j < 2; ++j) {
+                vr[j] = u1[h][pp][j] + u2[h][pp][j];
+                vi[j] = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+              }
             }
             auto o = [&](int e, int row, int col, double& re, double& im) {  // o_e(alpha_row, col)
               const int idx = o_index(e, q, p, col, row);
@@ -432,8 +451,8 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
             for (int j = 0; j < 2; ++j) {
               const int y = 2 * (lane & 1) + j;
               const int idx = o_index(ep, q, p, y, xa);
-              const double vr = u1[h][pp][j] + u2[h][pp][j];
-              const double vi = u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+              const double vr = OZ ? (j ? ovr[h][pp].y : ovr[h][pp].x) : u1[h][pp][j] + u2[h][pp][j];
+              const double vi = OZ ? (j ? ovi[h][pp].y : ovi[h][pp].x) : u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
               f += sO[idx] * vr - sO[idx + 1] * vi;
             }
             f += __shfl_xor_sync(0xffffffffu, f, 1);
@@ -557,9 +576,12 @@ cudaError_t KR_API(pair_kr_kernel_setup)() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_kr[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaFuncSetAttribute(KR_API(pair_kr_kernel)<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(KR_API(pair_kr_kernel)<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  for (auto k : {KR_API(pair_kr_kernel)<false, false>, KR_API(pair_kr_kernel)<true, false>,
+                 KR_API(pair_kr_kernel)<false, true>, KR_API(pair_kr_kernel)<true, true>}) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 void KR_API(launch_pair_kr)(const PairParams& P, cudaStream_t s) {
@@ -568,10 +590,10 @@ void KR_API(launch_pair_kr)(const PairParams& P, cudaStream_t s) {
   const int ntiles = P.nens > 1 ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   const int grid = ntiles < slots ? ntiles : slots;
-  if (P.physical)
-    pdl_launch(KR_API(pair_kr_kernel)<true>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
-  else
-    pdl_launch(KR_API(pair_kr_kernel)<false>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+  const bool oz = P.vtiles != nullptr && P.nens <= 1;
+  auto k = P.physical ? (oz ? KR_API(pair_kr_kernel)<true, true> : KR_API(pair_kr_kernel)<true, false>)
+                      : (oz ? KR_API(pair_kr_kernel)<false, true> : KR_API(pair_kr_kernel)<false, false>);
+  pdl_launch(k, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
 }
 
 }  // namespace mcmp2dev

@@ -1,0 +1,332 @@
+// pair_oz.cu — the virtual Green's-function blocks of the Kramers pair stage on the INT8 tensor
+// cores (tcgen05.mma kind::i8), FP64-accurate by Ozaki splitting.
+//
+// For every walker tile of pair_kr.cu (16 Q walkers x 8 P walkers, the same triangle and tile
+// numbering t = a (a + 1) + b), the V phase computes, for Q points q (alpha channels x) and
+// P points p (all channels y),
+//   V(q x, p y) = sum_a Phi_v(q, x, a) conj Phi_v(p, y, a)          (greens.cpp:73-79)
+// with Phi_v already carrying sqrt(exp(-eps_a tau)) and the walker weights (mo_kernel). As real
+// GEMMs over K' = [re | im] (K' = 2 KH, KH = n_vir rounded up to 16):
+//   Re V = [re_q | im_q] . [re_p | im_p],   Im V = [im_q | -re_q] . [re_p | im_p],
+// so the A operand (Q side) has 128 rows per tile: (q walker 16, e_q 2, x_alpha 2, re/im 2),
+// and B (P side) 64 rows: (p walker 8, e_p 2, y 4).
+//
+// Ozaki splitting: every row (point, channel) is scaled by its power-of-two maximum 2^e and cut
+// into six signed 7-bit slices (rounded digits), x 2^-e = sum_s d_s 2^(-7 (s + 1)), |d_s| <= 127. The 21 slice
+// products with s + t <= 5 are exact int8 x int8 -> int32 UMMA products; those of one diagonal
+// d = s + t accumulate in one TMEM accumulator (|acc| < 6 K' 127^2 < 2^31). The epilogue merges
+// the six accumulators exactly into one int64 per element (X = sum_d acc_d 128^(5-d), |X| < 2^59)
+// and rounds once to FP64: V = X 2^(e_q + e_p - 49). The error (slice remainders and the dropped
+// products s + t > 5) is ~2^-42 of |row_q| |row_p| K' -- the precision budget pinned on the
+// oracle by tests/test_ozaki_budget.py.
+//
+// Kernels per step (after mo_kernel, before pair_kr_kernel<OZ>):
+//  * oz_slice_kernel: one warp per point, all four channels: row exponents, the six slices of the
+//    [re | im] rows, written directly in the UMMA canonical K-major layout of their tile blocks;
+//  * oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each
+//    k-step's 6 A + 6 B slices (36 KB) into a 5-stage mbarrier ring with cp.async.bulk, one
+//    thread issues the 21 tcgen05.mma per k-step, four epilogue warps drain TMEM (tcgen05.ld),
+//    merge, release the accumulators and write the tile's V in the order pair_kr's epilogue
+//    lanes read it: V[t][q 16][p 8][re/im][e_q x_alpha e_p y>>1 (16)][y&1].
+// Measured prototype (tools/oz_gemm.cu, cfg4 triangle): 1.6 ms incl. the 1.08 GB V write,
+// vs ~3.6 ms for the DMMA V phase of pair_kr.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "pair_common.cuh"
+
+namespace mcmp2dev {
+
+namespace {
+using namespace pairk;
+
+constexpr int S = OZ_SLICES;
+constexpr int MA = 128, NB = 64;   // A rows (Q side) and B rows (P side) of a tile
+constexpr int A_KS = S * MA * 32;  // bytes of one k-step (32 of K') of a Q block, all slices
+constexpr int B_KS = S * NB * 32;
+constexpr int STAGE = A_KS + B_KS;
+constexpr int STAGES = 5;
+constexpr int THREADS = 6 * 32;    // warps 0-3 epilogue (TMEM lanes 0-127), 4 producer, 5 MMA
+constexpr int SMEM_BYTES = STAGES * STAGE;
+constexpr int TMEM_COLS = 512;     // 6 x 64 used
+
+// canonical K-major, no-swizzle UMMA operand layout of one k-step: [row / 8][k / 16][row % 8][16 B]
+__host__ __device__ __forceinline__ int op_off(int r, int kk) {
+  return ((r >> 3) * 2 + (kk >> 4)) * 128 + (r & 7) * 16 + (kk & 15);
+}
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {  // LBO 128 B (k chunk), SBO 256 B (8 rows)
+  return uint64_t((smem_u32(p) >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
+         (uint64_t(1) << 46);
+}
+// instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = 64
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+// tile t = a (a + 1) + b: Q block a (walkers 16a ..), P block b < 2 (a + 1) (walkers 8b ..)
+__device__ __forceinline__ void oz_tile(int t, int& a, int& b) {
+  int r = int((sqrt(4.0 * double(t) + 1.0) - 1.0) * 0.5);
+  while ((r + 1) * (r + 2) <= t) ++r;
+  while (r * (r + 1) > t) --r;
+  a = r;
+  b = t - r * (r + 1);
+}
+
+// six signed digits of 4 values in (-1, 1): x = sum_s d_s 128^-(s+1) + rem, each digit the
+// nearest integer clamped to [-127, 127] (a clamped digit carries its excess into the next one;
+// all steps exact in FP64). Rounded digits are centred and, after the first, mostly |d| <= 64:
+// on the oracle's cfg3 inputs the step's exchange sum is 20x closer to FP64 than with truncated
+// digits (7e-12 vs 1.2e-10 relative), at the same 21 products (tests/test_ozaki_budget.py)
+__device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[S]) {
+  double r[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      r[i] *= 128.0;
+      const double q = fmin(fmax(rint(r[i]), -127.0), 127.0);
+      r[i] -= q;
+      w |= (uint32_t(int(q)) & 0xFFu) << (8 * i);
+    }
+    out[s] = w;
+  }
+}
+__device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of 4 int8 digits
+  uint32_t o = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o |= (uint32_t(-int(int8_t(w >> (8 * i)))) & 0xFFu) << (8 * i);
+  return o;
+}
+
+__global__ void __launch_bounds__(256) oz_slice_kernel(OzParams P) {
+  pdl_wait();
+  pdl_trigger();
+  const int pt = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
+  if (pt >= P.npts_oz) return;
+  const PhiChunks ch{P.Go, P.Gv};
+  const int KH = P.kh, ks_n = P.ks, nq = KH / 4;
+  const bool live = pt < P.npts;
+  const int swz = phi_swz(pt);
+  const int qb = pt >> 5, qrow = ((pt & 31) >> 1) * 8 + (pt & 1) * 4;  // A row of (x_alpha 0, re)
+  const int pb = pt >> 4, prow = ((pt & 15) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
+  int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KS;
+  int8_t* const sb = P.sb + size_t(pb) * ks_n * B_KS;
+  for (int x = 0; x < NCH; ++x) {
+    // this lane's spinor quads a0 = 4 (lane + 32 j)
+    constexpr int MAXJ = 4;  // KH <= 512 (n_vir <= 512)
+    double re[MAXJ][4], im[MAXJ][4];
+    double mx = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int qd = lane + 32 * j;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) re[j][i] = im[j][i] = 0.0;
+      if (live && qd < nq && 4 * qd < P.n_vir) {
+        const double* src = P.phi + ch.offset(P.Go + qd, pt, P.npts_pad);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (4 * qd + i < P.n_vir) {
+            re[j][i] = src[(x * 4 + i) ^ swz];
+            im[j][i] = src[16 + ((x * 4 + i) ^ swz)];
+          }
+          mx = fmax(mx, fmax(fabs(re[j][i]), fabs(im[j][i])));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int e = (mx > 0.0 && mx <= 1.7e308) ? ilogb(mx) + 1 : 0;  // |value| 2^-e < 1
+    const double sc = ldexp(1.0, -e);
+    const bool alpha = (x & 1) == 0;
+    const int ra = qrow + (x >> 1) * 2;  // A rows ra (re variant), ra + 1 (im variant)
+    const int rb = prow + x;
+    if (lane == 0) {
+      P.sb_scale[size_t(pb) * NB + rb] = ldexp(1.0, e);
+      if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 49);
+    }
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int qd = lane + 32 * j;
+      if (qd >= nq) break;
+      double xr[4], xi[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xr[i] = re[j][i] * sc, xi[i] = im[j][i] * sc;
+      uint32_t dr[S], di[S];
+      digits4(xr, dr);
+      digits4(xi, di);
+      const int kre = 4 * qd, kim = KH + 4 * qd;  // K' positions of the re and im halves
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        // B row [re | im]
+        *reinterpret_cast<uint32_t*>(sb + (size_t(kre >> 5) * S + s) * NB * 32 + op_off(rb, kre & 31)) = dr[s];
+        *reinterpret_cast<uint32_t*>(sb + (size_t(kim >> 5) * S + s) * NB * 32 + op_off(rb, kim & 31)) = di[s];
+        if (alpha) {  // A rows [re | im] and [im | -re]
+          int8_t* a0 = sa + (size_t(kre >> 5) * S + s) * MA * 32;
+          int8_t* a1 = sa + (size_t(kim >> 5) * S + s) * MA * 32;
+          *reinterpret_cast<uint32_t*>(a0 + op_off(ra, kre & 31)) = dr[s];
+          *reinterpret_cast<uint32_t*>(a1 + op_off(ra, kim & 31)) = di[s];
+          *reinterpret_cast<uint32_t*>(a0 + op_off(ra + 1, kre & 31)) = di[s];
+          *reinterpret_cast<uint32_t*>(a1 + op_off(ra + 1, kim & 31)) = neg4(dr[s]);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KS = P.ks;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  const int ntiles = P.ntiles;
+  const int my = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+
+  if (warp == 4) {
+    if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < my; ++it) {
+        int a, b;
+        oz_tile(int(blockIdx.x) + it * int(gridDim.x), a, b);
+        const int8_t* ga = P.sa + size_t(a) * KS * A_KS;
+        const int8_t* gb = P.sb + size_t(b) * KS * B_KS;
+        for (int ks = 0; ks < KS; ++ks) {
+          mbar_wait(&empty[stage], ph ^ 1u);
+          int8_t* dst = sm + stage * STAGE;
+          mbar_expect_tx(&full[stage], STAGE);
+          bulk_g2s(dst, ga + size_t(ks) * A_KS, A_KS, &full[stage]);
+          bulk_g2s(dst + A_KS, gb + size_t(ks) * B_KS, B_KS, &full[stage]);
+          if (++stage == STAGES) stage = 0, ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer: 21 slice products per k-step into the diagonal accumulators
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int it = 0; it < my; ++it) {
+        mbar_wait(&tempty, (it & 1) ^ 1u);  // the epilogue has drained the previous tile
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int ks = 0; ks < KS; ++ks) {
+          mbar_wait(&full[stage], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const int8_t* sa = sm + stage * STAGE;
+          const int8_t* sb = sa + A_KS;
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int t = 0; s + t < S; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
+              umma_i8(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32), umma_desc(sb + t * NB * 32),
+                      ks > 0 || s > 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);  // the stage is free once these MMAs have read it
+          if (++stage == STAGES) stage = 0, ph ^= 1u;
+        }
+        umma_commit(&tfull);
+      }
+    }
+  } else {  // epilogue: TMEM lane = A row
+    const int row = warp * 32 + lane;
+    const int q = row >> 3, plane = row & 1, exq = (row >> 1) & 3;
+    for (int it = 0; it < my; ++it) {
+      const int t = int(blockIdx.x) + it * int(gridDim.x);
+      int a, b;
+      oz_tile(t, a, b);
+      mbar_wait(&tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      long long X[NB];
+#pragma unroll
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        uint32_t v[S][16];
+#pragma unroll
+        for (int d = 0; d < S; ++d) tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(d * NB + c0), v[d]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          long long x = int32_t(v[0][c]);
+#pragma unroll
+          for (int d = 1; d < S; ++d) x = x * 128 + int32_t(v[d][c]);
+          X[c0 + c] = x;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the stores below
+      const double sr = P.sa_scale[size_t(a) * MA + row];
+      const double* sbv = P.sb_scale + size_t(b) * NB;
+      double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8;
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int c = 0; c < 8; c += 2)
+          __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
+                 make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
+                              double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+int g_sms_oz[64];
+}  // namespace
+
+void oz_layout(int n_vir, int& kh, int& ks) {
+  kh = (n_vir + 15) / 16 * 16;
+  ks = 2 * kh / 32;
+}
+size_t oz_slice_bytes_a(int npts_pad, int ks) { return size_t(npts_pad / 32) * ks * A_KS; }
+size_t oz_slice_bytes_b(int npts_pad, int ks) { return size_t(npts_pad / 16) * ks * B_KS; }
+
+cudaError_t oz_kernel_setup() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms_oz[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return cudaFuncSetAttribute(oz_vgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
+void launch_oz(const OzParams& P, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 7) / 8), dim3(256), 0, s, P);
+  const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
+  const int grid = P.ntiles < sms ? P.ntiles : sms;
+  pdl_launch(oz_vgemm_kernel, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+}
+
+}  // namespace mcmp2dev

@@ -213,6 +213,12 @@ class DeviceWalker:
         """Kramers-restricted pair kernel: -1 query, 0 off, 1 on when eligible."""
         return bool(self._d.mcmp2dev_kramers(self._h, mode))
 
+    def int8_v(self, mode: int = -1) -> bool:
+        """V blocks of the Kramers pair stage on the INT8 tensor cores (Ozaki slices,
+        csrc/pair_oz.cu): -1 query, 0 DMMA, 1 INT8 (default). True when selected and eligible;
+        it runs for single ensembles whose 16 x 8 pair tiles cover the SMs (m >= ~180)."""
+        return bool(self._d.mcmp2dev_pair_path(self._h, mode))
+
     @property
     def stream_ptr(self) -> int:
         return int(self._d.mcmp2dev_stream(self._h))

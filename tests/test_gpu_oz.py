@@ -1,0 +1,79 @@
+"""The INT8 (Ozaki) V blocks of the Kramers pair stage (csrc/pair_oz.cu) against the CPU oracle:
+the replayed step estimates and the advanced chains of single ensembles large enough for the
+path (m >= ~180 walkers: the 16 x 8 pair tiles cover the SMs), literal and physical estimators.
+Tolerance as every parity test: 1e-10 relative (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import oracle_py
+from paper_2203_05632_b200 import DeviceWalker, System
+from paper_2203_05632_b200.walker import EnsembleState
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+def rel_err(got, ref):
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)))
+
+
+@pytest.mark.parametrize("name,m,nsteps", [("cfg2", 256, 2), ("cfg3", 192, 2), ("cfg4", 192, 1), ("cfg5-10", 200, 1)])
+def test_int8_v_replay_matches_oracle(cfgdir, name, m, nsteps):
+    sp = cfgdir / f"{name}.spinor"
+    text = (cfgdir / f"{name}.conf").read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=13, stream=0, m=m, burn=20, nsteps=nsteps)
+    dw = DeviceWalker(System(sp, text), max_walkers=m)
+    assert dw.kramers() and dw.int8_v()
+    got = dw.replay(tr["walkers"], tr["tau"])
+    dw.int8_v(0)
+    dmma = dw.replay(tr["walkers"], tr["tau"])
+    for k in (0, 2, 4):
+        assert rel_err(got[:, k], tr["est"][:, k]) < REL, k
+        assert rel_err(got[:, k], dmma[:, k]) < REL, k
+    assert np.all(got[:, 1] == 0.0)  # the Kramers epilogue's real f values
+
+
+def test_int8_v_physical_replay_matches_oracle(cfgdir):
+    sp = cfgdir / "cfg3.spinor"
+    text = (cfgdir / "cfg3.conf").read_text() + "estimator physical\n"
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=17, stream=0, m=192, burn=20, nsteps=1, physical=True)
+    dw = DeviceWalker(System(sp, text), max_walkers=192)
+    assert dw.int8_v()
+    got = dw.replay(tr["walkers"], tr["tau"])
+    for k in (0, 2, 4):
+        assert rel_err(got[:, k], tr["est"][:, k]) < REL, k
+
+
+def test_int8_v_chain_matches_oracle(cfgdir):
+    """advance() through the captured graphs (walk, chi, mo, slice, V GEMM, pair) follows the
+    oracle's chain step by step, with the same RNG state at the end."""
+    sp = cfgdir / "cfg3.spinor"
+    text = (cfgdir / "cfg3.conf").read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    m, nsteps = 192, 34  # one 32-step graph and two single launches
+    tr = orc.trajectory(seed=9, stream=2, m=m, burn=50, nsteps=nsteps)
+    dw = DeviceWalker(System(sp, text), max_walkers=m)
+    dw.set_ensemble(EnsembleState(**oracle_py.state_to_ensemble(tr["init"], m)))
+    assert dw.int8_v()
+    v, _ = dw.advance(nsteps)
+    assert rel_err(v, tr["est"][:, 0]) < REL
+    fin = dw.get_ensemble()
+    ref = oracle_py.state_to_ensemble(tr["final"], m)
+    assert fin.rng_counter == ref["rng_counter"] and fin.rng_idx == ref["rng_idx"]
+    assert fin.accepted == tr["accepted"]
+
+
+def test_int8_v_not_used_where_ineligible(cfgdir):
+    """Small ensembles (QB = 1 tiles) and the general kernel keep the FP64 DMMA path; the mode
+    switch is per handle and reversible."""
+    sp = cfgdir / "cfg2.spinor"
+    text = (cfgdir / "cfg2.conf").read_text()
+    dw = DeviceWalker(System(sp, text), max_walkers=64)
+    assert dw.int8_v()  # selected and eligible system; m decides per step
+    dw.kramers(0)
+    assert not dw.int8_v()
+    dw.kramers(1)
+    assert not dw.int8_v(0) and dw.int8_v(1)

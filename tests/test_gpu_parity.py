@@ -192,12 +192,14 @@ def test_full_size_replay_matches_oracle(cfgdir, name, m):
     w = dw.get_ensemble().walkers[:, :8]
     tau = 0.37
     ref = orc.replay_parallel(w, tau, threads=max(1, min(32, os.cpu_count() or 1)))
-    for mode in (1, 0):
-        dw.kramers(mode)
+    # Kramers kernel with the INT8 (Ozaki) V blocks, with the DMMA V phase, then the general kernel
+    for kr, i8 in ((1, 1), (1, 0), (0, 0)):
+        dw.kramers(kr)
+        assert dw.int8_v(i8) == bool(kr and i8)
         got = dw.replay(w[None], np.array([tau]))[0]
-        assert abs(got[0] - ref[0]) <= REL * abs(ref[0])
+        assert abs(got[0] - ref[0]) <= REL * abs(ref[0]), (kr, i8)
         for k in (2, 4):
-            assert abs(got[k] - ref[k]) <= REL * abs(ref[k])
+            assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), (kr, i8, k)
 
 
 def test_full_size_physical_replay_matches_oracle(cfgdir):
@@ -217,8 +219,9 @@ def test_full_size_physical_replay_matches_oracle(cfgdir):
     w = dw.get_ensemble().walkers[:, :8]
     tau = 0.21
     ref = orc.replay_parallel(w, tau, threads=max(1, min(32, os.cpu_count() or 1)), physical=True)
-    for mode in (1, 0):
-        dw.kramers(mode)
+    for kr, i8 in ((1, 1), (1, 0), (0, 0)):
+        dw.kramers(kr)
+        assert dw.int8_v(i8) == bool(kr and i8)
         got = dw.replay(w[None], np.array([tau]))[0]
         for k in (0, 2, 4):
-            assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), (mode, k)
+            assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), (kr, i8, k)
