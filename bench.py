@@ -119,6 +119,13 @@ def clocks_summary(path: Path, index: int):
             "reasons": sorted(reasons), "samples": len(rows)}
 
 
+# dense tcgen05 INT8 rate measured on this pool's B200 (tools/umma_i8.cu, one MMA stream per SM;
+# cuBLASLt torch._int_mm 2840 TOPS); nominal dense INT8/FP8 4.5 POPS (B200_PROFILING.md)
+INT8_PEAK = 2858.0
+INT8_PEAK_SOURCE = ("measured: tools/umma_i8.cu tcgen05.mma kind::i8 M128 N64 K32 loop, 2858 TOPS "
+                    "(profiles/r01_legacy_mma_peaks.txt); nominal dense 4500 TOPS")
+
+
 def peaks():
     fp64 = json.loads((ROOT / "MEASURED_FP64.json").read_text())
     return fp64["dmma_tflops"], "MEASURED_FP64.json dmma_tflops (mma.sync m8n8k4 f64 loop on this pool's B200)"
@@ -314,10 +321,13 @@ def main():
     achieved = work["pair_flop"] / (pair_ms / 1e3) / 1e12
     kramers = dw.kramers()
     kernel_name = "pair_kr_kernel (DMMA m8n8k4 f64, Kramers-restricted)" if kramers else "pair_kernel (DMMA m8n8k4 f64)"
-    traffic = None
-    tf = ROOT / "profiles" / f"traffic_{cfg}.json"  # dram bytes per launch from the committed ncu --set full capture
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    oz = prof.get("int8_v", {})
+    int8_path = oz.get("steps", 0) > 0  # V blocks on the INT8 tensor cores (pair_oz.cu)
+
+    def traffic_of(kernel):  # dram bytes per launch from the committed ncu --set full capture
+        tf = ROOT / "profiles" / f"traffic_{cfg}_{kernel}.json"
+        return json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
+    traffic = traffic_of("pair_kr_kernel" if kramers else "pair_kernel")
 
     # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
     dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
@@ -342,34 +352,58 @@ def main():
             dist.destroy_process_group()
         return
 
+    fp64_view = {"kernel": kernel_name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                 "achieved_basis": "algorithmic: C(m,2) x F_pair, F_pair = 8 nc^2 (2 n_occ + 4 n_vir) + 32 nc^2 "
+                                   "(SURVEY 8d, 8 FLOP per complex MAC of the reference's full 4x4 blocks) over the "
+                                   "pair stage's device time",
+                 "executed_dmma_flop_per_launch": work["pair_dmma_flop_executed"],
+                 "kramers_path": kramers,
+                 "pair_flop_per_launch": work["pair_flop"], "pair_ms_per_launch": pair_ms,
+                 "pair_share_of_step": prof["ms"]["pair"] / prof["ms"]["total"],
+                 "spinor_ms_per_launch": prof["ms"]["spinor"] / prof["launches"]["spinor"],
+                 "walk_ms_per_launch": prof["ms"]["walk"] / prof["launches"]["walk"],
+                 "step_ms_profiled": step_ms_prof}
+    if int8_path:
+        n = oz["steps"]
+        vg_ms, sl_ms, kr_ms = oz["vgemm_ms"] / n, oz["slice_ms"] / n, oz["pair_kr_ms"] / n
+        a8 = oz["vgemm_int8_ops"] / (vg_ms / 1e3) / 1e12
+        roofline = {
+            "bound": "tensor", "kernel": "oz_vgemm_kernel (tcgen05.mma kind::i8: the V blocks as 6-slice Ozaki "
+                                         "sums of exact int8 products, pair_oz.cu)",
+            "achieved": a8, "peak": INT8_PEAK, "unit": "TFLOP/s", "frac": a8 / INT8_PEAK,
+            "traffic": traffic_of("oz_vgemm_kernel"),
+            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 64 x K' per launch",
+            "peak_source": INT8_PEAK_SOURCE,
+            "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
+            "vgemm_share_of_step": vg_ms / step_ms_prof,
+            "pair_stage_fp64": dict(fp64_view, kernel="pair stage: oz_slice_kernel + oz_vgemm_kernel + pair_kr_kernel "
+                                    "(O blocks by DMMA, V blocks read back)", why_frac_above_1=(
+                "the pair stage computes the reference's FP64 contraction with fewer FP64 operations: the V blocks "
+                "(~90% of the work) as exact int8 tensor products (Ozaki splitting, pair_oz.cu), the O blocks by DMMA "
+                "with 3M complex products on the Kramers alpha rows (pair_kr.cu)"))}
+    else:
+        roofline = dict(fp64_view, bound="tensor",
+                        executed_tflops=work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12,
+                        executed_frac=work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12 / peak,
+                        why_frac_above_1="the kernel issues fewer DMMA FLOPs than the algorithmic count: complex "
+                                         "products as 3 real products (3M) and, for exact Kramers pairs, only the "
+                                         "alpha rows of each 4x4 block (pair_kr.cu); executed_frac is the tensor-pipe "
+                                         "utilisation" if kramers else "3M complex products (3 real per complex)")
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64/c128", "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
         "config": dict(config, parallelism=f"{world * ens} independent workers ({ens} per GPU)",
                        l2="flushed between timed steps (256 MiB write on the handle's stream)"),
-        "roofline": {"bound": "tensor", "kernel": kernel_name, "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "achieved_basis": "algorithmic: C(m,2) x F_pair, F_pair = 8 nc^2 (2 n_occ + 4 n_vir) + 32 nc^2 "
-                                       "(SURVEY 8d, 8 FLOP per complex MAC of the reference's full 4x4 blocks)",
-                     "executed_dmma_flop_per_launch": work["pair_dmma_flop_executed"],
-                     "executed_tflops": work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12,
-                     "executed_frac": work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12 / peak,
-                     "why_frac_above_1": "the kernel issues fewer DMMA FLOPs than the algorithmic count: complex "
-                                         "products as 3 real products (3M) and, for exact Kramers pairs, only the "
-                                         "alpha rows of each 4x4 block (pair_kr.cu); executed_frac is the tensor-pipe "
-                                         "utilisation" if kramers else "3M complex products (3 real per complex)",
-                     "kramers_path": kramers,
-                     "pair_flop_per_launch": work["pair_flop"], "pair_ms_per_launch": pair_ms,
-                     "pair_share_of_step": prof["ms"]["pair"] / prof["ms"]["total"],
-                     "spinor_ms_per_launch": prof["ms"]["spinor"] / prof["launches"]["spinor"],
-                     "walk_ms_per_launch": prof["ms"]["walk"] / prof["launches"]["walk"],
-                     "step_ms_profiled": step_ms_prof},
+"roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"
                         " + interval merge (all_gather of per-rank summaries, merge_estimates)",
                 "merged": merged},
-        "gpu_launches": 4 * args.steps,  # walk_kernel, chi_kernel, mo_kernel, pair kernel per step
+        # per step: walk_kernel, chi_kernel, mo_kernel, [oz_slice_kernel, oz_vgemm_kernel,] pair kernel
+        "gpu_launches": (6 if int8_path else 4) * args.steps,
         "step_values_checksum": float(np.sum(vals)),
     }
     cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", dev)

@@ -142,6 +142,10 @@ int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, co
  * reset, measured with CUDA events on the handle's stream:
  * out[0..3] = ms of {walk, spinor, pair, total}, out[4..7] = launches of the same. */
 int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out);
+/* The pair stage's kernels on the INT8 V path, accumulated like mcmp2dev_profile (same enable
+ * and reset): out[0..2] = ms of {oz_slice_kernel, oz_vgemm_kernel, pair_kr_kernel}, out[3] =
+ * profiled steps that took the path, out[4] = int8 tensor ops of the last V-GEMM launch. */
+int mcmp2dev_profile_pair(mcmp2dev_t* h, double* out);
 /* Algorithmic work of one step at the current m: FLOP of the pair stage
  * (C(m,2) * F_pair) and of the spinor stage (2m * 4 * R * n_p), bytes written to Phi. */
 int mcmp2dev_work(mcmp2dev_t* h, double* pair_flop, double* spinor_flop, double* phi_bytes);

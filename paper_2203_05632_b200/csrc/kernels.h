@@ -99,7 +99,9 @@ struct OzParams {
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);
 size_t oz_slice_bytes_b(int npts_oz, int ks);
-void launch_oz(const OzParams& P, cudaStream_t s);
+void launch_oz_slice(const OzParams& P, cudaStream_t s);
+void launch_oz_vgemm(const OzParams& P, cudaStream_t s);
+double oz_int8_ops(const OzParams& P);  // executed int8 tensor ops of one V-GEMM launch
 cudaError_t oz_kernel_setup();
 
 void launch_walk(const WalkParams& P, cudaStream_t s);

@@ -120,6 +120,9 @@ struct mcmp2dev_handle {
   // profiling
   bool prof = false;
   cudaEvent_t ev[4]{};
+  cudaEvent_t ev_oz[2]{};                   // after oz_slice_kernel, after oz_vgemm_kernel
+  double prof_oz[4] = {0, 0, 0, 0};          // ms of slice, V-GEMM, pair_kr (INT8 V path), launches
+  double oz_ops = 0;                         // int8 ops of the last V-GEMM launch
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_n[4] = {0, 0, 0, 0};
 
@@ -262,7 +265,11 @@ struct mcmp2dev_handle {
       o.npts_oz = 32 * nbq;
       oz_layout(n_vir, o.kh, o.ks);
       o.ntiles = nbq * (nbq + 1);
-      launch_oz(o, stream);
+      launch_oz_slice(o, stream);
+      if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
+      launch_oz_vgemm(o, stream);
+      if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+      oz_ops = oz_int8_ops(o);
       p.vtiles = o.v;
     }
     if (kramers && qb1) launch_pair_kr_qb1(p, stream);
@@ -279,6 +286,16 @@ struct mcmp2dev_handle {
       prof_ms[1] += b;
       prof_ms[2] += c;
       prof_ms[3] += a + b + c;
+      if (p.vtiles) {
+        float x = 0, y = 0, z = 0;
+        ck(cudaEventElapsedTime(&x, ev[2], ev_oz[0]), "elapsed");
+        ck(cudaEventElapsedTime(&y, ev_oz[0], ev_oz[1]), "elapsed");
+        ck(cudaEventElapsedTime(&z, ev_oz[1], ev[3]), "elapsed");
+        prof_oz[0] += x;
+        prof_oz[1] += y;
+        prof_oz[2] += z;
+        prof_oz[3] += 1;
+      }
       prof_n[0] += 1;
       prof_n[1] += 1;
       prof_n[2] += 1;
@@ -459,6 +476,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(pair_kr_kernel_setup_qb1(), "pair_kr (QB 1) kernel attributes");
   ck(oz_kernel_setup(), "pair_oz kernel attributes");
   for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+  for (auto& e : h->ev_oz) ck(cudaEventCreate(&e), "cudaEventCreate");
 
   h->ncomp = s->ncomp;
   h->n_occ = s->n_occ;
@@ -634,6 +652,8 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
   if (h->d_bsteps) cudaFree(h->d_bsteps);
   if (h->h_bsteps) cudaFreeHost(h->h_bsteps);
   for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h->ev_oz)
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs)
     if (g) cudaGraphExecDestroy(g);
@@ -876,7 +896,7 @@ int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out) {
         out[4 + i] = h->prof_n[i];
       }
     if (reset)
-      for (int i = 0; i < 4; ++i) h->prof_ms[i] = h->prof_n[i] = 0;
+      for (int i = 0; i < 4; ++i) h->prof_ms[i] = h->prof_n[i] = h->prof_oz[i] = 0;
     h->prof = enable != 0;
   });
 }
@@ -1125,6 +1145,13 @@ int mcmp2dev_kramers(mcmp2dev_t* h, int mode) {
   if (mode == 0) h->kramers = false;
   if (mode == 1) h->kramers = h->kramers_eligible;
   return h->kramers ? 1 : 0;
+}
+
+int mcmp2dev_profile_pair(mcmp2dev_t* h, double* out) {
+  return guard(h, [&] {
+    for (int i = 0; i < 4; ++i) out[i] = h->prof_oz[i];
+    out[4] = h->oz_ops;
+  });
 }
 
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode) {

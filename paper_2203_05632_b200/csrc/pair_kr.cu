@@ -21,6 +21,8 @@
 //    registers), 16 DMMA warps per SM;
 //  * epilogue: the element-wise contraction is reduced with shuffles and the four f values of a
 //    pair meet in one lane by shuffles; the walker weights are already in Phi_v (mo_kernel).
+// OZ instantiation (single ensembles, pair_oz.cu): phase 2 is replaced by the V tile that
+// oz_vgemm_kernel wrote for this tile (INT8 tensor cores); the ring carries the O chunks only.
 #include <cuda_runtime.h>
 
 #include "common.cuh"

@@ -320,10 +320,15 @@ cudaError_t oz_kernel_setup() {
   return cudaFuncSetAttribute(oz_vgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
-void launch_oz(const OzParams& P, cudaStream_t s) {
+void launch_oz_slice(const OzParams& P, cudaStream_t s) {
+  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 7) / 8), dim3(256), 0, s, P);
+}
+
+double oz_int8_ops(const OzParams& P) { return double(P.ntiles) * (S * (S + 1) / 2) * 2.0 * MA * NB * 32.0 * P.ks; }
+
+void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
-  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 7) / 8), dim3(256), 0, s, P);
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
   const int grid = P.ntiles < sms ? P.ntiles : sms;
   pdl_launch(oz_vgemm_kernel, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);

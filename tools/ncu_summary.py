@@ -8,8 +8,10 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-KERNELS = ["pair_kr_kernel", "mo_kernel", "chi_kernel", "walk_kernel"]
-WANT = ["gpu__time_duration.sum", "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+KERNELS = ["oz_vgemm_kernel", "oz_slice_kernel", "pair_kr_kernel", "mo_kernel", "chi_kernel", "walk_kernel"]
+WANT = ["gpu__time_duration.sum", "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
@@ -51,20 +53,19 @@ def main(tag):
         tot = sum(a for a, _ in st) or 1.0
         lines.append("  stall mix: " + ", ".join(f"{n.replace('smsp__pcsamp_warps_issue_stalled_', '')} "
                                                  f"{a / tot * 100:.1f}%" for a, n in sorted(st, reverse=True)[:6]))
-        if k == "pair_kr_kernel":
-            num = lambda n: float(vals[n][0].replace(",", "")) * SCALE.get(vals[n][1], 1.0)
-            r, w = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
-            traffic = {"kernel": k, "config": "cfg4 (m=2048)", "dram_bytes_per_launch": int(r + w),
-                       "dram_read_bytes": int(r), "dram_write_bytes": int(w),
-                       "source": f"ncu --set full --clock-control none, gpurun_out/{rep.name}, one steady-state launch",
-                       "note": "Phi (88 MB) is re-read by tile CTAs mostly from L2; DRAM traffic is a few x Phi, far "
-                               "below the HBM roofline: the kernel is FP64-tensor bound"}
+        num = lambda n: float(vals[n][0].replace(",", "")) * SCALE.get(vals[n][1], 1.0)  # noqa: E731
+        r, w = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+        notes = {"pair_kr_kernel": "O chunks of Phi re-read by tile CTAs mostly from L2, plus the V tiles (INT8 path)",
+                 "oz_vgemm_kernel": "slices (113 MB) re-read by tile CTAs mostly from L2; writes are the V tiles (1.08 GB)"}
+        traffic = {"kernel": k, "config": "cfg4 (m=2048)", "dram_bytes_per_launch": int(r + w),
+                   "dram_read_bytes": int(r), "dram_write_bytes": int(w),
+                   "source": f"ncu --set full --clock-control none, gpurun_out/{rep.name}, one steady-state launch",
+                   "note": notes.get(k, "")}
+        (ROOT / "profiles" / f"traffic_cfg4_{k}.json").write_text(json.dumps(traffic, indent=1) + "\n")
         details = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"], capture_output=True, text=True,
                                  check=True).stdout
-        (ROOT / "profiles" / f"r01_{k}_ncu_details.csv").write_text(details)
-    (ROOT / "profiles" / "r01_ncu_raw_summary_cfg4.txt").write_text("\n".join(lines) + "\n")
-    if traffic:
-        (ROOT / "profiles" / "traffic_cfg4.json").write_text(json.dumps(traffic, indent=1) + "\n")
+        (ROOT / "profiles" / f"{tag}_{k}_ncu_details.csv").write_text(details)
+    (ROOT / "profiles" / f"{tag}_ncu_raw_summary_cfg4.txt").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 

@@ -21,7 +21,7 @@ python tools/batch_scan.py cfg2 --nens 1,4,8,16,32 --out $OUT/${TAG}_batch_cfg2.
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches_cfg4.csv \
   python bench.py --steps 3 --warmup 3 --burnin 20 --no-cpu-baseline > $OUT/${TAG}_ncu_launches.log 2>&1
 # one steady-state launch of each kernel, full set
-for k in pair_kr_kernel mo_kernel chi_kernel walk_kernel; do
+for k in oz_vgemm_kernel pair_kr_kernel oz_slice_kernel mo_kernel chi_kernel walk_kernel; do
   skip=1
   [ $k = walk_kernel ] && skip=22   # past init + 20 burn-in sweeps: a production sweep
   ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 -f \
