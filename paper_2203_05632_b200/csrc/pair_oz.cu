@@ -21,12 +21,13 @@
 // oracle by tests/test_ozaki_budget.py.
 //
 // Kernels per step (after mo_kernel, before pair_kr_kernel<OZ>):
-//  * oz_slice_kernel: one warp per point, all four channels: row exponents, the six slices of the
+//  * oz_slice_kernel: one warp per (point, channel): the row exponent, the six slices of the
 //    [re | im] rows, written directly in the UMMA canonical K-major layout of their tile blocks;
 //  * oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each
 //    k-step's 6 A + 6 B slices (36 KB) into a 5-stage mbarrier ring with cp.async.bulk, one
-//    thread issues the 21 tcgen05.mma per k-step, four epilogue warps drain TMEM (tcgen05.ld),
-//    merge, release the accumulators and write the tile's V in the order pair_kr's epilogue
+//    thread issues the 21 tcgen05.mma per k-step, four epilogue warps drain TMEM (tcgen05.ld)
+//    diagonal by diagonal into eight rotating accumulator slots (a tile's MMAs start while the
+//    previous tile drains), merge, and write the tile's V in the order pair_kr's epilogue
 //    lanes read it: V[t][q 16][p 8][re/im][e_q x_alpha e_p y>>1 (16)][y&1].
 // Measured prototype (tools/oz_gemm.cu, cfg4 triangle): 1.6 ms incl. the 1.08 GB V write,
 // vs ~3.6 ms for the DMMA V phase of pair_kr.
@@ -116,10 +117,12 @@ __device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of
   return o;
 }
 
-__global__ void __launch_bounds__(256) oz_slice_kernel(OzParams P) {
+__global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
-  const int pt = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
+  // one warp per (point, channel): 8 warps = 2 points per CTA
+  const int wg = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
+  const int pt = wg >> 2, x = wg & 3;
   if (pt >= P.npts_oz) return;
   const PhiChunks ch{P.Go, P.Gv};
   const int KH = P.kh, ks_n = P.ks, nq = KH / 4;
@@ -129,27 +132,28 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzParams P) {
   const int pb = pt >> 4, prow = ((pt & 15) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
   int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KS;
   int8_t* const sb = P.sb + size_t(pb) * ks_n * B_KS;
-  for (int x = 0; x < NCH; ++x) {
-    // this lane's spinor quads a0 = 4 (lane + 32 j)
-    constexpr int MAXJ = 4;  // KH <= 512 (n_vir <= 512)
-    double re[MAXJ][4], im[MAXJ][4];
-    double mx = 0.0;
+  {
+    // this lane's spinor quads a0 = 4 (lane + 32 j); two passes over them (the row maximum, then
+    // the digits), the second from L1, so no values are held across the reduction
+    auto load = [&](int qd, double (&re)[4], double (&im)[4]) {
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const int qd = lane + 32 * j;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) re[j][i] = im[j][i] = 0.0;
-      if (live && qd < nq && 4 * qd < P.n_vir) {
+      for (int i = 0; i < 4; ++i) re[i] = im[i] = 0.0;
+      if (live && 4 * qd < P.n_vir) {
         const double* src = P.phi + ch.offset(P.Go + qd, pt, P.npts_pad);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i)
           if (4 * qd + i < P.n_vir) {
-            re[j][i] = src[(x * 4 + i) ^ swz];
-            im[j][i] = src[16 + ((x * 4 + i) ^ swz)];
+            re[i] = src[(x * 4 + i) ^ swz];
+            im[i] = src[16 + ((x * 4 + i) ^ swz)];
           }
-          mx = fmax(mx, fmax(fabs(re[j][i]), fabs(im[j][i])));
-        }
       }
+    };
+    double mx = 0.0;
+    for (int qd = lane; qd < nq; qd += 32) {
+      double re[4], im[4];
+      load(qd, re, im);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mx = fmax(mx, fmax(fabs(re[i]), fabs(im[i])));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -162,13 +166,11 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzParams P) {
       P.sb_scale[size_t(pb) * NB + rb] = ldexp(1.0, e);
       if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 49);
     }
-#pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const int qd = lane + 32 * j;
-      if (qd >= nq) break;
+    for (int qd = lane; qd < nq; qd += 32) {
       double xr[4], xi[4];
+      load(qd, xr, xi);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) xr[i] = re[j][i] * sc, xi[i] = im[j][i] * sc;
+      for (int i = 0; i < 4; ++i) xr[i] *= sc, xi[i] *= sc;
       uint32_t dr[S], di[S];
       digits4(xr, dr);
       digits4(xi, di);
@@ -195,6 +197,12 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(1024) int8_t sm[];
+  // Measured and rejected: eight rotating 64-column accumulator slots (tile i's diagonal d in slot
+  // (6 i + d) % 8, drained and freed diagonal by diagonal so the next tile starts early): V-GEMM
+  // 1.733 vs 1.571 ms on the same box; the next tile's k-step 0 waits on the drain diagonal by
+  // diagonal anyway, and TMEM reads under running MMAs are slower. Also rejected: A from TMEM
+  // (tcgen05.cp 128x256b per slice and k-step, MMA with [a_tmem]): exact, but 1.89 vs 1.59 ms
+  // (tools/oz_gemm.cu -DA_TMEM).
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -321,7 +329,7 @@ cudaError_t oz_kernel_setup() {
 }
 
 void launch_oz_slice(const OzParams& P, cudaStream_t s) {
-  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 7) / 8), dim3(256), 0, s, P);
+  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
 }
 
 double oz_int8_ops(const OzParams& P) { return double(P.ntiles) * (S * (S + 1) / 2) * 2.0 * MA * NB * 32.0 * P.ks; }

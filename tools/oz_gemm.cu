@@ -134,6 +134,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int8_t* sa = sm + stage * STAGE;
           const int8_t* sb = sa + A_KS;
 #ifndef NO_MMA  // probe: the operand stream alone
+#ifdef A_TMEM  // A slices copied once per k-step into TMEM (tcgen05.cp), MMAs read A from TMEM
+          const uint32_t abuf = tmem + 384u + uint32_t((ks & 1) * 48);
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(abuf + 8u * s),
+                         "l"(smem_desc(sa + s * MA * 32)));
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int t = 0; s + t < S; ++t) {
+              const uint32_t d = tmem + uint32_t((s + t) * NB);
+              const uint32_t acc = ks > 0 || s > 0 ? 1u : 0u;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                  "r"(abuf + 8u * s), "l"(smem_desc(sb + t * NB * 32)), "r"(idesc), "r"(acc));
+            }
+#else
 #pragma unroll
           for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -145,6 +163,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
                   "l"(smem_desc(sa + s * MA * 32)), "l"(smem_desc(sb + t * NB * 32)), "r"(idesc), "r"(acc));
             }
+#endif
 #else
           (void)sb;
 #endif
