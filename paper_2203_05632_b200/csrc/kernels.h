@@ -78,6 +78,8 @@ struct PairParams {
   int nens, ens_tiles;       // batched ensembles: m walkers each, st_ro[nens]
   const double* vtiles;      // pair_kr only, single ensemble: V blocks of every tile from
                              // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
+  double* otiles;            // pair_kr only, single ensemble, literal: write the o blocks of every
+                             // tile for oz_vgemm_kernel<true> and skip the V phase and the sums
 };
 
 // INT8 (Ozaki) V blocks of the Kramers pair stage (pair_oz.cu)
@@ -94,7 +96,15 @@ struct OzParams {
   int8_t* sb;                // [npts_oz / 16][ks][slice][64 rows x 32] B slices (P side)
   double* sa_scale;          // [npts_oz / 32][128]: 2^(e - 49)
   double* sb_scale;          // [npts_oz / 16][64]: 2^e
-  double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order
+  double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order (physical)
+  // fused literal contraction (oz_vgemm_kernel<true>): o blocks in, the step's sums out
+  const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>
+  int m;
+  double ng2, w_direct, w_exchange;
+  const DevState* st_ro;
+  DevState* st;
+  double* partials;          // [grid][4]
+  double* step_out;          // [6]
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);

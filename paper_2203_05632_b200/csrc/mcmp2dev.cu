@@ -89,6 +89,7 @@ struct mcmp2dev_handle {
   bool oz = true;
   int oz_m = 0;
   OzParams ozp{};
+  double* oz_otiles = nullptr;
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
   DevSites sites{};
   double* d_energies = nullptr;
@@ -195,10 +196,12 @@ struct mcmp2dev_handle {
     return oz && kramers && ne == 1 && mm >= 2 && !kr_qb1(mm, ne) && n_vir > 0 && n_vir <= 512;
   }
   void oz_free() {
-    for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v})
+    for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
+                    (void*)oz_otiles})
       if (p) cudaFree(p);
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
+    oz_otiles = nullptr;
     oz_m = 0;
   }
   // buffers of the INT8 V path for mm walkers (no-op when inactive or already large enough)
@@ -214,7 +217,12 @@ struct mcmp2dev_handle {
     ck(cudaMalloc(&ozp.sb, oz_slice_bytes_b(npts_oz, ks)), "cudaMalloc oz slices");
     ck(cudaMalloc(&ozp.sa_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
     ck(cudaMalloc(&ozp.sb_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
-    ck(cudaMalloc(&ozp.v, sizeof(double) * 8192 * ntiles), "cudaMalloc oz V blocks");
+    // physical estimator: V tiles for pair_kr's trace epilogue; literal: o tiles for the fused
+    // contraction in the V-GEMM epilogue
+    if (estimator == MCMP2DEV_ESTIMATOR_PHYSICAL)
+      ck(cudaMalloc(&ozp.v, sizeof(double) * 8192 * ntiles), "cudaMalloc oz V blocks");
+    else
+      ck(cudaMalloc(&oz_otiles, sizeof(double) * 4096 * ntiles), "cudaMalloc oz o blocks");
     oz_m = 16 * nbq;
   }
 
@@ -252,7 +260,10 @@ struct mcmp2dev_handle {
     p.nens = ne;
     p.ens_tiles = ne > 1 ? (kramers ? (qb1 ? pair_kr_tiles_qb1(p.nb) : pair_kr_tiles(p.nb)) : p.nb * (p.nb + 1) / 2) : 0;
     p.vtiles = nullptr;
-    if (oz_active(mm, ne)) {
+    p.otiles = nullptr;
+    const bool oz_path = oz_active(mm, ne);
+    const bool fused = oz_path && !p.physical;
+    if (oz_path) {
       if (mm > oz_m) throw RtError("mcmp2dev: INT8 V buffers not prepared for this ensemble size");
       OzParams o = ozp;
       o.phi = d_phi;
@@ -265,16 +276,36 @@ struct mcmp2dev_handle {
       o.npts_oz = 32 * nbq;
       oz_layout(n_vir, o.kh, o.ks);
       o.ntiles = nbq * (nbq + 1);
+      o.otiles = fused ? oz_otiles : nullptr;
+      o.m = mm;
+      o.ng2 = p.ng2;
+      o.w_direct = w_direct;
+      o.w_exchange = w_exchange;
+      o.st_ro = d_state;
+      o.st = d_state;
+      o.partials = d_partials;
+      o.step_out = step_out;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
-      launch_oz_vgemm(o, stream);
-      if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+      if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
+        p.otiles = oz_otiles;
+        launch_pair_kr(p, stream);
+        if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+        launch_oz_vgemm(o, stream);
+      } else {
+        launch_oz_vgemm(o, stream);
+        if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+        p.vtiles = o.v;
+        launch_pair_kr(p, stream);
+      }
       oz_ops = oz_int8_ops(o);
-      p.vtiles = o.v;
+    } else if (kramers && qb1) {
+      launch_pair_kr_qb1(p, stream);
+    } else if (kramers) {
+      launch_pair_kr(p, stream);
+    } else {
+      launch_pair(p, stream);
     }
-    if (kramers && qb1) launch_pair_kr_qb1(p, stream);
-    else if (kramers) launch_pair_kr(p, stream);
-    else launch_pair(p, stream);
     if (prof) {
       ck(cudaEventRecord(ev[3], stream), "event");
       ck(cudaEventSynchronize(ev[3]), "event sync");
@@ -286,14 +317,14 @@ struct mcmp2dev_handle {
       prof_ms[1] += b;
       prof_ms[2] += c;
       prof_ms[3] += a + b + c;
-      if (p.vtiles) {
+      if (oz_path) {  // slice, then V-GEMM and pair_kr in launch order (fused: pair_kr first)
         float x = 0, y = 0, z = 0;
         ck(cudaEventElapsedTime(&x, ev[2], ev_oz[0]), "elapsed");
         ck(cudaEventElapsedTime(&y, ev_oz[0], ev_oz[1]), "elapsed");
         ck(cudaEventElapsedTime(&z, ev_oz[1], ev[3]), "elapsed");
         prof_oz[0] += x;
-        prof_oz[1] += y;
-        prof_oz[2] += z;
+        prof_oz[1] += fused ? z : y;
+        prof_oz[2] += fused ? y : z;
         prof_oz[3] += 1;
       }
       prof_n[0] += 1;

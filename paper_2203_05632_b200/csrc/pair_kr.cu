@@ -142,9 +142,12 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 }
 }  // namespace
 
-// OZ: the V blocks come precomputed per tile from pair_oz.cu (P.vtiles, single ensemble): the
-// ring streams the occupied chunks only, and the V phase becomes one load per lane and (h, pp)
-template <bool PHYS, bool OZ>
+// OZ (single ensembles, pair_oz.cu; the ring streams the occupied chunks only):
+//  1: the V blocks come precomputed per tile (P.vtiles); the V phase becomes one load per lane
+//     and (h, pp) -- the physical estimator;
+//  2: O only: the tile's o values go to HBM (P.otiles, [q][x_alpha][re/im][p][e_p][y] doubles)
+//     and oz_vgemm_kernel<true> contracts them with its V blocks -- the literal estimator
+template <bool PHYS, int OZ>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
   pdl_wait();     // Phi of this step is visible
   pdl_trigger();  // persistent: the next step's walk may launch next to it
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
   const PhiChunks ch{P.Go, P.Gv};
   const int cO = ch.occ_chunks();  // chunks hold occupied or virtual groups, never both
   const int nchunks = OZ ? cO : ch.count();
+  static_assert(OZ != 2 || !PHYS, "the O-only mode serves the literal estimator");
   const int my_tiles = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (tid == 0) {
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
       double* const sO = sO0 + (it % OBUF) * SO_DOUBLES;
       // OZ: this lane's V values (h, pp) of the tile, loaded before the O phase hides their latency
       double2 ovr[2][PW], ovi[2][PW];
-      if constexpr (OZ) {
+      if constexpr (OZ == 1) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -292,8 +296,23 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
           }
           release();
         }
-        if constexpr (OBUF == 1) consumer_barrier(q1w);  // the group is done reading the previous o rows
         const int y = (lane >> 2) & 3, pp = lane & 3;
+        if constexpr (OZ == 2) {  // o = conj O~ to the tile's O block in HBM; no V phase here
+          double* ot = P.otiles + size_t(tt) * 4096;
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int n = 0; n < NB1; ++n)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
+                double* d = ot + (q * 4 + j * 2) * 64 + (p * 2 + e1) * 4 + y;
+                __stcg(d, t1[h][n][j] + t2[h][n][j]);
+                __stcg(d + 64, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]));
+              }
+          continue;
+        }
+        if constexpr (OBUF == 1) consumer_barrier(q1w);  // the group is done reading the previous o rows
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -366,7 +385,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
           for (int pp = 0; pp < PW; ++pp) {
             const int q = 4 * wq + 2 * h + hl, p = PW * wp + pp;
             double vr[2], vi[2];
-            if constexpr (OZ) {
+            if constexpr (OZ == 1) {
               vr[0] = ovr[h][pp].x, vr[1] = ovr[h][pp].y, vi[0] = ovi[h][pp].x, vi[1] = ovi[h][pp].y;
             } else {
 #pragma unroll
@@ -453,8 +472,8 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
             for (int j = 0; j < 2; ++j) {
               const int y = 2 * (lane & 1) + j;
               const int idx = o_index(ep, q, p, y, xa);
-              const double vr = OZ ? (j ? ovr[h][pp].y : ovr[h][pp].x) : u1[h][pp][j] + u2[h][pp][j];
-              const double vi = OZ ? (j ? ovi[h][pp].y : ovi[h][pp].x) : u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
+              const double vr = OZ == 1 ? (j ? ovr[h][pp].y : ovr[h][pp].x) : u1[h][pp][j] + u2[h][pp][j];
+              const double vi = OZ == 1 ? (j ? ovi[h][pp].y : ovi[h][pp].x) : u3[h][pp][j] - u1[h][pp][j] + u2[h][pp][j];
               f += sO[idx] * vr - sO[idx + 1] * vi;
             }
             f += __shfl_xor_sync(0xffffffffu, f, 1);
@@ -494,6 +513,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
       s_red[warp][1] = acc_x * cw;
     }
   }
+  if constexpr (OZ == 2) return;  // the step's sums are oz_vgemm_kernel<true>'s
   __syncthreads();
   if (batched) {
     if (tid == 0) {
@@ -578,8 +598,8 @@ cudaError_t KR_API(pair_kr_kernel_setup)() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_kr[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  for (auto k : {KR_API(pair_kr_kernel)<false, false>, KR_API(pair_kr_kernel)<true, false>,
-                 KR_API(pair_kr_kernel)<false, true>, KR_API(pair_kr_kernel)<true, true>}) {
+  for (auto k : {KR_API(pair_kr_kernel)<false, 0>, KR_API(pair_kr_kernel)<true, 0>, KR_API(pair_kr_kernel)<false, 1>,
+                 KR_API(pair_kr_kernel)<true, 1>, KR_API(pair_kr_kernel)<false, 2>}) {
     const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
   }
@@ -592,9 +612,11 @@ void KR_API(launch_pair_kr)(const PairParams& P, cudaStream_t s) {
   const int ntiles = P.nens > 1 ? P.nens * P.ens_tiles : kr_ntiles(P.nb);
   const int slots = MINB * (g_sms_kr[dev & 63] > 0 ? g_sms_kr[dev & 63] : 148);
   const int grid = ntiles < slots ? ntiles : slots;
-  const bool oz = P.vtiles != nullptr && P.nens <= 1;
-  auto k = P.physical ? (oz ? KR_API(pair_kr_kernel)<true, true> : KR_API(pair_kr_kernel)<true, false>)
-                      : (oz ? KR_API(pair_kr_kernel)<false, true> : KR_API(pair_kr_kernel)<false, false>);
+  const bool single = P.nens <= 1;
+  auto k = P.physical ? (single && P.vtiles ? KR_API(pair_kr_kernel)<true, 1> : KR_API(pair_kr_kernel)<true, 0>)
+           : single && P.otiles ? KR_API(pair_kr_kernel)<false, 2>
+           : single && P.vtiles ? KR_API(pair_kr_kernel)<false, 1>
+                                : KR_API(pair_kr_kernel)<false, 0>;
   pdl_launch(k, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
 }
 

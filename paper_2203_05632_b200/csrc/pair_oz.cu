@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
   }
 }
 
+template <bool FUSED>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
@@ -205,8 +206,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // (tools/oz_gemm.cu -DA_TMEM).
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_base;
+  __shared__ double s_red[4][2];
+  __shared__ bool s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
+  double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums (lanes with row % 8 == 0)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     mbar_init(&tfull, 1);
@@ -296,19 +300,91 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the stores below
       const double sr = P.sa_scale[size_t(a) * MA + row];
       const double* sbv = P.sb_scale + size_t(b) * NB;
-      double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8;
+      if constexpr (!FUSED) {
+        double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8;
 #pragma unroll
-      for (int p = 0; p < 8; ++p)
+        for (int p = 0; p < 8; ++p)
 #pragma unroll
-        for (int c = 0; c < 8; c += 2)
-          __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
-                 make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
-                              double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
+          for (int c = 0; c < 8; c += 2)
+            __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
+                   make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
+                                double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
+      } else {
+        // literal contraction (estimator.cpp:26-32) on the Kramers alpha rows, as pair_kr's epilogue:
+        // f(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) V(q e_q x_alpha; p e_p y),
+        // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds
+        // Re V (plane 0) or Im V (plane 1) for all (p, e_p, y): partial g = sum_y o_re Re V, or
+        // -sum_y o_im Im V, then the four lanes of (x_alpha, plane) add up.
+        const double* o = P.otiles + size_t(t) * 4096 + (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
+        double g[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k));
+          const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k + 2));
+          const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
+          const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
+          const double sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+          g[k] = plane ? -sgp : sgp;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          g[k] += __shfl_xor_sync(0xffffffffu, g[k], 1);
+          g[k] += __shfl_xor_sync(0xffffffffu, g[k], 2);
+          g[k] *= 2.0;
+        }
+        // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1)
+        const int qg = 16 * a + q, pg0 = 8 * b;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
+          const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
+          const int pg = pg0 + p;
+          if ((row & 7) == 0 && qg < P.m && pg < P.m && qg > pg) {
+            acc_d += (-P.w_direct * g[2 * p]) * f11;       // f1d f2d
+            acc_x += (-P.w_exchange * f10) * g[2 * p + 1];  // f1x f2x
+          }
+        }
+      }
+    }
+    if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the four epilogue warps in order
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        acc_d += __shfl_down_sync(0xffffffffu, acc_d, o);
+        acc_x += __shfl_down_sync(0xffffffffu, acc_x, o);
+      }
+      if (lane == 0) s_red[warp][0] = acc_d, s_red[warp][1] = acc_x;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  if constexpr (FUSED) {  // per-CTA partials, then the last CTA's fixed-order sum (as pair_kr.cu)
+    if (tid == 0) {
+      const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
+      P.partials[size_t(blockIdx.x) * 4 + 0] = (((s_red[0][0] + s_red[1][0]) + s_red[2][0]) + s_red[3][0]) * cw;
+      P.partials[size_t(blockIdx.x) * 4 + 1] = 0.0;
+      P.partials[size_t(blockIdx.x) * 4 + 2] = (((s_red[0][1] + s_red[1][1]) + s_red[2][1]) + s_red[3][1]) * cw;
+      P.partials[size_t(blockIdx.x) * 4 + 3] = 0.0;
+      __threadfence();
+      s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    double d = 0.0, x = 0.0;
+    for (unsigned c = 0; c < gridDim.x; ++c) {
+      d += P.partials[size_t(c) * 4 + 0];
+      x += P.partials[size_t(c) * 4 + 2];
+    }
+    const double npairs = 0.5 * P.m * (P.m - 1);
+    P.step_out[0] = (d + x) / npairs;
+    P.step_out[1] = 0.0;
+    P.step_out[2] = d;
+    P.step_out[3] = 0.0;
+    P.step_out[4] = x;
+    P.step_out[5] = 0.0;
+    P.st->done_pair = 0;
+  }
 }
 
 int g_sms_oz[64];
@@ -325,7 +401,9 @@ cudaError_t oz_kernel_setup() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_oz[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return cudaFuncSetAttribute(oz_vgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(oz_vgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
 void launch_oz_slice(const OzParams& P, cudaStream_t s) {
@@ -339,7 +417,10 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   cudaGetDevice(&dev);
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
   const int grid = P.ntiles < sms ? P.ntiles : sms;
-  pdl_launch(oz_vgemm_kernel, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+  if (P.otiles)
+    pdl_launch(oz_vgemm_kernel<true>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+  else
+    pdl_launch(oz_vgemm_kernel<false>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
 }
 
 }  // namespace mcmp2dev
