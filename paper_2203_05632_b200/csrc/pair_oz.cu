@@ -48,7 +48,14 @@ constexpr int A_KS = S * MA * 32;  // bytes of one k-step (32 of K') of a Q bloc
 constexpr int B_KS = S * NB * 32;
 constexpr int STAGE = A_KS + B_KS;
 constexpr int STAGES = 5;
-constexpr int THREADS = 6 * 32;    // warps 0-3 epilogue (TMEM lanes 0-127), 4 producer, 5 MMA
+#ifndef OZ_EPW
+#define OZ_EPW 8
+#endif
+// epilogue warps: EPW / 4 per TMEM lane quarter (warp w reads lanes 32 (w % 4) ..), each with
+// NB / (EPW / 4) accumulator columns; then the producer warp and the MMA warp
+constexpr int EPW = OZ_EPW;
+constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
+constexpr int THREADS = (EPW + 2) * 32;
 constexpr int SMEM_BYTES = STAGES * STAGE;
 constexpr int TMEM_COLS = 512;     // 6 x 64 used
 
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // (tools/oz_gemm.cu -DA_TMEM).
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_base;
-  __shared__ double s_red[4][2];
+  __shared__ double s_red[EPW][2];
   __shared__ bool s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
@@ -214,7 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     mbar_init(&tfull, 1);
-    mbar_init(&tempty, 128);
+    mbar_init(&tempty, 32 * EPW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   const int ntiles = P.ntiles;
   const int my = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
-  if (warp == 4) {
+  if (warp == EPW) {
     if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
       int stage = 0;
       uint32_t ph = 0;
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == EPW + 1) {
     if (lane == 0) {  // MMA issuer: 21 slice products per k-step into the diagonal accumulators
       int stage = 0;
       uint32_t ph = 0;
@@ -272,8 +279,9 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         umma_commit(&tfull);
       }
     }
-  } else {  // epilogue: TMEM lane = A row
-    const int row = warp * 32 + lane;
+  } else {  // epilogue: TMEM lane = A row; this warp's columns [c_lo, c_lo + CPW)
+    const int lq = warp & 3, c_lo = (warp >> 2) * CPW;
+    const int row = lq * 32 + lane;
     const int q = row >> 3, plane = row & 1, exq = (row >> 1) & 3;
     for (int it = 0; it < my; ++it) {
       const int t = int(blockIdx.x) + it * int(gridDim.x);
@@ -281,12 +289,13 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       oz_tile(t, a, b);
       mbar_wait(&tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      long long X[NB];
+      long long X[CPW];
 #pragma unroll
-      for (int c0 = 0; c0 < NB; c0 += 16) {
+      for (int c0 = 0; c0 < CPW; c0 += 16) {
         uint32_t v[S][16];
 #pragma unroll
-        for (int d = 0; d < S; ++d) tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(d * NB + c0), v[d]);
+        for (int d = 0; d < S; ++d)
+          tmem_ld16(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -297,13 +306,13 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the stores below
+      mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the work below
       const double sr = P.sa_scale[size_t(a) * MA + row];
-      const double* sbv = P.sb_scale + size_t(b) * NB;
+      const double* sbv = P.sb_scale + size_t(b) * NB + c_lo;
       if constexpr (!FUSED) {
-        double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8;
+        double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8 + c_lo * 8;
 #pragma unroll
-        for (int p = 0; p < 8; ++p)
+        for (int p = 0; p < CPW / 8; ++p)
 #pragma unroll
           for (int c = 0; c < 8; c += 2)
             __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
@@ -313,12 +322,13 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // literal contraction (estimator.cpp:26-32) on the Kramers alpha rows, as pair_kr's epilogue:
         // f(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) V(q e_q x_alpha; p e_p y),
         // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds
-        // Re V (plane 0) or Im V (plane 1) for all (p, e_p, y): partial g = sum_y o_re Re V, or
+        // Re V (plane 0) or Im V (plane 1) for its (p, e_p, y): partial g = sum_y o_re Re V, or
         // -sum_y o_im Im V, then the four lanes of (x_alpha, plane) add up.
-        const double* o = P.otiles + size_t(t) * 4096 + (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
-        double g[16];
+        const double* o = P.otiles + size_t(t) * 4096 + (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64 + c_lo;
+        constexpr int NK = CPW / 4;  // (p, e_p) of this warp
+        double g[NK];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < NK; ++k) {
           const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k));
           const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k + 2));
           const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
@@ -327,15 +337,15 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           g[k] = plane ? -sgp : sgp;
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < NK; ++k) {
           g[k] += __shfl_xor_sync(0xffffffffu, g[k], 1);
           g[k] += __shfl_xor_sync(0xffffffffu, g[k], 2);
           g[k] *= 2.0;
         }
         // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1)
-        const int qg = 16 * a + q, pg0 = 8 * b;
+        const int qg = 16 * a + q, pg0 = 8 * b + c_lo / 8;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
+        for (int p = 0; p < NK / 2; ++p) {
           const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
           const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
           const int pg = pg0 + p;
@@ -346,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
       }
     }
-    if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the four epilogue warps in order
+    if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         acc_d += __shfl_down_sync(0xffffffffu, acc_d, o);
@@ -361,9 +371,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   if constexpr (FUSED) {  // per-CTA partials, then the last CTA's fixed-order sum (as pair_kr.cu)
     if (tid == 0) {
       const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
-      P.partials[size_t(blockIdx.x) * 4 + 0] = (((s_red[0][0] + s_red[1][0]) + s_red[2][0]) + s_red[3][0]) * cw;
+      double d = 0.0, x = 0.0;
+      for (int w = 0; w < EPW; ++w) d += s_red[w][0], x += s_red[w][1];
+      P.partials[size_t(blockIdx.x) * 4 + 0] = d * cw;
       P.partials[size_t(blockIdx.x) * 4 + 1] = 0.0;
-      P.partials[size_t(blockIdx.x) * 4 + 2] = (((s_red[0][1] + s_red[1][1]) + s_red[2][1]) + s_red[3][1]) * cw;
+      P.partials[size_t(blockIdx.x) * 4 + 2] = x * cw;
       P.partials[size_t(blockIdx.x) * 4 + 3] = 0.0;
       __threadfence();
       s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;

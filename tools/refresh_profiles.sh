@@ -4,7 +4,7 @@
 #   `ncu --set full` capture of each kernel at cfg4 (tools/ncu_summary.py TAG reads them back).
 # usage: gpurun --timeout 1800 -- 'bash tools/refresh_profiles.sh r01k'
 set -u
-TAG=${1:-r01k}
+TAG=${1:-r03}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/${TAG}_smi.txt 2>&1
