@@ -119,11 +119,14 @@ def clocks_summary(path: Path, index: int):
             "reasons": sorted(reasons), "samples": len(rows)}
 
 
-# dense tcgen05 INT8 rate measured on this pool's B200 (tools/umma_i8.cu, one MMA stream per SM;
-# cuBLASLt torch._int_mm 2840 TOPS); nominal dense INT8/FP8 4.5 POPS (B200_PROFILING.md)
-INT8_PEAK = 2858.0
-INT8_PEAK_SOURCE = ("measured: tools/umma_i8.cu tcgen05.mma kind::i8 M128 N64 K32 loop, 2858 TOPS "
-                    "(profiles/r01_legacy_mma_peaks.txt); nominal dense 4500 TOPS")
+# dense tcgen05 INT8 rate measured on this pool's B200 (tools/umma_rate.cu: M128 N256 K32 kind::i8
+# MMAs from shared memory, one issuing thread per SM, 4570 TOPS; nominal dense INT8/FP8 4.5 POPS,
+# B200_PROFILING.md). Shape ceiling of the kernel's own M128 N80 instruction mix: 3132 TOPS
+# (the same probe at N = 80: an M128 kind::i8 MMA costs ~61 cycles for any N <= 80).
+INT8_PEAK = 4570.0
+INT8_SHAPE_CEILING = 3132.0
+INT8_PEAK_SOURCE = ("measured: tools/umma_rate.cu tcgen05.mma kind::i8 M128 N256 K32, 4570 TOPS (nominal dense 4500); "
+                    "ceiling of the kernel's M128 N80 MMA shape on the same probe 3132 TOPS (profiles/r03_umma_rate.txt)")
 
 
 def peaks():
@@ -373,8 +376,9 @@ def main():
                                          "sums of exact int8 products, pair_oz.cu)",
             "achieved": a8, "peak": INT8_PEAK, "unit": "TFLOP/s", "frac": a8 / INT8_PEAK,
             "traffic": traffic_of("oz_vgemm_kernel"),
-            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 64 x K' per launch",
-            "peak_source": INT8_PEAK_SOURCE,
+            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 80 x K' per launch",
+            "peak_source": INT8_PEAK_SOURCE, "shape_ceiling": INT8_SHAPE_CEILING,
+            "frac_of_shape_ceiling": a8 / INT8_SHAPE_CEILING,
             "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
             "vgemm_share_of_step": vg_ms / step_ms_prof,
             "pair_stage_fp64": dict(fp64_view, kernel="pair stage: oz_slice_kernel + oz_vgemm_kernel + pair_kr_kernel "

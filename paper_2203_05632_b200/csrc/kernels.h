@@ -91,11 +91,12 @@ struct OzParams {
   int npts;                  // 2m points with data
   int npts_oz;               // points covered by the slice blocks (32 per Q block)
   int kh, ks;                // K' = 2 kh = 32 ks
-  int ntiles;                // pair_kr tile triangle (16 x 8 walkers)
+  int ntiles;                // V-GEMM tile triangle (16 x nb_rows / 8 walkers)
+  int nb_rows;               // B rows per tile: 64 (physical; pair_kr's 16 x 8 tiles) or 80 (fused)
   int8_t* sa;                // [npts_oz / 32][ks][slice][128 rows x 32] A slices (Q side)
-  int8_t* sb;                // [npts_oz / 16][ks][slice][64 rows x 32] B slices (P side)
+  int8_t* sb;                // [P blocks][ks][slice][nb_rows x 32] B slices (P side, nb_rows / 4 points each)
   double* sa_scale;          // [npts_oz / 32][128]: 2^(e - 49)
-  double* sb_scale;          // [npts_oz / 16][64]: 2^e
+  double* sb_scale;          // [P blocks][nb_rows]: 2^e
   double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order (physical)
   // fused literal contraction (oz_vgemm_kernel<true>): o blocks in, the step's sums out
   const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>
@@ -108,7 +109,10 @@ struct OzParams {
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);
-size_t oz_slice_bytes_b(int npts_oz, int ks);
+size_t oz_slice_bytes_b(int npts_oz, int ks, int nb_rows);
+int oz_p_blocks(int npts_oz, int nb_rows);
+int oz_nb_rows(bool fused);
+int oz_ntiles(int nbq, bool fused);
 void launch_oz_slice(const OzParams& P, cudaStream_t s);
 void launch_oz_vgemm(const OzParams& P, cudaStream_t s);
 double oz_int8_ops(const OzParams& P);  // executed int8 tensor ops of one V-GEMM launch

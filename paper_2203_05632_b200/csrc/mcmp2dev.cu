@@ -214,9 +214,15 @@ struct mcmp2dev_handle {
     const size_t ntiles = size_t(nbq) * (nbq + 1);
     ck(cudaStreamSynchronize(stream), "oz sync");
     ck(cudaMalloc(&ozp.sa, oz_slice_bytes_a(npts_oz, ks)), "cudaMalloc oz slices");
-    ck(cudaMalloc(&ozp.sb, oz_slice_bytes_b(npts_oz, ks)), "cudaMalloc oz slices");
+    // B blocks: 8 walkers (physical) or 10 (literal, fused); rows past the last point stay zero
+    const int nbr = oz_nb_rows(estimator != MCMP2DEV_ESTIMATOR_PHYSICAL);
+    const size_t sb_bytes = oz_slice_bytes_b(npts_oz, ks, nbr);
+    const size_t sbs_bytes = sizeof(double) * oz_p_blocks(npts_oz, nbr) * nbr;
+    ck(cudaMalloc(&ozp.sb, sb_bytes), "cudaMalloc oz slices");
+    ck(cudaMemset(ozp.sb, 0, sb_bytes), "memset oz slices");
     ck(cudaMalloc(&ozp.sa_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
-    ck(cudaMalloc(&ozp.sb_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
+    ck(cudaMalloc(&ozp.sb_scale, sbs_bytes), "cudaMalloc oz scales");
+    ck(cudaMemset(ozp.sb_scale, 0, sbs_bytes), "memset oz scales");
     // physical estimator: V tiles for pair_kr's trace epilogue; literal: o tiles for the fused
     // contraction in the V-GEMM epilogue
     if (estimator == MCMP2DEV_ESTIMATOR_PHYSICAL)
@@ -275,7 +281,8 @@ struct mcmp2dev_handle {
       const int nbq = (mm + 15) / 16;
       o.npts_oz = 32 * nbq;
       oz_layout(n_vir, o.kh, o.ks);
-      o.ntiles = nbq * (nbq + 1);
+      o.ntiles = oz_ntiles(nbq, fused);
+      o.nb_rows = oz_nb_rows(fused);
       o.otiles = fused ? oz_otiles : nullptr;
       o.m = mm;
       o.ng2 = p.ng2;

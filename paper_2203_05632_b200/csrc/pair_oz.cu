@@ -43,10 +43,8 @@ namespace {
 using namespace pairk;
 
 constexpr int S = OZ_SLICES;
-constexpr int MA = 128, NB = 64;   // A rows (Q side) and B rows (P side) of a tile
-constexpr int A_KS = S * MA * 32;  // bytes of one k-step (32 of K') of a Q block, all slices
-constexpr int B_KS = S * NB * 32;
-constexpr int STAGE = A_KS + B_KS;
+constexpr int MA = 128;             // A rows (Q side) of a tile: 16 walkers
+constexpr int A_KS = S * MA * 32;   // bytes of one k-step (32 of K') of a Q block, all slices
 constexpr int STAGES = 5;
 #ifndef OZ_EPW
 #define OZ_EPW 8
@@ -54,10 +52,25 @@ constexpr int STAGES = 5;
 // epilogue warps: EPW / 4 per TMEM lane quarter (warp w reads lanes 32 (w % 4) ..), each with
 // NB / (EPW / 4) accumulator columns; then the producer warp and the MMA warp
 constexpr int EPW = OZ_EPW;
-constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
 constexpr int THREADS = (EPW + 2) * 32;
-constexpr int SMEM_BYTES = STAGES * STAGE;
-constexpr int TMEM_COLS = 512;     // 6 x 64 used
+constexpr int TMEM_COLS = 512;      // 6 x NB used
+// B rows (P side) per tile: 8 walkers (64 rows, the V tiles of the physical path follow
+// pair_kr's 16 x 8 tiles) or 10 walkers (80 rows, the fused literal path: a kind::i8 M128 MMA
+// costs the same ~61 cycles for N = 32..80 (tools/umma_rate.cu), so N = 80 -- the widest that
+// fits six accumulators in 512 TMEM columns -- does 25% more work per instruction)
+template <bool FUSED>
+struct OzShape {
+  static constexpr int NB = FUSED ? 80 : 64;
+  static constexpr int PW = NB / 8;  // P walkers per tile
+  static constexpr int B_KS = S * NB * 32;
+  static constexpr int STAGE = A_KS + B_KS;
+  static constexpr int SMEM_BYTES = STAGES * STAGE;
+  static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
+  // instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = NB
+  static constexpr uint32_t IDESC =
+      (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
+};
+static_assert(5 * OzShape<true>::STAGE <= 227 * 1024, "stage ring");
 
 // canonical K-major, no-swizzle UMMA operand layout of one k-step: [row / 8][k / 16][row % 8][16 B]
 __host__ __device__ __forceinline__ int op_off(int r, int kk) {
@@ -67,9 +80,7 @@ __device__ __forceinline__ uint64_t umma_desc(const void* p) {  // LBO 128 B (k 
   return uint64_t((smem_u32(p) >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
          (uint64_t(1) << 46);
 }
-// instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = 64
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
-
+template <uint32_t IDESC>
 __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -87,14 +98,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(addr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr));
+}
 
-// tile t = a (a + 1) + b: Q block a (walkers 16a ..), P block b < 2 (a + 1) (walkers 8b ..)
-__device__ __forceinline__ void oz_tile(int t, int& a, int& b) {
-  int r = int((sqrt(4.0 * double(t) + 1.0) - 1.0) * 0.5);
-  while ((r + 1) * (r + 2) <= t) ++r;
-  while (r * (r + 1) > t) --r;
-  a = r;
-  b = t - r * (r + 1);
+// the tile triangle, row by row: Q block a (walkers 16a ..) holds P blocks b < ceil(16 (a+1) / pw)
+// (walkers pw b ..); a CTA walks tiles t0, t0 + stride, ... (for pw = 8, t = a (a + 1) + b is
+// pair_kr's tile numbering)
+struct OzWalk {
+  int a = 0, b, pw;
+  __device__ OzWalk(int t0, int pw_) : b(t0), pw(pw_) { settle(); }
+  __device__ int len() const { return (16 * (a + 1) + pw - 1) / pw; }
+  __device__ void settle() {
+    while (b >= len()) b -= len(), ++a;
+  }
+  __device__ void next(int stride) { b += stride, settle(); }
+};
+int oz_tiles(int nbq, int pw) {
+  int n = 0;
+  for (int a = 0; a < nbq; ++a) n += (16 * (a + 1) + pw - 1) / pw;
+  return n;
 }
 
 // six signed digits of 4 values in (-1, 1): x = sum_s d_s 128^-(s+1) + rem, each digit the
@@ -136,9 +161,10 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
   const bool live = pt < P.npts;
   const int swz = phi_swz(pt);
   const int qb = pt >> 5, qrow = ((pt & 31) >> 1) * 8 + (pt & 1) * 4;  // A row of (x_alpha 0, re)
-  const int pb = pt >> 4, prow = ((pt & 15) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
+  const int NB = P.nb_rows, bpts = NB / 4;  // B rows and points per P block
+  const int pb = pt / bpts, prow = ((pt % bpts) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
   int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KS;
-  int8_t* const sb = P.sb + size_t(pb) * ks_n * B_KS;
+  int8_t* const sb = P.sb + size_t(pb) * ks_n * S * NB * 32;
   {
     // this lane's spinor quads a0 = 4 (lane + 32 j); two passes over them (the row maximum, then
     // the digits), the second from L1, so no values are held across the reduction
@@ -202,6 +228,8 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
 
 template <bool FUSED>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
+  using Sh = OzShape<FUSED>;
+  constexpr int NB = Sh::NB, PW = Sh::PW, B_KS = Sh::B_KS, STAGE = Sh::STAGE, CPW = Sh::CPW;
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(1024) int8_t sm[];
@@ -240,9 +268,9 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
       int stage = 0;
       uint32_t ph = 0;
-      for (int it = 0; it < my; ++it) {
-        int a, b;
-        oz_tile(int(blockIdx.x) + it * int(gridDim.x), a, b);
+      OzWalk w(int(blockIdx.x), PW);
+      for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
+        const int a = w.a, b = w.b;
         const int8_t* ga = P.sa + size_t(a) * KS * A_KS;
         const int8_t* gb = P.sb + size_t(b) * KS * B_KS;
         for (int ks = 0; ks < KS; ++ks) {
@@ -271,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int t = 0; s + t < S; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
-              umma_i8(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32), umma_desc(sb + t * NB * 32),
+              umma_i8<Sh::IDESC>(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32), umma_desc(sb + t * NB * 32),
                       ks > 0 || s > 0 ? 1u : 0u);
           umma_commit(&empty[stage]);  // the stage is free once these MMAs have read it
           if (++stage == STAGES) stage = 0, ph ^= 1u;
@@ -283,27 +311,39 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     const int lq = warp & 3, c_lo = (warp >> 2) * CPW;
     const int row = lq * 32 + lane;
     const int q = row >> 3, plane = row & 1, exq = (row >> 1) & 3;
-    for (int it = 0; it < my; ++it) {
+    OzWalk w(int(blockIdx.x), PW);
+    for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
       const int t = int(blockIdx.x) + it * int(gridDim.x);
-      int a, b;
-      oz_tile(t, a, b);
+      const int a = w.a, b = w.b;
       mbar_wait(&tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       long long X[CPW];
-#pragma unroll
-      for (int c0 = 0; c0 < CPW; c0 += 16) {
-        uint32_t v[S][16];
-#pragma unroll
-        for (int d = 0; d < S; ++d)
-          tmem_ld16(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      auto merge = [&](const uint32_t (&v)[S][16], int c0, int n) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
+          if (c >= n) break;
           long long x = int32_t(v[0][c]);
 #pragma unroll
           for (int d = 1; d < S; ++d) x = x * 128 + int32_t(v[d][c]);
           X[c0 + c] = x;
         }
+      };
+#pragma unroll
+      for (int c0 = 0; c0 + 16 <= CPW; c0 += 16) {
+        uint32_t v[S][16];
+#pragma unroll
+        for (int d = 0; d < S; ++d)
+          tmem_ld16(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        merge(v, c0, 16);
+      }
+      if constexpr (CPW % 16 != 0) {  // N = 80: a last 8-column chunk
+        constexpr int c0 = CPW / 16 * 16;
+        uint32_t v[S][16];
+#pragma unroll
+        for (int d = 0; d < S; ++d) tmem_ld8(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        merge(v, c0, 8);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the work below
@@ -324,16 +364,23 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds
         // Re V (plane 0) or Im V (plane 1) for its (p, e_p, y): partial g = sum_y o_re Re V, or
         // -sum_y o_im Im V, then the four lanes of (x_alpha, plane) add up.
-        const double* o = P.otiles + size_t(t) * 4096 + (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64 + c_lo;
+        // o blocks are in pair_kr's 16 x 8 tiles: walker p of this tile is p_g = PW b + p, in pair_kr
+        // tile a (a + 1) + p_g / 8 (none past the triangle row: those pairs are masked below)
+        const int row_o = (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
         double g[NK];
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
-          const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k));
-          const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 4 * k + 2));
-          const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
-          const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
-          const double sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+          const int pg = PW * b + (c_lo + 4 * k) / 8;
+          double sgp = 0.0;
+          if (pg < 16 * (a + 1)) {
+            const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+            const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o));
+            const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 2));
+            const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
+            const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
+            sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+          }
           g[k] = plane ? -sgp : sgp;
         }
 #pragma unroll
@@ -343,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           g[k] *= 2.0;
         }
         // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1)
-        const int qg = 16 * a + q, pg0 = 8 * b + c_lo / 8;
+        const int qg = 16 * a + q, pg0 = PW * b + c_lo / 8;
 #pragma unroll
         for (int p = 0; p < NK / 2; ++p) {
           const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
@@ -407,22 +454,31 @@ void oz_layout(int n_vir, int& kh, int& ks) {
   ks = 2 * kh / 32;
 }
 size_t oz_slice_bytes_a(int npts_pad, int ks) { return size_t(npts_pad / 32) * ks * A_KS; }
-size_t oz_slice_bytes_b(int npts_pad, int ks) { return size_t(npts_pad / 16) * ks * B_KS; }
+int oz_p_blocks(int npts_oz, int nb_rows) { return (npts_oz + nb_rows / 4 - 1) / (nb_rows / 4); }
+size_t oz_slice_bytes_b(int npts_oz, int ks, int nb_rows) {
+  return size_t(oz_p_blocks(npts_oz, nb_rows)) * ks * S * nb_rows * 32;
+}
+int oz_nb_rows(bool fused) { return fused ? OzShape<true>::NB : OzShape<false>::NB; }
+int oz_ntiles(int nbq, bool fused) { return oz_tiles(nbq, oz_nb_rows(fused) / 8); }
 
 cudaError_t oz_kernel_setup() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_oz[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  const cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             OzShape<false>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(oz_vgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  return cudaFuncSetAttribute(oz_vgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              OzShape<true>::SMEM_BYTES);
 }
 
 void launch_oz_slice(const OzParams& P, cudaStream_t s) {
   pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
 }
 
-double oz_int8_ops(const OzParams& P) { return double(P.ntiles) * (S * (S + 1) / 2) * 2.0 * MA * NB * 32.0 * P.ks; }
+double oz_int8_ops(const OzParams& P) {
+  return double(P.ntiles) * (S * (S + 1) / 2) * 2.0 * MA * P.nb_rows * 32.0 * P.ks;
+}
 
 void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   int dev = 0;
@@ -430,9 +486,9 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
   const int grid = P.ntiles < sms ? P.ntiles : sms;
   if (P.otiles)
-    pdl_launch(oz_vgemm_kernel<true>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+    pdl_launch(oz_vgemm_kernel<true>, dim3(grid), dim3(THREADS), OzShape<true>::SMEM_BYTES, s, P);
   else
-    pdl_launch(oz_vgemm_kernel<false>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, P);
+    pdl_launch(oz_vgemm_kernel<false>, dim3(grid), dim3(THREADS), OzShape<false>::SMEM_BYTES, s, P);
 }
 
 }  // namespace mcmp2dev
