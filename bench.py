@@ -382,7 +382,7 @@ def main():
             "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
             "vgemm_share_of_step": vg_ms / step_ms_prof,
             "pair_stage_fp64": dict(fp64_view, kernel="pair stage: oz_slice_kernel + oz_vgemm_kernel + pair_kr_kernel "
-                                    "(O blocks by DMMA, V blocks read back)", why_frac_above_1=(
+                                    "(literal: O blocks by DMMA, V blocks by INT8 with the contraction fused into the V-GEMM epilogue)", why_frac_above_1=(
                 "the pair stage computes the reference's FP64 contraction with fewer FP64 operations: the V blocks "
                 "(~90% of the work) as exact int8 tensor products (Ozaki splitting, pair_oz.cu), the O blocks by DMMA "
                 "with 3M complex products on the Kramers alpha rows (pair_kr.cu)"))}
