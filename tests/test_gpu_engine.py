@@ -150,3 +150,21 @@ def test_batched_kill_and_resume_is_bit_exact(cfgdir, tmp_path):
     full = walker.run_config_text(cfg)
     walker.run_config_text(cfg, abort_after_intervals=1)
     assert walker.resume(ck) == full
+
+
+def test_int8_v_path_engine_run_matches_oracle_and_resumes_bit_exact(cfgdir, tmp_path):
+    """cfg3 with 192 walkers takes the INT8 (Ozaki) V path through the C++ Engine: the run agrees
+    with the CPU oracle's Engine to 1e-9 (same Philox stream, per-step values within 1e-10), and a
+    run killed after one checkpoint interval resumes bit-exactly (fixed-order reductions)."""
+    ck = tmp_path / "oz.ckpt"
+    cfg = small(cfgdir, name="cfg3", walkers=192, steps=40, burnin=20, **{"checkpoint-interval": 20},
+                checkpoint=str(ck))
+    full = walker.run_config_text(cfg)
+    walker.run_config_text(cfg, abort_after_intervals=1)
+    assert walker.resume(ck) == full
+    dev = parse(full)
+    ref = parse(oracle_py.run_config(small(cfgdir, name="cfg3", walkers=192, steps=40, burnin=20,
+                                           **{"checkpoint-interval": 20})))
+    assert dev["steps"] == ref["steps"] == 40
+    assert dev["value"] == pytest.approx(ref["value"], rel=1e-9)
+    assert dev["sigma_bar"] == pytest.approx(ref["sigma_bar"], rel=1e-6)
