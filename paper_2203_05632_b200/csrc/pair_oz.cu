@@ -149,7 +149,10 @@ __device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of
   return o;
 }
 
-__global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
+// HELD: n_vir <= 384 (at most 3 quads per lane): one load pass, the values held in registers
+// across the row-maximum reduction (3x the loads in flight); otherwise two passes (max, digits)
+template <bool HELD>
+__global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
   // one warp per (point, channel): 8 warps = 2 points per CTA
@@ -182,11 +185,22 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
       }
     };
     double mx = 0.0;
-    for (int qd = lane; qd < nq; qd += 32) {
-      double re[4], im[4];
-      load(qd, re, im);
+    constexpr int MAXJ = HELD ? 3 : 1;
+    double hr[MAXJ][4], hi[MAXJ][4];
+    if constexpr (HELD) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) mx = fmax(mx, fmax(fabs(re[i]), fabs(im[i])));
+      for (int j = 0; j < MAXJ; ++j) load(lane + 32 * j < nq ? lane + 32 * j : nq, hr[j], hi[j]);
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx = fmax(mx, fmax(fabs(hr[j][i]), fabs(hi[j][i])));
+    } else {
+      for (int qd = lane; qd < nq; qd += 32) {
+        double re[4], im[4];
+        load(qd, re, im);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mx = fmax(mx, fmax(fabs(re[i]), fabs(im[i])));
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -199,9 +213,7 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
       P.sb_scale[size_t(pb) * NB + rb] = ldexp(1.0, e);
       if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 49);
     }
-    for (int qd = lane; qd < nq; qd += 32) {
-      double xr[4], xi[4];
-      load(qd, xr, xi);
+    auto emit = [&](int qd, double (&xr)[4], double (&xi)[4]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) xr[i] *= sc, xi[i] *= sc;
       uint32_t dr[S], di[S];
@@ -221,6 +233,17 @@ __global__ void __launch_bounds__(256, 3) oz_slice_kernel(OzParams P) {
           *reinterpret_cast<uint32_t*>(a0 + op_off(ra + 1, kre & 31)) = di[s];
           *reinterpret_cast<uint32_t*>(a1 + op_off(ra + 1, kim & 31)) = neg4(dr[s]);
         }
+      }
+    };
+    if constexpr (HELD) {
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j)
+        if (lane + 32 * j < nq) emit(lane + 32 * j, hr[j], hi[j]);
+    } else {
+      for (int qd = lane; qd < nq; qd += 32) {
+        double xr[4], xi[4];
+        load(qd, xr, xi);
+        emit(qd, xr, xi);
       }
     }
   }
@@ -473,7 +496,10 @@ cudaError_t oz_kernel_setup() {
 }
 
 void launch_oz_slice(const OzParams& P, cudaStream_t s) {
-  pdl_launch(oz_slice_kernel, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
+  if (P.kh / 4 <= 96)
+    pdl_launch(oz_slice_kernel<true>, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
+  else
+    pdl_launch(oz_slice_kernel<false>, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
 }
 
 double oz_int8_ops(const OzParams& P) {
