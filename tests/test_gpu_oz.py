@@ -77,3 +77,26 @@ def test_int8_v_not_used_where_ineligible(cfgdir):
     assert not dw.int8_v()
     dw.kramers(1)
     assert not dw.int8_v(0) and dw.int8_v(1)
+
+
+@pytest.mark.parametrize("name,m", [("cfg5-86", 1024), ("cfg5-36", 640)])
+def test_int8_v_heavy_atoms_match_oracle(cfgdir, tmp_path, name, m):
+    """cfg5 sweep members with other K' (n_vir 208 / 94: 13 / 6 k-steps) and ensemble sizes that
+    are not multiples of the 10-walker P blocks, one production step each, against the oracle's
+    full C(m,2) pair loop (rows over host threads)."""
+    import os
+    from paper_2203_05632_b200 import generate_config
+    sp, conf = generate_config(name, tmp_path)
+    text = conf.read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    dw = DeviceWalker(System(sp, text), max_walkers=m)
+    assert dw.int8_v()
+    dw.init_ensemble(m, seed=8)
+    dw.burn_in(20)
+    dw.advance(1)
+    w = dw.get_ensemble().walkers[:, :8]
+    tau = 0.05
+    ref = orc.replay_parallel(w, tau, threads=max(1, min(32, os.cpu_count() or 1)))
+    got = dw.replay(w[None], np.array([tau]))[0]
+    for k in (0, 2, 4):
+        assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), k
