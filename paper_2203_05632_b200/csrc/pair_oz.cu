@@ -1,15 +1,15 @@
 // pair_oz.cu — the virtual Green's-function blocks of the Kramers pair stage on the INT8 tensor
 // cores (tcgen05.mma kind::i8), FP64-accurate by Ozaki splitting.
 //
-// For every walker tile of pair_kr.cu (16 Q walkers x 8 P walkers, the same triangle and tile
-// numbering t = a (a + 1) + b), the V phase computes, for Q points q (alpha channels x) and
-// P points p (all channels y),
+// Over a walker-tile triangle (16 Q walkers x PW P walkers, Q walker > P walker), the V phase
+// computes, for Q points q (alpha channels x) and P points p (all channels y),
 //   V(q x, p y) = sum_a Phi_v(q, x, a) conj Phi_v(p, y, a)          (greens.cpp:73-79)
 // with Phi_v already carrying sqrt(exp(-eps_a tau)) and the walker weights (mo_kernel). As real
 // GEMMs over K' = [re | im] (K' = 2 KH, KH = n_vir rounded up to 16):
 //   Re V = [re_q | im_q] . [re_p | im_p],   Im V = [im_q | -re_q] . [re_p | im_p],
 // so the A operand (Q side) has 128 rows per tile: (q walker 16, e_q 2, x_alpha 2, re/im 2),
-// and B (P side) 64 rows: (p walker 8, e_p 2, y 4).
+// and B (P side) 8 PW rows: (p walker PW, e_p 2, y 4); PW = 10 (N = 80) for the literal
+// estimator, PW = 8 (N = 64, pair_kr's own 16 x 8 tiles) for the physical one.
 //
 // Ozaki splitting: every row (point, channel) is scaled by its power-of-two maximum 2^e and cut
 // into six signed 7-bit slices (rounded digits), x 2^-e = sum_s d_s 2^(-7 (s + 1)), |d_s| <= 127. The 21 slice
@@ -20,17 +20,21 @@
 // products s + t > 5) is ~2^-42 of |row_q| |row_p| K' -- the precision budget pinned on the
 // oracle by tests/test_ozaki_budget.py.
 //
-// Kernels per step (after mo_kernel, before pair_kr_kernel<OZ>):
+// Kernels per step (after mo_kernel):
 //  * oz_slice_kernel: one warp per (point, channel): the row exponent, the six slices of the
 //    [re | im] rows, written directly in the UMMA canonical K-major layout of their tile blocks;
-//  * oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each
-//    k-step's 6 A + 6 B slices (36 KB) into a 5-stage mbarrier ring with cp.async.bulk, one
-//    thread issues the 21 tcgen05.mma per k-step, four epilogue warps drain TMEM (tcgen05.ld)
-//    diagonal by diagonal into eight rotating accumulator slots (a tile's MMAs start while the
-//    previous tile drains), merge, and write the tile's V in the order pair_kr's epilogue
-//    lanes read it: V[t][q 16][p 8][re/im][e_q x_alpha e_p y>>1 (16)][y&1].
-// Measured prototype (tools/oz_gemm.cu, cfg4 triangle): 1.6 ms incl. the 1.08 GB V write,
-// vs ~3.6 ms for the DMMA V phase of pair_kr.
+//  * literal estimator: pair_kr_kernel<false, 2> writes the o blocks of its 16 x 8 tiles, then
+//    oz_vgemm_kernel<true> computes each 16 x 10 tile's V blocks and contracts them with the o
+//    blocks in its epilogue (the reference's literal pair term), with the step's fixed-order sums;
+//  * physical estimator: oz_vgemm_kernel<false> writes V tiles
+//    V[t][q 16][p 8][re/im][e_q x_alpha e_p y>>1 (16)][y&1] in the order pair_kr's trace
+//    epilogue lanes read them, then pair_kr_kernel<true, 1>.
+// oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each
+// k-step's 6 A + 6 B slices into a 5-stage mbarrier ring with cp.async.bulk, one thread issues
+// the 21 tcgen05.mma per k-step, eight epilogue warps (two per TMEM lane quarter) drain TMEM
+// (tcgen05.ld), merge, release the accumulators and finish the tile while the next one runs.
+// Measured (cfg4, profiles/r05): 1.34 ms at 2447 int8 TOPS, 0.78 of the M128 N80 shape's
+// ceiling, vs ~3.6 ms for the DMMA V phase of pair_kr.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
