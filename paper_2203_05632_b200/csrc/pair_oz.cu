@@ -49,7 +49,10 @@ using namespace pairk;
 constexpr int S = OZ_SLICES;
 constexpr int MA = 128;             // A rows (Q side) of a tile: 16 walkers
 constexpr int A_KS = S * MA * 32;   // bytes of one k-step (32 of K') of a Q block, all slices
-constexpr int STAGES = 5;
+#ifndef OZ_STAGES
+#define OZ_STAGES 5
+#endif
+constexpr int STAGES = OZ_STAGES;
 #ifndef OZ_EPW
 #define OZ_EPW 8
 #endif
@@ -74,7 +77,7 @@ struct OzShape {
   static constexpr uint32_t IDESC =
       (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
 };
-static_assert(5 * OzShape<true>::STAGE <= 227 * 1024, "stage ring");
+static_assert(STAGES * OzShape<true>::STAGE <= 227 * 1024, "stage ring");
 
 // canonical K-major, no-swizzle UMMA operand layout of one k-step: [row / 8][k / 16][row % 8][16 B]
 __host__ __device__ __forceinline__ int op_off(int r, int kk) {
@@ -265,7 +268,9 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // 1.733 vs 1.571 ms on the same box; the next tile's k-step 0 waits on the drain diagonal by
   // diagonal anyway, and TMEM reads under running MMAs are slower. Also rejected: A from TMEM
   // (tcgen05.cp 128x256b per slice and k-step, MMA with [a_tmem]): exact, but 1.89 vs 1.59 ms
-  // (tools/oz_gemm.cu -DA_TMEM).
+  // (tools/oz_gemm.cu -DA_TMEM). At N = 80 (same-box A/B, V-GEMM ms): 3 / 4 / 5 ring stages
+  // 1.333 / 1.335 / 1.335; 4 epilogue warps 1.482 vs 8 warps 1.335 (the drain is the epilogue
+  // warps' instruction latency while the MMA waits for TMEM).
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_base;
   __shared__ double s_red[EPW][2];
