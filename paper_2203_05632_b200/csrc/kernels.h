@@ -129,6 +129,10 @@ void launch_pair_kr(const PairParams& P, cudaStream_t s);
 cudaError_t pair_kr_kernel_setup();
 // QB = 1 build of pair_kr.cu (8 x 8 tiles, two CTAs per SM) for ensembles of fewer than 64 walkers
 void launch_pair_kr_qb1(const PairParams& P, cudaStream_t s);
+// PW = 4 build of pair_kr.cu (8 consumer warps) for the O-only pass of the INT8 V path
+void launch_pair_kr_pw4(const PairParams& P, cudaStream_t s);
+cudaError_t pair_kr_kernel_setup_pw4();
+void pair_kr_ring_pw4(int max_width, int& ring, int& ring_doubles);
 cudaError_t pair_kr_kernel_setup_qb1();
 double pair_kr_block_tiles_qb1(int nb);
 int pair_kr_tiles_qb1(int nb);

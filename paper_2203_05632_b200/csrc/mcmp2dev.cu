@@ -72,6 +72,11 @@ T* dupload(const T* src, size_t n, std::vector<void*>& owned) {
 
 }  // namespace
 
+#ifndef OZ_O_PW4
+#define OZ_O_PW4 1  // O-only pass of the INT8 path on the PW = 4 build of pair_kr (8 consumer warps):
+                    // 0.443 -> 0.392 ms at cfg4 (same-box A/B), more independent DMMA chains per warp
+#endif
+
 struct mcmp2dev_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -296,7 +301,13 @@ struct mcmp2dev_handle {
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
         p.otiles = oz_otiles;
-        launch_pair_kr(p, stream);
+        if (OZ_O_PW4) {
+          const int wmax = std::min(KC4, std::max(Go, 1));
+          pair_kr_ring_pw4(wmax, p.ring, p.ring_doubles);
+          launch_pair_kr_pw4(p, stream);
+        } else {
+          launch_pair_kr(p, stream);
+        }
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
         launch_oz_vgemm(o, stream);
       } else {
@@ -513,6 +524,7 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   ck(pair_kr_kernel_setup(), "pair_kr kernel attributes");
   ck(pair_kr_kernel_setup_qb1(), "pair_kr (QB 1) kernel attributes");
   ck(oz_kernel_setup(), "pair_oz kernel attributes");
+  ck(pair_kr_kernel_setup_pw4(), "pair_kr (PW 4) kernel attributes");
   for (auto& e : h->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
   for (auto& e : h->ev_oz) ck(cudaEventCreate(&e), "cudaEventCreate");
 

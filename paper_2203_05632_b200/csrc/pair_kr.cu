@@ -45,6 +45,11 @@ using namespace pairk;
 #ifdef KR_QB1_VARIANT
 #define KR_QB 1
 #define KR_API(name) name##_qb1
+#elif defined(KR_PW4_VARIANT)
+// third build (csrc/Makefile): 8 phase-1 warps of 4 x 8 walkers (NB1 = 2 fragments, more
+// independent DMMA chains per warp) for the O-only pass of the INT8 path
+#define KR_PW 4
+#define KR_API(name) name##_pw4
 #else
 #define KR_API(name) name
 #endif
