@@ -212,6 +212,9 @@ struct mcmp2dev_handle {
   // buffers of the INT8 V path for mm walkers (no-op when inactive or already large enough)
   void ensure_oz(int mm) {
     if (!oz_active(mm, 1) || mm <= oz_m) return;
+    ck(cudaStreamSynchronize(stream), "oz sync");
+    for (auto& g : graphs)  // captured steps hold the old buffers' addresses
+      if (g) cudaGraphExecDestroy(g), g = nullptr;
     oz_free();
     const int nbq = (mm + 15) / 16, npts_oz = 32 * nbq;
     int kh = 0, ks = 0;

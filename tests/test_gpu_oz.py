@@ -100,3 +100,24 @@ def test_int8_v_heavy_atoms_match_oracle(cfgdir, tmp_path, name, m):
     got = dw.replay(w[None], np.array([tau]))[0]
     for k in (0, 2, 4):
         assert abs(got[k] - ref[k]) <= REL * abs(ref[k]), k
+
+
+def test_int8_v_buffers_grow_after_capture(cfgdir):
+    """A replay with more walkers grows the INT8 path's buffers after advance() captured its CUDA
+    graphs; the graphs must be re-captured (not replayed against freed buffers): the chain after
+    the growth still equals the one of a fresh handle."""
+    sp = cfgdir / "cfg3.spinor"
+    text = (cfgdir / "cfg3.conf").read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=21, stream=0, m=256, burn=20, nsteps=1)
+    a = DeviceWalker(System(sp, text), max_walkers=256)
+    b = DeviceWalker(System(sp, text), max_walkers=256)
+    for dw in (a, b):
+        dw.init_ensemble(192, seed=4)
+        dw.burn_in(10)
+    a.advance(32)                            # graphs captured with buffers for 192 walkers
+    a.replay(tr["walkers"], tr["tau"])       # grows them to 256
+    b.advance(32)
+    va, _ = a.advance(34)
+    vb, _ = b.advance(34)
+    assert np.array_equal(va, vb)
