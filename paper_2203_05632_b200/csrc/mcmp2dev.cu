@@ -209,12 +209,16 @@ struct mcmp2dev_handle {
     oz_otiles = nullptr;
     oz_m = 0;
   }
+  // captured steps hold the addresses of every work buffer: any reallocation drops them first
+  void drop_graphs() {
+    ck(cudaStreamSynchronize(stream), "graph drop sync");
+    for (auto& g : graphs)
+      if (g) cudaGraphExecDestroy(g), g = nullptr;
+  }
   // buffers of the INT8 V path for mm walkers (no-op when inactive or already large enough)
   void ensure_oz(int mm) {
     if (!oz_active(mm, 1) || mm <= oz_m) return;
-    ck(cudaStreamSynchronize(stream), "oz sync");
-    for (auto& g : graphs)  // captured steps hold the old buffers' addresses
-      if (g) cudaGraphExecDestroy(g), g = nullptr;
+    drop_graphs();
     oz_free();
     const int nbq = (mm + 15) / 16, npts_oz = 32 * nbq;
     int kh = 0, ks = 0;
@@ -1009,14 +1013,15 @@ int mcmp2dev_init_batch(mcmp2dev_t* h, int nens, int m, uint64_t seed, uint32_t 
                                                    size_t(pair_kr_tiles_qb1(nb)) * pair_kr_consumers_qb1() * 2,
                                                    size_t(nb) * (nb + 1) / 2 * pair_consumers() * 4});
       if (part > h->bpart_cap) {
+        h->drop_graphs();
         if (h->d_bpart) cudaFree(h->d_bpart);
-  h->oz_free();
         h->d_bpart = nullptr;
         ck(cudaMalloc(&h->d_bpart, part * sizeof(double)), "cudaMalloc");
         h->bpart_cap = part;
       }
       const size_t steps = size_t(kGraphSteps) * nens * 6;
       if (steps > h->bsteps_cap) {
+        h->drop_graphs();
         if (h->d_bsteps) cudaFree(h->d_bsteps);
         if (h->h_bsteps) cudaFreeHost(h->h_bsteps);
         h->d_bsteps = nullptr;

@@ -95,7 +95,20 @@ def parse_run_config(text: str) -> dict:
         cfg[k] = v
     return {"steps": int(cfg["steps"]) if "steps" in cfg else None,
             "target": float(cfg["target-rel-err"]) if "target-rel-err" in cfg else None,
-            "interval": int(cfg["checkpoint-interval"]), "workers": int(cfg.get("workers", "1"))}
+            "interval": int(cfg["checkpoint-interval"]), "workers": int(cfg.get("workers", "1")),
+            "checkpoint": cfg.get("checkpoint"), "trace": cfg.get("trace")}
+
+
+def require_no_files(rc: dict) -> None:
+    """The multi-process driver merges estimates only; the checkpoint (driver.cpp:218-305) and
+    trace files of the reference Engine hold every worker's record in one file written by one
+    process, which this driver does not assemble. A run that asks for them is refused rather
+    than silently run without them: use the single-process Engine (`mcmp2 run`, one device
+    handle per worker) for checkpointed or traced runs."""
+    for key in ("checkpoint", "trace"):
+        if rc.get(key):
+            raise ValueError(f"distributed driver: '{key}' is not supported across ranks "
+                             "(run the config with the single-process Engine, `mcmp2 run`)")
 
 
 class HostGroup:
@@ -145,9 +158,13 @@ class _OneWorker:
 
 
 def rank_workers(total: int, world: int, rank: int) -> tuple[int, int]:
-    """Workers of this rank: a contiguous range of the run's `workers` (at least one per rank),
-    split as worker_share splits steps (driver.cpp:307-309)."""
-    total = max(total, world)
+    """Workers of this rank: a contiguous range of the run's `workers`, split as worker_share
+    splits steps (driver.cpp:307-309). Every rank needs at least one worker: fewer workers than
+    ranks would change the Philox streams and step shares of the run (its config hash names the
+    worker count), so that is an error, not a silent increase."""
+    if total < world:
+        raise ValueError(f"distributed driver: workers {total} < world size {world} "
+                         "(set `workers` to at least the number of ranks)")
     first = sum(worker_share(total, world, r) for r in range(rank))
     return first, worker_share(total, world, rank)
 
@@ -231,9 +248,10 @@ def main(argv=None):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rc = parse_run_config(text)
+    require_no_files(rc)
     first, count = rank_workers(rc["workers"], world, rank)
     group = HostGroup(text, first, count, local)
-    rep = drive_group(group, max(rc["workers"], world), rc["steps"], rc["target"], rc["interval"],
+    rep = drive_group(group, rc["workers"], rc["steps"], rc["target"], rc["interval"],
                       torch_all_gather(dist))
     if rank == 0:
         sys.stdout.write(format_report(rep))

@@ -225,3 +225,21 @@ def test_device_groups_over_two_ranks_match_the_engine(cfgdir):
         p.join(timeout=60)
     assert out[0][1] == out[1][1]
     assert out[0][1] == walker.run_config_text(text)
+
+
+def test_fewer_workers_than_ranks_is_an_error():
+    """rank_workers refuses to raise the worker count (it would change the run's streams and
+    shares, which the config hash names); an exact split is accepted."""
+    with pytest.raises(ValueError, match="workers 1 < world size 2"):
+        D.rank_workers(1, 2, 0)
+    assert [D.rank_workers(2, 2, r) for r in range(2)] == [(0, 1), (1, 1)]
+
+
+def test_checkpoint_and_trace_are_refused_across_ranks(cfgdir):
+    """The torchrun driver does not assemble the Engine's checkpoint/trace files, so a config
+    naming them is refused with a clear error instead of silently running without them."""
+    base = f"spinors {cfgdir / 'cfg1.spinor'}\nsteps 100\nworkers 2\n"
+    D.require_no_files(D.parse_run_config(base))
+    for extra in ("checkpoint /tmp/ck\n", "trace /tmp/tr\n"):
+        with pytest.raises(ValueError, match="not supported across ranks"):
+            D.require_no_files(D.parse_run_config(base + extra))

@@ -134,3 +134,31 @@ def test_bulk_state_round_trip(cfgdir):
     dw.set_ensembles(bulk)
     v2, _ = dw.advance(5)
     assert np.array_equal(v1, v2)
+
+
+def test_reinit_with_other_batch_sizes_drops_stale_graphs(cfgdir):
+    """A handle re-initialised with more ensembles reallocates its batched buffers; the graphs
+    captured before hold the old addresses and must be dropped (mcmp2dev.cu drop_graphs). Going
+    4 -> 8 -> 4 ensembles with the same seed must give the chain a fresh 4-ensemble handle gives."""
+    sp = cfgdir / "cfg1.spinor"
+    text = (cfgdir / "cfg1.conf").read_text()
+    sysd = System(sp, text)
+    m, nsteps = 16, 64  # two captured graphs of 32 steps per advance
+
+    def run(dw, nens):
+        dw.init_batch(nens, m, seed=11, stream0=0)
+        dw.set_sigma_step(0.3)
+        dw.burn_in(20, adapt=False)
+        dw.prepare()
+        return dw.advance(nsteps)[0]
+
+    fresh = DeviceWalker(sysd, max_walkers=8 * m)
+    ref4 = run(fresh, 4)
+    fresh.close()
+    dw = DeviceWalker(sysd, max_walkers=8 * m)
+    first = run(dw, 4)
+    eight = run(dw, 8)
+    again = run(dw, 4)
+    dw.close()
+    assert np.array_equal(first, ref4) and np.array_equal(again, ref4)
+    assert rel_err(eight[:, :4], ref4) < 1e-12  # streams 0..3 are the same chains
