@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define MCMP2DEV_ABI_VERSION 1
+#define MCMP2DEV_ABI_VERSION 2
 
 /* status codes (SURVEY.md section 8(b) "Errors") */
 enum {
@@ -81,6 +81,21 @@ typedef struct mcmp2dev_step {
   double direct_re, direct_im, exchange_re, exchange_im;
 } mcmp2dev_step;
 
+/* Per-step record with the INT8 V path's accuracy guard (mcmp2dev_advance_ex / _replay_ex).
+ * est_err_*: the guard's estimate of the INT8 error of the direct / exchange pair sums (a
+ * model of the slice remainders and dropped slice products propagated through the literal
+ * contraction, csrc/pair_oz.cu); abs_*: sums of |pair term| (the condition-aware error of
+ * SURVEY 7 is |error| / (abs / C(m,2))); int8_v: 1 when the V blocks of this step ran on the
+ * INT8 path; fallback: 1 when the guard rejected the INT8 result and the step was recomputed
+ * on the FP64 DMMA pair kernel (value and sums are then the DMMA ones). All four guard
+ * fields are 0 on the DMMA path. */
+typedef struct mcmp2dev_step_ex {
+  double value, imag;
+  double direct_re, direct_im, exchange_re, exchange_im;
+  double est_err_direct, est_err_exchange, abs_direct, abs_exchange;
+  int int8_v, fallback;
+} mcmp2dev_step_ex;
+
 /* ---- lifetime ---------------------------------------------------------------------- */
 /* Deep-copies `sys` to `device`, sized for up to max_walkers electron pairs.
  * Replaces Engine construction of the per-worker state (driver.cpp:338-374). */
@@ -136,6 +151,10 @@ int mcmp2dev_prepare(mcmp2dev_t* h);
  * ensemble is not modified. m = 2 is sample_term (estimator.cpp:65-75). */
 int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
                     mcmp2dev_step* out);
+/* advance / replay with the full per-step record (guard fields); single ensembles */
+int mcmp2dev_advance_ex(mcmp2dev_t* h, long nsteps, mcmp2dev_step_ex* out);
+int mcmp2dev_replay_ex(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
+                       mcmp2dev_step_ex* out);
 
 /* ---- instrumentation (not on the reference surface) -------------------------------- */
 /* Accumulated device time (ms) and launch counts of the kernel classes since the last
@@ -167,10 +186,22 @@ int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
  * int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers
  * path with n_vir <= 512 and the 16 x 8 pair tiles (m >= 64 walkers, enough tiles for the
  * SMs); elsewhere the DMMA V phase runs. mode -1 queries, 0 selects DMMA, 1 selects INT8
- * (the default); returns 1 when the INT8 V path is selected and the system is eligible.
- * Agreement with the FP64 path: step values within ~3e-11 relative at cfg4
- * (tests/test_ozaki_budget.py, tests/test_gpu_oz.py). */
+ * (the default of the literal estimator; the physical estimator defaults to DMMA and runs
+ * INT8 unguarded when selected); returns 1 when the INT8 V path is selected and the system is
+ * eligible. Agreement with the FP64 path: see mcmp2dev_guard. */
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
+/* Accuracy guard of the INT8 V path (literal estimator). After each INT8 step the V-GEMM's
+ * last CTA compares the estimated error of the direct sum, the exchange sum and the step
+ * value with tol times their magnitude; a step that fails (or is not finite) is recomputed on
+ * the FP64 DMMA pair kernel in the same launch sequence (a guarded launch that exits at once
+ * otherwise), so the reported value is the FP64 one. tol <= 0 turns the guard off; default
+ * 3e-11; NaN only queries. previous (may be NULL) receives the old tolerance. The estimate is a model calibrated
+ * against the oracle (3-250x above the measured error, tests/test_oz_guard_model.py), not a
+ * rigorous bound (that would be ~1e-7 relative and reject every step). */
+int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous);
+/* out4 = {INT8-path steps checked, steps recomputed on DMMA, largest estimated relative
+ * error of a kept step, tolerance} since the last call; resets the counters. */
+int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out4);
 
 #ifdef __cplusplus
 }

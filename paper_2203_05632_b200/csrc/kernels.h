@@ -74,12 +74,15 @@ struct PairParams {
   double ng2, w_direct, w_exchange;
   int physical;              // 1: Tr(o1 va) Tr(o2 vb), Tr(o1 vd o2 vc) epilogue (opt-in)
   double* partials;          // [ntiles][4]; batched: [nens * ens_tiles][consumer warps][2]
-  double* step_out;          // [6] of this step; batched: [nens][6]
+  double* step_out;          // [6] of this step (single ensembles: a kStepDoubles record); batched: [nens][6]
   int nens, ens_tiles;       // batched ensembles: m walkers each, st_ro[nens]
   const double* vtiles;      // pair_kr only, single ensemble: V blocks of every tile from
                              // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
   double* otiles;            // pair_kr only, single ensemble, literal: write the o blocks of every
                              // tile for oz_vgemm_kernel<true> and skip the V phase and the sums
+  int guard_fallback;        // pair_kr only: the INT8 path's guard launch -- exit at once unless
+                             // st->oz_trip, else recompute the step on DMMA (writes step_out[0..5],
+                             // clears oz_trip)
 };
 
 // INT8 (Ozaki) V blocks of the Kramers pair stage (pair_oz.cu)
@@ -104,8 +107,13 @@ struct OzParams {
   double ng2, w_direct, w_exchange;
   const DevState* st_ro;
   DevState* st;
-  double* partials;          // [grid][4]
-  double* step_out;          // [6]
+  double* partials;          // [grid][8]: direct, 0, exchange, 0, sum eps_d^2, sum eps_x^2, sum |t_d|, sum |t_x|
+  double* step_out;          // [kStepDoubles] (common.cuh)
+  // accuracy guard (literal estimator): per-point stats from oz_slice_kernel, the step's
+  // estimated INT8 error against guard_tol (<= 0: no guard)
+  int n_occ;
+  double* pstat;             // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, N = |Phi_o(pt)|_F, 0
+  double guard_tol;
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);

@@ -31,6 +31,10 @@ namespace {
 constexpr int kChunk = 1024;  // steps per device->host copy of StepEstimates
 constexpr int kGraphSteps = 32;  // production steps per captured CUDA graph (even)
 constexpr int kBatchMaxWalkers = 480;  // per batched ensemble (2m + 32 threads <= 1024, m % 16 == 0)
+// default guard tolerance of the INT8 V path: the estimated error (a model 3-250x above the
+// measured error on the oracle's steps) must stay below 3e-11 of |direct|, |exchange| and
+// |value|, so kept steps sit ~30x inside the 1e-10 replay gate
+constexpr double kGuardTol = 3e-11;
 thread_local std::string g_create_error;
 
 struct CudaError : std::runtime_error {
@@ -95,6 +99,13 @@ struct mcmp2dev_handle {
   int oz_m = 0;
   OzParams ozp{};
   double* oz_otiles = nullptr;
+  // accuracy guard of the INT8 path (literal estimator): a step whose estimated INT8 error of
+  // the direct sum, the exchange sum or the step value exceeds guard_tol of that quantity is
+  // recomputed on the DMMA pair kernel (pair_oz.cu, pair_kr.cu guard_fallback); <= 0: off
+  double guard_tol = kGuardTol;
+  double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
+  long long guard_steps = 0, guard_trips = 0;
+  double guard_max_est = 0.0;  // largest estimated relative error of a step kept on INT8
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
   DevSites sites{};
   double* d_energies = nullptr;
@@ -135,15 +146,16 @@ struct mcmp2dev_handle {
   // captured production steps, one per walker-buffer parity; valid for one (m, RNG key/stream,
   // kernel path)
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
-  double* d_gsteps = nullptr;  // [kGraphSteps][6] step results written by the graph
+  double* d_gsteps = nullptr;  // [kGraphSteps][kStepDoubles] step results written by the graph
   struct GraphKey {
     int m = -1, kramers = -1, nens = 1, oz = -1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
+    double guard_tol = -1.0;
     bool operator==(const GraphKey&) const = default;
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, k0, k1, rstream};
+    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, k0, k1, rstream, guard_tol};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -154,7 +166,7 @@ struct mcmp2dev_handle {
       launch_walk(walk_params(WALK_PRODUCTION, 0, 0), stream);
       cur ^= 1;
       if (nens > 1) launch_estimate(buf[cur], m, d_bsteps + size_t(6) * nens * s, nens);
-      else launch_estimate(buf[cur], m, d_gsteps + 6 * s);
+      else launch_estimate(buf[cur], m, d_gsteps + kStepDoubles * s);
     }
     cur = c0;
     ck(cudaStreamEndCapture(stream, &g), "graph capture end");
@@ -202,11 +214,12 @@ struct mcmp2dev_handle {
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
-                    (void*)oz_otiles})
+                    (void*)oz_otiles, (void*)d_pstat})
       if (p) cudaFree(p);
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     oz_otiles = nullptr;
+    d_pstat = nullptr;
     oz_m = 0;
   }
   // captured steps hold the addresses of every work buffer: any reallocation drops them first
@@ -241,6 +254,8 @@ struct mcmp2dev_handle {
       ck(cudaMalloc(&ozp.v, sizeof(double) * 8192 * ntiles), "cudaMalloc oz V blocks");
     else
       ck(cudaMalloc(&oz_otiles, sizeof(double) * 4096 * ntiles), "cudaMalloc oz o blocks");
+    ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
+    ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
     oz_m = 16 * nbq;
   }
 
@@ -281,6 +296,8 @@ struct mcmp2dev_handle {
     p.otiles = nullptr;
     const bool oz_path = oz_active(mm, ne);
     const bool fused = oz_path && !p.physical;
+    const bool guarded = fused && guard_tol > 0.0;
+    const PairParams p_full = p;  // the DMMA pair stage (the guard's fallback launch)
     if (oz_path) {
       if (mm > oz_m) throw RtError("mcmp2dev: INT8 V buffers not prepared for this ensemble size");
       OzParams o = ozp;
@@ -304,6 +321,9 @@ struct mcmp2dev_handle {
       o.st = d_state;
       o.partials = d_partials;
       o.step_out = step_out;
+      o.n_occ = n_occ;
+      o.pstat = guarded ? d_pstat : nullptr;
+      o.guard_tol = guard_tol;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
@@ -317,6 +337,11 @@ struct mcmp2dev_handle {
         }
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
         launch_oz_vgemm(o, stream);
+        if (guarded) {  // exits at once unless the V-GEMM's guard failed this step
+          PairParams f = p_full;
+          f.guard_fallback = 1;
+          launch_pair_kr(f, stream);
+        }
       } else {
         launch_oz_vgemm(o, stream);
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
@@ -544,6 +569,9 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   h->w_direct = s->w_direct;
   h->w_exchange = s->w_exchange;
   h->estimator = s->estimator;
+  // the INT8 V path is the default of the literal estimator, where its accuracy guard runs; the
+  // opt-in physical estimator keeps the FP64 DMMA pair stage unless mcmp2dev_pair_path selects it
+  h->oz = s->estimator == MCMP2DEV_ESTIMATOR_LITERAL;
   if (s->estimator != MCMP2DEV_ESTIMATOR_LITERAL && s->estimator != MCMP2DEV_ESTIMATOR_PHYSICAL)
     throw ArgError("mcmp2dev_create: unknown estimator");
 
@@ -658,11 +686,14 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   // per-CTA partials: the grid of any pair kernel is at most its tile count
   const size_t ntiles = std::max({size_t(h->nbmax) * (h->nbmax + 1) / 2, size_t(pair_kr_tiles(h->nbmax)),
                                   size_t(pair_kr_tiles_qb1(h->nbmax))});
-  h->d_partials = dalloc<double>(ntiles * 4, o);
-  h->d_steps = dalloc<double>(size_t(kChunk) * 6, o);
-  h->d_gsteps = dalloc<double>(size_t(kGraphSteps) * 6, o);
+  // (oz_vgemm_kernel: one CTA per SM, 8 doubles each)
+  h->d_partials = dalloc<double>(std::max(ntiles * 4, size_t(h->sms) * 8), o);
+  h->d_steps = dalloc<double>(size_t(kChunk) * kStepDoubles, o);
+  h->d_gsteps = dalloc<double>(size_t(kGraphSteps) * kStepDoubles, o);
+  ck(cudaMemset(h->d_steps, 0, sizeof(double) * kChunk * kStepDoubles), "memset steps");
+  ck(cudaMemset(h->d_gsteps, 0, sizeof(double) * kGraphSteps * kStepDoubles), "memset steps");
   h->d_replay = dalloc<double>(size_t(h->mmax) * 8, o);
-  ck(cudaMallocHost(&h->h_steps, sizeof(double) * kChunk * 6), "cudaMallocHost");
+  ck(cudaMallocHost(&h->h_steps, sizeof(double) * kChunk * kStepDoubles), "cudaMallocHost");
   ck(cudaMallocHost(&h->h_replay, sizeof(double) * h->mmax * 8), "cudaMallocHost");
   ck(cudaDeviceSynchronize(), "setup sync");
 }
@@ -867,6 +898,82 @@ void advance_batched(mcmp2dev_t* h, long nsteps, int nactive, double* values, do
 }
 }  // namespace
 
+namespace {
+// the guard's bookkeeping over one step record (kStepDoubles) of the INT8 path
+void guard_account(mcmp2dev_t* h, const double* r) {
+  if (r[10] == 0.0) return;
+  ++h->guard_steps;
+  if (r[11] != 0.0) {
+    ++h->guard_trips;
+    return;
+  }
+  const double d = std::fabs(r[2]), x = std::fabs(r[4]), v = std::fabs(r[2] + r[4]);
+  double est = 0.0;
+  if (d > 0) est = std::max(est, r[6] / d);
+  if (x > 0) est = std::max(est, r[7] / x);
+  if (v > 0) est = std::max(est, std::sqrt(r[6] * r[6] + r[7] * r[7]) / v);
+  h->guard_max_est = std::max(h->guard_max_est, est);
+}
+
+void fill_ex(const double* r, mcmp2dev_step_ex* o) {
+  o->value = r[0];
+  o->imag = r[1];
+  o->direct_re = r[2];
+  o->direct_im = r[3];
+  o->exchange_re = r[4];
+  o->exchange_im = r[5];
+  o->est_err_direct = r[6];
+  o->est_err_exchange = r[7];
+  o->abs_direct = r[8];
+  o->abs_exchange = r[9];
+  o->int8_v = r[10] != 0.0 ? 1 : 0;
+  o->fallback = r[11] != 0.0 ? 1 : 0;
+}
+
+// single-ensemble advance: chunks of kChunk steps, whole graphs of kGraphSteps where possible
+void advance_single(mcmp2dev_t* h, long nsteps, double* values, double* imags, mcmp2dev_step_ex* ex) {
+  h->ensure_oz(h->m);
+  const bool oz = h->oz_active(h->m, 1);
+  constexpr int R = kStepDoubles;
+  long done = 0;
+  while (done < nsteps) {
+    const long n = std::min<long>(kChunk, nsteps - done);
+    long s = 0;
+    // whole blocks of kGraphSteps steps replay one captured CUDA graph
+    if (!h->prof && n >= kGraphSteps) {
+      cudaGraphExec_t graph = h->ensure_graph();
+      for (; s + kGraphSteps <= n; s += kGraphSteps) {
+        ck(cudaGraphLaunch(graph, h->stream), "cudaGraphLaunch");
+        ck(cudaMemcpyAsync(h->h_steps + R * s, h->d_gsteps, sizeof(double) * R * kGraphSteps,
+                           cudaMemcpyDeviceToHost, h->stream),
+           "steps D2H");
+      }
+    }
+    const long s0 = s;
+    for (; s < n; ++s) {
+      if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
+      launch_walk(h->walk_params(WALK_PRODUCTION, 0, 0), h->stream);
+      h->cur ^= 1;
+      h->launch_estimate(h->buf[h->cur], h->m, h->d_steps + R * s);
+    }
+    if (n > s0)
+      ck(cudaMemcpyAsync(h->h_steps + R * s0, h->d_steps + R * s0, sizeof(double) * R * (n - s0),
+                         cudaMemcpyDeviceToHost, h->stream),
+         "steps D2H");
+    h->check_state_errors();  // synchronises
+    for (long k = 0; k < n; ++k) {
+      double* r = h->h_steps + R * k;
+      if (!oz) std::fill(r + 6, r + R, 0.0);  // the guard fields exist on the INT8 path only
+      guard_account(h, r);
+      if (values) values[done + k] = r[0];
+      if (imags) imags[done + k] = r[1];
+      if (ex) fill_ex(r, ex + done + k);
+    }
+    done += n;
+  }
+}
+}  // namespace
+
 int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) {
   return guard(h, [&] {
     require_ensemble(h);
@@ -875,73 +982,84 @@ int mcmp2dev_advance(mcmp2dev_t* h, long nsteps, double* values, double* imags) 
       advance_batched(h, nsteps, h->nens, values, imags);
       return;
     }
-    h->ensure_oz(h->m);
-    long done = 0;
-    const bool want = values || imags;
-    while (done < nsteps) {
-      const long n = std::min<long>(kChunk, nsteps - done);
-      long s = 0;
-      // whole blocks of kGraphSteps steps replay one captured CUDA graph (4 launches per step)
-      if (!h->prof && n >= kGraphSteps) {
-        cudaGraphExec_t graph = h->ensure_graph();
-        for (; s + kGraphSteps <= n; s += kGraphSteps) {
-          ck(cudaGraphLaunch(graph, h->stream), "cudaGraphLaunch");
-          if (want)
-            ck(cudaMemcpyAsync(h->h_steps + 6 * s, h->d_gsteps, sizeof(double) * 6 * kGraphSteps,
-                               cudaMemcpyDeviceToHost, h->stream),
-               "steps D2H");
-        }
-      }
-      const long s0 = s;
-      for (; s < n; ++s) {
-        if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
-        launch_walk(h->walk_params(WALK_PRODUCTION, 0, 0), h->stream);
-        h->cur ^= 1;
-        h->launch_estimate(h->buf[h->cur], h->m, h->d_steps + 6 * s);
-      }
-      if (want && n > s0) {
-        ck(cudaMemcpyAsync(h->h_steps + 6 * s0, h->d_steps + 6 * s0, sizeof(double) * 6 * (n - s0),
-                           cudaMemcpyDeviceToHost, h->stream),
-           "steps D2H");
-      }
-      h->check_state_errors();  // synchronises
-      for (long s = 0; s < n; ++s) {
-        if (values) values[done + s] = h->h_steps[6 * s];
-        if (imags) imags[done + s] = h->h_steps[6 * s + 1];
-      }
-      done += n;
-    }
+    advance_single(h, nsteps, values, imags, nullptr);
   });
 }
 
+int mcmp2dev_advance_ex(mcmp2dev_t* h, long nsteps, mcmp2dev_step_ex* out) {
+  return guard(h, [&] {
+    require_ensemble(h);
+    if (nsteps < 0) throw ArgError("advance: negative step count");
+    if (h->nens > 1) throw ArgError("advance_ex: batched handle (use mcmp2dev_advance_batch)");
+    if (!out && nsteps > 0) throw ArgError("advance_ex: null output");
+    advance_single(h, nsteps, nullptr, nullptr, out);
+  });
+}
+
+namespace {
+void replay_steps(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau, mcmp2dev_step* out,
+                  mcmp2dev_step_ex* ex) {
+  if (m < 2) throw ArgError("replay: at least two electron-pair walkers");
+  if (m > h->mmax) throw ArgError("replay: more walkers than the handle was sized for");
+  h->ensure_oz(m);
+  const bool oz = h->oz_active(m, 1);
+  for (long st = 0; st < nsteps; ++st) {
+    if (tau[st] < 0) throw ArgError("sample_term: tau must be non-negative");
+    std::memcpy(h->h_replay, walkers + size_t(st) * m * 8, sizeof(double) * 8 * m);
+    ck(cudaMemcpyAsync(h->d_replay, h->h_replay, sizeof(double) * 8 * m, cudaMemcpyHostToDevice, h->stream),
+       "replay H2D");
+    if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
+    WalkParams P = h->walk_params(WALK_PRODUCTION, 0, 0);
+    P.out = h->rbuf;
+    P.m = m;
+    launch_replay_load(P, h->d_replay, tau[st], h->stream);
+    h->launch_estimate(h->rbuf, m, h->d_steps);
+    ck(cudaMemcpyAsync(h->h_steps, h->d_steps, sizeof(double) * kStepDoubles, cudaMemcpyDeviceToHost, h->stream),
+       "steps D2H");
+    h->check_state_errors();
+    double* r = h->h_steps;
+    if (!oz) std::fill(r + 6, r + kStepDoubles, 0.0);
+    guard_account(h, r);
+    if (out) {
+      out[st].value = r[0];
+      out[st].imag = r[1];
+      out[st].direct_re = r[2];
+      out[st].direct_im = r[3];
+      out[st].exchange_re = r[4];
+      out[st].exchange_im = r[5];
+    }
+    if (ex) fill_ex(r, ex + st);
+  }
+}
+}  // namespace
+
 int mcmp2dev_replay(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
                     mcmp2dev_step* out) {
+  return guard(h, [&] { replay_steps(h, m, nsteps, walkers, tau, out, nullptr); });
+}
+
+int mcmp2dev_replay_ex(mcmp2dev_t* h, int m, long nsteps, const double* walkers, const double* tau,
+                       mcmp2dev_step_ex* out) {
+  return guard(h, [&] { replay_steps(h, m, nsteps, walkers, tau, nullptr, out); });
+}
+
+int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous) {
   return guard(h, [&] {
-    if (m < 2) throw ArgError("replay: at least two electron-pair walkers");
-    if (m > h->mmax) throw ArgError("replay: more walkers than the handle was sized for");
-    h->ensure_oz(m);
-    for (long st = 0; st < nsteps; ++st) {
-      if (tau[st] < 0) throw ArgError("sample_term: tau must be non-negative");
-      std::memcpy(h->h_replay, walkers + size_t(st) * m * 8, sizeof(double) * 8 * m);
-      ck(cudaMemcpyAsync(h->d_replay, h->h_replay, sizeof(double) * 8 * m, cudaMemcpyHostToDevice,
-                         h->stream),
-         "replay H2D");
-      if (h->prof) ck(cudaEventRecord(h->ev[0], h->stream), "event");
-      WalkParams P = h->walk_params(WALK_PRODUCTION, 0, 0);
-      P.out = h->rbuf;
-      P.m = m;
-      launch_replay_load(P, h->d_replay, tau[st], h->stream);
-      h->launch_estimate(h->rbuf, m, h->d_steps);
-      ck(cudaMemcpyAsync(h->h_steps, h->d_steps, sizeof(double) * 6, cudaMemcpyDeviceToHost, h->stream),
-         "steps D2H");
-      h->check_state_errors();
-      out[st].value = h->h_steps[0];
-      out[st].imag = h->h_steps[1];
-      out[st].direct_re = h->h_steps[2];
-      out[st].direct_im = h->h_steps[3];
-      out[st].exchange_re = h->h_steps[4];
-      out[st].exchange_im = h->h_steps[5];
-    }
+    if (previous) *previous = h->guard_tol;
+    if (!(tol == tol)) return;  // NaN: query only
+    h->guard_tol = tol > 0.0 ? tol : 0.0;  // a different value re-captures the graphs (GraphKey)
+  });
+}
+
+int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out4) {
+  return guard(h, [&] {
+    if (!out4) throw ArgError("guard_stats: null output");
+    out4[0] = double(h->guard_steps);
+    out4[1] = double(h->guard_trips);
+    out4[2] = h->guard_max_est;
+    out4[3] = h->guard_tol;
+    h->guard_steps = h->guard_trips = 0;
+    h->guard_max_est = 0.0;
   });
 }
 

@@ -156,6 +156,8 @@ template <bool PHYS, int OZ>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
   pdl_wait();     // Phi of this step is visible
   pdl_trigger();  // persistent: the next step's walk may launch next to it
+  // the INT8 path's guard launch: nothing to do unless oz_vgemm_kernel failed this step's check
+  if (P.guard_fallback && *reinterpret_cast<volatile const int*>(&P.st->oz_trip) == 0) return;
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);
@@ -582,6 +584,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
     P.step_out[4] = x;
     P.step_out[5] = 0.0;
     P.st->done_pair = 0;
+    if (P.guard_fallback) P.st->oz_trip = 0;
   }
 }
 

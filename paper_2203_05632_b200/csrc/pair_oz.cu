@@ -157,15 +157,20 @@ __device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of
 }
 
 // HELD: n_vir <= 384 (at most 3 quads per lane): one load pass, the values held in registers
-// across the row-maximum reduction (3x the loads in flight); otherwise two passes (max, digits)
+// across the row-maximum reduction (3x the loads in flight); otherwise two passes (max, digits).
+// With P.pstat (the accuracy guard of the literal path) each warp also reduces its scaled row's
+// sum of squares and count of digits-relevant entries (|x| 2^-e > 2^-8) and its channel's share
+// of |Phi_o(pt)|^2; the first warp of each point combines the four channels into the point's
+// stats S, A, N (oz_vgemm_kernel's error model, see there).
 template <bool HELD>
 __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
-  // one warp per (point, channel): 8 warps = 2 points per CTA
+  __shared__ double s_st[8][3];
+  // one warp per (point, channel): 8 warps = 2 points per CTA (npts_oz is a multiple of 32, so
+  // every CTA's points exist)
   const int wg = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
   const int pt = wg >> 2, x = wg & 3;
-  if (pt >= P.npts_oz) return;
   const PhiChunks ch{P.Go, P.Gv};
   const int KH = P.kh, ks_n = P.ks, nq = KH / 4;
   const bool live = pt < P.npts;
@@ -175,6 +180,8 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   const int pb = pt / bpts, prow = ((pt % bpts) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
   int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KS;
   int8_t* const sb = P.sb + size_t(pb) * ks_n * S * NB * 32;
+  const bool stats = P.pstat != nullptr;
+  double ss = 0.0, nbig = 0.0, n2 = 0.0, row_scale = 1.0;
   {
     // this lane's spinor quads a0 = 4 (lane + 32 j); two passes over them (the row maximum, then
     // the digits), the second from L1, so no values are held across the reduction
@@ -213,6 +220,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int e = (mx > 0.0 && mx <= 1.7e308) ? ilogb(mx) + 1 : 0;  // |value| 2^-e < 1
     const double sc = ldexp(1.0, -e);
+    row_scale = ldexp(1.0, e);
     const bool alpha = (x & 1) == 0;
     const int ra = qrow + (x >> 1) * 2;  // A rows ra (re variant), ra + 1 (im variant)
     const int rb = prow + x;
@@ -223,6 +231,13 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
     auto emit = [&](int qd, double (&xr)[4], double (&xi)[4]) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) xr[i] *= sc, xi[i] *= sc;
+      if (stats) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ss += xr[i] * xr[i] + xi[i] * xi[i];
+          nbig += (fabs(xr[i]) > 0x1p-8 ? 1.0 : 0.0) + (fabs(xi[i]) > 0x1p-8 ? 1.0 : 0.0);
+        }
+      }
       uint32_t dr[S], di[S];
       digits4(xr, dr);
       digits4(xi, di);
@@ -254,6 +269,41 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
       }
     }
   }
+  if (!stats) return;  // uniform over the grid
+  // this channel's share of |Phi_o(pt)|_F^2 (occupied groups; spinors past n_occ skipped)
+  if (live)
+    for (int g = lane; g < P.Go; g += 32) {
+      const double* src = P.phi + ch.offset(g, pt, P.npts_pad);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * g + i < P.n_occ) {
+          const double re = src[(x * 4 + i) ^ swz], im = src[16 + ((x * 4 + i) ^ swz)];
+          n2 += re * re + im * im;
+        }
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    nbig += __shfl_xor_sync(0xffffffffu, nbig, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  }
+  const int w = int(threadIdx.x) >> 5;
+  if (lane == 0) {
+    s_st[w][0] = row_scale;
+    s_st[w][1] = row_scale * sqrt(ss * (1.0 / 3.0) + 0.6 * nbig);
+    s_st[w][2] = n2;
+  }
+  __syncthreads();
+  if (lane == 0 && x == 0) {
+    double Sx = 0.0, Ax = 0.0, N2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      Sx = fmax(Sx, s_st[w + c][0]);
+      Ax = fmax(Ax, s_st[w + c][1]);
+      N2 += s_st[w + c][2];
+    }
+    reinterpret_cast<double4*>(P.pstat)[pt] = make_double4(Sx, Ax, sqrt(N2), 0.0);
+  }
 }
 
 template <bool FUSED>
@@ -273,11 +323,14 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // warps' instruction latency while the MMA waits for TMEM).
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_base;
-  __shared__ double s_red[EPW][2];
+  __shared__ double s_red[EPW][6];
   __shared__ bool s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
   double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums (lanes with row % 8 == 0)
+  // FUSED, guard: sums of the squared per-pair error estimates and of |pair term|
+  double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
+  const bool guard = FUSED && P.pstat != nullptr;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     mbar_init(&tfull, 1);
@@ -423,25 +476,55 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
         // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1)
         const int qg = 16 * a + q, pg0 = PW * b + c_lo / 8;
+        // accuracy guard: the INT8 error of each f is modelled per element as a random sum over
+        // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
+        // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
+        // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
+        // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
+        // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
+        // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
+        // actual error (tests/test_oz_guard_model.py); it is a model, not a bound.
+        double4 Sc = make_double4(0, 0, 0, 0), Sd = Sc;
+        if (guard && (row & 7) == 0 && qg < P.m) {
+          Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
+          Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
+        }
 #pragma unroll
         for (int p = 0; p < NK / 2; ++p) {
           const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
           const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
           const int pg = pg0 + p;
           if ((row & 7) == 0 && qg < P.m && pg < P.m && qg > pg) {
-            acc_d += (-P.w_direct * g[2 * p]) * f11;       // f1d f2d
-            acc_x += (-P.w_exchange * f10) * g[2 * p + 1];  // f1x f2x
+            const double td = (-P.w_direct * g[2 * p]) * f11;   // f1d f2d
+            const double tx = (-P.w_exchange * f10) * g[2 * p + 1];  // f1x f2x
+            acc_d += td;
+            acc_x += tx;
+            if (guard) {
+              const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
+              const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
+              const double nac = 0x1p-42 * Sa.z * Sc.z, nbd = 0x1p-42 * Sb.z * Sd.z;
+              const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
+              const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
+              const double ed = fabs(P.w_direct) * (s1d * fabs(f11) + fabs(g[2 * p]) * s2d);
+              const double ex = fabs(P.w_exchange) * (s1x * fabs(g[2 * p + 1]) + fabs(f10) * s2x);
+              acc_ed += ed * ed;
+              acc_ex += ex * ex;
+              acc_ad += fabs(td);
+              acc_ax += fabs(tx);
+            }
           }
         }
       }
     }
     if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
+      double r[6] = {acc_d, acc_x, acc_ed, acc_ex, acc_ad, acc_ax};
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        acc_d += __shfl_down_sync(0xffffffffu, acc_d, o);
-        acc_x += __shfl_down_sync(0xffffffffu, acc_x, o);
-      }
-      if (lane == 0) s_red[warp][0] = acc_d, s_red[warp][1] = acc_x;
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) r[k] += __shfl_down_sync(0xffffffffu, r[k], o);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s_red[warp][k] = r[k];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -450,23 +533,30 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   if constexpr (FUSED) {  // per-CTA partials, then the last CTA's fixed-order sum (as pair_kr.cu)
     if (tid == 0) {
       const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
-      double d = 0.0, x = 0.0;
-      for (int w = 0; w < EPW; ++w) d += s_red[w][0], x += s_red[w][1];
-      P.partials[size_t(blockIdx.x) * 4 + 0] = d * cw;
-      P.partials[size_t(blockIdx.x) * 4 + 1] = 0.0;
-      P.partials[size_t(blockIdx.x) * 4 + 2] = x * cw;
-      P.partials[size_t(blockIdx.x) * 4 + 3] = 0.0;
+      double r[6] = {0, 0, 0, 0, 0, 0};
+      for (int w = 0; w < EPW; ++w)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) r[k] += s_red[w][k];
+      double* pp = P.partials + size_t(blockIdx.x) * 8;
+      pp[0] = r[0] * cw;
+      pp[1] = 0.0;
+      pp[2] = r[1] * cw;
+      pp[3] = 0.0;
+      pp[4] = r[2] * cw * cw;
+      pp[5] = r[3] * cw * cw;
+      pp[6] = r[4] * cw;
+      pp[7] = r[5] * cw;
       __threadfence();
       s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!s_last || tid != 0) return;
     __threadfence();
-    double d = 0.0, x = 0.0;
-    for (unsigned c = 0; c < gridDim.x; ++c) {
-      d += P.partials[size_t(c) * 4 + 0];
-      x += P.partials[size_t(c) * 4 + 2];
-    }
+    double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (unsigned c = 0; c < gridDim.x; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] += P.partials[size_t(c) * 8 + k];
+    const double d = r[0], x = r[2];
     const double npairs = 0.5 * P.m * (P.m - 1);
     P.step_out[0] = (d + x) / npairs;
     P.step_out[1] = 0.0;
@@ -474,6 +564,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     P.step_out[3] = 0.0;
     P.step_out[4] = x;
     P.step_out[5] = 0.0;
+    // guard: estimated error of the direct and exchange sums and of the step value against
+    // guard_tol; a failed (or non-finite) step is recomputed by the guarded DMMA launch
+    const double ed = sqrt(r[4]), ex = sqrt(r[5]), tol = P.guard_tol;
+    const bool trip = guard && tol > 0.0 &&
+                      (!(ed <= tol * fabs(d)) || !(ex <= tol * fabs(x)) || !(sqrt(r[4] + r[5]) <= tol * fabs(d + x)));
+    P.step_out[6] = ed;
+    P.step_out[7] = ex;
+    P.step_out[8] = r[6];
+    P.step_out[9] = r[7];
+    P.step_out[10] = 1.0;
+    P.step_out[11] = trip ? 1.0 : 0.0;
+    if (trip) P.st->oz_trip = 1;
     P.st->done_pair = 0;
   }
 }

@@ -46,6 +46,13 @@ class Step(C.Structure):  # mcmp2dev_step
                 ("value", "imag", "direct_re", "direct_im", "exchange_re", "exchange_im")]
 
 
+class StepEx(C.Structure):  # mcmp2dev_step_ex
+    _fields_ = [(n, C.c_double) for n in
+                ("value", "imag", "direct_re", "direct_im", "exchange_re", "exchange_im",
+                 "est_err_direct", "est_err_exchange", "abs_direct", "abs_exchange")] + \
+               [("int8_v", C.c_int), ("fallback", C.c_int)]
+
+
 _dev = None
 _host = None
 
@@ -92,6 +99,10 @@ def dev() -> C.CDLL:
         d.mcmp2dev_get_ensembles.argtypes = [vp, C.POINTER(Ensemble)]
         d.mcmp2dev_set_ensembles.argtypes = [vp, C.POINTER(Ensemble)]
         d.mcmp2dev_advance_batch.argtypes = [vp, C.c_long, ip, dp, dp]
+        d.mcmp2dev_advance_ex.argtypes = [vp, C.c_long, C.POINTER(StepEx)]
+        d.mcmp2dev_replay_ex.argtypes = [vp, ip, C.c_long, dp, dp, C.POINTER(StepEx)]
+        d.mcmp2dev_guard.argtypes = [vp, C.c_double, dp]
+        d.mcmp2dev_guard_stats.argtypes = [vp, dp]
         _dev = d
     return _dev
 

@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 from . import native
-from .native import Ensemble, Step, check_dev, check_host, dptr
+from .native import StepEx, Ensemble, Step, check_dev, check_host, dptr
 
 
 class System:
@@ -193,6 +193,45 @@ class DeviceWalker:
         check_dev(self._d.mcmp2dev_replay(self._h, m, n, dptr(walkers), dptr(tau), out), self._h)
         return np.array([[s.value, s.imag, s.direct_re, s.direct_im, s.exchange_re, s.exchange_im]
                          for s in out])
+
+    STEP_EX_FIELDS = ("value", "imag", "direct_re", "direct_im", "exchange_re", "exchange_im",
+                      "est_err_direct", "est_err_exchange", "abs_direct", "abs_exchange", "int8_v", "fallback")
+
+    @classmethod
+    def _ex_array(cls, out) -> np.ndarray:
+        return np.array([[getattr(s, f) for f in cls.STEP_EX_FIELDS] for s in out], dtype=np.float64)
+
+    def advance_ex(self, nsteps: int) -> np.ndarray:
+        """advance() returning the full per-step record [nsteps, 12] (STEP_EX_FIELDS): the
+        value and pair sums, the INT8 path's guard estimate, |term| sums and flags."""
+        out = (StepEx * max(nsteps, 1))()
+        check_dev(self._d.mcmp2dev_advance_ex(self._h, nsteps, out), self._h)
+        return self._ex_array(out[:nsteps])
+
+    def replay_ex(self, walkers: np.ndarray, tau: np.ndarray) -> np.ndarray:
+        """replay() with the full per-step record [nsteps, 12] (STEP_EX_FIELDS)."""
+        walkers = np.ascontiguousarray(walkers, dtype=np.float64)
+        if walkers.ndim == 2:
+            walkers = walkers[None]
+        tau = np.ascontiguousarray(np.atleast_1d(tau), dtype=np.float64)
+        n, m, _ = walkers.shape
+        out = (StepEx * n)()
+        check_dev(self._d.mcmp2dev_replay_ex(self._h, m, n, dptr(walkers), dptr(tau), out), self._h)
+        return self._ex_array(out)
+
+    def guard(self, tol: float | None = None) -> float:
+        """The INT8 path's accuracy guard tolerance (<= 0: off); sets it when tol is given and
+        returns the previous value."""
+        prev = C.c_double()
+        check_dev(self._d.mcmp2dev_guard(self._h, float("nan") if tol is None else float(tol), C.byref(prev)),
+                  self._h)
+        return prev.value
+
+    def guard_stats(self, reset: bool = True) -> dict:
+        """{checked, fallbacks, max_est_rel, tol} since the last call (the call resets them)."""
+        o = np.zeros(4)
+        check_dev(self._d.mcmp2dev_guard_stats(self._h, dptr(o)), self._h)
+        return {"checked": int(o[0]), "fallbacks": int(o[1]), "max_est_rel": float(o[2]), "tol": float(o[3])}
 
     # -- instrumentation ------------------------------------------------------------
     def profile(self, enable: bool = True, reset: bool = True) -> dict:

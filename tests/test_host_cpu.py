@@ -24,7 +24,7 @@ def test_libraries_export_every_declared_symbol(header, lib):
 
 
 def test_abi_version():
-    assert native.dev().mcmp2dev_abi_version() == 1
+    assert native.dev().mcmp2dev_abi_version() == 2
 
 
 def test_create_without_gpu_fails_loudly(cfgdir):
