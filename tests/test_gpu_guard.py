@@ -155,13 +155,18 @@ def test_long_chain_int8_against_dmma(cfgdir, name, m, nsteps):
     dw.burn_in(200)
     st = dw.get_ensemble()
     runs = {}
-    for label, int8, tol in (("guarded", 1, 3e-11), ("raw", 1, 0.0), ("dmma", 0, 3e-11)):
+    # "raw": the estimate is computed (tol 1e300) but never rejects a step
+    for label, int8, tol in (("guarded", 1, 3e-11), ("raw", 1, 1e300), ("dmma", 0, 3e-11)):
         dw.set_ensemble(st)
         dw.int8_v(int8)
         dw.guard(tol)
         runs[label] = dw.advance_ex(nsteps)
         runs[label + "_stats"] = dw.guard_stats()
     g, r, d = runs["guarded"], runs["raw"], runs["dmma"]
+    root = os.environ.get("GRAFT_REPO_ROOT")
+    if root:
+        (Path(root) / "gpurun_out").mkdir(exist_ok=True)
+        np.savez_compressed(Path(root) / "gpurun_out" / f"guard_chain_{name}.npz", guarded=g, raw=r, dmma=d)
     assert np.all(g[:, F["int8_v"]] == 1) and np.all(d[:, F["int8_v"]] == 0)
     npairs = 0.5 * m * (m - 1)
     out = {"config": name, "m": m, "steps": nsteps, "guard_tol": 3e-11,
