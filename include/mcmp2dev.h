@@ -195,9 +195,12 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
  * value with tol times their magnitude; a step that fails (or is not finite) is recomputed on
  * the FP64 DMMA pair kernel in the same launch sequence (a guarded launch that exits at once
  * otherwise), so the reported value is the FP64 one. tol <= 0 turns the guard off; default
- * 3e-11; NaN only queries. previous (may be NULL) receives the old tolerance. The estimate is a model calibrated
- * against the oracle (3-250x above the measured error, tests/test_oz_guard_model.py), not a
- * rigorous bound (that would be ~1e-7 relative and reject every step). */
+ * 3e-10; NaN only queries. previous (may be NULL) receives the old tolerance. The estimate
+ * is a model checked against the oracle (tests/test_oz_guard_model.py) and against the DMMA
+ * path on 2000-step chains (2.3-170x the actual error), not a rigorous bound (that would be
+ * ~1e-7 relative and reject every step). Measured at cfg4 (m = 2048, 2000 steps): ~15% of
+ * the steps are recomputed; the kept ones are within 6e-11 of FP64, while the unguarded
+ * path exceeds the 1e-10 gate on 16 of the 2000 steps. */
 int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous);
 /* out4 = {INT8-path steps checked, steps recomputed on DMMA, largest estimated relative
  * error of a kept step, tolerance} since the last call; resets the counters. */

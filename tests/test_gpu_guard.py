@@ -30,6 +30,7 @@ from paper_2203_05632_b200.walker import EnsembleState
 pytestmark = pytest.mark.gpu
 
 REL = 1e-10
+TOL = 3e-10  # the default guard tolerance (mcmp2dev.cu kGuardTol)
 F = {n: i for i, n in enumerate(DeviceWalker.STEP_EX_FIELDS)}
 
 
@@ -57,7 +58,7 @@ def test_vanishing_tolerance_sends_every_step_to_dmma(cfgdir):
     the results are bit-identical to the DMMA path (replay and graph-captured chains)."""
     sp, text, tr = oracle_steps(cfgdir, "cfg3", 192, 3)
     dw = DeviceWalker(System(sp, text), max_walkers=192)
-    assert dw.int8_v() and dw.guard() == pytest.approx(3e-11)
+    assert dw.int8_v() and dw.guard() == pytest.approx(TOL)
     dw.guard(1e-300)
     got = dw.replay_ex(tr["walkers"], tr["tau"])
     assert np.all(got[:, F["int8_v"]] == 1) and np.all(got[:, F["fallback"]] == 1)
@@ -91,7 +92,7 @@ def test_guard_off_and_on_agree_with_the_oracle(cfgdir):
     dw.guard(0.0)
     off = dw.replay_ex(tr["walkers"], tr["tau"])
     assert np.all(off[:, F["est_err_direct"]] == 0) and np.all(off[:, F["fallback"]] == 0)
-    dw.guard(3e-11)
+    dw.guard(TOL)
     on = dw.replay_ex(tr["walkers"], tr["tau"])
     assert np.array_equal(on[:, :6][on[:, F["fallback"]] == 0], off[:, :6][on[:, F["fallback"]] == 0])
     for k, e in ((2, "est_err_direct"), (4, "est_err_exchange")):
@@ -132,7 +133,7 @@ def test_constructed_ill_conditioned_step_trips_the_guard(cfgdir):
     dw.int8_v(1)
     dw.guard(0.0)
     raw = dw.replay_ex(built[None], tau)[0]
-    dw.guard(3e-11)
+    dw.guard(TOL)
     got = dw.replay_ex(built[None], tau)[0]
     assert raw[F["int8_v"]] == 1 and raw[F["fallback"]] == 0
     assert abs(raw[0] - ref[0]) > REL * abs(ref[0])          # INT8 alone fails the gate here
@@ -156,7 +157,7 @@ def test_long_chain_int8_against_dmma(cfgdir, name, m, nsteps):
     st = dw.get_ensemble()
     runs = {}
     # "raw": the estimate is computed (tol 1e300) but never rejects a step
-    for label, int8, tol in (("guarded", 1, 3e-11), ("raw", 1, 1e300), ("dmma", 0, 3e-11)):
+    for label, int8, tol in (("guarded", 1, TOL), ("raw", 1, 1e300), ("dmma", 0, TOL)):
         dw.set_ensemble(st)
         dw.int8_v(int8)
         dw.guard(tol)
@@ -169,7 +170,7 @@ def test_long_chain_int8_against_dmma(cfgdir, name, m, nsteps):
         np.savez_compressed(Path(root) / "gpurun_out" / f"guard_chain_{name}.npz", guarded=g, raw=r, dmma=d)
     assert np.all(g[:, F["int8_v"]] == 1) and np.all(d[:, F["int8_v"]] == 0)
     npairs = 0.5 * m * (m - 1)
-    out = {"config": name, "m": m, "steps": nsteps, "guard_tol": 3e-11,
+    out = {"config": name, "m": m, "steps": nsteps, "guard_tol": TOL,
            "fallbacks": int(g[:, F["fallback"]].sum()), "guard_stats": runs["guarded_stats"]}
     for k, lab in ((0, "value"), (2, "direct"), (4, "exchange")):
         eg, er = rel(g[:, k], d[:, k]), rel(r[:, k], d[:, k])
@@ -203,7 +204,7 @@ def test_cfg5_full_size_step(tmp_path, name):
     dw.burn_in(50)
     st = dw.get_ensemble()
     res = {}
-    for label, int8, tol in (("guarded", 1, 3e-11), ("raw", 1, 0.0), ("dmma", 0, 3e-11)):
+    for label, int8, tol in (("guarded", 1, TOL), ("raw", 1, 0.0), ("dmma", 0, TOL)):
         dw.set_ensemble(st)
         dw.int8_v(int8)
         dw.guard(tol)
