@@ -86,9 +86,10 @@ typedef struct mcmp2dev_step {
  * model of the slice remainders and dropped slice products propagated through the literal
  * contraction, csrc/pair_oz.cu); abs_*: sums of |pair term| (the condition-aware error of
  * SURVEY 7 is |error| / (abs / C(m,2))); int8_v: 1 when the V blocks of this step ran on the
- * INT8 path; fallback: 1 when the guard rejected the INT8 result and the step was recomputed
- * on the FP64 DMMA pair kernel (value and sums are then the DMMA ones). All four guard
- * fields are 0 on the DMMA path. */
+ * INT8 path; fallback: 0 the main INT8 pass was kept, 1 the guard rejected it and the
+ * refinement pass (one more slice diagonal) was kept, 2 the step was recomputed on the FP64
+ * DMMA pair kernel (value and sums are then the DMMA ones). The guard fields are 0 on the DMMA
+ * path. */
 typedef struct mcmp2dev_step_ex {
   double value, imag;
   double direct_re, direct_im, exchange_re, exchange_im;
@@ -191,20 +192,22 @@ int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
  * eligible. Agreement with the FP64 path: see mcmp2dev_guard. */
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
 /* Accuracy guard of the INT8 V path (literal estimator). After each INT8 step the V-GEMM's
- * last CTA compares the estimated error of the direct sum, the exchange sum and the step
- * value with tol times their magnitude; a step that fails (or is not finite) is recomputed on
- * the FP64 DMMA pair kernel in the same launch sequence (a guarded launch that exits at once
- * otherwise), so the reported value is the FP64 one. tol <= 0 turns the guard off; default
- * 3e-10; NaN only queries. previous (may be NULL) receives the old tolerance. The estimate
- * is a model checked against the oracle (tests/test_oz_guard_model.py) and against the DMMA
- * path on 2000-step chains (2.3-170x the actual error), not a rigorous bound (that would be
- * ~1e-7 relative and reject every step). Measured at cfg4 (m = 2048, 2000 steps): ~15% of
- * the steps are recomputed; the kept ones are within 6e-11 of FP64, while the unguarded
- * path exceeds the 1e-10 gate on 16 of the 2000 steps. */
+ * last CTA compares the estimated error of the direct sum, the exchange sum and the step value
+ * with tol times their magnitude. A step that fails (or is not finite) gets a refinement pass
+ * on the INT8 tensor cores (the 7th slices and the next slice diagonal, ~1/128 of the error;
+ * the main pass keeps every pair's f values for it), and if the refined step still fails it
+ * is recomputed on the FP64 DMMA pair kernel. Both are launched every step and exit at once
+ * unless needed, so the graphs stay fixed. tol <= 0 turns the guard off; default 3e-10; NaN
+ * only queries. previous (may be NULL) receives the old tolerance. The estimate is a model
+ * checked against the oracle (tests/test_oz_guard_model.py) and against the DMMA path on
+ * 2000-step chains (2.3-170x the actual error), not a rigorous bound (that would be ~1e-7
+ * relative and reject every step). At cfg4 (m = 2048, 2000 steps) ~15% of the steps fail the
+ * main pass, steps kept on it are within 6e-11 of FP64, while the unguarded path exceeds the
+ * 1e-10 gate on 16 of the 2000 steps (tests/test_gpu_guard.py). */
 int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous);
-/* out4 = {INT8-path steps checked, steps recomputed on DMMA, largest estimated relative
- * error of a kept step, tolerance} since the last call; resets the counters. */
-int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out4);
+/* out5 = {INT8-path steps checked, steps refined, steps recomputed on DMMA, largest estimated
+ * relative error of a step kept on INT8, tolerance} since the last call; resets the counters. */
+int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out5);
 
 #ifdef __cplusplus
 }

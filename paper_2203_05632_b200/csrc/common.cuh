@@ -34,7 +34,7 @@ constexpr int WB = 8;           // walkers per pair-kernel tile side
 constexpr int NCH = 4;          // channels per point in the Phi layout (ncomp <= 4, zero padded)
 // per-step record of a single ensemble (include/mcmp2dev.h mcmp2dev_step_ex): value, imag,
 // direct re/im, exchange re/im, then the INT8 path's guard: estimated error of the direct and
-// exchange sums, sums of |pair term|, INT8 flag, fallback flag
+// exchange sums, sums of |pair term|, INT8 flag, fallback level (0 main pass, 1 refined, 2 DMMA)
 constexpr int kStepDoubles = 12;
 
 // Bank swizzle of the Phi layout: element (x, k) of point pt sits at (x*4 + k) ^ phi_swz(pt).
@@ -132,8 +132,9 @@ struct DevState {
   int spec_error_idx;         // overflow index from the speculative tau draw (INT_MAX: none)
   unsigned int mo_next;       // mo_kernel tile counter (dynamic scheduling)
   unsigned int mo_done;       // mo_kernel CTAs finished (the last one resets both)
-  int oz_trip;                // INT8 V path: this step's error estimate failed the guard; the
-                              // guarded DMMA pair launch recomputes the step and clears it
+  int oz_trip;                // INT8 V path: this step's error estimate failed the guard; 1: the
+                              // refinement pass runs (oz_vgemm_kernel<true, true>), 2: the guarded
+                              // DMMA pair launch recomputes the step; each clears it when done
 };
 
 }  // namespace mcmp2dev

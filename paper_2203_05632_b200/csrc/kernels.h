@@ -114,6 +114,8 @@ struct OzParams {
   int n_occ;
   double* pstat;             // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, N = |Phi_o(pt)|_F, 0
   double guard_tol;
+  double* fstore;            // [C(m,2)][4] f(0,0), f(1,1), f(1,0), f(0,1) of each pair q > p (index
+                             // q (q - 1) / 2 + p), written by the main pass for the refinement pass
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);
@@ -123,6 +125,7 @@ int oz_nb_rows(bool fused);
 int oz_ntiles(int nbq, bool fused);
 void launch_oz_slice(const OzParams& P, cudaStream_t s);
 void launch_oz_vgemm(const OzParams& P, cudaStream_t s);
+void launch_oz_refine(const OzParams& P, cudaStream_t s);  // exits at once unless st->oz_trip == 1
 double oz_int8_ops(const OzParams& P);  // executed int8 tensor ops of one V-GEMM launch
 cudaError_t oz_kernel_setup();
 

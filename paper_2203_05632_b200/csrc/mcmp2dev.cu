@@ -105,7 +105,8 @@ struct mcmp2dev_handle {
   // recomputed on the DMMA pair kernel (pair_oz.cu, pair_kr.cu guard_fallback); <= 0: off
   double guard_tol = kGuardTol;
   double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
-  long long guard_steps = 0, guard_trips = 0;
+  double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
+  long long guard_steps = 0, guard_refined = 0, guard_dmma = 0;
   double guard_max_est = 0.0;  // largest estimated relative error of a step kept on INT8
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
   DevSites sites{};
@@ -215,12 +216,13 @@ struct mcmp2dev_handle {
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
-                    (void*)oz_otiles, (void*)d_pstat})
+                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore})
       if (p) cudaFree(p);
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     oz_otiles = nullptr;
     d_pstat = nullptr;
+    d_fstore = nullptr;
     oz_m = 0;
   }
   // captured steps hold the addresses of every work buffer: any reallocation drops them first
@@ -253,8 +255,11 @@ struct mcmp2dev_handle {
     // contraction in the V-GEMM epilogue
     if (estimator == MCMP2DEV_ESTIMATOR_PHYSICAL)
       ck(cudaMalloc(&ozp.v, sizeof(double) * 8192 * ntiles), "cudaMalloc oz V blocks");
-    else
+    else {
       ck(cudaMalloc(&oz_otiles, sizeof(double) * 4096 * ntiles), "cudaMalloc oz o blocks");
+      const size_t mq = size_t(16) * nbq;
+      ck(cudaMalloc(&d_fstore, sizeof(double) * 4 * (mq * (mq - 1) / 2)), "cudaMalloc oz pair f values");
+    }
     ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
     ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
     oz_m = 16 * nbq;
@@ -325,6 +330,7 @@ struct mcmp2dev_handle {
       o.n_occ = n_occ;
       o.pstat = guarded ? d_pstat : nullptr;
       o.guard_tol = guard_tol;
+      o.fstore = guarded ? d_fstore : nullptr;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
@@ -338,7 +344,8 @@ struct mcmp2dev_handle {
         }
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
         launch_oz_vgemm(o, stream);
-        if (guarded) {  // exits at once unless the V-GEMM's guard failed this step
+        if (guarded) {  // each exits at once unless the step failed the check before it
+          launch_oz_refine(o, stream);
           PairParams f = p_full;
           f.guard_fallback = 1;
           launch_pair_kr(f, stream);
@@ -904,10 +911,11 @@ namespace {
 void guard_account(mcmp2dev_t* h, const double* r) {
   if (r[10] == 0.0) return;
   ++h->guard_steps;
-  if (r[11] != 0.0) {
-    ++h->guard_trips;
+  if (r[11] == 2.0) {
+    ++h->guard_dmma;
     return;
   }
+  if (r[11] == 1.0) ++h->guard_refined;
   const double d = std::fabs(r[2]), x = std::fabs(r[4]), v = std::fabs(r[2] + r[4]);
   double est = 0.0;
   if (d > 0) est = std::max(est, r[6] / d);
@@ -928,7 +936,7 @@ void fill_ex(const double* r, mcmp2dev_step_ex* o) {
   o->abs_direct = r[8];
   o->abs_exchange = r[9];
   o->int8_v = r[10] != 0.0 ? 1 : 0;
-  o->fallback = r[11] != 0.0 ? 1 : 0;
+  o->fallback = int(r[11]);
 }
 
 // single-ensemble advance: chunks of kChunk steps, whole graphs of kGraphSteps where possible
@@ -1052,14 +1060,15 @@ int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous) {
   });
 }
 
-int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out4) {
+int mcmp2dev_guard_stats(mcmp2dev_t* h, double* out5) {
   return guard(h, [&] {
-    if (!out4) throw ArgError("guard_stats: null output");
-    out4[0] = double(h->guard_steps);
-    out4[1] = double(h->guard_trips);
-    out4[2] = h->guard_max_est;
-    out4[3] = h->guard_tol;
-    h->guard_steps = h->guard_trips = 0;
+    if (!out5) throw ArgError("guard_stats: null output");
+    out5[0] = double(h->guard_steps);
+    out5[1] = double(h->guard_refined);
+    out5[2] = double(h->guard_dmma);
+    out5[3] = h->guard_max_est;
+    out5[4] = h->guard_tol;
+    h->guard_steps = h->guard_refined = h->guard_dmma = 0;
     h->guard_max_est = 0.0;
   });
 }

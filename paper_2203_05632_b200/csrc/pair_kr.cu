@@ -156,8 +156,9 @@ template <bool PHYS, int OZ>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
   pdl_wait();     // Phi of this step is visible
   pdl_trigger();  // persistent: the next step's walk may launch next to it
-  // the INT8 path's guard launch: nothing to do unless oz_vgemm_kernel failed this step's check
-  if (P.guard_fallback && *reinterpret_cast<volatile const int*>(&P.st->oz_trip) == 0) return;
+  // the INT8 path's guard launch: nothing to do unless this step failed the INT8 checks (the
+  // main pass without refinement, or the refinement pass: oz_trip 2)
+  if (P.guard_fallback && *reinterpret_cast<volatile const int*>(&P.st->oz_trip) != 2) return;
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);

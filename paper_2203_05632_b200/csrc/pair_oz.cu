@@ -46,9 +46,11 @@ namespace mcmp2dev {
 namespace {
 using namespace pairk;
 
-constexpr int S = OZ_SLICES;
+constexpr int S = OZ_SLICES;        // slices per operand in the main pass (products s + t <= 5)
+constexpr int SL = S + 1;           // slices stored per operand: the 7th feeds the refinement pass
 constexpr int MA = 128;             // A rows (Q side) of a tile: 16 walkers
-constexpr int A_KS = S * MA * 32;   // bytes of one k-step (32 of K') of a Q block, all slices
+constexpr int A_KS = S * MA * 32;   // bytes of one k-step (32 of K') of a Q block's main slices
+constexpr int A_KSM = SL * MA * 32; // stored bytes of one k-step of a Q block (the main slices first)
 #ifndef OZ_STAGES
 #define OZ_STAGES 5
 #endif
@@ -65,19 +67,28 @@ constexpr int TMEM_COLS = 512;      // 6 x NB used
 // pair_kr's 16 x 8 tiles) or 10 walkers (80 rows, the fused literal path: a kind::i8 M128 MMA
 // costs the same ~61 cycles for N = 32..80 (tools/umma_rate.cu), so N = 80 -- the widest that
 // fits six accumulators in 512 TMEM columns -- does 25% more work per instruction)
-template <bool FUSED>
+// CORR: the refinement pass (all SL slices per k-step, one accumulator per tile)
+template <bool FUSED, bool CORR = false>
 struct OzShape {
   static constexpr int NB = FUSED ? 80 : 64;
   static constexpr int PW = NB / 8;  // P walkers per tile
-  static constexpr int B_KS = S * NB * 32;
-  static constexpr int STAGE = A_KS + B_KS;
-  static constexpr int SMEM_BYTES = STAGES * STAGE;
+  static constexpr int B_KSM = SL * NB * 32;  // stored bytes of one k-step of a P block
+  static constexpr int NSL = CORR ? SL : S;   // slices copied per k-step
+  static constexpr int A_CP = NSL * MA * 32, B_CP = NSL * NB * 32;
+  static constexpr int STAGE = A_CP + B_CP;
+  static constexpr int NSTAGE = CORR ? 4 : STAGES;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE;
+  static constexpr int NACC = CORR ? 1 : S;   // accumulators per tile (slice diagonals)
+  static constexpr int NSLOT = CORR ? 6 : 1;  // tiles in flight in TMEM
   static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
   // instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = NB
   static constexpr uint32_t IDESC =
       (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
 };
-static_assert(STAGES * OzShape<true>::STAGE <= 227 * 1024, "stage ring");
+static_assert(OzShape<true>::SMEM_BYTES <= 227 * 1024, "stage ring");
+static_assert(OzShape<true, true>::SMEM_BYTES <= 227 * 1024, "stage ring");
+static_assert(OzShape<true>::NACC * OzShape<true>::NB <= 512 && OzShape<true, true>::NSLOT * OzShape<true>::NB <= 512,
+              "TMEM columns");
 
 // canonical K-major, no-swizzle UMMA operand layout of one k-step: [row / 8][k / 16][row % 8][16 B]
 __host__ __device__ __forceinline__ int op_off(int r, int kk) {
@@ -134,10 +145,10 @@ int oz_tiles(int nbq, int pw) {
 // all steps exact in FP64). Rounded digits are centred and, after the first, mostly |d| <= 64:
 // on the oracle's cfg3 inputs the step's exchange sum is 20x closer to FP64 than with truncated
 // digits (7e-12 vs 1.2e-10 relative), at the same 21 products (tests/test_ozaki_budget.py)
-__device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[S]) {
+__device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[SL]) {
   double r[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
+  for (int s = 0; s < SL; ++s) {
     uint32_t w = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -178,8 +189,8 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   const int qb = pt >> 5, qrow = ((pt & 31) >> 1) * 8 + (pt & 1) * 4;  // A row of (x_alpha 0, re)
   const int NB = P.nb_rows, bpts = NB / 4;  // B rows and points per P block
   const int pb = pt / bpts, prow = ((pt % bpts) >> 1) * 8 + (pt & 1) * 4;  // B row of channel 0
-  int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KS;
-  int8_t* const sb = P.sb + size_t(pb) * ks_n * S * NB * 32;
+  int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KSM;
+  int8_t* const sb = P.sb + size_t(pb) * ks_n * SL * NB * 32;
   const bool stats = P.pstat != nullptr;
   double ss = 0.0, nbig = 0.0, n2 = 0.0, row_scale = 1.0;
   {
@@ -238,18 +249,18 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
           nbig += (fabs(xr[i]) > 0x1p-8 ? 1.0 : 0.0) + (fabs(xi[i]) > 0x1p-8 ? 1.0 : 0.0);
         }
       }
-      uint32_t dr[S], di[S];
+      uint32_t dr[SL], di[SL];
       digits4(xr, dr);
       digits4(xi, di);
       const int kre = 4 * qd, kim = KH + 4 * qd;  // K' positions of the re and im halves
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
+      for (int s = 0; s < SL; ++s) {
         // B row [re | im]
-        *reinterpret_cast<uint32_t*>(sb + (size_t(kre >> 5) * S + s) * NB * 32 + op_off(rb, kre & 31)) = dr[s];
-        *reinterpret_cast<uint32_t*>(sb + (size_t(kim >> 5) * S + s) * NB * 32 + op_off(rb, kim & 31)) = di[s];
+        *reinterpret_cast<uint32_t*>(sb + (size_t(kre >> 5) * SL + s) * NB * 32 + op_off(rb, kre & 31)) = dr[s];
+        *reinterpret_cast<uint32_t*>(sb + (size_t(kim >> 5) * SL + s) * NB * 32 + op_off(rb, kim & 31)) = di[s];
         if (alpha) {  // A rows [re | im] and [im | -re]
-          int8_t* a0 = sa + (size_t(kre >> 5) * S + s) * MA * 32;
-          int8_t* a1 = sa + (size_t(kim >> 5) * S + s) * MA * 32;
+          int8_t* a0 = sa + (size_t(kre >> 5) * SL + s) * MA * 32;
+          int8_t* a1 = sa + (size_t(kim >> 5) * SL + s) * MA * 32;
           *reinterpret_cast<uint32_t*>(a0 + op_off(ra, kre & 31)) = dr[s];
           *reinterpret_cast<uint32_t*>(a1 + op_off(ra, kim & 31)) = di[s];
           *reinterpret_cast<uint32_t*>(a0 + op_off(ra + 1, kre & 31)) = di[s];
@@ -306,12 +317,24 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   }
 }
 
-template <bool FUSED>
+// CORR (FUSED only): the guard's refinement pass. A step whose error estimate failed in the main
+// pass (st->oz_trip == 1) gets the next slice diagonal, d = s + t = 6 (seven products per k-step,
+// the 7th slices included), in one int32 accumulator per tile: dV = acc 2^(e_q + e_p - 56). The
+// main pass stored each pair's f values (P.fstore); this pass adds df = sum o dV, re-forms the
+// pair terms from f + df and the step's sums, and re-checks them with the estimate scaled by
+// 2^-7; a step that still fails goes on to the DMMA kernel (oz_trip = 2). The accumulator is
+// small, so six tiles rotate through TMEM and the drain never stalls the MMAs.
+template <bool FUSED, bool CORR>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
-  using Sh = OzShape<FUSED>;
-  constexpr int NB = Sh::NB, PW = Sh::PW, B_KS = Sh::B_KS, STAGE = Sh::STAGE, CPW = Sh::CPW;
+  using Sh = OzShape<FUSED, CORR>;
+  constexpr int NB = Sh::NB, PW = Sh::PW, STAGE = Sh::STAGE, CPW = Sh::CPW;
+  constexpr int A_CP = Sh::A_CP, B_CP = Sh::B_CP, B_KSM = Sh::B_KSM, NST = Sh::NSTAGE;
+  constexpr int NACC = Sh::NACC, NSLOT = Sh::NSLOT;
+  static_assert(!CORR || FUSED, "the refinement pass serves the fused literal path");
   pdl_wait();
   pdl_trigger();
+  if constexpr (CORR)  // nothing to refine unless the main pass rejected this step
+    if (*reinterpret_cast<volatile const int*>(&P.st->oz_trip) != 1) return;
   extern __shared__ __align__(1024) int8_t sm[];
   // Measured and rejected: eight rotating 64-column accumulator slots (tile i's diagonal d in slot
   // (6 i + d) % 8, drained and freed diagonal by diagonal so the next tile starts early): V-GEMM
@@ -321,7 +344,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // (tools/oz_gemm.cu -DA_TMEM). At N = 80 (same-box A/B, V-GEMM ms): 3 / 4 / 5 ring stages
   // 1.333 / 1.335 / 1.335; 4 epilogue warps 1.482 vs 8 warps 1.335 (the drain is the epilogue
   // warps' instruction latency while the MMA waits for TMEM).
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[NSLOT], tempty[NSLOT];
   __shared__ uint32_t tmem_base;
   __shared__ double s_red[EPW][6];
   __shared__ bool s_last;
@@ -332,9 +355,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
   const bool guard = FUSED && P.pstat != nullptr;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
-    mbar_init(&tfull, 1);
-    mbar_init(&tempty, 32 * EPW);
+    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 32 * EPW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -356,40 +378,48 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       OzWalk w(int(blockIdx.x), PW);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
         const int a = w.a, b = w.b;
-        const int8_t* ga = P.sa + size_t(a) * KS * A_KS;
-        const int8_t* gb = P.sb + size_t(b) * KS * B_KS;
+        const int8_t* ga = P.sa + size_t(a) * KS * A_KSM;
+        const int8_t* gb = P.sb + size_t(b) * KS * B_KSM;
         for (int ks = 0; ks < KS; ++ks) {
           mbar_wait(&empty[stage], ph ^ 1u);
           int8_t* dst = sm + stage * STAGE;
           mbar_expect_tx(&full[stage], STAGE);
-          bulk_g2s(dst, ga + size_t(ks) * A_KS, A_KS, &full[stage]);
-          bulk_g2s(dst + A_KS, gb + size_t(ks) * B_KS, B_KS, &full[stage]);
-          if (++stage == STAGES) stage = 0, ph ^= 1u;
+          bulk_g2s(dst, ga + size_t(ks) * A_KSM, A_CP, &full[stage]);
+          bulk_g2s(dst + A_CP, gb + size_t(ks) * B_KSM, B_CP, &full[stage]);
+          if (++stage == NST) stage = 0, ph ^= 1u;
         }
       }
     }
   } else if (warp == EPW + 1) {
-    if (lane == 0) {  // MMA issuer: 21 slice products per k-step into the diagonal accumulators
+    if (lane == 0) {  // MMA issuer: the slice products of each k-step into the tile's accumulators
       int stage = 0;
       uint32_t ph = 0;
       for (int it = 0; it < my; ++it) {
-        mbar_wait(&tempty, (it & 1) ^ 1u);  // the epilogue has drained the previous tile
+        const int slot = it % NSLOT;
+        mbar_wait(&tempty[slot], ((it / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int ks = 0; ks < KS; ++ks) {
           mbar_wait(&full[stage], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const int8_t* sa = sm + stage * STAGE;
-          const int8_t* sb = sa + A_KS;
+          const int8_t* sb = sa + A_CP;
+          if constexpr (CORR) {
 #pragma unroll
-          for (int s = 0; s < S; ++s)
+            for (int s = 0; s < SL; ++s)  // diagonal 6: (s, 6 - s)
+              umma_i8<Sh::IDESC>(tmem + uint32_t(slot * NB), umma_desc(sa + s * MA * 32),
+                                 umma_desc(sb + (SL - 1 - s) * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
+          } else {
 #pragma unroll
-            for (int t = 0; s + t < S; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
-              umma_i8<Sh::IDESC>(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32), umma_desc(sb + t * NB * 32),
-                      ks > 0 || s > 0 ? 1u : 0u);
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+              for (int t = 0; s + t < S; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
+                umma_i8<Sh::IDESC>(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32),
+                                   umma_desc(sb + t * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
+          }
           umma_commit(&empty[stage]);  // the stage is free once these MMAs have read it
-          if (++stage == STAGES) stage = 0, ph ^= 1u;
+          if (++stage == NST) stage = 0, ph ^= 1u;
         }
-        umma_commit(&tfull);
+        umma_commit(&tfull[slot]);
       }
     }
   } else {  // epilogue: TMEM lane = A row; this warp's columns [c_lo, c_lo + CPW)
@@ -400,39 +430,41 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
       const int t = int(blockIdx.x) + it * int(gridDim.x);
       const int a = w.a, b = w.b;
-      mbar_wait(&tfull, it & 1);
+      const int slot = it % NSLOT;
+      mbar_wait(&tfull[slot], (it / NSLOT) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tbase = tmem + (uint32_t(lq * 32) << 16) + uint32_t(slot * NB + c_lo);
       long long X[CPW];
-      auto merge = [&](const uint32_t (&v)[S][16], int c0, int n) {
+      auto merge = [&](const uint32_t (&v)[NACC][16], int c0, int n) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           if (c >= n) break;
           long long x = int32_t(v[0][c]);
 #pragma unroll
-          for (int d = 1; d < S; ++d) x = x * 128 + int32_t(v[d][c]);
+          for (int d = 1; d < NACC; ++d) x = x * 128 + int32_t(v[d][c]);
           X[c0 + c] = x;
         }
       };
 #pragma unroll
       for (int c0 = 0; c0 + 16 <= CPW; c0 += 16) {
-        uint32_t v[S][16];
+        uint32_t v[NACC][16];
 #pragma unroll
-        for (int d = 0; d < S; ++d)
-          tmem_ld16(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
+        for (int d = 0; d < NACC; ++d) tmem_ld16(tbase + uint32_t(d * NB + c0), v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         merge(v, c0, 16);
       }
       if constexpr (CPW % 16 != 0) {  // N = 80: a last 8-column chunk
         constexpr int c0 = CPW / 16 * 16;
-        uint32_t v[S][16];
+        uint32_t v[NACC][16];
 #pragma unroll
-        for (int d = 0; d < S; ++d) tmem_ld8(tmem + (uint32_t(lq * 32) << 16) + uint32_t(d * NB + c_lo + c0), v[d]);
+        for (int d = 0; d < NACC; ++d) tmem_ld8(tbase + uint32_t(d * NB + c0), v[d]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         merge(v, c0, 8);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&tempty);  // accumulators free: the next tile's MMAs overlap the work below
-      const double sr = P.sa_scale[size_t(a) * MA + row];
+      mbar_arrive(&tempty[slot]);  // accumulators free: the next tile's MMAs overlap the work below
+      // main pass: V = X 2^(e_q + e_p - 49); refinement: dV = acc 2^(e_q + e_p - 56)
+      const double sr = P.sa_scale[size_t(a) * MA + row] * (CORR ? 0x1p-7 : 1.0);
       const double* sbv = P.sb_scale + size_t(b) * NB + c_lo;
       if constexpr (!FUSED) {
         double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8 + c_lo * 8;
@@ -484,7 +516,9 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
         // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
         // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
-        // (tests/test_gpu_guard.py); it is a model, not a bound.
+        // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
+        // (one more slice and diagonal) the same model with 2^-49.
+        constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
         double4 Sc = make_double4(0, 0, 0, 0), Sd = Sc;
         if (guard && (row & 7) == 0 && qg < P.m) {
           Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
@@ -496,18 +530,27 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
           const int pg = pg0 + p;
           if ((row & 7) == 0 && qg < P.m && pg < P.m && qg > pg) {
-            const double td = (-P.w_direct * g[2 * p]) * f11;   // f1d f2d
-            const double tx = (-P.w_exchange * f10) * g[2 * p + 1];  // f1x f2x
+            // f(0,0) = f1d, f(1,1) = f2d, f(1,0) = f1x, f(0,1) = f2x
+            double F00 = g[2 * p], F11 = f11, F10 = f10, F01 = g[2 * p + 1];
+            double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
+            if constexpr (CORR) {  // f of the main pass plus this pass's corrections
+              const double4 f6 = *fs;
+              F00 += f6.x, F11 += f6.y, F10 += f6.z, F01 += f6.w;
+            } else if (fs) {
+              *fs = make_double4(F00, F11, F10, F01);
+            }
+            const double td = (-P.w_direct * F00) * F11;   // f1d f2d
+            const double tx = (-P.w_exchange * F10) * F01;  // f1x f2x
             acc_d += td;
             acc_x += tx;
             if (guard) {
               const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
               const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
-              const double nac = 0x1p-42 * Sa.z * Sc.z, nbd = 0x1p-42 * Sb.z * Sd.z;
+              const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
               const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
               const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
-              const double ed = fabs(P.w_direct) * (s1d * fabs(f11) + fabs(g[2 * p]) * s2d);
-              const double ex = fabs(P.w_exchange) * (s1x * fabs(g[2 * p + 1]) + fabs(f10) * s2x);
+              const double ed = fabs(P.w_direct) * (s1d * fabs(F11) + fabs(F00) * s2d);
+              const double ex = fabs(P.w_exchange) * (s1x * fabs(F01) + fabs(F10) * s2x);
               acc_ed += ed * ed;
               acc_ex += ex * ex;
               acc_ad += fabs(td);
@@ -566,7 +609,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     P.step_out[4] = x;
     P.step_out[5] = 0.0;
     // guard: estimated error of the direct and exchange sums and of the step value against
-    // guard_tol; a failed (or non-finite) step is recomputed by the guarded DMMA launch
+    // guard_tol; a failed (or non-finite) step goes to the refinement pass (oz_trip 1: when the
+    // main pass stored the f values) or to the DMMA kernel (oz_trip 2)
     const double ed = sqrt(r[4]), ex = sqrt(r[5]), tol = P.guard_tol;
     const bool trip = guard && tol > 0.0 &&
                       (!(ed <= tol * fabs(d)) || !(ex <= tol * fabs(x)) || !(sqrt(r[4] + r[5]) <= tol * fabs(d + x)));
@@ -575,8 +619,13 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     P.step_out[8] = r[6];
     P.step_out[9] = r[7];
     P.step_out[10] = 1.0;
-    P.step_out[11] = trip ? 1.0 : 0.0;
-    if (trip) P.st->oz_trip = 1;
+    if constexpr (CORR) {
+      P.step_out[11] = trip ? 2.0 : 1.0;  // refined; DMMA next if the refined step still fails
+      P.st->oz_trip = trip ? 2 : 0;
+    } else {
+      P.step_out[11] = trip && !P.fstore ? 2.0 : 0.0;
+      if (trip) P.st->oz_trip = P.fstore ? 1 : 2;
+    }
     P.st->done_pair = 0;
   }
 }
@@ -588,10 +637,10 @@ void oz_layout(int n_vir, int& kh, int& ks) {
   kh = (n_vir + 15) / 16 * 16;
   ks = 2 * kh / 32;
 }
-size_t oz_slice_bytes_a(int npts_pad, int ks) { return size_t(npts_pad / 32) * ks * A_KS; }
+size_t oz_slice_bytes_a(int npts_pad, int ks) { return size_t(npts_pad / 32) * ks * A_KSM; }
 int oz_p_blocks(int npts_oz, int nb_rows) { return (npts_oz + nb_rows / 4 - 1) / (nb_rows / 4); }
 size_t oz_slice_bytes_b(int npts_oz, int ks, int nb_rows) {
-  return size_t(oz_p_blocks(npts_oz, nb_rows)) * ks * S * nb_rows * 32;
+  return size_t(oz_p_blocks(npts_oz, nb_rows)) * ks * SL * nb_rows * 32;
 }
 int oz_nb_rows(bool fused) { return fused ? OzShape<true>::NB : OzShape<false>::NB; }
 int oz_ntiles(int nbq, bool fused) { return oz_tiles(nbq, oz_nb_rows(fused) / 8); }
@@ -600,11 +649,14 @@ cudaError_t oz_kernel_setup() {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sms_oz[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  const cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             OzShape<false>::SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       OzShape<false>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(oz_vgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              OzShape<true>::SMEM_BYTES);
+  e = cudaFuncSetAttribute(oz_vgemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           OzShape<true>::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(oz_vgemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              OzShape<true, true>::SMEM_BYTES);
 }
 
 void launch_oz_slice(const OzParams& P, cudaStream_t s) {
@@ -624,9 +676,17 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
   const int grid = P.ntiles < sms ? P.ntiles : sms;
   if (P.otiles)
-    pdl_launch(oz_vgemm_kernel<true>, dim3(grid), dim3(THREADS), OzShape<true>::SMEM_BYTES, s, P);
+    pdl_launch(oz_vgemm_kernel<true, false>, dim3(grid), dim3(THREADS), OzShape<true>::SMEM_BYTES, s, P);
   else
-    pdl_launch(oz_vgemm_kernel<false>, dim3(grid), dim3(THREADS), OzShape<false>::SMEM_BYTES, s, P);
+    pdl_launch(oz_vgemm_kernel<false, false>, dim3(grid), dim3(THREADS), OzShape<false>::SMEM_BYTES, s, P);
+}
+
+void launch_oz_refine(const OzParams& P, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
+  const int grid = P.ntiles < sms ? P.ntiles : sms;
+  pdl_launch(oz_vgemm_kernel<true, true>, dim3(grid), dim3(THREADS), OzShape<true, true>::SMEM_BYTES, s, P);
 }
 
 }  // namespace mcmp2dev

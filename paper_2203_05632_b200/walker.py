@@ -227,11 +227,12 @@ class DeviceWalker:
                   self._h)
         return prev.value
 
-    def guard_stats(self, reset: bool = True) -> dict:
-        """{checked, fallbacks, max_est_rel, tol} since the last call (the call resets them)."""
-        o = np.zeros(4)
+    def guard_stats(self) -> dict:
+        """{checked, refined, dmma, max_est_rel, tol} since the last call (the call resets them)."""
+        o = np.zeros(5)
         check_dev(self._d.mcmp2dev_guard_stats(self._h, dptr(o)), self._h)
-        return {"checked": int(o[0]), "fallbacks": int(o[1]), "max_est_rel": float(o[2]), "tol": float(o[3])}
+        return {"checked": int(o[0]), "refined": int(o[1]), "dmma": int(o[2]), "max_est_rel": float(o[3]),
+                "tol": float(o[4])}
 
     # -- instrumentation ------------------------------------------------------------
     def profile(self, enable: bool = True, reset: bool = True) -> dict:

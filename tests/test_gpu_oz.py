@@ -41,7 +41,8 @@ def test_int8_v_physical_replay_matches_oracle(cfgdir):
     orc = oracle_py.OracleSystem(sp, text)
     tr = orc.trajectory(seed=17, stream=0, m=192, burn=20, nsteps=1, physical=True)
     dw = DeviceWalker(System(sp, text), max_walkers=192)
-    assert dw.int8_v()
+    assert not dw.int8_v()  # the physical estimator defaults to the DMMA pair stage
+    assert dw.int8_v(1)     # INT8 V blocks on request (unguarded)
     got = dw.replay(tr["walkers"], tr["tau"])
     for k in (0, 2, 4):
         assert rel_err(got[:, k], tr["est"][:, k]) < REL, k
