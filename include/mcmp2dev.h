@@ -197,7 +197,7 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
  * on the INT8 tensor cores (the 7th slices and the next slice diagonal, ~1/128 of the error;
  * the main pass keeps every pair's f values for it), and if the refined step still fails it
  * is recomputed on the FP64 DMMA pair kernel. Both are launched every step and exit at once
- * unless needed, so the graphs stay fixed. tol <= 0 turns the guard off; default 3e-10; NaN
+ * unless needed, so the graphs stay fixed. tol <= 0 turns the guard off; default 2e-10; NaN
  * only queries. previous (may be NULL) receives the old tolerance. The estimate is a model
  * checked against the oracle (tests/test_oz_guard_model.py) and against the DMMA path on
  * 2000-step chains (2.3-170x the actual error), not a rigorous bound (that would be ~1e-7

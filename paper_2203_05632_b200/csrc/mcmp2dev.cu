@@ -31,11 +31,14 @@ namespace {
 constexpr int kChunk = 1024;  // steps per device->host copy of StepEstimates
 constexpr int kGraphSteps = 32;  // production steps per captured CUDA graph (even)
 constexpr int kBatchMaxWalkers = 480;  // per batched ensemble (2m + 32 threads <= 1024, m % 16 == 0)
-// default guard tolerance of the INT8 V path: the estimated error must stay below 3e-10 of
+// default guard tolerance of the INT8 V path: the estimated error must stay below 2e-10 of
 // |direct|, |exchange| and |value|. Measured on 2000-step chains (profiles/r07_guard_*): the
-// estimate is 2.3-170x the actual error; kept steps stay within 6e-11 of FP64 (the unguarded
-// path exceeds the 1e-10 gate on 0.6-0.8% of the steps, by up to 3e-7 on the value)
-constexpr double kGuardTol = 3e-10;
+// estimate is 2.3-170x the actual error; at 3e-10 the steps kept on the main pass stay within
+// 6e-11 of FP64 (the unguarded path exceeds the 1e-10 gate on 0.6-0.8% of the steps, by up to
+// 3e-7 on the value); 2e-10 keeps a 2x margin at the smallest measured estimate/error ratio.
+// Cost at cfg4 (profiles/r07_guard_cost_cfg4.json): estimate 0.09 ms/step, each refined step
+// ~0.9 ms (10-15% of the steps at 3e-10)
+constexpr double kGuardTol = 2e-10;
 thread_local std::string g_create_error;
 
 struct CudaError : std::runtime_error {

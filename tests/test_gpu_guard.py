@@ -30,7 +30,7 @@ from paper_2203_05632_b200.walker import EnsembleState
 pytestmark = pytest.mark.gpu
 
 REL = 1e-10
-TOL = 3e-10  # the default guard tolerance (mcmp2dev.cu kGuardTol)
+TOL = 2e-10  # the default guard tolerance (mcmp2dev.cu kGuardTol)
 F = {n: i for i, n in enumerate(DeviceWalker.STEP_EX_FIELDS)}
 
 
