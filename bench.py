@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Benchmark of the MC-MP2 walker loop (BASELINE.json metric: walker-pair x tau samples/s).
+"""Benchmark of the MC-MP2 walker loop (BASELINE.json metric: walker-pair x tau samples/s, and
+time to 1% relative error).
 
 One step = one pass of the hot path over one ensemble: Metropolis sweep of m walker pairs,
 tau draw, spinor values + MO transform at 2m points, O/V Green's-function blocks and the
@@ -7,9 +8,18 @@ fused direct/exchange integrand over all C(m,2) walker pairs, block reduction
 (reference driver.cpp:440-450). samples/step = C(m,2).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+                  [--scaling strong|weak] [--strong-total-steps S] [--ttt cfg5-10,cfg5-2]
 
 N > 1 runs under torchrun, one process per GPU; each rank is one reference worker (its own
-ensemble, Philox stream = rank, driver.cpp:354-356), so per-GPU work is fixed ("weak").
+ensemble, Philox stream = rank, driver.cpp:354-356). --scaling strong (default): the K timed
+steps are the run's total, split over the ranks with worker_share (driver.cpp:307-309);
+weak: K steps per rank. Beside the timed steps the line carries
+  strong_run:     the north_star strong-scaling job -- a fixed total step budget of the config
+                  (2 x 10^4 at cfg4) split with worker_share over the ranks, wall time from
+                  handle creation (init + burn-in included) to the merged estimate, max over ranks;
+  time_to_target: wall time to sigma_bar/|E| <= 1% through the Engine stop rule
+                  (driver.cpp:401-412) on the cfg5 sweep members named by --ttt, all ranks
+                  merging at every checkpoint interval, with the CPU counterpart extrapolated.
 `--impl reference` times the CPU restatement of the reference path (oracle/, the reference
 itself needs Eigen3 and cannot be built here) on all host cores, rank 0 only.
 """
@@ -33,12 +43,32 @@ sys.path.insert(0, str(ROOT / "tests"))
 METRIC = "MC-MP2 walker-pair x tau samples/sec"
 UNIT = "samples/s"
 WALKERS = {"cfg1": 16, "cfg2": 128, "cfg3": 512, "cfg4": 2048}
+WALKERS.update({f"cfg5-{n}": 8192 for n in (2, 10, 18, 36, 54, 86)})
 WORKLOAD = {
     "cfg1": "2e atom, 4c, 12s L + 36p S, n_occ 2, n_vir 22, m 16",
     "cfg2": "10e atom, 4c, 14s9p L (R 274), n_occ 10, n_vir 72, m 128",
     "cfg3": "18e diatomic, 4c, 17s12p4d+6s2p L (R 556), n_occ 18, n_vir 152, m 512",
     "cfg4": "54e heavy diatomic, 4c, 24s20p14d+6s2p L (R 1056), n_occ 54, n_vir 278, m 2048/GPU",
 }
+WORKLOAD.update({f"cfg5-{n}": f"size sweep: {n}e atom, 4c, even-tempered s/p/d/f, m 8192/GPU" for n in (2, 10, 18, 36, 54, 86)})
+STRONG_TOTAL = {"cfg1": 2000, "cfg2": 10000, "cfg3": 10000, "cfg4": 20000}  # BASELINE configs' step budgets
+DTYPE = ("f64/c128 (reference arithmetic); the V blocks (~90% of the pair FLOPs) as 6-slice int8 Ozaki sums on "
+         "tcgen05 with a per-step error guard: steps whose estimated error exceeds 2e-10 of their sums get a "
+         "7th-slice refinement or an FP64 DMMA recompute")
+MCMP2_CLI = ROOT / "paper_2203_05632_b200" / "lib" / "mcmp2"
+
+
+def generate_inputs(cfg: str, directory: Path) -> tuple[Path, Path]:
+    """The config's SPINOR-TEXT and run config, written by the C++ CLI in a child process
+    (`mcmp2 generate`), so the reference arm's process maps no product library."""
+    directory.mkdir(parents=True, exist_ok=True)
+    subprocess.run([str(MCMP2_CLI), "generate", cfg, "--output", str(directory)], check=True,
+                   stdout=subprocess.DEVNULL)
+    return directory / f"{cfg}.spinor", directory / f"{cfg}.conf"
+
+
+def worker_share(total: int, workers: int, index: int) -> int:  # driver.cpp:307-309
+    return total // workers + (1 if index < total % workers else 0)
 
 
 class NvmlClocks:
@@ -134,40 +164,60 @@ def peaks():
     return fp64["dmma_tflops"], "MEASURED_FP64.json dmma_tflops (mma.sync m8n8k4 f64 loop on this pool's B200)"
 
 
-def cpu_leg(cfg: str, spinor: Path, conf_text: str, steps: int, warmup: int, quick: bool):
-    """CPU restatement (oracle/, kind 'port') on all host cores, bounded sample per step."""
+# bounded CPU samples: a step restricted to walker rows [0, r) of the pair loop (the Metropolis
+# sweep and the spinor values always cover all 2m points), at three row counts
+SAMPLE_ROWS = {"cfg3": (8, 32, 128), "cfg4": (4, 16, 64)}
+SAMPLE_ROWS.update({f"cfg5-{n}": (1, 2, 4) for n in (2, 10, 18, 36, 54, 86)})
+
+
+def cpu_steps(orc, cfg: str, m: int, nsteps: int, threads: int, seed0: int = 1) -> list:
+    """nsteps timed steps of the CPU restatement (oracle/, one std::thread worker per core as
+    driver.cpp:423-438, each on its own ensemble): step k runs the full pair loop (cfg1/cfg2) or
+    rows [0, r_k) with r_k cycling over SAMPLE_ROWS[cfg]. Returns [(rows, seconds, samples/worker)]."""
+    step_size = 0.3 if cfg == "cfg1" else 0.0
+    rows = SAMPLE_ROWS.get(cfg, (m,))
+    out = []
+    for k in range(nsteps):
+        r = rows[k % len(rows)]
+        sec, samples = orc.cpu_baseline(seed=seed0 + k, m=m, rows=r, burn=5, step_size=step_size, steps=1,
+                                        threads=threads)
+        out.append((r, sec, samples / threads))
+    return out
+
+
+def cpu_full_step(pts: list, npairs: int) -> dict:
+    """Per-worker time of a full C(m,2) step from the sampled steps: least squares of
+    t = t0 + c n (t0 the O(m) part, c per pair sample) when rows were restricted (extrapolated),
+    else the mean measured step."""
+    import numpy as np
+    n = np.array([p[2] for p in pts])
+    t = np.array([p[1] for p in pts])
+    if len(set(np.round(n))) < 2:
+        return {"t_full": float(t.mean()), "extrapolated": False}
+    A = np.stack([np.ones_like(n), n], 1)
+    (t0, c), *_ = np.linalg.lstsq(A, t, rcond=None)
+    resid = t - A @ np.array([t0, c])
+    return {"t_full": float(t0 + c * npairs), "extrapolated": True, "t0_s": float(t0), "us_per_sample": float(c * 1e6),
+            "fit_residual_rel": float(np.sqrt(np.mean(resid ** 2)) / t.mean()),
+            "rows": sorted({int(p[0]) for p in pts})}
+
+
+def cpu_leg(cfg: str, spinor: Path, conf_text: str, nsteps: int) -> dict:
+    """cpu_baseline of our arm (rank 0, N = 1): the CPU restatement (kind 'port') on all host cores."""
     import oracle_py
     threads = os.cpu_count() or 1
     orc = oracle_py.OracleSystem(spinor, conf_text)
     m = WALKERS[cfg]
     npairs = m * (m - 1) // 2
-    step_size = 0.3 if cfg == "cfg1" else 0.0
-    full = cfg in ("cfg1", "cfg2")
-    if full:  # whole steps fit the time budget
-        if warmup:
-            orc.cpu_baseline(seed=1, m=m, rows=m, burn=20, step_size=step_size, steps=warmup, threads=threads)
-        sec, samples = orc.cpu_baseline(seed=1, m=m, rows=m, burn=20, step_size=step_size, steps=steps,
-                                        threads=threads)
-        return {"value": samples / sec, "unit": UNIT, "cores": threads, "kind": "port", "seconds": sec,
-                "samples": samples, "sample": f"{threads} workers (std::thread, driver.cpp:423-438) x {steps} "
-                f"full steps of m={m}"}
-    # bounded sample: per worker one step restricted to walker rows [0, r) of the pair loop (Metropolis
-    # and spinor values always cover all 2m points); two row counts give the fixed O(m) cost and the
-    # per-sample cost, extrapolated to the full C(m,2) step and stated as such.
-    ra, rb = {"cfg3": (8, 48), "cfg4": (4, 36)}[cfg] if not quick else (1, 2)
-    reps = max(2, steps // 8)
-    ta, na = orc.cpu_baseline(seed=1, m=m, rows=ra, burn=5, step_size=step_size, steps=reps, threads=threads)
-    tb, nb = orc.cpu_baseline(seed=1, m=m, rows=rb, burn=5, step_size=step_size, steps=reps, threads=threads)
-    # ta = reps*T0 + c*na/threads (workers run concurrently), same for tb
-    c = (tb - ta) * threads / max(nb - na, 1)                # s per sample per worker
-    t0 = max(ta - c * na / threads, 0.0) / reps              # fixed s per step per worker
-    t_full = t0 + c * npairs
-    value = threads * npairs / t_full
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "seconds": ta + tb,
-            "samples": na + nb,
-            "sample": f"{threads} workers x {reps} step(s) at walker rows [0,{ra}) and [0,{rb}) of m={m} "
-                      f"({na + nb} pair samples, {ta + tb:.1f} s); full-step rate extrapolated linearly "
-                      f"(fixed {t0:.2f} s/step + {c * 1e6:.2f} us/sample per worker)"}
+    pts = cpu_steps(orc, cfg, m, nsteps, threads)
+    fit = cpu_full_step(pts, npairs)
+    secs = sum(p[1] for p in pts)
+    sample = (f"{threads} workers (std::thread, driver.cpp:423-438) x {len(pts)} step(s) of m={m}"
+              + (f" at walker rows {fit['rows']} of the pair loop ({secs:.1f} s); full-step rate extrapolated by a "
+                 f"least-squares fit t = t0 + c n (t0 {fit['t0_s']:.2f} s, {fit['us_per_sample']:.2f} us/sample per worker, "
+                 f"residual {100 * fit['fit_residual_rel']:.1f}%)" if fit["extrapolated"] else f", full steps ({secs:.1f} s)"))
+    return {"value": threads * npairs / fit["t_full"], "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": sample, "t_full_step_s": fit["t_full"], "fit": fit}
 
 
 def interval_merge(vals, first_index: int, dist):
@@ -194,6 +244,74 @@ def interval_merge(vals, first_index: int, dist):
     return {"E2": value, "sigma_bar": sigma_bar, "steps": total, "workers": len(parts)}
 
 
+def reference_arm(args, cfg: str) -> None:
+    """--impl reference (rank 0): the CPU restatement of the reference path on all host cores, K
+    timed bounded steps (plus W untimed) of the same workload; only oracle/ libraries are mapped."""
+    import oracle_py
+    tmp = Path(tempfile.mkdtemp(prefix="mcmp2_ref_"))
+    spinor, conf = generate_inputs(cfg, tmp)
+    conf_text = conf.read_text()
+    m = WALKERS[cfg]
+    npairs = m * (m - 1) // 2
+    threads = os.cpu_count() or 1
+    orc = oracle_py.OracleSystem(spinor, conf_text)
+    if args.warmup:
+        cpu_steps(orc, cfg, m, args.warmup, threads, seed0=1000)
+    t0 = time.perf_counter()
+    pts = cpu_steps(orc, cfg, m, args.steps, threads)
+    wall = time.perf_counter() - t0
+    fit = cpu_full_step(pts, npairs)
+    value = threads * npairs / fit["t_full"]
+    secs = sum(p[1] for p in pts)
+    sample = (f"{threads} workers (std::thread, driver.cpp:423-438), each one ensemble of m={m}; {len(pts)} timed steps"
+              + (f" restricted to walker rows {fit['rows']} of the pair loop (cycled); full-step rate from a least-squares "
+                 f"fit t = t0 + c n over the timed steps (t0 {fit['t0_s']:.2f} s, {fit['us_per_sample']:.2f} us/sample per "
+                 f"worker, residual {100 * fit['fit_residual_rel']:.1f}%), extrapolated to C(m,2) = {npairs} samples"
+                 if fit["extrapolated"] else " of the full pair loop"))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / len(pts),  # what was timed: the sampled steps
+            "timed_region_s": wall,
+            "full_step_ms_extrapolated": 1e3 * fit["t_full"] if fit["extrapolated"] else None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64/c128",
+            "data": "synthetic (seeded SPINOR-TEXT from `mcmp2 generate`, host/generate.cpp)",
+            "config": {"workload": f"{cfg}: {WORKLOAD[cfg]}", "walkers_per_worker": m,
+                       "estimator": "literal (reference estimator.cpp:26-32)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "fit": fit,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_config_text(cfg: str, spinor: Path, conf_text: str, extra: str) -> str:
+    """A reference run config (driver.cpp:65-121) for the generated system: the generator's
+    weight lines plus the run-control keys of `extra`."""
+    keep = "".join(l + "\n" for l in conf_text.splitlines() if l.split()[:1] in (["weight"], ["step-size"]))
+    return f"spinors {spinor}\n" + keep + extra
+
+
+def engine_job(text: str, rank: int, world: int, dev: int, dist) -> dict:
+    """One fixed job through the host Engine's per-rank group (include/mcmp2host.h mcmp2h_group:
+    System load, device handle, init_ensemble + burn-in at creation) and the distributed driver's
+    interval merges (distributed.py drive_group, driver.cpp:376-420); wall time from a barrier
+    before the creation to the merged estimate, max over ranks."""
+    import torch
+    from paper_2203_05632_b200 import distributed as D
+    rc = D.parse_run_config(text)
+    first, count = D.rank_workers(rc["workers"], world, rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    group = D.HostGroup(text, first, count, dev)
+    rep = D.drive_group(group, rc["workers"], rc["steps"], rc["target"], rc["interval"],
+                        D.torch_all_gather(dist) if dist else (lambda a: [a]))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    group.close()
+    return {"seconds": wall, "report": rep}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -202,6 +320,14 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(WALKERS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--burnin", type=int, default=1000)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the K timed steps are the run's total, split over the ranks (worker_share); "
+                         "weak: K steps per rank")
+    ap.add_argument("--strong-total-steps", type=int, default=None,
+                    help="step budget of the strong_run job (default: the BASELINE config's, 2e4 at cfg4; 0 skips)")
+    ap.add_argument("--ttt", default="cfg5-10,cfg5-2",
+                    help="cfg5 members timed to 1%% relative error (comma list; empty skips)")
+    ap.add_argument("--target-rel-err", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ensembles", type=int, default=1,
                     help="reference workers per GPU, batched in one handle (mcmp2dev_init_batch); each is an "
@@ -213,6 +339,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = args.config
     m = WALKERS[cfg]
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, cfg)
+        return
+
     from paper_2203_05632_b200 import generate_config
 
     tmp = Path(tempfile.mkdtemp(prefix=f"mcmp2_bench_r{rank}_"))
@@ -220,24 +352,14 @@ def main():
     conf_text = conf.read_text()
     ens = max(1, args.ensembles)
     samples_per_step = ens * (m * (m - 1) // 2)
+    strong = args.scaling == "strong"
+    my_steps = worker_share(args.steps, world, rank) if strong else args.steps
+    total_steps = args.steps if strong else args.steps * world
     config = {"workload": f"{cfg}: {WORKLOAD[cfg]}" + (f" x {ens} ensembles per GPU" if ens > 1 else ""),
               "walkers_per_gpu": ens * m, "ensembles_per_gpu": ens, "samples_per_step_per_gpu": samples_per_step,
-              "estimator": "literal (reference estimator.cpp:26-32)", "rng": "reference Philox stream per worker"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        leg = cpu_leg(cfg, spinor, conf_text, args.steps, args.warmup, quick=False)
-        # ms_per_step: host time per step of the workload (one ensemble's C(m,2) samples) at the
-        # measured rate of all cores; the bounded sample behind it is stated in cpu_baseline
-        line = {"metric": METRIC, "value": leg["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * samples_per_step / leg["value"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/c128",
-                "data": "synthetic (seeded, host/generate.cpp)", "config": config,
-                "cpu_baseline": {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": leg["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
+              "estimator": "literal (reference estimator.cpp:26-32)", "rng": "reference Philox stream per worker",
+              "timed_steps": f"{total_steps} in total" + (f", split over {world} ranks by worker_share (driver.cpp:307-309)"
+                                                         if strong and world > 1 else "")}
 
     import numpy as np
     import torch
@@ -278,9 +400,11 @@ def main():
     # warm-up
     dw.advance(args.warmup, keep_on_device=True)
     dw.synchronize()
+    if ens == 1:
+        dw.guard_stats()  # counters from here on
 
-    # ---- timed region: K steps, device time per step on the handle's stream, L2 flushed between ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # ---- timed region: this rank's steps, device time per step on the handle's stream, L2 flushed ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(my_steps)]
     try:
         clk = NvmlClocks(dev)
     except Exception:  # NVML unavailable: fall back to nvidia-smi sampling
@@ -291,7 +415,7 @@ def main():
     torch.cuda.synchronize()
     if clk:
         clk.__enter__()
-    for k in range(args.steps):
+    for k in range(my_steps):
         with torch.cuda.stream(stream):
             flush.zero_()
             ev[k][0].record(stream)
@@ -310,7 +434,7 @@ def main():
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     t_ms = sum(ms_steps)
     t_max = reduce_max(t_ms)
-    value = world * samples_per_step * args.steps / (t_max / 1e3)
+    value = samples_per_step * total_steps / (t_max / 1e3)
 
     # ---- per-kernel device time (profiling pass, events around each launch) ----
     dw.profile(enable=True, reset=True)
@@ -332,7 +456,7 @@ def main():
         return json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
     traffic = traffic_of("pair_kr_kernel" if kramers else "pair_kernel")
 
-    # ---- e2e through the C ABI: one checkpoint interval of K steps with host buffers ----
+    # ---- e2e through the C ABI: one checkpoint interval of this rank's steps with host buffers ----
     dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
     import paper_2203_05632_b200.distributed  # noqa: F401  (module import is setup, not step time)
     st = dw.get_ensembles() if ens > 1 else dw.get_ensemble()
@@ -341,14 +465,62 @@ def main():
         dist.barrier()
     t0 = time.perf_counter()
     (dw.set_ensembles if ens > 1 else dw.set_ensemble)(st)   # H2D walker state (resume)
-    vals, ims = dw.advance(args.steps)                       # every step's (value, imag) D2H
+    vals, ims = dw.advance(my_steps)                         # every step's (value, imag) D2H
     st2 = dw.get_ensembles() if ens > 1 else dw.get_ensemble()  # D2H walker state (checkpoint)
     merged = interval_merge(vals, rank * ens, dist)  # per-worker summaries -> one estimate (driver.cpp:183-196)
     e2e_s = time.perf_counter() - t0
-    e2e_value = world * samples_per_step * args.steps / reduce_max(e2e_s)
+    e2e_value = samples_per_step * total_steps / reduce_max(e2e_s)
     state_bytes = ens * (m * 9 * 8 + 64)
-    h2d = state_bytes / args.steps
-    d2h = 16 * ens + state_bytes / args.steps
+    h2d = state_bytes / max(my_steps, 1)
+    d2h = 16 * ens + state_bytes / max(my_steps, 1)
+    guard = dw.guard_stats() if ens == 1 else None
+    dw.close()
+    del flush
+
+    # ---- strong_run: the fixed total budget of the config split over the ranks, setup included ----
+    strong_run = None
+    budget = STRONG_TOTAL.get(cfg, 0) if args.strong_total_steps is None else args.strong_total_steps
+    if budget > 0 and ens == 1:
+        text = run_config_text(cfg, spinor, conf_text,
+                               f"steps {budget}\nwalkers {m}\nworkers {world}\nseed 1\nburnin {args.burnin}\n"
+                               f"checkpoint-interval {budget}\n")
+        job = engine_job(text, rank, world, dev, dist)
+        secs = reduce_max(job["seconds"])
+        rep = job["report"]
+        strong_run = {"steps_total": budget, "workers": world, "seconds": secs,
+                      "value": samples_per_step * budget / secs, "unit": UNIT,
+                      "includes": "System load, device handle, init_ensemble + burn-in "
+                                  f"{args.burnin}, production, merge (max over ranks, wall clock)",
+                      "E2": rep["value"], "sigma_bar": rep["sigma_bar"]}
+
+    # ---- time to target: sigma_bar/|E| <= target through the stop rule, cfg5 members ----
+    ttt = []
+    for name in [x for x in args.ttt.split(",") if x]:
+        sp5, conf5 = generate_config(name, tmp)
+        c5 = conf5.read_text()
+        m5 = WALKERS[name]
+        text = run_config_text(name, sp5, c5, f"target-rel-err {args.target_rel_err}\nwalkers {m5}\nworkers {world}\n"
+                                              f"seed 1\nburnin {args.burnin}\ncheckpoint-interval 100\n")
+        job = engine_job(text, rank, world, dev, dist)
+        secs = reduce_max(job["seconds"])
+        rep = job["report"]
+        entry = {"config": name, "workload": WORKLOAD[name], "target_rel_err": args.target_rel_err, "seconds": secs,
+                 "steps": rep["total_steps"], "stopped_on_target": rep["stopped_on_target"], "E2": rep["value"],
+                 "sigma_bar": rep["sigma_bar"], "rel_err": rep["sigma_bar"] / abs(rep["value"]) if rep["value"] else None,
+                 "checkpoint_interval": 100, "workers": world,
+                 "includes": f"System load, device handle, init + burn-in {args.burnin}, production to the stop rule"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            import oracle_py
+            threads = os.cpu_count() or 1
+            fit = cpu_full_step(cpu_steps(oracle_py.OracleSystem(sp5, c5), name, m5, 3, threads), m5 * (m5 - 1) // 2)
+            per_worker = -(-rep["total_steps"] // threads)
+            entry["cpu_extrapolated"] = {
+                "seconds": per_worker * fit["t_full"], "cores": threads, "kind": "port",
+                "basis": f"the device run's {rep['total_steps']} steps spread over {threads} CPU workers "
+                         f"({per_worker} steps each) x the extrapolated full-step time {fit['t_full']:.2f} s per worker "
+                         f"(bounded samples at rows {fit.get('rows')}, fit residual "
+                         f"{100 * fit.get('fit_residual_rel', 0):.1f}%); burn-in not counted"}
+        ttt.append(entry)
 
     if rank != 0:
         if dist:
@@ -371,6 +543,13 @@ def main():
         n = oz["steps"]
         vg_ms, sl_ms, kr_ms = oz["vgemm_ms"] / n, oz["slice_ms"] / n, oz["pair_kr_ms"] / n
         a8 = oz["vgemm_int8_ops"] / (vg_ms / 1e3) / 1e12
+        equiv = {k: v for k, v in fp64_view.items() if k not in ("frac", "peak", "peak_source")}
+        equiv.update(kernel="pair stage: oz_slice_kernel + pair_kr_kernel (O blocks, DMMA) + oz_vgemm_kernel (V "
+                            "blocks, INT8, contraction fused) + the guard's refinement / DMMA launches",
+                     dmma_peak=peak, ratio_to_dmma_peak=achieved / peak,
+                     note="throughput-equivalent, not a roofline fraction: the reference's FP64 operation count over "
+                          "the pair stage's time; the kernels do fewer FP64 operations (V blocks as exact int8 "
+                          "products, O blocks with 3M complex products on the Kramers alpha rows)")
         roofline = {
             "bound": "tensor", "kernel": "oz_vgemm_kernel (tcgen05.mma kind::i8: the V blocks as 6-slice Ozaki "
                                          "sums of exact int8 products, pair_oz.cu)",
@@ -381,11 +560,7 @@ def main():
             "frac_of_shape_ceiling": a8 / INT8_SHAPE_CEILING,
             "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
             "vgemm_share_of_step": vg_ms / step_ms_prof,
-            "pair_stage_fp64": dict(fp64_view, kernel="pair stage: oz_slice_kernel + oz_vgemm_kernel + pair_kr_kernel "
-                                    "(literal: O blocks by DMMA, V blocks by INT8 with the contraction fused into the V-GEMM epilogue)", why_frac_above_1=(
-                "the pair stage computes the reference's FP64 contraction with fewer FP64 operations: the V blocks "
-                "(~90% of the work) as exact int8 tensor products (Ozaki splitting, pair_oz.cu), the O blocks by DMMA "
-                "with 3M complex products on the Kramers alpha rows (pair_kr.cu)"))}
+            "pair_stage_throughput_equivalent": equiv}
     else:
         roofline = dict(fp64_view, bound="tensor",
                         executed_tflops=work["pair_dmma_flop_executed"] / (pair_ms / 1e3) / 1e12,
@@ -397,24 +572,34 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64/c128", "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
+        "ms_per_step": t_max / max(my_steps, 1), "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": DTYPE if int8_path else "f64/c128",
+        "data": "synthetic (seeded SPINOR-TEXT from host/generate.cpp; no public dataset)",
         "config": dict(config, parallelism=f"{world * ens} independent workers ({ens} per GPU)",
                        l2="flushed between timed steps (256 MiB write on the handle's stream)"),
-"roofline": roofline,
+        "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "mcmp2dev_set_ensemble + mcmp2dev_advance(K, host values) + mcmp2dev_get_ensemble"
                         " + interval merge (all_gather of per-rank summaries, merge_estimates)",
                 "merged": merged},
-        # per step: walk_kernel, chi_kernel, mo_kernel, [oz_slice_kernel, oz_vgemm_kernel,] pair kernel
-        "gpu_launches": (6 if int8_path else 4) * args.steps,
+        # per step: walk_kernel, chi_kernel, mo_kernel, then the pair stage: INT8 path oz_slice_kernel,
+        # pair_kr_kernel_pw4 (O), oz_vgemm_kernel, the guard's refinement and DMMA launches (both exit at
+        # once unless the step failed its check); DMMA path one pair kernel
+        "gpu_launches": (8 if int8_path else 4) * my_steps,
         "step_values_checksum": float(np.sum(vals)),
     }
+    if guard is not None:
+        line["guard"] = dict(guard, note="INT8 steps checked / refined (7th slice) / recomputed on DMMA over the "
+                                         "e2e interval; max_est_rel = largest estimated relative error of a kept step")
+    if strong_run:
+        line["strong_run"] = strong_run
+    if ttt:
+        line["time_to_target"] = ttt
     cl = clk.summary() if clk else clocks_summary(tmp / "clocks.csv", dev)
     if cl:
         line["clocks"] = cl
     if world == 1 and not args.no_cpu_baseline:
-        leg = cpu_leg(cfg, spinor, conf_text, steps=1, warmup=0, quick=False)
+        leg = cpu_leg(cfg, spinor, conf_text, nsteps=3)
         line["cpu_baseline"] = {k: leg[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
     if dist:
