@@ -167,7 +167,7 @@ def peaks():
 # bounded CPU samples: a step restricted to walker rows [0, r) of the pair loop (the Metropolis
 # sweep and the spinor values always cover all 2m points), at three row counts
 SAMPLE_ROWS = {"cfg3": (8, 32, 128), "cfg4": (4, 16, 64)}
-SAMPLE_ROWS.update({f"cfg5-{n}": (1, 2, 4) for n in (2, 10, 18, 36, 54, 86)})
+SAMPLE_ROWS.update({f"cfg5-{n}": (4, 32, 128) for n in (2, 10, 18, 36, 54, 86)})
 
 
 def cpu_steps(orc, cfg: str, m: int, nsteps: int, threads: int, seed0: int = 1) -> list:
@@ -283,6 +283,12 @@ def reference_arm(args, cfg: str) -> None:
     print(json.dumps(line), flush=True)
 
 
+def trace(msg: str) -> None:
+    """progress markers on stderr (MCMP2_BENCH_TRACE=1), rank-tagged"""
+    if os.environ.get("MCMP2_BENCH_TRACE"):
+        print(f"[bench r{os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_config_text(cfg: str, spinor: Path, conf_text: str, extra: str) -> str:
     """A reference run config (driver.cpp:65-121) for the generated system: the generator's
     weight lines plus the run-control keys of `extra`."""
@@ -290,7 +296,7 @@ def run_config_text(cfg: str, spinor: Path, conf_text: str, extra: str) -> str:
     return f"spinors {spinor}\n" + keep + extra
 
 
-def engine_job(text: str, rank: int, world: int, dev: int, dist) -> dict:
+def engine_job(text: str, rank: int, world: int, dev: int, dist, max_intervals: int | None = None) -> dict:
     """One fixed job through the host Engine's per-rank group (include/mcmp2host.h mcmp2h_group:
     System load, device handle, init_ensemble + burn-in at creation) and the distributed driver's
     interval merges (distributed.py drive_group, driver.cpp:376-420); wall time from a barrier
@@ -305,7 +311,7 @@ def engine_job(text: str, rank: int, world: int, dev: int, dist) -> dict:
     t0 = time.perf_counter()
     group = D.HostGroup(text, first, count, dev)
     rep = D.drive_group(group, rc["workers"], rc["steps"], rc["target"], rc["interval"],
-                        D.torch_all_gather(dist) if dist else (lambda a: [a]))
+                        D.torch_all_gather(dist) if dist else (lambda a: [a]), max_intervals=max_intervals)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     group.close()
@@ -328,6 +334,9 @@ def main():
     ap.add_argument("--ttt", default="cfg5-10,cfg5-2",
                     help="cfg5 members timed to 1%% relative error (comma list; empty skips)")
     ap.add_argument("--target-rel-err", type=float, default=0.01)
+    ap.add_argument("--ttt-max-steps", type=int, default=12000,
+                    help="cap on a time_to_target run's total steps (all workers); a capped run reports "
+                         "stopped_on_target false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ensembles", type=int, default=1,
                     help="reference workers per GPU, batched in one handle (mcmp2dev_init_batch); each is an "
@@ -397,6 +406,7 @@ def main():
     stream = torch.cuda.ExternalStream(dw.stream_ptr, device=torch.device("cuda", dev))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
 
+    trace("setup done")
     # warm-up
     dw.advance(args.warmup, keep_on_device=True)
     dw.synchronize()
@@ -436,6 +446,7 @@ def main():
     t_max = reduce_max(t_ms)
     value = samples_per_step * total_steps / (t_max / 1e3)
 
+    trace("timed region done")
     # ---- per-kernel device time (profiling pass, events around each launch) ----
     dw.profile(enable=True, reset=True)
     nprof = max(2, min(args.steps, 5))
@@ -456,6 +467,7 @@ def main():
         return json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
     traffic = traffic_of("pair_kr_kernel" if kramers else "pair_kernel")
 
+    trace("profile done")
     # ---- e2e through the C ABI: one checkpoint interval of this rank's steps with host buffers ----
     dw.prepare()  # graph capture is setup (as in the host Engine after burn-in), not step time
     import paper_2203_05632_b200.distributed  # noqa: F401  (module import is setup, not step time)
@@ -477,6 +489,7 @@ def main():
     dw.close()
     del flush
 
+    trace("e2e done")
     # ---- strong_run: the fixed total budget of the config split over the ranks, setup included ----
     strong_run = None
     budget = STRONG_TOTAL.get(cfg, 0) if args.strong_total_steps is None else args.strong_total_steps
@@ -493,6 +506,7 @@ def main():
                                   f"{args.burnin}, production, merge (max over ranks, wall clock)",
                       "E2": rep["value"], "sigma_bar": rep["sigma_bar"]}
 
+    trace("strong_run done")
     # ---- time to target: sigma_bar/|E| <= target through the stop rule, cfg5 members ----
     ttt = []
     for name in [x for x in args.ttt.split(",") if x]:
@@ -501,13 +515,15 @@ def main():
         m5 = WALKERS[name]
         text = run_config_text(name, sp5, c5, f"target-rel-err {args.target_rel_err}\nwalkers {m5}\nworkers {world}\n"
                                               f"seed 1\nburnin {args.burnin}\ncheckpoint-interval 100\n")
-        job = engine_job(text, rank, world, dev, dist)
+        interval = 100
+        job = engine_job(text, rank, world, dev, dist, max_intervals=-(-args.ttt_max_steps // (interval * world)))
         secs = reduce_max(job["seconds"])
         rep = job["report"]
+        trace(f"ttt {name}: {rep['total_steps']} steps, {secs:.1f} s, on target {rep['stopped_on_target']}")
         entry = {"config": name, "workload": WORKLOAD[name], "target_rel_err": args.target_rel_err, "seconds": secs,
                  "steps": rep["total_steps"], "stopped_on_target": rep["stopped_on_target"], "E2": rep["value"],
                  "sigma_bar": rep["sigma_bar"], "rel_err": rep["sigma_bar"] / abs(rep["value"]) if rep["value"] else None,
-                 "checkpoint_interval": 100, "workers": world,
+                 "checkpoint_interval": interval, "workers": world, "max_steps": args.ttt_max_steps,
                  "includes": f"System load, device handle, init + burn-in {args.burnin}, production to the stop rule"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             import oracle_py
@@ -522,6 +538,7 @@ def main():
                          f"{100 * fit.get('fit_residual_rel', 0):.1f}%); burn-in not counted"}
         ttt.append(entry)
 
+    trace("ttt done")
     if rank != 0:
         if dist:
             dist.destroy_process_group()
