@@ -324,6 +324,18 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
 // pair terms from f + df and the step's sums, and re-checks them with the estimate scaled by
 // 2^-7; a step that still fails goes on to the DMMA kernel (oz_trip = 2). The accumulator is
 // small, so six tiles rotate through TMEM and the drain never stalls the MMAs.
+#ifdef OZ_TIMELINE
+// debug build (tools/oz_timeline.py): clock64 stamps per CTA and tile -- MMA thread: wait for the
+// accumulators, accumulators acquired, last commit issued; each epilogue warp: accumulators full,
+// released, tile finished
+constexpr int TL_TILES = 128;
+__device__ unsigned long long g_oz_tl[160][TL_TILES][3 + 3 * EPW];
+#define TL(t, k, v) \
+  if ((t) < TL_TILES) g_oz_tl[blockIdx.x][t][k] = (v)
+#else
+#define TL(t, k, v)
+#endif
+
 template <bool FUSED, bool CORR>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   using Sh = OzShape<FUSED, CORR>;
@@ -348,9 +360,12 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   __shared__ uint32_t tmem_base;
   __shared__ double s_red[EPW][6];
   __shared__ bool s_last;
+  // FUSED: the f values of the last two tiles, [q 16][p PW] each (written before, read after the
+  // epilogue warps' named barrier; two buffers so one barrier per tile suffices)
+  __shared__ __align__(32) double4 s_f[2][FUSED ? 16 * PW : 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
-  double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums (lanes with row % 8 == 0)
+  double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums
   // FUSED, guard: sums of the squared per-pair error estimates and of |pair term|
   double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
   const bool guard = FUSED && P.pstat != nullptr;
@@ -396,8 +411,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       uint32_t ph = 0;
       for (int it = 0; it < my; ++it) {
         const int slot = it % NSLOT;
+        TL(it, 0, clock64());
         mbar_wait(&tempty[slot], ((it / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
         asm volatile("tcgen05.fence::after_thread_sync;");
+        TL(it, 1, clock64());
         for (int ks = 0; ks < KS; ++ks) {
           mbar_wait(&full[stage], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -420,6 +437,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           if (++stage == NST) stage = 0, ph ^= 1u;
         }
         umma_commit(&tfull[slot]);
+        TL(it, 2, clock64());
       }
     }
   } else {  // epilogue: TMEM lane = A row; this warp's columns [c_lo, c_lo + CPW)
@@ -433,6 +451,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       const int slot = it % NSLOT;
       mbar_wait(&tfull[slot], (it / NSLOT) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) TL(it, 3 + 3 * warp, clock64());
       const uint32_t tbase = tmem + (uint32_t(lq * 32) << 16) + uint32_t(slot * NB + c_lo);
       long long X[CPW];
       auto merge = [&](const uint32_t (&v)[NACC][16], int c0, int n) {
@@ -463,6 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[slot]);  // accumulators free: the next tile's MMAs overlap the work below
+      if (lane == 0) TL(it, 4 + 3 * warp, clock64());
       // main pass: V = X 2^(e_q + e_p - 49); refinement: dV = acc 2^(e_q + e_p - 56)
       const double sr = P.sa_scale[size_t(a) * MA + row] * (CORR ? 0x1p-7 : 1.0);
       const double* sbv = P.sb_scale + size_t(b) * NB + c_lo;
@@ -475,14 +495,24 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
             __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
                    make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
                                 double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
-      } else {
+      } else
+#ifdef OZ_EXP_NO_CONTRACT  // experiment: drain only (the contraction never runs)
+      if (X[0] != 0x7FFFFFFFFFFFFFFll) acc_d += double(X[0] & 1); else
+#endif
+      {
         // literal contraction (estimator.cpp:26-32) on the Kramers alpha rows, as pair_kr's epilogue:
         // f(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) V(q e_q x_alpha; p e_p y),
         // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds
         // Re V (plane 0) or Im V (plane 1) for its (p, e_p, y): partial g = sum_y o_re Re V, or
         // -sum_y o_im Im V, then the four lanes of (x_alpha, plane) add up.
         // o blocks are in pair_kr's 16 x 8 tiles: walker p of this tile is p_g = PW b + p, in pair_kr
-        // tile a (a + 1) + p_g / 8 (none past the triangle row: those pairs are masked below)
+        // tile a (a + 1) + p_g / 8 (none past the triangle row: those pairs are masked below).
+        // FP64 SIMT work runs ~12x slower while tcgen05 MMAs occupy the SM (tools/fp64_vs_umma.cu).
+        // An exact integer form of sum_y o_y V_y (53-bit mantissas aligned per quad, 128-bit
+        // products) was measured slower, 1.60 vs 1.42 ms at cfg4 (1.26 vs 0.85 ms in the refinement
+        // pass): its instruction stream competes with the MMA-issuing warp for issue slots. So the
+        // FP64 form stays and the per-pair terms are packed into whole warps after the named barrier
+        // (1.42 -> 1.35 ms with the guard's estimate; 1.29 ms with no contraction at all).
         const int row_o = (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
         double g[NK];
@@ -504,61 +534,63 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         for (int k = 0; k < NK; ++k) {
           g[k] += __shfl_xor_sync(0xffffffffu, g[k], 1);
           g[k] += __shfl_xor_sync(0xffffffffu, g[k], 2);
-          g[k] *= 2.0;
         }
-        // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1)
-        const int qg = 16 * a + q, pg0 = PW * b + c_lo / 8;
-        // accuracy guard: the INT8 error of each f is modelled per element as a random sum over
-        // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
-        // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
-        // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
-        // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
-        // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
-        // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
-        // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
-        // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
-        // (one more slice and diagonal) the same model with 2^-49.
-        constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
-        double4 Sc = make_double4(0, 0, 0, 0), Sd = Sc;
-        if (guard && (row & 7) == 0 && qg < P.m) {
-          Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
-          Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
-        }
+        // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1) and park the tile's f
+        // values in shared memory; the per-pair terms are formed below by all epilogue lanes
+        double4* sf = s_f[it & 1];
 #pragma unroll
         for (int p = 0; p < NK / 2; ++p) {
           const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
           const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
-          const int pg = pg0 + p;
-          if ((row & 7) == 0 && qg < P.m && pg < P.m && qg > pg) {
-            // f(0,0) = f1d, f(1,1) = f2d, f(1,0) = f1x, f(0,1) = f2x
-            double F00 = g[2 * p], F11 = f11, F10 = f10, F01 = g[2 * p + 1];
-            double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
-            if constexpr (CORR) {  // f of the main pass plus this pass's corrections
-              const double4 f6 = *fs;
-              F00 += f6.x, F11 += f6.y, F10 += f6.z, F01 += f6.w;
-            } else if (fs) {
-              *fs = make_double4(F00, F11, F10, F01);
-            }
-            const double td = (-P.w_direct * F00) * F11;   // f1d f2d
-            const double tx = (-P.w_exchange * F10) * F01;  // f1x f2x
-            acc_d += td;
-            acc_x += tx;
-            if (guard) {
-              const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
-              const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
-              const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
-              const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
-              const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
-              const double ed = fabs(P.w_direct) * (s1d * fabs(F11) + fabs(F00) * s2d);
-              const double ex = fabs(P.w_exchange) * (s1x * fabs(F01) + fabs(F10) * s2x);
-              acc_ed += ed * ed;
-              acc_ex += ex * ex;
-              acc_ad += fabs(td);
-              acc_ax += fabs(tx);
-            }
+          // f(0,0) = f1d, f(1,1) = f2d, f(1,0) = f1x, f(0,1) = f2x (the factor 2 of 2 Re here)
+          if ((row & 7) == 0) sf[q * PW + c_lo / 8 + p] = make_double4(2.0 * g[2 * p], 2.0 * f11, 2.0 * f10, 2.0 * g[2 * p + 1]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPW) : "memory");  // the tile's 16 x PW f values are parked
+        const int qg0 = 16 * a, pg0 = PW * b;
+        for (int id = (warp * 32 + lane); id < 16 * PW; id += 32 * EPW) {
+          const int q2 = id / PW, p2 = id % PW, qg = qg0 + q2, pg = pg0 + p2;
+          if (!(qg < P.m && pg < P.m && qg > pg)) continue;
+          double4 F = sf[id];
+          double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
+          if constexpr (CORR) {  // f of the main pass plus this pass's corrections
+            const double4 f6 = *fs;
+            F.x += f6.x, F.y += f6.y, F.z += f6.z, F.w += f6.w;
+          } else if (fs) {
+            *fs = F;
+          }
+          const double td = (-P.w_direct * F.x) * F.y;    // f1d f2d
+          const double tx = (-P.w_exchange * F.z) * F.w;  // f1x f2x
+          acc_d += td;
+          acc_x += tx;
+          if (guard) {
+            // accuracy guard: the INT8 error of each f is modelled per element as a random sum over
+            // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
+            // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
+            // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
+            // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
+            // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
+            // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
+            // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
+            // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
+            // (one more slice and diagonal) the same model with 2^-49.
+            constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
+            const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
+            const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
+            const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
+            const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
+            const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
+            const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
+            const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
+            const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
+            const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
+            acc_ed += ed * ed;
+            acc_ex += ex * ex;
+            acc_ad += fabs(td);
+            acc_ax += fabs(tx);
           }
         }
       }
+      if (lane == 0) TL(it, 5 + 3 * warp, clock64());
     }
     if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
       double r[6] = {acc_d, acc_x, acc_ed, acc_ex, acc_ad, acc_ax};
@@ -680,6 +712,14 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   else
     pdl_launch(oz_vgemm_kernel<false, false>, dim3(grid), dim3(THREADS), OzShape<false>::SMEM_BYTES, s, P);
 }
+
+#ifdef OZ_TIMELINE
+}  // namespace mcmp2dev
+extern "C" int mcmp2dev_debug_oz_timeline(void* host, size_t bytes) {
+  return int(cudaMemcpyFromSymbol(host, mcmp2dev::g_oz_tl, bytes < sizeof(mcmp2dev::g_oz_tl) ? bytes : sizeof(mcmp2dev::g_oz_tl)));
+}
+namespace mcmp2dev {
+#endif
 
 void launch_oz_refine(const OzParams& P, cudaStream_t s) {
   int dev = 0;

@@ -1,5 +1,7 @@
 """Profiling driver: a few production steps of one config on cuda:0 (for ncu / sanitizer).
-usage: python tools/prof_step.py [cfg4] [steps] [burnin]"""
+usage: python tools/prof_step.py [cfg4] [steps] [burnin]; MCMP2_GUARD_TOL sets the INT8 path's
+guard tolerance (e.g. 1e-300 forces the refinement and DMMA launches)."""
+import os
 import sys
 import tempfile
 from pathlib import Path
@@ -16,6 +18,8 @@ with tempfile.TemporaryDirectory() as d:
     sp, conf = generate_config(cfg, d)
     m = WALKERS[cfg]
     dw = DeviceWalker(System(sp, conf.read_text()), max_walkers=m)
+    if os.environ.get("MCMP2_GUARD_TOL"):
+        dw.guard(float(os.environ["MCMP2_GUARD_TOL"]))
     dw.init_ensemble(m, seed=1, stream=0)
     dw.burn_in(burn)
     v, im = dw.advance(steps)
