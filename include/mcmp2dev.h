@@ -177,11 +177,15 @@ int mcmp2dev_work_executed(mcmp2dev_t* h, double* pair_dmma_flop);
 int mcmp2dev_synchronize(mcmp2dev_t* h);
 /* the handle's cudaStream_t (as void*), for callers that time or order work around it */
 void* mcmp2dev_stream(mcmp2dev_t* h);
-/* Kramers-restricted pair kernel: detected at create when the spinor columns are exact
- * time-reversal pairs (the only case it is used). mode -1 queries, 0 disables, 1 enables
- * if eligible; returns the active state (1/0). Results agree with the general path to
- * rounding (see csrc/pair_kr.cu). */
+/* Kramers-restricted pair kernel: used when the spinor columns are time-reversal pairs to
+ * within 1e-12 (relative deviation of the pairing relations from max |C|, of the pair energies
+ * from max |eps|; the kernel derives each odd column from its even partner, so results move by
+ * O(deviation)). mode -1 queries, 0 disables, 1 enables if eligible; returns the active state
+ * (1/0). Results agree with the general path to rounding (see csrc/pair_kr.cu). */
 int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
+/* the deviation from exact time-reversal pairing measured at create (+inf: the basis lists or
+ * column counts do not pair) */
+int mcmp2dev_kramers_deviation(const mcmp2dev_t* h, double* deviation);
 /* V blocks of the Kramers pair stage (K = n_vir, ~90% of the pair work) on the INT8 tensor
  * cores: FP64 operands split into six 7-bit slices (Ozaki), exact int8 products summed in
  * int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers

@@ -97,6 +97,7 @@ struct mcmp2dev_handle {
   double ng = 0, lambda = 0, w_direct = 0, w_exchange = 0;
   int estimator = 0;
   bool kramers_eligible = false, kramers = false;  // pair_kr.cu path
+  double kramers_dev = 0.0;                         // deviation from exact time-reversal pairing
   // V blocks of the Kramers pair stage on the INT8 tensor cores (pair_oz.cu), single ensembles
   // of QB = 2 tiles; buffers sized for oz_m walkers, grown outside graph capture (ensure_oz)
   bool oz = true;
@@ -456,37 +457,46 @@ int guard(mcmp2dev_t* h, F&& f) {
   }
 }
 
-// Exact time-reversal pairing of the spinor columns (oracle.cpp:346-355 generalised): channel
-// pairs (0,1) [and (2,3)] carry identical basis lists, columns (2k, 2k+1) satisfy
-// (a, b) -> (-b*, a*) per channel pair bit for bit, and pair energies are equal.
-bool kramers_paired(const mcmp2dev_system* s, const std::vector<int>& ch_off) {
-  if (s->ncomp == 1 || s->n_occ % 2 || s->n_vir % 2) return false;
+// Time-reversal pairing of the spinor columns (oracle.cpp:346-355 generalised): channel pairs
+// (0,1) [and (2,3)] carry identical basis lists, columns (2k, 2k+1) satisfy (a, b) -> (-b*, a*)
+// per channel pair and pair energies are equal. Returns the largest deviation from exact pairing
+// relative to max |C| (coefficients) and max |eps| (energies), or +inf when the structure does
+// not pair (odd counts, basis lists that differ). The Kramers path derives every odd column
+// from its even partner, so a deviation d changes the results by O(d) relative: inputs within
+// kKramersTol use it (a Dirac-Hartree-Fock set paired to rounding, not bit for bit).
+constexpr double kKramersTol = 1e-12;
+double kramers_deviation(const mcmp2dev_system* s, const std::vector<int>& ch_off) {
+  const double inf = HUGE_VAL;
+  if (s->ncomp == 1 || s->n_occ % 2 || s->n_vir % 2) return inf;
   const int np = s->n_occ + s->n_vir;
-  for (int k = 0; k < np; k += 2)
-    if (s->energies[k] != s->energies[k + 1]) return false;
+  double emax = 0.0, cmax = 0.0, de = 0.0, dc = 0.0;
+  for (int k = 0; k < np; ++k) emax = std::max(emax, std::fabs(s->energies[k]));
+  for (int k = 0; k < np; k += 2) de = std::max(de, std::fabs(s->energies[k] - s->energies[k + 1]));
+  for (int i = 0; i < 2 * ch_off[s->ncomp] * np; ++i) cmax = std::max(cmax, std::fabs(s->coeff[i]));
   for (int pr = 0; pr < s->ncomp / 2; ++pr) {
     const int a0 = ch_off[2 * pr], b0 = ch_off[2 * pr + 1], n = ch_off[2 * pr + 1] - ch_off[2 * pr];
-    if (ch_off[2 * pr + 2] - b0 != n) return false;
+    if (ch_off[2 * pr + 2] - b0 != n) return inf;
     for (int i = 0; i < n; ++i) {
       const int fa = a0 + i, fb = b0 + i;
       for (int d = 0; d < 3; ++d)
-        if (s->fn_center[3 * fa + d] != s->fn_center[3 * fb + d]) return false;
-      if (s->fn_lm[2 * fa] != s->fn_lm[2 * fb] || s->fn_lm[2 * fa + 1] != s->fn_lm[2 * fb + 1]) return false;
+        if (s->fn_center[3 * fa + d] != s->fn_center[3 * fb + d]) return inf;
+      if (s->fn_lm[2 * fa] != s->fn_lm[2 * fb] || s->fn_lm[2 * fa + 1] != s->fn_lm[2 * fb + 1]) return inf;
       const int pa = s->fn_prim_offset[fa], pb = s->fn_prim_offset[fb];
       const int na = s->fn_prim_offset[fa + 1] - pa;
-      if (s->fn_prim_offset[fb + 1] - pb != na) return false;
+      if (s->fn_prim_offset[fb + 1] - pb != na) return inf;
       for (int q = 0; q < na; ++q)
         if (s->prim_zeta[pa + q] != s->prim_zeta[pb + q] || s->prim_coeff[pa + q] != s->prim_coeff[pb + q])
-          return false;
+          return inf;
       for (int k = 0; k < np; k += 2) {
         const double* ca = s->coeff + 2 * (size_t(fa) * np + k);  // (a re, a im) of column k
         const double* cb = s->coeff + 2 * (size_t(fb) * np + k);
         // partner column k+1: alpha = -conj(beta_k), beta = conj(alpha_k)
-        if (ca[2] != -cb[0] || ca[3] != cb[1] || cb[2] != ca[0] || cb[3] != -ca[1]) return false;
+        dc = std::max({dc, std::fabs(ca[2] + cb[0]), std::fabs(ca[3] - cb[1]), std::fabs(cb[2] - ca[0]),
+                       std::fabs(cb[3] + ca[1])});
       }
     }
   }
-  return true;
+  return std::max(cmax > 0 ? dc / cmax : dc, emax > 0 ? de / emax : de);
 }
 
 // Basis groups of the MO transform and the coefficient matrix in DMMA B-fragment order
@@ -634,7 +644,8 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   sp.nuniq = int(uz.size());
   sp.uniq_center = dupload(uc.data(), uc.size(), o);
   sp.uniq_zeta = dupload(uz.data(), uz.size(), o);
-  h->kramers_eligible = kramers_paired(s, ch_off);  // literal and physical epilogues both exist
+  h->kramers_dev = kramers_deviation(s, ch_off);
+  h->kramers_eligible = h->kramers_dev <= kKramersTol;  // literal and physical epilogues both exist
   h->kramers = h->kramers_eligible;
   sp.n_occ = h->n_occ;
   sp.n_vir = h->n_vir;
@@ -1327,6 +1338,12 @@ int mcmp2dev_set_ensemble_at(mcmp2dev_t* h, int ens, const mcmp2dev_ensemble* e)
     st.spec_error_idx = INT_MAX;
     ck(scopy(h->stream, h->d_state + ens, &st, sizeof st, cudaMemcpyHostToDevice), "state H2D");
   });
+}
+
+int mcmp2dev_kramers_deviation(const mcmp2dev_t* h, double* deviation) {
+  if (!h || !deviation) return MCMP2DEV_INVALID_ARGUMENT;
+  *deviation = h->kramers_dev;
+  return MCMP2DEV_OK;
 }
 
 int mcmp2dev_kramers(mcmp2dev_t* h, int mode) {

@@ -103,6 +103,7 @@ def dev() -> C.CDLL:
         d.mcmp2dev_replay_ex.argtypes = [vp, ip, C.c_long, dp, dp, C.POINTER(StepEx)]
         d.mcmp2dev_guard.argtypes = [vp, C.c_double, dp]
         d.mcmp2dev_guard_stats.argtypes = [vp, dp]
+        d.mcmp2dev_kramers_deviation.argtypes = [vp, dp]
         _dev = d
     return _dev
 

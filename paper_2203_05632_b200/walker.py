@@ -258,6 +258,12 @@ class DeviceWalker:
         """Kramers-restricted pair kernel: -1 query, 0 off, 1 on when eligible."""
         return bool(self._d.mcmp2dev_kramers(self._h, mode))
 
+    def kramers_deviation(self) -> float:
+        """Deviation of the spinor columns from exact time-reversal pairing (inf: no pairing)."""
+        d = C.c_double()
+        check_dev(self._d.mcmp2dev_kramers_deviation(self._h, C.byref(d)), self._h)
+        return d.value
+
     def int8_v(self, mode: int = -1) -> bool:
         """V blocks of the Kramers pair stage on the INT8 tensor cores (Ozaki slices,
         csrc/pair_oz.cu): -1 query, 0 DMMA, 1 INT8 (default). True when selected and eligible;
