@@ -558,7 +558,7 @@ def main():
                  "step_ms_profiled": step_ms_prof}
     if int8_path:
         n = oz["steps"]
-        vg_ms, sl_ms, kr_ms = oz["vgemm_ms"] / n, oz["slice_ms"] / n, oz["pair_kr_ms"] / n
+        vg_ms, sl_ms, kr_ms, gd_ms = oz["vgemm_ms"] / n, oz["slice_ms"] / n, oz["pair_kr_ms"] / n, oz["guard_ms"] / n
         a8 = oz["vgemm_int8_ops"] / (vg_ms / 1e3) / 1e12
         equiv = {k: v for k, v in fp64_view.items() if k not in ("frac", "peak", "peak_source")}
         equiv.update(kernel="pair stage: oz_slice_kernel + pair_kr_kernel (O blocks, DMMA) + oz_vgemm_kernel (V "
@@ -576,6 +576,7 @@ def main():
             "peak_source": INT8_PEAK_SOURCE, "shape_ceiling": INT8_SHAPE_CEILING,
             "frac_of_shape_ceiling": a8 / INT8_SHAPE_CEILING,
             "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
+            "guard_ms_per_step": gd_ms,
             "vgemm_share_of_step": vg_ms / step_ms_prof,
             "pair_stage_throughput_equivalent": equiv}
     else:

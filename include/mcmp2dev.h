@@ -164,7 +164,8 @@ int mcmp2dev_replay_ex(mcmp2dev_t* h, int m, long nsteps, const double* walkers,
 int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out);
 /* The pair stage's kernels on the INT8 V path, accumulated like mcmp2dev_profile (same enable
  * and reset): out[0..2] = ms of {oz_slice_kernel, oz_vgemm_kernel, pair_kr_kernel}, out[3] =
- * profiled steps that took the path, out[4] = int8 tensor ops of the last V-GEMM launch. */
+ * profiled steps that took the path, out[4] = int8 tensor ops of the last V-GEMM launch,
+ * out[5] = ms of the accuracy guard's refinement and DMMA launches (literal estimator). */
 int mcmp2dev_profile_pair(mcmp2dev_t* h, double* out);
 /* Algorithmic work of one step at the current m: FLOP of the pair stage
  * (C(m,2) * F_pair) and of the spinor stage (2m * 4 * R * n_p), bytes written to Phi. */

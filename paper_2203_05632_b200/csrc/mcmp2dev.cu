@@ -143,8 +143,9 @@ struct mcmp2dev_handle {
   // profiling
   bool prof = false;
   cudaEvent_t ev[4]{};
-  cudaEvent_t ev_oz[2]{};                   // after oz_slice_kernel, after oz_vgemm_kernel
-  double prof_oz[4] = {0, 0, 0, 0};          // ms of slice, V-GEMM, pair_kr (INT8 V path), launches
+  cudaEvent_t ev_oz[3]{};                   // after oz_slice_kernel, before / after oz_vgemm_kernel
+  double prof_oz[5] = {0, 0, 0, 0, 0};       // ms of slice, V-GEMM, pair_kr (INT8 V path), launches,
+                                             // the guard's refinement + DMMA launches
   double oz_ops = 0;                         // int8 ops of the last V-GEMM launch
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_n[4] = {0, 0, 0, 0};
@@ -348,6 +349,7 @@ struct mcmp2dev_handle {
         }
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
         launch_oz_vgemm(o, stream);
+        if (prof) ck(cudaEventRecord(ev_oz[2], stream), "event");
         if (guarded) {  // each exits at once unless the step failed the check before it
           launch_oz_refine(o, stream);
           PairParams f = p_full;
@@ -357,6 +359,7 @@ struct mcmp2dev_handle {
       } else {
         launch_oz_vgemm(o, stream);
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+        if (prof) ck(cudaEventRecord(ev_oz[2], stream), "event");
         p.vtiles = o.v;
         launch_pair_kr(p, stream);
       }
@@ -380,14 +383,16 @@ struct mcmp2dev_handle {
       prof_ms[2] += c;
       prof_ms[3] += a + b + c;
       if (oz_path) {  // slice, then V-GEMM and pair_kr in launch order (fused: pair_kr first)
-        float x = 0, y = 0, z = 0;
+        float x = 0, y = 0, z = 0, gz = 0;
         ck(cudaEventElapsedTime(&x, ev[2], ev_oz[0]), "elapsed");
         ck(cudaEventElapsedTime(&y, ev_oz[0], ev_oz[1]), "elapsed");
-        ck(cudaEventElapsedTime(&z, ev_oz[1], ev[3]), "elapsed");
+        ck(cudaEventElapsedTime(&z, ev_oz[1], ev_oz[2]), "elapsed");
+        ck(cudaEventElapsedTime(&gz, ev_oz[2], ev[3]), "elapsed");
         prof_oz[0] += x;
         prof_oz[1] += fused ? z : y;
-        prof_oz[2] += fused ? y : z;
+        prof_oz[2] += fused ? y : z + gz;
         prof_oz[3] += 1;
+        prof_oz[4] += fused ? gz : 0.0;
       }
       prof_n[0] += 1;
       prof_n[1] += 1;
@@ -1095,7 +1100,8 @@ int mcmp2dev_profile(mcmp2dev_t* h, int enable, int reset, double* out) {
         out[4 + i] = h->prof_n[i];
       }
     if (reset)
-      for (int i = 0; i < 4; ++i) h->prof_ms[i] = h->prof_n[i] = h->prof_oz[i] = 0;
+      for (int i = 0; i < 4; ++i) h->prof_ms[i] = h->prof_n[i] = 0;
+      for (double& x : h->prof_oz) x = 0;
     h->prof = enable != 0;
   });
 }
@@ -1357,6 +1363,7 @@ int mcmp2dev_profile_pair(mcmp2dev_t* h, double* out) {
   return guard(h, [&] {
     for (int i = 0; i < 4; ++i) out[i] = h->prof_oz[i];
     out[4] = h->oz_ops;
+    out[5] = h->prof_oz[4];
   });
 }
 

@@ -237,13 +237,13 @@ class DeviceWalker:
     # -- instrumentation ------------------------------------------------------------
     def profile(self, enable: bool = True, reset: bool = True) -> dict:
         out = np.zeros(8)
-        oz = np.zeros(5)  # the INT8 V path's kernels, read before a reset
+        oz = np.zeros(6)  # the INT8 V path's kernels, read before a reset
         check_dev(self._d.mcmp2dev_profile_pair(self._h, dptr(oz)), self._h)
         check_dev(self._d.mcmp2dev_profile(self._h, int(enable), int(reset), dptr(out)), self._h)
         names = ("walk", "spinor", "pair", "total")
         res = {"ms": dict(zip(names, out[:4])), "launches": dict(zip(names, out[4:].astype(int)))}
         res["int8_v"] = {"slice_ms": oz[0], "vgemm_ms": oz[1], "pair_kr_ms": oz[2], "steps": int(oz[3]),
-                         "vgemm_int8_ops": oz[4]}
+                         "vgemm_int8_ops": oz[4], "guard_ms": oz[5]}
         return res
 
     def work(self) -> dict:

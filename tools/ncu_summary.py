@@ -8,7 +8,9 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-KERNELS = ["oz_vgemm_kernel", "oz_slice_kernel", "pair_kr_kernel", "mo_kernel", "chi_kernel", "walk_kernel"]
+KERNELS = ["oz_vgemm_kernel", "oz_slice_kernel", "pair_kr_kernel", "pair_kr_kernel_pw4", "mo_kernel", "chi_kernel",
+           "walk_kernel"]
+TRAFFIC_NAME = {"pair_kr_kernel_pw4": "pair_kr_kernel"}  # the file bench.py reads for the Kramers path
 WANT = ["gpu__time_duration.sum", "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg.pct_of_peak_sustained_elapsed",
         "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -37,7 +39,7 @@ def main(tag):
             continue
         h, u, v = raw(rep)
         lines.append(f"== {k} ({rep.name}; ncu --set full --clock-control none --import-source on, one steady-state "
-                     f"launch of python tools/prof_step.py cfg4 3 20)")
+                     f"launch of python tools/prof_step.py cfg4 6 20)")
         vals = {}
         for n, uu, x in zip(h, u, v):
             if n in WANT:
@@ -55,13 +57,16 @@ def main(tag):
                                                  f"{a / tot * 100:.1f}%" for a, n in sorted(st, reverse=True)[:6]))
         num = lambda n: float(vals[n][0].replace(",", "")) * SCALE.get(vals[n][1], 1.0)  # noqa: E731
         r, w = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
-        notes = {"pair_kr_kernel": "O chunks of Phi re-read by tile CTAs mostly from L2, plus the V tiles (INT8 path)",
-                 "oz_vgemm_kernel": "slices (113 MB) re-read by tile CTAs mostly from L2; writes are the V tiles (1.08 GB)"}
+        notes = {"pair_kr_kernel_pw4": "O-only pass of the INT8 path: reads the occupied chunks of Phi (mostly from L2); "
+                                       "writes the o tiles (0.49 GB) that oz_vgemm_kernel's epilogue reads",
+                 "oz_vgemm_kernel": "reads: the o tiles (0.49 GB) plus the int8 slices re-read by tile CTAs, partly from L2; "
+                                    "writes: the pair f values for the guard's refinement pass (67 MB) and the partials",
+                 "oz_slice_kernel": "reads Phi (occupied and virtual rows); writes 7 int8 slices per row in the UMMA layout"}
         traffic = {"kernel": k, "config": "cfg4 (m=2048)", "dram_bytes_per_launch": int(r + w),
                    "dram_read_bytes": int(r), "dram_write_bytes": int(w),
                    "source": f"ncu --set full --clock-control none, gpurun_out/{rep.name}, one steady-state launch",
                    "note": notes.get(k, "")}
-        (ROOT / "profiles" / f"traffic_cfg4_{k}.json").write_text(json.dumps(traffic, indent=1) + "\n")
+        (ROOT / "profiles" / f"traffic_cfg4_{TRAFFIC_NAME.get(k, k)}.json").write_text(json.dumps(traffic, indent=1) + "\n")
         details = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"], capture_output=True, text=True,
                                  check=True).stdout
         (ROOT / "profiles" / f"{tag}_{k}_ncu_details.csv").write_text(details)
