@@ -80,8 +80,6 @@ struct PairParams {
                              // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
   double* otiles;            // pair_kr only, single ensemble, literal: write the o blocks of every
                              // tile for oz_vgemm_kernel<true> and skip the V phase and the sums
-  double* onorm;             // pair_kr O-only pass, guarded: [C(m,2)][2] |O(a,c)|_F^2, |O(b,d)|_F^2 of
-                             // each pair q > p (index q (q - 1) / 2 + p), for the guard's estimate
   int guard_fallback;        // pair_kr only: the INT8 path's guard launch -- exit at once unless
                              // st->oz_trip, else recompute the step on DMMA (writes step_out[0..5],
                              // clears oz_trip)
@@ -114,8 +112,7 @@ struct OzParams {
   // accuracy guard (literal estimator): per-point stats from oz_slice_kernel, the step's
   // estimated INT8 error against guard_tol (<= 0: no guard)
   int n_occ;
-  double* pstat;             // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, 0, 0
-  const double* onorm;       // [C(m,2)][2] squared o-block norms from the O pass
+  double* pstat;             // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, N = |Phi_o(pt)|_F, 0
   double guard_tol;
   double* fstore;            // [C(m,2)][4] f(0,0), f(1,1), f(1,0), f(0,1) of each pair q > p (index
                              // q (q - 1) / 2 + p), written by the main pass for the refinement pass

@@ -110,7 +110,6 @@ struct mcmp2dev_handle {
   double guard_tol = kGuardTol;
   double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
   double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
-  double* d_onorm = nullptr;  // [C(oz_m, 2)][2] squared o-block norms (O pass) for the estimate
   long long guard_steps = 0, guard_refined = 0, guard_dmma = 0;
   double guard_max_est = 0.0;  // largest estimated relative error of a step kept on INT8
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
@@ -222,14 +221,13 @@ struct mcmp2dev_handle {
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
-                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_onorm})
+                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore})
       if (p) cudaFree(p);
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     oz_otiles = nullptr;
     d_pstat = nullptr;
     d_fstore = nullptr;
-    d_onorm = nullptr;
     oz_m = 0;
   }
   // captured steps hold the addresses of every work buffer: any reallocation drops them first
@@ -266,7 +264,6 @@ struct mcmp2dev_handle {
       ck(cudaMalloc(&oz_otiles, sizeof(double) * 4096 * ntiles), "cudaMalloc oz o blocks");
       const size_t mq = size_t(16) * nbq;
       ck(cudaMalloc(&d_fstore, sizeof(double) * 4 * (mq * (mq - 1) / 2)), "cudaMalloc oz pair f values");
-      ck(cudaMalloc(&d_onorm, sizeof(double) * 2 * (mq * (mq - 1) / 2)), "cudaMalloc oz o-block norms");
     }
     ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
     ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
@@ -339,12 +336,10 @@ struct mcmp2dev_handle {
       o.pstat = guarded ? d_pstat : nullptr;
       o.guard_tol = guard_tol;
       o.fstore = guarded ? d_fstore : nullptr;
-      o.onorm = guarded ? d_onorm : nullptr;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
         p.otiles = oz_otiles;
-        p.onorm = guarded ? d_onorm : nullptr;
         if (OZ_O_PW4) {
           const int wmax = std::min(KC4, std::max(Go, 1));
           pair_kr_ring_pw4(wmax, p.ring, p.ring_doubles);

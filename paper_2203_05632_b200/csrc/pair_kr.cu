@@ -310,25 +310,14 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int n = 0; n < NB1; ++n) {
-              const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
-              double nrm = 0.0;
+            for (int n = 0; n < NB1; ++n)
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
+                const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
                 double* d = ot + (q * 4 + j * 2) * 64 + (p * 2 + e1) * 4 + y;
-                const double ore = t1[h][n][j] + t2[h][n][j], oim = -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]);
-                __stcg(d, ore);
-                __stcg(d + 64, oim);
-                nrm += ore * ore + oim * oim;
+                __stcg(d, t1[h][n][j] + t2[h][n][j]);
+                __stcg(d + 64, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]));
               }
-              if (P.onorm) {  // |O_block|_F^2 = 2 sum over the alpha rows (Kramers), summed over y lanes
-                nrm += __shfl_xor_sync(0xffffffffu, nrm, 4);
-                nrm += __shfl_xor_sync(0xffffffffu, nrm, 8);
-                const int qg = q0 + q, pg = p0 + p;
-                if (y == 0 && qg < P.m && pg < qg)
-                  P.onorm[(size_t(qg) * (qg - 1) / 2 + pg) * 2 + e1] = 2.0 * nrm;
-              }
-            }
           continue;
         }
         if constexpr (OBUF == 1) consumer_barrier(q1w);  // the group is done reading the previous o rows

@@ -170,13 +170,14 @@ __device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of
 // HELD: n_vir <= 384 (at most 3 quads per lane): one load pass, the values held in registers
 // across the row-maximum reduction (3x the loads in flight); otherwise two passes (max, digits).
 // With P.pstat (the accuracy guard of the literal path) each warp also reduces its scaled row's
-// sum of squares and count of digits-relevant entries (|x| 2^-e > 2^-8); the first warp of each
-// point combines the four channels into the point's stats S, A (oz_vgemm_kernel's error model).
+// sum of squares and count of digits-relevant entries (|x| 2^-e > 2^-8) and its channel's share
+// of |Phi_o(pt)|^2; the first warp of each point combines the four channels into the point's
+// stats S, A, N (oz_vgemm_kernel's error model, see there).
 template <bool HELD>
 __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
-  __shared__ double s_st[8][2];
+  __shared__ double s_st[8][3];
   // one warp per (point, channel): 8 warps = 2 points per CTA (npts_oz is a multiple of 32, so
   // every CTA's points exist)
   const int wg = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   int8_t* const sa = P.sa + size_t(qb) * ks_n * A_KSM;
   int8_t* const sb = P.sb + size_t(pb) * ks_n * SL * NB * 32;
   const bool stats = P.pstat != nullptr;
-  double ss = 0.0, nbig = 0.0, row_scale = 1.0;
+  double ss = 0.0, nbig = 0.0, n2 = 0.0, row_scale = 1.0;
   {
     // this lane's spinor quads a0 = 4 (lane + 32 j); two passes over them (the row maximum, then
     // the digits), the second from L1, so no values are held across the reduction
@@ -280,28 +281,49 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
     }
   }
   if (!stats) return;  // uniform over the grid
+  // this channel's share of |Phi_o(pt)|_F^2 (occupied groups; spinors past n_occ skipped)
+  if (live)
+    for (int g = lane; g < P.Go; g += 32) {
+      const double* src = P.phi + ch.offset(g, pt, P.npts_pad);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * g + i < P.n_occ) {
+          const double re = src[(x * 4 + i) ^ swz], im = src[16 + ((x * 4 + i) ^ swz)];
+          n2 += re * re + im * im;
+        }
+    }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     ss += __shfl_xor_sync(0xffffffffu, ss, o);
     nbig += __shfl_xor_sync(0xffffffffu, nbig, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
   }
   const int w = int(threadIdx.x) >> 5;
   if (lane == 0) {
     s_st[w][0] = row_scale;
     s_st[w][1] = row_scale * sqrt(ss * (1.0 / 3.0) + 0.6 * nbig);
+    s_st[w][2] = n2;
   }
   __syncthreads();
   if (lane == 0 && x == 0) {
-    double Sx = 0.0, Ax = 0.0;
+    double Sx = 0.0, Ax = 0.0, N2 = 0.0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       Sx = fmax(Sx, s_st[w + c][0]);
       Ax = fmax(Ax, s_st[w + c][1]);
+      N2 += s_st[w + c][2];
     }
-    reinterpret_cast<double2*>(P.pstat)[2 * pt] = make_double2(Sx, Ax);
+    reinterpret_cast<double4*>(P.pstat)[pt] = make_double4(Sx, Ax, sqrt(N2), 0.0);
   }
 }
 
+// CORR (FUSED only): the guard's refinement pass. A step whose error estimate failed in the main
+// pass (st->oz_trip == 1) gets the next slice diagonal, d = s + t = 6 (seven products per k-step,
+// the 7th slices included), in one int32 accumulator per tile: dV = acc 2^(e_q + e_p - 56). The
+// main pass stored each pair's f values (P.fstore); this pass adds df = sum o dV, re-forms the
+// pair terms from f + df and the step's sums, and re-checks them with the estimate scaled by
+// 2^-7; a step that still fails goes on to the DMMA kernel (oz_trip = 2). The accumulator is
+// small, so six tiles rotate through TMEM and the drain never stalls the MMAs.
 #ifdef OZ_TIMELINE
 // debug build (tools/oz_timeline.py): clock64 stamps per CTA and tile -- MMA thread: wait for the
 // accumulators, accumulators acquired, last commit issued; each epilogue warp: accumulators full,
@@ -314,13 +336,6 @@ __device__ unsigned long long g_oz_tl[160][TL_TILES][3 + 3 * EPW];
 #define TL(t, k, v)
 #endif
 
-// CORR (FUSED only): the guard's refinement pass. A step whose error estimate failed in the main
-// pass (st->oz_trip == 1) gets the next slice diagonal, d = s + t = 6 (seven products per k-step,
-// the 7th slices included), in one int32 accumulator per tile: dV = acc 2^(e_q + e_p - 56). The
-// main pass stored each pair's f values (P.fstore); this pass adds df = sum o dV, re-forms the
-// pair terms from f + df and the step's sums, and re-checks them with the estimate scaled by
-// 2^-7; a step that still fails goes on to the DMMA kernel (oz_trip = 2). The accumulator is
-// small, so six tiles rotate through TMEM and the drain never stalls the MMAs.
 template <bool FUSED, bool CORR>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   using Sh = OzShape<FUSED, CORR>;
@@ -552,17 +567,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
             // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
             // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
             // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
-            // with the o block's Frobenius norm from the O pass: eps = |w| (sigma_f1 |f2| + |f1|
-            // sigma_f2), sigma_f = |o|_F sigma, per pair, summed in quadrature over the step (the
-            // last CTA compares sqrt(sum eps^2) with guard_tol |sum|). On the oracle's cfg3/cfg4
-            // steps this estimate is 3-60x the actual error (tests/test_oz_guard_model.py); it is a
-            // model, not a bound. After the refinement pass (one more slice and diagonal) the same
-            // model with 2^-49.
+            // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
+            // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
+            // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
+            // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
+            // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
+            // (one more slice and diagonal) the same model with 2^-49.
             constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
-            const double2* ps = reinterpret_cast<const double2*>(P.pstat);
-            const double2 Sc = ps[4 * qg], Sd = ps[4 * qg + 2], Sa = ps[4 * pg], Sb = ps[4 * pg + 2];
-            const double2 on = reinterpret_cast<const double2*>(P.onorm)[size_t(qg) * (qg - 1) / 2 + pg];
-            const double nac = kSig * sqrt(on.x), nbd = kSig * sqrt(on.y);
+            const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
+            const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
+            const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
+            const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
+            const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
             const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
             const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
             const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
