@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // (tcgen05.cp 128x256b per slice and k-step, MMA with [a_tmem]): exact, but 1.89 vs 1.59 ms
   // (tools/oz_gemm.cu -DA_TMEM). At N = 80 (same-box A/B, V-GEMM ms): 3 / 4 / 5 ring stages
   // 1.333 / 1.335 / 1.335; 4 epilogue warps 1.482 vs 8 warps 1.335 (the drain is the epilogue
-  // warps' instruction latency while the MMA waits for TMEM).
+  // warps' instruction latency while the MMA waits for TMEM). Round 2: a diagonal-major drain
+  // releasing each diagonal at once, with the next tile's first k-step issued diagonal by
+  // diagonal, 1.475 vs 1.35 ms (tile period 30.5k vs 28.75k cycles: TMEM reads under the
+  // restarted MMAs slow both).
   __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[NSLOT], tempty[NSLOT];
   __shared__ uint32_t tmem_base;
   __shared__ double s_red[EPW][6];
