@@ -145,17 +145,28 @@ int oz_tiles(int nbq, int pw) {
 // all steps exact in FP64). Rounded digits are centred and, after the first, mostly |d| <= 64:
 // on the oracle's cfg3 inputs the step's exchange sum is 20x closer to FP64 than with truncated
 // digits (7e-12 vs 1.2e-10 relative), at the same 21 products (tests/test_ozaki_budget.py)
+// Three FP64 operations per digit (the kernel is FP64-issue-bound): t = r 128 + 1.5 2^52 rounds
+// r 128 to the nearest integer (ties to even, as rint) and leaves it in t's low mantissa bits (two's
+// complement), so no rint / clamp / conversion is needed unless the digit must be clamped (only
+// after |x 128| > 127.5); the remainder r 128 - q is exact. Digits identical to the
+// rint / fmin / fmax form.
 __device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[SL]) {
+  constexpr double kRound = 6755399441055744.0;  // 1.5 * 2^52
   double r[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
   for (int s = 0; s < SL; ++s) {
     uint32_t w = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      r[i] *= 128.0;
-      const double q = fmin(fmax(rint(r[i]), -127.0), 127.0);
-      r[i] -= q;
-      w |= (uint32_t(int(q)) & 0xFFu) << (8 * i);
+      const double t = fma(r[i], 128.0, kRound);
+      double qd = t - kRound;
+      int q = __double2loint(t);
+      if (q > 127 || q < -127) {
+        q = q > 0 ? 127 : -127;
+        qd = double(q);
+      }
+      r[i] = fma(r[i], 128.0, -qd);
+      w |= (uint32_t(q) & 0xFFu) << (8 * i);
     }
     out[s] = w;
   }
