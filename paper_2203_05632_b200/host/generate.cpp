@@ -157,8 +157,21 @@ Recipe recipe(const std::string& name) {
                                                   {"Xe", "0.1 0.1 0.8 0.6"},  {"Rn", "0.05 0.6 4.0 0.8"}};
     r.weights = {"weight " + el.at(n) + " " + w.at(el.at(n))};
     r.seed = 0x22030500ull + std::uint64_t(n);
+  } else if (name == "wide") {  // stress set: n_vir 446 > 384 (the INT8 path's two-pass slicing)
+    r.nuclei = {{54.0, o}};
+    even_tempered(r.shells, o, 0, 30, 0.02, 2.0);
+    even_tempered(r.shells, o, 1, 30, 0.03, 2.0);
+    even_tempered(r.shells, o, 2, 26, 0.05, 2.0);
+    r.occ_pairs = 27;
+    r.occ_lo = -1200.0, r.occ_hi = -0.4;
+    r.occ_fixed = false;
+    r.vir_lo = 0.1, r.vir_hi = 1e4;
+    r.walkers = 2048;
+    r.steps = 2000;
+    r.weights = {"weight Xe 0.1 0.1 0.8 0.6"};
+    r.seed = 0x22039001ull;
   } else {
-    throw std::invalid_argument("generate: unknown config '" + name + "' (cfg1..cfg4, cfg5-N)");
+    throw std::invalid_argument("generate: unknown config '" + name + "' (cfg1..cfg4, cfg5-N, syn1c, syn2c, wide)");
   }
   return r;
 }

@@ -122,3 +122,25 @@ def test_int8_v_buffers_grow_after_capture(cfgdir):
     va, _ = a.advance(34)
     vb, _ = b.advance(34)
     assert np.array_equal(va, vb)
+
+
+def test_int8_v_two_pass_slicing_wide_set(tmp_path):
+    """n_vir 446 > 384: oz_slice_kernel's two-pass form (the row maximum, then the digits; no
+    values held across the reduction). Replayed steps against the oracle and the DMMA path,
+    guarded and unguarded (the generator's 'wide' stress set, host/generate.cpp)."""
+    from paper_2203_05632_b200 import generate_config
+    sp, conf = generate_config("wide", tmp_path)
+    text = conf.read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    assert orc.n_vir > 384
+    tr = orc.trajectory(seed=3, stream=0, m=192, burn=20, nsteps=2)
+    dw = DeviceWalker(System(sp, text), max_walkers=192)
+    assert dw.kramers() and dw.int8_v()
+    for tol in (0.0, 2e-10):
+        dw.guard(tol)
+        got = dw.replay(tr["walkers"], tr["tau"])
+        for k in (0, 2, 4):
+            assert rel_err(got[:, k], tr["est"][:, k]) < REL, (tol, k)
+    dw.int8_v(0)
+    dmma = dw.replay(tr["walkers"], tr["tau"])
+    assert rel_err(dmma[:, 0], tr["est"][:, 0]) < REL
