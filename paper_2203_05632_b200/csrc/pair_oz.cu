@@ -67,19 +67,25 @@ constexpr int TMEM_COLS = 512;      // 6 x NB used
 // pair_kr's 16 x 8 tiles) or 10 walkers (80 rows, the fused literal path: a kind::i8 M128 MMA
 // costs the same ~61 cycles for N = 32..80 (tools/umma_rate.cu), so N = 80 -- the widest that
 // fits six accumulators in 512 TMEM columns -- does 25% more work per instruction)
-// CORR: the refinement pass (all SL slices per k-step, one accumulator per tile)
+// CORR: the refinement pass (all SL slices per k-step, one accumulator per P block) on tiles of
+// PB P blocks, so each k-step's A slices serve PB blocks (the pass is bound by the L2 -> SMEM
+// operand stream)
+#ifndef OZ_REFINE_PB
+#define OZ_REFINE_PB 3
+#endif
 template <bool FUSED, bool CORR = false>
 struct OzShape {
   static constexpr int NB = FUSED ? 80 : 64;
-  static constexpr int PW = NB / 8;  // P walkers per tile
+  static constexpr int PW = NB / 8;  // P walkers per P block
+  static constexpr int PB = CORR ? OZ_REFINE_PB : 1;  // P blocks per tile
   static constexpr int B_KSM = SL * NB * 32;  // stored bytes of one k-step of a P block
   static constexpr int NSL = CORR ? SL : S;   // slices copied per k-step
   static constexpr int A_CP = NSL * MA * 32, B_CP = NSL * NB * 32;
-  static constexpr int STAGE = A_CP + B_CP;
-  static constexpr int NSTAGE = CORR ? 4 : STAGES;
+  static constexpr int STAGE = A_CP + PB * B_CP;
+  static constexpr int NSTAGE = CORR ? (227 * 1024 - 16 * 1024) / STAGE : STAGES;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE;
-  static constexpr int NACC = CORR ? 1 : S;   // accumulators per tile (slice diagonals)
-  static constexpr int NSLOT = CORR ? 6 : 1;  // tiles in flight in TMEM
+  static constexpr int NACC = CORR ? 1 : S;   // accumulators per P block (slice diagonals)
+  static constexpr int NSLOT = CORR ? 512 / (PB * NB) : 1;  // tiles in flight in TMEM
   static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
   // instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = NB
   static constexpr uint32_t IDESC =
@@ -87,8 +93,9 @@ struct OzShape {
 };
 static_assert(OzShape<true>::SMEM_BYTES <= 227 * 1024, "stage ring");
 static_assert(OzShape<true, true>::SMEM_BYTES <= 227 * 1024, "stage ring");
-static_assert(OzShape<true>::NACC * OzShape<true>::NB <= 512 && OzShape<true, true>::NSLOT * OzShape<true>::NB <= 512,
-              "TMEM columns");
+static_assert(OzShape<true>::NACC * OzShape<true>::NB <= 512 && OzShape<true, true>::NSLOT >= 2 &&
+                  OzShape<true, true>::NSTAGE >= 2,
+              "TMEM columns / stage ring");
 
 // canonical K-major, no-swizzle UMMA operand layout of one k-step: [row / 8][k / 16][row % 8][16 B]
 __host__ __device__ __forceinline__ int op_off(int r, int kk) {
@@ -137,6 +144,28 @@ struct OzWalk {
 int oz_tiles(int nbq, int pw) {
   int n = 0;
   for (int a = 0; a < nbq; ++a) n += (16 * (a + 1) + pw - 1) / pw;
+  return n;
+}
+// the same triangle in tiles of pb consecutive P blocks (the refinement pass): row a holds
+// ceil(len / pb) of them; a tile's P blocks past the row are skipped
+struct OzGroupWalk {
+  int a = 0, g, pw, pb;
+  __device__ OzGroupWalk(int t0, int pw_, int pb_) : g(t0), pw(pw_), pb(pb_) { settle(); }
+  __device__ int row_blocks() const { return (16 * (a + 1) + pw - 1) / pw; }
+  __device__ int len() const { return (row_blocks() + pb - 1) / pb; }
+  __device__ void settle() {
+    while (g >= len()) g -= len(), ++a;
+  }
+  __device__ void next(int stride) { g += stride, settle(); }
+};
+__device__ int oz_group_tiles_dev(int nbq, int pw, int pb) {
+  int n = 0;
+  for (int a = 0; a < nbq; ++a) n += ((16 * (a + 1) + pw - 1) / pw + pb - 1) / pb;
+  return n;
+}
+int oz_group_tiles(int nbq, int pw, int pb) {
+  int n = 0;
+  for (int a = 0; a < nbq; ++a) n += ((16 * (a + 1) + pw - 1) / pw + pb - 1) / pb;
   return n;
 }
 
@@ -352,7 +381,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   using Sh = OzShape<FUSED, CORR>;
   constexpr int NB = Sh::NB, PW = Sh::PW, STAGE = Sh::STAGE, CPW = Sh::CPW;
   constexpr int A_CP = Sh::A_CP, B_CP = Sh::B_CP, B_KSM = Sh::B_KSM, NST = Sh::NSTAGE;
-  constexpr int NACC = Sh::NACC, NSLOT = Sh::NSLOT;
+  constexpr int NACC = Sh::NACC, NSLOT = Sh::NSLOT, PB = Sh::PB;
   static_assert(!CORR || FUSED, "the refinement pass serves the fused literal path");
   pdl_wait();
   pdl_trigger();
@@ -397,24 +426,25 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  const int ntiles = P.ntiles;
+  const int ntiles = CORR ? oz_group_tiles_dev(P.npts_oz / 32, PW, PB) : P.ntiles;
   const int my = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (warp == EPW) {
     if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
       int stage = 0;
       uint32_t ph = 0;
-      OzWalk w(int(blockIdx.x), PW);
+      OzGroupWalk w(int(blockIdx.x), PW, PB);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
-        const int a = w.a, b = w.b;
+        const int a = w.a, b0 = w.g * PB, nb = min(PB, w.row_blocks() - b0);
         const int8_t* ga = P.sa + size_t(a) * KS * A_KSM;
-        const int8_t* gb = P.sb + size_t(b) * KS * B_KSM;
+        const int8_t* gb = P.sb + size_t(b0) * KS * B_KSM;
         for (int ks = 0; ks < KS; ++ks) {
           mbar_wait(&empty[stage], ph ^ 1u);
           int8_t* dst = sm + stage * STAGE;
-          mbar_expect_tx(&full[stage], STAGE);
+          mbar_expect_tx(&full[stage], A_CP + nb * B_CP);
           bulk_g2s(dst, ga + size_t(ks) * A_KSM, A_CP, &full[stage]);
-          bulk_g2s(dst + A_CP, gb + size_t(ks) * B_KSM, B_CP, &full[stage]);
+          for (int j = 0; j < nb; ++j)
+            bulk_g2s(dst + A_CP + j * B_CP, gb + (size_t(j) * KS + ks) * B_KSM, B_CP, &full[stage]);
           if (++stage == NST) stage = 0, ph ^= 1u;
         }
       }
@@ -423,8 +453,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     if (lane == 0) {  // MMA issuer: the slice products of each k-step into the tile's accumulators
       int stage = 0;
       uint32_t ph = 0;
-      for (int it = 0; it < my; ++it) {
+      OzGroupWalk w(int(blockIdx.x), PW, PB);
+      for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
         const int slot = it % NSLOT;
+        const int nb = min(PB, w.row_blocks() - w.g * PB);
         TL(it, 0, clock64());
         mbar_wait(&tempty[slot], ((it / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -435,10 +467,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           const int8_t* sa = sm + stage * STAGE;
           const int8_t* sb = sa + A_CP;
           if constexpr (CORR) {
+            for (int j = 0; j < nb; ++j)
 #pragma unroll
-            for (int s = 0; s < SL; ++s)  // diagonal 6: (s, 6 - s)
-              umma_i8<Sh::IDESC>(tmem + uint32_t(slot * NB), umma_desc(sa + s * MA * 32),
-                                 umma_desc(sb + (SL - 1 - s) * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
+              for (int s = 0; s < SL; ++s)  // diagonal 6: (s, 6 - s)
+                umma_i8<Sh::IDESC>(tmem + uint32_t((slot * PB + j) * NB), umma_desc(sa + s * MA * 32),
+                                   umma_desc(sb + j * B_CP + (SL - 1 - s) * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
           } else {
 #pragma unroll
             for (int s = 0; s < S; ++s)
@@ -458,15 +491,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     const int lq = warp & 3, c_lo = (warp >> 2) * CPW;
     const int row = lq * 32 + lane;
     const int q = row >> 3, plane = row & 1, exq = (row >> 1) & 3;
-    OzWalk w(int(blockIdx.x), PW);
+    OzGroupWalk w(int(blockIdx.x), PW, PB);
+    int sub = 0;  // P blocks processed: the parity of the shared f buffer
     for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
       const int t = int(blockIdx.x) + it * int(gridDim.x);
-      const int a = w.a, b = w.b;
+      const int a = w.a, nbk = min(PB, w.row_blocks() - w.g * PB);
       const int slot = it % NSLOT;
       mbar_wait(&tfull[slot], (it / NSLOT) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) TL(it, 3 + 3 * warp, clock64());
-      const uint32_t tbase = tmem + (uint32_t(lq * 32) << 16) + uint32_t(slot * NB + c_lo);
+      for (int j = 0; j < nbk; ++j, ++sub) {  // the tile's P blocks in turn (one in the main pass)
+      const int b = w.g * PB + j;
+      const uint32_t tbase = tmem + (uint32_t(lq * 32) << 16) + uint32_t((slot * PB + j) * NB + c_lo);
       long long X[CPW];
       auto merge = [&](const uint32_t (&v)[NACC][16], int c0, int n) {
 #pragma unroll
@@ -494,8 +530,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         merge(v, c0, 8);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&tempty[slot]);  // accumulators free: the next tile's MMAs overlap the work below
+      if (j == nbk - 1) {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(&tempty[slot]);  // accumulators free: the next tile's MMAs overlap the work below
+      }
       if (lane == 0) TL(it, 4 + 3 * warp, clock64());
       // main pass: V = X 2^(e_q + e_p - 49); refinement: dV = acc 2^(e_q + e_p - 56)
       const double sr = P.sa_scale[size_t(a) * MA + row] * (CORR ? 0x1p-7 : 1.0);
@@ -530,17 +568,60 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         const int row_o = (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
         double g[NK];
+        // the refinement pass has too few MMAs to hide the o-tile loads behind: load all of this
+        // thread's o quads for the P block first (one latency instead of NK), then contract
+        constexpr int NPF = CORR ? NK : 1;
+        longlong2 opf[NPF][2];
+        if constexpr (CORR) {
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            const int pg = min(PW * b + (c_lo + 4 * k) / 8, 16 * (a + 1) - 1);
+            const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+            opf[k][0] = __ldcs(reinterpret_cast<const longlong2*>(o));
+            opf[k][1] = __ldcs(reinterpret_cast<const longlong2*>(o + 2));
+          }
+        }
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
           const int pg = PW * b + (c_lo + 4 * k) / 8;
           double sgp = 0.0;
           if (pg < 16 * (a + 1)) {
-            const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
-            const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o));
-            const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 2));
-            const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
-            const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
-            sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+            if constexpr (!CORR) {
+              const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+              const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o));
+              const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 2));
+              const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
+              const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
+              sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+            } else {
+              // the refinement's correction df = sum o dV is ~2^-42 of f, so FP32 carries it with
+              // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
+              // with an integer exponent (read from the bits), terms aligned to the quad's largest
+              // exponent, one conversion and scaling
+              const long long ob[4] = {opf[CORR ? k : 0][0].x, opf[CORR ? k : 0][0].y, opf[CORR ? k : 0][1].x,
+                                       opf[CORR ? k : 0][1].y};
+              int E[4], emax = 0;
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                const int ex = int((ob[y] >> 52) & 0x7FF);  // zero / subnormal o: dropped
+                E[y] = ex ? ex + int((__double_as_longlong(sbv[4 * k + y]) >> 52) & 0x7FF) : 0;
+                emax = max(emax, E[y]);
+              }
+              float acc = 0.0f;
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                const int dsh = E[y] - emax;
+                if (E[y] == 0 || dsh < -120) continue;
+                const float mf = __int_as_float(0x3F800000 | int((ob[y] >> 29) & 0x7FFFFF)) *
+                                 __int_as_float((127 + dsh) << 23);
+                acc = fmaf(ob[y] < 0 ? -mf : mf, __int2float_rn(int(X[4 * k + y])), acc);
+              }
+              if (emax) {  // sum = acc 2^(emax - 2046) sr, sr = 2^(srx - 1023)
+                const int tt = emax + int((__double_as_longlong(sr) >> 52) & 0x7FF) - 3069;
+                const double scale = (tt > -1023 && tt < 1024) ? __longlong_as_double((long long)(tt + 1023) << 52) : ldexp(1.0, tt);
+                sgp = double(acc) * scale;
+              }
+            }
           }
           g[k] = plane ? -sgp : sgp;
         }
@@ -551,7 +632,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
         // lanes row % 8 == 0 (e_q 0) take f(1, e_p) from row + 4 (e_q 1) and park the tile's f
         // values in shared memory; the per-pair terms are formed below by all epilogue lanes
-        double4* sf = s_f[it & 1];
+        double4* sf = s_f[sub & 1];
 #pragma unroll
         for (int p = 0; p < NK / 2; ++p) {
           const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
@@ -604,6 +685,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           }
         }
       }
+      }  // P blocks of the tile
       if (lane == 0) TL(it, 5 + 3 * warp, clock64());
     }
     if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
@@ -739,7 +821,8 @@ void launch_oz_refine(const OzParams& P, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
-  const int grid = P.ntiles < sms ? P.ntiles : sms;
+  const int nt = oz_group_tiles(P.npts_oz / 32, OzShape<true, true>::PW, OzShape<true, true>::PB);
+  const int grid = nt < sms ? nt : sms;
   pdl_launch(oz_vgemm_kernel<true, true>, dim3(grid), dim3(THREADS), OzShape<true, true>::SMEM_BYTES, s, P);
 }
 

@@ -2,7 +2,8 @@
 the MMA issuer's wait for the accumulators and each epilogue warp's drain and contraction, in
 SM cycles. Build: make -C paper_2203_05632_b200/csrc OUT=../lib_tl OBJ=build_tl
 EXTRA_NVFLAGS=-DOZ_TIMELINE && cp paper_2203_05632_b200/lib/libmcmp2host.so paper_2203_05632_b200/lib_tl/
-usage: MCMP2_LIBDIR=paper_2203_05632_b200/lib_tl python tools/oz_timeline.py [cfg4]"""
+usage: MCMP2_LIBDIR=paper_2203_05632_b200/lib_tl python tools/oz_timeline.py [cfg4] [tol]
+(tol 1e-300 forces the guard's refinement pass; its stamps then overwrite the main pass's)"""
 import ctypes as C
 import json
 import sys
@@ -20,7 +21,7 @@ m = {"cfg3": 512, "cfg4": 2048}.get(cfg, 8192)
 with tempfile.TemporaryDirectory() as d:
     sp, conf = generate_config(cfg, d)
     dw = DeviceWalker(System(sp, conf.read_text()), max_walkers=m)
-    dw.guard(1e300)  # estimate only: the refinement pass never runs (and never stamps)
+    dw.guard(float(sys.argv[2]) if len(sys.argv) > 2 else 1e300)  # default: the refinement never runs
     dw.init_ensemble(m, seed=1)
     dw.burn_in(20)
     dw.advance(3)
