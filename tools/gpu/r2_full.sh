@@ -1,14 +1,16 @@
 set -u
 O=gpurun_out
-T=${TAG:-r2p}
+T=${TAG:-r2x}
 timeout 2400 python -m pytest tests -m gpu -q > $O/${T}_pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/${T}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1
 timeout 900 python bench.py > $O/${T}_bench_cfg4.json 2> $O/${T}_bench_cfg4.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $O/${T}_bench_ref.json 2> $O/${T}_bench_ref.err
+for c in cfg3; do timeout 600 python bench.py --config $c --strong-total-steps 0 --ttt "" > $O/${T}_bench_$c.json 2> $O/${T}_bench_$c.err; done
+timeout 1500 python tools/sweep_cfg5.py --max-seconds 60 --out $O/${T}_sweep_cfg5.json > $O/${T}_sweep.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${T}_launches_cfg4.csv \
   python bench.py --steps 4 --warmup 3 --burnin 100 --no-cpu-baseline --strong-total-steps 0 --ttt "" > $O/${T}_ncu_launches.log 2>&1
-for k in oz_vgemm_kernel pair_kr_kernel_pw4 oz_slice_kernel mo_kernel; do
+for k in oz_vgemm_kernel oz_slice_kernel; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 -f \
-    -o $O/${T}_prof_$k python tools/prof_step.py cfg4 6 20 > $O/${T}_ncu_$k.log 2>&1
+    -o $O/prof_${T}_$k python tools/prof_step.py cfg4 6 20 > $O/${T}_ncu_$k.log 2>&1
 done
-ls -la $O | tail -12
+ls -la $O | tail -5
