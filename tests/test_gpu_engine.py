@@ -107,13 +107,17 @@ def test_full_run_matches_oracle_engine(cfgdir, name, extra):
     assert dev["sigma_bar"] == pytest.approx(ref["sigma_bar"], rel=1e-6)
 
 
-def test_independent_rng_runs_agree_within_2_sigma(cfgdir):
+@pytest.mark.parametrize("name,kw", [
+    ("cfg1", {"walkers": 16, "step-size": 0.3, "steps": 4000}),
+    ("cfg2", {"walkers": 16, "workers": 4, "steps": 4000, "burnin": 200}),  # 4c, 10e atom, batched workers
+    ("syn2c", {"walkers": 8, "workers": 2, "steps": 6000}),                 # 2-component set
+])
+def test_independent_rng_runs_agree_within_2_sigma(cfgdir, name, kw):
     """north_star: independent-RNG full runs agree with the reference E(2) within combined 2 sigma
-    (literal estimator). cfg1, 4000 steps, device seed 101 vs oracle seed 202."""
-    dev = parse(walker.run_config_text(small(cfgdir, name="cfg1", walkers=16, **{"step-size": 0.3},
-                                             steps=4000, seed=101)))
-    ref = parse(oracle_py.run_config(small(cfgdir, name="cfg1", walkers=16, **{"step-size": 0.3},
-                                           steps=4000, seed=202)))
+    (literal estimator): the device Engine on seed 101 against the oracle Engine on seed 202."""
+    dev = parse(walker.run_config_text(small(cfgdir, name=name, seed=101, **kw)))
+    ref = parse(oracle_py.run_config(small(cfgdir, name=name, seed=202, **kw)))
+    assert dev["steps"] == ref["steps"] == kw["steps"]
     assert abs(dev["value"] - ref["value"]) <= 2 * math.hypot(dev["sigma_bar"], ref["sigma_bar"])
 
 
