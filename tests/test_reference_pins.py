@@ -77,3 +77,33 @@ def test_engine_runs_match_the_reference(cfgdir, name, extra):
         assert b == pytest.approx(a, rel=1e-12, abs=0)  # each worker's mean I
     assert o["E2"] == pytest.approx(r["E2"], rel=1e-10, abs=0)
     assert o["sigma_bar"] == pytest.approx(r["sigma_bar"], rel=1e-10, abs=0)
+
+
+# the reference's own unit tests (tests/test_{rng,model,weights,greens,estimator,sampler,driver,
+# oracle}.cpp) built against the reference sources here (oracle/build_ref.sh: eigen_subset and
+# doctest_subset stand in for the absent Eigen3 and doctest); three fail for reasons inside the
+# reference, not the build:
+KNOWN_REFERENCE_FAILURES = {
+    # asserts sigma_bar == 0.0 for a constant 0.7 stream; IEEE accumulation gives mean
+    # 0.7000000000000013 against block means 0.7000000000000001 (DESIGN.md findings)
+    "blocking accumulator: hand examples",
+    # runs the he_dz fixture (Z = 2) without a weight line; the default table (weights.cpp:30-38)
+    # has no entry for He, so run() throws "no weight parameters for element Z=2"
+    "merging two independent seeded runs",
+    # expects "energies 2 2" on h2_svp to trip HOMO < LUMO, i.e. bit-equal degenerate orbital
+    # energies from Eigen's eigensolver (any other solver leaves them 1 ulp apart)
+    "spinor file error paths",
+}
+
+
+@pytest.mark.skipif(not (ref_py.REF_LIB.parent / "ref_unit_tests").exists(), reason="ref_unit_tests not built")
+def test_reference_unit_suite_passes_on_this_build(tmp_path):
+    import re
+    import subprocess
+    out = subprocess.run([str(ref_py.REF_LIB.parent / "ref_unit_tests")], cwd=tmp_path, capture_output=True,
+                         text=True, timeout=900).stdout
+    summary = re.search(r"test cases: (\d+) \| passed: (\d+) \| failed: (\d+)", out)
+    assert summary, out[-2000:]
+    total, passed, failed = map(int, summary.groups())
+    failing = {m.group(1) for m in re.finditer(r"^\[FAIL\] (.+) \(/", out, re.M)}
+    assert total >= 100 and failing == KNOWN_REFERENCE_FAILURES, (failing, out[-3000:])
