@@ -9,6 +9,7 @@
 //   ref2_evaluate      SpinorSet::evaluate_into (model.cpp:166-178)
 //   ref2_g             WeightSpec::g (weights.cpp:92-99)
 //   ref2_run_config    run(parse_config_text(text)) + format_report (driver.cpp:477-480, :523-539)
+//   ref2_fixture       the deterministic oracle's fixtures (oracle.cpp: make_fixture, MP2 energy)
 // Errors: return 1 (std::invalid_argument) or 2 (other exceptions), message in ref2_last_error.
 #include <cstdint>
 #include <cstdio>
@@ -23,6 +24,7 @@
 #include "mcmp2/driver.hpp"
 #include "mcmp2/estimator.hpp"
 #include "mcmp2/model.hpp"
+#include "mcmp2/oracle.hpp"
 #include "mcmp2/sampler.hpp"
 #include "mcmp2/weights.hpp"
 
@@ -162,6 +164,16 @@ REF2_API int ref2_g(void* h, const double* pts, int n, double* out) {
   return guarded([&] {
     auto* s = static_cast<RefSystem*>(h);
     for (int i = 0; i < n; ++i) out[i] = s->spec->g(mcmp2::Vec3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+  });
+}
+
+// the reference's deterministic oracle: the fixture's MP2 energy (oracle.cpp, make_fixture) and
+// its SPINOR-TEXT (save_spinor_set), e.g. syn4c
+REF2_API int ref2_fixture(const char* name, const char* spinor_out, double* e2) {
+  return guarded([&] {
+    const mcmp2::Fixture fx = mcmp2::make_fixture(name);
+    *e2 = fx.e2;
+    if (spinor_out && *spinor_out) mcmp2::save_spinor_set(fx.spinors, spinor_out);
   });
 }
 

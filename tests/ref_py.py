@@ -32,6 +32,7 @@ def lib() -> C.CDLL:
         L.ref2_evaluate.argtypes = [vp, dp, ip, dp, dp]
         L.ref2_g.argtypes = [vp, dp, ip, dp]
         L.ref2_run_config.argtypes = [C.c_char_p, C.c_char_p, ip]
+        L.ref2_fixture.argtypes = [C.c_char_p, C.c_char_p, dp]
         _lib = L
     return _lib
 
@@ -93,3 +94,11 @@ def run_config(text: str) -> str:
     buf = C.create_string_buffer(1 << 16)
     _check(lib().ref2_run_config(text.encode(), buf, len(buf)))
     return buf.value.decode()
+
+
+def fixture(name: str, spinor_out=None) -> float:
+    """The reference oracle's fixture (oracle.cpp make_fixture): its deterministic MP2 energy,
+    and its SPINOR-TEXT written to spinor_out when given."""
+    e2 = C.c_double()
+    _check(lib().ref2_fixture(name.encode(), str(spinor_out or "").encode(), C.byref(e2)))
+    return e2.value

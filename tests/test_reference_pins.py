@@ -107,3 +107,16 @@ def test_reference_unit_suite_passes_on_this_build(tmp_path):
     total, passed, failed = map(int, summary.groups())
     failing = {m.group(1) for m in re.finditer(r"^\[FAIL\] (.+) \(/", out, re.M)}
     assert total >= 100 and failing == KNOWN_REFERENCE_FAILURES, (failing, out[-3000:])
+
+
+def test_syn4c_deterministic_energy_matches_the_reference_oracle(tmp_path):
+    """The physical MP2 energy of syn4c that tests/syn4c.py restates (and the device MC
+    converges to in physical mode, tests/test_syn4c.py) against the reference's own deterministic
+    oracle (oracle.cpp make_fixture / oracle_mp2_energy), and the fixture's spinors as the
+    reference writes them against the restated ones."""
+    import syn4c
+    e2 = ref_py.fixture("syn4c", tmp_path / "syn4c_ref.spinor")
+    assert e2 == pytest.approx(-0.003932252921, abs=5e-12)
+    ours = tmp_path / "syn4c_ours.spinor"
+    syn4c.write_spinor_file(ours)
+    assert syn4c.mp2_energy(syn4c.coefficients()) == pytest.approx(e2, rel=1e-9)
