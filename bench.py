@@ -268,6 +268,31 @@ def reference_arm(args, cfg: str) -> None:
                  f"fit t = t0 + c n over the timed steps (t0 {fit['t0_s']:.2f} s, {fit['us_per_sample']:.2f} us/sample per "
                  f"worker, residual {100 * fit['fit_residual_rel']:.1f}%), extrapolated to C(m,2) = {npairs} samples"
                  if fit["extrapolated"] else " of the full pair loop"))
+    # the reference's own code, compiled here against the stand-in dense header (oracle/_ref):
+    # its per-core rate on replayed sub-ensembles beside the port's, for context (its dense algebra
+    # runs on oracle/eigen_subset, not Eigen, so it is not the timed arm)
+    ref_build = None
+    try:
+        import ref_py
+        if ref_py.available():
+            rs = ref_py.RefSystem(spinor, conf_text)
+            tr = orc.trajectory(seed=3, stream=0, m=64, burn=5, nsteps=1)
+            pts = []
+            for msub in (32, 64):
+                w = tr["walkers"][0][:msub]
+                t1 = time.perf_counter()
+                rs.replay(w[None], tr["tau"][:1], pair_sums=False)
+                pts.append((msub, time.perf_counter() - t1))
+            (m1, ta), (m2, tb) = pts
+            pa, pb = m1 * (m1 - 1) / 2, m2 * (m2 - 1) / 2
+            c = (tb - ta) / (pb - pa)  # s per pair sample, one core
+            ref_build = {"samples_per_s_per_core": 1.0 / c, "cores": threads, "value": threads / c,
+                         "port_samples_per_s_per_core": value / threads,
+                         "note": "oracle/_ref/libref_mcmp2.so (the reference's estimator/greens/model sources) "
+                                 "on replayed sub-ensembles of 32 and 64 walkers, one core, pair cost by "
+                                 "difference; dense algebra on the stand-in oracle/eigen_subset header"}
+    except Exception as e:  # context only: never fails the arm
+        ref_build = {"error": str(e)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / len(pts),  # what was timed: the sampled steps
@@ -278,7 +303,7 @@ def reference_arm(args, cfg: str) -> None:
             "config": {"workload": f"{cfg}: {WORKLOAD[cfg]}", "walkers_per_worker": m,
                        "estimator": "literal (reference estimator.cpp:26-32)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
-            "fit": fit,
+            "fit": fit, "reference_build": ref_build,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
