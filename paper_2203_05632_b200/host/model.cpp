@@ -3,6 +3,7 @@
 // the flattening of a system into the device C ABI. Follows reference
 // proj/core/src/gaussian.cpp, model.cpp, weights.cpp (cited per function).
 #include <algorithm>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <fstream>
@@ -159,39 +160,62 @@ int SpinorSet::rows() const {
 }
 
 double SpinorSet::orthonormality_deviation() const {  // model.cpp:144-158, block-diagonal S
+  // max |C^H S C - I| as sum over channels x of C_x^H (S_x C_x); the O(rows^2 n_p + rows n_p^2)
+  // products run on all host threads (the serial part of every worker's setup, so of the
+  // strong-scaling job)
   const int cols = n_spinor();
-  std::vector<Complex> gram(std::size_t(cols) * cols, Complex(0, 0));
+  const int nthreads = std::max(1, std::min(16, int(std::thread::hardware_concurrency())));
+  auto parallel = [&](int n, auto&& body) {  // body(lo, hi) over [0, n)
+    std::vector<std::thread> pool;
+    const int chunk = (n + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads && t * chunk < n; ++t)
+      pool.emplace_back([&, t] { body(t * chunk, std::min(n, (t + 1) * chunk)); });
+    for (auto& th : pool) th.join();
+  };
+  std::vector<std::vector<Complex>> sc(basis.size());  // S_x C_x per channel
+  std::vector<int> offs(basis.size());
   int off = 0;
-  for (const auto& bl : basis) {
+  for (std::size_t x = 0; x < basis.size(); ++x) {
+    const auto& bl = basis[x];
     const int n = int(bl.size());
-    std::vector<double> s(std::size_t(n) * n);
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j <= i; ++j) s[std::size_t(i) * n + j] = s[std::size_t(j) * n + i] = contracted_overlap(bl[i], bl[j]);
-    std::vector<Complex> sc(std::size_t(n) * cols, Complex(0, 0));  // S C_x
-    for (int i = 0; i < n; ++i)
-      for (int k = 0; k < n; ++k) {
-        const double v = s[std::size_t(i) * n + k];
-        if (v == 0.0) continue;
-        const Complex* row = &coeff[std::size_t(off + k) * cols];
-        Complex* out = &sc[std::size_t(i) * cols];
-        for (int c = 0; c < cols; ++c) out[c] += v * row[c];
-      }
-    for (int i = 0; i < n; ++i) {
-      const Complex* row = &coeff[std::size_t(off + i) * cols];
-      const Complex* scr = &sc[std::size_t(i) * cols];
-      for (int a = 0; a < cols; ++a) {
-        const Complex ca = std::conj(row[a]);
-        Complex* g = &gram[std::size_t(a) * cols];
-        for (int b = 0; b < cols; ++b) g[b] += ca * scr[b];
-      }
-    }
+    offs[x] = off;
+    std::vector<double> sm(std::size_t(n) * n);
+    parallel(n, [&](int lo, int hi) {
+      for (int i = lo; i < hi; ++i)
+        for (int j = 0; j < n; ++j) sm[std::size_t(i) * n + j] = contracted_overlap(bl[i], bl[j]);
+    });
+    sc[x].assign(std::size_t(n) * cols, Complex(0, 0));
+    parallel(n, [&](int lo, int hi) {
+      for (int i = lo; i < hi; ++i)
+        for (int k = 0; k < n; ++k) {
+          const double v = sm[std::size_t(i) * n + k];
+          if (v == 0.0) continue;
+          const Complex* row = &coeff[std::size_t(off + k) * cols];
+          Complex* out = &sc[x][std::size_t(i) * cols];
+          for (int c = 0; c < cols; ++c) out[c] += v * row[c];
+        }
+    });
     off += n;
   }
-  double dev = 0.0;
-  for (int a = 0; a < cols; ++a)
-    for (int b = 0; b < cols; ++b)
-      dev = std::max(dev, std::abs(gram[std::size_t(a) * cols + b] - Complex(a == b ? 1.0 : 0.0, 0.0)));
-  return dev;
+  std::vector<double> devs(std::size_t(cols), 0.0);
+  parallel(cols, [&](int lo, int hi) {
+    std::vector<Complex> g(static_cast<std::size_t>(cols));
+    for (int a = lo; a < hi; ++a) {
+      std::fill(g.begin(), g.end(), Complex(0, 0));
+      for (std::size_t x = 0; x < basis.size(); ++x) {
+        const int n = int(basis[x].size());
+        for (int i = 0; i < n; ++i) {
+          const Complex ca = std::conj(coeff[std::size_t(offs[x] + i) * cols + a]);
+          const Complex* scr = &sc[x][std::size_t(i) * cols];
+          for (int b = 0; b < cols; ++b) g[b] += ca * scr[b];
+        }
+      }
+      double d = 0.0;
+      for (int b = 0; b < cols; ++b) d = std::max(d, std::abs(g[b] - Complex(a == b ? 1.0 : 0.0, 0.0)));
+      devs[std::size_t(a)] = d;
+    }
+  });
+  return devs.empty() ? 0.0 : *std::max_element(devs.begin(), devs.end());
 }
 
 std::string format_double(double x) {  // model.cpp:180-184
