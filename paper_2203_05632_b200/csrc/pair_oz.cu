@@ -547,11 +547,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
             __stcg(reinterpret_cast<double2*>(dst + p * 64 + c),
                    make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
                                 double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
-      } else
-#ifdef OZ_EXP_NO_CONTRACT  // experiment: drain only (the contraction never runs)
-      if (X[0] != 0x7FFFFFFFFFFFFFFll) acc_d += double(X[0] & 1); else
-#endif
-      {
+      } else {
         // literal contraction (estimator.cpp:26-32) on the Kramers alpha rows, as pair_kr's epilogue:
         // f(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) V(q e_q x_alpha; p e_p y),
         // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds

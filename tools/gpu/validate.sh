@@ -1,3 +1,7 @@
+# One GPU validation pass (run with gpurun from the repo root): the GPU suite, smoke, the bench
+# lines (cfg4 with strong_run and time_to_target, cfg3, the reference arm), the cfg5 sweep, the
+# kernel launch list and ncu captures of the V-GEMM and the slice kernel, all into gpurun_out/.
+#   gpurun --timeout 5400 -- 'TAG=r2x bash tools/gpu/validate.sh'
 set -u
 O=gpurun_out
 T=${TAG:-r2x}
