@@ -1,14 +1,21 @@
 // Does FP64 SIMT work slow down while tcgen05.mma kind::i8 runs on the same SM? One CTA per SM:
 // thread 0 issues the Ozaki V-GEMM's MMA mix (21 x M128 N80 K32 per k-step, commit per k-step)
 // for KSTEPS k-steps (or nothing), while 8 other warps run a fixed loop of one instruction kind
-// (8 independent chains). Prints the work warps' cycles with and without the MMA stream.
+// (8 independent chains). Prints the work warps' cycles with and without the MMA stream, and the MMA
+// stream's cycles per MMA (does the work slow the MMAs down?). -DNN=128 for the N = 128 mix.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_vs_umma tools/fp64_vs_umma.cu
 #include <cstdint>
 #include <cstdio>
 
 #include <cuda_runtime.h>
 
-constexpr int S = 6, MM = 128, NN = 80, KSTEPS = 2048, WORK = 4096;
+#ifndef NN
+#define NN 80
+#endif
+#ifndef WORK
+#define WORK 4096
+#endif
+constexpr int S = 6, MM = 128, KSTEPS = 2048;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint64_t desc(const void* p) {
   return uint64_t((smem_u32(p) >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) |
@@ -17,7 +24,8 @@ __device__ __forceinline__ uint64_t desc(const void* p) {
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NN >> 3) << 17) | (uint32_t(MM >> 4) << 24);
 
 template <int OP>
-__device__ __forceinline__ void work(double* out, long long* cyc) {
+__device__ __forceinline__ void work(double* out, long long* cyc, const int8_t* sm) {
+  const long long* sml = reinterpret_cast<const long long*>(sm);
   double a[8];
   float f[8];
   long long q[8];
@@ -32,6 +40,17 @@ __device__ __forceinline__ void work(double* out, long long* cyc) {
       if (OP == 2) a[i] += double(q[i] + it);                  // I2F.F64.S64 + DADD
       if (OP == 3) f[i] = fmaf(f[i], 0.999999f, 1e-7f);       // FFMA
       if (OP == 4) q[i] = q[i] * 128 + it;                     // int64 IMAD
+      if (OP == 5) q[i] += sml[(threadIdx.x + 32 * i + 8 * it) & 2047];  // LDS.64 (the operand region)
+      if (OP == 6) {  // the contraction's mix: LDS.64 o, int64 -> FP64, DFMA, a double shuffle
+        const long long o = sml[((threadIdx.x >> 3) * 4 + (threadIdx.x & 3) + 64 * i + 8 * it) & 2047];
+        a[i] = fma(__longlong_as_double((o & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL), double(q[i] + it), a[i]);
+        a[i] += __shfl_xor_sync(0xffffffffu, a[i], 1);
+      }
+      if (OP == 7) {  // FP32 mix: LDS.64, FFMA, a float shuffle
+        const long long o = sml[((threadIdx.x >> 3) * 4 + (threadIdx.x & 3) + 64 * i + 8 * it) & 2047];
+        f[i] = fmaf(__int_as_float(int(o) | 0x3F800000), float(it), f[i]);
+        f[i] += __shfl_xor_sync(0xffffffffu, f[i], 1);
+      }
     }
   }
   const long long t1 = clock64();
@@ -81,7 +100,7 @@ __global__ void probe(int mma, double* out, long long* cyc, long long* mma_cyc) 
           for (int t = 0; s + t < S; ++t)
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + uint32_t((s + t) * NN)),
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + uint32_t(((s + t) % (512 / NN)) * NN)),
                 "l"(desc(sa + s * MM * 32)), "l"(desc(sb + t * NN * 32)), "r"(IDESC), "r"(ks > 0 ? 1u : 0u));
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&bar[ks & 1])));
@@ -96,7 +115,7 @@ __global__ void probe(int mma, double* out, long long* cyc, long long* mma_cyc) 
       atomicMax((unsigned long long*)mma_cyc, (unsigned long long)(clock64() - t0));
     }
   } else {
-    work<OP>(out, cyc);
+    work<OP>(out, cyc, sm);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -115,9 +134,9 @@ void run(const char* name, int sms, double* out, long long* d) {
     probe<OP><<<sms, 288, smem>>>(mma, out, d, d + 1);
     cudaMemcpy(h[mma], d, 16, cudaMemcpyDeviceToHost);
   }
-  printf("%-18s work warps: %8lld cycles alone, %8lld cycles beside the MMA stream (x%.2f); MMA stream %lld cycles "
+  printf("N %d %-18s work warps: %8lld cycles alone, %8lld cycles beside the MMA stream (x%.2f); MMA stream %lld cycles "
          "(%.1f per MMA) -- %s\n",
-         name, h[0][0], h[1][0], double(h[1][0]) / h[0][0], h[1][1], double(h[1][1]) / (KSTEPS * 21.0),
+         NN, name, h[0][0], h[1][0], double(h[1][0]) / h[0][0], h[1][1], double(h[1][1]) / (KSTEPS * 21.0),
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -133,5 +152,8 @@ int main() {
   run<2>("I2F.F64.S64+DADD", sms, out, d);
   run<3>("FFMA", sms, out, d);
   run<4>("IMAD int64", sms, out, d);
+  run<5>("LDS.64", sms, out, d);
+  run<6>("mix FP64", sms, out, d);
+  run<7>("mix FP32", sms, out, d);
   return 0;
 }
