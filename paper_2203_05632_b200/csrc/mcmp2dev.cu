@@ -247,7 +247,7 @@ struct mcmp2dev_handle {
     const size_t ntiles = size_t(nbq) * (nbq + 1);
     ck(cudaStreamSynchronize(stream), "oz sync");
     ck(cudaMalloc(&ozp.sa, oz_slice_bytes_a(npts_oz, ks)), "cudaMalloc oz slices");
-    // B blocks: 8 walkers (physical) or 16 (literal, fused); rows past the last point stay zero
+    // B blocks: 8 walkers (physical) or 10 (literal, fused); rows past the last point stay zero
     const int nbr = oz_nb_rows(estimator != MCMP2DEV_ESTIMATOR_PHYSICAL);
     const size_t sb_bytes = oz_slice_bytes_b(npts_oz, ks, nbr);
     const size_t sbs_bytes = sizeof(double) * oz_p_blocks(npts_oz, nbr) * nbr;

@@ -306,9 +306,6 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
         }
         const int y = (lane >> 2) & 3, pp = lane & 3;
         if constexpr (OZ == 2) {  // o = conj O~ to the tile's O block in HBM; no V phase here
-          // walker-major [p][e_p][y][q x_alpha re/im]: tile a (a + 1) + b of Q block a holds its P
-          // walkers 8 b .., so a Q block's P walkers are contiguous (oz_vgemm_fused_kernel stages
-          // 16 of them per tile with one bulk copy)
           double* ot = P.otiles + size_t(tt) * 4096;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
@@ -317,9 +314,9 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
-                double* d = ot + p * 512 + (e1 * 4 + y) * 64 + q * 4 + j * 2;
-                __stcg(reinterpret_cast<double2*>(d),
-                       make_double2(t1[h][n][j] + t2[h][n][j], -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j])));
+                double* d = ot + (q * 4 + j * 2) * 64 + (p * 2 + e1) * 4 + y;
+                __stcg(d, t1[h][n][j] + t2[h][n][j]);
+                __stcg(d + 64, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]));
               }
           continue;
         }

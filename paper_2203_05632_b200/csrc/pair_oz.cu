@@ -37,8 +37,6 @@
 // ceiling, vs ~3.6 ms for the DMMA V phase of pair_kr.
 #include <cuda_runtime.h>
 
-#include <type_traits>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "pair_common.cuh"
@@ -73,11 +71,11 @@ constexpr int TMEM_COLS = 512;      // 6 x NB used
 // PB P blocks, so each k-step's A slices serve PB blocks (the pass is bound by the L2 -> SMEM
 // operand stream)
 #ifndef OZ_REFINE_PB
-#define OZ_REFINE_PB 1
+#define OZ_REFINE_PB 3
 #endif
 template <bool FUSED, bool CORR = false>
 struct OzShape {
-  static constexpr int NB = FUSED ? 128 : 64;
+  static constexpr int NB = FUSED ? 80 : 64;
   static constexpr int PW = NB / 8;  // P walkers per P block
   static constexpr int PB = CORR ? OZ_REFINE_PB : 1;  // P blocks per tile
   static constexpr int B_KSM = SL * NB * 32;  // stored bytes of one k-step of a P block
@@ -93,8 +91,9 @@ struct OzShape {
   static constexpr uint32_t IDESC =
       (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
 };
+static_assert(OzShape<true>::SMEM_BYTES <= 227 * 1024, "stage ring");
 static_assert(OzShape<true, true>::SMEM_BYTES <= 227 * 1024, "stage ring");
-static_assert(OzShape<false>::NACC * OzShape<false>::NB <= 512 && OzShape<true, true>::NSLOT >= 2 &&
+static_assert(OzShape<true>::NACC * OzShape<true>::NB <= 512 && OzShape<true, true>::NSLOT >= 2 &&
                   OzShape<true, true>::NSTAGE >= 2,
               "TMEM columns / stage ring");
 
@@ -112,28 +111,6 @@ __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_i8r(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-// issued by a whole convergent warp: one elected lane (the lowest, the same for every call)
-// executes the MMA / commit, while the operands stay warp-uniform (no per-MMA waterfall loop
-// moving per-thread registers into uniform ones, as when issued under `if (lane == 0)`)
-template <uint32_t IDESC>
-__device__ __forceinline__ void umma_i8_warp(uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
-      : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -395,178 +372,9 @@ constexpr int TL_TILES = 128;
 __device__ unsigned long long g_oz_tl[160][TL_TILES][3 + 3 * EPW];
 #define TL(t, k, v) \
   if ((t) < TL_TILES) g_oz_tl[blockIdx.x][t][k] = (v)
-// oz_vgemm_fused_kernel: [0] MMA thread before its TMEM waits, [1] pass A acquired, [2] pass A
-// issued, [3] pass B acquired, [4] pass B issued; epilogue warp w at 8 + 7 w: pass A full, d = 0, 1
-// released, d = 2, 3 released, A contracted, pass B full, B released, tile done
-constexpr int TLF_TILES = 64;
-__device__ unsigned long long g_fz_tl[160][TLF_TILES][64];
-#define TLF(t, k, v) \
-  if ((t) < TLF_TILES) g_fz_tl[blockIdx.x][t][k] = (v)
 #else
 #define TL(t, k, v)
-#define TLF(t, k, v)
 #endif
-
-// sum_y o_y x_y sbv_y sr of one (p, e_p) quad in FP32, for a part of V that is a small fraction of
-// the term (the refinement's diagonal 6, the split main pass's diagonals 3..5): o_y sbv_y as a 24-bit
-// float mantissa with an integer exponent (read from the bits; sbv, sr powers of two), the terms
-// aligned to the quad's largest exponent, one conversion and scaling at the end
-__device__ __forceinline__ double quad_f32(const long long (&ob)[4], const double* sbv, const float (&xf)[4], double sr) {
-  int E[4], emax = 0;
-#pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    const int ex = int((ob[y] >> 52) & 0x7FF);  // zero / subnormal o: dropped
-    E[y] = ex ? ex + int((__double_as_longlong(sbv[y]) >> 52) & 0x7FF) : 0;
-    emax = max(emax, E[y]);
-  }
-  float acc = 0.0f;
-#pragma unroll
-  for (int y = 0; y < 4; ++y) {
-    const int dsh = E[y] - emax;
-    if (E[y] == 0 || dsh < -120) continue;
-    const float mf = __int_as_float(0x3F800000 | int((ob[y] >> 29) & 0x7FFFFF)) * __int_as_float((127 + dsh) << 23);
-    acc = fmaf(ob[y] < 0 ? -mf : mf, xf[y], acc);
-  }
-  if (!emax) return 0.0;
-  // sum = acc 2^(emax - 2046) sr, sr = 2^(srx - 1023)
-  const int tt = emax + int((__double_as_longlong(sr) >> 52) & 0x7FF) - 3069;
-  const double scale = (tt > -1023 && tt < 1024) ? __longlong_as_double((long long)(tt + 1023) << 52) : ldexp(1.0, tt);
-  return double(acc) * scale;
-}
-
-// o s for s a power of two: an exponent add on the bits (integer pipe: FP64 SIMT is throttled
-// ~12x beside the running MMAs), a multiply for zero / subnormal o or an out-of-range result
-__device__ __forceinline__ double mul_pow2(long long ob, double s) {
-  const long long sx = __double_as_longlong(s) - (1023LL << 52);
-  const int eo = int((ob >> 52) & 0x7FF), ef = eo + int(sx >> 52);
-  return (eo != 0 && ef > 0 && ef < 2047) ? __longlong_as_double(ob + sx) : __longlong_as_double(ob) * s;
-}
-
-// int64 -> float for |x| < 2^43 on the integer and FP32 pipes (two magic-number conversions of
-// 22-bit halves, one rounding)
-__device__ __forceinline__ float ll2f_fast(long long x) {
-  const int hi = int(x >> 21), lo = int(x & 0x1FFFFF);
-  const float fh = __int_as_float(0x4B400000 + hi) - 12582912.0f;
-  const float fl = __int_as_float(0x4B400000 + lo) - 12582912.0f;
-  return fmaf(fh, 2097152.0f, fl);
-}
-
-// one pair's literal term from its f values (estimator.cpp:26-32) into the thread's sums, with the
-// accuracy guard's error estimate: the INT8 error of each f is modelled per element as a random sum
-// over K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v) with the
-// row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of 2^e sqrt(|x 2^-e|^2 /
-// 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction with |o block|_F <= |Phi_o(u)|_F
-// |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2) per pair, summed in quadrature over the
-// step (the last CTA compares sqrt(sum eps^2) with guard_tol |sum|). On the oracle's cfg3/cfg4
-// steps this estimate is 3-250x the actual error (tests/test_oz_guard_model.py), on 2000-step
-// device chains 2.3-170x (tests/test_gpu_guard.py); it is a model, not a bound. After the
-// refinement pass (one more slice and diagonal) the same model with 2^-49.
-// CORR: F is this pass's correction; the main pass's f values come from P.fstore. Main pass: F
-// is stored there (when P.fstore is set) for a refinement pass.
-struct OzSums {
-  double d = 0.0, x = 0.0, ed = 0.0, ex = 0.0, ad = 0.0, ax = 0.0;
-};
-template <bool CORR>
-__device__ __forceinline__ void oz_pair_term(const OzParams& P, double4 F, int qg, int pg, bool guard, OzSums& acc) {
-  double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
-  if constexpr (CORR) {  // f of the main pass plus this pass's corrections
-    const double4 f6 = *fs;
-    F.x += f6.x, F.y += f6.y, F.z += f6.z, F.w += f6.w;
-  } else if (fs) {
-    *fs = F;
-  }
-  const double td = (-P.w_direct * F.x) * F.y;    // f1d f2d
-  const double tx = (-P.w_exchange * F.z) * F.w;  // f1x f2x
-  acc.d += td;
-  acc.x += tx;
-  if (guard) {
-    constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
-    const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
-    const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
-    const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
-    const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
-    const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
-    const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
-    const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
-    const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
-    const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
-    acc.ed += ed * ed;
-    acc.ex += ex * ex;
-    acc.ad += fabs(td);
-    acc.ax += fabs(tx);
-  }
-}
-
-// the literal kernels' end of launch, all threads: each epilogue warp's sums (fixed-order warp
-// shuffles) into s_red, the CTA's partials in epilogue-warp order, then the last CTA's fixed-order
-// sum over CTAs (as pair_kr.cu), the step's values and the guard's verdict: a failed (or
-// non-finite) step goes to the refinement pass (oz_trip 1: when the main pass stored the f
-// values) or to the DMMA kernel (oz_trip 2)
-template <bool CORR>
-__device__ void oz_finish(const OzParams& P, const OzSums& acc, bool epi, int epw, double (*s_red)[6], bool guard,
-                          bool* s_last) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (epi) {
-    double r[6] = {acc.d, acc.x, acc.ed, acc.ex, acc.ad, acc.ax};
-#pragma unroll
-    for (int o = 16; o; o >>= 1)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) r[k] += __shfl_down_sync(0xffffffffu, r[k], o);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) s_red[warp][k] = r[k];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
-    double r[6] = {0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < epw; ++w)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) r[k] += s_red[w][k];
-    double* pp = P.partials + size_t(blockIdx.x) * 8;
-    pp[0] = r[0] * cw;
-    pp[1] = 0.0;
-    pp[2] = r[1] * cw;
-    pp[3] = 0.0;
-    pp[4] = r[2] * cw * cw;
-    pp[5] = r[3] * cw * cw;
-    pp[6] = r[4] * cw;
-    pp[7] = r[5] * cw;
-    __threadfence();
-    *s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!*s_last || tid != 0) return;
-  __threadfence();
-  double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (unsigned c = 0; c < gridDim.x; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] += P.partials[size_t(c) * 8 + k];
-  const double d = r[0], x = r[2];
-  const double npairs = 0.5 * P.m * (P.m - 1);
-  P.step_out[0] = (d + x) / npairs;
-  P.step_out[1] = 0.0;
-  P.step_out[2] = d;
-  P.step_out[3] = 0.0;
-  P.step_out[4] = x;
-  P.step_out[5] = 0.0;
-  const double ed = sqrt(r[4]), ex = sqrt(r[5]), tol = P.guard_tol;
-  const bool trip = guard && tol > 0.0 &&
-                    (!(ed <= tol * fabs(d)) || !(ex <= tol * fabs(x)) || !(sqrt(r[4] + r[5]) <= tol * fabs(d + x)));
-  P.step_out[6] = ed;
-  P.step_out[7] = ex;
-  P.step_out[8] = r[6];
-  P.step_out[9] = r[7];
-  P.step_out[10] = 1.0;
-  if constexpr (CORR) {
-    P.step_out[11] = trip ? 2.0 : 1.0;  // refined; DMMA next if the refined step still fails
-    P.st->oz_trip = trip ? 2 : 0;
-  } else {
-    P.step_out[11] = trip && !P.fstore ? 2.0 : 0.0;
-    if (trip) P.st->oz_trip = P.fstore ? 1 : 2;
-  }
-  P.st->done_pair = 0;
-}
 
 template <bool FUSED, bool CORR>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
@@ -600,7 +408,9 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   __shared__ __align__(32) double4 s_f[2][FUSED ? 16 * PW : 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
-  OzSums acc;  // FUSED: this thread's pair sums (and the guard's sums)
+  double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums
+  // FUSED, guard: sums of the squared per-pair error estimates and of |pair term|
+  double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
   const bool guard = FUSED && P.pstat != nullptr;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
@@ -693,8 +503,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       for (int j = 0; j < nbk; ++j, ++sub) {  // the tile's P blocks in turn (one in the main pass)
       const int b = w.g * PB + j;
       const uint32_t tbase = tmem + (uint32_t(lq * 32) << 16) + uint32_t((slot * PB + j) * NB + c_lo);
-      using XT = std::conditional_t<NACC == 1, int, long long>;  // the merged accumulators
-      XT X[CPW];
+      long long X[CPW];
       auto merge = [&](const uint32_t (&v)[NACC][16], int c0, int n) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
@@ -702,7 +511,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           long long x = int32_t(v[0][c]);
 #pragma unroll
           for (int d = 1; d < NACC; ++d) x = x * 128 + int32_t(v[d][c]);
-          X[c0 + c] = XT(x);
+          X[c0 + c] = x;
         }
       };
 #pragma unroll
@@ -739,40 +548,78 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
                    make_double2(double(X[8 * p + c]) * sr * sbv[8 * p + c],
                                 double(X[8 * p + c + 1]) * sr * sbv[8 * p + c + 1]));
       } else {
-        // the refinement's contraction (estimator.cpp:26-32 on the Kramers alpha rows, as the main
-        // pass): df(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) dV(q e_q x_alpha; p e_p y),
-        // o = conj O~ from pair_kr_kernel<false, 2> (walker-major: o of Q block a, P walker pg at
-        // a (a + 1) 4096 + pg 512 + (e_p 4 + y) 64 + (q, x_alpha, re/im)). This thread holds dV for its
-        // (p, e_p, y): partial g = sum_y o_re Re dV, or -sum_y o_im Im dV, then the four lanes of
-        // (x_alpha, plane) add up. df is ~2^-42 of f, so FP32 carries it with room to spare (its
-        // rounding is ~2^-66 of f). The pass has few MMAs per tile to hide loads behind and four
-        // tiles in flight in TMEM: the o quads are loaded four at a time.
-        static_assert(CORR, "the fused main pass is oz_vgemm_fused_kernel");
+        // literal contraction (estimator.cpp:26-32) on the Kramers alpha rows, as pair_kr's epilogue:
+        // f(e_q, e_p) = 2 Re sum_{x_alpha, y} o_{e_p}(q, p; y, x_alpha) V(q e_q x_alpha; p e_p y),
+        // o = conj O~ from pair_kr_kernel<false, 2>. This thread (q, e_q, x_alpha, re/im plane) holds
+        // Re V (plane 0) or Im V (plane 1) for its (p, e_p, y): partial g = sum_y o_re Re V, or
+        // -sum_y o_im Im V, then the four lanes of (x_alpha, plane) add up.
+        // o blocks are in pair_kr's 16 x 8 tiles: walker p of this tile is p_g = PW b + p, in pair_kr
+        // tile a (a + 1) + p_g / 8 (none past the triangle row: those pairs are masked below).
+        // FP64 SIMT work runs ~12x slower while tcgen05 MMAs occupy the SM (tools/fp64_vs_umma.cu).
+        // An exact integer form of sum_y o_y V_y (53-bit mantissas aligned per quad, 128-bit
+        // products) was measured slower, 1.60 vs 1.42 ms at cfg4 (1.26 vs 0.85 ms in the refinement
+        // pass): its instruction stream competes with the MMA-issuing warp for issue slots. So the
+        // FP64 form stays and the per-pair terms are packed into whole warps after the named barrier
+        // (1.42 -> 1.35 ms with the guard's estimate; 1.29 ms with no contraction at all).
+        const int row_o = (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
-        static_assert(NK % 4 == 0, "o batches");
-        const double* ob0 = P.otiles + size_t(a) * (a + 1) * 4096 + q * 4 + (row & 3);
         double g[NK];
+        // the refinement pass has too few MMAs to hide the o-tile loads behind: load all of this
+        // thread's o quads for the P block first (one latency instead of NK), then contract
+        constexpr int NPF = CORR ? NK : 1;
+        longlong2 opf[NPF][2];
+        if constexpr (CORR) {
 #pragma unroll
-        for (int k0 = 0; k0 < NK; k0 += 4) {
-          long long ob[4][4];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int k = k0 + kk, pg = min(PW * b + (c_lo + 4 * k) / 8, 16 * (a + 1) - 1);
-            const double* o = ob0 + size_t(pg) * 512 + (k & 1) * 256;
-#pragma unroll
-            for (int y = 0; y < 4; ++y) ob[kk][y] = __double_as_longlong(__ldcs(o + 64 * y));
+          for (int k = 0; k < NK; ++k) {
+            const int pg = min(PW * b + (c_lo + 4 * k) / 8, 16 * (a + 1) - 1);
+            const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+            opf[k][0] = __ldcs(reinterpret_cast<const longlong2*>(o));
+            opf[k][1] = __ldcs(reinterpret_cast<const longlong2*>(o + 2));
           }
+        }
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int k = k0 + kk, pg = PW * b + (c_lo + 4 * k) / 8;
-            double sgp = 0.0;
-            if (pg < 16 * (a + 1)) {
-              const float xf[4] = {__int2float_rn(int(X[4 * k])), __int2float_rn(int(X[4 * k + 1])),
-                                   __int2float_rn(int(X[4 * k + 2])), __int2float_rn(int(X[4 * k + 3]))};
-              sgp = quad_f32(ob[kk], sbv + 4 * k, xf, sr);
+        for (int k = 0; k < NK; ++k) {
+          const int pg = PW * b + (c_lo + 4 * k) / 8;
+          double sgp = 0.0;
+          if (pg < 16 * (a + 1)) {
+            if constexpr (!CORR) {
+              const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+              const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o));
+              const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 2));
+              const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
+              const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
+              sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+            } else {
+              // the refinement's correction df = sum o dV is ~2^-42 of f, so FP32 carries it with
+              // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
+              // with an integer exponent (read from the bits), terms aligned to the quad's largest
+              // exponent, one conversion and scaling
+              const long long ob[4] = {opf[CORR ? k : 0][0].x, opf[CORR ? k : 0][0].y, opf[CORR ? k : 0][1].x,
+                                       opf[CORR ? k : 0][1].y};
+              int E[4], emax = 0;
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                const int ex = int((ob[y] >> 52) & 0x7FF);  // zero / subnormal o: dropped
+                E[y] = ex ? ex + int((__double_as_longlong(sbv[4 * k + y]) >> 52) & 0x7FF) : 0;
+                emax = max(emax, E[y]);
+              }
+              float acc = 0.0f;
+#pragma unroll
+              for (int y = 0; y < 4; ++y) {
+                const int dsh = E[y] - emax;
+                if (E[y] == 0 || dsh < -120) continue;
+                const float mf = __int_as_float(0x3F800000 | int((ob[y] >> 29) & 0x7FFFFF)) *
+                                 __int_as_float((127 + dsh) << 23);
+                acc = fmaf(ob[y] < 0 ? -mf : mf, __int2float_rn(int(X[4 * k + y])), acc);
+              }
+              if (emax) {  // sum = acc 2^(emax - 2046) sr, sr = 2^(srx - 1023)
+                const int tt = emax + int((__double_as_longlong(sr) >> 52) & 0x7FF) - 3069;
+                const double scale = (tt > -1023 && tt < 1024) ? __longlong_as_double((long long)(tt + 1023) << 52) : ldexp(1.0, tt);
+                sgp = double(acc) * scale;
+              }
             }
-            g[k] = plane ? -sgp : sgp;
           }
+          g[k] = plane ? -sgp : sgp;
         }
 #pragma unroll
         for (int k = 0; k < NK; ++k) {
@@ -794,316 +641,117 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         for (int id = (warp * 32 + lane); id < 16 * PW; id += 32 * EPW) {
           const int q2 = id / PW, p2 = id % PW, qg = qg0 + q2, pg = pg0 + p2;
           if (!(qg < P.m && pg < P.m && qg > pg)) continue;
-          oz_pair_term<CORR>(P, sf[id], qg, pg, guard, acc);
+          double4 F = sf[id];
+          double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
+          if constexpr (CORR) {  // f of the main pass plus this pass's corrections
+            const double4 f6 = *fs;
+            F.x += f6.x, F.y += f6.y, F.z += f6.z, F.w += f6.w;
+          } else if (fs) {
+            *fs = F;
+          }
+          const double td = (-P.w_direct * F.x) * F.y;    // f1d f2d
+          const double tx = (-P.w_exchange * F.z) * F.w;  // f1x f2x
+          acc_d += td;
+          acc_x += tx;
+          if (guard) {
+            // accuracy guard: the INT8 error of each f is modelled per element as a random sum over
+            // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
+            // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
+            // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
+            // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
+            // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
+            // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
+            // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
+            // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
+            // (one more slice and diagonal) the same model with 2^-49.
+            constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
+            const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
+            const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
+            const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
+            const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
+            const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
+            const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
+            const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
+            const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
+            const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
+            acc_ed += ed * ed;
+            acc_ex += ex * ex;
+            acc_ad += fabs(td);
+            acc_ax += fabs(tx);
+          }
         }
       }
       }  // P blocks of the tile
       if (lane == 0) TL(it, 5 + 3 * warp, clock64());
     }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
-  if constexpr (FUSED) oz_finish<CORR>(P, acc, warp < EPW, EPW, s_red, guard, &s_last);
-}
-
-// The literal path's main pass (oz_vgemm_fused_kernel): tiles of 16 Q x 16 P walkers, N = 128.
-// A kind::i8 M128 MMA takes ~61 cycles for every N <= 80 but ~71 at N = 128 (tools/umma_rate.cu:
-// 3132 vs 4282 TOPS), while six slice-diagonal accumulators fit the 512 TMEM columns only up to
-// N = 80. So the 21 slice products run in two passes over K:
-//   A  the diagonals d = 0..3 (10 products per k-step) into four 128-column accumulators;
-//   B  the diagonals 4, 5 (11 products) into the first two, once A's d = 0, 1 are drained.
-// Each pass is merged exactly (X_A = sum_{d<4} acc_d 128^(3-d), X_B = acc_4 128 + acc_5, so
-// V = (X_A 2^14 + X_B) 2^(e_q + e_p - 49)) and contracted with the o blocks on its own -- the
-// contraction is linear in V: pass A in FP64; pass B in FP32, as X_B is ~2^-27 of V (FP32's
-// 2^-24 rounding is ~2^-51 of the term, below the refinement pass's 2^-49). The tile's o block
-// (16 P walkers x 512 doubles, pair_kr's walker-major layout) is staged in shared memory by one
-// bulk copy, so the contraction reads it conflict-free (one (p, e_p, y) value per 16 consecutive
-// doubles across a warp) instead of holding it in registers. Per 16 x 16 walkers: 21 MMAs of ~71
-// cycles per k-step against 21 x 1.6 of ~61 for the same walkers in N = 80 tiles (0.73 of the
-// tensor time), and two exposed TMEM drains of half size.
-namespace fz {
-constexpr int NB = 128, PW = 16, EPW = 8, THREADS = (EPW + 2) * 32;
-constexpr int ASL = MA * 32, BSL = NB * 32;  // one slice of one k-step
-constexpr int B_KSM = SL * BSL;              // stored bytes of one k-step of a P block
-constexpr int STAGE = S * (ASL + BSL);       // A slices, then B slices
-constexpr int NST = 3;
-constexpr int O_DOUBLES = PW * 512;          // the tile's o block
-constexpr int SMEM_BYTES = NST * STAGE + O_DOUBLES * 8;
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
-static_assert(4 * NB <= 512 && SMEM_BYTES + 16 * 1024 + 1024 <= 227 * 1024, "TMEM columns / shared memory");
-}  // namespace fz
-
-__global__ void __launch_bounds__(fz::THREADS, 1) oz_vgemm_fused_kernel(OzParams P) {
-  constexpr int NB = fz::NB, PW = fz::PW, EPW = fz::EPW, ASL = fz::ASL, BSL = fz::BSL, B_KSM = fz::B_KSM;
-  constexpr int STAGE = fz::STAGE, NST = fz::NST, CPW = NB / 2;  // columns per epilogue warp
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ __align__(1024) int8_t sm[];
-  const double* const so = reinterpret_cast<const double*>(sm + NST * STAGE);
-  // tfull: [0] pass A, [1] pass B; tempty: [0] A's d = 0, 1 drained, [1] A's d = 2, 3, [2] pass B
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[3], ofull, oempty;
-  __shared__ uint32_t tmem_base;
-  __shared__ double s_red[EPW][6];
-  __shared__ bool s_last;
-  __shared__ __align__(32) double4 s_f[2][16 * PW];  // the f values of the last two tiles, [q][p]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int KS = P.ks;
-  OzSums acc;
-  const bool guard = P.pstat != nullptr;
-  if (tid == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&tfull[s], 1);
-    for (int s = 0; s < 3; ++s) mbar_init(&tempty[s], 32 * EPW);
-    mbar_init(&ofull, 1), mbar_init(&oempty, 32 * EPW);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
-  const int ntiles = P.ntiles;
-  const int my = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
-
-  if (warp == EPW) {
-    if (lane == 0) {  // producer: pass A k-steps (slices 0..3), the o block, pass B k-steps (all six)
-      int stage = 0;
-      uint32_t ph = 0;
-      OzWalk w(int(blockIdx.x), PW);
-      for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
-        const int8_t* ga = P.sa + size_t(w.a) * KS * A_KSM;
-        const int8_t* gb = P.sb + size_t(w.b) * KS * B_KSM;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int nsl = pass ? S : 4;
-          for (int ks = 0; ks < KS; ++ks) {
-            mbar_wait(&empty[stage], ph ^ 1u);
-            int8_t* dst = sm + stage * STAGE;
-#ifdef OZ_NOFILL  // experiment: MMAs on whatever the stages hold (timing only)
-            mbar_arrive(&full[stage]);
-            (void)dst, (void)ga, (void)gb;
-#else
-            mbar_expect_tx(&full[stage], nsl * (ASL + BSL));
-            bulk_g2s(dst, ga + size_t(ks) * A_KSM, nsl * ASL, &full[stage]);
-            bulk_g2s(dst + S * ASL, gb + size_t(ks) * B_KSM, nsl * BSL, &full[stage]);
-#endif
-            if (++stage == NST) stage = 0, ph ^= 1u;
-          }
-          if (pass == 0) {  // the previous tile's contraction is done with the o buffer
-            mbar_wait(&oempty, uint32_t(it & 1) ^ 1u);
-            mbar_expect_tx(&ofull, fz::O_DOUBLES * 8);
-            const double* src = P.otiles + (size_t(w.a) * (w.a + 1) * 4096 + size_t(PW * w.b) * 512);
-            bulk_g2s(sm + NST * STAGE, src, fz::O_DOUBLES * 8, &ofull);
-          }
-        }
-      }
-    }
-  } else if (warp == EPW + 1) {
-    {  // MMA issuer: the whole warp (elect.sync in the MMA and commit asm)
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int it = 0; it < my; ++it) {
-        const uint32_t tp = uint32_t(it & 1);
-        if (lane == 0) TLF(it, 0, clock64());
-        mbar_wait(&tempty[2], tp ^ 1u);  // the previous tile's pass B and A's d = 2, 3 are drained
-        mbar_wait(&tempty[1], tp ^ 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) TLF(it, 1, clock64());
-        for (int ks = 0; ks < KS; ++ks) {
-          mbar_wait(&full[stage], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const int8_t* sa = sm + stage * STAGE;
-          const int8_t* sb = sa + S * ASL;
+    if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
+      double r[6] = {acc_d, acc_x, acc_ed, acc_ex, acc_ad, acc_ax};
 #pragma unroll
-          for (int s = 0; s < 4; ++s)
+      for (int o = 16; o; o >>= 1)
 #pragma unroll
-            for (int t = 0; s + t < 4; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
-              umma_i8_warp<fz::IDESC>(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * ASL), umma_desc(sb + t * BSL),
-                                 ks > 0 || s > 0 ? 1u : 0u);
-          umma_commit_warp(&empty[stage]);
-          if (++stage == NST) stage = 0, ph ^= 1u;
-        }
-        umma_commit_warp(&tfull[0]);
-        if (lane == 0) TLF(it, 2, clock64());
-        mbar_wait(&tempty[0], tp);  // A's d = 0, 1 drained: pass B reuses their columns
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) TLF(it, 3, clock64());
-        for (int ks = 0; ks < KS; ++ks) {
-          mbar_wait(&full[stage], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const int8_t* sa = sm + stage * STAGE;
-          const int8_t* sb = sa + S * ASL;
+        for (int k = 0; k < 6; ++k) r[k] += __shfl_down_sync(0xffffffffu, r[k], o);
+      if (lane == 0)
 #pragma unroll
-          for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int t = 0; t < S; ++t)
-              if (s + t >= 4 && s + t < S)
-                umma_i8_warp<fz::IDESC>(tmem + uint32_t((s + t - 4) * NB), umma_desc(sa + s * ASL), umma_desc(sb + t * BSL),
-                                   ks > 0 || s > 0 ? 1u : 0u);
-          umma_commit_warp(&empty[stage]);
-          if (++stage == NST) stage = 0, ph ^= 1u;
-        }
-        umma_commit_warp(&tfull[1]);
-        if (lane == 0) TLF(it, 4, clock64());
-      }
-    }
-  } else {  // epilogue: TMEM lane = A row (lane quarter lq = warp % 4); columns h 64 .. (P walkers 8 h ..)
-    const int lq = warp & 3, h = warp >> 2;
-    const int row = lq * 32 + lane;
-    const int q = row >> 3, plane = row & 1;
-    const int orow = q * 4 + (row & 3);  // o row (q, x_alpha, re/im) of this A row
-    const uint32_t tb = tmem + (uint32_t(lq * 32) << 16) + uint32_t(h * CPW);
-    OzWalk w(int(blockIdx.x), PW);
-    for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
-      const int a = w.a, b = w.b;
-      const uint32_t tp = uint32_t(it & 1);
-      const double sra = P.sa_scale[size_t(a) * MA + row];
-      const double* sbv = P.sb_scale + size_t(b) * NB + h * CPW;
-      double4* sf = s_f[it & 1];
-      // this thread's contribution g to f(q; p, e_p) of quad k = (p = 8 h + k / 2, e_p = k & 1) ->
-      // the four f values of (q, p) in sf (lanes row % 8 == 0; pass B adds to pass A's)
-      auto park = [&](double (&g)[CPW / 4], bool add) {
-#pragma unroll
-        for (int k = 0; k < CPW / 4; ++k) {
-          if (plane) g[k] = -g[k];
-          g[k] += __shfl_xor_sync(0xffffffffu, g[k], 1);
-          g[k] += __shfl_xor_sync(0xffffffffu, g[k], 2);
-        }
-#pragma unroll
-        for (int p = 0; p < CPW / 8; ++p) {
-          const double f10 = __shfl_xor_sync(0xffffffffu, g[2 * p], 4);
-          const double f11 = __shfl_xor_sync(0xffffffffu, g[2 * p + 1], 4);
-          // f(0,0) = f1d, f(1,1) = f2d, f(1,0) = f1x, f(0,1) = f2x (the factor 2 of 2 Re here)
-          if ((row & 7) == 0) {
-            double4& d = sf[q * PW + h * (CPW / 8) + p];
-            const double4 v = make_double4(2.0 * g[2 * p], 2.0 * f11, 2.0 * f10, 2.0 * g[2 * p + 1]);
-            if (add)
-              d.x += v.x, d.y += v.y, d.z += v.z, d.w += v.w;
-            else
-              d = v;
-          }
-        }
-      };
-      // o_y of quad k: so[(p_local 512) + (e_p 4 + y) 64 + orow]
-      auto o_at = [&](int k, int y) {
-        return __double_as_longlong(so[(h * (CPW / 8) + k / 2) * 512 + ((k & 1) * 4 + y) * 64 + orow]);
-      };
-      // pass A: d = 0, 1 merged and released, then d = 2, 3; FP64 contraction
-      {
-        mbar_wait(&tfull[0], tp);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) TLF(it, 8 + 7 * warp, clock64());
-        long long X[CPW];
-#pragma unroll
-        for (int c0 = 0; c0 < CPW; c0 += 8) {
-          uint32_t v[2][8];
-          tmem_ld8(tb + uint32_t(c0), v[0]);
-          tmem_ld8(tb + uint32_t(NB + c0), v[1]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int c = 0; c < 8; ++c) X[c0 + c] = static_cast<long long>(int32_t(v[0][c])) * 128 + int32_t(v[1][c]);
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        mbar_arrive(&tempty[0]);
-        if (lane == 0) TLF(it, 9 + 7 * warp, clock64());
-#pragma unroll
-        for (int c0 = 0; c0 < CPW; c0 += 8) {
-          uint32_t v[2][8];
-          tmem_ld8(tb + uint32_t(2 * NB + c0), v[0]);
-          tmem_ld8(tb + uint32_t(3 * NB + c0), v[1]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            X[c0 + c] = X[c0 + c] * 16384 + static_cast<long long>(int32_t(v[0][c])) * 128 + int32_t(v[1][c]);
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        mbar_arrive(&tempty[1]);
-        if (lane == 0) TLF(it, 10 + 7 * warp, clock64());
-        mbar_wait(&ofull, tp);
-        const double sr = sra * 0x1p14;
-        double g[CPW / 4];
-#pragma unroll
-        for (int k = 0; k < CPW / 4; ++k) {
-          double sgp = 0.0;
-#if defined(OZ_EXPER) && (OZ_EXPER & 1)  // experiment: no pass-A contraction (timing only)
-          g[k] = double(X[4 * k]);
-          continue;
-#endif
-#if defined(OZ_EXPER) && (OZ_EXPER & 8)  // experiment: pass A's loads and an FP32-only contraction
-          {
-            float gf = 0.0f;
-#pragma unroll
-            for (int y = 0; y < 4; ++y)
-              gf = fmaf(__int_as_float(int(o_at(k, y)) | 0x3F800000), ll2f_fast(X[4 * k + y]), gf);
-            g[k] = __int_as_float(__float_as_int(gf) & 0x7F800000);  // keep park's inputs tiny and finite
-            continue;
-          }
-#endif
-#pragma unroll
-          for (int y = 0; y < 4; ++y) sgp = fma(mul_pow2(o_at(k, y), sbv[4 * k + y]), double(X[4 * k + y]), sgp);
-          g[k] = sgp * sr;
-        }
-        park(g, false);
-        if (lane == 0) TLF(it, 11 + 7 * warp, clock64());
-      }
-      // pass B: d = 4, 5 merged to FP32 and released; FP32 contraction
-      {
-        mbar_wait(&tfull[1], tp);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) TLF(it, 12 + 7 * warp, clock64());
-        float X[CPW];
-#pragma unroll
-        for (int c0 = 0; c0 < CPW; c0 += 8) {
-          uint32_t v[2][8];
-          tmem_ld8(tb + uint32_t(c0), v[0]);
-          tmem_ld8(tb + uint32_t(NB + c0), v[1]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int c = 0; c < 8; ++c) X[c0 + c] = ll2f_fast(static_cast<long long>(int32_t(v[0][c])) * 128 + int32_t(v[1][c]));
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        mbar_arrive(&tempty[2]);
-        if (lane == 0) TLF(it, 13 + 7 * warp, clock64());
-        double g[CPW / 4];
-#pragma unroll
-        for (int k = 0; k < CPW / 4; ++k) {
-#if defined(OZ_EXPER) && (OZ_EXPER & 2)  // experiment: no pass-B contraction (timing only)
-          g[k] = X[4 * k];
-          continue;
-#endif
-#if defined(OZ_EXPER) && (OZ_EXPER & 4)  // experiment: pass B's loads and an FP32-only contraction
-          {
-            float gf = 0.0f;
-#pragma unroll
-            for (int y = 0; y < 4; ++y) gf = fmaf(__int_as_float(int(o_at(k, y)) | 0x3F800000), X[4 * k + y], gf);
-            g[k] = __int_as_float(__float_as_int(gf) & 0x7F800000);
-            continue;
-          }
-#endif
-          const long long ob[4] = {o_at(k, 0), o_at(k, 1), o_at(k, 2), o_at(k, 3)};
-          const float xf[4] = {X[4 * k], X[4 * k + 1], X[4 * k + 2], X[4 * k + 3]};
-          g[k] = quad_f32(ob, sbv + 4 * k, xf, sra);
-        }
-        mbar_arrive(&oempty);  // this thread's reads of the o buffer are done
-        park(g, true);
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * EPW) : "memory");  // the tile's 16 x 16 f values are parked
-      {
-        const int id = warp * 32 + lane;  // one pair per epilogue thread
-        const int qg = 16 * a + id / PW, pg = PW * b + id % PW;
-        if (qg < P.m && pg < P.m && qg > pg) oz_pair_term<false>(P, sf[id], qg, pg, guard, acc);
-        if (lane == 0) TLF(it, 14 + 7 * warp, clock64());
-      }
+        for (int k = 0; k < 6; ++k) s_red[warp][k] = r[k];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
-  oz_finish<false>(P, acc, warp < EPW, EPW, s_red, guard, &s_last);
+  if constexpr (FUSED) {  // per-CTA partials, then the last CTA's fixed-order sum (as pair_kr.cu)
+    if (tid == 0) {
+      const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
+      double r[6] = {0, 0, 0, 0, 0, 0};
+      for (int w = 0; w < EPW; ++w)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) r[k] += s_red[w][k];
+      double* pp = P.partials + size_t(blockIdx.x) * 8;
+      pp[0] = r[0] * cw;
+      pp[1] = 0.0;
+      pp[2] = r[1] * cw;
+      pp[3] = 0.0;
+      pp[4] = r[2] * cw * cw;
+      pp[5] = r[3] * cw * cw;
+      pp[6] = r[4] * cw;
+      pp[7] = r[5] * cw;
+      __threadfence();
+      s_last = atomicAdd(&P.st->done_pair, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (unsigned c = 0; c < gridDim.x; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] += P.partials[size_t(c) * 8 + k];
+    const double d = r[0], x = r[2];
+    const double npairs = 0.5 * P.m * (P.m - 1);
+    P.step_out[0] = (d + x) / npairs;
+    P.step_out[1] = 0.0;
+    P.step_out[2] = d;
+    P.step_out[3] = 0.0;
+    P.step_out[4] = x;
+    P.step_out[5] = 0.0;
+    // guard: estimated error of the direct and exchange sums and of the step value against
+    // guard_tol; a failed (or non-finite) step goes to the refinement pass (oz_trip 1: when the
+    // main pass stored the f values) or to the DMMA kernel (oz_trip 2)
+    const double ed = sqrt(r[4]), ex = sqrt(r[5]), tol = P.guard_tol;
+    const bool trip = guard && tol > 0.0 &&
+                      (!(ed <= tol * fabs(d)) || !(ex <= tol * fabs(x)) || !(sqrt(r[4] + r[5]) <= tol * fabs(d + x)));
+    P.step_out[6] = ed;
+    P.step_out[7] = ex;
+    P.step_out[8] = r[6];
+    P.step_out[9] = r[7];
+    P.step_out[10] = 1.0;
+    if constexpr (CORR) {
+      P.step_out[11] = trip ? 2.0 : 1.0;  // refined; DMMA next if the refined step still fails
+      P.st->oz_trip = trip ? 2 : 0;
+    } else {
+      P.step_out[11] = trip && !P.fstore ? 2.0 : 0.0;
+      if (trip) P.st->oz_trip = P.fstore ? 1 : 2;
+    }
+    P.st->done_pair = 0;
+  }
 }
 
 int g_sms_oz[64];
@@ -1128,7 +776,8 @@ cudaError_t oz_kernel_setup() {
   cudaError_t e = cudaFuncSetAttribute(oz_vgemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        OzShape<false>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(oz_vgemm_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fz::SMEM_BYTES);
+  e = cudaFuncSetAttribute(oz_vgemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           OzShape<true>::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(oz_vgemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               OzShape<true, true>::SMEM_BYTES);
@@ -1151,7 +800,7 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
   const int sms = g_sms_oz[dev & 63] > 0 ? g_sms_oz[dev & 63] : 148;
   const int grid = P.ntiles < sms ? P.ntiles : sms;
   if (P.otiles)
-    pdl_launch(oz_vgemm_fused_kernel, dim3(grid), dim3(fz::THREADS), fz::SMEM_BYTES, s, P);
+    pdl_launch(oz_vgemm_kernel<true, false>, dim3(grid), dim3(THREADS), OzShape<true>::SMEM_BYTES, s, P);
   else
     pdl_launch(oz_vgemm_kernel<false, false>, dim3(grid), dim3(THREADS), OzShape<false>::SMEM_BYTES, s, P);
 }
@@ -1160,9 +809,6 @@ void launch_oz_vgemm(const OzParams& P, cudaStream_t s) {
 }  // namespace mcmp2dev
 extern "C" int mcmp2dev_debug_oz_timeline(void* host, size_t bytes) {
   return int(cudaMemcpyFromSymbol(host, mcmp2dev::g_oz_tl, bytes < sizeof(mcmp2dev::g_oz_tl) ? bytes : sizeof(mcmp2dev::g_oz_tl)));
-}
-extern "C" int mcmp2dev_debug_fz_timeline(void* host, size_t bytes) {
-  return int(cudaMemcpyFromSymbol(host, mcmp2dev::g_fz_tl, bytes < sizeof(mcmp2dev::g_fz_tl) ? bytes : sizeof(mcmp2dev::g_fz_tl)));
 }
 namespace mcmp2dev {
 #endif
