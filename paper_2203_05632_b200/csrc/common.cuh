@@ -135,6 +135,8 @@ struct DevState {
   int oz_trip;                // INT8 V path: this step's error estimate failed the guard; 1: the
                               // refinement pass runs (oz_vgemm_kernel<true, true>), 2: the guarded
                               // DMMA pair launch recomputes the step; each clears it when done
+  double oz_thr[3];           // the refinement pass's group thresholds on the main pass's error
+                              // estimates (sum eps_d^2, sum eps_x^2, their sum), set with oz_trip 1
 };
 
 }  // namespace mcmp2dev

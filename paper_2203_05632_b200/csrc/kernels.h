@@ -116,6 +116,8 @@ struct OzParams {
   double guard_tol;
   double* fstore;            // [C(m,2)][4] f(0,0), f(1,1), f(1,0), f(0,1) of each pair q > p (index
                              // q (q - 1) / 2 + p), written by the main pass for the refinement pass
+  double* tile_eps;          // [ntiles][2] the main pass's sum eps_d^2, sum eps_x^2 per tile: the
+                             // refinement pass refines only the tile groups that carry the error
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);

@@ -110,6 +110,7 @@ struct mcmp2dev_handle {
   double guard_tol = kGuardTol;
   double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
   double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
+  double* d_tile_eps = nullptr;  // [main tiles][2] the main pass's error estimate per tile
   long long guard_steps = 0, guard_refined = 0, guard_dmma = 0;
   double guard_max_est = 0.0;  // largest estimated relative error of a step kept on INT8
   SpinorParams sp{}, sp_kr{};  // general / Kramers-pair MO transform groups
@@ -221,13 +222,14 @@ struct mcmp2dev_handle {
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
-                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore})
+                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_tile_eps})
       if (p) cudaFree(p);
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     oz_otiles = nullptr;
     d_pstat = nullptr;
     d_fstore = nullptr;
+    d_tile_eps = nullptr;
     oz_m = 0;
   }
   // captured steps hold the addresses of every work buffer: any reallocation drops them first
@@ -264,6 +266,7 @@ struct mcmp2dev_handle {
       ck(cudaMalloc(&oz_otiles, sizeof(double) * 4096 * ntiles), "cudaMalloc oz o blocks");
       const size_t mq = size_t(16) * nbq;
       ck(cudaMalloc(&d_fstore, sizeof(double) * 4 * (mq * (mq - 1) / 2)), "cudaMalloc oz pair f values");
+      ck(cudaMalloc(&d_tile_eps, sizeof(double) * 2 * oz_ntiles(nbq, true)), "cudaMalloc oz tile estimates");
     }
     ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
     ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
@@ -336,6 +339,7 @@ struct mcmp2dev_handle {
       o.pstat = guarded ? d_pstat : nullptr;
       o.guard_tol = guard_tol;
       o.fstore = guarded ? d_fstore : nullptr;
+      o.tile_eps = guarded ? d_tile_eps : nullptr;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums

@@ -150,14 +150,28 @@ int oz_tiles(int nbq, int pw) {
 // ceil(len / pb) of them; a tile's P blocks past the row are skipped
 struct OzGroupWalk {
   int a = 0, g, pw, pb;
+  int rs = 0;  // tile index (pb = 1 numbering) of row a's first P block
   __device__ OzGroupWalk(int t0, int pw_, int pb_) : g(t0), pw(pw_), pb(pb_) { settle(); }
   __device__ int row_blocks() const { return (16 * (a + 1) + pw - 1) / pw; }
   __device__ int len() const { return (row_blocks() + pb - 1) / pb; }
   __device__ void settle() {
-    while (g >= len()) g -= len(), ++a;
+    while (g >= len()) g -= len(), rs += row_blocks(), ++a;
   }
   __device__ void next(int stride) { g += stride, settle(); }
 };
+// the refinement pass's choice for the tile group at w: the main pass's estimates of its P blocks
+// against the thresholds the main pass's last CTA set (each at most 1 / groups of the step's
+// budget, so the groups left unrefined carry at most the budget between them)
+__device__ __forceinline__ bool oz_refine_group(const OzParams& P, const OzGroupWalk& w) {
+  const int b0 = w.g * w.pb, nb = min(w.pb, w.row_blocks() - b0);
+  double ed = 0.0, ex = 0.0;
+  for (int j = 0; j < nb; ++j) {
+    const double2 e = reinterpret_cast<const double2*>(P.tile_eps)[w.rs + b0 + j];
+    ed += e.x, ex += e.y;
+  }
+  const volatile double* thr = P.st->oz_thr;
+  return ed > thr[0] || ex > thr[1] || ed + ex > thr[2];
+}
 __device__ int oz_group_tiles_dev(int nbq, int pw, int pb) {
   int n = 0;
   for (int a = 0; a < nbq; ++a) n += ((16 * (a + 1) + pw - 1) / pw + pb - 1) / pb;
@@ -376,6 +390,13 @@ __device__ unsigned long long g_oz_tl[160][TL_TILES][3 + 3 * EPW];
 #define TL(t, k, v)
 #endif
 
+// the CTA's estimate of one main-pass tile: the epilogue warps' sums in fixed order
+__device__ __forceinline__ void oz_store_tile_eps(const OzParams& P, const double2* te, int t) {
+  double e0 = 0.0, e1 = 0.0;
+  for (int w = 0; w < EPW; ++w) e0 += te[w].x, e1 += te[w].y;
+  reinterpret_cast<double2*>(P.tile_eps)[t] = make_double2(e0, e1);
+}
+
 template <bool FUSED, bool CORR>
 __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   using Sh = OzShape<FUSED, CORR>;
@@ -406,6 +427,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // FUSED: the f values of the last two tiles, [q 16][p PW] each (written before, read after the
   // epilogue warps' named barrier; two buffers so one barrier per tile suffices)
   __shared__ __align__(32) double4 s_f[2][FUSED ? 16 * PW : 1];
+  // main pass with a refinement pass behind it: each epilogue warp's estimate of the last two tiles
+  __shared__ double2 s_te[2][EPW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
   double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums
@@ -435,6 +458,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       uint32_t ph = 0;
       OzGroupWalk w(int(blockIdx.x), PW, PB);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
+        if constexpr (CORR)
+          if (P.tile_eps && !oz_refine_group(P, w)) continue;
         const int a = w.a, b0 = w.g * PB, nb = min(PB, w.row_blocks() - b0);
         const int8_t* ga = P.sa + size_t(a) * KS * A_KSM;
         const int8_t* gb = P.sb + size_t(b0) * KS * B_KSM;
@@ -451,14 +476,16 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     }
   } else if (warp == EPW + 1) {
     if (lane == 0) {  // MMA issuer: the slice products of each k-step into the tile's accumulators
-      int stage = 0;
+      int stage = 0, u = 0;  // u: tiles through TMEM (the refinement pass skips unrefined groups)
       uint32_t ph = 0;
       OzGroupWalk w(int(blockIdx.x), PW, PB);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
-        const int slot = it % NSLOT;
+        if constexpr (CORR)
+          if (P.tile_eps && !oz_refine_group(P, w)) continue;
+        const int slot = u % NSLOT;
         const int nb = min(PB, w.row_blocks() - w.g * PB);
         TL(it, 0, clock64());
-        mbar_wait(&tempty[slot], ((it / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
+        mbar_wait(&tempty[slot], ((u / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
         asm volatile("tcgen05.fence::after_thread_sync;");
         TL(it, 1, clock64());
         for (int ks = 0; ks < KS; ++ks) {
@@ -485,6 +512,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         }
         umma_commit(&tfull[slot]);
         TL(it, 2, clock64());
+        ++u;
       }
     }
   } else {  // epilogue: TMEM lane = A row; this warp's columns [c_lo, c_lo + CPW)
@@ -493,11 +521,65 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     const int q = row >> 3, plane = row & 1, exq = (row >> 1) & 3;
     OzGroupWalk w(int(blockIdx.x), PW, PB);
     int sub = 0;  // P blocks processed: the parity of the shared f buffer
+    int u = 0;    // tiles through TMEM
+    double te_d = 0.0, te_x = 0.0;  // main pass: this thread's estimate of the current tile
+    // one pair's literal term (estimator.cpp:26-32) from its f values into the thread's sums.
+    // Main pass: F is stored for a refinement pass. Refinement pass: F is this pass's correction
+    // to the stored f values (refined groups) or zero (groups left unrefined).
+    // Accuracy guard: the INT8 error of each f is modelled per element as a random sum over K' of
+    // slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v) with the row
+    // stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of 2^e sqrt(|x 2^-e|^2 /
+    // 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction with |o block|_F <=
+    // |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2) per pair, summed in
+    // quadrature over the step (the last CTA compares sqrt(sum eps^2) with guard_tol |sum|). On the
+    // oracle's cfg3/cfg4 steps this estimate is 3-250x the actual error
+    // (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x (tests/test_gpu_guard.py);
+    // it is a model, not a bound. Pairs of refined groups (one more slice and diagonal): 2^-49.
+    auto pair_term = [&](double4 F, int qg, int pg, bool refined) {
+      double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
+      if constexpr (CORR) {
+        const double4 f6 = *fs;
+        F.x += f6.x, F.y += f6.y, F.z += f6.z, F.w += f6.w;
+      } else if (fs) {
+        *fs = F;
+      }
+      const double td = (-P.w_direct * F.x) * F.y;    // f1d f2d
+      const double tx = (-P.w_exchange * F.z) * F.w;  // f1x f2x
+      acc_d += td;
+      acc_x += tx;
+      if (guard) {
+        const double kSig = CORR && refined ? 0x1p-49 : 0x1p-42;
+        const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
+        const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
+        const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
+        const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
+        const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
+        const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
+        const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
+        const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
+        const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
+        acc_ed += ed * ed;
+        acc_ex += ex * ex;
+        acc_ad += fabs(td);
+        acc_ax += fabs(tx);
+        if constexpr (!CORR) te_d += ed * ed, te_x += ex * ex;
+      }
+    };
     for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
       const int t = int(blockIdx.x) + it * int(gridDim.x);
       const int a = w.a, nbk = min(PB, w.row_blocks() - w.g * PB);
-      const int slot = it % NSLOT;
-      mbar_wait(&tfull[slot], (it / NSLOT) & 1);
+      if constexpr (CORR) {
+        if (P.tile_eps && !oz_refine_group(P, w)) {  // the main pass's terms and estimates stand
+          for (int j = 0; j < nbk; ++j)
+            for (int id = warp * 32 + lane; id < 16 * PW; id += 32 * EPW) {
+              const int qg = 16 * a + id / PW, pg = PW * (w.g * PB + j) + id % PW;
+              if (qg < P.m && pg < P.m && qg > pg) pair_term(make_double4(0.0, 0.0, 0.0, 0.0), qg, pg, false);
+            }
+          continue;
+        }
+      }
+      const int slot = u % NSLOT;
+      mbar_wait(&tfull[slot], (u / NSLOT) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) TL(it, 3 + 3 * warp, clock64());
       for (int j = 0; j < nbk; ++j, ++sub) {  // the tile's P blocks in turn (one in the main pass)
@@ -637,52 +719,29 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           if ((row & 7) == 0) sf[q * PW + c_lo / 8 + p] = make_double4(2.0 * g[2 * p], 2.0 * f11, 2.0 * f10, 2.0 * g[2 * p + 1]);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPW) : "memory");  // the tile's 16 x PW f values are parked
+        if constexpr (!CORR)
+          if (P.tile_eps && tid == 0 && sub > 0) oz_store_tile_eps(P, s_te[(sub - 1) & 1], t - int(gridDim.x));
         const int qg0 = 16 * a, pg0 = PW * b;
         for (int id = (warp * 32 + lane); id < 16 * PW; id += 32 * EPW) {
           const int q2 = id / PW, p2 = id % PW, qg = qg0 + q2, pg = pg0 + p2;
           if (!(qg < P.m && pg < P.m && qg > pg)) continue;
-          double4 F = sf[id];
-          double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
-          if constexpr (CORR) {  // f of the main pass plus this pass's corrections
-            const double4 f6 = *fs;
-            F.x += f6.x, F.y += f6.y, F.z += f6.z, F.w += f6.w;
-          } else if (fs) {
-            *fs = F;
-          }
-          const double td = (-P.w_direct * F.x) * F.y;    // f1d f2d
-          const double tx = (-P.w_exchange * F.z) * F.w;  // f1x f2x
-          acc_d += td;
-          acc_x += tx;
-          if (guard) {
-            // accuracy guard: the INT8 error of each f is modelled per element as a random sum over
-            // K' of slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v)
-            // with the row stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of
-            // 2^e sqrt(|x 2^-e|^2 / 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction
-            // with |o block|_F <= |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2)
-            // per pair, summed in quadrature over the step (the last CTA compares sqrt(sum eps^2)
-            // with guard_tol |sum|). On the oracle's cfg3/cfg4 steps this estimate is 3-250x the
-            // actual error (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x
-            // (tests/test_gpu_guard.py); it is a model, not a bound. After the refinement pass
-            // (one more slice and diagonal) the same model with 2^-49.
-            constexpr double kSig = CORR ? 0x1p-49 : 0x1p-42;
-            const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
-            const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
-            const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
-            const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
-            const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
-            const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
-            const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
-            const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
-            const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
-            acc_ed += ed * ed;
-            acc_ex += ex * ex;
-            acc_ad += fabs(td);
-            acc_ax += fabs(tx);
-          }
+          pair_term(sf[id], qg, pg, true);
         }
+        if constexpr (!CORR)
+          if (P.tile_eps) {  // this tile's estimate: warp sums now, the CTA's after the next barrier
+            double e0 = te_d, e1 = te_x;
+            te_d = te_x = 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              e0 += __shfl_down_sync(0xffffffffu, e0, o);
+              e1 += __shfl_down_sync(0xffffffffu, e1, o);
+            }
+            if (lane == 0) s_te[sub & 1][warp] = make_double2(e0, e1);
+          }
       }
       }  // P blocks of the tile
       if (lane == 0) TL(it, 5 + 3 * warp, clock64());
+      ++u;
     }
     if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
       double r[6] = {acc_d, acc_x, acc_ed, acc_ex, acc_ad, acc_ax};
@@ -698,6 +757,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  if constexpr (FUSED && !CORR)
+    if (P.tile_eps && tid == 0 && my > 0) oz_store_tile_eps(P, s_te[(my - 1) & 1], int(blockIdx.x) + (my - 1) * int(gridDim.x));
   if constexpr (FUSED) {  // per-CTA partials, then the last CTA's fixed-order sum (as pair_kr.cu)
     if (tid == 0) {
       const double cw = P.ng2 / P.st_ro->wtau;  // estimator.cpp:55
@@ -749,6 +810,17 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     } else {
       P.step_out[11] = trip && !P.fstore ? 2.0 : 0.0;
       if (trip) P.st->oz_trip = P.fstore ? 1 : 2;
+      if (trip && P.fstore && P.tile_eps) {
+        // the refinement pass refines the tile groups whose estimate exceeds 1 / groups of the
+        // step's budget (tol |sum|)^2 -- those left carry at most the budget between them -- and
+        // re-forms the others' terms from the stored f values (d, x carry cw, the estimates not)
+        const double cw = P.ng2 / P.st_ro->wtau;
+        const double ng = double(oz_group_tiles_dev(P.npts_oz / 32, OzShape<true, true>::PW, OzShape<true, true>::PB));
+        const double t2 = tol * tol / (cw * cw) / ng;
+        P.st->oz_thr[0] = t2 * d * d;
+        P.st->oz_thr[1] = t2 * x * x;
+        P.st->oz_thr[2] = t2 * (d + x) * (d + x);
+      }
     }
     P.st->done_pair = 0;
   }

@@ -103,9 +103,9 @@ def test_guard_off_and_on_agree_with_the_oracle(cfgdir):
 
 
 def test_refinement_pass_reduces_the_int8_error(cfgdir):
-    """A tolerance just below the main pass's estimate sends each step to the refinement pass
-    (7th slices, diagonal s + t = 6) and no further: the refined step is kept (fallback 1) and
-    its error against the oracle drops by about the slice radix (>= 8x here)."""
+    """A tolerance of 0.1 of the main pass's estimate sends each step to the refinement pass (7th
+    slices, diagonal s + t = 6, on the tile groups that carry the error) and no further: the
+    refined step is kept (fallback 1) and its error against the oracle drops >= 8x."""
     m = 192
     sp, text, tr = oracle_steps(cfgdir, "cfg3", m, 3, seed=31)
     dw = DeviceWalker(System(sp, text), max_walkers=m)
@@ -122,7 +122,10 @@ def test_refinement_pass_reduces_the_int8_error(cfgdir):
         for j in (2, 4):
             e_raw, e_ref = abs(r[j] - tr["est"][k, j]), abs(got[j] - tr["est"][k, j])
             assert e_ref <= e_raw / 8 + 1e-14 * abs(tr["est"][k, j]), (k, j, e_raw, e_ref)
-        assert got[F["est_err_direct"]] < r[F["est_err_direct"]] / 64
+        # selective refinement: the tile groups above 1 / groups of the budget get the 7th slice,
+        # so the refined step's estimate meets the tolerance it failed (0.1 of its estimate here)
+        assert got[F["est_err_direct"]] < r[F["est_err_direct"]] / 8
+        assert got[F["est_err_exchange"]] < r[F["est_err_exchange"]] / 8
 
 
 def test_constructed_ill_conditioned_step_trips_the_guard(cfgdir):
