@@ -631,6 +631,19 @@ def main():
         "gpu_launches": (8 if int8_path else 4) * my_steps,
         "step_values_checksum": float(np.sum(vals)),
     }
+    # which pair stage ran, and why not the INT8 V path when it did not (n_vir > 512, spinors not
+    # Kramers-paired within 1e-12, batched ensembles or m below ~180: mcmp2dev.cu oz_active)
+    if int8_path:
+        line["pair_path"] = "INT8 V blocks (tcgen05 kind::i8, 6-slice Ozaki, guarded) + DMMA O blocks"
+    else:
+        why = []
+        if not kramers:
+            why.append(f"spinor set not Kramers-paired within 1e-12 (deviation {dw.kramers_deviation():.3g})")
+        if sysd.n_vir > 512:
+            why.append(f"n_vir {sysd.n_vir} > 512")
+        if ens > 1:
+            why.append("batched ensembles")
+        line["pair_path"] = "DMMA only (INT8 V path inactive: " + ("; ".join(why) or "ensemble below the INT8 tiling size") + ")"
     if guard is not None:
         line["guard"] = dict(guard, note="INT8 steps checked / refined (7th slice) / recomputed on DMMA over the "
                                          "e2e interval; max_est_rel = largest estimated relative error of a kept step")
