@@ -196,6 +196,18 @@ int mcmp2dev_kramers_deviation(const mcmp2dev_t* h, double* deviation);
  * INT8 unguarded when selected); returns 1 when the INT8 V path is selected and the system is
  * eligible. Agreement with the FP64 path: see mcmp2dev_guard. */
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
+/* Energy-ordered truncation of the INT8 V-GEMM's K loop (on by default; exact). The virtual
+ * energies ascend (model.cpp:126-127) and Phi_v carries exp(-eps tau / 2), so at this step's tau
+ * the high-energy spinors may fall below the last slice of every row they appear in: their
+ * digits are all zero. oz_slice_kernel records, per point pair, the last 16-spinor k-step with
+ * a nonzero digit, and oz_vgemm_kernel runs each tile's k-steps only up to the smaller of its
+ * Q block's and P block's counts. The skipped slice products are exact zeros, so the step's sums
+ * are bit-identical to the full loop (tests/test_gpu_oz.py). mode -1 queries, 0 runs every
+ * k-step, 1 truncates; returns the active state. */
+int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode);
+/* out2 = {k-steps (32 of K' = 2 n_vir) issued by the main-pass V-GEMM launches since the INT8
+ * buffers were allocated, k-steps of one untruncated launch at the last step's sizes}. */
+int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2);
 /* Accuracy guard of the INT8 V path (literal estimator). After each INT8 step the V-GEMM's
  * last CTA compares the estimated error of the direct sum, the exchange sum and the step value
  * with tol times their magnitude. A step that fails (or is not finite) gets a refinement pass

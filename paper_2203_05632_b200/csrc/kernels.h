@@ -80,6 +80,10 @@ struct PairParams {
                              // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
   double* otiles;            // pair_kr only, single ensemble, literal: write the o blocks of every
                              // tile for oz_vgemm_kernel<true> and skip the V phase and the sums
+  const double* oscale;      // with otiles: the o values are stored times oscale[8 p + 4 e_p + y], the
+                             // power-of-two row scales of the INT8 V operands (OzParams::sb_scale of the
+                             // 10-walker P blocks), so the V-GEMM epilogue contracts them with the
+                             // integer sums directly; nullptr: unscaled
   int guard_fallback;        // pair_kr only: the INT8 path's guard launch -- exit at once unless
                              // st->oz_trip, else recompute the step on DMMA (writes step_out[0..5],
                              // clears oz_trip)
@@ -102,7 +106,7 @@ struct OzParams {
   double* sb_scale;          // [P blocks][nb_rows]: 2^e
   double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order (physical)
   // fused literal contraction (oz_vgemm_kernel<true>): o blocks in, the step's sums out
-  const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>
+  const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>, times the P rows' scales (sb_scale)
   int m;
   double ng2, w_direct, w_exchange;
   const DevState* st_ro;
@@ -118,6 +122,13 @@ struct OzParams {
                              // q (q - 1) / 2 + p), written by the main pass for the refinement pass
   double* tile_eps;          // [ntiles][2] the main pass's sum eps_d^2, sum eps_x^2 per tile: the
                              // refinement pass refines only the tile groups that carry the error
+  // active k-steps: K' is ordered by virtual energy (16 spinors' [re | im] per k-step), so the
+  // spinors whose exp(-eps tau / 2) leaves no digit in any slice sit in the trailing k-steps;
+  // oz_slice_kernel records each point pair's last k-step with a nonzero digit and the V-GEMM
+  // runs a tile's k-steps only up to min(Q block's, P block's) -- the products beyond are exact
+  // zeros, so the sums are bit-identical to the full K' loop. nullptr: every tile runs all ks.
+  uint8_t* ks_cnt;           // [npts_oz / 2]
+  unsigned long long* ks_exec;  // k-steps issued by the main-pass V-GEMM launches (cumulative)
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);

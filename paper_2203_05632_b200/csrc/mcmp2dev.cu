@@ -110,6 +110,11 @@ struct mcmp2dev_handle {
   double guard_tol = kGuardTol;
   double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
   double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
+  // per-tile k-step truncation of the INT8 V-GEMM (OzParams::ks_cnt): on by default, exact
+  bool oz_trunc = true;
+  uint8_t* d_ks_cnt = nullptr;             // [npts_oz / 2]
+  unsigned long long* d_ks_exec = nullptr; // k-steps issued by the main-pass V-GEMM launches
+  double oz_ks_full = 0;                   // k-steps of one untruncated launch (last launch's sizes)
   double* d_tile_eps = nullptr;  // [main tiles][2] the main pass's error estimate per tile
   long long guard_steps = 0, guard_refined = 0, guard_dmma = 0;
   double guard_max_est = 0.0;  // largest estimated relative error of a step kept on INT8
@@ -156,14 +161,14 @@ struct mcmp2dev_handle {
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   double* d_gsteps = nullptr;  // [kGraphSteps][kStepDoubles] step results written by the graph
   struct GraphKey {
-    int m = -1, kramers = -1, nens = 1, oz = -1;
+    int m = -1, kramers = -1, nens = 1, oz = -1, trunc = -1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
     double guard_tol = -1.0;
     bool operator==(const GraphKey&) const = default;
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, k0, k1, rstream, guard_tol};
+    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, oz_trunc ? 1 : 0, k0, k1, rstream, guard_tol};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -222,8 +227,11 @@ struct mcmp2dev_handle {
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
-                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_tile_eps})
+                    (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_tile_eps, (void*)d_ks_cnt,
+                    (void*)d_ks_exec})
       if (p) cudaFree(p);
+    d_ks_cnt = nullptr;
+    d_ks_exec = nullptr;
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     oz_otiles = nullptr;
@@ -270,6 +278,10 @@ struct mcmp2dev_handle {
     }
     ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
     ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
+    ck(cudaMalloc(&d_ks_cnt, npts_oz / 2), "cudaMalloc oz k-step counts");
+    ck(cudaMemset(d_ks_cnt, 0, npts_oz / 2), "memset oz k-step counts");
+    ck(cudaMalloc(&d_ks_exec, sizeof(unsigned long long)), "cudaMalloc oz k-step counter");
+    ck(cudaMemset(d_ks_exec, 0, sizeof(unsigned long long)), "memset oz k-step counter");
     oz_m = 16 * nbq;
   }
 
@@ -340,10 +352,13 @@ struct mcmp2dev_handle {
       o.guard_tol = guard_tol;
       o.fstore = guarded ? d_fstore : nullptr;
       o.tile_eps = guarded ? d_tile_eps : nullptr;
+      o.ks_cnt = oz_trunc ? d_ks_cnt : nullptr;
+      o.ks_exec = d_ks_exec;
       launch_oz_slice(o, stream);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
         p.otiles = oz_otiles;
+        p.oscale = o.sb_scale;
         if (OZ_O_PW4) {
           const int wmax = std::min(KC4, std::max(Go, 1));
           pair_kr_ring_pw4(wmax, p.ring, p.ring_doubles);
@@ -368,6 +383,7 @@ struct mcmp2dev_handle {
         launch_pair_kr(p, stream);
       }
       oz_ops = oz_int8_ops(o);
+      oz_ks_full = double(o.ntiles) * o.ks;
     } else if (kramers && qb1) {
       launch_pair_kr_qb1(p, stream);
     } else if (kramers) {
@@ -1376,6 +1392,25 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode) {
   if (mode == 0) h->oz = false;
   if (mode == 1) h->oz = true;
   return h->oz && h->kramers && h->n_vir > 0 && h->n_vir <= 512 ? 1 : 0;
+}
+
+int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode) {
+  if (!h) return -1;
+  if (mode == 0) h->oz_trunc = false;
+  if (mode == 1) h->oz_trunc = true;
+  return h->oz_trunc ? 1 : 0;
+}
+
+int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2) {
+  return guard(h, [&] {
+    out2[0] = out2[1] = 0.0;
+    if (!h->d_ks_exec) return;
+    unsigned long long n = 0;
+    ck(cudaStreamSynchronize(h->stream), "stream sync");
+    ck(cudaMemcpy(&n, h->d_ks_exec, sizeof n, cudaMemcpyDeviceToHost), "k-step counter D2H");
+    out2[0] = double(n);
+    out2[1] = h->oz_ks_full;
+  });
 }
 
 int mcmp2dev_synchronize(mcmp2dev_t* h) {

@@ -150,7 +150,7 @@ __host__ __device__ constexpr int kr_ntiles(int nb) {
 // OZ (single ensembles, pair_oz.cu; the ring streams the occupied chunks only):
 //  1: the V blocks come precomputed per tile (P.vtiles); the V phase becomes one load per lane
 //     and (h, pp) -- the physical estimator;
-//  2: O only: the tile's o values go to HBM (P.otiles, [q][x_alpha][re/im][p][e_p][y] doubles)
+//  2: O only: the tile's o values go to HBM (P.otiles, [Q block row][p][q][x_alpha][re/im][e_p][y] doubles)
 //     and oz_vgemm_kernel<true> contracts them with its V blocks -- the literal estimator
 template <bool PHYS, int OZ>
 __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairParams P) {
@@ -306,7 +306,15 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
         }
         const int y = (lane >> 2) & 3, pp = lane & 3;
         if constexpr (OZ == 2) {  // o = conj O~ to the tile's O block in HBM; no V phase here
-          double* ot = P.otiles + size_t(tt) * 4096;
+          // [Q block row ta][p walker][q 16][x_alpha][re/im][e_p][y]: the P walkers of the row are
+          // contiguous, so any 10-walker P block of the V-GEMM's tiles is one bulk copy
+          double* ot = P.otiles + size_t(ta) * (ta + 1) * 4096 + size_t(p0) * 512;
+          // times the power-of-two scale of the V operand row (p, e_p, y) this value meets in the
+          // V-GEMM epilogue (exact)
+          double osc[NB1];
+#pragma unroll
+          for (int n = 0; n < NB1; ++n)
+            osc[n] = P.oscale ? P.oscale[size_t(p0 + 4 * (NB1 * p1w + n) + pp) * 8 + 4 * e1 + y] : 1.0;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -314,9 +322,9 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
-                double* d = ot + (q * 4 + j * 2) * 64 + (p * 2 + e1) * 4 + y;
-                __stcg(d, t1[h][n][j] + t2[h][n][j]);
-                __stcg(d + 64, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]));
+                double* d = ot + p * 512 + q * 32 + j * 16 + e1 * 4 + y;
+                __stcg(d, (t1[h][n][j] + t2[h][n][j]) * osc[n]);
+                __stcg(d + 8, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]) * osc[n]);
               }
           continue;
         }

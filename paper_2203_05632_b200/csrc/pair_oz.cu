@@ -63,6 +63,7 @@ constexpr int STAGES = OZ_STAGES;
 constexpr int EPW = OZ_EPW;
 constexpr int THREADS = (EPW + 2) * 32;
 constexpr int TMEM_COLS = 512;      // 6 x NB used
+constexpr int KA_MAX = 1024, KB_MAX = 2048;  // Q / P blocks with per-block k-step counts in shared memory
 // B rows (P side) per tile: 8 walkers (64 rows, the V tiles of the physical path follow
 // pair_kr's 16 x 8 tiles) or 10 walkers (80 rows, the fused literal path: a kind::i8 M128 MMA
 // costs the same ~61 cycles for N = 32..80 (tools/umma_rate.cu), so N = 80 -- the widest that
@@ -82,8 +83,13 @@ struct OzShape {
   static constexpr int NSL = CORR ? SL : S;   // slices copied per k-step
   static constexpr int A_CP = NSL * MA * 32, B_CP = NSL * NB * 32;
   static constexpr int STAGE = A_CP + PB * B_CP;
-  static constexpr int NSTAGE = CORR ? (227 * 1024 - 16 * 1024) / STAGE : STAGES;
-  static constexpr int SMEM_BYTES = NSTAGE * STAGE;
+  // main fused pass: the tile's o values (16 x PW walker pairs x 32 doubles, one bulk copy from
+  // the O pass's [Q block row][p walker][q][x_alpha][re/im][e_p][y] layout) double-buffered in
+  // shared memory next to a 3-stage ring (3 / 4 / 5 stages measured alike), so the epilogue never
+  // waits on HBM for them
+  static constexpr int OT_BYTES = FUSED && !CORR ? PW * 16 * 32 * 8 : 0;
+  static constexpr int NSTAGE = CORR ? (227 * 1024 - 16 * 1024) / STAGE : FUSED ? 3 : STAGES;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE + 2 * OT_BYTES;
   static constexpr int NACC = CORR ? 1 : S;   // accumulators per P block (slice diagonals)
   static constexpr int NSLOT = CORR ? 512 / (PB * NB) : 1;  // tiles in flight in TMEM
   static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
@@ -232,6 +238,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   pdl_wait();
   pdl_trigger();
   __shared__ double s_st[8][3];
+  __shared__ int s_k[8];
   // one warp per (point, channel): 8 warps = 2 points per CTA (npts_oz is a multiple of 32, so
   // every CTA's points exist)
   const int wg = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
@@ -247,6 +254,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
   int8_t* const sb = P.sb + size_t(pb) * ks_n * SL * NB * 32;
   const bool stats = P.pstat != nullptr;
   double ss = 0.0, nbig = 0.0, n2 = 0.0, row_scale = 1.0;
+  int kact = 0;  // k-steps up to this lane's last nonzero digit
   {
     // this lane's spinor quads a0 = 4 (lane + 32 j); two passes over them (the row maximum, then
     // the digits), the second from L1, so no values are held across the reduction
@@ -306,7 +314,16 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
       uint32_t dr[SL], di[SL];
       digits4(xr, dr);
       digits4(xi, di);
-      const int kre = 4 * qd, kim = KH + 4 * qd;  // K' positions of the re and im halves
+      // K' positions: k-step qd / 4 holds spinors 16 (qd / 4) .. + 15 as [re (16) | im (16)], so
+      // K' follows the virtual energies (ascending, model.cpp:126-127) and the spinors that
+      // exp(-eps tau / 2) has pushed below the last slice fill the trailing k-steps with zeros
+      const int kre = (qd >> 2) * 32 + (qd & 3) * 4, kim = kre + 16;
+      {
+        uint32_t any = 0;
+#pragma unroll
+        for (int s = 0; s < SL; ++s) any |= dr[s] | di[s];
+        if (any) kact = max(kact, (qd >> 2) + 1);
+      }
 #pragma unroll
       for (int s = 0; s < SL; ++s) {
         // B row [re | im]
@@ -332,6 +349,17 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
         load(qd, xr, xi);
         emit(qd, xr, xi);
       }
+    }
+  }
+  if (P.ks_cnt) {  // the CTA's point pair: k-steps up to the last nonzero digit of its 8 rows
+    kact = __reduce_max_sync(0xffffffffu, kact);
+    if (lane == 0) s_k[int(threadIdx.x) >> 5] = kact;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) k = max(k, s_k[w]);
+      P.ks_cnt[blockIdx.x] = uint8_t(k);
     }
   }
   if (!stats) return;  // uniform over the grid
@@ -420,7 +448,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   // releasing each diagonal at once, with the next tile's first k-step issued diagonal by
   // diagonal, 1.475 vs 1.35 ms (tile period 30.5k vs 28.75k cycles: TMEM reads under the
   // restarted MMAs slow both).
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[NSLOT], tempty[NSLOT];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[NSLOT], tempty[NSLOT], ofull[2], oempty[2];
+  constexpr bool OSM = Sh::OT_BYTES > 0;  // o values through shared memory
   __shared__ uint32_t tmem_base;
   __shared__ double s_red[EPW][6];
   __shared__ bool s_last;
@@ -431,6 +460,33 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   __shared__ double2 s_te[2][EPW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KS = P.ks;
+  // active k-steps of each Q block (32 points) and P block (NB / 4 points) from the slice
+  // kernel's per-point-pair records: a tile runs min(Q block's, P blocks') k-steps (at least one)
+  __shared__ uint8_t s_ka[KA_MAX], s_kb[KB_MAX];
+  const int nqa = P.npts_oz / 32, npb = (P.npts_oz + NB / 4 - 1) / (NB / 4);
+  const bool trunc = P.ks_cnt != nullptr && nqa <= KA_MAX && npb <= KB_MAX;
+  if (trunc) {
+    const int ncnt = P.npts_oz / 2;
+    for (int i = tid; i < nqa; i += THREADS) {
+      const uint4 v = *reinterpret_cast<const uint4*>(P.ks_cnt + 16 * i);
+      uint32_t mx = __vmaxu4(__vmaxu4(v.x, v.y), __vmaxu4(v.z, v.w));
+      mx = __vmaxu4(mx, mx >> 16);
+      s_ka[i] = uint8_t(max(mx & 0xFFu, (mx >> 8) & 0xFFu));
+    }
+    constexpr int BC = NB / 8;  // records per P block
+    for (int i = tid; i < npb; i += THREADS) {
+      int mx = 0;
+      for (int j = 0; j < BC; ++j)
+        if (BC * i + j < ncnt) mx = max(mx, int(P.ks_cnt[BC * i + j]));
+      s_kb[i] = uint8_t(mx);
+    }
+  }
+  auto tile_ks = [&](int a, int b0, int nb) {
+    if (!trunc) return KS;
+    int kb = 0;
+    for (int j = 0; j < nb; ++j) kb = max(kb, int(s_kb[b0 + j]));
+    return max(1, min(min(int(s_ka[a]), kb), KS));
+  };
   double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums
   // FUSED, guard: sums of the squared per-pair error estimates and of |pair term|
   double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
@@ -438,6 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     for (int s = 0; s < NSLOT; ++s) mbar_init(&tfull[s], 1), mbar_init(&tempty[s], 32 * EPW);
+    for (int s = 0; s < 2; ++s) mbar_init(&ofull[s], 1), mbar_init(&oempty[s], EPW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -456,6 +513,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
       int stage = 0;
       uint32_t ph = 0;
+      unsigned long long issued = 0;  // k-steps of this CTA's tiles
       OzGroupWalk w(int(blockIdx.x), PW, PB);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
         if constexpr (CORR)
@@ -463,7 +521,16 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         const int a = w.a, b0 = w.g * PB, nb = min(PB, w.row_blocks() - b0);
         const int8_t* ga = P.sa + size_t(a) * KS * A_KSM;
         const int8_t* gb = P.sb + size_t(b0) * KS * B_KSM;
-        for (int ks = 0; ks < KS; ++ks) {
+        const int nk = tile_ks(a, b0, nb);
+        if constexpr (!CORR) issued += nk;
+        if constexpr (OSM) {  // the tile's o values: walkers PW b0 .. of Q block row a (up to the diagonal)
+          const int ob = it & 1, np = min(PW, 16 * (a + 1) - PW * b0);
+          mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1u);
+          mbar_expect_tx(&ofull[ob], np * 4096);
+          bulk_g2s(sm + NST * STAGE + ob * Sh::OT_BYTES, P.otiles + size_t(a) * (a + 1) * 4096 + size_t(PW * b0) * 512,
+                   np * 4096, &ofull[ob]);
+        }
+        for (int ks = 0; ks < nk; ++ks) {
           mbar_wait(&empty[stage], ph ^ 1u);
           int8_t* dst = sm + stage * STAGE;
           mbar_expect_tx(&full[stage], A_CP + nb * B_CP);
@@ -473,6 +540,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           if (++stage == NST) stage = 0, ph ^= 1u;
         }
       }
+      if constexpr (!CORR)
+        if (P.ks_exec) atomicAdd(P.ks_exec, issued);
     }
   } else if (warp == EPW + 1) {
     if (lane == 0) {  // MMA issuer: the slice products of each k-step into the tile's accumulators
@@ -488,7 +557,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         mbar_wait(&tempty[slot], ((u / NSLOT) & 1) ^ 1u);  // the epilogue has drained this slot
         asm volatile("tcgen05.fence::after_thread_sync;");
         TL(it, 1, clock64());
-        for (int ks = 0; ks < KS; ++ks) {
+        const int nk = tile_ks(w.a, w.g * PB, nb);
+        for (int ks = 0; ks < nk; ++ks) {
           mbar_wait(&full[stage], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const int8_t* sa = sm + stage * STAGE;
@@ -643,7 +713,12 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // pass): its instruction stream competes with the MMA-issuing warp for issue slots. So the
         // FP64 form stays and the per-pair terms are packed into whole warps after the named barrier
         // (1.42 -> 1.35 ms with the guard's estimate; 1.29 ms with no contraction at all).
-        const int row_o = (q * 4 + ((row >> 1) & 1) * 2 + plane) * 64;
+        const int row_o = q * 32 + ((row >> 1) & 1) * 16 + plane * 8;  // + p 512 + e_p 4 + y
+        const double* so = nullptr;
+        if constexpr (OSM) {
+          mbar_wait(&ofull[u & 1], (u >> 1) & 1);
+          so = reinterpret_cast<const double*>(sm + NST * STAGE + (u & 1) * Sh::OT_BYTES);
+        }
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
         double g[NK];
         // the refinement pass has too few MMAs to hide the o-tile loads behind: load all of this
@@ -654,7 +729,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
 #pragma unroll
           for (int k = 0; k < NK; ++k) {
             const int pg = min(PW * b + (c_lo + 4 * k) / 8, 16 * (a + 1) - 1);
-            const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
+            const double* o = P.otiles + size_t(a) * (a + 1) * 4096 + size_t(pg) * 512 + row_o + (k & 1) * 4;
             opf[k][0] = __ldcs(reinterpret_cast<const longlong2*>(o));
             opf[k][1] = __ldcs(reinterpret_cast<const longlong2*>(o + 2));
           }
@@ -665,12 +740,13 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           double sgp = 0.0;
           if (pg < 16 * (a + 1)) {
             if constexpr (!CORR) {
-              const double* o = P.otiles + size_t(a * (a + 1) + pg / 8) * 4096 + row_o + ((pg & 7) * 2 + (k & 1)) * 4;
-              const double2 o01 = __ldcs(reinterpret_cast<const double2*>(o));
-              const double2 o23 = __ldcs(reinterpret_cast<const double2*>(o + 2));
-              const double v0 = double(X[4 * k]) * sr * sbv[4 * k], v1 = double(X[4 * k + 1]) * sr * sbv[4 * k + 1];
-              const double v2 = double(X[4 * k + 2]) * sr * sbv[4 * k + 2], v3 = double(X[4 * k + 3]) * sr * sbv[4 * k + 3];
-              sgp = (o01.x * v0 + o01.y * v1) + (o23.x * v2 + o23.y * v3);
+              const double* o = so + ((c_lo + 4 * k) / 8) * 512 + row_o + (k & 1) * 4;
+              const double2 o01 = *reinterpret_cast<const double2*>(o);
+              const double2 o23 = *reinterpret_cast<const double2*>(o + 2);
+              // the o values carry the P rows' scales (pair_kr's O pass), the Q row's follows below:
+              // five FP64 operations per quad beside the conversions
+              sgp = (o01.x * double(X[4 * k]) + o01.y * double(X[4 * k + 1])) +
+                    (o23.x * double(X[4 * k + 2]) + o23.y * double(X[4 * k + 3]));
             } else {
               // the refinement's correction df = sum o dV is ~2^-42 of f, so FP32 carries it with
               // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
@@ -682,7 +758,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
 #pragma unroll
               for (int y = 0; y < 4; ++y) {
                 const int ex = int((ob[y] >> 52) & 0x7FF);  // zero / subnormal o: dropped
-                E[y] = ex ? ex + int((__double_as_longlong(sbv[4 * k + y]) >> 52) & 0x7FF) : 0;
+                E[y] = ex ? ex + 1023 : 0;                  // (the P row's scale is in o already)
                 emax = max(emax, E[y]);
               }
               float acc = 0.0f;
@@ -694,14 +770,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
                                  __int_as_float((127 + dsh) << 23);
                 acc = fmaf(ob[y] < 0 ? -mf : mf, __int2float_rn(int(X[4 * k + y])), acc);
               }
-              if (emax) {  // sum = acc 2^(emax - 2046) sr, sr = 2^(srx - 1023)
-                const int tt = emax + int((__double_as_longlong(sr) >> 52) & 0x7FF) - 3069;
+              if (emax) {  // sum = acc 2^(emax - 2046) (the Q row's scale sr follows below)
+                const int tt = emax - 2046;
                 const double scale = (tt > -1023 && tt < 1024) ? __longlong_as_double((long long)(tt + 1023) << 52) : ldexp(1.0, tt);
                 sgp = double(acc) * scale;
               }
             }
           }
-          g[k] = plane ? -sgp : sgp;
+          g[k] = sgp * (plane ? -sr : sr);
+        }
+        if constexpr (OSM) {  // this warp is done with the o buffer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&oempty[u & 1]);
         }
 #pragma unroll
         for (int k = 0; k < NK; ++k) {

@@ -270,6 +270,17 @@ class DeviceWalker:
         it runs for single ensembles whose 16 x 8 pair tiles cover the SMs (m >= ~180)."""
         return bool(self._d.mcmp2dev_pair_path(self._h, mode))
 
+    def int8_truncation(self, mode: int = -1) -> bool:
+        """Energy-ordered truncation of the INT8 V-GEMM's K loop (exact; on by default):
+        -1 query, 0 every k-step, 1 only the k-steps that hold a nonzero digit."""
+        return bool(self._d.mcmp2dev_oz_truncation(self._h, mode))
+
+    def int8_ksteps(self) -> tuple[float, float]:
+        """(k-steps issued by the main-pass V-GEMM launches so far, k-steps of one full launch)."""
+        o = np.zeros(2)
+        check_dev(self._d.mcmp2dev_oz_ksteps(self._h, dptr(o)), self._h)
+        return float(o[0]), float(o[1])
+
     @property
     def stream_ptr(self) -> int:
         return int(self._d.mcmp2dev_stream(self._h))

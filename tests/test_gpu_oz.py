@@ -144,3 +144,41 @@ def test_int8_v_two_pass_slicing_wide_set(tmp_path):
     dw.int8_v(0)
     dmma = dw.replay(tr["walkers"], tr["tau"])
     assert rel_err(dmma[:, 0], tr["est"][:, 0]) < REL
+
+
+@pytest.mark.parametrize("name,m", [("cfg3", 256), ("cfg4", 192), ("cfg5-36", 330)])
+def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
+    """The V-GEMM skips a tile's trailing k-steps when every digit there is zero (high virtual
+    energies at this tau, include/mcmp2dev.h mcmp2dev_oz_truncation): the skipped products are
+    exact zeros, so every field of the step records is bit-identical to the full K' loop; at
+    large tau k-steps are actually skipped, at tau -> 0 none are; the oracle still agrees."""
+    from paper_2203_05632_b200 import generate_config
+    if (cfgdir / f"{name}.spinor").exists():
+        sp, text = cfgdir / f"{name}.spinor", (cfgdir / f"{name}.conf").read_text()
+    else:
+        sp, conf = generate_config(name, tmp_path)
+        text = conf.read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=31, stream=0, m=m, burn=20, nsteps=1)
+    taus = np.array([1e-6, 0.05, 0.7, 3.0])
+    walkers = np.repeat(tr["walkers"][:1], len(taus), axis=0)
+    dw = DeviceWalker(System(sp, text), max_walkers=m)
+    assert dw.int8_v() and dw.int8_truncation()
+    frac = []
+    on = []
+    for k, tau in enumerate(taus):  # one replay per tau, to read the k-steps each one issued
+        e0, full = dw.int8_ksteps()
+        on.append(dw.replay_ex(walkers[k:k + 1], taus[k:k + 1]))
+        e1, full = dw.int8_ksteps()
+        frac.append((e1 - e0) / full)
+    on = np.concatenate(on)
+    assert not dw.int8_truncation(0)
+    e0, full = dw.int8_ksteps()
+    off = dw.replay_ex(walkers, taus)
+    e1, _ = dw.int8_ksteps()
+    assert e1 - e0 == len(taus) * full
+    assert on.tobytes() == off.tobytes()
+    assert frac[0] > 0.99 and frac[-1] < 0.8 and all(a >= b for a, b in zip(frac, frac[1:])), frac
+    ref = orc.replay(walkers, taus)
+    for c, r in ((0, 0), (2, 2), (4, 4)):
+        assert rel_err(on[:, c], ref[:, r]) < REL, (c, frac)
