@@ -74,6 +74,10 @@ constexpr int KA_MAX = 1024, KB_MAX = 2048;  // Q / P blocks with per-block k-st
 #ifndef OZ_REFINE_PB
 #define OZ_REFINE_PB 3
 #endif
+// instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N columns
+__host__ __device__ constexpr uint32_t oz_idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
 template <bool FUSED, bool CORR = false>
 struct OzShape {
   static constexpr int NB = FUSED ? 80 : 64;
@@ -93,9 +97,7 @@ struct OzShape {
   static constexpr int NACC = CORR ? 1 : S;   // accumulators per P block (slice diagonals)
   static constexpr int NSLOT = CORR ? 512 / (PB * NB) : 1;  // tiles in flight in TMEM
   static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
-  // instruction descriptor: s32 accumulator, s8 x s8, both K-major, M = 128, N = NB
-  static constexpr uint32_t IDESC =
-      (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(MA >> 4) << 24);
+  static constexpr uint32_t IDESC = oz_idesc(NB);
 };
 static_assert(OzShape<true>::SMEM_BYTES <= 227 * 1024, "stage ring");
 static_assert(OzShape<true, true>::SMEM_BYTES <= 227 * 1024, "stage ring");
@@ -133,6 +135,31 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t* v) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(addr));
+}
+
+// One k-step's slice products of the main pass. A slice s meets B slices t = 0 .. S-1-s, and the
+// product (s, t) belongs to the accumulator of diagonal s + t at TMEM columns (s + t) NB. The B
+// slices of a stage are consecutive in shared memory ([slice][NB rows x 32], every slice whole
+// 8-row groups of the canonical layout) and so are the accumulators in TMEM, so A_s x [B_0; ..;
+// B_{S-1-s}] is ONE GEMM of N = NB (S - s) columns landing on diagonals s .. S-1 -- issued as one
+// MMA, or two halves when N > 256: 9 MMAs per k-step instead of 21 for the same products. The
+// kernel is bound by shared-memory operand reads (an SS-mode MMA reads 128 x 32 B of A and
+// N x 32 B of B; 21 N = 80 MMAs read 136 KB per k-step, next to the 39 KB the ring's fills write,
+// against 128 B/clk); the merged MMAs read each A slice once or twice instead of 6 - s times
+// (88 KB per k-step) and run at the dense rate (N >= 160 is compute-bound).
+// The first write of every diagonal is by A slice 0 (acc0 = 0 on k-step 0), the others accumulate.
+template <int NB, int s>
+__device__ __forceinline__ void oz_issue_diagonals(uint32_t tmem, const int8_t* sa, const int8_t* sb, uint32_t acc0) {
+  if constexpr (s < S) {
+    constexpr int TOT = NB * (S - s);
+    constexpr int N0 = TOT > 256 ? (TOT / 2 + 15) / 16 * 16 : TOT, N1 = TOT - N0;
+    static_assert(N0 % 16 == 0 && N0 <= 256 && N1 % 16 == 0 && N1 <= 256, "MMA N");
+    const uint64_t da = umma_desc(sa + s * MA * 32);
+    const uint32_t acc = s == 0 ? acc0 : 1u;
+    umma_i8<oz_idesc(N0)>(tmem + uint32_t(s * NB), da, umma_desc(sb), acc);
+    if constexpr (N1 > 0) umma_i8<oz_idesc(N1)>(tmem + uint32_t(s * NB + N0), da, umma_desc(sb + N0 * 32), acc);
+    oz_issue_diagonals<NB, s + 1>(tmem, sa, sb, acc0);
+  }
 }
 
 // the tile triangle, row by row: Q block a (walkers 16a ..) holds P blocks b < ceil(16 (a+1) / pw)
@@ -570,12 +597,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
                 umma_i8<Sh::IDESC>(tmem + uint32_t((slot * PB + j) * NB), umma_desc(sa + s * MA * 32),
                                    umma_desc(sb + j * B_CP + (SL - 1 - s) * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
           } else {
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-#pragma unroll
-              for (int t = 0; s + t < S; ++t)  // the first write of diagonal d is (s 0, t d) of k-step 0
-                umma_i8<Sh::IDESC>(tmem + uint32_t((s + t) * NB), umma_desc(sa + s * MA * 32),
-                                   umma_desc(sb + t * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
+            oz_issue_diagonals<NB, 0>(tmem, sa, sb, ks > 0 ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // the stage is free once these MMAs have read it
           if (++stage == NST) stage = 0, ph ^= 1u;

@@ -2,7 +2,7 @@
 the MMA issuer's wait for the accumulators and each epilogue warp's drain and contraction, in
 SM cycles. Build: make -C paper_2203_05632_b200/csrc OUT=../lib_tl OBJ=build_tl
 EXTRA_NVFLAGS=-DOZ_TIMELINE && cp paper_2203_05632_b200/lib/libmcmp2host.so paper_2203_05632_b200/lib_tl/
-usage: MCMP2_LIBDIR=paper_2203_05632_b200/lib_tl python tools/oz_timeline.py [cfg4] [tol]
+usage: MCMP2_LIBDIR=paper_2203_05632_b200/lib_tl python tools/oz_timeline.py [cfg4] [tol] [tau]
 (tol 1e-300 forces the guard's refinement pass; its stamps then overwrite the main pass's)"""
 import ctypes as C
 import json
@@ -25,6 +25,8 @@ with tempfile.TemporaryDirectory() as d:
     dw.init_ensemble(m, seed=1)
     dw.burn_in(20)
     dw.advance(3)
+    if len(sys.argv) > 3:  # one replayed step at a chosen tau (the k-step truncation follows it)
+        dw.replay(dw.get_ensemble().walkers[:, :8][None], np.array([float(sys.argv[3])]))
     buf = np.zeros((CTAS, TILES, 3 + 3 * EPW), dtype=np.uint64)
     f = native.dev().mcmp2dev_debug_oz_timeline
     f.argtypes = [C.c_void_p, C.c_size_t]
