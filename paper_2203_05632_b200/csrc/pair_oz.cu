@@ -11,14 +11,16 @@
 // and B (P side) 8 PW rows: (p walker PW, e_p 2, y 4); PW = 10 (N = 80) for the literal
 // estimator, PW = 8 (N = 64, pair_kr's own 16 x 8 tiles) for the physical one.
 //
-// Ozaki splitting: every row (point, channel) is scaled by its power-of-two maximum 2^e and cut
-// into six signed 7-bit slices (rounded digits), x 2^-e = sum_s d_s 2^(-7 (s + 1)), |d_s| <= 127. The 21 slice
-// products with s + t <= 5 are exact int8 x int8 -> int32 UMMA products; those of one diagonal
-// d = s + t accumulate in one TMEM accumulator (|acc| < 6 K' 127^2 < 2^31). The epilogue merges
-// the six accumulators exactly into one int64 per element (X = sum_d acc_d 128^(5-d), |X| < 2^59)
-// and rounds once to FP64: V = X 2^(e_q + e_p - 49). The error (slice remainders and the dropped
-// products s + t > 5) is ~2^-42 of |row_q| |row_p| K' -- the precision budget pinned on the
-// oracle by tests/test_ozaki_budget.py.
+// Ozaki splitting: every row (point, channel) is scaled by a power of two 2^e (|x| 2^-e < 127.5 / 128)
+// and cut into six int8 slices of balanced radix-256 digits, x 2^-e = sum_s d_s 2^-(7 + 8 s),
+// d_s in [-128, 127] (digits4). The 21 slice products with s + t <= 5 are exact int8 x int8 -> int32
+// UMMA products; those of one diagonal d = s + t accumulate in one TMEM accumulator
+// (|acc| <= 6 K' 2^14 < 2^31). The epilogue merges the accumulators into one int64 per element,
+// X = sum_{d <= 4} acc_d 256^(4-d) + rint(acc_5 / 256) (|X| < 2^56; all six would not fit 63
+// bits) and rounds once to FP64: V = X 2^(e_q + e_p - 46). The error (slice remainders <= 2^-48
+// and the dropped products s + t > 5) is ~2^-46 of |row_q| |row_p| sqrt(K') -- 16x below the
+// rounded 7-bit digits of round 1 at the same 21 products, pinned on the oracle by
+// tests/test_ozaki_budget.py.
 //
 // Kernels per step (after mo_kernel):
 //  * oz_slice_kernel: one warp per (point, channel): the row exponent, the six slices of the
@@ -216,42 +218,32 @@ int oz_group_tiles(int nbq, int pw, int pb) {
   return n;
 }
 
-// six signed digits of 4 values in (-1, 1): x = sum_s d_s 128^-(s+1) + rem, each digit the
-// nearest integer clamped to [-127, 127] (a clamped digit carries its excess into the next one;
-// all steps exact in FP64). Rounded digits are centred and, after the first, mostly |d| <= 64:
-// on the oracle's cfg3 inputs the step's exchange sum is 20x closer to FP64 than with truncated
-// digits (7e-12 vs 1.2e-10 relative), at the same 21 products (tests/test_ozaki_budget.py)
-// Three FP64 operations per digit (the kernel is FP64-issue-bound): t = r 128 + 1.5 2^52 rounds
-// r 128 to the nearest integer (ties to even, as rint) and leaves it in t's low mantissa bits (two's
-// complement), so no rint / clamp / conversion is needed unless the digit must be clamped (only
-// after |x 128| > 127.5); the remainder r 128 - q is exact. Digits identical to the
-// rint / fmin / fmax form.
-__device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[SL]) {
-  constexpr double kRound = 6755399441055744.0;  // 1.5 * 2^52
-  double r[4] = {x[0], x[1], x[2], x[3]};
+// SL balanced radix-256 digits of 4 values, |x| < 127.5 / 128 (the row scale guarantees it):
+//   x = d_0 2^-7 + sum_{s >= 1} d_s 2^-(7 + 8 s) + rem,  d_s in [-128, 127] (d_0 in [-127, 127]),
+// read off the integer X = rint(x 2^(7 + 8 (SL - 1))) from the low end: d = the signed low byte,
+// X <- (X - d) / 256. The first S digits are then the S-slice representation rounded to nearest
+// (|rem| <= 2^-(8 + 8 (S - 1))), one bit per slice more than rounded 7-bit digits in the same
+// int8 operands: the six-slice sums are ~16x closer to FP64 at the same 21 products
+// (tests/test_ozaki_budget.py). One FP64 multiply and one conversion per value, the rest
+// integer work. A balanced digit -128 has no negative, so the negated rows of the A operand
+// take the digits of -x (neg = true), not negated digits.
+__device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[SL], bool neg = false) {
+  constexpr double kScale = double(1ull << (7 + 8 * (SL - 1)));
+  long long X[4];
 #pragma unroll
-  for (int s = 0; s < SL; ++s) {
-    uint32_t w = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double t = fma(r[i], 128.0, kRound);
-      double qd = t - kRound;
-      int q = __double2loint(t);
-      if (q > 127 || q < -127) {
-        q = q > 0 ? 127 : -127;
-        qd = double(q);
-      }
-      r[i] = fma(r[i], 128.0, -qd);
-      w |= (uint32_t(q) & 0xFFu) << (8 * i);
-    }
-    out[s] = w;
+  for (int i = 0; i < 4; ++i) {
+    X[i] = __double2ll_rn(x[i] * kScale);
+    if (neg) X[i] = -X[i];
   }
-}
-__device__ __forceinline__ uint32_t neg4(uint32_t w) {  // byte-wise negation of 4 int8 digits
-  uint32_t o = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) o |= (uint32_t(-int(int8_t(w >> (8 * i)))) & 0xFFu) << (8 * i);
-  return o;
+  for (int s = SL - 1; s >= 0; --s) {
+    const uint32_t b0 = uint32_t(X[0]), b1 = uint32_t(X[1]), b2 = uint32_t(X[2]), b3 = uint32_t(X[3]);
+    out[s] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+    if (s > 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) X[i] = (X[i] + 128) >> 8;
+    }
+  }
 }
 
 // HELD: n_vir <= 384 (at most 3 quads per lane): one load pass, the values held in registers
@@ -318,7 +310,9 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = (mx > 0.0 && mx <= 1.7e308) ? ilogb(mx) + 1 : 0;  // |value| 2^-e < 1
+    // |value| 2^-e < 127.5 / 128: the leading balanced digit fits an int8
+    int e = (mx > 0.0 && mx <= 1.7e308) ? ilogb(mx) + 1 : 0;
+    if (mx * ldexp(1.0, -e) > 0.995) ++e;
     const double sc = ldexp(1.0, -e);
     row_scale = ldexp(1.0, e);
     const bool alpha = (x & 1) == 0;
@@ -326,7 +320,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
     const int rb = prow + x;
     if (lane == 0) {
       P.sb_scale[size_t(pb) * NB + rb] = ldexp(1.0, e);
-      if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 49);
+      if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 46);
     }
     auto emit = [&](int qd, double (&xr)[4], double (&xi)[4]) {
 #pragma unroll
@@ -338,9 +332,10 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
           nbig += (fabs(xr[i]) > 0x1p-8 ? 1.0 : 0.0) + (fabs(xi[i]) > 0x1p-8 ? 1.0 : 0.0);
         }
       }
-      uint32_t dr[SL], di[SL];
+      uint32_t dr[SL], di[SL], drn[SL];
       digits4(xr, dr);
       digits4(xi, di);
+      if (alpha) digits4(xr, drn, true);
       // K' positions: k-step qd / 4 holds spinors 16 (qd / 4) .. + 15 as [re (16) | im (16)], so
       // K' follows the virtual energies (ascending, model.cpp:126-127) and the spinors that
       // exp(-eps tau / 2) has pushed below the last slice fill the trailing k-steps with zeros
@@ -362,7 +357,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
           *reinterpret_cast<uint32_t*>(a0 + op_off(ra, kre & 31)) = dr[s];
           *reinterpret_cast<uint32_t*>(a1 + op_off(ra, kim & 31)) = di[s];
           *reinterpret_cast<uint32_t*>(a0 + op_off(ra + 1, kre & 31)) = di[s];
-          *reinterpret_cast<uint32_t*>(a1 + op_off(ra + 1, kim & 31)) = neg4(dr[s]);
+          *reinterpret_cast<uint32_t*>(a1 + op_off(ra + 1, kim & 31)) = drn[s];
         }
       }
     };
@@ -428,7 +423,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
 
 // CORR (FUSED only): the guard's refinement pass. A step whose error estimate failed in the main
 // pass (st->oz_trip == 1) gets the next slice diagonal, d = s + t = 6 (seven products per k-step,
-// the 7th slices included), in one int32 accumulator per tile: dV = acc 2^(e_q + e_p - 56). The
+// the 7th slices included), in one int32 accumulator per tile: dV = acc 2^(e_q + e_p - 62). The
 // main pass stored each pair's f values (P.fstore); this pass adds df = sum o dV, re-forms the
 // pair terms from f + df and the step's sums, and re-checks them with the estimate scaled by
 // 2^-7; a step that still fails goes on to the DMMA kernel (oz_trip = 2). The accumulator is
@@ -619,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     // Main pass: F is stored for a refinement pass. Refinement pass: F is this pass's correction
     // to the stored f values (refined groups) or zero (groups left unrefined).
     // Accuracy guard: the INT8 error of each f is modelled per element as a random sum over K' of
-    // slice remainders and dropped products, sigma(u, v) = 2^-42 (A_u S_v + S_u A_v) with the row
+    // slice remainders and dropped products, sigma(u, v) = 2^-46 (A_u S_v + S_u A_v) with the row
     // stats of oz_slice_kernel (S = max row scale 2^e of the point, A = max of 2^e sqrt(|x 2^-e|^2 /
     // 3 + 0.6 #{|x 2^-e| > 2^-8})), propagated through the contraction with |o block|_F <=
     // |Phi_o(u)|_F |Phi_o(v)|_F: eps = |w| (sigma_f1 |f2| + |f1| sigma_f2) per pair, summed in
@@ -640,7 +635,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       acc_d += td;
       acc_x += tx;
       if (guard) {
-        const double kSig = CORR && refined ? 0x1p-49 : 0x1p-42;
+        const double kSig = CORR && refined ? 0x1p-49 : 0x1p-46;
         const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
         const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
         const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
@@ -684,7 +679,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           if (c >= n) break;
           long long x = int32_t(v[0][c]);
 #pragma unroll
-          for (int d = 1; d < NACC; ++d) x = x * 128 + int32_t(v[d][c]);
+          for (int d = 1; d < NACC; ++d)  // the last diagonal joins rounded to the one before it
+            x = d < S - 1 ? x * 256 + int32_t(v[d][c]) : x + ((int32_t(v[d][c]) + 128) >> 8);
           X[c0 + c] = x;
         }
       };
@@ -709,8 +705,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         mbar_arrive(&tempty[slot]);  // accumulators free: the next tile's MMAs overlap the work below
       }
       if (lane == 0) TL(it, 4 + 3 * warp, clock64());
-      // main pass: V = X 2^(e_q + e_p - 49); refinement: dV = acc 2^(e_q + e_p - 56)
-      const double sr = P.sa_scale[size_t(a) * MA + row] * (CORR ? 0x1p-7 : 1.0);
+      // main pass: V = X 2^(e_q + e_p - 46); refinement: dV = acc 2^(e_q + e_p - 62)
+      const double sr = P.sa_scale[size_t(a) * MA + row] * (CORR ? 0x1p-16 : 1.0);
       const double* sbv = P.sb_scale + size_t(b) * NB + c_lo;
       if constexpr (!FUSED) {
         double* dst = P.v + size_t(t) * (MA * NB) + q * 512 + plane * 32 + exq * 8 + c_lo * 8;
@@ -770,7 +766,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
               sgp = (o01.x * double(X[4 * k]) + o01.y * double(X[4 * k + 1])) +
                     (o23.x * double(X[4 * k + 2]) + o23.y * double(X[4 * k + 3]));
             } else {
-              // the refinement's correction df = sum o dV is ~2^-42 of f, so FP32 carries it with
+              // the refinement's correction df = sum o dV is ~2^-46 of f, so FP32 carries it with
               // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
               // with an integer exponent (read from the bits), terms aligned to the quad's largest
               // exponent, one conversion and scaling

@@ -92,32 +92,48 @@ def test_slice_budget(step_inputs):
 
 
 # ---- the device scheme (csrc/pair_oz.cu): only V on the INT8 path, one power-of-two scale per
-# (point, channel) row over [re | im], six digits, s + t <= 5; rounded vs truncated digits ----
+# (point, channel) row over [re | im], six int8 digits, s + t <= 5. Digits: balanced radix 256
+# (round 2, "r256": x 2^-e = sum_s d_s 2^-(7 + 8 s), d_s in [-128, 127], read off
+# rint(x 2^-e 2^55) from the low end), rounded 7-bit digits (round 1, "r128") or truncated ones ----
 
-def device_slices(X, S, rounded):
+def device_slices(X, S, scheme="r256"):
     mx = np.max(np.abs(X), axis=1)
     e = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) + 1, 0)   # ilogb(mx) + 1
+    if scheme == "r256":
+        e = np.where(mx * 2.0 ** -e > 0.995, e + 1, e)   # the leading digit fits an int8
+        I = np.rint(X * (2.0 ** (55 - e))[:, None]).astype(np.int64)   # seven slices: 7 + 8 * 6 bits
+        ds = []
+        for _ in range(6):
+            d = ((I + 128) & 255) - 128
+            ds.append(d)
+            I = (I - d) >> 8
+        ds.append(I)
+        assert np.abs(I).max() <= 127 and all(d.min() >= -128 and d.max() <= 127 for d in ds)
+        return [d.astype(np.float64) for d in ds[::-1]][:S], e, lambda s, t: 2.0 ** -(14 + 8 * (s + t))
     r = X / (2.0 ** e)[:, None]
     out = []
     for _ in range(S):
         r = r * 128.0
-        q = np.clip(np.rint(r), -127, 127) if rounded else np.trunc(r)
+        q = np.clip(np.rint(r), -127, 127) if scheme == "r128" else np.trunc(r)
         out.append(q)
         r = r - q
-    return out, e
+    return out, e, lambda s, t: 2.0 ** (-7 * (s + t + 2))
 
 
-def device_v(av, rounded, S=6):
-    """V = av av^H as the device computes it: Re V = [re | im] . [re | im], Im V = [im | -re] . [re | im]"""
+def device_v(av, scheme="r256", S=6, diagonals=None):
+    """V = av av^H as the device computes it: Re V = [re | im] . [re | im], Im V = [im | -re] . [re | im]
+    (the negated row from the digits of -x); S = 7, diagonals = 6 adds the guard's refinement"""
+    diagonals = S - 1 if diagonals is None else diagonals
     B = np.concatenate([av.real, av.imag], 1)
     out = []
     for A in (B, np.concatenate([av.imag, -av.real], 1)):
-        xs, ex = device_slices(A, S, rounded)   # the [im | -re] row has the [re | im] row's scale
-        ys, ey = device_slices(B, S, rounded)
+        xs, ex, wgt = device_slices(A, S, scheme)   # the [im | -re] row has the [re | im] row's scale
+        ys, ey, _ = device_slices(B, S, scheme)
         C = np.zeros((A.shape[0], B.shape[0]))
         for s in range(S):
-            for t in range(S - s):
-                C += (xs[s] @ ys[t].T) * 2.0 ** (-7 * (s + t + 2))
+            for t in range(S):
+                if s + t <= diagonals:
+                    C += (xs[s] @ ys[t].T) * wgt(s, t)
         out.append(C * (2.0 ** ex)[:, None] * (2.0 ** ey)[None, :])
     return out[0] + 1j * out[1]
 
@@ -136,11 +152,13 @@ def contract_dx(O, V, W, m):
     return d.real, x.real
 
 
-def test_device_scheme_rounded_digits(cfgdir):
-    """cfg3, m = 64, two steps: with rounded digits the device scheme keeps the direct and the
-    exchange sums within 5e-12 of FP64 (measured 5e-13), an order of magnitude inside the 1e-10
-    gate; truncated digits (the first device build) are ~10x worse (measured 1e-11, and 1.2e-10 on
-    the exchange sum of a cfg3 m = 192 step -- the GPU test that failed with them)."""
+def test_device_scheme_digits(cfgdir):
+    """cfg3, m = 64, two steps. Balanced radix-256 digits (the device scheme) keep every V element
+    within 2e-13 of max |V| (measured 8e-14) and the direct and exchange sums within 2e-12 of FP64
+    (measured 6e-13); the rounded 7-bit digits of round 1 are ~16x worse per element (1.5e-12),
+    truncated 7-bit digits (the first device build) another ~10x (1.2e-10 on the exchange sum of
+    a cfg3 m = 192 step -- the GPU test that failed with them). With the 7th slice and the
+    diagonal s + t = 6 (the guard's refinement pass) the elements are at FP64 rounding."""
     m = 64
     sp = cfgdir / "cfg3.spinor"
     orc = oracle_py.OracleSystem(sp, (cfgdir / "cfg3.conf").read_text())
@@ -157,10 +175,16 @@ def test_device_scheme_rounded_digits(cfgdir):
         ao = (occ * np.exp(0.5 * eps[:no] * tau)).reshape(8 * m, no)
         av = (vir * np.exp(-0.5 * eps[no:] * tau)).reshape(8 * m, nv)
         O = ao @ ao.conj().T
-        ed, ex = contract_dx(O, av @ av.conj().T, W, m)
-        rd, rx = contract_dx(O, device_v(av, True), W, m)
-        td, tx = contract_dx(O, device_v(av, False), W, m)
-        err_r = max(abs(rd / ed - 1), abs(rx / ex - 1))
-        err_t = max(abs(td / ed - 1), abs(tx / ex - 1))
-        assert err_r < 5e-12, (k, err_r)
-        assert err_t > 3 * err_r, (k, err_t, err_r)
+        V = av @ av.conj().T
+        ed, ex = contract_dx(O, V, W, m)
+        elem, sums = {}, {}
+        for scheme in ("r256", "r128", "trunc"):
+            Vd = device_v(av, scheme)
+            elem[scheme] = np.abs(Vd - V).max() / np.abs(V).max()
+            d, x = contract_dx(O, Vd, W, m)
+            sums[scheme] = max(abs(d / ed - 1), abs(x / ex - 1))
+        assert elem["r256"] < 2e-13 and sums["r256"] < 2e-12, (k, elem, sums)
+        assert elem["r128"] > 8 * elem["r256"] and elem["trunc"] > 3 * elem["r128"], (k, elem)
+        assert sums["trunc"] > 3 * sums["r128"], (k, sums)
+        refined = device_v(av, "r256", S=7, diagonals=6)
+        assert np.abs(refined - V).max() / np.abs(V).max() < 1e-15, k

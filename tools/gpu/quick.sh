@@ -3,8 +3,9 @@
 set -u
 O=gpurun_out
 T=${TAG:-q}
-timeout 900 python -m pytest tests -m gpu -q -x ${PYTEST_ARGS:-} > $O/${T}_pytest.log 2>&1; echo "pytest exit $?" >> $O/${T}_pytest.log
-tail -15 $O/${T}_pytest.log
+timeout ${PYTEST_TIMEOUT:-900} python -m pytest tests -m gpu -q ${PYTEST_ARGS:--x} -k "${PYTEST_K:-}" > $O/${T}_pytest.log 2>&1; echo "pytest exit $?" >> $O/${T}_pytest.log
+tail -${PYTEST_TAIL:-15} $O/${T}_pytest.log
+[ -n "${NO_BENCH:-}" ] && exit 0
 timeout 600 python bench.py ${BENCH_ARGS:-} > $O/${T}_bench_cfg4.json 2> $O/${T}_bench_cfg4.err
 tail -3 $O/${T}_bench_cfg4.err
 python - <<PY
