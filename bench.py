@@ -52,9 +52,10 @@ WORKLOAD = {
 }
 WORKLOAD.update({f"cfg5-{n}": f"size sweep: {n}e atom, 4c, even-tempered s/p/d/f, m 8192/GPU" for n in (2, 10, 18, 36, 54, 86)})
 STRONG_TOTAL = {"cfg1": 2000, "cfg2": 10000, "cfg3": 10000, "cfg4": 20000}  # BASELINE configs' step budgets
-DTYPE = ("f64/c128 (reference arithmetic); the V blocks (~90% of the pair FLOPs) as 6-slice int8 Ozaki sums on "
-         "tcgen05 with a per-step error guard: steps whose estimated error exceeds 2e-10 of their sums get a "
-         "7th-slice refinement or an FP64 DMMA recompute")
+DTYPE = ("f64/c128 (reference arithmetic); the V blocks (~90% of the pair FLOPs) as Ozaki sums of exact int8 "
+         "products on tcgen05 (six slices of balanced radix-256 digits per FP64 operand, 21 slice products) with a "
+         "per-step error guard: steps whose estimated error exceeds 2e-10 of their sums get a 7th-slice refinement "
+         "or an FP64 DMMA recompute")
 MCMP2_CLI = ROOT / "paper_2203_05632_b200" / "lib" / "mcmp2"
 
 
@@ -151,12 +152,13 @@ def clocks_summary(path: Path, index: int):
 
 # dense tcgen05 INT8 rate measured on this pool's B200 (tools/umma_rate.cu: M128 N256 K32 kind::i8
 # MMAs from shared memory, one issuing thread per SM, 4570 TOPS; nominal dense INT8/FP8 4.5 POPS,
-# B200_PROFILING.md). Shape ceiling of the kernel's own M128 N80 instruction mix: 3132 TOPS
-# (the same probe at N = 80: an M128 kind::i8 MMA costs ~61 cycles for any N <= 80).
+# B200_PROFILING.md). The kernel's own bound is shared-memory bandwidth: per k-step (32 of K') of a
+# 128 x 80 tile the 9 merged MMAs read 36 KB of A and 52.5 KB of B slices and the ring's fills write
+# 39.9 KB, 128.4 KB against 128 B/clk/SM -> 1003 cycles for 21 x 2 x 128 x 80 x 32 ops = 3993 TOPS per GPU.
 INT8_PEAK = 4570.0
-INT8_SHAPE_CEILING = 3132.0
-INT8_PEAK_SOURCE = ("measured: tools/umma_rate.cu tcgen05.mma kind::i8 M128 N256 K32, 4570 TOPS (nominal dense 4500); "
-                    "ceiling of the kernel's M128 N80 MMA shape on the same probe 3132 TOPS (profiles/r03_umma_rate.txt)")
+INT8_SMEM_BOUND = 148 * 1.965e9 * (21 * 2 * 128 * 80 * 32) / ((36864 + 53760 + 39936) / 128) / 1e12
+INT8_PEAK_SOURCE = ("measured: tools/umma_rate.cu tcgen05.mma kind::i8 M128 N256 K32, 4570 TOPS (nominal dense 4500; "
+                    "profiles/r03_umma_rate.txt)")
 
 
 def peaks():
@@ -473,10 +475,12 @@ def main():
 
     trace("timed region done")
     # ---- per-kernel device time (profiling pass, events around each launch) ----
+    ks_timed = dw.int8_ksteps()
     dw.profile(enable=True, reset=True)
     nprof = max(2, min(args.steps, 5))
     dw.advance(nprof, keep_on_device=True)
     prof = dw.profile(enable=False, reset=True)
+    ks_prof = dw.int8_ksteps()
     work = dw.work()
     pair_ms = prof["ms"]["pair"] / prof["launches"]["pair"]
     step_ms_prof = prof["ms"]["total"] / prof["launches"]["total"]
@@ -584,7 +588,12 @@ def main():
     if int8_path:
         n = oz["steps"]
         vg_ms, sl_ms, kr_ms, gd_ms = oz["vgemm_ms"] / n, oz["slice_ms"] / n, oz["pair_kr_ms"] / n, oz["guard_ms"] / n
-        a8 = oz["vgemm_int8_ops"] / (vg_ms / 1e3) / 1e12
+        # k-steps the V-GEMM issued (energy-ordered truncation, exact) over those of the full K' loop:
+        # in the profiling pass (the launches vg_ms times) and over the run so far (warm-up + timed steps)
+        ks_frac = (ks_prof[0] - ks_timed[0]) / (n * ks_prof[1]) if ks_prof[1] else 1.0
+        ks_frac_run = ks_timed[0] / ((args.warmup + my_steps) * ks_timed[1]) if ks_timed[1] and my_steps else None
+        a8_full = oz["vgemm_int8_ops"] / (vg_ms / 1e3) / 1e12
+        a8 = a8_full * ks_frac
         equiv = {k: v for k, v in fp64_view.items() if k not in ("frac", "peak", "peak_source")}
         equiv.update(kernel="pair stage: oz_slice_kernel + pair_kr_kernel (O blocks, DMMA) + oz_vgemm_kernel (V "
                             "blocks, INT8, contraction fused) + the guard's refinement / DMMA launches",
@@ -597,9 +606,20 @@ def main():
                                          "sums of exact int8 products, pair_oz.cu)",
             "achieved": a8, "peak": INT8_PEAK, "unit": "TFLOP/s", "frac": a8 / INT8_PEAK,
             "traffic": traffic_of("oz_vgemm_kernel"),
-            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 80 x K' per launch",
-            "peak_source": INT8_PEAK_SOURCE, "shape_ceiling": INT8_SHAPE_CEILING,
-            "frac_of_shape_ceiling": a8 / INT8_SHAPE_CEILING,
+            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 80 x 32 x the "
+                        "k-steps issued (the device counter of mcmp2dev_oz_ksteps over the profiled launches)",
+            "peak_source": INT8_PEAK_SOURCE,
+            "ksteps_frac": ks_frac, "ksteps_frac_run": ks_frac_run,
+            "ksteps_note": "K' follows the virtual energies; k-steps whose digits are all zero at this step's tau "
+                           "(exp(-eps tau / 2) below the last slice) are skipped, bit-identical to the full loop "
+                           "(tests/test_gpu_oz.py); ksteps_frac = issued / full over the profiled launches, "
+                           "ksteps_frac_run over warm-up + timed steps",
+            "full_loop_equivalent": a8_full, "full_loop_equivalent_note": "the full K' loop's int8 ops over the same "
+                                                                          "time (what an untruncated kernel would need)",
+            "smem_bound": INT8_SMEM_BOUND, "frac_of_smem_bound": a8 / INT8_SMEM_BOUND,
+            "smem_bound_note": "the kernel's binding resource is shared-memory bandwidth (128 B/clk/SM): per k-step "
+                               "of a 128 x 80 tile the 9 merged MMAs read 36 + 52.5 KB of slices and the ring's "
+                               "fills write 39.9 KB",
             "vgemm_ms_per_launch": vg_ms, "slice_ms_per_launch": sl_ms, "pair_kr_ms_per_launch": kr_ms,
             "guard_ms_per_step": gd_ms,
             "vgemm_share_of_step": vg_ms / step_ms_prof,
@@ -634,7 +654,7 @@ def main():
     # which pair stage ran, and why not the INT8 V path when it did not (n_vir > 512, spinors not
     # Kramers-paired within 1e-12, batched ensembles or m below ~180: mcmp2dev.cu oz_active)
     if int8_path:
-        line["pair_path"] = "INT8 V blocks (tcgen05 kind::i8, 6-slice Ozaki, guarded) + DMMA O blocks"
+        line["pair_path"] = "INT8 V blocks (tcgen05 kind::i8, 6-slice radix-256 Ozaki, guarded, energy-ordered k-step truncation) + DMMA O blocks"
     else:
         why = []
         if not kramers:
