@@ -116,7 +116,7 @@ struct OzParams {
   // accuracy guard (literal estimator): per-point stats from oz_slice_kernel, the step's
   // estimated INT8 error against guard_tol (<= 0: no guard)
   int n_occ;
-  double* pstat;             // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, N = |Phi_o(pt)|_F, 0
+  float* pstat;              // [npts_oz][4]: S = max_x 2^e_x, A = max_x 2^e_x a_x, N = |Phi_o(pt)|_F, 0
   double guard_tol;
   double* fstore;            // [C(m,2)][4] f(0,0), f(1,1), f(1,0), f(0,1) of each pair q > p (index
                              // q (q - 1) / 2 + p), written by the main pass for the refinement pass

@@ -108,7 +108,7 @@ struct mcmp2dev_handle {
   // the direct sum, the exchange sum or the step value exceeds guard_tol of that quantity is
   // recomputed on the DMMA pair kernel (pair_oz.cu, pair_kr.cu guard_fallback); <= 0: off
   double guard_tol = kGuardTol;
-  double* d_pstat = nullptr;  // [npts_oz][4] point stats (oz_slice_kernel)
+  float* d_pstat = nullptr;   // [npts_oz][4] point stats (oz_slice_kernel)
   double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
   // per-tile k-step truncation of the INT8 V-GEMM (OzParams::ks_cnt): on by default, exact
   bool oz_trunc = true;
@@ -276,8 +276,8 @@ struct mcmp2dev_handle {
       ck(cudaMalloc(&d_fstore, sizeof(double) * 4 * (mq * (mq - 1) / 2)), "cudaMalloc oz pair f values");
       ck(cudaMalloc(&d_tile_eps, sizeof(double) * 2 * oz_ntiles(nbq, true)), "cudaMalloc oz tile estimates");
     }
-    ck(cudaMalloc(&d_pstat, sizeof(double) * 4 * npts_oz), "cudaMalloc oz point stats");
-    ck(cudaMemset(d_pstat, 0, sizeof(double) * 4 * npts_oz), "memset oz point stats");
+    ck(cudaMalloc(&d_pstat, sizeof(float) * 4 * npts_oz), "cudaMalloc oz point stats");
+    ck(cudaMemset(d_pstat, 0, sizeof(float) * 4 * npts_oz), "memset oz point stats");
     ck(cudaMalloc(&d_ks_cnt, npts_oz / 2), "cudaMalloc oz k-step counts");
     ck(cudaMemset(d_ks_cnt, 0, npts_oz / 2), "memset oz k-step counts");
     ck(cudaMalloc(&d_ks_exec, sizeof(unsigned long long)), "cudaMalloc oz k-step counter");

@@ -306,15 +306,21 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
         }
         const int y = (lane >> 2) & 3, pp = lane & 3;
         if constexpr (OZ == 2) {  // o = conj O~ to the tile's O block in HBM; no V phase here
-          // [Q block row ta][p walker][q 16][x_alpha][re/im][e_p][y]: the P walkers of the row are
-          // contiguous, so any 10-walker P block of the V-GEMM's tiles is one bulk copy
-          double* ot = P.otiles + size_t(ta) * (ta + 1) * 4096 + size_t(p0) * 512;
-          // times the power-of-two scale of the V operand row (p, e_p, y) this value meets in the
-          // V-GEMM epilogue (exact)
+          // The tile's 4096 o values are staged in shared memory in their HBM order,
+          //   [p 8][q 16][quad c = (x_alpha, re/im, e_p) ^ (p & 3)][y 4]
+          // (the P walkers of a Q block row are contiguous in HBM, so a tile is one 32 KB block and
+          // any 10-walker P block of the V-GEMM's tiles one bulk copy; the XOR spreads the four p
+          // of a store over the 32-byte slots of a 128-byte row), and leave with one bulk store.
+          // Each value carries the power-of-two scale of the V operand row (p, e_p, y) it meets
+          // in the V-GEMM epilogue (exact).
           double osc[NB1];
 #pragma unroll
           for (int n = 0; n < NB1; ++n)
             osc[n] = P.oscale ? P.oscale[size_t(p0 + 4 * (NB1 * p1w + n) + pp) * 8 + 4 * e1 + y] : 1.0;
+          if (it > 0) {  // the previous tile's store has read the buffer
+            if (tid == 0) bulk_store_wait_read();
+            asm volatile("bar.sync 15, %0;" ::"n"(CONSUMERS * 32) : "memory");
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -322,10 +328,13 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
-                double* d = ot + p * 512 + q * 32 + j * 16 + e1 * 4 + y;
-                __stcg(d, (t1[h][n][j] + t2[h][n][j]) * osc[n]);
-                __stcg(d + 8, -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]) * osc[n]);
+                double* d = sO0 + p * 512 + q * 32 + y;
+                d[(((j * 2 + 0) * 2 + e1) ^ pp) * 4] = (t1[h][n][j] + t2[h][n][j]) * osc[n];
+                d[(((j * 2 + 1) * 2 + e1) ^ pp) * 4] = -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]) * osc[n];
               }
+          fence_proxy_async();
+          asm volatile("bar.sync 15, %0;" ::"n"(CONSUMERS * 32) : "memory");
+          if (tid == 0) bulk_s2g(P.otiles + size_t(ta) * (ta + 1) * 4096 + size_t(p0) * 512, sO0, 4096 * 8);
           continue;
         }
         if constexpr (OBUF == 1) consumer_barrier(q1w);  // the group is done reading the previous o rows
@@ -529,7 +538,10 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
       s_red[warp][1] = acc_x * cw;
     }
   }
-  if constexpr (OZ == 2) return;  // the step's sums are oz_vgemm_kernel<true>'s
+  if constexpr (OZ == 2) {  // the step's sums are oz_vgemm_kernel<true>'s
+    if (tid == 0) bulk_store_wait_read();  // the last tile's store is done with shared memory
+    return;
+  }
   __syncthreads();
   if (batched) {
     if (tid == 0) {

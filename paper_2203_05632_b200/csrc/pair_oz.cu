@@ -252,8 +252,11 @@ __device__ __forceinline__ void digits4(const double (&x)[4], uint32_t (&out)[SL
 // sum of squares and count of digits-relevant entries (|x| 2^-e > 2^-8) and its channel's share
 // of |Phi_o(pt)|^2; the first warp of each point combines the four channels into the point's
 // stats S, A, N (oz_vgemm_kernel's error model, see there).
+#ifndef OZ_SLICE_MINB
+#define OZ_SLICE_MINB 3
+#endif
 template <bool HELD>
-__global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P) {
+__global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
   __shared__ double s_st[8][3];
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(256, HELD ? 2 : 3) oz_slice_kernel(OzParams P)
       Ax = fmax(Ax, s_st[w + c][1]);
       N2 += s_st[w + c][2];
     }
-    reinterpret_cast<double4*>(P.pstat)[pt] = make_double4(Sx, Ax, sqrt(N2), 0.0);
+    reinterpret_cast<float4*>(P.pstat)[pt] = make_float4(float(Sx), float(Ax), float(sqrt(N2)), 0.0f);
   }
 }
 
@@ -511,7 +514,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   };
   double acc_d = 0.0, acc_x = 0.0;  // FUSED: this thread's pair sums
   // FUSED, guard: sums of the squared per-pair error estimates and of |pair term|
-  double acc_ed = 0.0, acc_ex = 0.0, acc_ad = 0.0, acc_ax = 0.0;
+  // (the estimates in FP32, in units of the model constant 2^-46: FP32 work costs nothing beside
+  // the MMAs, FP64 instructions ~12x their usual time)
+  float acc_ed = 0.0f, acc_ex = 0.0f;
+  double acc_ad = 0.0, acc_ax = 0.0;
+  constexpr double kSig2 = 0x1p-92;  // (2^-46)^2: the estimates' unit, applied with the CTA sums
   const bool guard = FUSED && P.pstat != nullptr;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
@@ -609,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     OzGroupWalk w(int(blockIdx.x), PW, PB);
     int sub = 0;  // P blocks processed: the parity of the shared f buffer
     int u = 0;    // tiles through TMEM
-    double te_d = 0.0, te_x = 0.0;  // main pass: this thread's estimate of the current tile
+    float te_d = 0.0f, te_x = 0.0f;  // main pass: this thread's estimate of the current tile
     // one pair's literal term (estimator.cpp:26-32) from its f values into the thread's sums.
     // Main pass: F is stored for a refinement pass. Refinement pass: F is this pass's correction
     // to the stored f values (refined groups) or zero (groups left unrefined).
@@ -622,7 +629,16 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
     // oracle's cfg3/cfg4 steps this estimate is 3-250x the actual error
     // (tests/test_oz_guard_model.py), on 2000-step device chains 2.3-170x (tests/test_gpu_guard.py);
     // it is a model, not a bound. Pairs of refined groups (one more slice and diagonal): 2^-49.
-    auto pair_term = [&](double4 F, int qg, int pg, bool refined) {
+    // Evaluated in FP32 from float point stats (a model needs no more; sums of squares far below
+    // the largest terms may flush to zero).
+    const float wdf = fabsf(float(P.w_direct)), wxf = fabsf(float(P.w_exchange));
+    // the four points' stats of a pair (q walker's two points, p walker's two)
+    struct PairStats { float4 c, d, a, b; };
+    auto load_stats = [&](int qg, int pg) {
+      const float4* ps = reinterpret_cast<const float4*>(P.pstat);
+      return PairStats{ps[2 * qg], ps[2 * qg + 1], ps[2 * pg], ps[2 * pg + 1]};
+    };
+    auto pair_term = [&](double4 F, int qg, int pg, bool refined, const PairStats& st) {
       double4* fs = P.fstore ? reinterpret_cast<double4*>(P.fstore) + (size_t(qg) * (qg - 1) / 2 + pg) : nullptr;
       if constexpr (CORR) {
         const double4 f6 = *fs;
@@ -635,16 +651,14 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       acc_d += td;
       acc_x += tx;
       if (guard) {
-        const double kSig = CORR && refined ? 0x1p-49 : 0x1p-46;
-        const double4 Sc = reinterpret_cast<const double4*>(P.pstat)[2 * qg];
-        const double4 Sd = reinterpret_cast<const double4*>(P.pstat)[2 * qg + 1];
-        const double4 Sa = reinterpret_cast<const double4*>(P.pstat)[2 * pg];
-        const double4 Sb = reinterpret_cast<const double4*>(P.pstat)[2 * pg + 1];
-        const double nac = kSig * Sa.z * Sc.z, nbd = kSig * Sb.z * Sd.z;
-        const double s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
-        const double s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
-        const double ed = fabs(P.w_direct) * (s1d * fabs(F.y) + fabs(F.x) * s2d);
-        const double ex = fabs(P.w_exchange) * (s1x * fabs(F.w) + fabs(F.z) * s2x);
+        const float kRef = CORR && refined ? 0.125f : 1.0f;  // refined pairs: 2^-49 against 2^-46
+        const float4 Sc = st.c, Sd = st.d, Sa = st.a, Sb = st.b;
+        const float nac = kRef * Sa.z * Sc.z, nbd = kRef * Sb.z * Sd.z;
+        const float s1d = nac * (Sc.y * Sa.x + Sc.x * Sa.y), s2d = nbd * (Sd.y * Sb.x + Sd.x * Sb.y);
+        const float s1x = nac * (Sd.y * Sa.x + Sd.x * Sa.y), s2x = nbd * (Sc.y * Sb.x + Sc.x * Sb.y);
+        const float fx = fabsf(float(F.x)), fy = fabsf(float(F.y)), fz = fabsf(float(F.z)), fw = fabsf(float(F.w));
+        const float ed = wdf * (s1d * fy + fx * s2d);
+        const float ex = wxf * (s1x * fw + fz * s2x);
         acc_ed += ed * ed;
         acc_ex += ex * ex;
         acc_ad += fabs(td);
@@ -660,12 +674,20 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           for (int j = 0; j < nbk; ++j)
             for (int id = warp * 32 + lane; id < 16 * PW; id += 32 * EPW) {
               const int qg = 16 * a + id / PW, pg = PW * (w.g * PB + j) + id % PW;
-              if (qg < P.m && pg < P.m && qg > pg) pair_term(make_double4(0.0, 0.0, 0.0, 0.0), qg, pg, false);
+              if (qg < P.m && pg < P.m && qg > pg)
+                pair_term(make_double4(0.0, 0.0, 0.0, 0.0), qg, pg, false, guard ? load_stats(qg, pg) : PairStats{});
             }
           continue;
         }
       }
       const int slot = u % NSLOT;
+      // main pass: this thread's pair of the tile (16 x PW pairs over the epilogue threads); its
+      // point stats are fetched now, behind the wait for the accumulators
+      PairStats pst{};
+      if constexpr (!CORR) {
+        const int id = warp * 32 + lane, qg = 16 * a + id / PW, pg = PW * w.g + id % PW;
+        if (guard && id < 16 * PW && qg < P.m && pg < P.m && qg > pg) pst = load_stats(qg, pg);
+      }
       mbar_wait(&tfull[slot], (u / NSLOT) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) TL(it, 3 + 3 * warp, clock64());
@@ -731,7 +753,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // pass): its instruction stream competes with the MMA-issuing warp for issue slots. So the
         // FP64 form stays and the per-pair terms are packed into whole warps after the named barrier
         // (1.42 -> 1.35 ms with the guard's estimate; 1.29 ms with no contraction at all).
-        const int row_o = q * 32 + ((row >> 1) & 1) * 16 + plane * 8;  // + p 512 + e_p 4 + y
+        // o values [p][q 16][quad (x_alpha, re/im, e_p) ^ (p & 3)][y 4] (pair_kr's O pass)
+        const int row_o = q * 32, quad_o = ((row >> 1) & 1) * 4 + plane * 2;
         const double* so = nullptr;
         if constexpr (OSM) {
           mbar_wait(&ofull[u & 1], (u >> 1) & 1);
@@ -747,7 +770,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
 #pragma unroll
           for (int k = 0; k < NK; ++k) {
             const int pg = min(PW * b + (c_lo + 4 * k) / 8, 16 * (a + 1) - 1);
-            const double* o = P.otiles + size_t(a) * (a + 1) * 4096 + size_t(pg) * 512 + row_o + (k & 1) * 4;
+            const double* o = P.otiles + size_t(a) * (a + 1) * 4096 + size_t(pg) * 512 + row_o +
+                              ((quad_o + (k & 1)) ^ (pg & 3)) * 4;
             opf[k][0] = __ldcs(reinterpret_cast<const longlong2*>(o));
             opf[k][1] = __ldcs(reinterpret_cast<const longlong2*>(o + 2));
           }
@@ -758,7 +782,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           double sgp = 0.0;
           if (pg < 16 * (a + 1)) {
             if constexpr (!CORR) {
-              const double* o = so + ((c_lo + 4 * k) / 8) * 512 + row_o + (k & 1) * 4;
+              const double* o = so + ((c_lo + 4 * k) / 8) * 512 + row_o + ((quad_o + (k & 1)) ^ (pg & 3)) * 4;
               const double2 o01 = *reinterpret_cast<const double2*>(o);
               const double2 o23 = *reinterpret_cast<const double2*>(o + 2);
               // the o values carry the P rows' scales (pair_kr's O pass), the Q row's follows below:
@@ -823,18 +847,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         for (int id = (warp * 32 + lane); id < 16 * PW; id += 32 * EPW) {
           const int q2 = id / PW, p2 = id % PW, qg = qg0 + q2, pg = pg0 + p2;
           if (!(qg < P.m && pg < P.m && qg > pg)) continue;
-          pair_term(sf[id], qg, pg, true);
+          pair_term(sf[id], qg, pg, true, CORR ? (guard ? load_stats(qg, pg) : PairStats{}) : pst);
         }
         if constexpr (!CORR)
           if (P.tile_eps) {  // this tile's estimate: warp sums now, the CTA's after the next barrier
-            double e0 = te_d, e1 = te_x;
-            te_d = te_x = 0.0;
+            float e0 = te_d, e1 = te_x;
+            te_d = te_x = 0.0f;
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
               e0 += __shfl_down_sync(0xffffffffu, e0, o);
               e1 += __shfl_down_sync(0xffffffffu, e1, o);
             }
-            if (lane == 0) s_te[sub & 1][warp] = make_double2(e0, e1);
+            if (lane == 0) s_te[sub & 1][warp] = make_double2(double(e0) * kSig2, double(e1) * kSig2);
           }
       }
       }  // P blocks of the tile
@@ -842,7 +866,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       ++u;
     }
     if constexpr (FUSED) {  // fixed-order CTA sums: warp shuffles, then the epilogue warps in order
-      double r[6] = {acc_d, acc_x, acc_ed, acc_ex, acc_ad, acc_ax};
+      double r[6] = {acc_d, acc_x, double(acc_ed) * kSig2, double(acc_ex) * kSig2, acc_ad, acc_ax};
 #pragma unroll
       for (int o = 16; o; o >>= 1)
 #pragma unroll

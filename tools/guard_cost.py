@@ -49,7 +49,7 @@ with tempfile.TemporaryDirectory() as d:
         timed(f"tol_{t:.0e}", 1, t)
     timed("dmma", 0, 0.0)
     # per-kernel split (events around each launch): estimate-only and the default tolerance
-    for label, tol in (("split_estimate_only", 1e300), ("split_default", tols[0])):
+    for label, tol in (("split_guard_off", 0.0), ("split_estimate_only", 1e300), ("split_default", tols[0])):
         dw.set_ensemble(st)
         dw.int8_v(1)
         dw.guard(tol)
