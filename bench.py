@@ -365,6 +365,11 @@ def main():
                     help="cap on a time_to_target run's total steps (all workers); a capped run reports "
                          "stopped_on_target false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--series", action="store_true",
+                    help="A/B only: oz_slice_kernel in series with the O pass instead of beside it "
+                         "(mcmp2dev_oz_overlap 0)")
+    ap.add_argument("--full-k", action="store_true",
+                    help="A/B only: every k-step of K' in the V-GEMM (mcmp2dev_oz_truncation 0)")
     ap.add_argument("--ensembles", type=int, default=1,
                     help="reference workers per GPU, batched in one handle (mcmp2dev_init_batch); each is an "
                          "independent ensemble of the config's walker count on Philox stream rank*E + e")
@@ -421,6 +426,10 @@ def main():
 
     sysd = System(spinor, conf_text)
     dw = DeviceWalker(sysd, device=dev, max_walkers=ens * m)
+    if args.series:
+        dw.int8_overlap(0)
+    if args.full_k:
+        dw.int8_truncation(0)
     if ens > 1:
         dw.init_batch(ens, m, seed=1, stream0=rank * ens)
     else:

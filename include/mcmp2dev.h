@@ -205,6 +205,11 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
  * are bit-identical to the full loop (tests/test_gpu_oz.py). mode -1 queries, 0 runs every
  * k-step, 1 truncates; returns the active state. */
 int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode);
+/* INT8 V path, literal estimator: oz_slice_kernel on a side stream of the handle, concurrent
+ * with the O pass (both read Phi only; the V-GEMM waits for both). mode -1 queries, 0 runs them
+ * in series on the handle's stream, 1 overlaps them (default; profiling passes always serialise
+ * so each kernel is timed alone). Results do not depend on it. */
+int mcmp2dev_oz_overlap(mcmp2dev_t* h, int mode);
 /* out2 = {k-steps (32 of K' = 2 n_vir) issued by the main-pass V-GEMM launches since the INT8
  * buffers were allocated, k-steps of one untruncated launch at the last step's sizes}. */
 int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2);

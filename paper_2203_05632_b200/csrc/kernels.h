@@ -80,10 +80,6 @@ struct PairParams {
                              // pair_oz.cu (INT8 Ozaki); null: the DMMA V phase
   double* otiles;            // pair_kr only, single ensemble, literal: write the o blocks of every
                              // tile for oz_vgemm_kernel<true> and skip the V phase and the sums
-  const double* oscale;      // with otiles: the o values are stored times oscale[8 p + 4 e_p + y], the
-                             // power-of-two row scales of the INT8 V operands (OzParams::sb_scale of the
-                             // 10-walker P blocks), so the V-GEMM epilogue contracts them with the
-                             // integer sums directly; nullptr: unscaled
   int guard_fallback;        // pair_kr only: the INT8 path's guard launch -- exit at once unless
                              // st->oz_trip, else recompute the step on DMMA (writes step_out[0..5],
                              // clears oz_trip)
@@ -104,9 +100,10 @@ struct OzParams {
   int8_t* sb;                // [P blocks][ks][slice][nb_rows x 32] B slices (P side, nb_rows / 4 points each)
   double* sa_scale;          // [npts_oz / 32][128]: 2^(e - 49)
   double* sb_scale;          // [P blocks][nb_rows]: 2^e
+  int* sb_exp;               // [P blocks][nb_rows]: e 2^20 (the exponent-field increment of 2^e)
   double* v;                 // [ntiles][8192] V blocks in pair_kr's epilogue order (physical)
   // fused literal contraction (oz_vgemm_kernel<true>): o blocks in, the step's sums out
-  const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>, times the P rows' scales (sb_scale)
+  const double* otiles;      // [ntiles][4096] from pair_kr_kernel<false, 2>
   int m;
   double ng2, w_direct, w_exchange;
   const DevState* st_ro;
@@ -136,7 +133,7 @@ size_t oz_slice_bytes_b(int npts_oz, int ks, int nb_rows);
 int oz_p_blocks(int npts_oz, int nb_rows);
 int oz_nb_rows(bool fused);
 int oz_ntiles(int nbq, bool fused);
-void launch_oz_slice(const OzParams& P, cudaStream_t s);
+void launch_oz_slice(const OzParams& P, cudaStream_t s, bool pdl = true);  // pdl: programmatic launch after the stream's previous kernel
 void launch_oz_vgemm(const OzParams& P, cudaStream_t s);
 void launch_oz_refine(const OzParams& P, cudaStream_t s);  // exits at once unless st->oz_trip == 1
 double oz_int8_ops(const OzParams& P);  // executed int8 tensor ops of one V-GEMM launch

@@ -88,6 +88,10 @@ T* dupload(const T* src, size_t n, std::vector<void*>& owned) {
 struct mcmp2dev_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // INT8 V path: oz_slice_kernel runs here, next to the O pass on `stream`
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool oz_overlap = true;
   std::vector<void*> owned;
   std::string err;
 
@@ -161,14 +165,14 @@ struct mcmp2dev_handle {
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   double* d_gsteps = nullptr;  // [kGraphSteps][kStepDoubles] step results written by the graph
   struct GraphKey {
-    int m = -1, kramers = -1, nens = 1, oz = -1, trunc = -1;
+    int m = -1, kramers = -1, nens = 1, oz = -1, trunc = -1, overlap = -1;
     uint32_t k0 = 0, k1 = 0, stream = 0;
     double guard_tol = -1.0;
     bool operator==(const GraphKey&) const = default;
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, oz_trunc ? 1 : 0, k0, k1, rstream, guard_tol};
+    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, oz_trunc ? 1 : 0, oz_overlap ? 1 : 0, k0, k1, rstream, guard_tol};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -226,7 +230,7 @@ struct mcmp2dev_handle {
     return oz && kramers && ne == 1 && mm >= 2 && !kr_qb1(mm, ne) && n_vir > 0 && n_vir <= 512;
   }
   void oz_free() {
-    for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.v,
+    for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.sb_exp, (void*)ozp.v,
                     (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_tile_eps, (void*)d_ks_cnt,
                     (void*)d_ks_exec})
       if (p) cudaFree(p);
@@ -234,6 +238,7 @@ struct mcmp2dev_handle {
     d_ks_exec = nullptr;
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
+    ozp.sb_exp = nullptr;
     oz_otiles = nullptr;
     d_pstat = nullptr;
     d_fstore = nullptr;
@@ -266,6 +271,8 @@ struct mcmp2dev_handle {
     ck(cudaMalloc(&ozp.sa_scale, sizeof(double) * npts_oz * 4), "cudaMalloc oz scales");
     ck(cudaMalloc(&ozp.sb_scale, sbs_bytes), "cudaMalloc oz scales");
     ck(cudaMemset(ozp.sb_scale, 0, sbs_bytes), "memset oz scales");
+    ck(cudaMalloc(&ozp.sb_exp, sbs_bytes / 2), "cudaMalloc oz scale exponents");
+    ck(cudaMemset(ozp.sb_exp, 0, sbs_bytes / 2), "memset oz scale exponents");
     // physical estimator: V tiles for pair_kr's trace epilogue; literal: o tiles for the fused
     // contraction in the V-GEMM epilogue
     if (estimator == MCMP2DEV_ESTIMATOR_PHYSICAL)
@@ -354,11 +361,17 @@ struct mcmp2dev_handle {
       o.tile_eps = guarded ? d_tile_eps : nullptr;
       o.ks_cnt = oz_trunc ? d_ks_cnt : nullptr;
       o.ks_exec = d_ks_exec;
-      launch_oz_slice(o, stream);
+      // Literal estimator: the slice kernel (integer / load-store work, 1 KB of shared memory) and
+      // the O pass (DMMA, one CTA per SM) need only Phi, so the slices are cut on a side stream
+      // next to the O pass and the V-GEMM waits for both (the fork and join are captured into
+      // the step graphs like any other dependency). Profiling runs keep them in series so each
+      // kernel's events time it alone.
+      const bool fork = fused && !prof && oz_overlap;
+      if (fork) ck(cudaEventRecord(ev_fork, stream), "fork event");
+      else launch_oz_slice(o, stream, true);
       if (prof) ck(cudaEventRecord(ev_oz[0], stream), "event");
       if (fused) {  // o blocks first, then V blocks with the contraction and the step's sums
         p.otiles = oz_otiles;
-        p.oscale = o.sb_scale;
         if (OZ_O_PW4) {
           const int wmax = std::min(KC4, std::max(Go, 1));
           pair_kr_ring_pw4(wmax, p.ring, p.ring_doubles);
@@ -367,6 +380,12 @@ struct mcmp2dev_handle {
           launch_pair_kr(p, stream);
         }
         if (prof) ck(cudaEventRecord(ev_oz[1], stream), "event");
+        if (fork) {  // the O pass is in flight (its CTAs take their SMs first); the slices beside it
+          ck(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+          launch_oz_slice(o, side, false);
+          ck(cudaEventRecord(ev_join, side), "join event");
+          ck(cudaStreamWaitEvent(stream, ev_join, 0), "join wait");
+        }
         launch_oz_vgemm(o, stream);
         if (prof) ck(cudaEventRecord(ev_oz[2], stream), "event");
         if (guarded) {  // each exits at once unless the step failed the check before it
@@ -596,7 +615,14 @@ void build(mcmp2dev_t* h, const mcmp2dev_system* s, int device, int max_walkers)
   if (!(s->lambda > 0.0)) throw ArgError("TauSampler: lambda must be positive");
   h->device = device;
   ck(cudaSetDevice(device), "cudaSetDevice");
-  ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  {  // the side stream's kernels fill what the main stream's leave (lower priority)
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priority range");
+    ck(cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, hi), "cudaStreamCreate");
+    ck(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, lo), "cudaStreamCreate");
+  }
+  ck(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming), "cudaEventCreate");
   ck(pair_kernel_setup(), "pair kernel attributes");
   ck(spinor_kernel_setup(), "spinor kernel attributes");
   ck(pair_kr_kernel_setup(), "pair_kr kernel attributes");
@@ -792,6 +818,9 @@ int mcmp2dev_destroy(mcmp2dev_t* h) {
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs)
     if (g) cudaGraphExecDestroy(g);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return MCMP2DEV_OK;
@@ -1399,6 +1428,13 @@ int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode) {
   if (mode == 0) h->oz_trunc = false;
   if (mode == 1) h->oz_trunc = true;
   return h->oz_trunc ? 1 : 0;
+}
+
+int mcmp2dev_oz_overlap(mcmp2dev_t* h, int mode) {
+  if (!h) return -1;
+  if (mode == 0) h->oz_overlap = false;
+  if (mode == 1) h->oz_overlap = true;
+  return h->oz_overlap ? 1 : 0;
 }
 
 int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2) {

@@ -311,12 +311,6 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
           // (the P walkers of a Q block row are contiguous in HBM, so a tile is one 32 KB block and
           // any 10-walker P block of the V-GEMM's tiles one bulk copy; the XOR spreads the four p
           // of a store over the 32-byte slots of a 128-byte row), and leave with one bulk store.
-          // Each value carries the power-of-two scale of the V operand row (p, e_p, y) it meets
-          // in the V-GEMM epilogue (exact).
-          double osc[NB1];
-#pragma unroll
-          for (int n = 0; n < NB1; ++n)
-            osc[n] = P.oscale ? P.oscale[size_t(p0 + 4 * (NB1 * p1w + n) + pp) * 8 + 4 * e1 + y] : 1.0;
           if (it > 0) {  // the previous tile's store has read the buffer
             if (tid == 0) bulk_store_wait_read();
             asm volatile("bar.sync 15, %0;" ::"n"(CONSUMERS * 32) : "memory");
@@ -329,8 +323,8 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
               for (int j = 0; j < 2; ++j) {
                 const int q = 4 * q1w + 2 * h + hl, p = 4 * (NB1 * p1w + n) + pp;
                 double* d = sO0 + p * 512 + q * 32 + y;
-                d[(((j * 2 + 0) * 2 + e1) ^ pp) * 4] = (t1[h][n][j] + t2[h][n][j]) * osc[n];
-                d[(((j * 2 + 1) * 2 + e1) ^ pp) * 4] = -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]) * osc[n];
+                d[(((j * 2 + 0) * 2 + e1) ^ pp) * 4] = t1[h][n][j] + t2[h][n][j];
+                d[(((j * 2 + 1) * 2 + e1) ^ pp) * 4] = -(t3[h][n][j] - t1[h][n][j] + t2[h][n][j]);
               }
           fence_proxy_async();
           asm volatile("bar.sync 15, %0;" ::"n"(CONSUMERS * 32) : "memory");

@@ -94,8 +94,10 @@ struct OzShape {
   // shared memory next to a 3-stage ring (3 / 4 / 5 stages measured alike), so the epilogue never
   // waits on HBM for them
   static constexpr int OT_BYTES = FUSED && !CORR ? PW * 16 * 32 * 8 : 0;
+  // ... followed by the P block's NB row-scale exponents (sb_exp)
+  static constexpr int OT_BUF = OT_BYTES ? OT_BYTES + (NB * 4 + 127) / 128 * 128 : 0;
   static constexpr int NSTAGE = CORR ? (227 * 1024 - 16 * 1024) / STAGE : FUSED ? 3 : STAGES;
-  static constexpr int SMEM_BYTES = NSTAGE * STAGE + 2 * OT_BYTES;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE + 2 * OT_BUF;
   static constexpr int NACC = CORR ? 1 : S;   // accumulators per P block (slice diagonals)
   static constexpr int NSLOT = CORR ? 512 / (PB * NB) : 1;  // tiles in flight in TMEM
   static constexpr int CPW = NB / (EPW / 4);  // columns per epilogue warp
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
     const int rb = prow + x;
     if (lane == 0) {
       P.sb_scale[size_t(pb) * NB + rb] = ldexp(1.0, e);
+      P.sb_exp[size_t(pb) * NB + rb] = e * (1 << 20);
       if (alpha) P.sa_scale[size_t(qb) * MA + ra] = P.sa_scale[size_t(qb) * MA + ra + 1] = ldexp(1.0, e - 46);
     }
     auto emit = [&](int qd, double (&xr)[4], double (&xi)[4]) {
@@ -555,9 +558,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         if constexpr (OSM) {  // the tile's o values: walkers PW b0 .. of Q block row a (up to the diagonal)
           const int ob = it & 1, np = min(PW, 16 * (a + 1) - PW * b0);
           mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1u);
-          mbar_expect_tx(&ofull[ob], np * 4096);
-          bulk_g2s(sm + NST * STAGE + ob * Sh::OT_BYTES, P.otiles + size_t(a) * (a + 1) * 4096 + size_t(PW * b0) * 512,
+          mbar_expect_tx(&ofull[ob], np * 4096 + NB * 4);
+          bulk_g2s(sm + NST * STAGE + ob * Sh::OT_BUF, P.otiles + size_t(a) * (a + 1) * 4096 + size_t(PW * b0) * 512,
                    np * 4096, &ofull[ob]);
+          bulk_g2s(sm + NST * STAGE + ob * Sh::OT_BUF + Sh::OT_BYTES, P.sb_exp + size_t(b0) * NB, NB * 4, &ofull[ob]);
         }
         for (int ks = 0; ks < nk; ++ks) {
           mbar_wait(&empty[stage], ph ^ 1u);
@@ -756,9 +760,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         // o values [p][q 16][quad (x_alpha, re/im, e_p) ^ (p & 3)][y 4] (pair_kr's O pass)
         const int row_o = q * 32, quad_o = ((row >> 1) & 1) * 4 + plane * 2;
         const double* so = nullptr;
+        const int* se = nullptr;  // the P rows' scale exponents (e 2^20) of this warp's columns
         if constexpr (OSM) {
           mbar_wait(&ofull[u & 1], (u >> 1) & 1);
-          so = reinterpret_cast<const double*>(sm + NST * STAGE + (u & 1) * Sh::OT_BYTES);
+          so = reinterpret_cast<const double*>(sm + NST * STAGE + (u & 1) * Sh::OT_BUF);
+          se = reinterpret_cast<const int*>(sm + NST * STAGE + (u & 1) * Sh::OT_BUF + Sh::OT_BYTES) + c_lo;
         }
         constexpr int NK = CPW / 4;  // (p, e_p) of this warp
         double g[NK];
@@ -785,10 +791,18 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
               const double* o = so + ((c_lo + 4 * k) / 8) * 512 + row_o + ((quad_o + (k & 1)) ^ (pg & 3)) * 4;
               const double2 o01 = *reinterpret_cast<const double2*>(o);
               const double2 o23 = *reinterpret_cast<const double2*>(o + 2);
-              // the o values carry the P rows' scales (pair_kr's O pass), the Q row's follows below:
-              // five FP64 operations per quad beside the conversions
-              sgp = (o01.x * double(X[4 * k]) + o01.y * double(X[4 * k + 1])) +
-                    (o23.x * double(X[4 * k + 2]) + o23.y * double(X[4 * k + 3]));
+              // V 2^-(e_q - 46) = X 2^(e_p): the P row's power-of-two scale goes into the converted
+              // sum's exponent field on the integer pipe (a nonzero X converts to a normal number; the
+              // scales keep it one), the Q row's follows below: five FP64 operations per quad beside
+              // the conversions
+              const int4 eb = *reinterpret_cast<const int4*>(se + 4 * k);
+              auto vx = [](long long x, int e20) {
+                const double v = double(x);
+                const int hi = __double2hiint(v);
+                return __hiloint2double(hi ? hi + e20 : 0, __double2loint(v));
+              };
+              sgp = (o01.x * vx(X[4 * k], eb.x) + o01.y * vx(X[4 * k + 1], eb.y)) +
+                    (o23.x * vx(X[4 * k + 2], eb.z) + o23.y * vx(X[4 * k + 3], eb.w));
             } else {
               // the refinement's correction df = sum o dV is ~2^-46 of f, so FP32 carries it with
               // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
@@ -800,7 +814,7 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
 #pragma unroll
               for (int y = 0; y < 4; ++y) {
                 const int ex = int((ob[y] >> 52) & 0x7FF);  // zero / subnormal o: dropped
-                E[y] = ex ? ex + 1023 : 0;                  // (the P row's scale is in o already)
+                E[y] = ex ? ex + int((__double_as_longlong(sbv[4 * k + y]) >> 52) & 0x7FF) : 0;
                 emax = max(emax, E[y]);
               }
               float acc = 0.0f;
@@ -977,11 +991,17 @@ cudaError_t oz_kernel_setup() {
                               OzShape<true, true>::SMEM_BYTES);
 }
 
-void launch_oz_slice(const OzParams& P, cudaStream_t s) {
-  if (P.kh / 4 <= 96)
-    pdl_launch(oz_slice_kernel<true>, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
-  else
-    pdl_launch(oz_slice_kernel<false>, dim3((P.npts_oz + 1) / 2), dim3(256), 0, s, P);
+void launch_oz_slice(const OzParams& P, cudaStream_t s, bool pdl) {
+  const dim3 grid((P.npts_oz + 1) / 2);
+  const bool held = P.kh / 4 <= 96;
+  if (!pdl) {  // on the side stream, behind an event: a plain launch (griddepcontrol.wait is a no-op)
+    if (held) oz_slice_kernel<true><<<grid, 256, 0, s>>>(P);
+    else oz_slice_kernel<false><<<grid, 256, 0, s>>>(P);
+  } else if (held) {
+    pdl_launch(oz_slice_kernel<true>, grid, dim3(256), 0, s, P);
+  } else {
+    pdl_launch(oz_slice_kernel<false>, grid, dim3(256), 0, s, P);
+  }
 }
 
 double oz_int8_ops(const OzParams& P) {

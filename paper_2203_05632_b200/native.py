@@ -92,6 +92,7 @@ def dev() -> C.CDLL:
         d.mcmp2dev_profile_pair.argtypes = [vp, dp]
         d.mcmp2dev_oz_truncation.argtypes = [vp, ip]
         d.mcmp2dev_oz_ksteps.argtypes = [vp, dp]
+        d.mcmp2dev_oz_overlap.argtypes = [vp, ip]
         d.mcmp2dev_work_executed.argtypes = [vp, dp]
         d.mcmp2dev_prepare.argtypes = [vp]
         d.mcmp2dev_init_batch.argtypes = [vp, ip, ip, C.c_uint64, C.c_uint32]

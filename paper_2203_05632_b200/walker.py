@@ -275,6 +275,11 @@ class DeviceWalker:
         -1 query, 0 every k-step, 1 only the k-steps that hold a nonzero digit."""
         return bool(self._d.mcmp2dev_oz_truncation(self._h, mode))
 
+    def int8_overlap(self, mode: int = -1) -> bool:
+        """oz_slice_kernel on a side stream next to the O pass: -1 query, 0 in series, 1 overlapped
+        (default)."""
+        return bool(self._d.mcmp2dev_oz_overlap(self._h, mode))
+
     def int8_ksteps(self) -> tuple[float, float]:
         """(k-steps issued by the main-pass V-GEMM launches so far, k-steps of one full launch)."""
         o = np.zeros(2)

@@ -182,3 +182,20 @@ def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
     ref = orc.replay(walkers, taus)
     for c, r in ((0, 0), (2, 2), (4, 4)):
         assert rel_err(on[:, c], ref[:, r]) < REL, (c, frac)
+
+
+def test_int8_v_slice_overlap_does_not_change_results(cfgdir):
+    """oz_slice_kernel runs on a side stream next to the O pass (mcmp2dev_oz_overlap); the same
+    chain with the two kernels in series gives bit-identical step records, through the captured
+    graphs (64 steps) and single launches (3 more)."""
+    sp = cfgdir / "cfg3.spinor"
+    text = (cfgdir / "cfg3.conf").read_text()
+    recs = []
+    for mode in (1, 0):
+        dw = DeviceWalker(System(sp, text), max_walkers=256)
+        assert dw.int8_overlap(mode) == bool(mode)
+        dw.init_ensemble(256, seed=12)
+        dw.burn_in(30)
+        recs.append(dw.advance_ex(67))
+        dw.close()
+    assert recs[0].tobytes() == recs[1].tobytes()
