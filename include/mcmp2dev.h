@@ -188,8 +188,8 @@ int mcmp2dev_kramers(mcmp2dev_t* h, int mode);
  * column counts do not pair) */
 int mcmp2dev_kramers_deviation(const mcmp2dev_t* h, double* deviation);
 /* V blocks of the Kramers pair stage (K = n_vir, ~90% of the pair work) on the INT8 tensor
- * cores: FP64 operands split into six 7-bit slices (Ozaki), exact int8 products summed in
- * int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers
+ * cores: FP64 operands split into six int8 slices of balanced radix-256 digits (Ozaki), exact
+ * int8 products summed in int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers
  * path with n_vir <= 512 and the 16 x 8 pair tiles (m >= 64 walkers, enough tiles for the
  * SMs); elsewhere the DMMA V phase runs. mode -1 queries, 0 selects DMMA, 1 selects INT8
  * (the default of the literal estimator; the physical estimator defaults to DMMA and runs
@@ -216,16 +216,16 @@ int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2);
 /* Accuracy guard of the INT8 V path (literal estimator). After each INT8 step the V-GEMM's
  * last CTA compares the estimated error of the direct sum, the exchange sum and the step value
  * with tol times their magnitude. A step that fails (or is not finite) gets a refinement pass
- * on the INT8 tensor cores (the 7th slices and the next slice diagonal, ~1/128 of the error;
+ * on the INT8 tensor cores (the 7th slices and the next slice diagonal, ~1/8 of the modelled error;
  * the main pass keeps every pair's f values for it), and if the refined step still fails it
  * is recomputed on the FP64 DMMA pair kernel. Both are launched every step and exit at once
  * unless needed, so the graphs stay fixed. tol <= 0 turns the guard off; default 2e-10; NaN
  * only queries. previous (may be NULL) receives the old tolerance. The estimate is a model
  * checked against the oracle (tests/test_oz_guard_model.py) and against the DMMA path on
- * 2000-step chains (2.3-170x the actual error), not a rigorous bound (that would be ~1e-7
- * relative and reject every step). At cfg4 (m = 2048, 2000 steps) ~15% of the steps fail the
- * main pass, steps kept on it are within 6e-11 of FP64, while the unguarded path exceeds the
- * 1e-10 gate on 16 of the 2000 steps (tests/test_gpu_guard.py). */
+ * chains of up to 2 x 10^4 steps (>= 2.5x the actual error, median 22x), not a rigorous bound
+ * (that would reject every step). At cfg4 (m = 2048, 2 x 10^4 steps) 1.1% of the steps fail the
+ * main pass and 0.2% the refinement, kept steps are within 3.8e-11 of FP64, while the unguarded
+ * path exceeds the 1e-10 gate on 6-16 steps (tests/test_gpu_guard.py, tools/guard_chain.py). */
 int mcmp2dev_guard(mcmp2dev_t* h, double tol, double* previous);
 /* out5 = {INT8-path steps checked, steps refined, steps recomputed on DMMA, largest estimated
  * relative error of a step kept on INT8, tolerance} since the last call; resets the counters. */
