@@ -368,6 +368,7 @@ def main():
     ap.add_argument("--series", action="store_true",
                     help="A/B only: oz_slice_kernel in series with the O pass instead of beside it "
                          "(mcmp2dev_oz_overlap 0)")
+    ap.add_argument("--dmma", action="store_true", help="A/B only: the all-DMMA pair stage (mcmp2dev_pair_path 0)")
     ap.add_argument("--full-k", action="store_true",
                     help="A/B only: every k-step of K' in the V-GEMM (mcmp2dev_oz_truncation 0)")
     ap.add_argument("--ensembles", type=int, default=1,
@@ -430,6 +431,8 @@ def main():
         dw.int8_overlap(0)
     if args.full_k:
         dw.int8_truncation(0)
+    if args.dmma:
+        dw.int8_v(0)
     if ens > 1:
         dw.init_batch(ens, m, seed=1, stream0=rank * ens)
     else:
@@ -670,6 +673,8 @@ def main():
             why.append(f"spinor set not Kramers-paired within 1e-12 (deviation {dw.kramers_deviation():.3g})")
         if sysd.n_vir > 512:
             why.append(f"n_vir {sysd.n_vir} > 512")
+        if sysd.n_vir <= 16:
+            why.append(f"n_vir {sysd.n_vir} <= 16: one k-step of K', the DMMA kernel is faster")
         if ens > 1:
             why.append("batched ensembles")
         line["pair_path"] = "DMMA only (INT8 V path inactive: " + ("; ".join(why) or "ensemble below the INT8 tiling size") + ")"

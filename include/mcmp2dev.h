@@ -191,10 +191,12 @@ int mcmp2dev_kramers_deviation(const mcmp2dev_t* h, double* deviation);
  * cores: FP64 operands split into six int8 slices of balanced radix-256 digits (Ozaki), exact
  * int8 products summed in int32/int64, one FP64 rounding (csrc/pair_oz.cu). Used for single ensembles on the Kramers
  * path with n_vir <= 512 and the 16 x 8 pair tiles (m >= 64 walkers, enough tiles for the
- * SMs); elsewhere the DMMA V phase runs. mode -1 queries, 0 selects DMMA, 1 selects INT8
- * (the default of the literal estimator; the physical estimator defaults to DMMA and runs
- * INT8 unguarded when selected); returns 1 when the INT8 V path is selected and the system is
- * eligible. Agreement with the FP64 path: see mcmp2dev_guard. */
+ * SMs); elsewhere the DMMA V phase runs. mode -1 queries, 0 selects DMMA, 1 selects INT8.
+ * Default: INT8 for the literal estimator when n_vir > 16 (with a single 32-wide k-step of K'
+ * the V-GEMM's per-tile epilogue, not its MMAs, sets the pace and the DMMA kernel is faster);
+ * the physical estimator defaults to DMMA and runs INT8 unguarded when selected. Returns 1 when
+ * the INT8 V path is selected and the system is eligible. Agreement with the FP64 path: see
+ * mcmp2dev_guard. */
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
 /* Energy-ordered truncation of the INT8 V-GEMM's K loop (on by default; exact). The virtual
  * energies ascend (model.cpp:126-127) and Phi_v carries exp(-eps tau / 2), so at this step's tau

@@ -105,6 +105,12 @@ struct mcmp2dev_handle {
   // V blocks of the Kramers pair stage on the INT8 tensor cores (pair_oz.cu), single ensembles
   // of QB = 2 tiles; buffers sized for oz_m walkers, grown outside graph capture (ensure_oz)
   bool oz = true;
+  // Selected by default only above 16 virtual spinors (more than one 32-wide k-step of K'): with
+  // a single k-step the V-GEMM is bound by its per-tile epilogue, not by MMAs, and the DMMA pair
+  // kernel is faster (cfg5-2, n_vir 10, m 8192: 5.3 vs 6.6 ms per step; cfg5-10, n_vir 30: 10.0
+  // vs 8.0). mcmp2dev_pair_path(h, 1) selects it regardless.
+  static constexpr int kOzAutoMinVir = 16;
+  bool oz_forced = false;
   int oz_m = 0;
   OzParams ozp{};
   double* oz_otiles = nullptr;
@@ -227,7 +233,8 @@ struct mcmp2dev_handle {
   }
 
   bool oz_active(int mm, int ne) const {
-    return oz && kramers && ne == 1 && mm >= 2 && !kr_qb1(mm, ne) && n_vir > 0 && n_vir <= 512;
+    return oz && kramers && ne == 1 && mm >= 2 && !kr_qb1(mm, ne) && n_vir > 0 && n_vir <= 512 &&
+           (oz_forced || n_vir > kOzAutoMinVir);
   }
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.sb_exp, (void*)ozp.v,
@@ -1418,9 +1425,12 @@ int mcmp2dev_profile_pair(mcmp2dev_t* h, double* out) {
 
 int mcmp2dev_pair_path(mcmp2dev_t* h, int mode) {
   if (!h) return -1;
-  if (mode == 0) h->oz = false;
-  if (mode == 1) h->oz = true;
-  return h->oz && h->kramers && h->n_vir > 0 && h->n_vir <= 512 ? 1 : 0;
+  if (mode == 0) h->oz = false, h->oz_forced = false;
+  if (mode == 1) h->oz = true, h->oz_forced = true;
+  return h->oz && h->kramers && h->n_vir > 0 && h->n_vir <= 512 &&
+                 (h->oz_forced || h->n_vir > mcmp2dev_handle::kOzAutoMinVir)
+             ? 1
+             : 0;
 }
 
 int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode) {

@@ -199,3 +199,22 @@ def test_int8_v_slice_overlap_does_not_change_results(cfgdir):
         recs.append(dw.advance_ex(67))
         dw.close()
     assert recs[0].tobytes() == recs[1].tobytes()
+
+
+def test_int8_v_default_needs_more_than_one_kstep(cfgdir):
+    """n_vir <= 16 (one 32-wide k-step of K'): the DMMA pair kernel is the default (the V-GEMM's
+    per-tile epilogue would set the pace); mcmp2dev_pair_path(h, 1) still selects INT8, and the
+    two agree with the oracle."""
+    sp = cfgdir / "cfg5-2.spinor"
+    text = (cfgdir / "cfg5-2.conf").read_text()
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=3, stream=0, m=208, burn=20, nsteps=1)
+    dw = DeviceWalker(System(sp, text), max_walkers=208)
+    assert dw.kramers() and not dw.int8_v()
+    dmma = dw.replay(tr["walkers"], tr["tau"])
+    assert dw.int8_v(1)
+    got = dw.replay(tr["walkers"], tr["tau"])
+    for k in (0, 2, 4):
+        assert rel_err(dmma[:, k], tr["est"][:, k]) < REL, k
+        assert rel_err(got[:, k], tr["est"][:, k]) < REL, k
+    assert not dw.int8_v(0)
