@@ -23,20 +23,25 @@
 // tests/test_ozaki_budget.py.
 //
 // Kernels per step (after mo_kernel):
-//  * oz_slice_kernel: one warp per (point, channel): the row exponent, the six slices of the
-//    [re | im] rows, written directly in the UMMA canonical K-major layout of their tile blocks;
+//  * oz_slice_kernel: one warp per (point, channel): the row exponent, the seven slices of the
+//    [re | im] rows (K' in energy order, 16 spinors per k-step), written directly in the UMMA
+//    canonical K-major layout of their tile blocks; per point pair the last k-step with a nonzero
+//    digit. On the literal path it runs on a side stream beside the O pass;
 //  * literal estimator: pair_kr_kernel<false, 2> writes the o blocks of its 16 x 8 tiles, then
 //    oz_vgemm_kernel<true> computes each 16 x 10 tile's V blocks and contracts them with the o
 //    blocks in its epilogue (the reference's literal pair term), with the step's fixed-order sums;
 //  * physical estimator: oz_vgemm_kernel<false> writes V tiles
 //    V[t][q 16][p 8][re/im][e_q x_alpha e_p y>>1 (16)][y&1] in the order pair_kr's trace
 //    epilogue lanes read them, then pair_kr_kernel<true, 1>.
-// oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each
-// k-step's 6 A + 6 B slices into a 5-stage mbarrier ring with cp.async.bulk, one thread issues
-// the 21 tcgen05.mma per k-step, eight epilogue warps (two per TMEM lane quarter) drain TMEM
+// oz_vgemm_kernel: persistent CTAs over the tile triangle; a producer thread streams each active
+// k-step's 6 A + 6 B slices into a 3-stage mbarrier ring with cp.async.bulk (and the tile's o
+// values into a double buffer), one thread issues the k-step's 21 slice products as 9 merged
+// tcgen05.mma (oz_issue_diagonals), eight epilogue warps (two per TMEM lane quarter) drain TMEM
 // (tcgen05.ld), merge, release the accumulators and finish the tile while the next one runs.
-// Measured (cfg4, profiles/r05): 1.34 ms at 2447 int8 TOPS, 0.78 of the M128 N80 shape's
-// ceiling, vs ~3.6 ms for the DMMA V phase of pair_kr.
+// Measured (cfg4, profiles/r11): 1.11 ms at 2960 int8 TOPS on the full K' loop (0.65 of the
+// dense tcgen05 rate; the bound is shared-memory bandwidth, see oz_issue_diagonals), 0.98 ms on
+// the chain's tau draws with the empty k-steps skipped, vs ~3.6 ms for the DMMA V phase of
+// pair_kr.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
