@@ -321,10 +321,17 @@ __global__ void __launch_bounds__(MO_THREADS, MO_CTAS) mo_kernel(SpinorParams P)
               const double sv = swb ? swb[col] : swc[jj][0];
               const double w = col < P.n_occ ? sv : sv * hpv[i];
               const double ar = acc[i][0][jj], ai = acc[i][1][jj], br = acc[i][2][jj], bi = acc[i][3][jj];
-              put(xa, pt, w, col, ar, ai);
-              put(xb, pt, w, col, br, bi);
-              put(xa, pt, w, col + 1, -br, bi);  // -conj(Phi^b_2j)
-              put(xb, pt, w, col + 1, ar, -ai);  //  conj(Phi^a_2j)
+              // columns 2j (a, b) and 2j + 1 (-conj b, conj a) are neighbours in Phi (n_occ is even
+              // on this path, so both sit in one group of four): one 16-byte store per plane
+              const int kidx = col < P.n_occ ? col : col - P.n_occ;
+              const int grp = col < P.n_occ ? (kidx >> 2) : P.Go + (kidx >> 2);
+              double* base = P.phi + ch.offset(grp, pt, P.npts_pad);
+              double* da = base + ((xa * 4 + (kidx & 3)) ^ phi_swz(pt));
+              double* db = base + ((xb * 4 + (kidx & 3)) ^ phi_swz(pt));
+              *reinterpret_cast<double2*>(da) = make_double2(ar * w, -br * w);       // re: a, -conj b
+              *reinterpret_cast<double2*>(da + 16) = make_double2(ai * w, bi * w);   // im
+              *reinterpret_cast<double2*>(db) = make_double2(br * w, ar * w);        // re: b, conj a
+              *reinterpret_cast<double2*>(db + 16) = make_double2(bi * w, -ai * w);  // im
             }
           }
         }
