@@ -39,3 +39,18 @@ def test_engine_job_configs_parse(cfgdir):
     rc = D.parse_run_config(text)
     assert rc["target"] == 0.01 and rc["steps"] is None and rc["interval"] == 100
     assert any(l.startswith("weight") for l in text.splitlines())
+
+
+def test_vgemm_shared_memory_bound_restates_the_kernel_shape():
+    """bench.py's shared-memory bound of oz_vgemm_kernel from the kernel's own shape: per k-step
+    (32 of K') of a 128 x 80 tile, 9 merged MMAs read 9 x 128 x 32 B of A and 21 x 80 x 32 B of B
+    slices and the ring's fills write 6 x (128 + 80) x 32 B, against 128 B/clk/SM on 148 SMs at
+    1965 MHz; it must sit between the kernel's measured rate and the dense tcgen05 rate."""
+    import bench
+    a_reads, b_reads, fills = 9 * 128 * 32, 21 * 80 * 32, 6 * (128 + 80) * 32
+    assert (a_reads, b_reads, fills) == (36864, 53760, 39936)
+    cycles = (a_reads + b_reads + fills) / 128
+    ops = 21 * 2 * 128 * 80 * 32
+    bound = 148 * 1.965e9 * ops / cycles / 1e12
+    assert abs(bound - bench.INT8_SMEM_BOUND) < 1e-6 * bound
+    assert 3000 < bench.INT8_SMEM_BOUND < bench.INT8_PEAK
