@@ -809,8 +809,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
                 const int hi = __double2hiint(v);
                 return __hiloint2double(hi ? hi + e20 : 0, __double2loint(v));
               };
-              sgp = (o01.x * vx(X[4 * k], eb.x) + o01.y * vx(X[4 * k + 1], eb.y)) +
-                    (o23.x * vx(X[4 * k + 2], eb.z) + o23.y * vx(X[4 * k + 3], eb.w));
+              sgp = fma(o23.y, vx(X[4 * k + 3], eb.w),
+                        fma(o23.x, vx(X[4 * k + 2], eb.z), fma(o01.y, vx(X[4 * k + 1], eb.y), o01.x * vx(X[4 * k], eb.x))));
             } else {
               // the refinement's correction df = sum o dV is ~2^-46 of f, so FP32 carries it with
               // room to spare (its rounding is ~2^-66 of f): o_y sb_y as a 24-bit float mantissa
