@@ -102,6 +102,33 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 #endif
 
+// ------------------------------------------------------------------ overlap timeline (debug)
+// OZ_OVERLAP_TL build (tools/overlap_timeline.py): first CTA start and last CTA end of a kernel
+// on the global nanosecond timer, in a per-translation-unit pair g_tl[2] (pair_oz.cu: the slice
+// kernel, pair_kr.cu: the O pass)
+#ifdef OZ_OVERLAP_TL
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define OVERLAP_TL_BEGIN(g) \
+  if (threadIdx.x == 0) atomicMin(&(g)[0], global_ns())
+#define OVERLAP_TL_END(g) \
+  if (threadIdx.x == 0) atomicMax(&(g)[1], global_ns())
+#define OVERLAP_TL_DEFINE(g, getter)                                                       \
+  static __device__ unsigned long long g[2] = {~0ull, 0ull};                              \
+  extern "C" int getter(unsigned long long* host2, int reset) {                          \
+    int e = int(cudaMemcpyFromSymbol(host2, g, 16));                                      \
+    const unsigned long long init[2] = {~0ull, 0ull};                                    \
+    if (reset) e |= int(cudaMemcpyToSymbol(g, init, 16));                                 \
+    return e;                                                                             \
+  }
+#else
+#define OVERLAP_TL_BEGIN(g)
+#define OVERLAP_TL_END(g)
+#endif
+
 // ------------------------------------------------------------------ device system
 struct DevSites {
   int n;

@@ -29,6 +29,16 @@
 #include "kernels.h"
 #include "pair_common.cuh"
 
+#ifdef OZ_OVERLAP_TL
+#if defined(KR_PW4_VARIANT)
+OVERLAP_TL_DEFINE(g_tl_opass, mcmp2dev_debug_tl_opass)
+#elif defined(KR_QB1_VARIANT)
+OVERLAP_TL_DEFINE(g_tl_opass, mcmp2dev_debug_tl_opass_qb1)
+#else
+OVERLAP_TL_DEFINE(g_tl_opass, mcmp2dev_debug_tl_opass_pw2)
+#endif
+#endif
+
 namespace mcmp2dev {
 
 namespace {
@@ -159,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
   // the INT8 path's guard launch: nothing to do unless this step failed the INT8 checks (the
   // main pass without refinement, or the refinement pass: oz_trip 2)
   if (P.guard_fallback && *reinterpret_cast<volatile const int*>(&P.st->oz_trip) != 2) return;
+  if constexpr (OZ == 2) OVERLAP_TL_BEGIN(g_tl_opass);
   extern __shared__ __align__(128) double sm[];
   double* const sO0 = sm + STAGES * STAGE_DOUBLES;
   uint64_t* const full = reinterpret_cast<uint64_t*>(sO0 + OBUF * SO_DOUBLES);
@@ -534,6 +545,7 @@ __global__ void __launch_bounds__(THREADS, MINB) KR_API(pair_kr_kernel)(PairPara
   }
   if constexpr (OZ == 2) {  // the step's sums are oz_vgemm_kernel<true>'s
     if (tid == 0) bulk_store_wait_read();  // the last tile's store is done with shared memory
+    OVERLAP_TL_END(g_tl_opass);
     return;
   }
   __syncthreads();

@@ -48,6 +48,10 @@
 #include "kernels.h"
 #include "pair_common.cuh"
 
+#ifdef OZ_OVERLAP_TL
+OVERLAP_TL_DEFINE(g_tl_slice, mcmp2dev_debug_tl_slice)
+#endif
+
 namespace mcmp2dev {
 
 namespace {
@@ -266,6 +270,7 @@ template <bool HELD>
 __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P) {
   pdl_wait();
   pdl_trigger();
+  OVERLAP_TL_BEGIN(g_tl_slice);
   __shared__ double s_st[8][3];
   __shared__ int s_k[8];
   // one warp per (point, channel): 8 warps = 2 points per CTA (npts_oz is a multiple of 32, so
@@ -306,6 +311,20 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
     if constexpr (HELD) {
 #pragma unroll
       for (int j = 0; j < MAXJ; ++j) load(lane + 32 * j < nq ? lane + 32 * j : nq, hr[j], hi[j]);
+    }
+    // the guard's N stat: this channel's share of |Phi_o(pt)|_F^2 (occupied groups; spinors past
+    // n_occ skipped), read here so its latency runs beside the virtual rows'
+    if (stats && live)
+      for (int g = lane; g < P.Go; g += 32) {
+        const double* src = P.phi + ch.offset(g, pt, P.npts_pad);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * g + i < P.n_occ) {
+            const double re = src[(x * 4 + i) ^ swz], im = src[16 + ((x * 4 + i) ^ swz)];
+            n2 += re * re + im * im;
+          }
+      }
+    if constexpr (HELD) {
 #pragma unroll
       for (int j = 0; j < MAXJ; ++j)
 #pragma unroll
@@ -395,18 +414,8 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
       P.ks_cnt[blockIdx.x] = uint8_t(k);
     }
   }
+  OVERLAP_TL_END(g_tl_slice);
   if (!stats) return;  // uniform over the grid
-  // this channel's share of |Phi_o(pt)|_F^2 (occupied groups; spinors past n_occ skipped)
-  if (live)
-    for (int g = lane; g < P.Go; g += 32) {
-      const double* src = P.phi + ch.offset(g, pt, P.npts_pad);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (4 * g + i < P.n_occ) {
-          const double re = src[(x * 4 + i) ^ swz], im = src[16 + ((x * 4 + i) ^ swz)];
-          n2 += re * re + im * im;
-        }
-    }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     ss += __shfl_xor_sync(0xffffffffu, ss, o);
