@@ -493,6 +493,24 @@ def main():
     dw.advance(nprof, keep_on_device=True)
     prof = dw.profile(enable=False, reset=True)
     ks_prof = dw.int8_ksteps()
+    # ---- the same steps with every k-step of K' issued (the truncation is exact; this is the
+    # untruncated kernel's time for the record, outside the timed region) ----
+    full_k_ms = None
+    if ens == 1 and dw.int8_v() and dw.int8_truncation() and not args.full_k:
+        dw.int8_truncation(0)
+        nfk = max(3, min(args.steps, 10))
+        evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nfk)]
+        dw.advance(1, keep_on_device=True)
+        for k in range(nfk):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                evf[k][0].record(stream)
+            dw.advance(1, keep_on_device=True)
+            with torch.cuda.stream(stream):
+                evf[k][1].record(stream)
+        torch.cuda.synchronize()
+        full_k_ms = sum(a.elapsed_time(b) for a, b in evf) / nfk
+        dw.int8_truncation(1)
     work = dw.work()
     pair_ms = prof["ms"]["pair"] / prof["launches"]["pair"]
     step_ms_prof = prof["ms"]["total"] / prof["launches"]["total"]
@@ -626,6 +644,10 @@ def main():
                            "(exp(-eps tau / 2) below the last slice) are skipped, bit-identical to the full loop "
                            "(tests/test_gpu_oz.py); ksteps_frac = issued / full over the profiled launches, "
                            "ksteps_frac_run over warm-up + timed steps",
+            "full_k_ms_per_step": full_k_ms,
+            "full_k_samples_per_s": samples_per_step / (full_k_ms / 1e3) if full_k_ms else None,
+            "full_k_note": "device time per step of this rank with the truncation switched off "
+                           "(mcmp2dev_oz_truncation 0), measured after the timed region over a few steps",
             "full_loop_equivalent": a8_full, "full_loop_equivalent_note": "the full K' loop's int8 ops over the same "
                                                                           "time (what an untruncated kernel would need)",
             "smem_bound": INT8_SMEM_BOUND, "frac_of_smem_bound": a8 / INT8_SMEM_BOUND,
