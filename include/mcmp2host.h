@@ -57,6 +57,21 @@ int mcmp2h_group_size(const mcmp2h_group* g);
 int mcmp2h_group_advance(mcmp2h_group* g, const long long* nsteps);
 int mcmp2h_group_stats(mcmp2h_group* g, int k, double* out10);
 
+/* The checkpoint of a run whose workers live in several processes (one rank per GPU): the file
+ * is mcmp2h_checkpoint_header (driver.cpp:222-230) followed by every worker's
+ * mcmp2h_group_record in worker order (driver.cpp:232-247), byte-identical to what the
+ * single-process Engine writes, so `mcmp2 resume` / `mcmp2 merge` read it; mcmp2h_group_trace
+ * is a worker's trace lines (driver.cpp:311-321). Text calls copy when cap suffices and always
+ * set *need to the size with the terminator. mcmp2h_checkpoint_config checks the stored hash
+ * (driver.cpp:482-491) and returns the stored config; mcmp2h_group_resume builds workers
+ * [first_index, first_index + count) from their records instead of init + burn-in, the cached
+ * weights re-verified (driver.cpp:360-373). */
+int mcmp2h_checkpoint_header(const char* config_text, int nworkers, char* buf, long cap, long* need);
+int mcmp2h_group_record(mcmp2h_group* g, int k, char* buf, long cap, long* need);
+int mcmp2h_group_trace(mcmp2h_group* g, int k, char* buf, long cap, long* need);
+int mcmp2h_checkpoint_config(const char* checkpoint_path, char* canonical, int cap, int* nworkers);
+mcmp2h_group* mcmp2h_group_resume(const char* checkpoint_path, int first_index, int count, int device);
+
 /* writes <dir>/<name>.spinor and <dir>/<name>.conf for BASELINE configs cfg1..cfg4, cfg5-N */
 int mcmp2h_generate(const char* name, const char* dir);
 

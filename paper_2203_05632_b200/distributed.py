@@ -8,13 +8,21 @@ per-worker estimates by step-count weighting (driver.cpp:183-196) for the target
 rule (driver.cpp:401-412). Here each rank (torchrun, one GPU each) hosts a contiguous range of
 the workers (at least one; a range of several shares one batched device handle when the walker
 count allows it), and the interval merge is one all_gather of the workers' 7-double summaries --
-the only collective; the walker loop itself has no communication. Launch:
+the only collective of the stop rule; the walker loop itself has no communication. A config that
+names a `checkpoint` or `trace` file gets them as the reference Engine writes them
+(driver.cpp:218-251, 311-334): every interval each rank sends its workers' checkpoint records and
+trace lines to rank 0 (a second all_gather, of bytes), which writes the one file holding every
+worker's record, byte-identical to the single-process Engine's, so `resume` here, `mcmp2 resume`
+and `mcmp2 merge` all read it. Launch:
 
   torchrun --nproc-per-node N -m paper_2203_05632_b200.distributed CONFIG_FILE
+  torchrun --nproc-per-node N -m paper_2203_05632_b200.distributed resume CHECKPOINT_FILE
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
+import struct
 import sys
 from dataclasses import dataclass
 
@@ -99,16 +107,105 @@ def parse_run_config(text: str) -> dict:
             "checkpoint": cfg.get("checkpoint"), "trace": cfg.get("trace")}
 
 
-def require_no_files(rc: dict) -> None:
-    """The multi-process driver merges estimates only; the checkpoint (driver.cpp:218-305) and
-    trace files of the reference Engine hold every worker's record in one file written by one
-    process, which this driver does not assemble. A run that asks for them is refused rather
-    than silently run without them: use the single-process Engine (`mcmp2 run`, one device
-    handle per worker) for checkpointed or traced runs."""
-    for key in ("checkpoint", "trace"):
-        if rc.get(key):
-            raise ValueError(f"distributed driver: '{key}' is not supported across ranks "
-                             "(run the config with the single-process Engine, `mcmp2 run`)")
+def _sized_text(call, *args) -> bytes:
+    """A text-returning host call of the (buf, cap, need) shape (include/mcmp2host.h)."""
+    need = C.c_long(0)
+    check_host(call(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check_host(call(*args, buf, need.value, C.byref(need)))
+    return buf.value
+
+
+def gather_bytes(all_gather, blob: bytes) -> list[bytes]:
+    """Every rank's byte string on every rank: the lengths, then the padded bytes."""
+    lens = [int(a[0]) for a in all_gather(np.array([len(blob)], dtype=np.int64))]
+    send = np.zeros(max(max(lens), 1), dtype=np.uint8)
+    send[:len(blob)] = np.frombuffer(blob, dtype=np.uint8)
+    return [bytes(np.asarray(a, dtype=np.uint8)[:n]) for a, n in zip(all_gather(send), lens)]
+
+
+def _pack(items: list[bytes]) -> bytes:
+    return struct.pack("<q", len(items)) + b"".join(struct.pack("<q", len(x)) + x for x in items)
+
+
+def _unpack(blob: bytes) -> list[bytes]:
+    (n,), at, out = struct.unpack_from("<q", blob, 0), 8, []
+    for _ in range(n):
+        (k,) = struct.unpack_from("<q", blob, at)
+        out.append(blob[at + 8:at + 8 + k])
+        at += 8 + k
+    return out
+
+
+def _replace_file(path: str, data: bytes) -> None:
+    with open(path + ".tmp", "wb") as f:
+        f.write(data)
+    os.replace(path + ".tmp", path)
+
+
+class RunFiles:
+    """The Engine's per-interval files for workers spread over ranks. The checkpoint
+    (driver.cpp:218-251: written to <path>.tmp, then renamed) is the header plus every worker's
+    record in worker order; the trace (driver.cpp:311-334) is one <trace>.w<k> file per worker
+    rewritten every interval and joined in worker order when the run ends. Ranks hold
+    contiguous ascending worker ranges (rank_workers), so rank order is worker order. Rank 0
+    writes; the other ranks only send."""
+
+    def __init__(self, config_text: str, rc: dict, rank: int, all_gather):
+        self.checkpoint, self.trace = rc.get("checkpoint"), rc.get("trace")
+        self.rank, self.all_gather, self.nworkers = rank, all_gather, rc["workers"]
+        self.header = b""
+        if self.checkpoint and rank == 0:
+            self.header = _sized_text(native.host().mcmp2h_checkpoint_header, config_text.encode(), self.nworkers)
+
+    def __bool__(self):
+        return bool(self.checkpoint or self.trace)
+
+    def write_interval(self, group) -> None:
+        if not self:
+            return
+        records = group.records() if self.checkpoint else []
+        traces = group.traces() if self.trace else []
+        idx = [struct.pack("<q", group.first + k) for k in range(group.count)]
+        parts = [_unpack(b) for b in gather_bytes(self.all_gather, _pack(idx + records + traces))]
+        if self.rank != 0:
+            return
+        workers, recs, trs = [], [], []
+        for p in parts:
+            n = len(p) // (1 + bool(self.checkpoint) + bool(self.trace))
+            workers += [struct.unpack("<q", x)[0] for x in p[:n]]
+            if self.checkpoint:
+                recs += p[n:2 * n]
+            trs += p[len(p) - n:] if self.trace else []
+        if workers != list(range(self.nworkers)):
+            raise native.Mcmp2Error(f"distributed driver: gathered workers {workers}, expected 0..{self.nworkers - 1}")
+        if self.checkpoint:
+            _replace_file(self.checkpoint, self.header + b"".join(recs))
+        for k, t in zip(workers, trs):
+            _replace_file(f"{self.trace}.w{k}", t)
+
+    def finish(self) -> None:  # join_traces, driver.cpp:323-334
+        if not self.trace or self.rank != 0:
+            return
+        with open(self.trace, "wb") as out:
+            for k in range(self.nworkers):
+                if os.path.exists(f"{self.trace}.w{k}"):
+                    out.write(open(f"{self.trace}.w{k}", "rb").read())
+        for k in range(self.nworkers):
+            if os.path.exists(f"{self.trace}.w{k}"):
+                os.remove(f"{self.trace}.w{k}")
+
+
+def checkpoint_run_config(path: str) -> tuple[str, dict]:
+    """The config stored in a checkpoint after the hash check of resume (driver.cpp:482-491);
+    the run continues with the saved workers (driver.cpp:349: restored.size())."""
+    buf = C.create_string_buffer(1 << 14)
+    nw = C.c_int(0)
+    check_host(native.host().mcmp2h_checkpoint_config(str(path).encode(), buf, len(buf), C.byref(nw)))
+    text = buf.value.decode()
+    rc = parse_run_config(text)
+    rc["workers"] = nw.value
+    return text, rc
 
 
 class HostGroup:
@@ -116,9 +213,12 @@ class HostGroup:
     mcmp2h_group): one batched device handle when the walker count allows it
     (include/mcmp2dev.h, batched ensembles), else one handle each; init + burn-in at creation."""
 
-    def __init__(self, config_text: str, first: int, count: int, device: int):
+    def __init__(self, config_text: str, first: int, count: int, device: int, resume_from: str | None = None):
         h = native.host()
-        self._g = h.mcmp2h_group_create(config_text.encode(), first, count, device)
+        if resume_from is None:
+            self._g = h.mcmp2h_group_create(config_text.encode(), first, count, device)
+        else:  # workers restored from their checkpoint records (driver.cpp:360-373)
+            self._g = h.mcmp2h_group_resume(str(resume_from).encode(), first, count, device)
         if not self._g:
             raise native.Mcmp2Error(h.mcmp2h_last_error().decode())
         self.first, self.count = first, count
@@ -134,6 +234,12 @@ class HostGroup:
             check_host(native.host().mcmp2h_group_stats(self._g, k, dptr(o)))
             out.append(Summary(self.first + k, int(o[0]), o[3], o[4], o[8], o[9], int(o[7])))
         return out
+
+    def records(self) -> list[bytes]:
+        return [_sized_text(native.host().mcmp2h_group_record, self._g, k) for k in range(self.count)]
+
+    def traces(self) -> list[bytes]:
+        return [_sized_text(native.host().mcmp2h_group_trace, self._g, k) for k in range(self.count)]
 
     def close(self):
         if getattr(self, "_g", None):
@@ -170,14 +276,16 @@ def rank_workers(total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def drive_group(group, total_workers: int, steps: int | None, target: float | None, interval: int, all_gather,
-                max_intervals: int | None = None) -> dict:
+                max_intervals: int | None = None, files: "RunFiles | None" = None) -> dict:
     """Engine::drive (driver.cpp:376-420) over all ranks' workers: every interval each worker
     advances its share, the summaries of all workers are gathered (one all_gather; ranks hold
     different worker counts, so the rows are padded with index -1) and the stop rule is
-    evaluated identically on every rank."""
+    evaluated identically on every rank. `files` writes the interval's checkpoint and traces
+    before the stop rule, as the Engine does; `max_intervals` is its abort hook
+    (RunHooks::abort_after_intervals). Resumed workers carry their step counts in."""
     intervals = 0
     on_target = False
-    done = [0] * group.count
+    done = [s.steps for s in group.summaries()]
     while True:
         idx = range(group.first, group.first + group.count)
         chunk = [interval if steps is None else min(interval, worker_share(steps, total_workers, i) - d)
@@ -185,6 +293,8 @@ def drive_group(group, total_workers: int, steps: int | None, target: float | No
         group.advance(chunk)
         done = [d + max(c, 0) for d, c in zip(done, chunk)]
         intervals += 1
+        if files:
+            files.write_interval(group)
         local = np.stack([s.as_array() for s in group.summaries()])
         pad = np.full((total_workers - len(local), local.shape[1]), -1.0) if total_workers > len(local) else None
         send = np.concatenate([local, pad]) if pad is not None else local
@@ -199,7 +309,11 @@ def drive_group(group, total_workers: int, steps: int | None, target: float | No
                 on_target = True
                 break
         if max_intervals is not None and intervals >= max_intervals:
-            break
+            value, sigma_bar, total = merge_estimates(parts)
+            return {"value": value, "sigma_bar": sigma_bar, "total_steps": total, "stopped_on_target": False,
+                    "workers": parts, "intervals": intervals}
+    if files:
+        files.finish()
     value, sigma_bar, total = merge_estimates(parts)
     return {"value": value, "sigma_bar": sigma_bar, "total_steps": total, "stopped_on_target": on_target,
             "workers": parts, "intervals": intervals}
@@ -236,23 +350,25 @@ def torch_all_gather(dist):
 
 
 def main(argv=None):
-    import os
-
     import torch
     import torch.distributed as dist
 
     argv = sys.argv[1:] if argv is None else argv
-    text = open(argv[0]).read()
+    resume_from = argv[1] if argv[0] == "resume" else None
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rc = parse_run_config(text)
-    require_no_files(rc)
+    if resume_from is None:
+        text = open(argv[0]).read()
+        rc = parse_run_config(text)
+    else:
+        text, rc = checkpoint_run_config(resume_from)
     first, count = rank_workers(rc["workers"], world, rank)
-    group = HostGroup(text, first, count, local)
-    rep = drive_group(group, rc["workers"], rc["steps"], rc["target"], rc["interval"],
-                      torch_all_gather(dist))
+    group = HostGroup(text, first, count, local, resume_from)
+    gather = torch_all_gather(dist)
+    rep = drive_group(group, rc["workers"], rc["steps"], rc["target"], rc["interval"], gather,
+                      files=RunFiles(text, rc, rank, gather))
     if rank == 0:
         sys.stdout.write(format_report(rep))
     dist.destroy_process_group()

@@ -62,33 +62,90 @@ extern "C" {
 
 const char* mcmp2h_last_error(void) { return g_err.c_str(); }
 
+namespace {
+// workers [first, first + count) on one device; restored from `resume_path` when given, else
+// init + burn-in (driver.cpp:354-373)
+mcmp2h_group* make_group(const RunConfig& cfg, int first_index, int count, int device, const char* resume_path) {
+  if (count < 1) throw std::invalid_argument("group: at least one worker");
+  auto g = std::make_unique<mcmp2h_group>();
+  g->cfg = cfg;
+  g->cfg.validate();
+  g->spinors = std::make_unique<SpinorSet>(load_spinor_set(g->cfg.spinor_path));
+  if (!g->spinors->nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
+  g->spec = std::make_unique<WeightSpec>(*g->spinors->nuclei, g->cfg.weight_overrides);
+  if (count > 1 && g->cfg.walkers % 16 == 0 && g->cfg.walkers <= 480) {
+    DeviceSystem sys = make_device_system(*g->spinors, *g->spec,
+                                          g->cfg.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
+    g->batch = std::make_shared<DeviceBatch>();
+    check_dev(mcmp2dev_create(&sys.view, device, count * g->cfg.walkers, &g->batch->h), nullptr);
+    g->batch->first = first_index;
+    g->batch->nens = count;
+    g->batch->m = g->cfg.walkers;
+  }
+  for (int k = 0; k < count; ++k) {
+    if (g->batch) g->workers.push_back(std::make_unique<DeviceWorker>(g->batch, k, g->cfg, first_index + k));
+    else g->workers.push_back(std::make_unique<DeviceWorker>(*g->spinors, *g->spec, g->cfg, first_index + k, device));
+  }
+  if (resume_path) {
+    std::vector<DeviceWorker*> ws;
+    for (auto& w : g->workers) ws.push_back(w.get());
+    restore_workers(resume_path, *g->spec, g->cfg, ws);
+  } else {
+    for (auto& w : g->workers) w->init_and_burn_in();
+  }
+  return g.release();
+}
+
+int copy_sized(const std::string& s, char* buf, long cap, long* need) {
+  if (need) *need = long(s.size()) + 1;
+  if (buf && cap > long(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+}  // namespace
+
 mcmp2h_group* mcmp2h_group_create(const char* config_text, int first_index, int count, int device) {
   mcmp2h_group* out = nullptr;
-  guard([&] {
-    if (count < 1) throw std::invalid_argument("group: at least one worker");
-    auto g = std::make_unique<mcmp2h_group>();
-    g->cfg = parse_config_text(config_text);
-    g->cfg.validate();
-    g->spinors = std::make_unique<SpinorSet>(load_spinor_set(g->cfg.spinor_path));
-    if (!g->spinors->nuclei) throw std::runtime_error("spinor file has no nuclei record; the sampling weight needs it");
-    g->spec = std::make_unique<WeightSpec>(*g->spinors->nuclei, g->cfg.weight_overrides);
-    if (count > 1 && g->cfg.walkers % 16 == 0 && g->cfg.walkers <= 480) {
-      DeviceSystem sys = make_device_system(*g->spinors, *g->spec,
-                                            g->cfg.physical ? MCMP2DEV_ESTIMATOR_PHYSICAL : MCMP2DEV_ESTIMATOR_LITERAL);
-      g->batch = std::make_shared<DeviceBatch>();
-      check_dev(mcmp2dev_create(&sys.view, device, count * g->cfg.walkers, &g->batch->h), nullptr);
-      g->batch->first = first_index;
-      g->batch->nens = count;
-      g->batch->m = g->cfg.walkers;
-    }
-    for (int k = 0; k < count; ++k) {
-      if (g->batch) g->workers.push_back(std::make_unique<DeviceWorker>(g->batch, k, g->cfg, first_index + k));
-      else g->workers.push_back(std::make_unique<DeviceWorker>(*g->spinors, *g->spec, g->cfg, first_index + k, device));
-    }
-    for (auto& w : g->workers) w->init_and_burn_in();
-    out = g.release();
-  });
+  guard([&] { out = make_group(parse_config_text(config_text), first_index, count, device, nullptr); });
   return out;
+}
+
+mcmp2h_group* mcmp2h_group_resume(const char* checkpoint_path, int first_index, int count, int device) {
+  mcmp2h_group* out = nullptr;
+  guard([&] { out = make_group(checkpoint_config(checkpoint_path), first_index, count, device, checkpoint_path); });
+  return out;
+}
+
+int mcmp2h_checkpoint_config(const char* checkpoint_path, char* canonical, int cap, int* nworkers) {
+  return guard([&] {
+    std::vector<int> idx;
+    const RunConfig c = checkpoint_config(checkpoint_path, &idx);
+    for (std::size_t k = 0; k < idx.size(); ++k)
+      if (idx[k] != int(k)) throw std::runtime_error("checkpoint: worker records are not 0 .. workers - 1");
+    if (nworkers) *nworkers = int(idx.size());
+    copy_out(canonical_config_text(c), canonical, cap);
+  });
+}
+
+int mcmp2h_checkpoint_header(const char* config_text, int nworkers, char* buf, long cap, long* need) {
+  return guard([&] {
+    const RunConfig c = parse_config_text(config_text);
+    c.validate();
+    copy_sized(checkpoint_header_text(c, std::size_t(nworkers)), buf, cap, need);
+  });
+}
+
+int mcmp2h_group_record(mcmp2h_group* g, int k, char* buf, long cap, long* need) {
+  return guard([&] {
+    if (k < 0 || k >= int(g->workers.size())) throw std::invalid_argument("group: no such worker");
+    copy_sized(worker_record_text(*g->workers[k]), buf, cap, need);
+  });
+}
+
+int mcmp2h_group_trace(mcmp2h_group* g, int k, char* buf, long cap, long* need) {
+  return guard([&] {
+    if (k < 0 || k >= int(g->workers.size())) throw std::invalid_argument("group: no such worker");
+    copy_sized(worker_trace_text(*g->workers[k]), buf, cap, need);
+  });
 }
 
 void mcmp2h_group_free(mcmp2h_group* g) { delete g; }

@@ -382,6 +382,25 @@ void DeviceWorker::load_ensemble(const std::string& text) {  // sampler.cpp:107-
 }
 
 // ------------------------------------------------------------------ checkpoint (driver.cpp:218-305)
+// one worker's checkpoint record (driver.cpp:232-247) and trace lines (driver.cpp:311-321) as
+// text: the Engine writes them itself, a multi-process driver sends them to the writing rank
+std::string worker_record_text(const DeviceWorker& w) {
+  std::ostringstream out;
+  out << "worker " << w.index() << "\n" << "steps " << w.acc.count() << "\n";
+  out << "sums " << format_double(w.acc.real_sum()) << ' ' << format_double(w.acc.imag_sum()) << "\n";
+  out << "partial " << w.acc.in_block() << ' ' << format_double(w.acc.partial()) << "\n";
+  out << "blocks " << w.acc.block_means().size() << "\n";
+  for (double b : w.acc.block_means()) out << format_double(b) << "\n";
+  out << "ensemble\n" << w.save_ensemble() << "end-worker\n";
+  return out.str();
+}
+
+std::string worker_trace_text(const DeviceWorker& w) {
+  std::ostringstream out;
+  for (const auto& t : w.acc.trace()) out << t.n << ' ' << format_double(t.mean) << ' ' << format_double(t.sigma_bar) << "\n";
+  return out.str();
+}
+
 namespace {
 struct SavedWorker {
   int index = 0;
@@ -460,26 +479,48 @@ Checkpoint read_checkpoint(const std::string& path) {
   return ck;
 }
 
+std::string header_text(std::uint64_t hash, const RunConfig& cfg, std::size_t nworkers) {
+  std::ostringstream out;
+  out << "mcmp2-checkpoint 1\n" << "confighash " << hash << "\n";
+  out << "config-begin\n" << canonical_config_text(cfg) << "config-end\n";
+  out << "workers " << nworkers << "\n";
+  return out.str();
+}
+
 void write_checkpoint(const std::string& path, std::uint64_t hash, const RunConfig& cfg,
                       const std::vector<std::unique_ptr<DeviceWorker>>& workers) {
   const std::string tmp = path + ".tmp";
   {
     std::ofstream out(tmp);
     if (!out) throw std::runtime_error("cannot write checkpoint: " + tmp);
-    out << "mcmp2-checkpoint 1\n" << "confighash " << hash << "\n";
-    out << "config-begin\n" << canonical_config_text(cfg) << "config-end\n";
-    out << "workers " << workers.size() << "\n";
-    for (const auto& w : workers) {
-      out << "worker " << w->index() << "\n" << "steps " << w->acc.count() << "\n";
-      out << "sums " << format_double(w->acc.real_sum()) << ' ' << format_double(w->acc.imag_sum()) << "\n";
-      out << "partial " << w->acc.in_block() << ' ' << format_double(w->acc.partial()) << "\n";
-      out << "blocks " << w->acc.block_means().size() << "\n";
-      for (double b : w->acc.block_means()) out << format_double(b) << "\n";
-      out << "ensemble\n" << w->save_ensemble() << "end-worker\n";
-    }
+    out << header_text(hash, cfg, workers.size());
+    for (const auto& w : workers) out << worker_record_text(*w);
     if (!out) throw std::runtime_error("failed writing checkpoint: " + tmp);
   }
   std::filesystem::rename(tmp, path);
+}
+
+// one saved record back into a worker; cached weights re-verified against recomputation
+// (driver.cpp:360-373)
+void restore_worker(DeviceWorker& w, const SavedWorker& s, const WeightSpec& spec, const RunConfig& cfg) {
+  w.acc = BlockingAccumulator(cfg.block_size);
+  w.acc.restore(s.steps, s.sum, s.imag, s.in_block, s.partial, s.means);
+  w.done = s.steps;
+  std::istringstream is(s.ensemble);
+  int m;
+  is >> m;
+  if (m != cfg.walkers) throw std::runtime_error("checkpoint: walker count disagrees with config");
+  std::string line;
+  std::getline(is, line);
+  std::getline(is, line);
+  for (int p = 0; p < m; ++p) {
+    double v[9];
+    for (double& x : v) is >> x;
+    const double g1 = spec.g({v[0], v[1], v[2]}), g2 = spec.g({v[3], v[4], v[5]});
+    if (std::abs(g1 - v[6]) > 1e-12 * std::abs(g1) || std::abs(g2 - v[7]) > 1e-12 * std::abs(g2))
+      throw std::runtime_error("checkpoint: cached walker weights disagree with recomputation");
+  }
+  w.load_ensemble(s.ensemble);
 }
 
 WorkerSummary summarize_saved(const SavedWorker& w, long block_size) {
@@ -500,7 +541,7 @@ void write_trace(const std::string& trace_path, const DeviceWorker& w) {  // dri
   {
     std::ofstream out(path + ".tmp");
     if (!out) throw std::runtime_error("cannot write trace file: " + path + ".tmp");
-    for (const auto& t : w.acc.trace()) out << t.n << ' ' << format_double(t.mean) << ' ' << format_double(t.sigma_bar) << "\n";
+    out << worker_trace_text(w);
   }
   std::filesystem::rename(path + ".tmp", path);
 }
@@ -564,25 +605,7 @@ class Engine {  // driver.cpp:336-475
       for (std::size_t k = 0; k < restored.size(); ++k) {
         const SavedWorker& s = restored[k];
         DeviceWorker& w = *workers_[k];
-        w.acc = BlockingAccumulator(cfg_.block_size);
-        w.acc.restore(s.steps, s.sum, s.imag, s.in_block, s.partial, s.means);
-        w.done = s.steps;
-        // cached weights re-verified against recomputation (driver.cpp:360-373)
-        std::istringstream is(s.ensemble);
-        int m;
-        is >> m;
-        if (m != cfg_.walkers) throw std::runtime_error("checkpoint: walker count disagrees with config");
-        std::string line;
-        std::getline(is, line);
-        std::getline(is, line);
-        for (int p = 0; p < m; ++p) {
-          double v[9];
-          for (double& x : v) is >> x;
-          const double g1 = spec_->g({v[0], v[1], v[2]}), g2 = spec_->g({v[3], v[4], v[5]});
-          if (std::abs(g1 - v[6]) > 1e-12 * std::abs(g1) || std::abs(g2 - v[7]) > 1e-12 * std::abs(g2))
-            throw std::runtime_error("checkpoint: cached walker weights disagree with recomputation");
-        }
-        w.load_ensemble(s.ensemble);
+        restore_worker(w, s, *spec_, cfg_);
       }
     }
   }
@@ -687,6 +710,31 @@ RunReport resume(const std::string& path, const RunHooks& hooks) {  // driver.cp
     throw std::runtime_error("checkpoint: config hash mismatch (spinor file or physics settings changed)");
   Engine e(ck.config, std::move(ck.workers), hooks);
   return e.drive(hooks);
+}
+
+std::string checkpoint_header_text(const RunConfig& cfg, std::size_t nworkers) {
+  return header_text(config_hash(cfg, hash_file_contents(cfg.spinor_path)), cfg, nworkers);
+}
+
+RunConfig checkpoint_config(const std::string& path, std::vector<int>* indices) {
+  Checkpoint ck = read_checkpoint(path);
+  if (config_hash(ck.config, hash_file_contents(ck.config.spinor_path)) != ck.hash)
+    throw std::runtime_error("checkpoint: config hash mismatch (spinor file or physics settings changed)");
+  if (indices)
+    for (const auto& w : ck.workers) indices->push_back(w.index);
+  return ck.config;
+}
+
+void restore_workers(const std::string& path, const WeightSpec& spec, const RunConfig& cfg,
+                     const std::vector<DeviceWorker*>& ws) {
+  const Checkpoint ck = read_checkpoint(path);
+  for (DeviceWorker* w : ws) {
+    const SavedWorker* rec = nullptr;
+    for (const auto& s : ck.workers)
+      if (s.index == w->index()) rec = &s;
+    if (!rec) throw std::runtime_error("checkpoint: missing worker record");
+    restore_worker(*w, *rec, spec, cfg);
+  }
 }
 
 MergedEstimate merge_checkpoint_files(const std::vector<std::string>& paths,

@@ -241,6 +241,18 @@ class DeviceWorker {
 
 void check_dev(int rc, const mcmp2dev_t* h);
 
+// The checkpoint file in pieces, for a driver whose workers live in several processes
+// (distributed.py): header (driver.cpp:222-230; hashes the spinor file), then every worker's
+// record in worker order (driver.cpp:232-247); a worker's trace lines (driver.cpp:311-321).
+std::string checkpoint_header_text(const RunConfig& cfg, std::size_t nworkers);
+std::string worker_record_text(const DeviceWorker& w);
+std::string worker_trace_text(const DeviceWorker& w);
+// the stored config after the hash check of resume (driver.cpp:482-491); the saved worker indices
+RunConfig checkpoint_config(const std::string& path, std::vector<int>* indices = nullptr);
+// restores each worker from the record carrying its index (weights re-verified, driver.cpp:360-373)
+void restore_workers(const std::string& path, const WeightSpec& spec, const RunConfig& cfg,
+                     const std::vector<DeviceWorker*>& ws);
+
 // ---- BASELINE config generator (host/generate.cpp) ----
 SpinorSet generate_spinor_set(const std::string& name);  // cfg1..cfg4, cfg5-N
 std::string generate_run_config(const std::string& name, const std::string& spinor_path);

@@ -141,6 +141,20 @@ def host() -> C.CDLL:
         h.mcmp2h_worker_block_means.argtypes = [vp, dp, ip]
         h.mcmp2h_worker_device.restype = vp
         h.mcmp2h_worker_device.argtypes = [vp]
+        lp = C.POINTER(C.c_long)
+        h.mcmp2h_group_create.restype = vp
+        h.mcmp2h_group_create.argtypes = [cp, ip, ip, ip]
+        h.mcmp2h_group_resume.restype = vp
+        h.mcmp2h_group_resume.argtypes = [cp, ip, ip, ip]
+        h.mcmp2h_group_free.argtypes = [vp]
+        h.mcmp2h_group_size.argtypes = [vp]
+        h.mcmp2h_group_advance.argtypes = [vp, C.POINTER(C.c_longlong)]
+        h.mcmp2h_group_stats.argtypes = [vp, ip, dp]
+        h.mcmp2h_group_record.argtypes = [vp, ip, cp, C.c_long, lp]
+        h.mcmp2h_group_trace.argtypes = [vp, ip, cp, C.c_long, lp]
+        h.mcmp2h_checkpoint_header.argtypes = [cp, ip, cp, C.c_long, lp]
+        h.mcmp2h_checkpoint_config.argtypes = [cp, cp, ip, C.POINTER(C.c_int)]
+        h.mcmp2h_merge_estimates.argtypes = [dp, ip, dp]
         h.mcmp2h_generate.argtypes = [cp, cp]
         _host = h
     return _host

@@ -78,6 +78,30 @@ class OracleGroupStandIn:
     def summaries(self):
         return [w.summary() for w in self.ws]
 
+    def records(self):
+        """The Engine's worker record (driver.cpp:232-247) from the stand-in's accumulator; the
+        ensemble section is a two-walker placeholder in WalkerEnsemble::save's line layout."""
+        out = []
+        for w in self.ws:
+            a = w.acc
+            r = repr  # shortest round-trip text, as the host's format_double
+            txt = (f"worker {w.index}\nsteps {a.n}\nsums {r(float(a.sum))} {r(float(a.imag))}\n"
+                   f"partial {a.inb} {r(float(a.partial))}\nblocks {len(a.means)}\n" +
+                   "".join(r(float(b)) + "\n" for b in a.means) +
+                   "ensemble\n2 0.5 10 5\n0 0 0 0 0 0\n" + "0 0 0 0 0 0 1 1 0\n" * 2 + "end-worker\n")
+            out.append(txt.encode())
+        return out
+
+    def traces(self):
+        out = []
+        for w in self.ws:
+            lines, n = [], 0
+            for k in range(len(w.acc.means)):
+                n += w.acc.nb
+                lines.append(f"{n} {k} w{w.index}\n")
+            out.append("".join(lines).encode())
+        return out
+
 
 def _group_rank(rank, world, port, args, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -86,7 +110,13 @@ def _group_rank(rank, world, port, args, q):
     spinor, conf, m, burn, steps, interval, seed, block, workers = args
     first, count = D.rank_workers(workers, world, rank)
     g = OracleGroupStandIn(spinor, conf, first, count, m, burn, steps, workers, seed, block)
-    rep = D.drive_group(g, workers, steps, None, interval, D.torch_all_gather(dist))
+    gather = D.torch_all_gather(dist)
+    files = None
+    if os.environ.get("MCMP2_TEST_FILES"):
+        ck, tr = os.environ["MCMP2_TEST_FILES"].split(":")
+        text = conf + f"spinors {spinor}\nsteps {steps}\nworkers {workers}\ncheckpoint {ck}\ntrace {tr}\n"
+        files = D.RunFiles(text, D.parse_run_config(text), rank, gather)
+    rep = D.drive_group(g, workers, steps, None, interval, gather, files=files)
     q.put((rank, rep["value"], rep["sigma_bar"], rep["total_steps"], [(p.index, p.steps) for p in rep["workers"]]))
     dist.destroy_process_group()
 
@@ -227,6 +257,75 @@ def test_device_groups_over_two_ranks_match_the_engine(cfgdir):
     assert out[0][1] == walker.run_config_text(text)
 
 
+def _device_files_rank(rank, world, port, text, resume_from, max_intervals, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if resume_from:
+        text, rc = D.checkpoint_run_config(resume_from)
+    else:
+        rc = D.parse_run_config(text)
+    first, count = D.rank_workers(rc["workers"], world, rank)
+    g = D.HostGroup(text, first, count, 0, resume_from)
+    gather = D.torch_all_gather(dist)
+    rep = D.drive_group(g, rc["workers"], rc["steps"], rc["target"], rc["interval"], gather,
+                        max_intervals=max_intervals, files=D.RunFiles(text, rc, rank, gather))
+    q.put((rank, D.format_report(rep)))
+    g.close()
+    dist.destroy_process_group()
+
+
+def _run_device_files(text, resume_from=None, max_intervals=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_files_rank, args=(r, 2, port, text, resume_from, max_intervals, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert out[0][1] == out[1][1]
+    return out[0][1]
+
+
+@pytest.mark.gpu
+def test_device_groups_checkpoint_trace_and_resume_across_ranks(cfgdir, tmp_path):
+    """Two ranks (gloo, one GPU), 4 cfg1 workers, `checkpoint` and `trace` set: the files rank 0
+    assembles are byte-identical to the single-process Engine's (driver.cpp:218-251, 311-334);
+    a run stopped after one interval and resumed across ranks, or by the single-process
+    `resume`, ends on the uninterrupted report and checkpoint (SPEC: kill/resume matches an
+    uninterrupted run)."""
+    from paper_2203_05632_b200 import walker
+    ck, tr = tmp_path / "run.ck", tmp_path / "run.trace"
+    text = (f"spinors {cfgdir / 'cfg1.spinor'}\nsteps 1002\nwalkers 16\nworkers 4\nseed 9\nburnin 50\n"
+            f"checkpoint-interval 200\nstep-size 0.3\nblocksize 25\ncheckpoint {ck}\ntrace {tr}\n" +
+            "".join(l + "\n" for l in (cfgdir / "cfg1.conf").read_text().splitlines() if l.startswith("weight")))
+    ref_report = walker.run_config_text(text)
+    ref_ck, ref_tr = ck.read_bytes(), tr.read_bytes()
+    assert ref_tr
+    ck.unlink(), tr.unlink()
+
+    assert _run_device_files(text) == ref_report
+    assert ck.read_bytes() == ref_ck and tr.read_bytes() == ref_tr
+    ck.unlink(), tr.unlink()
+
+    partial = _run_device_files(text, max_intervals=1)
+    assert partial != ref_report and b"\nsteps 200\n" in ck.read_bytes()
+    stopped = ck.read_bytes()
+    assert _run_device_files(None, resume_from=str(ck)) == ref_report
+    assert ck.read_bytes() == ref_ck and tr.read_bytes() == ref_tr
+
+    ck.write_bytes(stopped)  # the same stopped run continued by the single-process Engine
+    assert walker.resume(ck) == ref_report
+    assert ck.read_bytes() == ref_ck
+
+    ck.write_bytes(stopped.replace(b"end-worker\n", b"", 1))
+    with pytest.raises(Exception, match="checkpoint"):
+        D.HostGroup("", 0, 2, 0, str(ck))
+
+
 def test_fewer_workers_than_ranks_is_an_error():
     """rank_workers refuses to raise the worker count (it would change the run's streams and
     shares, which the config hash names); an exact split is accepted."""
@@ -235,11 +334,48 @@ def test_fewer_workers_than_ranks_is_an_error():
     assert [D.rank_workers(2, 2, r) for r in range(2)] == [(0, 1), (1, 1)]
 
 
-def test_checkpoint_and_trace_are_refused_across_ranks(cfgdir):
-    """The torchrun driver does not assemble the Engine's checkpoint/trace files, so a config
-    naming them is refused with a clear error instead of silently running without them."""
-    base = f"spinors {cfgdir / 'cfg1.spinor'}\nsteps 100\nworkers 2\n"
-    D.require_no_files(D.parse_run_config(base))
-    for extra in ("checkpoint /tmp/ck\n", "trace /tmp/tr\n"):
-        with pytest.raises(ValueError, match="not supported across ranks"):
-            D.require_no_files(D.parse_run_config(base + extra))
+def test_checkpoint_and_trace_assembled_on_rank_0(cfgdir, tmp_path, monkeypatch):
+    """workers 5 over 2 ranks with `checkpoint` and `trace` set: rank 0 writes one checkpoint
+    holding all five records in worker order behind the host's header (driver.cpp:218-251), which
+    the host's `merge` (driver.cpp:502-521) reads back to the run's own merged estimate; the
+    per-worker trace files are joined in worker order at the end (driver.cpp:323-334)."""
+    from paper_2203_05632_b200 import walker
+    spinor = cfgdir / "syn1c.spinor"
+    conf = "walkers 6\nburnin 30\nblocksize 10\ncheckpoint-interval 40\nseed 4\n"
+    ck, tr = tmp_path / "run.ck", tmp_path / "run.trace"
+    monkeypatch.setenv("MCMP2_TEST_FILES", f"{ck}:{tr}")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = (str(spinor), conf, 6, 30, 203, 40, 4, 10, 5)
+    procs = [ctx.Process(target=_group_rank, args=(r, 2, port, args, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    text = ck.read_text()
+    assert text.startswith("mcmp2-checkpoint 1\nconfighash ") and "workers 5\nworker 0\n" in text
+    assert [int(l.split()[1]) for l in text.splitlines() if l.startswith("worker ")] == [0, 1, 2, 3, 4]
+    assert not ck.with_suffix(".ck.tmp").exists()
+    value, sigma_bar, steps = walker.merge([ck])
+    assert steps == out[0][3] == 203
+    assert value == pytest.approx(out[0][1], rel=1e-15, abs=0)
+    assert sigma_bar == pytest.approx(out[0][2], rel=1e-13, abs=0)
+    lines = tr.read_text().splitlines()
+    assert [l.split()[2] for l in lines] == [f"w{k}" for k in range(5) for _ in range(4)]
+    assert not list(tmp_path.glob("run.trace.w*"))
+
+
+def test_gather_bytes_and_framing():
+    """The byte gather pads to the longest rank's blob and cuts each back to its own length;
+    the framing round-trips empty and binary items."""
+    blobs = [b"", b"abc\x00\xff", b"x" * 1000]
+    for mine in range(3):
+        def all_gather(a, mine=mine):
+            if a.dtype == np.int64:
+                return [np.array([len(b)], dtype=np.int64) for b in blobs]
+            return [np.frombuffer(b.ljust(len(a), b"\0"), dtype=np.uint8) for b in blobs]
+        assert D.gather_bytes(all_gather, blobs[mine]) == blobs
+    items = [b"", b"\x00\x01", b"worker 3\n"]
+    assert D._unpack(D._pack(items)) == items and D._unpack(D._pack([])) == []
