@@ -155,6 +155,10 @@ def host() -> C.CDLL:
         h.mcmp2h_checkpoint_header.argtypes = [cp, ip, cp, C.c_long, lp]
         h.mcmp2h_checkpoint_config.argtypes = [cp, cp, ip, C.POINTER(C.c_int)]
         h.mcmp2h_merge_estimates.argtypes = [dp, ip, dp]
+        h.mcmp2h_blocking.argtypes = [dp, C.c_long, C.c_long, dp]
+        h.mcmp2h_config_hash.restype = C.c_uint64
+        h.mcmp2h_config_hash.argtypes = [cp, C.c_uint64]
+        h.mcmp2h_philox_stream.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, ip, C.POINTER(C.c_uint32)]
         h.mcmp2h_generate.argtypes = [cp, cp]
         _host = h
     return _host
