@@ -379,3 +379,32 @@ def test_gather_bytes_and_framing():
         assert D.gather_bytes(all_gather, blobs[mine]) == blobs
     items = [b"", b"\x00\x01", b"worker 3\n"]
     assert D._unpack(D._pack(items)) == items and D._unpack(D._pack([])) == []
+
+
+@pytest.mark.parametrize("which", ["checkpoint", "trace"])
+def test_run_files_with_only_one_of_checkpoint_and_trace(cfgdir, tmp_path, which):
+    """A config naming only one of the two files: the gathered sections are told apart by their
+    count, the other file is not written (single rank, identity gather)."""
+    class Group:
+        first, count = 0, 2
+
+        def records(self):
+            return [b"worker 0\nend-worker\n", b"worker 1\nend-worker\n"]
+
+        def traces(self):
+            return [b"10 a\n", b"10 b\n"]
+
+    path = tmp_path / f"run.{which}"
+    text = f"spinors {cfgdir / 'syn1c.spinor'}\nsteps 10\nworkers 2\n{which} {path}\n"
+    files = D.RunFiles(text, D.parse_run_config(text), 0, lambda a: [a])
+    assert files
+    files.write_interval(Group())
+    files.finish()
+    if which == "checkpoint":
+        body = path.read_bytes()
+        assert body.startswith(b"mcmp2-checkpoint 1\n") and body.endswith(b"workers 2\n" + b"".join(Group().records()))
+    else:
+        assert path.read_bytes() == b"10 a\n10 b\n"
+    assert sorted(p.name for p in tmp_path.iterdir()) == [path.name]
+    none = f"spinors {cfgdir / 'syn1c.spinor'}\nsteps 10\nworkers 2\n"
+    assert not D.RunFiles(none, D.parse_run_config(none), 0, lambda a: [a])
