@@ -369,6 +369,9 @@ def main():
                     help="A/B only: oz_slice_kernel in series with the O pass instead of beside it "
                          "(mcmp2dev_oz_overlap 0)")
     ap.add_argument("--dmma", action="store_true", help="A/B only: the all-DMMA pair stage (mcmp2dev_pair_path 0)")
+    ap.add_argument("--whole-ksteps", action="store_true",
+                    help="A/B: the INT8 V-GEMM skips only whole empty k-steps, not the leading zero slices "
+                         "of the partly empty ones (mcmp2dev_oz_truncation 2)")
     ap.add_argument("--full-k", action="store_true",
                     help="A/B only: every k-step of K' in the V-GEMM (mcmp2dev_oz_truncation 0)")
     ap.add_argument("--ensembles", type=int, default=1,
@@ -431,6 +434,8 @@ def main():
         dw.int8_overlap(0)
     if args.full_k:
         dw.int8_truncation(0)
+    if args.whole_ksteps:
+        dw.int8_truncation(2)
     if args.dmma:
         dw.int8_v(0)
     if ens > 1:
@@ -510,7 +515,7 @@ def main():
                 evf[k][1].record(stream)
         torch.cuda.synchronize()
         full_k_ms = sum(a.elapsed_time(b) for a, b in evf) / nfk
-        dw.int8_truncation(1)
+        dw.int8_truncation(2 if args.whole_ksteps else 1)
     work = dw.work()
     pair_ms = prof["ms"]["pair"] / prof["launches"]["pair"]
     step_ms_prof = prof["ms"]["total"] / prof["launches"]["total"]
@@ -636,13 +641,16 @@ def main():
                                          "sums of exact int8 products, pair_oz.cu)",
             "achieved": a8, "peak": INT8_PEAK, "unit": "TFLOP/s", "frac": a8 / INT8_PEAK,
             "traffic": traffic_of("oz_vgemm_kernel"),
-            "op_basis": "executed int8 tensor ops (2 per MAC): tiles x 21 slice products x 2 x 128 x 80 x 32 x the "
-                        "k-steps issued (the device counter of mcmp2dev_oz_ksteps over the profiled launches)",
+            "op_basis": "executed int8 tensor ops (2 per MAC): 2 x 128 x 80 x 32 per slice product issued (the "
+                        "device counter of mcmp2dev_oz_ksteps over the profiled launches; 21 products per whole "
+                        "k-step, fewer in a partly empty one)",
             "peak_source": INT8_PEAK_SOURCE,
             "ksteps_frac": ks_frac, "ksteps_frac_run": ks_frac_run,
             "ksteps_note": "K' follows the virtual energies; k-steps whose digits are all zero at this step's tau "
-                           "(exp(-eps tau / 2) below the last slice) are skipped, bit-identical to the full loop "
-                           "(tests/test_gpu_oz.py); ksteps_frac = issued / full over the profiled launches, "
+                           "(exp(-eps tau / 2) below the last slice) are skipped, and so are the slice products of "
+                           "the partly empty k-steps whose A or B slice is all zero there (leading digits), "
+                           "bit-identical to the full loop (tests/test_gpu_oz.py); ksteps_frac = slice products "
+                           "issued / full over the profiled launches, "
                            "ksteps_frac_run over warm-up + timed steps",
             "full_k_ms_per_step": full_k_ms,
             "full_k_samples_per_s": samples_per_step / (full_k_ms / 1e3) if full_k_ms else None,

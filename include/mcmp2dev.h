@@ -204,8 +204,13 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode);
  * digits are all zero. oz_slice_kernel records, per point pair, the last 16-spinor k-step with
  * a nonzero digit, and oz_vgemm_kernel runs each tile's k-steps only up to the smaller of its
  * Q block's and P block's counts. The skipped slice products are exact zeros, so the step's sums
- * are bit-identical to the full loop (tests/test_gpu_oz.py). mode -1 queries, 0 runs every
- * k-step, 1 truncates; returns the active state. */
+ * are bit-identical to the full loop (tests/test_gpu_oz.py). In the k-steps before those, the
+ * leading slices (most significant digits) of every row may be zero as well: the slice kernel
+ * also records, per point pair and k-step, the first slice with a nonzero digit, and a k-step
+ * whose A rows have a and whose B rows have b leading zero slices issues only the products
+ * (s, t) with s >= a, t >= b (none when a + b >= 6) and copies only those slices. mode -1
+ * queries, 0 runs every k-step in full, 1 skips empty k-steps and leading zero slices
+ * (default), 2 skips whole empty k-steps only; returns the active mode. */
 int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode);
 /* INT8 V path, literal estimator: oz_slice_kernel on a side stream of the handle, concurrent
  * with the O pass (both read Phi only; the V-GEMM waits for both). mode -1 queries, 0 runs them

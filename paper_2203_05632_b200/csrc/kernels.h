@@ -87,6 +87,7 @@ struct PairParams {
 
 // INT8 (Ozaki) V blocks of the Kramers pair stage (pair_oz.cu)
 #define OZ_SLICES 6
+#define OZ_LZ_STRIDE 32  // k-steps per record of OzParams::lz (n_vir <= 512: at most 32)
 struct OzParams {
   const double* phi;
   int npts_pad, Go, Gv;      // Phi layout (PhiChunks)
@@ -125,7 +126,12 @@ struct OzParams {
   // runs a tile's k-steps only up to min(Q block's, P block's) -- the products beyond are exact
   // zeros, so the sums are bit-identical to the full K' loop. nullptr: every tile runs all ks.
   uint8_t* ks_cnt;           // [npts_oz / 2]
-  unsigned long long* ks_exec;  // k-steps issued by the main-pass V-GEMM launches (cumulative)
+  // Per point pair and k-step, the first main slice with a nonzero digit (0 .. OZ_SLICES; low
+  // nibble: all four channel rows = the pair's B rows, high nibble: its alpha rows = A rows). A
+  // k-step whose A operand has `a` and B operand `b` leading zero slices needs only the products
+  // (s, t) with s >= a, t >= b (none when a + b >= OZ_SLICES): the rest are exact zeros.
+  uint8_t* lz;               // [npts_oz / 2][OZ_LZ_STRIDE]
+  unsigned long long* ks_exec;  // slice products issued by the main-pass V-GEMM launches (cumulative; 21 per full k-step)
 };
 void oz_layout(int n_vir, int& kh, int& ks);
 size_t oz_slice_bytes_a(int npts_oz, int ks);

@@ -122,7 +122,9 @@ struct mcmp2dev_handle {
   double* d_fstore = nullptr; // [C(oz_m, 2)][4] f values of the main pass for the refinement pass
   // per-tile k-step truncation of the INT8 V-GEMM (OzParams::ks_cnt): on by default, exact
   bool oz_trunc = true;
+  bool oz_trunc_slices = true;  // with oz_trunc: also the leading zero slices of each k-step (OzParams::lz)
   uint8_t* d_ks_cnt = nullptr;             // [npts_oz / 2]
+  uint8_t* d_lz = nullptr;                 // [npts_oz / 2][OZ_LZ_STRIDE] leading zero slices (OzParams::lz)
   unsigned long long* d_ks_exec = nullptr; // k-steps issued by the main-pass V-GEMM launches
   double oz_ks_full = 0;                   // k-steps of one untruncated launch (last launch's sizes)
   double* d_tile_eps = nullptr;  // [main tiles][2] the main pass's error estimate per tile
@@ -178,7 +180,7 @@ struct mcmp2dev_handle {
   } graph_keys[2];
 
   cudaGraphExec_t ensure_graph() {
-    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, oz_trunc ? 1 : 0, oz_overlap ? 1 : 0, k0, k1, rstream, guard_tol};
+    const GraphKey key{m, kramers ? 1 : 0, nens, oz_active(m, nens) ? 1 : 0, oz_trunc ? (oz_trunc_slices ? 2 : 1) : 0, oz_overlap ? 1 : 0, k0, k1, rstream, guard_tol};
     cudaGraphExec_t& graph_exec = graphs[cur];
     if (graph_exec && key == graph_keys[cur]) return graph_exec;
     if (graph_exec) cudaGraphExecDestroy(graph_exec), graph_exec = nullptr;
@@ -239,10 +241,11 @@ struct mcmp2dev_handle {
   void oz_free() {
     for (void* p : {(void*)ozp.sa, (void*)ozp.sb, (void*)ozp.sa_scale, (void*)ozp.sb_scale, (void*)ozp.sb_exp, (void*)ozp.v,
                     (void*)oz_otiles, (void*)d_pstat, (void*)d_fstore, (void*)d_tile_eps, (void*)d_ks_cnt,
-                    (void*)d_ks_exec})
+                    (void*)d_ks_exec, (void*)d_lz})
       if (p) cudaFree(p);
     d_ks_cnt = nullptr;
     d_ks_exec = nullptr;
+    d_lz = nullptr;
     ozp.sa = ozp.sb = nullptr;
     ozp.sa_scale = ozp.sb_scale = ozp.v = nullptr;
     ozp.sb_exp = nullptr;
@@ -294,6 +297,8 @@ struct mcmp2dev_handle {
     ck(cudaMemset(d_pstat, 0, sizeof(float) * 4 * npts_oz), "memset oz point stats");
     ck(cudaMalloc(&d_ks_cnt, npts_oz / 2), "cudaMalloc oz k-step counts");
     ck(cudaMemset(d_ks_cnt, 0, npts_oz / 2), "memset oz k-step counts");
+    ck(cudaMalloc(&d_lz, size_t(npts_oz / 2) * OZ_LZ_STRIDE), "cudaMalloc oz leading-zero slices");
+    ck(cudaMemset(d_lz, 0, size_t(npts_oz / 2) * OZ_LZ_STRIDE), "memset oz leading-zero slices");
     ck(cudaMalloc(&d_ks_exec, sizeof(unsigned long long)), "cudaMalloc oz k-step counter");
     ck(cudaMemset(d_ks_exec, 0, sizeof(unsigned long long)), "memset oz k-step counter");
     oz_m = 16 * nbq;
@@ -367,6 +372,7 @@ struct mcmp2dev_handle {
       o.fstore = guarded ? d_fstore : nullptr;
       o.tile_eps = guarded ? d_tile_eps : nullptr;
       o.ks_cnt = oz_trunc ? d_ks_cnt : nullptr;
+      o.lz = oz_trunc && oz_trunc_slices && o.ks <= OZ_LZ_STRIDE ? d_lz : nullptr;
       o.ks_exec = d_ks_exec;
       // Literal estimator: the slice kernel (integer / load-store work, 1 KB of shared memory) and
       // the O pass (DMMA, one CTA per SM) need only Phi, so the slices are cut on a side stream
@@ -1436,8 +1442,9 @@ int mcmp2dev_pair_path(mcmp2dev_t* h, int mode) {
 int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode) {
   if (!h) return -1;
   if (mode == 0) h->oz_trunc = false;
-  if (mode == 1) h->oz_trunc = true;
-  return h->oz_trunc ? 1 : 0;
+  if (mode == 1) h->oz_trunc = true, h->oz_trunc_slices = true;
+  if (mode == 2) h->oz_trunc = true, h->oz_trunc_slices = false;
+  return h->oz_trunc ? (h->oz_trunc_slices ? 1 : 2) : 0;
 }
 
 int mcmp2dev_oz_overlap(mcmp2dev_t* h, int mode) {
@@ -1454,7 +1461,7 @@ int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2) {
     unsigned long long n = 0;
     ck(cudaStreamSynchronize(h->stream), "stream sync");
     ck(cudaMemcpy(&n, h->d_ks_exec, sizeof n, cudaMemcpyDeviceToHost), "k-step counter D2H");
-    out2[0] = double(n);
+    out2[0] = double(n) / 21.0;  // products -> k-steps (a partly empty k-step counts its share)
     out2[1] = h->oz_ks_full;
   });
 }

@@ -133,6 +133,12 @@ __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
 }
+__device__ __forceinline__ void umma_i8_rt(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -173,6 +179,28 @@ __device__ __forceinline__ void oz_issue_diagonals(uint32_t tmem, const int8_t* 
     if constexpr (N1 > 0) umma_i8<oz_idesc(N1)>(tmem + uint32_t(s * NB + N0), da, umma_desc(sb + N0 * 32), acc);
     oz_issue_diagonals<NB, s + 1>(tmem, sa, sb, acc0);
   }
+}
+
+// A k-step whose A slices below a0 and B slices below b0 are all zero (OzParams::lz, a0 + b0 < S):
+// the products (s, t) with s >= a0, t >= b0, s + t <= S - 1 as merged MMAs -- A slice s against
+// the consecutive B slices b0 .. S-1-s, landing on diagonals s + b0 .. S-1; the skipped products
+// are exact zeros. Never the tile's first k-step (every diagonal is first written there).
+template <int NB>
+__device__ __forceinline__ void oz_issue_partial(uint32_t tmem, const int8_t* sa, const int8_t* sb, int a0, int b0) {
+  const uint64_t db = umma_desc(sb + b0 * NB * 32);
+  for (int s = a0; s + b0 < S; ++s) {
+    const int tot = NB * (S - s - b0);
+    const int n0 = tot > 256 ? (tot / 2 + 15) / 16 * 16 : tot, n1 = tot - n0;
+    const uint64_t da = umma_desc(sa + s * MA * 32);
+    const uint32_t d = tmem + uint32_t((s + b0) * NB);
+    umma_i8_rt(d, da, db, oz_idesc(n0), 1u);
+    if (n1 > 0) umma_i8_rt(d + uint32_t(n0), da, umma_desc(sb + (b0 * NB + n0) * 32), oz_idesc(n1), 1u);
+  }
+}
+// slice products of such a k-step (21 for a full one)
+__device__ __forceinline__ int oz_products(int a0, int b0) {
+  const int n = S - a0 - b0;
+  return n > 0 ? n * (n + 1) / 2 : 0;
 }
 
 // the tile triangle, row by row: Q block a (walkers 16a ..) holds P blocks b < ceil(16 (a+1) / pw)
@@ -273,6 +301,13 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
   OVERLAP_TL_BEGIN(g_tl_slice);
   __shared__ double s_st[8][3];
   __shared__ int s_k[8];
+  // first main slice with a nonzero digit per k-step, over the CTA's alpha rows [0] and all of
+  // its rows [1] (OzParams::lz)
+  __shared__ int s_lz[2][OZ_LZ_STRIDE];
+  if (P.lz) {
+    if (threadIdx.x < 2 * OZ_LZ_STRIDE) (&s_lz[0][0])[threadIdx.x] = S;
+    __syncthreads();
+  }
   // one warp per (point, channel): 8 warps = 2 points per CTA (npts_oz is a multiple of 32, so
   // every CTA's points exist)
   const int wg = int(blockIdx.x) * 8 + (int(threadIdx.x) >> 5), lane = int(threadIdx.x) & 31;
@@ -376,6 +411,16 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
         for (int s = 0; s < SL; ++s) any |= dr[s] | di[s];
         if (any) kact = max(kact, (qd >> 2) + 1);
       }
+      if (P.lz) {
+        int fb = S, fa = S;
+#pragma unroll
+        for (int s = S - 1; s >= 0; --s) {
+          if (dr[s] | di[s]) fb = s;
+          if (alpha && (dr[s] | di[s] | drn[s])) fa = s;
+        }
+        if (fb < S) atomicMin(&s_lz[1][qd >> 2], fb);
+        if (fa < S) atomicMin(&s_lz[0][qd >> 2], fa);
+      }
 #pragma unroll
       for (int s = 0; s < SL; ++s) {
         // B row [re | im]
@@ -413,6 +458,8 @@ __global__ void __launch_bounds__(256, OZ_SLICE_MINB) oz_slice_kernel(OzParams P
       for (int w = 0; w < 8; ++w) k = max(k, s_k[w]);
       P.ks_cnt[blockIdx.x] = uint8_t(k);
     }
+    if (P.lz && threadIdx.x < OZ_LZ_STRIDE)  // (the barrier above follows every lane's atomicMin)
+      P.lz[size_t(blockIdx.x) * OZ_LZ_STRIDE + threadIdx.x] = uint8_t(s_lz[1][threadIdx.x] | (s_lz[0][threadIdx.x] << 4));
   }
   OVERLAP_TL_END(g_tl_slice);
   if (!stats) return;  // uniform over the grid
@@ -523,6 +570,16 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
       s_kb[i] = uint8_t(mx);
     }
   }
+  // main pass: the tile's k-step plan from the slice kernel's leading-zero records (OzParams::lz),
+  // written by the producer warp (lane = k-step) before the tile's first copy and read by the
+  // producer and MMA threads: a0 | b0 << 4 (issue the products s >= a0, t >= b0; copy only those
+  // slices), or PLAN_SKIP when a0 + b0 >= S (every product of the k-step has a zero factor).
+  // k-step 0 is always whole: it is every diagonal's first write. The producer is at most NST
+  // stages, so at most NST + 1 tiles, ahead of the MMA thread: 8 plans rotate.
+  constexpr int NPLAN = 8;
+  constexpr uint8_t PLAN_SKIP = 0xFF;
+  __shared__ uint8_t s_plan[NPLAN][OZ_LZ_STRIDE];
+  const bool use_plan = !CORR && trunc && P.lz != nullptr && KS <= OZ_LZ_STRIDE;
   auto tile_ks = [&](int a, int b0, int nb) {
     if (!trunc) return KS;
     int kb = 0;
@@ -556,10 +613,10 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
   const int my = int(blockIdx.x) < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   if (warp == EPW) {
-    if (lane == 0) {  // producer: one k-step of the tile's A and B slices per stage
+    {  // producer (lane 0; the other lanes help with the tile's plan): one k-step of the tile's A and B slices per stage
       int stage = 0;
       uint32_t ph = 0;
-      unsigned long long issued = 0;  // k-steps of this CTA's tiles
+      unsigned long long issued = 0;  // slice products of this CTA's tiles
       OzGroupWalk w(int(blockIdx.x), PW, PB);
       for (int it = 0; it < my; ++it, w.next(int(gridDim.x))) {
         if constexpr (CORR)
@@ -568,7 +625,21 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         const int8_t* ga = P.sa + size_t(a) * KS * A_KSM;
         const int8_t* gb = P.sb + size_t(b0) * KS * B_KSM;
         const int nk = tile_ks(a, b0, nb);
-        if constexpr (!CORR) issued += nk;
+        if (use_plan) {  // lane = k-step: leading zero slices of the Q block's A rows and the P block's B rows
+          uint8_t pl = 0;
+          if (lane > 0 && lane < nk) {
+            constexpr int BC = NB / 8;  // records per P block
+            const int ncnt = P.npts_oz / 2;
+            int la = S, lb = S;
+            for (int i = 0; i < 16; ++i) la = min(la, int(P.lz[size_t(16 * a + i) * OZ_LZ_STRIDE + lane] >> 4));
+            for (int j = 0; j < BC; ++j)
+              if (BC * b0 + j < ncnt) lb = min(lb, int(P.lz[size_t(BC * b0 + j) * OZ_LZ_STRIDE + lane] & 15));
+            pl = la + lb >= S ? PLAN_SKIP : uint8_t(la | (lb << 4));
+          }
+          s_plan[it % NPLAN][lane] = pl;
+          __syncwarp();
+        }
+        if (lane != 0) continue;
         if constexpr (OSM) {  // the tile's o values: walkers PW b0 .. of Q block row a (up to the diagonal)
           const int ob = it & 1, np = min(PW, 16 * (a + 1) - PW * b0);
           mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1u);
@@ -578,17 +649,31 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
           bulk_g2s(sm + NST * STAGE + ob * Sh::OT_BUF + Sh::OT_BYTES, P.sb_exp + size_t(b0) * NB, NB * 4, &ofull[ob]);
         }
         for (int ks = 0; ks < nk; ++ks) {
+          int a0 = 0, sb0 = 0;
+          if (use_plan) {
+            const uint8_t pl = s_plan[it % NPLAN][ks];
+            if (pl == PLAN_SKIP) continue;
+            a0 = pl & 15, sb0 = pl >> 4;
+          }
+          if constexpr (!CORR) issued += oz_products(a0, sb0);
           mbar_wait(&empty[stage], ph ^ 1u);
           int8_t* dst = sm + stage * STAGE;
-          mbar_expect_tx(&full[stage], A_CP + nb * B_CP);
-          bulk_g2s(dst, ga + size_t(ks) * A_KSM, A_CP, &full[stage]);
-          for (int j = 0; j < nb; ++j)
-            bulk_g2s(dst + A_CP + j * B_CP, gb + (size_t(j) * KS + ks) * B_KSM, B_CP, &full[stage]);
+          if (a0 | sb0) {  // A slices a0 .. S-1-sb0 and B slices sb0 .. S-1-a0 take part
+            const int ns = S - a0 - sb0;
+            mbar_expect_tx(&full[stage], ns * (MA * 32 + NB * 32));
+            bulk_g2s(dst + a0 * MA * 32, ga + size_t(ks) * A_KSM + a0 * MA * 32, ns * MA * 32, &full[stage]);
+            bulk_g2s(dst + A_CP + sb0 * NB * 32, gb + size_t(ks) * B_KSM + sb0 * NB * 32, ns * NB * 32, &full[stage]);
+          } else {
+            mbar_expect_tx(&full[stage], A_CP + nb * B_CP);
+            bulk_g2s(dst, ga + size_t(ks) * A_KSM, A_CP, &full[stage]);
+            for (int j = 0; j < nb; ++j)
+              bulk_g2s(dst + A_CP + j * B_CP, gb + (size_t(j) * KS + ks) * B_KSM, B_CP, &full[stage]);
+          }
           if (++stage == NST) stage = 0, ph ^= 1u;
         }
       }
       if constexpr (!CORR)
-        if (P.ks_exec) atomicAdd(P.ks_exec, issued);
+        if (lane == 0 && P.ks_exec) atomicAdd(P.ks_exec, issued);
     }
   } else if (warp == EPW + 1) {
     if (lane == 0) {  // MMA issuer: the slice products of each k-step into the tile's accumulators
@@ -606,6 +691,14 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
         TL(it, 1, clock64());
         const int nk = tile_ks(w.a, w.g * PB, nb);
         for (int ks = 0; ks < nk; ++ks) {
+          // the plan is read behind the wait for the tile's first stage (k-step 0 is always whole),
+          // which orders it after the producer's writes
+          int a0 = 0, sb0 = 0;
+          if (use_plan && ks > 0) {
+            const uint8_t pl = *reinterpret_cast<volatile const uint8_t*>(&s_plan[it % NPLAN][ks]);
+            if (pl == PLAN_SKIP) continue;
+            a0 = pl & 15, sb0 = pl >> 4;
+          }
           mbar_wait(&full[stage], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const int8_t* sa = sm + stage * STAGE;
@@ -616,6 +709,8 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
               for (int s = 0; s < SL; ++s)  // diagonal 6: (s, 6 - s)
                 umma_i8<Sh::IDESC>(tmem + uint32_t((slot * PB + j) * NB), umma_desc(sa + s * MA * 32),
                                    umma_desc(sb + j * B_CP + (SL - 1 - s) * NB * 32), ks > 0 || s > 0 ? 1u : 0u);
+          } else if (a0 | sb0) {
+            oz_issue_partial<NB>(tmem, sa, sb, a0, sb0);
           } else {
             oz_issue_diagonals<NB, 0>(tmem, sa, sb, ks > 0 ? 1u : 0u);
           }

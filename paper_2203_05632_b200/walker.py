@@ -272,7 +272,8 @@ class DeviceWalker:
 
     def int8_truncation(self, mode: int = -1) -> bool:
         """Energy-ordered truncation of the INT8 V-GEMM's K loop (exact; on by default):
-        -1 query, 0 every k-step, 1 only the k-steps that hold a nonzero digit."""
+        -1 query, 0 every k-step, 1 only the slice products whose slices hold a nonzero digit in the
+        k-step (whole k-steps and leading zero slices skipped), 2 whole empty k-steps only."""
         return bool(self._d.mcmp2dev_oz_truncation(self._h, mode))
 
     def int8_overlap(self, mode: int = -1) -> bool:

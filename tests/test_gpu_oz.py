@@ -149,8 +149,9 @@ def test_int8_v_two_pass_slicing_wide_set(tmp_path):
 @pytest.mark.parametrize("name,m", [("cfg3", 256), ("cfg4", 192), ("cfg5-36", 330)])
 def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
     """The V-GEMM skips a tile's trailing k-steps when every digit there is zero (high virtual
-    energies at this tau, include/mcmp2dev.h mcmp2dev_oz_truncation): the skipped products are
-    exact zeros, so every field of the step records is bit-identical to the full K' loop; at
+    energies at this tau, include/mcmp2dev.h mcmp2dev_oz_truncation) and, in the partly empty
+    k-steps before them, the slice products whose A or B slice is all zero: the skipped products
+    are exact zeros, so every field of the step records is bit-identical to the full K' loop; at
     large tau k-steps are actually skipped, at tau -> 0 none are; the oracle still agrees."""
     from paper_2203_05632_b200 import generate_config
     if (cfgdir / f"{name}.spinor").exists():
@@ -172,12 +173,19 @@ def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
         e1, full = dw.int8_ksteps()
         frac.append((e1 - e0) / full)
     on = np.concatenate(on)
+    assert dw.int8_truncation(2)  # whole empty k-steps only: the partly empty ones run all 21 products
+    e0, full = dw.int8_ksteps()
+    whole = dw.replay_ex(walkers, taus)
+    e1, _ = dw.int8_ksteps()
+    frac_whole = (e1 - e0) / (len(taus) * full)
     assert not dw.int8_truncation(0)
     e0, full = dw.int8_ksteps()
     off = dw.replay_ex(walkers, taus)
     e1, _ = dw.int8_ksteps()
     assert e1 - e0 == len(taus) * full
-    assert on.tobytes() == off.tobytes()
+    assert on.tobytes() == off.tobytes() and whole.tobytes() == off.tobytes()
+    # the leading zero slices of the partly empty k-steps are skipped on top of the empty k-steps
+    assert np.mean(frac) < frac_whole - 0.02 and frac_whole < 1.0, (frac, frac_whole)
     assert frac[0] > 0.99 and frac[-1] < 0.8 and all(a >= b for a, b in zip(frac, frac[1:])), frac
     ref = orc.replay(walkers, taus)
     for c, r in ((0, 0), (2, 2), (4, 4)):
