@@ -182,7 +182,7 @@ def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
     e0, full = dw.int8_ksteps()
     off = dw.replay_ex(walkers, taus)
     e1, _ = dw.int8_ksteps()
-    assert e1 - e0 == len(taus) * full
+    assert e1 - e0 == pytest.approx(len(taus) * full, rel=1e-12)  # (the counter is in slice products / 21)
     assert on.tobytes() == off.tobytes() and whole.tobytes() == off.tobytes()
     # the leading zero slices of the partly empty k-steps are skipped on top of the empty k-steps
     assert np.mean(frac) < frac_whole - 0.02 and frac_whole < 1.0, (frac, frac_whole)
