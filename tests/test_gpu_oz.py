@@ -146,6 +146,32 @@ def test_int8_v_two_pass_slicing_wide_set(tmp_path):
     assert rel_err(dmma[:, 0], tr["est"][:, 0]) < REL
 
 
+def test_int8_v_truncation_is_exact_on_the_physical_path(cfgdir):
+    """The opt-in INT8 V blocks of the physical estimator (64-column tiles, V written for pair_kr's
+    trace epilogue) under the three truncation modes: bit-identical step records, fewer slice
+    products issued with the leading zero slices skipped than with whole k-steps only."""
+    sp = cfgdir / "cfg4.spinor"
+    text = (cfgdir / "cfg4.conf").read_text() + "estimator physical\n"
+    orc = oracle_py.OracleSystem(sp, text)
+    tr = orc.trajectory(seed=5, stream=0, m=192, burn=20, nsteps=1, physical=True)
+    taus = np.array([0.02, 0.3, 2.0])
+    walkers = np.repeat(tr["walkers"][:1], len(taus), axis=0)
+    dw = DeviceWalker(System(sp, text), max_walkers=192)
+    assert dw.int8_v(1)
+    out, issued = {}, {}
+    for mode in (1, 2, 0):
+        dw.int8_truncation(mode)
+        e0, _ = dw.int8_ksteps()
+        out[mode] = dw.replay_ex(walkers, taus)
+        e1, full = dw.int8_ksteps()  # (the full count is set by the launch)
+        issued[mode] = (e1 - e0) / (len(taus) * full)
+    assert out[1].tobytes() == out[0].tobytes() and out[2].tobytes() == out[0].tobytes()
+    assert issued[1] < issued[2] - 0.02 < issued[0] - 0.02 and issued[0] == pytest.approx(1.0, rel=1e-12), issued
+    ref = orc.replay(walkers, taus, physical=True)
+    for c in (0, 2, 4):
+        assert rel_err(out[1][:, c], ref[:, c]) < REL, c
+
+
 @pytest.mark.parametrize("name,m", [("cfg3", 256), ("cfg4", 192), ("cfg5-36", 330)])
 def test_int8_v_kstep_truncation_is_exact(cfgdir, tmp_path, name, m):
     """The V-GEMM skips a tile's trailing k-steps when every digit there is zero (high virtual
