@@ -218,7 +218,8 @@ int mcmp2dev_oz_truncation(mcmp2dev_t* h, int mode);
  * so each kernel is timed alone). Results do not depend on it. */
 int mcmp2dev_oz_overlap(mcmp2dev_t* h, int mode);
 /* out2 = {k-steps (32 of K' = 2 n_vir) issued by the main-pass V-GEMM launches since the INT8
- * buffers were allocated, k-steps of one untruncated launch at the last step's sizes}. */
+ * buffers were allocated -- counted in slice products / 21, so a partly empty k-step counts the
+ * share of its 21 products that ran --, k-steps of one untruncated launch at the last step's sizes}. */
 int mcmp2dev_oz_ksteps(mcmp2dev_t* h, double* out2);
 /* Accuracy guard of the INT8 V path (literal estimator). After each INT8 step the V-GEMM's
  * last CTA compares the estimated error of the direct sum, the exchange sum and the step value

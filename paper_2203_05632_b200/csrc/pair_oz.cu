@@ -38,10 +38,11 @@
 // values into a double buffer), one thread issues the k-step's 21 slice products as 9 merged
 // tcgen05.mma (oz_issue_diagonals), eight epilogue warps (two per TMEM lane quarter) drain TMEM
 // (tcgen05.ld), merge, release the accumulators and finish the tile while the next one runs.
-// Measured (cfg4, profiles/r11): 1.11 ms at 2960 int8 TOPS on the full K' loop (0.65 of the
+// Measured (cfg4, profiles/r11, r16): 1.11 ms at 2960 int8 TOPS on the full K' loop (0.65 of the
 // dense tcgen05 rate; the bound is shared-memory bandwidth, see oz_issue_diagonals), 0.98 ms on
-// the chain's tau draws with the empty k-steps skipped, vs ~3.6 ms for the DMMA V phase of
-// pair_kr.
+// the chain's tau draws with the empty k-steps skipped, 0.95 ms with the leading zero slices of
+// the partly empty k-steps skipped as well (OzParams::lz, oz_issue_partial), vs ~3.6 ms for the
+// DMMA V phase of pair_kr.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
