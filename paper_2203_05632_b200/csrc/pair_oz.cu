@@ -817,7 +817,11 @@ __global__ void __launch_bounds__(THREADS, 1) oz_vgemm_kernel(OzParams P) {
 #pragma unroll
           // (measured and rejected: the same sum from the low end with 32 x 32 + 64 multiply-adds,
           // IMAD.WIDE -- 272 instead of 459 instructions up to the release, but V-GEMM 1.03 vs 0.98 ms
-          // at cfg4 and 6.6 vs 5.7 ms at cfg5-10: the wide multiply-adds issue at a lower rate)
+          // at cfg4 and 6.6 vs 5.7 ms at cfg5-10: the wide multiply-adds issue at a lower rate.
+          // Also rejected: each chunk's diagonals loaded in two halves, one half's tcgen05.ld in
+          // flight while the other is merged, no more registers: step 1.661 / 1.657 / 1.676 vs
+          // 1.656 / 1.658 / 1.665 ms in a same-box A/B -- the drain is TMEM-read-bound (~100 B/clk),
+          // not merge-latency-bound)
           for (int d = 1; d < NACC; ++d)  // the last diagonal joins rounded to the one before it
             x = d < S - 1 ? x * 256 + int32_t(v[d][c]) : x + ((int32_t(v[d][c]) + 128) >> 8);
           X[c0 + c] = x;
